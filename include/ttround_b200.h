@@ -1,0 +1,164 @@
+/* ttround_b200.h — C ABI of the B200-native TT-rounding library
+ * (paper_2511_03598_b200/lib/libttround_b200.so).
+ *
+ * This is the drop-in boundary for the reference's `ttround` core/ hot path
+ * (arXiv 2511.03598). The reference exposes plain C++ headers; each entry
+ * point below replaces one of them (file:line cited under proj/core/):
+ *
+ *   ttr_tt_upload/_download/_shape/_destroy   Core, TTTensor        include/ttround/tensor.hpp:17-84
+ *   ttr_tt_random_philox                      random_gaussian_tt    include/ttround/tensor.hpp:176-177 (device Philox draw)
+ *   ttr_tt_formal_sum                         formal_sum            include/ttround/tensor.hpp:172
+ *   ttr_tt_scale                              scaled                include/ttround/tensor.hpp:187
+ *   ttr_norm_exact                            norm_exact            include/ttround/tensor.hpp:181
+ *   ttr_relative_error                        relative_error        include/ttround/tensor.hpp:191
+ *   ttr_round_fixed_krp                       round_fixed_krp       include/ttround/round_rand.hpp:14-15
+ *   ttr_round_adaptive_krp                    round_adaptive_krp    include/ttround/round_rand.hpp:31 (AdaptiveConfig :18-25)
+ *   ttr_round_deterministic_tol / _ranks      round_deterministic   include/ttround/orthogonalize.hpp:50,54
+ *   ttr_estimate_norm_krp                     estimate_norm_krp     include/ttround/sketch.hpp:63
+ *   ttr_krp_partial_contractions              krp_partial_contractions_rl + draw_gaussian_factors
+ *                                                                   include/ttround/sketch.hpp:25-26,47-48
+ *   ttr_counters / ttr_counters_reset         flops::counters/reset include/ttround/flops.hpp:12-25
+ *
+ * Conventions
+ *  - Every function returns ttr_status. 0 = success; 1..15 = the reference's
+ *    Errc kinds in declaration order (types.hpp:15-31) plus one; 100+ are
+ *    device-side failures. No C++ exception crosses this boundary; the C++
+ *    wrapper include/ttround_b200/ttround.hpp rethrows ttround::Error(Errc).
+ *  - Host buffers are caller-owned; device TT tensors (ttr_tt) are owned by
+ *    the library and live in the HBM of the context's device until
+ *    ttr_tt_destroy. Cores keep the reference layout: core k is the
+ *    column-major vertical unfolding of an r_{k-1} x n_k x r_k core
+ *    (element (i,j,g) at g*r_{k-1}*n_k + j*r_{k-1} + i, tensor.hpp:11-16),
+ *    each core 256-byte aligned in one allocation.
+ *  - One ttr_ctx per host thread; all work of a context is ordered on its
+ *    CUDA stream. Calls that return host scalars or rank vectors synchronise.
+ *  - rng_mode: TTR_RNG_PHILOX draws Omega_k from the counter-based generator
+ *    in include/ttround_b200/philox_gauss.h on the device (default);
+ *    TTR_RNG_XOSHIRO reproduces the reference's single xoshiro256++ stream
+ *    and draw order (rng.cpp:34-67, sketch.cpp:44-65) on the host and uploads
+ *    the factors (compatibility mode).
+ */
+#ifndef TTROUND_B200_H
+#define TTROUND_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int ttr_status;
+
+enum {
+    TTR_OK = 0,
+    TTR_ERR_RANK_CHAIN_MISMATCH = 1,
+    TTR_ERR_BOUNDARY_RANK_NOT_ONE = 2,
+    TTR_ERR_EMPTY_CORE_LIST = 3,
+    TTR_ERR_INDEX_OUT_OF_RANGE = 4,
+    TTR_ERR_DENSE_TOO_LARGE = 5,
+    TTR_ERR_MODE_SIZE_MISMATCH = 6,
+    TTR_ERR_EMPTY_TERM_LIST = 7,
+    TTR_ERR_INVALID_RANK_CHAIN = 8,
+    TTR_ERR_SVD_FAILURE = 9,
+    TTR_ERR_INVALID_RANKS = 10,
+    TTR_ERR_NOT_LEFT_ORTHOGONAL = 11,
+    TTR_ERR_INVALID_GRID = 12,
+    TTR_ERR_BREAKDOWN = 13,
+    TTR_ERR_INVALID_ARGUMENT = 14,
+    TTR_ERR_IO = 15,
+    TTR_ERR_CUDA = 100,
+    TTR_ERR_OUT_OF_MEMORY = 101,
+    TTR_ERR_NCCL = 102,
+    TTR_ERR_INTERNAL = 103,
+    TTR_ERR_NO_DEVICE = 104
+};
+
+enum { TTR_RNG_XOSHIRO = 0, TTR_RNG_PHILOX = 1 };
+
+typedef struct ttr_ctx ttr_ctx;
+typedef struct ttr_tt ttr_tt;
+
+/* AdaptiveConfig (round_rand.hpp:18-25). has_known_norm / max_rank_cap
+ * (NULL or d-1 entries) stand in for the std::optional members. */
+typedef struct {
+    double tolerance; /* relative, in (0,1); reference default 1e-6 */
+    double f_init;    /* default 0.1 */
+    double f_inc;     /* default 0.05 */
+    uint64_t seed;
+    int has_known_norm;
+    double known_norm;
+    const int64_t* max_rank_cap;
+    int rng_mode;
+} ttr_adaptive_cfg;
+
+/* flops::Counts (flops.hpp:12-20): algorithmic flops charged with the
+ * reference's formulas (GEMM 2mnk, QR 4mnk, SVD 14mnk+8k^3, linalg.cpp:25-61). */
+typedef struct {
+    uint64_t gemm, qr, svd, sketch, rng;
+} ttr_counts;
+
+/* ---- context ------------------------------------------------------------ */
+ttr_status ttr_ctx_create(int device, void* cuda_stream, ttr_ctx** out);
+ttr_status ttr_ctx_destroy(ttr_ctx* ctx);
+ttr_status ttr_ctx_set_stream(ttr_ctx* ctx, void* cuda_stream);
+ttr_status ttr_ctx_synchronize(ttr_ctx* ctx);
+const char* ttr_last_error(void);
+const char* ttr_version(void);
+/* Number of CUDA kernels this context has launched so far. */
+ttr_status ttr_ctx_kernel_launches(ttr_ctx* ctx, uint64_t* out);
+
+/* ---- TT container (tensor.hpp:17-84) ------------------------------------- */
+ttr_status ttr_tt_upload(ttr_ctx* ctx, int64_t d, const int64_t* n, const int64_t* r,
+                         const double* host_cores, ttr_tt** out);
+/* Same, but from a device buffer (cores concatenated, reference layout). */
+ttr_status ttr_tt_from_device(ttr_ctx* ctx, int64_t d, const int64_t* n, const int64_t* r,
+                              const double* dev_cores, ttr_tt** out);
+ttr_status ttr_tt_shape(const ttr_tt* tt, int64_t* d, int64_t* n, int64_t* r, int64_t* total);
+ttr_status ttr_tt_download(ttr_ctx* ctx, const ttr_tt* tt, double* host_cores);
+ttr_status ttr_tt_core_ptr(const ttr_tt* tt, int64_t k, const double** dev_ptr);
+ttr_status ttr_tt_destroy(ttr_tt* tt);
+
+/* ---- construction / TT arithmetic --------------------------------------- */
+ttr_status ttr_tt_random_philox(ttr_ctx* ctx, int64_t d, const int64_t* n, const int64_t* r,
+                                uint64_t seed, ttr_tt** out);
+ttr_status ttr_tt_formal_sum(ttr_ctx* ctx, const ttr_tt* const* terms, int count, ttr_tt** out);
+ttr_status ttr_tt_scale(ttr_ctx* ctx, ttr_tt* tt, double alpha);
+ttr_status ttr_norm_exact(ttr_ctx* ctx, const ttr_tt* tt, double* out);
+ttr_status ttr_relative_error(ttr_ctx* ctx, const ttr_tt* a, const ttr_tt* b, double* out);
+
+/* ---- rounding (the hot path) -------------------------------------------- */
+ttr_status ttr_round_fixed_krp(ttr_ctx* ctx, const ttr_tt* tt, const int64_t* target_ranks,
+                               int64_t count, uint64_t seed, int rng_mode, ttr_tt** out);
+ttr_status ttr_round_adaptive_krp(ttr_ctx* ctx, const ttr_tt* tt, const ttr_adaptive_cfg* cfg,
+                                  ttr_tt** out);
+ttr_status ttr_round_deterministic_tol(ttr_ctx* ctx, const ttr_tt* tt, double eps, ttr_tt** out);
+ttr_status ttr_round_deterministic_ranks(ttr_ctx* ctx, const ttr_tt* tt, const int64_t* target_ranks,
+                                         int64_t count, ttr_tt** out);
+ttr_status ttr_estimate_norm_krp(ttr_ctx* ctx, const ttr_tt* tt, int64_t width, uint64_t seed,
+                                 int rng_mode, double* out);
+/* W_start..W_d (r_{k-1} x cols each, column-major, concatenated) of the KRP
+ * partial contractions. host_factors: Omega_start..Omega_d (n_k x cols,
+ * concatenated) or NULL to draw them on the device in Philox mode from
+ * (seed, mode, col0 + c). */
+ttr_status ttr_krp_partial_contractions(ttr_ctx* ctx, const ttr_tt* tt, int64_t start_mode,
+                                        int64_t cols, const double* host_factors, uint64_t seed,
+                                        int64_t col0, double* host_w);
+/* Omega_mode(:, col0:col0+cols) drawn on the device (Philox mode). */
+ttr_status ttr_philox_factor(ttr_ctx* ctx, uint64_t seed, int64_t mode, int64_t rows, int64_t cols,
+                             int64_t col0, double* host_out);
+/* Thin Householder QR with explicit Q of a host m x n matrix (m >= n), run on
+ * the device (linalg::thin_qr, linalg.hpp:22-25). q: m x n, r: n x n. */
+ttr_status ttr_thin_qr(ttr_ctx* ctx, int64_t m, int64_t n, const double* host_a, double* host_q,
+                       double* host_r);
+/* C = op(A) B on the device through the library's DMMA GEMM (for tests). */
+ttr_status ttr_gemm(ttr_ctx* ctx, int trans_a, int64_t m, int64_t n, int64_t k, const double* host_a,
+                    const double* host_b, double* host_c);
+
+ttr_status ttr_counters(ttr_ctx* ctx, ttr_counts* out);
+ttr_status ttr_counters_reset(ttr_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TTROUND_B200_H */

@@ -1,0 +1,381 @@
+"""paper_2511_03598_b200 — B200-native randomized TT-rounding with KRP sketches.
+
+Python mirror of the reference `ttround` core/ API for the hot path
+(proj/core/include/ttround/{tensor,sketch,round_rand,orthogonalize}.hpp),
+bound with ctypes to the C ABI in include/ttround_b200.h
+(paper_2511_03598_b200/lib/libttround_b200.so). Every computation runs in the
+CUDA library on the device; there is no CPU fallback — importing works
+without a GPU (so the build can be checked on a CPU host), but creating a
+Context raises TTRoundError(NoDevice) when no CUDA device exists.
+
+Names, argument meaning and error kinds follow the reference:
+
+    TTTensor            <- ttround::TTTensor (tensor.hpp:56-84), device resident
+    round_fixed_krp     <- round_rand.hpp:14-15
+    round_adaptive_krp  <- round_rand.hpp:31  (AdaptiveConfig :18-25)
+    round_deterministic <- orthogonalize.hpp:50,54
+    estimate_norm_krp   <- sketch.hpp:63
+    krp_partial_contractions_rl <- sketch.hpp:47-48
+    norm_exact, relative_error, formal_sum, scaled <- tensor.hpp:172-191
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libttround_b200.so")
+HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "ttround_b200.h")
+
+RNG_XOSHIRO = 0
+RNG_PHILOX = 1
+
+ERRC_NAMES = [
+    "RankChainMismatch", "BoundaryRankNotOne", "EmptyCoreList", "IndexOutOfRange",
+    "DenseTooLarge", "ModeSizeMismatch", "EmptyTermList", "InvalidRankChain", "SVDFailure",
+    "InvalidRanks", "NotLeftOrthogonal", "InvalidGrid", "Breakdown", "InvalidArgument", "IoError",
+]
+_EXTRA = {100: "Cuda", 101: "OutOfMemory", 102: "Nccl", 103: "Internal", 104: "NoDevice"}
+
+
+class TTRoundError(RuntimeError):
+    """Mirrors ttround::Error: `.code` is the Errc name (types.hpp:15-31)."""
+
+    def __init__(self, status: int, message: str):
+        self.status = status
+        self.code = ERRC_NAMES[status - 1] if 1 <= status <= 15 else _EXTRA.get(status, "Unknown")
+        super().__init__(message)
+
+
+_lib = None
+
+
+def build(verbose: bool = False) -> str:
+    """Compile libttround_b200.so for sm_100a (nvcc; no GPU needed)."""
+    import subprocess
+    cmd = ["make", "-C", os.path.join(_HERE, "csrc"), "-j8"]
+    subprocess.run(cmd, check=True, stdout=None if verbose else subprocess.DEVNULL)
+    return LIB_PATH
+
+
+def lib():
+    """Load the CUDA library (fails loudly if it was not built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: run paper_2511_03598_b200.build() "
+                              "(the product has no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        L.ttr_last_error.restype = C.c_char_p
+        L.ttr_version.restype = C.c_char_p
+        _lib = L
+    return _lib
+
+
+def _check(status: int):
+    if status != 0:
+        raise TTRoundError(status, lib().ttr_last_error().decode())
+
+
+def _i64(seq):
+    return (C.c_int64 * max(1, len(seq)))(*[int(x) for x in seq])
+
+
+def _dptr(a: np.ndarray):
+    return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+class Counts(C.Structure):
+    """flops::Counts (flops.hpp:12-20)."""
+    _fields_ = [("gemm", C.c_uint64), ("qr", C.c_uint64), ("svd", C.c_uint64),
+                ("sketch", C.c_uint64), ("rng", C.c_uint64)]
+
+    def total(self) -> int:
+        return self.gemm + self.qr + self.svd
+
+
+class _AdaptiveCfg(C.Structure):
+    _fields_ = [("tolerance", C.c_double), ("f_init", C.c_double), ("f_inc", C.c_double),
+                ("seed", C.c_uint64), ("has_known_norm", C.c_int), ("known_norm", C.c_double),
+                ("max_rank_cap", C.POINTER(C.c_int64)), ("rng_mode", C.c_int)]
+
+
+class Context:
+    """One CUDA device + stream (ttr_ctx). Pass `stream` (an int handle, e.g.
+    torch.cuda.current_stream().cuda_stream) to order work on a caller stream."""
+
+    def __init__(self, device: int = 0, stream: Optional[int] = None):
+        self._h = C.c_void_p()
+        _check(lib().ttr_ctx_create(C.c_int(device), C.c_void_p(stream) if stream else None, C.byref(self._h)))
+        self.device = device
+
+    def close(self):
+        if getattr(self, "_h", None) and self._h.value and _lib is not None:
+            _lib.ttr_ctx_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        self.close()
+
+    def set_stream(self, stream: Optional[int]):
+        _check(lib().ttr_ctx_set_stream(self._h, C.c_void_p(stream) if stream else None))
+
+    def synchronize(self):
+        _check(lib().ttr_ctx_synchronize(self._h))
+
+    def kernel_launches(self) -> int:
+        v = C.c_uint64()
+        _check(lib().ttr_ctx_kernel_launches(self._h, C.byref(v)))
+        return v.value
+
+    def counters(self) -> Counts:
+        c = Counts()
+        _check(lib().ttr_counters(self._h, C.byref(c)))
+        return c
+
+    def reset_counters(self):
+        _check(lib().ttr_counters_reset(self._h))
+
+
+_default_ctx: Optional[Context] = None
+
+
+def default_context() -> Context:
+    global _default_ctx
+    if _default_ctx is None:
+        _default_ctx = Context(0)
+    return _default_ctx
+
+
+class TTTensor:
+    """Device-resident TT tensor (ttr_tt). Cores keep the reference layout."""
+
+    def __init__(self, handle: C.c_void_p, ctx: Context):
+        self._h = handle
+        self.ctx = ctx
+
+    def __del__(self):
+        if getattr(self, "_h", None) and self._h.value and _lib is not None:
+            _lib.ttr_tt_destroy(self._h)
+            self._h = C.c_void_p()
+
+    @staticmethod
+    def _new(ctx: Context, fn, *args) -> "TTTensor":
+        out = C.c_void_p()
+        _check(fn(*args, C.byref(out)))
+        return TTTensor(out, ctx)
+
+    # -- construction ---------------------------------------------------
+    @staticmethod
+    def from_flat(mode_sizes: Sequence[int], ranks: Sequence[int], flat: np.ndarray,
+                  ctx: Optional[Context] = None) -> "TTTensor":
+        """Upload cores given as one flat buffer (core k = its column-major
+        vertical unfolding, concatenated)."""
+        ctx = ctx or default_context()
+        flat = np.ascontiguousarray(flat, dtype=np.float64)
+        return TTTensor._new(ctx, lib().ttr_tt_upload, ctx._h, C.c_int64(len(mode_sizes)), _i64(mode_sizes),
+                             _i64(ranks), _dptr(flat))
+
+    @staticmethod
+    def from_cores(cores: Sequence[np.ndarray], ctx: Optional[Context] = None) -> "TTTensor":
+        """cores[k] of shape (r_{k-1}, n_k, r_k)."""
+        if len(cores) == 0:
+            raise TTRoundError(3, "EmptyCoreList: TT tensor needs at least one core")
+        n = [c.shape[1] for c in cores]
+        r = [cores[0].shape[0]] + [c.shape[2] for c in cores]
+        if cores[0].shape[0] != 1 or cores[-1].shape[2] != 1:
+            raise TTRoundError(2, "BoundaryRankNotOne: boundary TT ranks must be 1")
+        for k in range(len(cores) - 1):
+            if cores[k].shape[2] != cores[k + 1].shape[0]:
+                raise TTRoundError(1, f"RankChainMismatch: adjacent core ranks differ at position {k + 1}")
+        flat = np.concatenate([np.asarray(c, dtype=np.float64).transpose(2, 1, 0).reshape(-1) for c in cores])
+        if not np.all(np.isfinite(flat)):
+            raise TTRoundError(14, "InvalidArgument: core entries must be finite")
+        return TTTensor.from_flat(n, r, flat, ctx)
+
+    @staticmethod
+    def random_philox(mode_sizes: Sequence[int], ranks: Sequence[int], seed: int,
+                      ctx: Optional[Context] = None) -> "TTTensor":
+        """Gaussian cores N(0, 1/(r n r)) drawn on the device (Philox)."""
+        ctx = ctx or default_context()
+        return TTTensor._new(ctx, lib().ttr_tt_random_philox, ctx._h, C.c_int64(len(mode_sizes)), _i64(mode_sizes),
+                             _i64(ranks), C.c_uint64(seed))
+
+    # -- shape / data ---------------------------------------------------
+    def shape(self):
+        d = C.c_int64()
+        _check(lib().ttr_tt_shape(self._h, C.byref(d), None, None, None))
+        n = (C.c_int64 * d.value)()
+        r = (C.c_int64 * (d.value + 1))()
+        tot = C.c_int64()
+        _check(lib().ttr_tt_shape(self._h, C.byref(d), n, r, C.byref(tot)))
+        return list(n), list(r), tot.value
+
+    @property
+    def order(self) -> int:
+        return len(self.shape()[0])
+
+    def mode_sizes(self) -> List[int]:
+        return self.shape()[0]
+
+    def ranks(self) -> List[int]:
+        return self.shape()[1]
+
+    def max_rank(self) -> int:
+        return max(self.ranks())
+
+    def flat(self) -> np.ndarray:
+        _, _, tot = self.shape()
+        out = np.empty(tot, dtype=np.float64)
+        _check(lib().ttr_tt_download(self.ctx._h, self._h, _dptr(out)))
+        return out
+
+    def cores(self) -> List[np.ndarray]:
+        n, r, _ = self.shape()
+        flat = self.flat()
+        out, off = [], 0
+        for k in range(len(n)):
+            cnt = r[k] * n[k] * r[k + 1]
+            out.append(flat[off:off + cnt].reshape(r[k + 1], n[k], r[k]).transpose(2, 1, 0).copy())
+            off += cnt
+        return out
+
+    def core_ptr(self, k: int) -> int:
+        p = C.c_void_p()
+        _check(lib().ttr_tt_core_ptr(self._h, C.c_int64(k), C.byref(p)))
+        return p.value
+
+
+# ---- TT arithmetic (tensor.hpp:172-191) ----------------------------------------
+
+def formal_sum(terms: Sequence[TTTensor]) -> TTTensor:
+    if len(terms) == 0:
+        raise TTRoundError(7, "EmptyTermList: formal sum of no terms")
+    ctx = terms[0].ctx
+    arr = (C.c_void_p * len(terms))(*[t._h.value for t in terms])
+    return TTTensor._new(ctx, lib().ttr_tt_formal_sum, ctx._h, arr, C.c_int(len(terms)))
+
+
+def scaled(tt: TTTensor, alpha: float) -> TTTensor:
+    out = formal_sum([tt])
+    _check(lib().ttr_tt_scale(out.ctx._h, out._h, C.c_double(alpha)))
+    return out
+
+
+def norm_exact(tt: TTTensor) -> float:
+    v = C.c_double()
+    _check(lib().ttr_norm_exact(tt.ctx._h, tt._h, C.byref(v)))
+    return v.value
+
+
+def relative_error(a: TTTensor, b: TTTensor) -> float:
+    v = C.c_double()
+    _check(lib().ttr_relative_error(a.ctx._h, a._h, b._h, C.byref(v)))
+    return v.value
+
+
+# ---- rounding (the hot path) -----------------------------------------------------
+
+def round_fixed_krp(tt: TTTensor, target_ranks: Sequence[int], seed: int, rng: int = RNG_PHILOX) -> TTTensor:
+    return TTTensor._new(tt.ctx, lib().ttr_round_fixed_krp, tt.ctx._h, tt._h, _i64(target_ranks),
+                         C.c_int64(len(target_ranks)), C.c_uint64(seed), C.c_int(rng))
+
+
+@dataclass
+class AdaptiveConfig:
+    """ttround::AdaptiveConfig (round_rand.hpp:18-25)."""
+    tolerance: float = 1e-6
+    f_init: float = 0.1
+    f_inc: float = 0.05
+    seed: int = 0
+    known_norm: Optional[float] = None
+    max_rank_cap: Optional[Sequence[int]] = None
+    rng: int = RNG_PHILOX
+
+
+def round_adaptive_krp(tt: TTTensor, cfg: AdaptiveConfig) -> TTTensor:
+    c = _AdaptiveCfg()
+    c.tolerance, c.f_init, c.f_inc, c.seed = cfg.tolerance, cfg.f_init, cfg.f_inc, cfg.seed
+    c.has_known_norm = 1 if cfg.known_norm is not None else 0
+    c.known_norm = cfg.known_norm or 0.0
+    cap = _i64(cfg.max_rank_cap) if cfg.max_rank_cap is not None else None
+    c.max_rank_cap = C.cast(cap, C.POINTER(C.c_int64)) if cap is not None else None
+    c.rng_mode = cfg.rng
+    return TTTensor._new(tt.ctx, lib().ttr_round_adaptive_krp, tt.ctx._h, tt._h, C.byref(c))
+
+
+def round_deterministic(tt: TTTensor, eps: Optional[float] = None,
+                        target_ranks: Optional[Sequence[int]] = None) -> TTTensor:
+    if target_ranks is not None:
+        return TTTensor._new(tt.ctx, lib().ttr_round_deterministic_ranks, tt.ctx._h, tt._h, _i64(target_ranks),
+                             C.c_int64(len(target_ranks)))
+    return TTTensor._new(tt.ctx, lib().ttr_round_deterministic_tol, tt.ctx._h, tt._h, C.c_double(eps))
+
+
+def estimate_norm_krp(tt: TTTensor, width: int, seed: int, rng: int = RNG_PHILOX) -> float:
+    v = C.c_double()
+    _check(lib().ttr_estimate_norm_krp(tt.ctx._h, tt._h, C.c_int64(width), C.c_uint64(seed), C.c_int(rng),
+                                       C.byref(v)))
+    return v.value
+
+
+def krp_partial_contractions_rl(tt: TTTensor, cols: int, factors: Optional[Sequence[np.ndarray]] = None,
+                                seed: int = 0, start_mode: int = 2, col0: int = 0) -> List[np.ndarray]:
+    """W_start..W_d (r_{k-1} x cols). `factors` = Omega_start..Omega_d (n_k x cols);
+    None draws Philox factors on the device for global columns col0..col0+cols."""
+    n, r, _ = tt.shape()
+    d = len(n)
+    if factors is not None:
+        flat = np.concatenate([np.asarray(f, dtype=np.float64).T.reshape(-1) for f in factors])
+        fptr = _dptr(flat)
+    else:
+        flat, fptr = None, None
+    tot = sum(r[k - 1] * cols for k in range(start_mode, d + 1))
+    out = np.empty(max(tot, 1), dtype=np.float64)
+    _check(lib().ttr_krp_partial_contractions(tt.ctx._h, tt._h, C.c_int64(start_mode), C.c_int64(cols), fptr,
+                                              C.c_uint64(seed), C.c_int64(col0), _dptr(out)))
+    res, off = [], 0
+    for k in range(start_mode, d + 1):
+        cnt = r[k - 1] * cols
+        res.append(out[off:off + cnt].reshape(cols, r[k - 1]).T.copy())
+        off += cnt
+    return res
+
+
+def philox_factor(seed: int, mode: int, rows: int, cols: int, col0: int = 0,
+                  ctx: Optional[Context] = None) -> np.ndarray:
+    ctx = ctx or default_context()
+    out = np.empty(rows * cols, dtype=np.float64)
+    _check(lib().ttr_philox_factor(ctx._h, C.c_uint64(seed), C.c_int64(mode), C.c_int64(rows), C.c_int64(cols),
+                                   C.c_int64(col0), _dptr(out)))
+    return out.reshape(cols, rows).T.copy()
+
+
+def thin_qr(a: np.ndarray, ctx: Optional[Context] = None):
+    ctx = ctx or default_context()
+    m, n = a.shape
+    k = min(m, n)
+    flat = np.ascontiguousarray(np.asarray(a, dtype=np.float64).T).reshape(-1)
+    q = np.empty(m * k)
+    r = np.empty(k * n)
+    _check(lib().ttr_thin_qr(ctx._h, C.c_int64(m), C.c_int64(n), _dptr(flat), _dptr(q), _dptr(r)))
+    return q.reshape(k, m).T.copy(), r.reshape(n, k).T.copy()
+
+
+def gemm(a: np.ndarray, b: np.ndarray, trans_a: bool = False, ctx: Optional[Context] = None) -> np.ndarray:
+    ctx = ctx or default_context()
+    if trans_a:
+        k, m = a.shape
+    else:
+        m, k = a.shape
+    n = b.shape[1]
+    fa = np.ascontiguousarray(np.asarray(a, dtype=np.float64).T).reshape(-1)
+    fb = np.ascontiguousarray(np.asarray(b, dtype=np.float64).T).reshape(-1)
+    out = np.empty(m * n)
+    _check(lib().ttr_gemm(ctx._h, C.c_int(1 if trans_a else 0), C.c_int64(m), C.c_int64(n), C.c_int64(k),
+                          _dptr(fa), _dptr(fb), _dptr(out)))
+    return out.reshape(n, m).T.copy()

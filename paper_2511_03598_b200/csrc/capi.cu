@@ -1,0 +1,350 @@
+// capi.cu — the extern "C" boundary (include/ttround_b200.h). Catches every
+// C++ exception and maps it to a ttr_status; messages are kept per thread.
+#include <cstring>
+#include <string>
+
+#include "common.cuh"
+#include "tt_round.h"
+
+using namespace ttr;
+
+namespace {
+thread_local std::string g_last_error;
+
+template <typename F>
+ttr_status guard(F&& f) {
+    try {
+        f();
+        return TTR_OK;
+    } catch (const Error& e) {
+        g_last_error = e.what();
+        return e.status;
+    } catch (const std::bad_alloc& e) {
+        g_last_error = std::string("host allocation failed: ") + e.what();
+        return TTR_ERR_OUT_OF_MEMORY;
+    } catch (const std::exception& e) {
+        g_last_error = std::string("internal: ") + e.what();
+        return TTR_ERR_INTERNAL;
+    }
+}
+
+void need(bool ok, const char* what) {
+    if (!ok) throw Error(TTR_ERR_INVALID_ARGUMENT, std::string("InvalidArgument: ") + what);
+}
+
+std::vector<i64> vec(const int64_t* p, int64_t n) { return std::vector<i64>(p, p + n); }
+
+ttr_tt* wrap(std::unique_ptr<TTDev> t) {
+    auto* o = new ttr_tt;
+    o->t = std::move(t);
+    return o;
+}
+
+void check_same_ctx(ttr_ctx* ctx, const ttr_tt* t) {
+    need(ctx && t && t->t, "null handle");
+    need(t->t->ctx == &ctx->c, "tensor belongs to another context");
+}
+}  // namespace
+
+extern "C" {
+
+const char* ttr_last_error(void) { return g_last_error.c_str(); }
+const char* ttr_version(void) { return "ttround_b200 0.1 (sm_100a, fp64 DMMA)"; }
+
+ttr_status ttr_ctx_create(int device, void* stream, ttr_ctx** out) {
+    return guard([&] {
+        need(out != nullptr, "out is null");
+        int count = 0;
+        if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0)
+            throw Error(TTR_ERR_NO_DEVICE, "no CUDA device available");
+        need(device >= 0 && device < count, "device index out of range");
+        TTR_CUDA(cudaSetDevice(device));
+        auto* ctx = new ttr_ctx;
+        ctx->c.device = device;
+        TTR_CUDA(cudaDeviceGetAttribute(&ctx->c.sm_count, cudaDevAttrMultiProcessorCount, device));
+        if (stream) {
+            ctx->c.stream = static_cast<cudaStream_t>(stream);
+        } else {
+            TTR_CUDA(cudaStreamCreateWithFlags(&ctx->c.stream, cudaStreamNonBlocking));
+            ctx->c.own_stream = true;
+        }
+        TTR_CUDA(cudaMallocHost(reinterpret_cast<void**>(&ctx->c.host_scalars), 64 * sizeof(double)));
+        // keep freed blocks in the stream-ordered pool (no release to the OS between calls)
+        cudaMemPool_t pool;
+        TTR_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+        std::uint64_t threshold = UINT64_MAX;
+        TTR_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold));
+        *out = ctx;
+    });
+}
+
+ttr_status ttr_ctx_destroy(ttr_ctx* ctx) {
+    return guard([&] {
+        if (!ctx) return;
+        cudaSetDevice(ctx->c.device);
+        if (ctx->c.work) cudaFreeAsync(ctx->c.work, ctx->c.stream);
+        cudaStreamSynchronize(ctx->c.stream);
+        if (ctx->c.host_scalars) cudaFreeHost(ctx->c.host_scalars);
+        if (ctx->c.own_stream) cudaStreamDestroy(ctx->c.stream);
+        delete ctx;
+    });
+}
+
+ttr_status ttr_ctx_set_stream(ttr_ctx* ctx, void* stream) {
+    return guard([&] {
+        need(ctx != nullptr, "null context");
+        TTR_CUDA(cudaStreamSynchronize(ctx->c.stream));
+        if (ctx->c.own_stream) {
+            TTR_CUDA(cudaStreamDestroy(ctx->c.stream));
+            ctx->c.own_stream = false;
+        }
+        if (stream) {
+            ctx->c.stream = static_cast<cudaStream_t>(stream);
+        } else {
+            TTR_CUDA(cudaStreamCreateWithFlags(&ctx->c.stream, cudaStreamNonBlocking));
+            ctx->c.own_stream = true;
+        }
+    });
+}
+
+ttr_status ttr_ctx_synchronize(ttr_ctx* ctx) {
+    return guard([&] {
+        need(ctx != nullptr, "null context");
+        TTR_CUDA(cudaStreamSynchronize(ctx->c.stream));
+    });
+}
+
+ttr_status ttr_ctx_kernel_launches(ttr_ctx* ctx, uint64_t* out) {
+    return guard([&] {
+        need(ctx && out, "null argument");
+        *out = ctx->c.launches;
+    });
+}
+
+ttr_status ttr_tt_upload(ttr_ctx* ctx, int64_t d, const int64_t* n, const int64_t* r, const double* host, ttr_tt** out) {
+    return guard([&] {
+        need(ctx && out, "null argument");
+        if (d < 1) fail(Errc::EmptyCoreList, "TT tensor needs at least one core");
+        need(n && r && host, "null argument");
+        auto t = std::make_unique<TTDev>(ctx->c, vec(n, d), vec(r, d + 1));
+        t->upload(host);
+        TTR_CUDA(cudaStreamSynchronize(ctx->c.stream));
+        *out = wrap(std::move(t));
+    });
+}
+
+ttr_status ttr_tt_from_device(ttr_ctx* ctx, int64_t d, const int64_t* n, const int64_t* r, const double* dev, ttr_tt** out) {
+    return guard([&] {
+        need(ctx && out && n && r && dev, "null argument");
+        if (d < 1) fail(Errc::EmptyCoreList, "TT tensor needs at least one core");
+        auto t = std::make_unique<TTDev>(ctx->c, vec(n, d), vec(r, d + 1));
+        i64 o = 0;
+        for (i64 k = 0; k < d; ++k) {
+            TTR_CUDA(cudaMemcpyAsync(t->core(k), dev + o, sizeof(double) * t->core_size(k), cudaMemcpyDeviceToDevice,
+                                     ctx->c.stream));
+            o += t->core_size(k);
+        }
+        *out = wrap(std::move(t));
+    });
+}
+
+ttr_status ttr_tt_shape(const ttr_tt* tt, int64_t* d, int64_t* n, int64_t* r, int64_t* total) {
+    return guard([&] {
+        need(tt && tt->t, "null tensor");
+        const TTDev& t = *tt->t;
+        if (d) *d = t.d();
+        if (n) for (i64 k = 0; k < t.d(); ++k) n[k] = t.n[k];
+        if (r) for (i64 k = 0; k <= t.d(); ++k) r[k] = t.r[k];
+        if (total) *total = t.total();
+    });
+}
+
+ttr_status ttr_tt_download(ttr_ctx* ctx, const ttr_tt* tt, double* host) {
+    return guard([&] {
+        check_same_ctx(ctx, tt);
+        need(host != nullptr, "null output");
+        tt->t->download(host);
+    });
+}
+
+ttr_status ttr_tt_core_ptr(const ttr_tt* tt, int64_t k, const double** ptr) {
+    return guard([&] {
+        need(tt && tt->t && ptr, "null argument");
+        if (k < 0 || k >= tt->t->d()) fail(Errc::IndexOutOfRange, "core index out of range");
+        *ptr = tt->t->core(k);
+    });
+}
+
+ttr_status ttr_tt_destroy(ttr_tt* tt) {
+    return guard([&] { delete tt; });
+}
+
+ttr_status ttr_tt_random_philox(ttr_ctx* ctx, int64_t d, const int64_t* n, const int64_t* r, uint64_t seed, ttr_tt** out) {
+    return guard([&] {
+        need(ctx && out && n && r, "null argument");
+        if (d < 1) fail(Errc::InvalidRankChain, "rank chain length must be d+1");
+        *out = wrap(random_philox_tt(ctx->c, vec(n, d), vec(r, d + 1), seed));
+    });
+}
+
+ttr_status ttr_tt_formal_sum(ttr_ctx* ctx, const ttr_tt* const* terms, int count, ttr_tt** out) {
+    return guard([&] {
+        need(ctx && out, "null argument");
+        std::vector<const TTDev*> ts;
+        for (int i = 0; i < count; ++i) {
+            check_same_ctx(ctx, terms[i]);
+            ts.push_back(terms[i]->t.get());
+        }
+        *out = wrap(formal_sum(ctx->c, ts));
+    });
+}
+
+ttr_status ttr_tt_scale(ttr_ctx* ctx, ttr_tt* tt, double alpha) {
+    return guard([&] {
+        check_same_ctx(ctx, tt);
+        scale_tt(ctx->c, *tt->t, alpha);
+    });
+}
+
+ttr_status ttr_norm_exact(ttr_ctx* ctx, const ttr_tt* tt, double* out) {
+    return guard([&] {
+        check_same_ctx(ctx, tt);
+        need(out != nullptr, "null output");
+        *out = norm_exact(ctx->c, *tt->t);
+    });
+}
+
+ttr_status ttr_relative_error(ttr_ctx* ctx, const ttr_tt* a, const ttr_tt* b, double* out) {
+    return guard([&] {
+        check_same_ctx(ctx, a);
+        check_same_ctx(ctx, b);
+        need(out != nullptr, "null output");
+        if (a->t->n != b->t->n) fail(Errc::ModeSizeMismatch, "formal sum mode sizes differ");
+        *out = relative_error(ctx->c, *a->t, *b->t);
+    });
+}
+
+ttr_status ttr_round_fixed_krp(ttr_ctx* ctx, const ttr_tt* tt, const int64_t* ranks, int64_t count, uint64_t seed,
+                               int rng_mode, ttr_tt** out) {
+    return guard([&] {
+        check_same_ctx(ctx, tt);
+        need(out != nullptr, "null output");
+        need(rng_mode == TTR_RNG_PHILOX || rng_mode == TTR_RNG_XOSHIRO, "unknown rng mode");
+        if (count < 0 || (count > 0 && !ranks)) fail(Errc::InvalidRanks, "expected d-1 target ranks");
+        *out = wrap(round_fixed_krp(ctx->c, *tt->t, vec(ranks, count), seed, rng_mode));
+    });
+}
+
+ttr_status ttr_round_adaptive_krp(ttr_ctx* ctx, const ttr_tt* tt, const ttr_adaptive_cfg* cfg, ttr_tt** out) {
+    return guard([&] {
+        check_same_ctx(ctx, tt);
+        need(cfg && out, "null argument");
+        need(cfg->rng_mode == TTR_RNG_PHILOX || cfg->rng_mode == TTR_RNG_XOSHIRO, "unknown rng mode");
+        AdaptiveCfg a;
+        a.tolerance = cfg->tolerance;
+        a.f_init = cfg->f_init;
+        a.f_inc = cfg->f_inc;
+        a.seed = cfg->seed;
+        a.has_known_norm = cfg->has_known_norm != 0;
+        a.known_norm = cfg->known_norm;
+        a.max_rank_cap = cfg->max_rank_cap;
+        a.rng_mode = cfg->rng_mode;
+        *out = wrap(round_adaptive_krp(ctx->c, *tt->t, a, nullptr));
+    });
+}
+
+ttr_status ttr_round_deterministic_tol(ttr_ctx* ctx, const ttr_tt* tt, double eps, ttr_tt** out) {
+    return guard([&] {
+        check_same_ctx(ctx, tt);
+        need(out != nullptr, "null output");
+        *out = wrap(round_deterministic_tol(ctx->c, *tt->t, eps));
+    });
+}
+
+ttr_status ttr_round_deterministic_ranks(ttr_ctx* ctx, const ttr_tt* tt, const int64_t* ranks, int64_t count, ttr_tt** out) {
+    return guard([&] {
+        check_same_ctx(ctx, tt);
+        need(out != nullptr, "null output");
+        if (count < 0 || (count > 0 && !ranks)) fail(Errc::InvalidRanks, "expected d-1 target ranks");
+        *out = wrap(round_deterministic_ranks(ctx->c, *tt->t, vec(ranks, count)));
+    });
+}
+
+ttr_status ttr_estimate_norm_krp(ttr_ctx* ctx, const ttr_tt* tt, int64_t width, uint64_t seed, int rng_mode, double* out) {
+    return guard([&] {
+        check_same_ctx(ctx, tt);
+        need(out != nullptr, "null output");
+        *out = estimate_norm_krp(ctx->c, *tt->t, width, seed, rng_mode);
+    });
+}
+
+ttr_status ttr_krp_partial_contractions(ttr_ctx* ctx, const ttr_tt* tt, int64_t start_mode, int64_t cols,
+                                        const double* host_factors, uint64_t seed, int64_t col0, double* host_w) {
+    return guard([&] {
+        check_same_ctx(ctx, tt);
+        need(host_w != nullptr, "null output");
+        krp_partial_contractions(ctx->c, *tt->t, start_mode, cols, host_factors, seed, col0, host_w);
+    });
+}
+
+ttr_status ttr_philox_factor(ttr_ctx* ctx, uint64_t seed, int64_t mode, int64_t rows, int64_t cols, int64_t col0,
+                             double* host_out) {
+    return guard([&] {
+        need(ctx && host_out, "null argument");
+        need(rows >= 1 && cols >= 1, "empty shape");
+        DBuf b(ctx->c, static_cast<std::size_t>(rows * cols));
+        philox_factor(ctx->c, seed, mode, rows, cols, col0, b.p, rows);
+        TTR_CUDA(cudaMemcpyAsync(host_out, b.p, sizeof(double) * rows * cols, cudaMemcpyDeviceToHost, ctx->c.stream));
+        TTR_CUDA(cudaStreamSynchronize(ctx->c.stream));
+    });
+}
+
+ttr_status ttr_thin_qr(ttr_ctx* ctx, int64_t m, int64_t n, const double* host_a, double* host_q, double* host_r) {
+    return guard([&] {
+        need(ctx && host_a, "null argument");
+        need(m >= 1 && n >= 1, "empty shape");
+        const i64 k = std::min(m, n);
+        DBuf a(ctx->c, static_cast<std::size_t>(m * n)), q(ctx->c, static_cast<std::size_t>(m * k)),
+            r(ctx->c, static_cast<std::size_t>(k * n));
+        TTR_CUDA(cudaMemcpyAsync(a.p, host_a, sizeof(double) * m * n, cudaMemcpyHostToDevice, ctx->c.stream));
+        thin_qr(ctx->c, m, n, a.p, m, q.p, m, r.p, k);
+        if (host_q) TTR_CUDA(cudaMemcpyAsync(host_q, q.p, sizeof(double) * m * k, cudaMemcpyDeviceToHost, ctx->c.stream));
+        if (host_r) TTR_CUDA(cudaMemcpyAsync(host_r, r.p, sizeof(double) * k * n, cudaMemcpyDeviceToHost, ctx->c.stream));
+        TTR_CUDA(cudaStreamSynchronize(ctx->c.stream));
+    });
+}
+
+ttr_status ttr_gemm(ttr_ctx* ctx, int trans_a, int64_t m, int64_t n, int64_t k, const double* host_a, const double* host_b,
+                    double* host_c) {
+    return guard([&] {
+        need(ctx && host_a && host_b && host_c, "null argument");
+        need(m >= 1 && n >= 1 && k >= 1, "empty shape");
+        DBuf a(ctx->c, static_cast<std::size_t>(m * k)), b(ctx->c, static_cast<std::size_t>(k * n)),
+            cc(ctx->c, static_cast<std::size_t>(m * n));
+        TTR_CUDA(cudaMemcpyAsync(a.p, host_a, sizeof(double) * m * k, cudaMemcpyHostToDevice, ctx->c.stream));
+        TTR_CUDA(cudaMemcpyAsync(b.p, host_b, sizeof(double) * k * n, cudaMemcpyHostToDevice, ctx->c.stream));
+        gemm(ctx->c, trans_a != 0, m, n, k, 1.0, a.p, trans_a ? k : m, b.p, k, 0.0, cc.p, m);
+        TTR_CUDA(cudaMemcpyAsync(host_c, cc.p, sizeof(double) * m * n, cudaMemcpyDeviceToHost, ctx->c.stream));
+        TTR_CUDA(cudaStreamSynchronize(ctx->c.stream));
+    });
+}
+
+ttr_status ttr_counters(ttr_ctx* ctx, ttr_counts* out) {
+    return guard([&] {
+        need(ctx && out, "null argument");
+        out->gemm = ctx->c.counts.gemm;
+        out->qr = ctx->c.counts.qr;
+        out->svd = ctx->c.counts.svd;
+        out->sketch = ctx->c.counts.sketch;
+        out->rng = ctx->c.counts.rng;
+    });
+}
+
+ttr_status ttr_counters_reset(ttr_ctx* ctx) {
+    return guard([&] {
+        need(ctx != nullptr, "null context");
+        ctx->c.counts = Counts{};
+    });
+}
+
+}  // extern "C"

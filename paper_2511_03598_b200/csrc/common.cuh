@@ -1,0 +1,150 @@
+// common.cuh — shared internals of libttround_b200: error plumbing, the
+// context (stream, stream-ordered allocator, counters) and device views.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/ttround_b200.h"
+
+namespace ttr {
+
+using i64 = std::int64_t;
+
+// Mirrors ttround::Errc (proj/core/include/ttround/types.hpp:15-31); the
+// status code at the C ABI is 1 + the enumerator.
+enum class Errc {
+    RankChainMismatch, BoundaryRankNotOne, EmptyCoreList, IndexOutOfRange, DenseTooLarge,
+    ModeSizeMismatch, EmptyTermList, InvalidRankChain, SVDFailure, InvalidRanks,
+    NotLeftOrthogonal, InvalidGrid, Breakdown, InvalidArgument, IoError,
+};
+const char* errc_name(Errc c);
+
+struct Error : std::runtime_error {
+    int status;
+    Error(int s, const std::string& m) : std::runtime_error(m), status(s) {}
+};
+[[noreturn]] inline void fail(Errc c, const std::string& what) {
+    throw Error(1 + static_cast<int>(c), std::string(errc_name(c)) + ": " + what);
+}
+[[noreturn]] void cuda_fail(cudaError_t e, const char* expr, const char* file, int line);
+
+#define TTR_CUDA(expr)                                                   \
+    do {                                                                 \
+        cudaError_t _e = (expr);                                         \
+        if (_e != cudaSuccess) ::ttr::cuda_fail(_e, #expr, __FILE__, __LINE__); \
+    } while (0)
+
+// Algorithmic flop counters with the reference's charges (linalg.cpp:14-18).
+struct Counts {
+    std::uint64_t gemm = 0, qr = 0, svd = 0, sketch = 0, rng = 0;
+};
+
+struct Ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    int sm_count = 148;
+    Counts counts;
+    int sketch_depth = 0;
+    std::uint64_t launches = 0;
+    // scratch for split-K partials, grown on demand (stream-ordered)
+    double* work = nullptr;
+    std::size_t work_bytes = 0;
+    // small pinned host staging buffer for scalars
+    double* host_scalars = nullptr;
+
+    void charge_gemm(std::uint64_t f) { counts.gemm += f; if (sketch_depth) counts.sketch += f; }
+    void charge_qr(std::uint64_t f) { counts.qr += f; if (sketch_depth) counts.sketch += f; }
+    void charge_svd(std::uint64_t f) { counts.svd += f; if (sketch_depth) counts.sketch += f; }
+    double* scratch(std::size_t bytes);
+    void launched(int k = 1) { launches += static_cast<std::uint64_t>(k); }
+};
+
+struct SketchScope {
+    Ctx& c;
+    explicit SketchScope(Ctx& cc) : c(cc) { ++c.sketch_depth; }
+    ~SketchScope() { --c.sketch_depth; }
+};
+
+// Stream-ordered device allocation (cudaMallocAsync pool on the ctx stream).
+double* dalloc(Ctx& c, std::size_t count);
+void dfree(Ctx& c, void* p);
+
+// Owning device buffer.
+struct DBuf {
+    Ctx* c = nullptr;
+    double* p = nullptr;
+    std::size_t n = 0;
+    DBuf() = default;
+    DBuf(Ctx& cc, std::size_t count) : c(&cc), p(dalloc(cc, count)), n(count) {}
+    DBuf(const DBuf&) = delete;
+    DBuf& operator=(const DBuf&) = delete;
+    DBuf(DBuf&& o) noexcept : c(o.c), p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+    DBuf& operator=(DBuf&& o) noexcept {
+        if (this != &o) { reset(); c = o.c; p = o.p; n = o.n; o.p = nullptr; o.n = 0; }
+        return *this;
+    }
+    ~DBuf() { reset(); }
+    void reset() { if (p && c) dfree(*c, p); p = nullptr; n = 0; }
+};
+
+// Column-major device matrix view.
+struct DMat {
+    double* p = nullptr;
+    i64 rows = 0, cols = 0, ld = 1;
+    double* col(i64 j) const { return p + j * ld; }
+};
+
+inline i64 round_up(i64 v, i64 m) { return (v + m - 1) / m * m; }
+inline i64 even_ld(i64 rows) { return rows < 1 ? 2 : round_up(rows, 2); }
+
+// ---- kernels (gemm_dmma.cu) -------------------------------------------------
+// C = alpha * op(A) * B + beta * C, fp64 on the DMMA tensor pipe.
+// op(A) = A (M x K, lda) or A^T (A stored K x M, lda). B is K x N (ldb).
+void gemm(Ctx& c, bool trans_a, i64 M, i64 N, i64 K, double alpha, const double* A, i64 lda,
+          const double* B, i64 ldb, double beta, double* C, i64 ldc, bool count = true);
+// KRP sketch step (sketch.cpp:15-40 restated as one GEMM):
+//   W_out(:, c) = sum_{g, j} H(X)(:, g*n + j) * Omega(j, c) * Wt(c, g)
+// X is the r_left x n x r_right core (H unfolding, ld = r_left), Omega is
+// n x N (ldo), Wt is the N x r_right transpose of W_{k+1} (ldwt; a column of
+// ones for the last core). Writes W_out (r_left x N, ldw) and its transpose
+// Wt_out (N x r_left, ldwt_out) if non-null.
+void krp_step(Ctx& c, i64 r_left, i64 n, i64 r_right, i64 N, const double* X, const double* Omega,
+              i64 ldo, const double* Wt, i64 ldwt, double* W_out, i64 ldw, double* Wt_out, i64 ldwt_out,
+              bool last_core);
+
+// ---- kernels (dense_ops.cu) -------------------------------------------------
+void philox_factor(Ctx& c, std::uint64_t seed, i64 mode, i64 rows, i64 cols, i64 col0, double* out, i64 ld);
+void fill(Ctx& c, double* p, std::size_t count, double v);
+void copy_matrix(Ctx& c, i64 rows, i64 cols, const double* src, i64 lds, double* dst, i64 ldd);
+void transpose(Ctx& c, i64 rows, i64 cols, const double* src, i64 lds, double* dst, i64 ldd);
+void scale(Ctx& c, double* p, std::size_t count, double alpha);
+void axpy_matrix(Ctx& c, i64 rows, i64 cols, double alpha, const double* x, i64 ldx, double* y, i64 ldy);
+// Deterministic Frobenius norm of a rows x cols matrix; result stays on device.
+void frob_norm_sq(Ctx& c, i64 rows, i64 cols, const double* a, i64 lda, double* d_out);
+double frob_norm(Ctx& c, i64 rows, i64 cols, const double* a, i64 lda);
+void random_normal(Ctx& c, std::uint64_t seed, std::uint32_t stream_tag, double* out, std::size_t count, double sigma);
+// out[row_off + i, j, col_off + g] = src(i, j, g) (formal-sum block placement)
+void place_block(Ctx& c, const double* src, i64 rl, i64 n, i64 rr, double* dst, i64 RL, i64 RR, i64 row_off, i64 col_off);
+// columns j of V-unfolding from H (k-th slab etc.)
+void scale_rows_cols(Ctx& c, double* a, i64 rows, i64 cols, i64 lda, const double* row_scale, const double* col_scale);
+
+// ---- QR (qr.cu) -------------------------------------------------------------
+// Thin Householder QR with explicit Q of an m x n matrix (m >= n assumed by
+// callers; for m < n only the first m columns are factored). Q: m x min(m,n)
+// (ldq), R (optional): min(m,n) x n upper trapezoidal (ldr). A is not modified.
+void thin_qr(Ctx& c, i64 m, i64 n, const double* A, i64 lda, double* Q, i64 ldq, double* R, i64 ldr);
+
+// ---- SVD (svd.cu) -----------------------------------------------------------
+// Thin SVD of a small m x n matrix (m, n <= ~1024) by one-sided Jacobi on the
+// device: U (m x k), s (k, descending), V (n x k), k = min(m, n). Host copies of
+// s are returned (needed for truncation decisions).
+void svd_small(Ctx& c, i64 m, i64 n, const double* A, i64 lda, double* U, i64 ldu, double* V, i64 ldv,
+               std::vector<double>& s_host, double* d_s);
+
+}  // namespace ttr

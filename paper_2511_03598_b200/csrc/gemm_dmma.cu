@@ -1,0 +1,437 @@
+// gemm_dmma.cu — fp64 GEMM on the B200 DMMA tensor pipe, including the fused
+// KRP sketch contraction.
+//
+// sm_100a has no tcgen05 kind for fp64: fp64 tensor-core math is the
+// warp-level mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4), measured at 37.0 TF/s on
+// this pool's B200 (profiles/r01_box_probe.log; cuBLAS DGEMM 35.5 TF/s). This
+// kernel stages A and B tiles in shared memory with a multi-stage cp.async
+// pipeline and feeds DMMA from conflict-free 64-bit LDS fragments.
+//
+// KRP mode is the reference's hot loop 1 (sketch.cpp:15-40, `mttkrp_step`
+// and `contract_tail`) restated as ONE GEMM over the horizontal unfolding:
+//   W_{k-1}(:, c) = sum_{g, j} H(X_k)(:, g*n + j) * [Omega_k(j, c) * W_k(g, c)]
+// The KRP operand (W_k (.) Omega_k) is never formed in memory: a K-tile lies
+// inside one slab g (BK divides n), its B tile is the Omega_k(j0:j0+BK, cols)
+// block and the W_k(g, cols) row is applied to the B fragment in registers.
+// The reference instead re-streams the core once per column (mul_vec).
+//
+// Determinism: every output element accumulates its K range in a fixed order;
+// split-K partials are reduced in split order by a separate kernel, and the
+// split count of the KRP step depends only on (r_left, n*r_right), never on
+// the column count — so a column's value is bitwise independent of how many
+// columns are contracted together (the append-vs-one-shot property of
+// tests/test_sketch.cpp:78-98).
+#include <algorithm>
+#include <cstdio>
+
+#include "common.cuh"
+
+namespace ttr {
+namespace {
+
+struct GemmArgs {
+    int M, N, K;
+    const double* A;
+    i64 lda;
+    const double* B;  // plain: B(k, n) = B[k + n*ldb]; KRP: Omega(j, n) = B[j + n*ldb]
+    i64 ldb;
+    const double* Wt;  // KRP only: W(g, n) = Wt[n + g*ldw]
+    i64 ldw;
+    int nmode;  // KRP only: k = g*nmode + j
+    double* C;
+    i64 ldc;
+    double alpha, beta;
+    double* work;  // split-K partials [split][N][M] (ld M)
+    int ktiles_per_split;
+};
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+
+// cp.async of VEC doubles (8 or 16 bytes) with zero fill beyond `bytes`.
+template <int VEC>
+__device__ __forceinline__ void cp_async(double* dst, const double* src, int bytes) {
+    if constexpr (VEC == 2) {
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(dst)), "l"(src), "r"(bytes));
+    } else {
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(smem_u32(dst)), "l"(src), "r"(bytes));
+    }
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(c0), "+d"(c1)
+                 : "d"(a), "d"(b));
+}
+
+// KM: 0 = plain B, 1 = KRP with every K-tile inside one slab (BK | n),
+//     2 = KRP general (tiles may straddle slabs; element-wise staging).
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool AT, int KM, int VA, int VB>
+struct Cfg {
+    static constexpr int kWarpsM = BM / WM, kWarpsN = BN / WN;
+    static constexpr int kThreads = kWarpsM * kWarpsN * 32;
+    // A tile: normal -> [BK][BM+4] (m contiguous); transposed -> [BM][BK+4]
+    static constexpr int kLdA = AT ? (BK + 4) : (BM + 4);
+    static constexpr int kASize = AT ? BM * (BK + 4) : BK * (BM + 4);
+    static constexpr int kLdB = BK + 4;  // B tile [BN][BK+4] (k contiguous)
+    static constexpr int kBSize = BN * (BK + 4);
+    static constexpr int kWSize = KM == 1 ? BN : (KM == 2 ? BN * (BK + 4) : 0);
+    static constexpr int kStage = kASize + kBSize + kWSize;
+    static constexpr int kSmemBytes = STAGES * kStage * 8;
+    static_assert((BM + 4) % 16 == 4 || AT, "A pad keeps 64-bit fragment loads conflict free");
+    static_assert((BK + 4) % 16 == 4 || BK == 4, "B pad keeps 64-bit fragment loads conflict free");
+};
+
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool AT, int KM, int VA, int VB>
+__global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32)
+    dgemm_kernel(const GemmArgs p) {
+    using C_ = Cfg<BM, BN, BK, WM, WN, STAGES, AT, KM, VA, VB>;
+    constexpr int FM = WM / 8, FN = WN / 8;
+    extern __shared__ __align__(16) double smem[];
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wm0 = (warp % C_::kWarpsM) * WM, wn0 = (warp / C_::kWarpsM) * WN;
+    const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
+    const int total_kt = (p.K + BK - 1) / BK;
+    const int kt_begin = blockIdx.z * p.ktiles_per_split;
+    const int kt_end = min(total_kt, kt_begin + p.ktiles_per_split);
+    const int nk = max(0, kt_end - kt_begin);
+
+    auto load_tile = [&](int stage, int kt) {
+        double* sA = smem + stage * C_::kStage;
+        double* sB = sA + C_::kASize;
+        const int k0 = kt * BK;
+        if constexpr (!AT) {
+            constexpr int CH = BM / VA;  // chunks per column
+            for (int idx = tid; idx < BK * CH; idx += C_::kThreads) {
+                const int kk = idx / CH, r = (idx % CH) * VA;
+                const int gm = m0 + r, gk = k0 + kk;
+                int bytes = 0;
+                const double* src = p.A;
+                if (gk < p.K && gm < p.M) {
+                    bytes = 8 * min(VA, p.M - gm);
+                    src = p.A + gm + static_cast<i64>(gk) * p.lda;
+                }
+                cp_async<VA>(sA + kk * C_::kLdA + r, src, bytes);
+            }
+        } else {
+            constexpr int CH = BK / VA;
+            for (int idx = tid; idx < BM * CH; idx += C_::kThreads) {
+                const int m = idx / CH, kk = (idx % CH) * VA;
+                const int gm = m0 + m, gk = k0 + kk;
+                int bytes = 0;
+                const double* src = p.A;
+                if (gm < p.M && gk < p.K) {
+                    bytes = 8 * min(VA, p.K - gk);
+                    src = p.A + gk + static_cast<i64>(gm) * p.lda;
+                }
+                cp_async<VA>(sA + m * C_::kLdA + kk, src, bytes);
+            }
+        }
+        if constexpr (KM != 2) {
+            constexpr int CH = BK / VB;
+            int jbase = k0;
+            if constexpr (KM == 1) jbase = k0 % p.nmode;  // BK divides nmode: tile inside one slab
+            for (int idx = tid; idx < BN * CH; idx += C_::kThreads) {
+                const int n = idx / CH, kk = (idx % CH) * VB;
+                const int gn = n0 + n;
+                int bytes = 0;
+                const double* src = p.B;
+                if (gn < p.N && k0 + kk < p.K) {
+                    bytes = 8 * min(VB, p.K - (k0 + kk));
+                    src = p.B + (jbase + kk) + static_cast<i64>(gn) * p.ldb;
+                }
+                cp_async<VB>(sB + n * C_::kLdB + kk, src, bytes);
+            }
+        }
+        if constexpr (KM == 1) {
+            double* sW = sA + C_::kASize + C_::kBSize;
+            const int g = k0 / p.nmode;
+            for (int idx = tid; idx < BN / VB; idx += C_::kThreads) {
+                const int n = idx * VB, gn = n0 + n;
+                int bytes = 0;
+                const double* src = p.Wt;
+                if (gn < p.N) {
+                    bytes = 8 * min(VB, p.N - gn);
+                    src = p.Wt + gn + static_cast<i64>(g) * p.ldw;
+                }
+                cp_async<VB>(sW + n, src, bytes);
+            }
+        }
+        if constexpr (KM == 2) {
+            // element-wise: Omega(j(k), n) and W(g(k), n) for every (n, k) of the tile
+            double* sW = sA + C_::kASize + C_::kBSize;
+            for (int idx = tid; idx < BN * BK; idx += C_::kThreads) {
+                const int n = idx / BK, kk = idx % BK;
+                const int gn = n0 + n, gk = k0 + kk;
+                int bytes = 0;
+                const double* so = p.B;
+                const double* sw = p.Wt;
+                if (gn < p.N && gk < p.K) {
+                    bytes = 8;
+                    const int g = gk / p.nmode, j = gk - g * p.nmode;
+                    so = p.B + j + static_cast<i64>(gn) * p.ldb;
+                    sw = p.Wt + gn + static_cast<i64>(g) * p.ldw;
+                }
+                cp_async<1>(sB + n * C_::kLdB + kk, so, bytes);
+                cp_async<1>(sW + n * C_::kLdB + kk, sw, bytes);
+            }
+        }
+    };
+
+    double acc[FM][FN][2];
+#pragma unroll
+    for (int i = 0; i < FM; ++i)
+#pragma unroll
+        for (int j = 0; j < FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+#pragma unroll
+    for (int s = 0; s < STAGES - 1; ++s) {
+        if (s < nk) load_tile(s, kt_begin + s);
+        cp_commit();
+    }
+
+    const int fr = lane >> 2, fc = lane & 3;  // fragment row (group) / column (thread in group)
+    for (int kt = 0; kt < nk; ++kt) {
+        cp_wait<STAGES - 2>();
+        __syncthreads();
+        {
+            const int nxt = kt + STAGES - 1;
+            if (nxt < nk) load_tile(nxt % STAGES, kt_begin + nxt);
+            cp_commit();
+        }
+        const double* sA = smem + (kt % STAGES) * C_::kStage;
+        const double* sB = sA + C_::kASize;
+        double wreg[FN];
+        if constexpr (KM == 1) {
+            const double* sW = sB + C_::kBSize;
+#pragma unroll
+            for (int j = 0; j < FN; ++j) wreg[j] = sW[wn0 + j * 8 + fr];
+        }
+#pragma unroll
+        for (int k4 = 0; k4 < BK; k4 += 4) {
+            double af[FM], bf[FN];
+#pragma unroll
+            for (int i = 0; i < FM; ++i) {
+                const int m = wm0 + i * 8 + fr, k = k4 + fc;
+                af[i] = AT ? sA[m * C_::kLdA + k] : sA[k * C_::kLdA + m];
+            }
+#pragma unroll
+            for (int j = 0; j < FN; ++j) {
+                const int n = wn0 + j * 8 + fr, k = k4 + fc;
+                bf[j] = sB[n * C_::kLdB + k];
+                if constexpr (KM == 1) bf[j] *= wreg[j];
+                if constexpr (KM == 2) bf[j] *= sB[C_::kBSize + n * C_::kLdB + k];
+            }
+#pragma unroll
+            for (int i = 0; i < FM; ++i)
+#pragma unroll
+                for (int j = 0; j < FN; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+        }
+    }
+    cp_wait<0>();
+
+    // epilogue: fragment (i, j) holds rows wm0+i*8+fr, cols wn0+j*8+2*fc+{0,1}
+    const bool split = gridDim.z > 1;
+#pragma unroll
+    for (int i = 0; i < FM; ++i) {
+        const int gm = m0 + wm0 + i * 8 + fr;
+        if (gm >= p.M) continue;
+#pragma unroll
+        for (int j = 0; j < FN; ++j)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int gn = n0 + wn0 + j * 8 + 2 * fc + h;
+                if (gn >= p.N) continue;
+                if (split) {
+                    p.work[(static_cast<i64>(blockIdx.z) * p.N + gn) * p.M + gm] = acc[i][j][h];
+                } else {
+                    double* dst = p.C + gm + static_cast<i64>(gn) * p.ldc;
+                    const double v = p.alpha * acc[i][j][h];
+                    *dst = (p.beta == 0.0) ? v : fma(p.beta, *dst, v);
+                }
+            }
+    }
+}
+
+// C = alpha * sum_s work[s] + beta * C (split order fixed); optional C^T copy.
+__global__ void splitk_reduce(const double* __restrict__ work, int S, int M, int N, double alpha, double beta,
+                              double* C, i64 ldc, double* Ct, i64 ldct) {
+    const i64 total = static_cast<i64>(M) * N;
+    for (i64 idx = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; idx < total;
+         idx += static_cast<i64>(gridDim.x) * blockDim.x) {
+        const int m = static_cast<int>(idx % M), n = static_cast<int>(idx / M);
+        double s = 0.0;
+        for (int z = 0; z < S; ++z) s += work[static_cast<i64>(z) * total + idx];
+        double v = alpha * s;
+        double* dst = C + m + static_cast<i64>(n) * ldc;
+        if (beta != 0.0) v = fma(beta, *dst, v);
+        *dst = v;
+        if (Ct) Ct[n + static_cast<i64>(m) * ldct] = v;
+    }
+}
+
+__global__ void transpose_copy(const double* __restrict__ src, i64 lds, int M, int N, double* dst, i64 ldd) {
+    __shared__ double tile[32][33];
+    const int bx = blockIdx.x * 32, by = blockIdx.y * 32;
+    for (int y = threadIdx.y; y < 32; y += blockDim.y) {
+        const int m = bx + threadIdx.x, n = by + y;
+        if (m < M && n < N) tile[y][threadIdx.x] = src[m + static_cast<i64>(n) * lds];
+    }
+    __syncthreads();
+    for (int y = threadIdx.y; y < 32; y += blockDim.y) {
+        const int n = by + threadIdx.x, m = bx + y;
+        if (m < M && n < N) dst[n + static_cast<i64>(m) * ldd] = tile[threadIdx.x][y];
+    }
+}
+
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool AT, int KM, int VA, int VB>
+void launch(Ctx& c, GemmArgs& a, int splits) {
+    using C_ = Cfg<BM, BN, BK, WM, WN, STAGES, AT, KM, VA, VB>;
+    auto kern = dgemm_kernel<BM, BN, BK, WM, WN, STAGES, AT, KM, VA, VB>;
+    static bool configured = false;  // per instantiation
+    if (!configured) {
+        TTR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C_::kSmemBytes));
+        configured = true;
+    }
+    dim3 grid((a.M + BM - 1) / BM, (a.N + BN - 1) / BN, splits);
+    kern<<<grid, C_::kThreads, C_::kSmemBytes, c.stream>>>(a);
+    TTR_CUDA(cudaGetLastError());
+    c.launched();
+}
+
+constexpr int kBM = 128, kBN = 64, kWM = 32, kWN = 32, kStages = 4;
+
+template <bool AT, int KM, int BK>
+void dispatch_vec(Ctx& c, GemmArgs& a, int splits, bool va2, bool vb2) {
+    if constexpr (KM == 2) {  // element-wise B staging: only the A vector width matters
+        if (va2) launch<kBM, kBN, BK, kWM, kWN, kStages, AT, KM, 2, 1>(c, a, splits);
+        else launch<kBM, kBN, BK, kWM, kWN, kStages, AT, KM, 1, 1>(c, a, splits);
+    } else {
+        if (va2 && vb2) launch<kBM, kBN, BK, kWM, kWN, kStages, AT, KM, 2, 2>(c, a, splits);
+        else if (va2) launch<kBM, kBN, BK, kWM, kWN, kStages, AT, KM, 2, 1>(c, a, splits);
+        else if (vb2) launch<kBM, kBN, BK, kWM, kWN, kStages, AT, KM, 1, 2>(c, a, splits);
+        else launch<kBM, kBN, BK, kWM, kWN, kStages, AT, KM, 1, 1>(c, a, splits);
+    }
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<std::uintptr_t>(p) & 15) == 0; }
+
+// Grid shaping: enough CTAs to cover 2 waves of 148 SMs when the MxN tile
+// grid alone does not.
+int choose_splits(Ctx& c, i64 tiles, int total_kt) {
+    const i64 target = 2LL * c.sm_count;
+    if (tiles >= target || total_kt < 8) return 1;
+    i64 s = (target + tiles - 1) / tiles;
+    s = std::min<i64>(s, std::max(1, total_kt / 4));
+    return static_cast<int>(std::max<i64>(1, s));
+}
+
+void run_gemm(Ctx& c, bool AT, int KM, int BK, GemmArgs& a, bool va2, bool vb2, int splits, double* C, i64 ldc,
+              double alpha, double beta, double* Ct, i64 ldct) {
+    const int total_kt = (a.K + BK - 1) / BK;
+    splits = std::max(1, std::min(splits, total_kt));
+    a.ktiles_per_split = (total_kt + splits - 1) / splits;
+    splits = (total_kt + a.ktiles_per_split - 1) / a.ktiles_per_split;
+    if (splits > 1) {
+        a.work = c.scratch(static_cast<std::size_t>(splits) * a.M * a.N * sizeof(double));
+    }
+    a.C = C;
+    a.ldc = ldc;
+    a.alpha = alpha;
+    a.beta = beta;
+    if (!AT && KM == 0) dispatch_vec<false, 0, 16>(c, a, splits, va2, vb2);
+    else if (AT && KM == 0) dispatch_vec<true, 0, 16>(c, a, splits, va2, vb2);
+    else if (!AT && KM == 1 && BK == 16) dispatch_vec<false, 1, 16>(c, a, splits, va2, vb2);
+    else if (!AT && KM == 1 && BK == 4) dispatch_vec<false, 1, 4>(c, a, splits, va2, vb2);
+    else if (!AT && KM == 2) dispatch_vec<false, 2, 16>(c, a, splits, va2, vb2);
+    else throw Error(TTR_ERR_INTERNAL, "unsupported gemm configuration");
+    if (splits > 1) {
+        const i64 total = static_cast<i64>(a.M) * a.N;
+        const int blocks = static_cast<int>(std::min<i64>((total + 255) / 256, 4LL * c.sm_count));
+        splitk_reduce<<<blocks, 256, 0, c.stream>>>(a.work, splits, a.M, a.N, alpha, beta, C, ldc, Ct, ldct);
+        TTR_CUDA(cudaGetLastError());
+        c.launched();
+    } else if (Ct) {
+        dim3 grid((a.M + 31) / 32, (a.N + 31) / 32);
+        transpose_copy<<<grid, dim3(32, 8), 0, c.stream>>>(C, ldc, a.M, a.N, Ct, ldct);
+        TTR_CUDA(cudaGetLastError());
+        c.launched();
+    }
+}
+
+}  // namespace
+
+void gemm(Ctx& c, bool trans_a, i64 M, i64 N, i64 K, double alpha, const double* A, i64 lda, const double* B,
+          i64 ldb, double beta, double* C, i64 ldc, bool count) {
+    if (M <= 0 || N <= 0) return;
+    if (count) c.charge_gemm(2ULL * static_cast<std::uint64_t>(M) * N * K);
+    if (K <= 0) {
+        if (beta == 0.0) {
+            for (i64 j = 0; j < N; ++j) TTR_CUDA(cudaMemsetAsync(C + j * ldc, 0, sizeof(double) * M, c.stream));
+        } else {
+            for (i64 j = 0; j < N; ++j) scale(c, C + j * ldc, static_cast<std::size_t>(M), beta);
+        }
+        return;
+    }
+    GemmArgs a{};
+    a.M = static_cast<int>(M);
+    a.N = static_cast<int>(N);
+    a.K = static_cast<int>(K);
+    a.A = A;
+    a.lda = lda;
+    a.B = B;
+    a.ldb = ldb;
+    const bool va2 = aligned16(A) && (lda % 2 == 0);
+    const bool vb2 = aligned16(B) && (ldb % 2 == 0);
+    const i64 tiles = ((M + kBM - 1) / kBM) * ((N + kBN - 1) / kBN);
+    const int total_kt = static_cast<int>((K + 15) / 16);
+    const int splits = choose_splits(c, tiles, total_kt);
+    run_gemm(c, trans_a, 0, 16, a, va2, vb2, splits, C, ldc, alpha, beta, nullptr, 0);
+}
+
+void krp_step(Ctx& c, i64 r_left, i64 n, i64 r_right, i64 N, const double* X, const double* Omega, i64 ldo,
+              const double* Wt, i64 ldwt, double* W_out, i64 ldw, double* Wt_out, i64 ldwt_out, bool last_core) {
+    if (r_left <= 0 || N <= 0) return;
+    // reference charges: r_right mul_vec of (r_left x n) + one (r_left x r_right) per column
+    // (sketch.cpp:19-23; for the last core one GEMM 2*r_left*n*N, sketch.cpp:34)
+    if (last_core)
+        c.charge_gemm(2ULL * r_left * n * N);
+    else
+        c.charge_gemm(static_cast<std::uint64_t>(N) * (2ULL * r_right * r_left * n + 2ULL * r_left * r_right));
+    GemmArgs a{};
+    a.M = static_cast<int>(r_left);
+    a.N = static_cast<int>(N);
+    a.K = static_cast<int>(n * r_right);
+    a.A = X;
+    a.lda = r_left;
+    a.B = Omega;
+    a.ldb = ldo;
+    a.Wt = Wt;
+    a.ldw = ldwt;
+    a.nmode = static_cast<int>(n);
+    // KM 1 when a K-tile always sits inside one slab, else the general path
+    const int KM = (n % 16 == 0 || n % 4 == 0) ? 1 : 2;
+    const int BK = (KM == 1 && n % 16 != 0) ? 4 : 16;
+    const bool va2 = aligned16(X) && (r_left % 2 == 0);
+    const bool vb2 = aligned16(Omega) && (ldo % 2 == 0) && aligned16(Wt) && (ldwt % 2 == 0);
+    // split count from (r_left, K) only: column results independent of N
+    const i64 mtiles = (r_left + kBM - 1) / kBM;
+    const int total_kt = static_cast<int>((a.K + BK - 1) / BK);
+    int splits = 1;
+    {
+        const i64 target = 4LL * c.sm_count;
+        if (mtiles < target && total_kt >= 8) {
+            i64 s = (target + mtiles - 1) / mtiles;
+            s = std::min<i64>(s, std::max(1, total_kt / 8));
+            splits = static_cast<int>(std::max<i64>(1, s));
+        }
+    }
+    run_gemm(c, false, KM, BK, a, va2, vb2, splits, W_out, ldw, 1.0, 0.0, Wt_out, ldwt_out);
+}
+
+}  // namespace ttr

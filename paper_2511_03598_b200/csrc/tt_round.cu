@@ -1,0 +1,502 @@
+// tt_round.cu — host orchestration of the rounding algorithms over
+// device-resident TT cores. Each function restates the reference algorithm
+// (cited file:line) with every dense step running as a CUDA kernel on the
+// context's stream; the host only sequences launches and, in the adaptive
+// loop, reads back the one scalar that drives each stopping decision.
+#include <algorithm>
+#include <array>
+#include <cmath>
+#include <cstring>
+#include <limits>
+
+#include "common.cuh"
+#include "rng_host.h"
+#include "tt_round.h"
+
+namespace ttr {
+
+const char* errc_name(Errc c) {
+    static const char* names[] = {"RankChainMismatch", "BoundaryRankNotOne", "EmptyCoreList", "IndexOutOfRange",
+                                  "DenseTooLarge",     "ModeSizeMismatch",   "EmptyTermList", "InvalidRankChain",
+                                  "SVDFailure",        "InvalidRanks",       "NotLeftOrthogonal", "InvalidGrid",
+                                  "Breakdown",         "InvalidArgument",    "IoError"};
+    const int i = static_cast<int>(c);
+    return (i >= 0 && i < 15) ? names[i] : "UnknownError";
+}
+
+void cuda_fail(cudaError_t e, const char* expr, const char* file, int line) {
+    const int status = (e == cudaErrorMemoryAllocation) ? TTR_ERR_OUT_OF_MEMORY : TTR_ERR_CUDA;
+    throw Error(status, std::string("CUDA error ") + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ") in " +
+                            expr + " at " + file + ":" + std::to_string(line));
+}
+
+double* dalloc(Ctx& c, std::size_t count) {
+    if (count == 0) count = 1;
+    void* p = nullptr;
+    TTR_CUDA(cudaMallocAsync(&p, count * sizeof(double), c.stream));
+    return static_cast<double*>(p);
+}
+void dfree(Ctx& c, void* p) {
+    if (p) cudaFreeAsync(p, c.stream);
+}
+
+double* Ctx::scratch(std::size_t bytes) {
+    if (bytes > work_bytes) {
+        if (work) TTR_CUDA(cudaFreeAsync(work, stream));
+        const std::size_t grow = std::max(bytes, work_bytes * 2);
+        TTR_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&work), grow, stream));
+        work_bytes = grow;
+    }
+    return work;
+}
+
+// ---------------------------------------------------------------------------
+// TT container
+TTDev::TTDev(Ctx& c, const std::vector<i64>& n_, const std::vector<i64>& r_) : ctx(&c), n(n_), r(r_) {
+    const i64 d = static_cast<i64>(n.size());
+    if (d < 1) fail(Errc::EmptyCoreList, "TT tensor needs at least one core");
+    if (static_cast<i64>(r.size()) != d + 1) fail(Errc::InvalidRankChain, "rank chain length must be d+1");
+    if (r.front() != 1 || r.back() != 1) fail(Errc::BoundaryRankNotOne, "boundary TT ranks must be 1");
+    for (i64 k = 0; k <= d; ++k)
+        if (r[k] < 1) fail(Errc::InvalidArgument, "core dimensions must be positive");
+    for (i64 k = 0; k < d; ++k)
+        if (n[k] < 1) fail(Errc::InvalidArgument, "core dimensions must be positive");
+    off.resize(d + 1);
+    i64 o = 0;
+    for (i64 k = 0; k < d; ++k) {
+        off[k] = o;
+        o += round_up(r[k] * n[k] * r[k + 1], 32);  // 256-byte aligned cores
+    }
+    off[d] = o;
+    buf = DBuf(c, static_cast<std::size_t>(o));
+}
+
+i64 TTDev::total() const {
+    i64 t = 0;
+    for (i64 k = 0; k < d(); ++k) t += core_size(k);
+    return t;
+}
+
+i64 TTDev::max_rank() const { return *std::max_element(r.begin(), r.end()); }
+
+void TTDev::upload(const double* host) {
+    i64 o = 0;
+    for (i64 k = 0; k < d(); ++k) {
+        TTR_CUDA(cudaMemcpyAsync(core(k), host + o, sizeof(double) * core_size(k), cudaMemcpyHostToDevice, ctx->stream));
+        o += core_size(k);
+    }
+}
+void TTDev::download(double* host) const {
+    i64 o = 0;
+    for (i64 k = 0; k < d(); ++k) {
+        TTR_CUDA(cudaMemcpyAsync(host + o, core(k), sizeof(double) * core_size(k), cudaMemcpyDeviceToHost, ctx->stream));
+        o += core_size(k);
+    }
+    TTR_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+std::unique_ptr<TTDev> copy_tt(Ctx& c, const TTDev& t) {
+    auto out = std::make_unique<TTDev>(c, t.n, t.r);
+    TTR_CUDA(cudaMemcpyAsync(out->buf.p, t.buf.p, sizeof(double) * t.off.back(), cudaMemcpyDeviceToDevice, c.stream));
+    return out;
+}
+
+// ---------------------------------------------------------------------------
+// construction / TT arithmetic — proj/core/src/tensor.cpp
+std::unique_ptr<TTDev> random_philox_tt(Ctx& c, const std::vector<i64>& n, const std::vector<i64>& r, std::uint64_t seed) {
+    auto t = std::make_unique<TTDev>(c, n, r);
+    for (i64 k = 0; k < t->d(); ++k) {
+        const double sigma = 1.0 / std::sqrt(static_cast<double>(r[k]) * n[k] * r[k + 1]);  // tensor.cpp:236
+        random_normal(c, seed, static_cast<std::uint32_t>(1000 + k), t->core(k), static_cast<std::size_t>(t->core_size(k)), sigma);
+    }
+    return t;
+}
+
+std::unique_ptr<TTDev> formal_sum(Ctx& c, const std::vector<const TTDev*>& terms) {  // tensor.cpp:176-215
+    if (terms.empty()) fail(Errc::EmptyTermList, "formal sum of no terms");
+    const auto& modes = terms.front()->n;
+    for (auto* t : terms)
+        if (t->n != modes) fail(Errc::ModeSizeMismatch, "formal sum mode sizes differ");
+    if (terms.size() == 1) return copy_tt(c, *terms.front());
+    const i64 d = static_cast<i64>(modes.size());
+    std::vector<i64> r(d + 1, 0);
+    r[0] = r[d] = 1;
+    for (i64 k = 1; k < d; ++k)
+        for (auto* t : terms) r[k] += t->r[k];
+    if (d == 1) {
+        auto out = std::make_unique<TTDev>(c, modes, r);
+        TTR_CUDA(cudaMemsetAsync(out->core(0), 0, sizeof(double) * out->core_size(0), c.stream));
+        for (auto* t : terms) axpy_matrix(c, modes[0], 1, 1.0, t->core(0), modes[0], out->core(0), modes[0]);
+        return out;
+    }
+    auto out = std::make_unique<TTDev>(c, modes, r);
+    TTR_CUDA(cudaMemsetAsync(out->buf.p, 0, sizeof(double) * out->off.back(), c.stream));
+    for (i64 k = 0; k < d; ++k) {
+        i64 ro = 0, co = 0;
+        for (auto* t : terms) {
+            place_block(c, t->core(k), t->r[k], modes[k], t->r[k + 1], out->core(k), r[k], r[k + 1], ro, co);
+            if (k > 0) ro += t->r[k];
+            if (k < d - 1) co += t->r[k + 1];
+        }
+    }
+    return out;
+}
+
+void scale_tt(Ctx& c, TTDev& t, double alpha) {  // tensor.cpp:258-262 (in place)
+    scale(c, t.core(0), static_cast<std::size_t>(t.core_size(0)), alpha);
+}
+
+// Right-to-left orthogonalisation (orthogonalize.cpp:13-26). With
+// keep_q == false only the R factors are formed (norm_exact needs the first
+// core only).
+static std::unique_ptr<TTDev> orthogonalize_rl(Ctx& c, const TTDev& t, bool keep_q) {
+    const i64 d = t.d();
+    // ranks shrink to min(n_k*r_k, r_{k-1}) from the right
+    std::vector<i64> r = t.r;
+    for (i64 k = d - 1; k >= 1; --k) r[k] = std::min(t.r[k], t.n[k] * r[k + 1]);
+    auto out = std::make_unique<TTDev>(c, t.n, r);
+    // working copy of the current core k-1 (grows from the right)
+    i64 max_core = 0;
+    for (i64 k = 0; k < d; ++k) max_core = std::max(max_core, t.r[k] * t.n[k] * r[k + 1]);
+    DBuf cur(c, static_cast<std::size_t>(max_core));
+    DBuf ht(c, static_cast<std::size_t>(max_core));
+    i64 maxr = t.max_rank();
+    DBuf R(c, static_cast<std::size_t>(maxr * maxr));
+    DBuf Rt(c, static_cast<std::size_t>(maxr * maxr));
+    DBuf Q(c, keep_q ? static_cast<std::size_t>(max_core) : 1);
+    // cur = core d-1
+    copy_matrix(c, t.core_size(d - 1), 1, t.core(d - 1), t.core_size(d - 1), cur.p, t.core_size(d - 1));
+    for (i64 k = d - 1; k >= 1; --k) {
+        const i64 rl = t.r[k], nk = t.n[k], rr = r[k + 1];
+        const i64 rows = nk * rr, kk = std::min(rows, rl);  // H^T is (n*rr) x rl
+        transpose(c, rl, rows, cur.p, rl, ht.p, rows);
+        thin_qr(c, rows, rl, ht.p, rows, keep_q ? Q.p : nullptr, rows, R.p, kk);
+        if (keep_q) transpose(c, rows, kk, Q.p, rows, out->core(k), kk);  // H(Y_k) = Q^T
+        // cores[k-1] = V(cores[k-1]) * R^T   (contract_third, internal.hpp:15-17)
+        transpose(c, kk, rl, R.p, kk, Rt.p, rl);
+        const i64 rl2 = t.r[k - 1], n2 = t.n[k - 1];
+        gemm(c, false, rl2 * n2, kk, rl, 1.0, t.core(k - 1), rl2 * n2, Rt.p, rl, 0.0, cur.p, rl2 * n2);
+    }
+    copy_matrix(c, out->core_size(0), 1, cur.p, out->core_size(0), out->core(0), out->core_size(0));
+    return out;
+}
+
+std::unique_ptr<TTDev> orthogonalize_rl_public(Ctx& c, const TTDev& t) { return orthogonalize_rl(c, t, true); }
+
+double norm_exact(Ctx& c, const TTDev& t) {  // orthogonalize.cpp:67-71
+    if (t.d() == 1) return frob_norm(c, t.core_size(0), 1, t.core(0), t.core_size(0));
+    auto o = orthogonalize_rl(c, t, false);
+    return frob_norm(c, o->core_size(0), 1, o->core(0), o->core_size(0));
+}
+
+double relative_error(Ctx& c, const TTDev& a, const TTDev& b) {  // tensor.cpp:264-268
+    const double na = norm_exact(c, a);
+    auto nb = copy_tt(c, b);
+    scale_tt(c, *nb, -1.0);
+    auto diff = formal_sum(c, {&a, nb.get()});
+    const double nd = norm_exact(c, *diff);
+    return na == 0.0 ? nd : nd / na;
+}
+
+// ---------------------------------------------------------------------------
+// KRP sketch state — sketch.cpp:44-92. Factors and contractions of modes
+// start..d with a column capacity so that adaptive appends are in place.
+struct Sketch {
+    Ctx& c;
+    const TTDev& t;
+    i64 cap, cols = 0;
+    std::vector<DBuf> omega;  // index k (1-based mode), n_k x cap, ld ldo[k]
+    std::vector<i64> ldo;
+    std::vector<DBuf> W;      // r_{k-1} x cap, ld ldw[k]
+    std::vector<i64> ldw;
+    std::vector<DBuf> Wt;     // cap x r_{k-1}, ld cap_even
+    i64 ldwt;
+    DBuf ones;
+    std::vector<i64> width;   // current column count per mode
+    int rng_mode;
+    std::uint64_t seed;
+    XoshiroGauss xo;
+
+    Sketch(Ctx& cc, const TTDev& tt, i64 capacity, int mode, std::uint64_t s)
+        : c(cc), t(tt), cap(capacity), rng_mode(mode), seed(s), xo(s) {
+        const i64 d = t.d();
+        omega.resize(d + 1);
+        W.resize(d + 1);
+        Wt.resize(d + 2);
+        ldo.assign(d + 1, 0);
+        ldw.assign(d + 1, 0);
+        width.assign(d + 2, 0);
+        ldwt = even_ld(cap);
+        for (i64 k = 2; k <= d; ++k) {
+            ldo[k] = even_ld(t.n[k - 1]);
+            omega[k] = DBuf(c, static_cast<std::size_t>(ldo[k] * cap));
+            ldw[k] = even_ld(t.r[k - 1]);
+            W[k] = DBuf(c, static_cast<std::size_t>(ldw[k] * cap));
+            if (k >= 3) Wt[k] = DBuf(c, static_cast<std::size_t>(ldwt * t.r[k - 1]));
+        }
+        ones = DBuf(c, static_cast<std::size_t>(ldwt));
+        fill(c, ones.p, static_cast<std::size_t>(ldwt), 1.0);
+    }
+
+    // Draw `extra` fresh columns for modes start..d (draw_gaussian_factors,
+    // sketch.cpp:44-56, in the reference's order) and contract them
+    // (contract_tail, sketch.cpp:29-40), appending to W_start..W_d.
+    void append(i64 start, i64 extra) {
+        const i64 d = t.d();
+        const i64 col0 = width[d];
+        if (col0 + extra > cap) throw Error(TTR_ERR_INTERNAL, "sketch capacity exceeded");
+        for (i64 k = start; k <= d; ++k) {
+            const i64 nk = t.n[k - 1];
+            double* dst = omega[k].p + col0 * ldo[k];
+            if (rng_mode == TTR_RNG_PHILOX) {
+                philox_factor(c, seed, k, nk, extra, col0, dst, ldo[k]);
+            } else {
+                auto host = xo.matrix(nk, extra);
+                c.counts.rng += static_cast<std::uint64_t>(nk * extra);
+                for (i64 j = 0; j < extra; ++j)
+                    TTR_CUDA(cudaMemcpyAsync(dst + j * ldo[k], host.data() + j * nk, sizeof(double) * nk,
+                                             cudaMemcpyHostToDevice, c.stream));
+                TTR_CUDA(cudaStreamSynchronize(c.stream));  // host staging buffer lifetime
+            }
+        }
+        SketchScope scope(c);
+        for (i64 k = d; k >= start; --k) {
+            const i64 rl = t.r[k - 1], nk = t.n[k - 1], rr = t.r[k];
+            const double* wt_next = (k == d) ? ones.p : Wt[k + 1].p + col0;
+            const i64 ld_next = ldwt;
+            double* wt_out = (k >= 3) ? Wt[k].p + col0 : nullptr;
+            krp_step(c, rl, nk, rr, extra, t.core(k - 1), omega[k].p + col0 * ldo[k], ldo[k], k == d ? ones.p : wt_next,
+                     ld_next, W[k].p + col0 * ldw[k], ldw[k], wt_out, ldwt, k == d);
+            width[k] = col0 + extra;
+        }
+    }
+};
+
+// krp_partial_contractions_rl (sketch.cpp:67-78) for caller-supplied factors
+// (host_factors = Omega_start..Omega_d, n_k x cols each) or, when NULL,
+// Philox factors drawn on the device for global columns col0..col0+cols.
+void krp_partial_contractions(Ctx& c, const TTDev& t, i64 start, i64 cols, const double* host_factors,
+                              std::uint64_t seed, i64 col0, double* host_w) {
+    const i64 d = t.d();
+    if (start < 2 || start > d) fail(Errc::InvalidArgument, "contraction start mode must lie in [2, d]");
+    if (cols < 1) fail(Errc::InvalidArgument, "factor column count must be >= 1");
+    const i64 ldwt = even_ld(cols);
+    std::vector<DBuf> om(d + 1), W(d + 1), Wt(d + 2);
+    std::vector<i64> ldo(d + 1, 0), ldw(d + 1, 0);
+    i64 foff = 0;
+    for (i64 k = start; k <= d; ++k) {
+        const i64 nk = t.n[k - 1];
+        ldo[k] = even_ld(nk);
+        om[k] = DBuf(c, static_cast<std::size_t>(ldo[k] * cols));
+        if (host_factors) {
+            TTR_CUDA(cudaMemcpy2DAsync(om[k].p, sizeof(double) * ldo[k], host_factors + foff, sizeof(double) * nk,
+                                       sizeof(double) * nk, cols, cudaMemcpyHostToDevice, c.stream));
+            foff += nk * cols;
+        } else {
+            philox_factor(c, seed, k, nk, cols, col0, om[k].p, ldo[k]);
+        }
+        ldw[k] = even_ld(t.r[k - 1]);
+        W[k] = DBuf(c, static_cast<std::size_t>(ldw[k] * cols));
+        Wt[k] = DBuf(c, static_cast<std::size_t>(ldwt * t.r[k - 1]));
+    }
+    DBuf ones(c, static_cast<std::size_t>(ldwt));
+    fill(c, ones.p, static_cast<std::size_t>(ldwt), 1.0);
+    {
+        SketchScope scope(c);
+        for (i64 k = d; k >= start; --k) {
+            krp_step(c, t.r[k - 1], t.n[k - 1], t.r[k], cols, t.core(k - 1), om[k].p, ldo[k],
+                     k == d ? ones.p : Wt[k + 1].p, ldwt, W[k].p, ldw[k], Wt[k].p, ldwt, k == d);
+        }
+    }
+    i64 woff = 0;
+    for (i64 k = start; k <= d; ++k) {
+        const i64 rl = t.r[k - 1];
+        TTR_CUDA(cudaMemcpy2DAsync(host_w + woff, sizeof(double) * rl, W[k].p, sizeof(double) * ldw[k],
+                                   sizeof(double) * rl, cols, cudaMemcpyDeviceToHost, c.stream));
+        woff += rl * cols;
+    }
+    TTR_CUDA(cudaStreamSynchronize(c.stream));
+}
+
+// ---------------------------------------------------------------------------
+// Fixed-rank KRP rounding — round_rand.cpp:52-64 with rand_orth_sweep :26-44
+static std::vector<i64> checked_targets(const TTDev& t, const std::vector<i64>& targets) {  // round_rand.cpp:14-20
+    if (static_cast<i64>(targets.size()) != t.d() - 1) fail(Errc::InvalidRanks, "expected d-1 target ranks");
+    for (i64 l : targets)
+        if (l < 1) fail(Errc::InvalidRanks, "target ranks must be >= 1");
+    return targets;
+}
+
+std::unique_ptr<TTDev> round_fixed_krp(Ctx& c, const TTDev& t, const std::vector<i64>& target_ranks,
+                                       std::uint64_t seed, int rng_mode) {
+    auto targets = checked_targets(t, target_ranks);
+    const i64 d = t.d();
+    if (d == 1) return copy_tt(c, t);
+    const i64 width = *std::max_element(targets.begin(), targets.end());
+    Sketch sk(c, t, width, rng_mode, seed);
+    sk.append(2, width);
+
+    // output ranks (l_eff caps, round_rand.cpp:34-35)
+    std::vector<i64> r(d + 1, 1);
+    for (i64 k = 1; k < d; ++k) r[k] = std::min({targets[k - 1], r[k - 1] * t.n[k - 1], t.r[k]});
+    auto out = std::make_unique<TTDev>(c, t.n, r);
+
+    i64 max_work = 0, max_s = 0;
+    for (i64 k = 1; k < d; ++k) {
+        max_work = std::max(max_work, r[k] * t.n[k] * t.r[k + 1]);
+        max_s = std::max(max_s, r[k - 1] * t.n[k - 1] * r[k]);
+    }
+    DBuf work(c, static_cast<std::size_t>(max_work));
+    DBuf S(c, static_cast<std::size_t>(max_s));
+    DBuf M(c, static_cast<std::size_t>(width * t.max_rank()));
+
+    const double* v = t.core(0);
+    for (i64 k = 1; k < d; ++k) {
+        const i64 rows = r[k - 1] * t.n[k - 1], cols = t.r[k], l = r[k];
+        // S = V(Y_k) W_{k+1}(:, 1:l)
+        gemm(c, false, rows, l, cols, 1.0, v, rows, sk.W[k + 1].p, sk.ldw[k + 1], 0.0, S.p, rows);
+        // Q = thin_qr_q(S) -> output core k
+        thin_qr(c, rows, l, S.p, rows, out->core(k - 1), rows, nullptr, 1);
+        // M = Q^T V  (l x r_k)
+        gemm(c, true, l, cols, rows, 1.0, out->core(k - 1), rows, v, rows, 0.0, M.p, l);
+        // H(Y_{k+1}) = M H(X_{k+1})  (contract_first, internal.hpp:10-12)
+        const i64 ncols = t.n[k] * t.r[k + 1];
+        double* dst = (k == d - 1) ? out->core(d - 1) : work.p;
+        gemm(c, false, l, ncols, cols, 1.0, M.p, l, t.core(k), cols, 0.0, dst, l);
+        v = dst;  // stream order: this iteration's reads of the old V precede the write
+    }
+    return out;
+}
+
+// ---------------------------------------------------------------------------
+// estimate_norm_krp — sketch.cpp:111-119
+double estimate_norm_krp(Ctx& c, const TTDev& t, i64 width, std::uint64_t seed, int rng_mode) {
+    if (width < 1) fail(Errc::InvalidArgument, "sketch width must be >= 1");
+    if (t.d() == 1) return frob_norm(c, t.core_size(0), 1, t.core(0), t.core_size(0));
+    Sketch sk(c, t, width, rng_mode, seed);
+    sk.append(2, width);
+    const i64 rows = t.n[0], cols = t.r[1];
+    DBuf S(c, static_cast<std::size_t>(rows * width));
+    gemm(c, false, rows, width, cols, 1.0, t.core(0), rows, sk.W[2].p, sk.ldw[2], 0.0, S.p, rows);
+    return frob_norm(c, rows, width, S.p, rows) / std::sqrt(static_cast<double>(width));
+}
+
+// ---------------------------------------------------------------------------
+// Adaptive KRP rounding — round_rand.cpp:80-153
+static i64 ceil_fraction(double f, i64 n) {  // round_rand.cpp:46-48
+    return std::max<i64>(1, static_cast<i64>(std::ceil(f * static_cast<double>(n))));
+}
+
+std::unique_ptr<TTDev> round_adaptive_krp(Ctx& c, const TTDev& t, const AdaptiveCfg& cfg, std::vector<double>* trace) {
+    if (!(cfg.tolerance > 0.0 && cfg.tolerance < 1.0)) fail(Errc::InvalidArgument, "adaptive tolerance must lie in (0,1)");
+    if (!(cfg.f_init > 0.0 && cfg.f_init < 1.0) || !(cfg.f_inc > 0.0 && cfg.f_inc < 1.0))
+        fail(Errc::InvalidArgument, "block fractions must lie in (0,1)");
+    const i64 d = t.d();
+    if (d == 1) return copy_tt(c, t);
+    const i64 maxr = t.max_rank();
+    const i64 width = ceil_fraction(cfg.f_init, maxr);
+    // column capacity: any mode uses at most rbar + b_inc columns
+    i64 cap = width;
+    for (i64 k = 1; k < d; ++k) {
+        const i64 rb = std::min(t.r[k], (k == 1 ? 1 : maxr) * t.n[k - 1]);
+        cap = std::max(cap, std::min(rb, maxr) + ceil_fraction(cfg.f_inc, std::min(rb, maxr)) + 1);
+    }
+    cap = std::max(cap, maxr + ceil_fraction(cfg.f_inc, maxr) + 1);
+    Sketch sk(c, t, cap, cfg.rng_mode, cfg.seed);
+    sk.append(2, width);
+
+    double nrm;
+    if (cfg.has_known_norm) {
+        nrm = cfg.known_norm;
+    } else {  // reuse the initial contraction (round_rand.cpp:113-116)
+        const i64 rows = t.n[0], cols = t.r[1];
+        DBuf S0(c, static_cast<std::size_t>(rows * width));
+        gemm(c, false, rows, width, cols, 1.0, t.core(0), rows, sk.W[2].p, sk.ldw[2], 0.0, S0.p, rows);
+        nrm = frob_norm(c, rows, width, S0.p, rows) / std::sqrt(static_cast<double>(width));
+    }
+    const double tau = cfg.tolerance * nrm / std::sqrt(static_cast<double>(d - 1));
+    if (trace) trace->clear();
+
+    // device buffers sized for the largest mode
+    i64 max_rows = 0, max_hcols = 0;
+    {
+        i64 rprev = 1;
+        for (i64 k = 1; k < d; ++k) {
+            const i64 rows = rprev * t.n[k - 1];
+            max_rows = std::max(max_rows, rows);
+            rprev = std::min(rows, t.r[k]);
+            if (cfg.max_rank_cap) rprev = std::min<i64>(rprev, cfg.max_rank_cap[k - 1]);
+            max_hcols = std::max(max_hcols, t.n[k] * t.r[k + 1]);
+        }
+    }
+    const i64 rcap = std::min(maxr, max_rows);
+    DBuf Qb(c, static_cast<std::size_t>(max_rows * (rcap + 1)));
+    DBuf Sb(c, static_cast<std::size_t>(max_rows * cap));
+    DBuf Qn(c, static_cast<std::size_t>(max_rows * cap));
+    DBuf P(c, static_cast<std::size_t>(std::max<i64>(rcap, cap) * std::max<i64>(cap, maxr)));
+    DBuf Mb(c, static_cast<std::size_t>(cap * maxr + maxr * maxr));
+    DBuf Hn(c, static_cast<std::size_t>(rcap * max_hcols));
+    DBuf cur(c, static_cast<std::size_t>(std::max<i64>(t.core_size(0), rcap * max_hcols)));
+    copy_matrix(c, t.core_size(0), 1, t.core(0), t.core_size(0), cur.p, t.core_size(0));
+
+    std::vector<DBuf> out_cores;
+    std::vector<std::array<i64, 3>> shapes;
+    i64 rl = 1;
+    for (i64 k = 1; k < d; ++k) {
+        const i64 nk = t.n[k - 1], rows = rl * nk, cols = t.r[k];
+        const double* v = cur.p;  // V(work): rows x cols, ld rows
+        i64 rbar = std::min(rows, cols);
+        if (cfg.max_rank_cap) rbar = std::min<i64>(rbar, cfg.max_rank_cap[k - 1]);
+        const i64 b_init = std::min(ceil_fraction(cfg.f_init, rbar), rbar);
+        const i64 hcols = t.n[k] * t.r[k + 1];
+        const i64 ldh = std::max<i64>(rbar, 1);
+        // Q = qr(V W_{k+1}(:, 1:b_init))
+        gemm(c, false, rows, b_init, cols, 1.0, v, rows, sk.W[k + 1].p, sk.ldw[k + 1], 0.0, Sb.p, rows);
+        thin_qr(c, rows, b_init, Sb.p, rows, Qb.p, rows, nullptr, 1);
+        i64 q = std::min(rows, b_init);
+        // H_next(0:q, :) = (Q^T V) H(X_{k+1})
+        gemm(c, true, q, cols, rows, 1.0, Qb.p, rows, v, rows, 0.0, Mb.p, q);
+        gemm(c, false, q, hcols, cols, 1.0, Mb.p, q, t.core(k), cols, 0.0, Hn.p, ldh);
+        const i64 b_inc = ceil_fraction(cfg.f_inc, rbar);
+        while (q < rbar) {
+            // generate_residual_sketch (round_rand.cpp:80-94)
+            const i64 have = sk.width[k + 1];
+            if (have < q + b_inc) sk.append(k + 1, q + b_inc - have);
+            gemm(c, false, rows, b_inc, cols, 1.0, v, rows, sk.W[k + 1].p + q * sk.ldw[k + 1], sk.ldw[k + 1], 0.0, Sb.p,
+                 rows);
+            // S -= Q (Q^T S)
+            gemm(c, true, q, b_inc, rows, 1.0, Qb.p, rows, Sb.p, rows, 0.0, P.p, q);
+            gemm(c, false, rows, b_inc, q, -1.0, Qb.p, rows, P.p, q, 1.0, Sb.p, rows);
+            const double est = frob_norm(c, rows, b_inc, Sb.p, rows) / std::sqrt(static_cast<double>(b_inc));
+            if (trace) trace->push_back(est);
+            if (est <= tau) break;
+            const i64 grow = std::min(b_inc, rbar - q);
+            thin_qr(c, rows, grow, Sb.p, rows, Qn.p, rows, nullptr, 1);
+            // re-orthogonalise: Qn2 = qr(Qn - Q (Q^T Qn))
+            gemm(c, true, q, grow, rows, 1.0, Qb.p, rows, Qn.p, rows, 0.0, P.p, q);
+            gemm(c, false, rows, grow, q, -1.0, Qb.p, rows, P.p, q, 1.0, Qn.p, rows);
+            thin_qr(c, rows, grow, Qn.p, rows, Qb.p + q * rows, rows, nullptr, 1);
+            // H_next rows [q, q+grow) = (Qn^T V) H(X_{k+1})
+            gemm(c, true, grow, cols, rows, 1.0, Qb.p + q * rows, rows, v, rows, 0.0, Mb.p, grow);
+            gemm(c, false, grow, hcols, cols, 1.0, Mb.p, grow, t.core(k), cols, 0.0, Hn.p + q, ldh);
+            q += grow;
+        }
+        // finished core k: Q (rows x q) with shape (rl, nk, q)
+        DBuf core(c, static_cast<std::size_t>(rows * q));
+        copy_matrix(c, rows, q, Qb.p, rows, core.p, rows);
+        out_cores.push_back(std::move(core));
+        shapes.push_back({rl, nk, q});
+        // next working core = H_next(0:q, :) compacted (ld q)
+        copy_matrix(c, q, hcols, Hn.p, ldh, cur.p, q);
+        rl = q;
+    }
+    std::vector<i64> r(d + 1, 1);
+    for (i64 k = 1; k < d; ++k) r[k] = shapes[k - 1][2];
+    auto out = std::make_unique<TTDev>(c, t.n, r);
+    for (i64 k = 0; k < d - 1; ++k)
+        copy_matrix(c, out->core_size(k), 1, out_cores[k].p, out->core_size(k), out->core(k), out->core_size(k));
+    copy_matrix(c, out->core_size(d - 1), 1, cur.p, out->core_size(d - 1), out->core(d - 1), out->core_size(d - 1));
+    return out;
+}
+
+}  // namespace ttr

@@ -1,0 +1,64 @@
+// tt_round.h — device-resident TT container and the rounding entry points
+// (host orchestration in tt_round.cu / tt_det.cu).
+#pragma once
+
+#include <memory>
+#include <vector>
+
+#include "common.cuh"
+
+namespace ttr {
+
+// Device TT tensor: all cores in one allocation, each 256-byte aligned, in
+// the reference layout (core k = column-major vertical unfolding of the
+// r_{k-1} x n_k x r_k core, proj/core/include/ttround/tensor.hpp:11-16).
+struct TTDev {
+    Ctx* ctx;
+    std::vector<i64> n, r, off;
+    DBuf buf;
+    TTDev(Ctx& c, const std::vector<i64>& n, const std::vector<i64>& r);
+    i64 d() const { return static_cast<i64>(n.size()); }
+    double* core(i64 k) const { return buf.p + off[k]; }
+    i64 core_size(i64 k) const { return r[k] * n[k] * r[k + 1]; }
+    i64 total() const;
+    i64 max_rank() const;
+    void upload(const double* host);
+    void download(double* host) const;
+};
+
+struct AdaptiveCfg {
+    double tolerance = 1e-6, f_init = 0.1, f_inc = 0.05;
+    std::uint64_t seed = 0;
+    bool has_known_norm = false;
+    double known_norm = 0.0;
+    const i64* max_rank_cap = nullptr;
+    int rng_mode = TTR_RNG_PHILOX;
+};
+
+std::unique_ptr<TTDev> copy_tt(Ctx& c, const TTDev& t);
+std::unique_ptr<TTDev> random_philox_tt(Ctx& c, const std::vector<i64>& n, const std::vector<i64>& r, std::uint64_t seed);
+std::unique_ptr<TTDev> formal_sum(Ctx& c, const std::vector<const TTDev*>& terms);
+void scale_tt(Ctx& c, TTDev& t, double alpha);
+std::unique_ptr<TTDev> orthogonalize_rl_public(Ctx& c, const TTDev& t);
+double norm_exact(Ctx& c, const TTDev& t);
+double relative_error(Ctx& c, const TTDev& a, const TTDev& b);
+
+std::unique_ptr<TTDev> round_fixed_krp(Ctx& c, const TTDev& t, const std::vector<i64>& target_ranks, std::uint64_t seed,
+                                       int rng_mode);
+std::unique_ptr<TTDev> round_adaptive_krp(Ctx& c, const TTDev& t, const AdaptiveCfg& cfg, std::vector<double>* trace);
+double estimate_norm_krp(Ctx& c, const TTDev& t, i64 width, std::uint64_t seed, int rng_mode);
+std::unique_ptr<TTDev> round_deterministic_tol(Ctx& c, const TTDev& t, double eps);
+std::unique_ptr<TTDev> round_deterministic_ranks(Ctx& c, const TTDev& t, const std::vector<i64>& ranks);
+
+// W_start..W_d of the KRP partial contractions for explicit (or Philox) factors.
+void krp_partial_contractions(Ctx& c, const TTDev& t, i64 start_mode, i64 cols, const double* host_factors,
+                              std::uint64_t seed, i64 col0, double* host_w);
+
+}  // namespace ttr
+
+struct ttr_tt {
+    std::unique_ptr<ttr::TTDev> t;
+};
+struct ttr_ctx {
+    ttr::Ctx c;
+};

@@ -1,0 +1,234 @@
+"""GPU parity tests: the CUDA library (through its C ABI) against the CPU
+oracle on identical inputs. Tolerances are the reference's own
+(tests/test_sketch.cpp, test_round_rand.cpp, test_orthogonalize.cpp) or the
+north-star bar (||Y_gpu - Y_ref|| / ||Y_ref|| <= 1e-10, identical ranks)."""
+import numpy as np
+import pytest
+
+from helpers import left_orth_defect, rel_err_vs_ref, to_device, to_oracle
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_2511_03598_b200 as P
+    return P
+
+
+@pytest.fixture(scope="module")
+def O():
+    import py_oracle as O
+    return O
+
+
+# ---- dense kernels ---------------------------------------------------------------
+
+@pytest.mark.parametrize("m,n,k,ta", [(7, 5, 3, False), (130, 70, 33, False), (1000, 320, 1000, False),
+                                      (33, 65, 4001, True), (320, 1000, 40960, True), (257, 129, 16, True),
+                                      (64, 1, 640, False)])
+def test_gemm_matches_numpy(P, m, n, k, ta):
+    rng = np.random.default_rng(m * 7 + n)
+    a = rng.standard_normal((k, m) if ta else (m, k))
+    b = rng.standard_normal((k, n))
+    c = P.gemm(a, b, trans_a=ta)
+    ref = (a.T if ta else a) @ b
+    assert np.linalg.norm(c - ref) <= 1e-13 * np.sqrt(k) * np.linalg.norm(np.abs(a)) * np.linalg.norm(np.abs(b)) + 1e-300
+
+
+@pytest.mark.parametrize("m,n", [(6, 3), (64, 64), (320, 20), (300, 15), (7040, 110), (2000, 70), (40, 60)])
+def test_thin_qr(P, m, n):
+    rng = np.random.default_rng(m + 13 * n)
+    a = rng.standard_normal((m, n))
+    q, r = P.thin_qr(a)
+    k = min(m, n)
+    assert q.shape == (m, k) and r.shape == (k, n)
+    assert np.linalg.norm(q.T @ q - np.eye(k)) <= 1e-12 * np.sqrt(k)
+    assert np.linalg.norm(q @ r - a) <= 1e-13 * np.sqrt(m * n) * np.linalg.norm(a)
+    assert np.allclose(np.tril(r, -1), 0.0)
+
+
+@pytest.mark.parametrize("m,n,rank", [(320, 60, 16), (5000, 96, 40), (50, 20, 0)])
+def test_thin_qr_rank_deficient_is_orthonormal(P, m, n, rank):
+    """linalg.hpp:22 — Q is orthonormal even for rank-deficient input."""
+    rng = np.random.default_rng(5)
+    a = rng.standard_normal((m, rank)) @ rng.standard_normal((rank, n)) if rank else np.zeros((m, n))
+    q, r = P.thin_qr(a)
+    assert np.all(np.isfinite(q))
+    assert np.linalg.norm(q.T @ q - np.eye(n)) <= 1e-10
+    assert np.linalg.norm(q @ r - a) <= 1e-12 * max(1.0, np.linalg.norm(a))
+
+
+# ---- K1: Philox factors are bit-identical on host and device ---------------------
+
+@pytest.mark.parametrize("seed,mode,rows,cols,col0", [(7, 2, 20, 15, 0), (7, 30, 64, 110, 0), (2**40 + 3, 5, 33, 9, 17),
+                                                      (0, 12, 128, 40, 400)])
+def test_philox_factor_bitwise(P, O, seed, mode, rows, cols, col0):
+    dev = P.philox_factor(seed, mode, rows, cols, col0)
+    host = O.philox_factor(seed, mode, rows, cols, col0)
+    assert np.array_equal(dev, host)
+
+
+# ---- K2: KRP partial contractions ----------------------------------------------------
+
+def test_krp_hand_example(P):
+    """tests/test_sketch.cpp:34-43: cores (1,2)/(3,4), Omega = ones -> W_2 = 7."""
+    tt = P.TTTensor.from_cores([np.array([[[1.0], [2.0]]]), np.array([[[3.0], [4.0]]])])
+    w = P.krp_partial_contractions_rl(tt, 1, factors=[np.ones((2, 1))])
+    assert w[0].shape == (1, 1) and abs(w[0][0, 0] - 7.0) < 1e-14
+
+
+def test_krp_zero_factors(P, O):
+    ott = O.random_gaussian_tt([3, 4, 3], [1, 2, 2, 1], 5)
+    w = P.krp_partial_contractions_rl(to_device(ott), 2, factors=[np.zeros((4, 2)), np.zeros((3, 2))])
+    assert all(np.linalg.norm(x) == 0.0 for x in w)
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_krp_matches_oracle_random_shapes(P, O, seed):
+    """tests/test_sketch.cpp:54-77 shapes (d<=5, small n, r) plus the reference tolerance."""
+    rng = np.random.default_rng(seed)
+    d = 3 + seed % 3
+    modes = [int(rng.integers(2, 7)) for _ in range(d)]
+    ranks = [1] + [int(rng.integers(1, 5)) for _ in range(d - 1)] + [1]
+    ott = O.random_gaussian_tt(modes, ranks, 900 + seed)
+    cols = 1 + seed % 4
+    f = O.draw_factors(ott, 2, cols, O.derive_seed(seed, 4))
+    w_ref = O.krp_contractions(ott, f)
+    w_gpu = P.krp_partial_contractions_rl(to_device(ott), cols, factors=f)
+    for a, b in zip(w_ref, w_gpu):
+        assert np.linalg.norm(a - b) <= 1e-12 * (1.0 + np.linalg.norm(a))
+
+
+@pytest.mark.parametrize("d,n,r,cols", [(6, 16, 24, 20), (5, 64, 130, 110), (4, 20, 50, 15), (4, 32, 200, 40)])
+def test_krp_matches_oracle_config_shapes(P, O, d, n, r, cols):
+    ranks = [1] + [r] * (d - 1) + [1]
+    ott = O.random_gaussian_tt([n] * d, ranks, 11)
+    f = O.draw_factors(ott, 2, cols, 3, rng=O.PHILOX)
+    w_ref = O.krp_contractions(ott, f)
+    w_gpu = P.krp_partial_contractions_rl(to_device(ott), cols, seed=3)  # device Philox draw
+    for a, b in zip(w_ref, w_gpu):
+        assert np.linalg.norm(a - b) <= 1e-12 * (1.0 + np.linalg.norm(a))
+
+
+def test_krp_append_equals_one_shot_bitwise(P, O):
+    """tests/test_sketch.cpp:78-98 on the device: columns are contraction-batch independent."""
+    ott = O.random_gaussian_tt([4, 32, 16, 4], [1, 3, 40, 2, 1], 77)
+    dtt = to_device(ott)
+    once = P.krp_partial_contractions_rl(dtt, 5, seed=500)
+    first = P.krp_partial_contractions_rl(dtt, 3, seed=500, col0=0)
+    rest = P.krp_partial_contractions_rl(dtt, 2, seed=500, col0=3)
+    for a, b, c in zip(once, first, rest):
+        assert np.array_equal(a, np.hstack([b, c]))
+
+
+# ---- TT arithmetic -------------------------------------------------------------------
+
+def test_norm_exact_and_relative_error(P, O):
+    ott = O.random_gaussian_tt([6, 6, 6, 6, 6], [1, 4, 4, 4, 4, 1], 21)
+    dtt = to_device(ott)
+    assert abs(P.norm_exact(dtt) - O.norm_exact(ott)) <= 1e-12 * O.norm_exact(ott)
+    other = O.random_gaussian_tt([6, 6, 6, 6, 6], [1, 3, 5, 2, 4, 1], 22)
+    ref = O.relative_error(ott, other)
+    assert abs(P.relative_error(dtt, to_device(other)) - ref) <= 1e-12 * ref
+    assert P.relative_error(dtt, dtt) <= 1e-14
+
+
+def test_formal_sum_matches_oracle(P, O):
+    ts = [O.random_gaussian_tt([3, 2, 4, 3], [1, 2, 3, 2, 1], 100 + i) for i in range(3)]
+    ref = O.formal_sum(ts)
+    got = P.formal_sum([to_device(t) for t in ts])
+    assert np.array_equal(got.flat(), ref.flat())
+
+
+# ---- fixed-rank KRP rounding -------------------------------------------------------------
+
+@pytest.mark.parametrize("rng_mode", [0, 1])
+def test_fixed_krp_config1_parity(P, O, rng_mode):
+    """BASELINE config 1 (d=10, n=20, rank 10 + 1e-4 rank 40, l = 15)."""
+    x = O.two_part_tt(10, 20, 10, 40, 1e-4, 1001)
+    y_ref = O.round_fixed_krp(x, [15] * 9, 7, rng=rng_mode)
+    y_gpu = P.round_fixed_krp(to_device(x), [15] * 9, 7, rng=rng_mode)
+    assert y_gpu.ranks() == y_ref.ranks == [1] + [15] * 9 + [1]
+    assert rel_err_vs_ref(y_ref, y_gpu) <= 1e-10
+    assert left_orth_defect(y_gpu.cores()) <= 1e-12
+
+
+def test_fixed_krp_exact_recovery(P, O):
+    """tests/test_round_rand.cpp:35-42: padded exact-rank tensor, true ranks."""
+    base = O.random_gaussian_tt([6, 5, 6, 5], [1, 3, 4, 3, 1], 88)
+    cores = base.cores()
+    pad = [1, 7, 8, 7, 1]
+    pc = []
+    for k, c in enumerate(cores):
+        z = np.zeros((pad[k], c.shape[1], pad[k + 1]))
+        z[: c.shape[0], :, : c.shape[2]] = c
+        pc.append(z)
+    padded = O.TT.from_cores(pc)
+    y = P.round_fixed_krp(to_device(padded), [3, 4, 3], 5)
+    assert y.ranks() == [1, 3, 4, 3, 1]
+    assert rel_err_vs_ref(padded, y) <= 1e-10
+    assert left_orth_defect(y.cores()) <= 1e-12
+
+
+def test_fixed_krp_invalid_ranks(P, O):
+    t = to_device(O.random_gaussian_tt([4, 4], [1, 2, 1], 0))
+    with pytest.raises(P.TTRoundError) as e:
+        P.round_fixed_krp(t, [2, 2], 0)
+    assert e.value.code == "InvalidRanks"
+    with pytest.raises(P.TTRoundError) as e:
+        P.round_fixed_krp(t, [0], 0)
+    assert e.value.code == "InvalidRanks"
+
+
+def test_fixed_krp_config3_shape_parity(P, O):
+    """Config 3 shapes at reduced order (d=6 instead of 30): n=64, formal rank 400, l=110."""
+    x = O.two_part_tt(6, 64, 100, 300, 1e-8, 1003)
+    y_ref = O.round_fixed_krp(x, [110] * 5, 7, rng=O.PHILOX)
+    y_gpu = P.round_fixed_krp(to_device(x), [110] * 5, 7, rng=P.RNG_PHILOX)
+    assert y_gpu.ranks() == y_ref.ranks == [1, 64, 110, 110, 110, 110, 1]
+    assert rel_err_vs_ref(y_ref, y_gpu) <= 1e-10
+
+
+# ---- adaptive KRP rounding -------------------------------------------------------------------
+
+@pytest.mark.parametrize("rng_mode", [0, 1])
+def test_adaptive_config2_small_parity(P, O, rng_mode):
+    """Config 2 structure at reduced order: identical ranks and <= 1e-10 difference."""
+    x = O.two_part_tt(6, 32, 30, 170, 1e-6, 1002)
+    y_ref = O.round_adaptive_krp(x, tolerance=1e-4, f_init=0.1, f_inc=0.05, seed=7, rng=rng_mode)
+    y_gpu = P.round_adaptive_krp(to_device(x), P.AdaptiveConfig(tolerance=1e-4, seed=7, rng=rng_mode))
+    assert y_gpu.ranks() == y_ref.ranks
+    assert rel_err_vs_ref(y_ref, y_gpu) <= 1e-10
+
+
+def test_adaptive_rank_caps(P, O):
+    x = O.synthetic_perturbed_tt(4, 10, 6, 1e-5, 23)
+    y = P.round_adaptive_krp(to_device(x), P.AdaptiveConfig(tolerance=1e-8, seed=2, max_rank_cap=[3, 3, 3]))
+    assert max(y.ranks()) <= 3
+
+
+# ---- deterministic TT-SVD rounding -------------------------------------------------------------
+
+def test_det_fixed_ranks_parity(P, O):
+    x = O.synthetic_perturbed_tt(5, 20, 10, 1e-5, 1234)
+    y_ref = O.round_deterministic(x, ranks=[10] * 4)
+    y_gpu = P.round_deterministic(to_device(x), target_ranks=[10] * 4)
+    assert y_gpu.ranks() == y_ref.ranks
+    assert rel_err_vs_ref(y_ref, y_gpu) <= 1e-10
+
+
+def test_det_tolerance_parity(P, O):
+    x = O.random_gaussian_tt([6, 5, 6, 5], [1, 5, 6, 4, 1], 41)
+    y_ref = O.round_deterministic(x, eps=1e-3)
+    y_gpu = P.round_deterministic(to_device(x), eps=1e-3)
+    assert y_gpu.ranks() == y_ref.ranks
+    assert rel_err_vs_ref(y_ref, y_gpu) <= 1e-10
+
+
+def test_estimate_norm_matches_oracle(P, O):
+    x = O.synthetic_perturbed_tt(4, 10, 5, 1e-5, 99)
+    for rng_mode in (0, 1):
+        ref = O.estimate_norm_krp(x, 64, 7000, rng=rng_mode)
+        got = P.estimate_norm_krp(to_device(x), 64, 7000, rng=rng_mode)
+        assert abs(got - ref) <= 1e-12 * ref
