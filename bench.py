@@ -1,0 +1,330 @@
+#!/usr/bin/env python3
+"""bench.py — headline benchmark: fixed-rank KRP TT-rounding (BASELINE config 5b)
+on B200 through the library's C ABI.
+
+Workload (config 5b, BASELINE.json configs[4](b)): d=20, n=128, Y = X + 1e-8 Z
+with X a unit-norm rank-300 Gaussian TT and Z a unit-norm rank-700 Gaussian TT
+(formal ranks 1000, 18.4 GB of cores), rounded with round_fixed_krp(Y, {320}x19,
+seed 7) — KRP sketch width l = 320. Cores are drawn on the device from Philox
+(synthetic; the reference has no dataset for this path). A "step" is one full
+round_fixed_krp call (sketch + left-to-right Rand-Orth sweep).
+
+  value  = algorithmic fp64 TFLOP/s of the whole round (reference flop charges,
+           proj/core/src/linalg.cpp:25-61) with the input resident in HBM,
+           summed over ranks (N>1: every rank rounds its own independent 5b
+           tensor — batch sharding, no collective; "scaling": "weak").
+  e2e    = the same metric through the C ABI with host buffers: H2D upload of
+           the input from pinned memory + rounding + D2H download of the result
+           inside the timed region.
+  roofline: the KRP sketch contraction kernel (krp_step = DMMA GEMM + split-K
+           reduce) against the measured fp64 DMMA peak.
+  cpu_baseline: the CPU oracle (restatement of the reference, OpenMP on all host
+           cores) on a bounded sample of the same workload: round_fixed_krp on
+           a d=3 slice (n=128, ranks 1000, l=320: one full middle-core mode).
+
+--impl reference times that CPU implementation alone (the reference itself
+cannot be built here: Eigen is absent — see DESIGN.md).
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "KRP TT-rounding time (ms) and fp64 TFLOP/s vs peak at 1/2/4/8 B200 vs host CPU"
+FP64_PEAK_TFLOPS = 36.9  # measured: DMMA m8n8k4 microbenchmark, profiles/r01_box_probe.log
+PEAK_SOURCE = "measured fp64 DMMA (mma.sync m8n8k4) burst peak on this pool's B200, profiles/r01_box_probe.log"
+
+CFG5B = dict(d=20, n=128, rx=300, rz=700, eps=1e-8, ell=320, seed=1005, round_seed=7)
+CPU_SAMPLE = dict(d=3, n=128, r=1000, ell=320, seed=5)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="5b", choices=["5b", "3"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# ---------------------------------------------------------------------------
+# CPU oracle sample (reference restatement) — used by cpu_baseline and --impl reference
+
+def cpu_sample(runs: int = 1):
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import py_oracle as O
+    s = CPU_SAMPLE
+    x = O.random_gaussian_tt([s["n"]] * s["d"], [1] + [s["r"]] * (s["d"] - 1) + [1], s["seed"])
+    out = []
+    for _ in range(runs):
+        sec = C.c_double()
+        fl = C.c_uint64()
+        O._check(O.lib().ttro_time_round_fixed_krp(x._h, O._i64([s["ell"]] * (s["d"] - 1)), C.c_int64(s["d"] - 1),
+                                                   C.c_uint64(7), C.c_int(O.PHILOX), C.byref(sec), C.byref(fl)))
+        out.append((sec.value, fl.value))
+    return out
+
+
+def cpu_threads() -> int:
+    return int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+
+
+def sample_desc():
+    s = CPU_SAMPLE
+    return (f"round_fixed_krp on a d={s['d']} slice of the workload (n={s['n']}, ranks {s['r']}, l={s['ell']}: "
+            f"one full middle-core sketch + LR mode), CPU oracle (reference restatement), wall clock around the call")
+
+
+def run_reference(args, world, rank):
+    if rank != 0:
+        return
+    for _ in range(args.warmup):
+        cpu_sample(1)
+    res = cpu_sample(args.steps)
+    secs = [r[0] for r in res]
+    flops = res[0][1]
+    tot = sum(secs)
+    tflops = flops * len(secs) / tot / 1e12
+    line = {
+        "impl": "reference", "metric": METRIC, "value": tflops, "unit": "TFLOP/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot / len(secs) * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "config 5b fixed-rank KRP rounding, bounded CPU sample", "sample": sample_desc()},
+        "cpu_baseline": {"value": tflops, "unit": "TFLOP/s", "cores": cpu_threads(), "kind": "port",
+                         "sample": sample_desc()},
+        "e2e": {"value": tflops, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, device: int):
+        self.device = device
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                vals = [v.strip() for v in out.stdout.strip().split(",")]
+                if len(vals) == 6:
+                    self.samples.append(vals)
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def build_input(P, ctx, cfg):
+    d, n = cfg["d"], cfg["n"]
+    from paper_2511_03598_b200.seeds import derive_seed
+    rx = [1] + [cfg["rx"]] * (d - 1) + [1]
+    rz = [1] + [cfg["rz"]] * (d - 1) + [1]
+    x = P.TTTensor.random_philox([n] * d, rx, derive_seed(cfg["seed"], 1), ctx)
+    z = P.TTTensor.random_philox([n] * d, rz, derive_seed(cfg["seed"], 2), ctx)
+    x = P.scaled(x, 1.0 / P.norm_exact(x))
+    z = P.scaled(z, cfg["eps"] / P.norm_exact(z))
+    return P.formal_sum([x, z])
+
+
+def run_ours(args, world, rank, local):
+    import torch
+    import paper_2511_03598_b200 as P
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    torch.cuda.set_device(local)
+    stream = torch.cuda.current_stream()
+    ctx = P.Context(local, stream.cuda_stream)
+
+    cfg = dict(CFG5B)
+    if args.config == "3":
+        cfg.update(d=30, n=64, rx=100, rz=300, eps=1e-8, ell=110, seed=1003)
+    cfg["seed"] = cfg["seed"] + 1000 * rank  # independent tensor per rank
+    y = build_input(P, ctx, cfg)
+    ranks = [cfg["ell"]] * (cfg["d"] - 1)
+    torch.cuda.synchronize()
+
+    def step():
+        return P.round_fixed_krp(y, ranks, cfg["round_seed"] if "round_seed" in cfg else 7)
+
+    # flops per step (reference charges) and launch count
+    ctx.reset_counters()
+    l0 = ctx.kernel_launches()
+    out = step()
+    torch.cuda.synchronize()
+    flops = ctx.counters().total()
+    sketch_flops = ctx.counters().sketch
+    launches_per_step = ctx.kernel_launches() - l0
+    out_ranks = out.ranks()
+    del out
+    for _ in range(max(0, args.warmup - 1)):
+        o = step()
+        del o
+    torch.cuda.synchronize()
+
+    # ---- timed region (inputs 18 GB >> 126 MB L2: no flush needed) ----
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    l0 = ctx.kernel_launches()
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            o = step()
+            del o
+        e1.record(stream)
+        torch.cuda.synchronize()
+    launches = ctx.kernel_launches() - l0
+    ms = e0.elapsed_time(e1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    value = flops * world / (ms * 1e-3) / 1e12
+
+    # ---- phase timing (separate step; events around each phase) ----
+    C_ = P.lib()
+    C_.ttr_ctx_enable_timing(ctx._h, 1)
+    C_.ttr_ctx_phase_times(ctx._h, None, None)
+    o = step()
+    del o
+    phase_ms = (C.c_double * 4)()
+    phase_n = (C.c_uint64 * 4)()
+    C_.ttr_ctx_phase_times(ctx._h, phase_ms, phase_n)
+    C_.ttr_ctx_enable_timing(ctx._h, 0)
+    sketch_ms = phase_ms[0]
+    achieved = sketch_flops / (sketch_ms * 1e-3) / 1e12 if sketch_ms > 0 else None
+
+    # ---- end to end through the C ABI with host buffers ----
+    e2e = None
+    if not args.no_e2e:
+        n_, r_, total = y.shape()
+        host_in = torch.empty(total, dtype=torch.float64, pin_memory=True)
+        C_.ttr_tt_download(ctx._h, y._h, C.c_void_p(host_in.data_ptr()))
+        out_total = None
+        reps = max(1, min(args.steps, 3))
+        host_out = None
+        torch.cuda.synchronize()
+        times = []
+        for it in range(reps + 1):
+            t0 = time.perf_counter()
+            a = P.TTTensor.from_flat(n_, r_, host_in.numpy(), ctx)  # H2D from pinned memory
+            o = P.round_fixed_krp(a, ranks, 7)
+            _, _, out_total = o.shape()
+            if host_out is None:
+                host_out = torch.empty(out_total, dtype=torch.float64, pin_memory=True)
+            C_.ttr_tt_download(ctx._h, o._h, C.c_void_p(host_out.data_ptr()))  # D2H + sync
+            dt = time.perf_counter() - t0
+            del a, o
+            if it > 0:
+                times.append(dt)
+        e2e_ms = sum(times) / len(times) * 1e3
+        if world > 1:
+            t = torch.tensor([e2e_ms], device="cuda")
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            e2e_ms = float(t.item())
+        e2e = {"value": flops * world / (e2e_ms * 1e-3) / 1e12, "unit": "TFLOP/s", "ms_per_step": e2e_ms,
+               "h2d_bytes_per_step": 8 * total, "d2h_bytes_per_step": 8 * out_total,
+               "timing": "host wall clock around upload + round + download (synchronising)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        res = cpu_sample(1)
+        sec, fl = res[0]
+        cpu = {"value": fl / sec / 1e12, "unit": "TFLOP/s", "cores": cpu_threads(), "kind": "port",
+               "sample": sample_desc(), "seconds": sec}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (device Philox Gaussian cores)",
+            "config": {"workload": f"config {args.config} fixed-rank KRP rounding round_fixed_krp(Y, {{{cfg['ell']}}}x{cfg['d'] - 1}, 7)",
+                       "d": cfg["d"], "n": cfg["n"], "formal_rank": cfg["rx"] + cfg["rz"], "l": cfg["ell"],
+                       "input_gb": total_bytes(y) / 1e9, "output_ranks": out_ranks,
+                       "flops_per_step": flops, "sketch_flops_per_step": sketch_flops,
+                       "l2": "inputs exceed L2 (18 GB vs 126 MB)" if args.config == "5b" else "inputs exceed L2",
+                       "parallelism": f"{world} independent tensors (batch sharding)"},
+            "tflops_fp64": value, "fraction_of_fp64_peak": value / world / FP64_PEAK_TFLOPS,
+            "phase_ms": {"sketch": phase_ms[0], "qr": phase_ms[1], "lr_gemm": phase_ms[2], "other": phase_ms[3]},
+            "roofline": {"bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                         "frac": (achieved / FP64_PEAK_TFLOPS) if achieved else None, "traffic": None,
+                         "kernel": "krp_step (dgemm_kernel<KM=1> + splitk_reduce), fp64 DMMA",
+                         "peak_source": PEAK_SOURCE},
+            "clocks": clk.summary(),
+            "gpu_launches": launches,
+            "gpu_launches_per_step": launches_per_step,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def total_bytes(y):
+    return 8 * y.shape()[2]
+
+
+def main():
+    args = parse()
+    world, rank, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+        return
+    run_ours(args, world, rank, local)
+
+
+if __name__ == "__main__":
+    main()

@@ -154,6 +154,13 @@ ttr_status ttr_thin_qr(ttr_ctx* ctx, int64_t m, int64_t n, const double* host_a,
 ttr_status ttr_gemm(ttr_ctx* ctx, int trans_a, int64_t m, int64_t n, int64_t k, const double* host_a,
                     const double* host_b, double* host_c);
 
+/* Phase timing with CUDA events on the context stream (bench/profiling):
+ * phases 0 = KRP sketch contraction, 1 = Householder QR, 2 = LR-sweep GEMMs,
+ * 3 = other. ttr_ctx_phase_times synchronises, returns the summed device
+ * milliseconds and event-pair counts per phase, and clears them. */
+ttr_status ttr_ctx_enable_timing(ttr_ctx* ctx, int on);
+ttr_status ttr_ctx_phase_times(ttr_ctx* ctx, double* ms_out /*4*/, uint64_t* count_out /*4*/);
+
 ttr_status ttr_counters(ttr_ctx* ctx, ttr_counts* out);
 ttr_status ttr_counters_reset(ttr_ctx* ctx);
 

@@ -329,6 +329,33 @@ ttr_status ttr_gemm(ttr_ctx* ctx, int trans_a, int64_t m, int64_t n, int64_t k, 
     });
 }
 
+ttr_status ttr_ctx_enable_timing(ttr_ctx* ctx, int on) {
+    return guard([&] {
+        need(ctx != nullptr, "null context");
+        ctx->c.timing = on != 0;
+    });
+}
+
+ttr_status ttr_ctx_phase_times(ttr_ctx* ctx, double* ms_out, uint64_t* count_out) {
+    return guard([&] {
+        need(ctx != nullptr, "null context");
+        TTR_CUDA(cudaStreamSynchronize(ctx->c.stream));
+        for (int p = 0; p < kNumPhases; ++p) {
+            double total = 0.0;
+            for (auto& ev : ctx->c.phase_events[p]) {
+                float ms = 0.f;
+                TTR_CUDA(cudaEventElapsedTime(&ms, ev.first, ev.second));
+                total += ms;
+                cudaEventDestroy(ev.first);
+                cudaEventDestroy(ev.second);
+            }
+            if (ms_out) ms_out[p] = total;
+            if (count_out) count_out[p] = ctx->c.phase_events[p].size();
+            ctx->c.phase_events[p].clear();
+        }
+    });
+}
+
 ttr_status ttr_counters(ttr_ctx* ctx, ttr_counts* out) {
     return guard([&] {
         need(ctx && out, "null argument");

@@ -44,8 +44,13 @@ struct Counts {
     std::uint64_t gemm = 0, qr = 0, svd = 0, sketch = 0, rng = 0;
 };
 
+// Phase timing (CUDA events on the context stream), for bench.py's roofline.
+enum Phase { kPhaseSketch = 0, kPhaseQr = 1, kPhaseGemm = 2, kPhaseOther = 3, kNumPhases = 4 };
+
 struct Ctx {
     int device = 0;
+    bool timing = false;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> phase_events[kNumPhases];
     cudaStream_t stream = nullptr;
     bool own_stream = false;
     int sm_count = 148;
@@ -69,6 +74,24 @@ struct SketchScope {
     Ctx& c;
     explicit SketchScope(Ctx& cc) : c(cc) { ++c.sketch_depth; }
     ~SketchScope() { --c.sketch_depth; }
+};
+
+// Records a (start, stop) event pair around a region when timing is on.
+struct PhaseScope {
+    Ctx& c;
+    int phase;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    PhaseScope(Ctx& cc, int ph) : c(cc), phase(ph) {
+        if (!c.timing) return;
+        cudaEventCreate(&e0);
+        cudaEventCreate(&e1);
+        cudaEventRecord(e0, c.stream);
+    }
+    ~PhaseScope() {
+        if (!e0) return;
+        cudaEventRecord(e1, c.stream);
+        c.phase_events[phase].emplace_back(e0, e1);
+    }
 };
 
 // Stream-ordered device allocation (cudaMallocAsync pool on the ctx stream).

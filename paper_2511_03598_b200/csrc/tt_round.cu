@@ -334,7 +334,10 @@ std::unique_ptr<TTDev> round_fixed_krp(Ctx& c, const TTDev& t, const std::vector
     if (d == 1) return copy_tt(c, t);
     const i64 width = *std::max_element(targets.begin(), targets.end());
     Sketch sk(c, t, width, rng_mode, seed);
-    sk.append(2, width);
+    {
+        PhaseScope ph(c, kPhaseSketch);
+        sk.append(2, width);
+    }
 
     // output ranks (l_eff caps, round_rand.cpp:34-35)
     std::vector<i64> r(d + 1, 1);
@@ -354,15 +357,24 @@ std::unique_ptr<TTDev> round_fixed_krp(Ctx& c, const TTDev& t, const std::vector
     for (i64 k = 1; k < d; ++k) {
         const i64 rows = r[k - 1] * t.n[k - 1], cols = t.r[k], l = r[k];
         // S = V(Y_k) W_{k+1}(:, 1:l)
-        gemm(c, false, rows, l, cols, 1.0, v, rows, sk.W[k + 1].p, sk.ldw[k + 1], 0.0, S.p, rows);
+        {
+            PhaseScope ph(c, kPhaseGemm);
+            gemm(c, false, rows, l, cols, 1.0, v, rows, sk.W[k + 1].p, sk.ldw[k + 1], 0.0, S.p, rows);
+        }
         // Q = thin_qr_q(S) -> output core k
-        thin_qr(c, rows, l, S.p, rows, out->core(k - 1), rows, nullptr, 1);
-        // M = Q^T V  (l x r_k)
-        gemm(c, true, l, cols, rows, 1.0, out->core(k - 1), rows, v, rows, 0.0, M.p, l);
-        // H(Y_{k+1}) = M H(X_{k+1})  (contract_first, internal.hpp:10-12)
+        {
+            PhaseScope ph(c, kPhaseQr);
+            thin_qr(c, rows, l, S.p, rows, out->core(k - 1), rows, nullptr, 1);
+        }
         const i64 ncols = t.n[k] * t.r[k + 1];
         double* dst = (k == d - 1) ? out->core(d - 1) : work.p;
-        gemm(c, false, l, ncols, cols, 1.0, M.p, l, t.core(k), cols, 0.0, dst, l);
+        {
+            PhaseScope ph(c, kPhaseGemm);
+            // M = Q^T V  (l x r_k)
+            gemm(c, true, l, cols, rows, 1.0, out->core(k - 1), rows, v, rows, 0.0, M.p, l);
+            // H(Y_{k+1}) = M H(X_{k+1})  (contract_first, internal.hpp:10-12)
+            gemm(c, false, l, ncols, cols, 1.0, M.p, l, t.core(k), cols, 0.0, dst, l);
+        }
         v = dst;  // stream order: this iteration's reads of the old V precede the write
     }
     return out;
