@@ -182,7 +182,9 @@ def run_ours(args, world, rank, local):
         torch.cuda.set_device(local)
         dist.init_process_group("nccl")
     torch.cuda.set_device(local)
-    stream = torch.cuda.current_stream()
+    # a dedicated (non-default) stream: the library and the timing events share it
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
     ctx = P.Context(local, stream.cuda_stream)
 
     cfg = dict(CFG5B)

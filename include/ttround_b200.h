@@ -150,6 +150,14 @@ ttr_status ttr_philox_factor(ttr_ctx* ctx, uint64_t seed, int64_t mode, int64_t 
  * the device (linalg::thin_qr, linalg.hpp:22-25). q: m x n, r: n x n. */
 ttr_status ttr_thin_qr(ttr_ctx* ctx, int64_t m, int64_t n, const double* host_a, double* host_q,
                        double* host_r);
+/* Device-pointer variants (column-major, caller-owned device memory, ordered
+ * on the context stream, no synchronisation): thin QR (Q and/or R may be
+ * NULL) and C = alpha op(A) B + beta C. */
+ttr_status ttr_dev_thin_qr(ttr_ctx* ctx, int64_t m, int64_t n, const double* dA, int64_t lda, double* dQ,
+                           int64_t ldq, double* dR, int64_t ldr);
+ttr_status ttr_dev_gemm(ttr_ctx* ctx, int trans_a, int64_t m, int64_t n, int64_t k, double alpha,
+                        const double* dA, int64_t lda, const double* dB, int64_t ldb, double beta,
+                        double* dC, int64_t ldc);
 /* C = op(A) B on the device through the library's DMMA GEMM (for tests). */
 ttr_status ttr_gemm(ttr_ctx* ctx, int trans_a, int64_t m, int64_t n, int64_t k, const double* host_a,
                     const double* host_b, double* host_c);

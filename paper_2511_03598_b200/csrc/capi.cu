@@ -314,6 +314,23 @@ ttr_status ttr_thin_qr(ttr_ctx* ctx, int64_t m, int64_t n, const double* host_a,
     });
 }
 
+ttr_status ttr_dev_thin_qr(ttr_ctx* ctx, int64_t m, int64_t n, const double* dA, int64_t lda, double* dQ, int64_t ldq,
+                           double* dR, int64_t ldr) {
+    return guard([&] {
+        need(ctx && dA, "null argument");
+        need(m >= 1 && n >= 1 && lda >= m && (!dQ || ldq >= m), "bad shape");
+        thin_qr(ctx->c, m, n, dA, lda, dQ, ldq, dR, ldr);
+    });
+}
+
+ttr_status ttr_dev_gemm(ttr_ctx* ctx, int trans_a, int64_t m, int64_t n, int64_t k, double alpha, const double* dA,
+                        int64_t lda, const double* dB, int64_t ldb, double beta, double* dC, int64_t ldc) {
+    return guard([&] {
+        need(ctx && dA && dB && dC, "null argument");
+        gemm(ctx->c, trans_a != 0, m, n, k, alpha, dA, lda, dB, ldb, beta, dC, ldc);
+    });
+}
+
 ttr_status ttr_gemm(ttr_ctx* ctx, int trans_a, int64_t m, int64_t n, int64_t k, const double* host_a, const double* host_b,
                     double* host_c) {
     return guard([&] {

@@ -305,17 +305,19 @@ void launch(Ctx& c, GemmArgs& a, int splits) {
 }
 
 constexpr int kBM = 128, kBN = 64, kWM = 32, kWN = 32, kStages = 4;
+// skinny-M tile (M <= 32: the V^T A products of the blocked QR)
+constexpr int kSkBM = 32, kSkBN = 128;
 
-template <bool AT, int KM, int BK>
+template <int BM, int BN, bool AT, int KM, int BK>
 void dispatch_vec(Ctx& c, GemmArgs& a, int splits, bool va2, bool vb2) {
     if constexpr (KM == 2) {  // element-wise B staging: only the A vector width matters
-        if (va2) launch<kBM, kBN, BK, kWM, kWN, kStages, AT, KM, 2, 1>(c, a, splits);
-        else launch<kBM, kBN, BK, kWM, kWN, kStages, AT, KM, 1, 1>(c, a, splits);
+        if (va2) launch<BM, BN, BK, kWM, kWN, kStages, AT, KM, 2, 1>(c, a, splits);
+        else launch<BM, BN, BK, kWM, kWN, kStages, AT, KM, 1, 1>(c, a, splits);
     } else {
-        if (va2 && vb2) launch<kBM, kBN, BK, kWM, kWN, kStages, AT, KM, 2, 2>(c, a, splits);
-        else if (va2) launch<kBM, kBN, BK, kWM, kWN, kStages, AT, KM, 2, 1>(c, a, splits);
-        else if (vb2) launch<kBM, kBN, BK, kWM, kWN, kStages, AT, KM, 1, 2>(c, a, splits);
-        else launch<kBM, kBN, BK, kWM, kWN, kStages, AT, KM, 1, 1>(c, a, splits);
+        if (va2 && vb2) launch<BM, BN, BK, kWM, kWN, kStages, AT, KM, 2, 2>(c, a, splits);
+        else if (va2) launch<BM, BN, BK, kWM, kWN, kStages, AT, KM, 2, 1>(c, a, splits);
+        else if (vb2) launch<BM, BN, BK, kWM, kWN, kStages, AT, KM, 1, 2>(c, a, splits);
+        else launch<BM, BN, BK, kWM, kWN, kStages, AT, KM, 1, 1>(c, a, splits);
     }
 }
 
@@ -332,7 +334,7 @@ int choose_splits(Ctx& c, i64 tiles, int total_kt) {
 }
 
 void run_gemm(Ctx& c, bool AT, int KM, int BK, GemmArgs& a, bool va2, bool vb2, int splits, double* C, i64 ldc,
-              double alpha, double beta, double* Ct, i64 ldct) {
+              double alpha, double beta, double* Ct, i64 ldct, bool skinny = false) {
     const int total_kt = (a.K + BK - 1) / BK;
     splits = std::max(1, std::min(splits, total_kt));
     a.ktiles_per_split = (total_kt + splits - 1) / splits;
@@ -344,11 +346,15 @@ void run_gemm(Ctx& c, bool AT, int KM, int BK, GemmArgs& a, bool va2, bool vb2, 
     a.ldc = ldc;
     a.alpha = alpha;
     a.beta = beta;
-    if (!AT && KM == 0) dispatch_vec<false, 0, 16>(c, a, splits, va2, vb2);
-    else if (AT && KM == 0) dispatch_vec<true, 0, 16>(c, a, splits, va2, vb2);
-    else if (!AT && KM == 1 && BK == 16) dispatch_vec<false, 1, 16>(c, a, splits, va2, vb2);
-    else if (!AT && KM == 1 && BK == 4) dispatch_vec<false, 1, 4>(c, a, splits, va2, vb2);
-    else if (!AT && KM == 2) dispatch_vec<false, 2, 16>(c, a, splits, va2, vb2);
+    if (skinny && KM == 0) {
+        if (AT) dispatch_vec<kSkBM, kSkBN, true, 0, 16>(c, a, splits, va2, vb2);
+        else dispatch_vec<kSkBM, kSkBN, false, 0, 16>(c, a, splits, va2, vb2);
+    }
+    else if (!AT && KM == 0) dispatch_vec<kBM, kBN, false, 0, 16>(c, a, splits, va2, vb2);
+    else if (AT && KM == 0) dispatch_vec<kBM, kBN, true, 0, 16>(c, a, splits, va2, vb2);
+    else if (!AT && KM == 1 && BK == 16) dispatch_vec<kBM, kBN, false, 1, 16>(c, a, splits, va2, vb2);
+    else if (!AT && KM == 1 && BK == 4) dispatch_vec<kBM, kBN, false, 1, 4>(c, a, splits, va2, vb2);
+    else if (!AT && KM == 2) dispatch_vec<kBM, kBN, false, 2, 16>(c, a, splits, va2, vb2);
     else throw Error(TTR_ERR_INTERNAL, "unsupported gemm configuration");
     if (splits > 1) {
         const i64 total = static_cast<i64>(a.M) * a.N;
@@ -388,10 +394,12 @@ void gemm(Ctx& c, bool trans_a, i64 M, i64 N, i64 K, double alpha, const double*
     a.ldb = ldb;
     const bool va2 = aligned16(A) && (lda % 2 == 0);
     const bool vb2 = aligned16(B) && (ldb % 2 == 0);
-    const i64 tiles = ((M + kBM - 1) / kBM) * ((N + kBN - 1) / kBN);
+    const bool skinny = M <= kSkBM;
+    const i64 bm = skinny ? kSkBM : kBM, bn = skinny ? kSkBN : kBN;
+    const i64 tiles = ((M + bm - 1) / bm) * ((N + bn - 1) / bn);
     const int total_kt = static_cast<int>((K + 15) / 16);
     const int splits = choose_splits(c, tiles, total_kt);
-    run_gemm(c, trans_a, 0, 16, a, va2, vb2, splits, C, ldc, alpha, beta, nullptr, 0);
+    run_gemm(c, trans_a, 0, 16, a, va2, vb2, splits, C, ldc, alpha, beta, nullptr, 0, skinny);
 }
 
 void krp_step(Ctx& c, i64 r_left, i64 n, i64 r_right, i64 N, const double* X, const double* Omega, i64 ldo,

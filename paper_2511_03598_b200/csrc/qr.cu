@@ -162,20 +162,25 @@ struct PanelArgs {
     double* diag;      // [2][kPanel]
 };
 
+// Layout: the CTA's row block lives in shared memory column-major with an
+// odd leading dimension (conflict-free 64-bit accesses); lane l of every
+// warp owns column l for the partial dot products, warps split the rows.
 __global__ void __launch_bounds__(kQrThreads) panel_kernel(PanelArgs p) {
     cg::grid_group grid = cg::this_grid();
     extern __shared__ double sm[];
-    const int rpc = p.rpc, b = p.b;
-    double* x = sm;                       // [b][rpc]
-    double* red = x + static_cast<i64>(rpc) * b;  // kPanel sums
-    double* sc = red + kPanel;            // scalars
+    const int rpc = p.rpc, b = p.b, ldx = rpc | 1;
+    double* x = sm;                                  // [b][ldx]
+    double* wred = x + static_cast<i64>(ldx) * b;    // [8][32] warp partials
+    double* red = wred + 8 * 32;                     // kPanel sums
+    double* sc = red + kPanel;                       // scalars
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
     const int r0 = blockIdx.x * rpc, r1 = min(p.rows, r0 + rpc), nr = max(0, r1 - r0);
     const int G = gridDim.x;
+    const int rpw = (nr + nw - 1) / nw;  // rows per warp
 
     for (int idx = tid; idx < nr * b; idx += blockDim.x) {
         const int rr = idx % nr, l = idx / nr;
-        x[rr + l * rpc] = p.P[(r0 + rr) + l * p.ld];
+        x[rr + l * ldx] = p.P[(r0 + rr) + l * p.ld];
     }
     __syncthreads();
 
@@ -184,31 +189,58 @@ __global__ void __launch_bounds__(kQrThreads) panel_kernel(PanelArgs p) {
         const int buf = i & 1;
         double* part = p.partials + static_cast<i64>(buf) * G * kPanel;
         double* dg = p.diag + buf * kPanel;
-        // partial sums over my rows strictly below the diagonal row i
-        const int lo = max(0, i + 1 - r0);  // first local row with global row > i
-        for (int l = i + warp; l < b; l += nw) {
-            double s = 0.0;
-            for (int rr = lo + lane; rr < nr; rr += 32) s = fma(x[rr + i * rpc], x[rr + l * rpc], s);
-            s = warp_sum(s);
-            if (lane == 0) part[blockIdx.x * kPanel + l] = s;
-        }
-        if (i >= r0 && i < r1)
-            for (int l = i + tid; l < b; l += blockDim.x) dg[l] = x[(i - r0) + l * rpc];
-        grid.sync();
-        // reduce partials in fixed CTA order (lane-strided, then fixed shuffle tree)
-        for (int l = i + warp; l < b; l += nw) {
-            double s = 0.0;
-            for (int c = lane; c < G; c += 32) s += __ldcg(part + c * kPanel + l);
-            s = warp_sum(s);
-            if (lane == 0) red[l] = s;
-        }
-        if (tid == 0) {
-            const double alpha = __ldcg(dg + i), tail = 0.0;
-            (void)tail;
-            sc[0] = alpha;
+        // (a) partial dot products x(:,i) . x(:,l) over my rows strictly below row i
+        {
+            const int lo = max(0, i + 1 - r0);
+            const int ra = max(lo, warp * rpw), rb = min(nr, (warp + 1) * rpw);
+            double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;  // 4 chains for ILP
+            if (lane >= i && lane < b) {
+                const double* xi = x + i * ldx;
+                const double* xl = x + lane * ldx;
+                int rr = ra;
+                for (; rr + 3 < rb; rr += 4) {
+                    s0 = fma(xi[rr], xl[rr], s0);
+                    s1 = fma(xi[rr + 1], xl[rr + 1], s1);
+                    s2 = fma(xi[rr + 2], xl[rr + 2], s2);
+                    s3 = fma(xi[rr + 3], xl[rr + 3], s3);
+                }
+                for (; rr < rb; ++rr) s0 = fma(xi[rr], xl[rr], s0);
+            }
+            wred[warp * 32 + lane] = (s0 + s1) + (s2 + s3);
         }
         __syncthreads();
-        const double alpha = sc[0], tail = red[i];
+        if (tid < 32) {
+            double s = 0.0;
+            for (int w = 0; w < nw; ++w) s += wred[w * 32 + tid];
+            part[blockIdx.x * kPanel + tid] = s;
+            if (i >= r0 && i < r1 && tid >= i && tid < b) dg[tid] = x[(i - r0) + tid * ldx];
+        }
+        grid.sync();
+        // (d) reduce partials in fixed order: 8 CTA groups x 32 columns, then groups in order
+        {
+            // all loads issued before any add: one L2 round trip (G <= 8 * kMaxLoads)
+            constexpr int kMaxLoads = 20;
+            const int grp = tid >> 5;
+            double v[kMaxLoads];
+#pragma unroll
+            for (int q = 0; q < kMaxLoads; ++q) {
+                const int c = grp + 8 * q;
+                v[q] = (c < G) ? __ldcg(part + c * kPanel + lane) : 0.0;
+            }
+            double s = 0.0;
+#pragma unroll
+            for (int q = 0; q < kMaxLoads; ++q) s += v[q];
+            wred[grp * 32 + lane] = s;
+        }
+        __syncthreads();
+        if (tid < 32) {
+            double s = 0.0;
+            for (int g = 0; g < 8; ++g) s += wred[g * 32 + tid];
+            red[tid] = s;
+            sc[40 + tid] = __ldcg(dg + tid);
+        }
+        __syncthreads();
+        const double alpha = sc[40 + i], tail = red[i];
         double tj, beta, inv;
         if (tail <= DBL_MIN) {
             tj = 0.0;
@@ -220,21 +252,21 @@ __global__ void __launch_bounds__(kQrThreads) panel_kernel(PanelArgs p) {
             inv = 1.0 / (alpha - beta);
             tj = (beta - alpha) / beta;
         }
-        // w_l = A(i,l) + s_l/(alpha-beta) for l > i
+        // w_l = tau * (A(i,l) + s_l/(alpha-beta)) for l > i
         if (tid < kPanel) {
             const int l = tid;
-            sc[1 + l] = (l > i && l < b) ? tj * (__ldcg(dg + l) + red[l] * inv) : 0.0;
+            sc[1 + l] = (l > i && l < b) ? tj * (sc[40 + l] + red[l] * inv) : 0.0;
         }
         __syncthreads();
         for (int idx = tid; idx < nr; idx += blockDim.x) {
             const int gr = r0 + idx;
             if (gr > i) {
-                const double v = x[idx + i * rpc] * inv;
-                x[idx + i * rpc] = v;
-                for (int l = i + 1; l < b; ++l) x[idx + l * rpc] = fma(-sc[1 + l], v, x[idx + l * rpc]);
+                const double v = x[idx + i * ldx] * inv;
+                x[idx + i * ldx] = v;
+                for (int l = i + 1; l < b; ++l) x[idx + l * ldx] = fma(-sc[1 + l], v, x[idx + l * ldx]);
             } else if (gr == i) {
-                x[idx + i * rpc] = beta;
-                for (int l = i + 1; l < b; ++l) x[idx + l * rpc] -= sc[1 + l];
+                x[idx + i * ldx] = beta;
+                for (int l = i + 1; l < b; ++l) x[idx + l * ldx] -= sc[1 + l];
             }
         }
         if (blockIdx.x == 0 && tid == 0) p.tau[i] = tj;
@@ -242,7 +274,7 @@ __global__ void __launch_bounds__(kQrThreads) panel_kernel(PanelArgs p) {
     }
     for (int idx = tid; idx < nr * b; idx += blockDim.x) {
         const int rr = idx % nr, l = idx / nr;
-        p.P[(r0 + rr) + l * p.ld] = x[rr + l * rpc];
+        p.P[(r0 + rr) + l * p.ld] = x[rr + l * ldx];
     }
 }
 
@@ -260,15 +292,22 @@ __global__ void extract_v(int rows, int b, const double* P, i64 ldp, double* V, 
 // G = V^T V: T(i,i) = tau_i, T(0:i,i) = -tau_i T(0:i,0:i) G(0:i,i).
 __global__ void build_t(int b, const double* G, i64 ldg, const double* tau, double* T, i64 ldt) {
     __shared__ double t[kPanel * kPanel];
+    __shared__ double g[kPanel * kPanel];
+    __shared__ double ts[kPanel];
     __shared__ double z[kPanel];
     const int tid = threadIdx.x;
-    for (int idx = tid; idx < kPanel * kPanel; idx += blockDim.x) t[idx] = 0.0;
+    for (int idx = tid; idx < kPanel * kPanel; idx += blockDim.x) {
+        t[idx] = 0.0;
+        const int r = idx % kPanel, cc = idx / kPanel;
+        g[idx] = (r < b && cc < b) ? G[r + cc * ldg] : 0.0;
+    }
+    if (tid < kPanel) ts[tid] = tid < b ? tau[tid] : 0.0;
     __syncthreads();
     for (int i = 0; i < b; ++i) {
-        const double ti = tau[i];
+        const double ti = ts[i];
         if (tid < i) {
             double s = 0.0;
-            for (int q = tid; q < i; ++q) s = fma(t[tid + q * kPanel], G[q + i * ldg], s);
+            for (int q = tid; q < i; ++q) s = fma(t[tid + q * kPanel], g[q + i * kPanel], s);
             z[tid] = -ti * s;
         }
         __syncthreads();
@@ -356,22 +395,17 @@ void thin_qr(Ctx& c, i64 m, i64 n, const double* A, i64 lda, double* Q, i64 ldq,
 
     for (i64 p = 0; p < npanels; ++p) {
         const i64 j0 = p * kPanel, bb = std::min<i64>(kPanel, k - j0), rows = m - j0;
-        // rows per CTA: at least 32, grid <= co-resident CTAs
-        i64 grid = std::min<i64>((rows + 63) / 64, 2LL * c.sm_count);
+        // one CTA per SM at most (grid barrier cost grows with the CTA count),
+        // at least 64 rows per CTA; the row block must fit in shared memory
+        auto smem_for = [&](i64 rpc_) {
+            return sizeof(double) * static_cast<std::size_t>((rpc_ | 1) * bb + 8 * 32 + kPanel + 80);
+        };
+        i64 grid = std::max<i64>(1, std::min<i64>((rows + 63) / 64, c.sm_count));
         i64 rpc = (rows + grid - 1) / grid;
-        std::size_t smem = sizeof(double) * static_cast<std::size_t>(rpc * bb + kPanel + kPanel + 8);
-        while (smem > 200 * 1024) {  // very tall panels: more CTAs
-            grid *= 2;
-            rpc = (rows + grid - 1) / grid;
-            smem = sizeof(double) * static_cast<std::size_t>(rpc * bb + kPanel + kPanel + 8);
-        }
+        std::size_t smem = smem_for(rpc);
         TTR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&max_blocks_per_sm, panel_kernel, kQrThreads, smem));
         const i64 max_grid = static_cast<i64>(max_blocks_per_sm) * c.sm_count;
-        if (grid > max_grid) {
-            grid = max_grid;
-            rpc = (rows + grid - 1) / grid;
-            smem = sizeof(double) * static_cast<std::size_t>(rpc * bb + kPanel + kPanel + 8);
-        }
+        if (smem > 220 * 1024 || grid > max_grid) throw Error(TTR_ERR_INTERNAL, "qr panel does not fit the GPU");
         grid = (rows + rpc - 1) / rpc;
         if (grid > 4LL * c.sm_count) throw Error(TTR_ERR_INTERNAL, "qr panel grid too large");
         PanelArgs pa{};

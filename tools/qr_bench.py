@@ -1,0 +1,60 @@
+"""Micro-benchmark of the device QR (and GEMM shapes) through the C ABI.
+Usage: python tools/qr_bench.py [m n]..."""
+import ctypes as C
+import os
+import sys
+import time
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2511_03598_b200 as P  # noqa: E402
+
+L = P.lib()
+L.ttr_dev_thin_qr.argtypes = [C.c_void_p, C.c_int64, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64,
+                              C.c_void_p, C.c_int64]
+
+
+def bench_qr(ctx, m, n, reps=5):
+    a = torch.randn(n, m, dtype=torch.float64, device="cuda")  # column-major m x n
+    q = torch.empty(n, m, dtype=torch.float64, device="cuda")
+    s = torch.cuda.current_stream()
+    for _ in range(2):
+        L.ttr_dev_thin_qr(ctx._h, m, n, a.data_ptr(), m, q.data_ptr(), m, None, 1)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(s)
+    for _ in range(reps):
+        L.ttr_dev_thin_qr(ctx._h, m, n, a.data_ptr(), m, q.data_ptr(), m, None, 1)
+    e1.record(s)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    qt = q.T  # m x n
+    orth = torch.linalg.norm(qt.T @ qt - torch.eye(n, dtype=torch.float64, device="cuda")).item()
+    at = a.T
+    res = torch.linalg.norm(qt @ (qt.T @ at) - at).item() / torch.linalg.norm(at).item()
+    print(f"qr {m}x{n}: {ms:.3f} ms  ({4 * m * n * n / ms / 1e9:.2f} TF/s charged)  orth {orth:.2e} resid {res:.2e}",
+          flush=True)
+
+
+def main():
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    ctx = P.Context(0, stream.cuda_stream)
+    shapes = [(40960, 320), (7040, 110), (51200, 40), (6400, 20), (89600, 700)]
+    if len(sys.argv) > 2:
+        shapes = [(int(sys.argv[i]), int(sys.argv[i + 1])) for i in range(1, len(sys.argv) - 1, 2)]
+    for m, n in shapes:
+        bench_qr(ctx, m, n)
+        a = torch.randn(m, n, dtype=torch.float64, device="cuda")
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        for _ in range(3):
+            torch.linalg.qr(a)
+        torch.cuda.synchronize()
+        print(f"   torch.linalg.qr (cuSOLVER) {m}x{n}: {(time.perf_counter() - t) / 3 * 1e3:.3f} ms", flush=True)
+
+
+if __name__ == "__main__":
+    main()
