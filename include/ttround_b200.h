@@ -115,6 +115,8 @@ ttr_status ttr_tt_from_device(ttr_ctx* ctx, int64_t d, const int64_t* n, const i
                               const double* dev_cores, ttr_tt** out);
 ttr_status ttr_tt_shape(const ttr_tt* tt, int64_t* d, int64_t* n, int64_t* r, int64_t* total);
 ttr_status ttr_tt_download(ttr_ctx* ctx, const ttr_tt* tt, double* host_cores);
+/* Overwrite the cores of an existing tensor from host memory (same shape). */
+ttr_status ttr_tt_copy_from_host(ttr_ctx* ctx, ttr_tt* tt, const double* host_cores);
 ttr_status ttr_tt_core_ptr(const ttr_tt* tt, int64_t k, const double** dev_ptr);
 ttr_status ttr_tt_destroy(ttr_tt* tt);
 
@@ -129,6 +131,18 @@ ttr_status ttr_relative_error(ttr_ctx* ctx, const ttr_tt* a, const ttr_tt* b, do
 /* ---- rounding (the hot path) -------------------------------------------- */
 ttr_status ttr_round_fixed_krp(ttr_ctx* ctx, const ttr_tt* tt, const int64_t* target_ranks,
                                int64_t count, uint64_t seed, int rng_mode, ttr_tt** out);
+/* CUDA-graph plan of round_fixed_krp (Philox mode): the whole sweep is
+ * captured once for this input buffer and replayed by ttr_plan_execute into
+ * the plan-owned output (borrow it with ttr_plan_output; it stays valid until
+ * ttr_plan_destroy). The input's contents may change between executions;
+ * its shape may not. No synchronisation. */
+typedef struct ttr_plan ttr_plan;
+ttr_status ttr_plan_fixed_krp(ttr_ctx* ctx, const ttr_tt* tt, const int64_t* target_ranks,
+                              int64_t count, uint64_t seed, int rng_mode, ttr_plan** out);
+ttr_status ttr_plan_execute(ttr_plan* plan);
+ttr_status ttr_plan_output(ttr_plan* plan, const ttr_tt** out);
+ttr_status ttr_plan_destroy(ttr_plan* plan);
+
 ttr_status ttr_round_adaptive_krp(ttr_ctx* ctx, const ttr_tt* tt, const ttr_adaptive_cfg* cfg,
                                   ttr_tt** out);
 ttr_status ttr_round_deterministic_tol(ttr_ctx* ctx, const ttr_tt* tt, double eps, ttr_tt** out);

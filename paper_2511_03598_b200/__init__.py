@@ -285,6 +285,50 @@ def round_fixed_krp(tt: TTTensor, target_ranks: Sequence[int], seed: int, rng: i
                          C.c_int64(len(target_ranks)), C.c_uint64(seed), C.c_int(rng))
 
 
+class FixedKrpPlan:
+    """CUDA-graph plan of round_fixed_krp for one input buffer (ttr_plan):
+    `execute()` replays the captured sweep; `output` is the plan-owned result
+    (valid until the plan is closed)."""
+
+    def __init__(self, tt: TTTensor, target_ranks: Sequence[int], seed: int, rng: int = RNG_PHILOX):
+        self.ctx = tt.ctx
+        self.input = tt
+        self._h = C.c_void_p()
+        _check(lib().ttr_plan_fixed_krp(tt.ctx._h, tt._h, _i64(target_ranks), C.c_int64(len(target_ranks)),
+                                        C.c_uint64(seed), C.c_int(rng), C.byref(self._h)))
+        out = C.c_void_p()
+        _check(lib().ttr_plan_output(self._h, C.byref(out)))
+        self.output = _BorrowedTT(out, tt.ctx, self)
+
+    def execute(self):
+        _check(lib().ttr_plan_execute(self._h))
+
+    def close(self):
+        if getattr(self, "_h", None) and self._h.value and _lib is not None:
+            _lib.ttr_plan_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        self.close()
+
+
+class _BorrowedTT(TTTensor):
+    """A TTTensor view owned by someone else (not destroyed on GC)."""
+
+    def __init__(self, handle, ctx, owner):
+        super().__init__(handle, ctx)
+        self._owner = owner
+
+    def __del__(self):
+        pass
+
+
+def copy_from_host(tt: TTTensor, flat: np.ndarray):
+    """Overwrite the cores of `tt` from a host buffer (same shape, reference layout)."""
+    flat = np.ascontiguousarray(flat, dtype=np.float64)
+    _check(lib().ttr_tt_copy_from_host(tt.ctx._h, tt._h, _dptr(flat)))
+
+
 @dataclass
 class AdaptiveConfig:
     """ttround::AdaptiveConfig (round_rand.hpp:18-25)."""

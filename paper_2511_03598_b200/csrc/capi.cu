@@ -167,6 +167,15 @@ ttr_status ttr_tt_download(ttr_ctx* ctx, const ttr_tt* tt, double* host) {
     });
 }
 
+ttr_status ttr_tt_copy_from_host(ttr_ctx* ctx, ttr_tt* tt, const double* host) {
+    return guard([&] {
+        check_same_ctx(ctx, tt);
+        need(host != nullptr, "null input");
+        tt->t->upload(host);
+        TTR_CUDA(cudaStreamSynchronize(ctx->c.stream));
+    });
+}
+
 ttr_status ttr_tt_core_ptr(const ttr_tt* tt, int64_t k, const double** ptr) {
     return guard([&] {
         need(tt && tt->t && ptr, "null argument");
@@ -232,6 +241,48 @@ ttr_status ttr_round_fixed_krp(ttr_ctx* ctx, const ttr_tt* tt, const int64_t* ra
         need(rng_mode == TTR_RNG_PHILOX || rng_mode == TTR_RNG_XOSHIRO, "unknown rng mode");
         if (count < 0 || (count > 0 && !ranks)) fail(Errc::InvalidRanks, "expected d-1 target ranks");
         *out = wrap(round_fixed_krp(ctx->c, *tt->t, vec(ranks, count), seed, rng_mode));
+    });
+}
+
+ttr_status ttr_plan_fixed_krp(ttr_ctx* ctx, const ttr_tt* tt, const int64_t* ranks, int64_t count, uint64_t seed,
+                              int rng_mode, ttr_plan** out) {
+    return guard([&] {
+        check_same_ctx(ctx, tt);
+        need(out != nullptr, "null output");
+        if (count < 0 || (count > 0 && !ranks)) fail(Errc::InvalidRanks, "expected d-1 target ranks");
+        auto* p = new ttr_plan;
+        try {
+            p->plan = std::make_unique<Plan>(ctx->c, *tt->t, vec(ranks, count), seed, rng_mode);
+        } catch (...) {
+            delete p;
+            throw;
+        }
+        p->out.t = std::move(p->plan->out);
+        p->ctx = ctx;
+        *out = p;
+    });
+}
+
+ttr_status ttr_plan_execute(ttr_plan* plan) {
+    return guard([&] {
+        need(plan && plan->plan, "null plan");
+        plan->plan->execute();
+    });
+}
+
+ttr_status ttr_plan_output(ttr_plan* plan, const ttr_tt** out) {
+    return guard([&] {
+        need(plan && out, "null argument");
+        *out = &plan->out;
+    });
+}
+
+ttr_status ttr_plan_destroy(ttr_plan* plan) {
+    return guard([&] {
+        if (!plan) return;
+        cudaStreamSynchronize(plan->ctx->c.stream);
+        plan->plan.reset();
+        delete plan;
     });
 }
 

@@ -237,6 +237,31 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32)
 
     // epilogue: fragment (i, j) holds rows wm0+i*8+fr, cols wn0+j*8+2*fc+{0,1}
     const bool split = gridDim.z > 1;
+    if (!split && p.beta != 0.0) {
+        // beta != 0: per fragment row, issue all C loads before the stores
+        // (no load->store chains; bounded extra registers)
+#pragma unroll
+        for (int i = 0; i < FM; ++i) {
+            const int gm = m0 + wm0 + i * 8 + fr;
+            double cv[FN][2];
+#pragma unroll
+            for (int j = 0; j < FN; ++j)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int gn = n0 + wn0 + j * 8 + 2 * fc + h;
+                    cv[j][h] = (gm < p.M && gn < p.N) ? __ldcg(p.C + gm + static_cast<i64>(gn) * p.ldc) : 0.0;
+                }
+#pragma unroll
+            for (int j = 0; j < FN; ++j)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int gn = n0 + wn0 + j * 8 + 2 * fc + h;
+                    if (gm < p.M && gn < p.N)
+                        p.C[gm + static_cast<i64>(gn) * p.ldc] = fma(p.beta, cv[j][h], p.alpha * acc[i][j][h]);
+                }
+        }
+        return;
+    }
 #pragma unroll
     for (int i = 0; i < FM; ++i) {
         const int gm = m0 + wm0 + i * 8 + fr;

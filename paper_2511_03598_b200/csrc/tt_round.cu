@@ -327,22 +327,39 @@ static std::vector<i64> checked_targets(const TTDev& t, const std::vector<i64>& 
     return targets;
 }
 
-std::unique_ptr<TTDev> round_fixed_krp(Ctx& c, const TTDev& t, const std::vector<i64>& target_ranks,
-                                       std::uint64_t seed, int rng_mode) {
+// Output ranks of the fixed-rank sweep: l_eff = min(l_k, rows, cols) of V(Y_k)
+// (round_rand.cpp:34-35).
+std::vector<i64> fixed_krp_ranks(const TTDev& t, const std::vector<i64>& target_ranks) {
     auto targets = checked_targets(t, target_ranks);
     const i64 d = t.d();
-    if (d == 1) return copy_tt(c, t);
+    std::vector<i64> r(d + 1, 1);
+    for (i64 k = 1; k < d; ++k) r[k] = std::min({targets[k - 1], r[k - 1] * t.n[k - 1], t.r[k]});
+    return r;
+}
+
+std::unique_ptr<TTDev> round_fixed_krp(Ctx& c, const TTDev& t, const std::vector<i64>& target_ranks,
+                                       std::uint64_t seed, int rng_mode) {
+    auto r = fixed_krp_ranks(t, target_ranks);
+    if (t.d() == 1) return copy_tt(c, t);
+    auto out = std::make_unique<TTDev>(c, t.n, r);
+    round_fixed_krp_into(c, t, target_ranks, seed, rng_mode, *out);
+    return out;
+}
+
+// The sweep proper, writing into a preallocated output (used directly by the
+// CUDA-graph plan: every launch below is a pure stream operation).
+void round_fixed_krp_into(Ctx& c, const TTDev& t, const std::vector<i64>& target_ranks, std::uint64_t seed,
+                          int rng_mode, TTDev& out_tt) {
+    auto targets = checked_targets(t, target_ranks);
+    const i64 d = t.d();
     const i64 width = *std::max_element(targets.begin(), targets.end());
     Sketch sk(c, t, width, rng_mode, seed);
     {
         PhaseScope ph(c, kPhaseSketch);
         sk.append(2, width);
     }
-
-    // output ranks (l_eff caps, round_rand.cpp:34-35)
-    std::vector<i64> r(d + 1, 1);
-    for (i64 k = 1; k < d; ++k) r[k] = std::min({targets[k - 1], r[k - 1] * t.n[k - 1], t.r[k]});
-    auto out = std::make_unique<TTDev>(c, t.n, r);
+    const std::vector<i64>& r = out_tt.r;
+    TTDev* out = &out_tt;
 
     i64 max_work = 0, max_s = 0;
     for (i64 k = 1; k < d; ++k) {
@@ -377,7 +394,61 @@ std::unique_ptr<TTDev> round_fixed_krp(Ctx& c, const TTDev& t, const std::vector
         }
         v = dst;  // stream order: this iteration's reads of the old V precede the write
     }
-    return out;
+}
+
+// ---------------------------------------------------------------------------
+// CUDA-graph plan for fixed-rank KRP rounding: one eager run sizes every
+// workspace (and the split-K scratch), then the whole sweep — ~2,400 launches
+// for config 5b — is captured once and replayed with a single graph launch.
+Plan::Plan(Ctx& cc, const TTDev& in_, const std::vector<i64>& ranks_, std::uint64_t seed_, int rng)
+    : c(cc), in(in_), ranks(ranks_), seed(seed_), rng_mode(rng) {
+    if (rng_mode != TTR_RNG_PHILOX) fail(Errc::InvalidArgument, "plans need the device (Philox) generator");
+    auto r = fixed_krp_ranks(in, ranks);
+    if (in.d() < 2) fail(Errc::InvalidArgument, "plans need d >= 2");
+    out = std::make_unique<TTDev>(c, in.n, r);
+    round_fixed_krp_into(c, in, ranks, seed, rng_mode, *out);  // eager run: sizes pools and scratch
+    TTR_CUDA(cudaStreamSynchronize(c.stream));
+    const bool timing = c.timing;
+    c.timing = false;
+    const Counts saved = c.counts;
+    const std::uint64_t l0 = c.launches;
+    TTR_CUDA(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal));
+    try {
+        round_fixed_krp_into(c, in, ranks, seed, rng_mode, *out);
+    } catch (...) {
+        cudaGraph_t g;
+        cudaStreamEndCapture(c.stream, &g);
+        if (g) cudaGraphDestroy(g);
+        c.timing = timing;
+        throw;
+    }
+    TTR_CUDA(cudaStreamEndCapture(c.stream, &graph));
+    launches_per_run = c.launches - l0;
+    flops = c.counts;  // counters of one run (captured run)
+    flops.gemm -= saved.gemm;
+    flops.qr -= saved.qr;
+    flops.svd -= saved.svd;
+    flops.sketch -= saved.sketch;
+    flops.rng -= saved.rng;
+    c.counts = saved;
+    c.launches = l0;
+    c.timing = timing;
+    TTR_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+}
+
+void Plan::execute() {
+    TTR_CUDA(cudaGraphLaunch(exec, c.stream));
+    c.counts.gemm += flops.gemm;
+    c.counts.qr += flops.qr;
+    c.counts.svd += flops.svd;
+    c.counts.sketch += flops.sketch;
+    c.counts.rng += flops.rng;
+    c.launched(static_cast<int>(launches_per_run));
+}
+
+Plan::~Plan() {
+    if (exec) cudaGraphExecDestroy(exec);
+    if (graph) cudaGraphDestroy(graph);
 }
 
 // ---------------------------------------------------------------------------

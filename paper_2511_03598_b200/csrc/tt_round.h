@@ -45,6 +45,28 @@ double relative_error(Ctx& c, const TTDev& a, const TTDev& b);
 
 std::unique_ptr<TTDev> round_fixed_krp(Ctx& c, const TTDev& t, const std::vector<i64>& target_ranks, std::uint64_t seed,
                                        int rng_mode);
+std::vector<i64> fixed_krp_ranks(const TTDev& t, const std::vector<i64>& target_ranks);
+void round_fixed_krp_into(Ctx& c, const TTDev& t, const std::vector<i64>& target_ranks, std::uint64_t seed,
+                          int rng_mode, TTDev& out);
+
+// Captured CUDA graph of round_fixed_krp for a fixed input buffer (contents
+// may change between executions) writing into an owned output tensor.
+struct Plan {
+    Ctx& c;
+    const TTDev& in;
+    std::vector<i64> ranks;
+    std::uint64_t seed;
+    int rng_mode;
+    std::unique_ptr<TTDev> out;
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    std::uint64_t launches_per_run = 0;
+    Counts flops;
+    Plan(Ctx& c, const TTDev& in, const std::vector<i64>& ranks, std::uint64_t seed, int rng_mode);
+    ~Plan();
+    void execute();
+};
+
 std::unique_ptr<TTDev> round_adaptive_krp(Ctx& c, const TTDev& t, const AdaptiveCfg& cfg, std::vector<double>* trace);
 double estimate_norm_krp(Ctx& c, const TTDev& t, i64 width, std::uint64_t seed, int rng_mode);
 std::unique_ptr<TTDev> round_deterministic_tol(Ctx& c, const TTDev& t, double eps);
@@ -61,4 +83,9 @@ struct ttr_tt {
 };
 struct ttr_ctx {
     ttr::Ctx c;
+};
+struct ttr_plan {
+    std::unique_ptr<ttr::Plan> plan;
+    ttr_tt out;
+    ttr_ctx* ctx = nullptr;
 };

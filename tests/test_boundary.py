@@ -1,0 +1,72 @@
+"""CPU-side checks of the drop-in boundary: the C-ABI library builds for
+sm_100a, loads without a GPU, and exports every entry point that
+include/ttround_b200.h declares; status codes mirror the reference Errc order."""
+import ctypes as C
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    text = open(os.path.join(ROOT, "include", "ttround_b200.h")).read()
+    return sorted(set(re.findall(r"^\s*(?:ttr_status|const char\*)\s+(ttr_\w+)\s*\(", text, re.M)))
+
+
+def test_header_declares_the_hot_path_entry_points():
+    syms = declared_symbols()
+    for s in ["ttr_round_fixed_krp", "ttr_round_adaptive_krp", "ttr_round_deterministic_tol",
+              "ttr_round_deterministic_ranks", "ttr_estimate_norm_krp", "ttr_tt_upload", "ttr_tt_download",
+              "ttr_norm_exact", "ttr_relative_error", "ttr_krp_partial_contractions", "ttr_plan_fixed_krp"]:
+        assert s in syms
+
+
+def test_library_exports_every_declared_symbol():
+    import paper_2511_03598_b200 as P
+    lib = P.lib()
+    missing = [s for s in declared_symbols() if not hasattr(lib, s)]
+    assert not missing, missing
+    out = subprocess.run(["nm", "-D", "--defined-only", P.LIB_PATH], capture_output=True, text=True).stdout
+    for s in declared_symbols():
+        assert re.search(rf"\bT {s}\b", out), s
+
+
+def test_library_is_sm100a_code():
+    import paper_2511_03598_b200 as P
+    out = subprocess.run(["cuobjdump", "--list-elf", P.LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_status_codes_mirror_reference_errc_order():
+    """types.hpp:15-31 order; the header assigns 1 + index."""
+    import paper_2511_03598_b200 as P
+    text = open(os.path.join(ROOT, "include", "ttround_b200.h")).read()
+    names = ["RANK_CHAIN_MISMATCH", "BOUNDARY_RANK_NOT_ONE", "EMPTY_CORE_LIST", "INDEX_OUT_OF_RANGE",
+             "DENSE_TOO_LARGE", "MODE_SIZE_MISMATCH", "EMPTY_TERM_LIST", "INVALID_RANK_CHAIN", "SVD_FAILURE",
+             "INVALID_RANKS", "NOT_LEFT_ORTHOGONAL", "INVALID_GRID", "BREAKDOWN", "INVALID_ARGUMENT", "IO"]
+    for i, n in enumerate(names):
+        assert re.search(rf"TTR_ERR_{n}\s*=\s*{i + 1}\b", text), n
+    assert P.ERRC_NAMES[9] == "InvalidRanks"
+
+
+def test_no_device_fails_loudly():
+    """Without a GPU the product raises instead of silently computing on the CPU."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    import paper_2511_03598_b200 as P
+    with pytest.raises(P.TTRoundError) as e:
+        P.Context(0)
+    assert e.value.code == "NoDevice"
+
+
+def test_product_package_does_not_import_the_oracle():
+    pkg = os.path.join(ROOT, "paper_2511_03598_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
+                text = open(os.path.join(dirpath, f)).read()
+                assert "py_oracle" not in text and "ttr_oracle" not in text, f
