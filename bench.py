@@ -237,11 +237,13 @@ def run_ours(args, world, rank, local):
     e1 = torch.cuda.Event(enable_timing=True)
     l0 = ctx.kernel_launches()
     with ClockSampler(local) as clk:
+        torch.cuda.profiler.start()  # ncu --profile-from-start off captures exactly the timed steps
         e0.record(stream)
         for _ in range(args.steps):
             step()
         e1.record(stream)
         torch.cuda.synchronize()
+        torch.cuda.profiler.stop()
     launches = ctx.kernel_launches() - l0
     ms = e0.elapsed_time(e1) / args.steps
     if world > 1:

@@ -508,10 +508,7 @@ void thin_qr(Ctx& c, i64 m, i64 n, const double* A, i64 lda, double* Q, i64 ldq,
     const i64 k = std::min(m, n);
     c.charge_qr(4ULL * static_cast<std::uint64_t>(m) * n * k);
     if (m <= 0 || n <= 0) return;
-    if (m * n <= kSmallMaxElems) {
-        qr_small_batched(c, m, n, A, lda, 0, Q, ldq, 0, R, ldr, 0, 1);
-        return;
-    }
+    (void)kSmallMaxElems;  // the single-CTA smem kernel serves the batched API only
     // Panels hold at most 2 rows x 32 columns per thread in registers (one CTA
     // per SM): taller R-only factorizations (norm_exact of very tall cores)
     // go through a TSQR split — R of each row block, then R of the stacked Rs.

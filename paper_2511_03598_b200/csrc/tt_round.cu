@@ -369,6 +369,7 @@ void round_fixed_krp_into(Ctx& c, const TTDev& t, const std::vector<i64>& target
     DBuf work(c, static_cast<std::size_t>(max_work));
     DBuf S(c, static_cast<std::size_t>(max_s));
     DBuf M(c, static_cast<std::size_t>(width * t.max_rank()));
+    DBuf Qt(c, static_cast<std::size_t>(max_s));
 
     const double* v = t.core(0);
     for (i64 k = 1; k < d; ++k) {
@@ -388,7 +389,10 @@ void round_fixed_krp_into(Ctx& c, const TTDev& t, const std::vector<i64>& target
         {
             PhaseScope ph(c, kPhaseGemm);
             // M = Q^T V  (l x r_k)
-            gemm(c, true, l, cols, rows, 1.0, out->core(k - 1), rows, v, rows, 0.0, M.p, l);
+            // (as Q^T then a plain GEMM: the column-major A-tile path streams
+            // 1 KB runs of HBM; the transposed-A path only 128 B ones)
+            transpose(c, rows, l, out->core(k - 1), rows, Qt.p, l);
+            gemm(c, false, l, cols, rows, 1.0, Qt.p, l, v, rows, 0.0, M.p, l);
             // H(Y_{k+1}) = M H(X_{k+1})  (contract_first, internal.hpp:10-12)
             gemm(c, false, l, ncols, cols, 1.0, M.p, l, t.core(k), cols, 0.0, dst, l);
         }

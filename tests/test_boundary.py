@@ -70,3 +70,27 @@ def test_product_package_does_not_import_the_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
                 text = open(os.path.join(dirpath, f)).read()
                 assert "py_oracle" not in text and "ttr_oracle" not in text, f
+
+
+def _build_wrapper_smoke(tmp_path):
+    import paper_2511_03598_b200 as P
+    exe = str(tmp_path / "wrapper_smoke")
+    libdir = os.path.dirname(P.LIB_PATH)
+    cmd = ["g++", "-std=c++17", "-O2", "-I", os.path.join(ROOT, "include"),
+           os.path.join(ROOT, "tests", "cpp", "wrapper_smoke.cpp"), "-L", libdir, "-lttround_b200",
+           f"-Wl,-rpath,{libdir}", "-o", exe]
+    subprocess.run(cmd, check=True)
+    return exe
+
+
+def test_cpp_wrapper_compiles_and_links(tmp_path):
+    """include/ttround_b200/ttround.hpp: the reference-shaped C++ API builds against the C ABI."""
+    assert os.path.exists(_build_wrapper_smoke(tmp_path))
+
+
+@pytest.mark.gpu
+def test_cpp_wrapper_runs_on_device(tmp_path):
+    exe = _build_wrapper_smoke(tmp_path)
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "wrapper ok" in out.stdout
