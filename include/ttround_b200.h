@@ -183,6 +183,26 @@ ttr_status ttr_gemm(ttr_ctx* ctx, int trans_a, int64_t m, int64_t n, int64_t k, 
 ttr_status ttr_ctx_enable_timing(ttr_ctx* ctx, int on);
 ttr_status ttr_ctx_phase_times(ttr_ctx* ctx, double* ms_out /*4*/, uint64_t* count_out /*4*/);
 
+/* ---- batches of independent, identically shaped tensors (config 5a) ------
+ * Tensor b of a batch is rounded exactly as
+ *   round_fixed_krp(Y_b, target_ranks, derive_seed(seed, b))   (Philox mode)
+ * with one launch per step for the whole batch (strided-batch GEMMs, one CTA
+ * per QR). Host buffers hold the tensors back to back, each in the
+ * ttr_tt_upload layout. */
+typedef struct ttr_batch ttr_batch;
+ttr_status ttr_batch_upload(ttr_ctx* ctx, int64_t batch, int64_t d, const int64_t* n, const int64_t* r,
+                            const double* host, ttr_batch** out);
+/* Y_b = X_b/||X_b|| + eps Z_b/||Z_b||, X_b, Z_b Gaussian TTs (ranks rx, rz) drawn
+ * on the device from derive_seed(derive_seed(seed, b), 1|2) (Philox). */
+ttr_status ttr_batch_two_part_philox(ttr_ctx* ctx, int64_t batch, int64_t d, int64_t n, int64_t rx,
+                                     int64_t rz, double eps, uint64_t seed, ttr_batch** out);
+ttr_status ttr_batch_shape(const ttr_batch* b, int64_t* batch, int64_t* d, int64_t* n, int64_t* r,
+                           int64_t* total);
+ttr_status ttr_batch_download(ttr_ctx* ctx, const ttr_batch* b, int64_t first, int64_t count, double* host);
+ttr_status ttr_batch_destroy(ttr_batch* b);
+ttr_status ttr_round_fixed_krp_batched(ttr_ctx* ctx, const ttr_batch* b, const int64_t* target_ranks,
+                                       int64_t count, uint64_t seed, ttr_batch** out);
+
 ttr_status ttr_counters(ttr_ctx* ctx, ttr_counts* out);
 ttr_status ttr_counters_reset(ttr_ctx* ctx);
 

@@ -329,6 +329,60 @@ def copy_from_host(tt: TTTensor, flat: np.ndarray):
     _check(lib().ttr_tt_copy_from_host(tt.ctx._h, tt._h, _dptr(flat)))
 
 
+class TTBatch:
+    """Batch of identically shaped device TT tensors (ttr_batch, config 5a)."""
+
+    def __init__(self, handle, ctx: Context):
+        self._h = handle
+        self.ctx = ctx
+
+    def __del__(self):
+        if getattr(self, "_h", None) and self._h.value and _lib is not None:
+            _lib.ttr_batch_destroy(self._h)
+            self._h = C.c_void_p()
+
+    @staticmethod
+    def from_flats(mode_sizes, ranks, flats: Sequence[np.ndarray], ctx: Optional[Context] = None) -> "TTBatch":
+        ctx = ctx or default_context()
+        host = np.ascontiguousarray(np.concatenate([np.asarray(f, dtype=np.float64) for f in flats]))
+        out = C.c_void_p()
+        _check(lib().ttr_batch_upload(ctx._h, C.c_int64(len(flats)), C.c_int64(len(mode_sizes)), _i64(mode_sizes),
+                                      _i64(ranks), _dptr(host), C.byref(out)))
+        return TTBatch(out, ctx)
+
+    @staticmethod
+    def two_part_philox(batch, d, n, rx, rz, eps, seed, ctx: Optional[Context] = None) -> "TTBatch":
+        ctx = ctx or default_context()
+        out = C.c_void_p()
+        _check(lib().ttr_batch_two_part_philox(ctx._h, C.c_int64(batch), C.c_int64(d), C.c_int64(n), C.c_int64(rx),
+                                               C.c_int64(rz), C.c_double(eps), C.c_uint64(seed), C.byref(out)))
+        return TTBatch(out, ctx)
+
+    def shape(self):
+        b, d = C.c_int64(), C.c_int64()
+        _check(lib().ttr_batch_shape(self._h, C.byref(b), C.byref(d), None, None, None))
+        n = (C.c_int64 * d.value)()
+        r = (C.c_int64 * (d.value + 1))()
+        tot = C.c_int64()
+        _check(lib().ttr_batch_shape(self._h, C.byref(b), C.byref(d), n, r, C.byref(tot)))
+        return b.value, list(n), list(r), tot.value
+
+    def flats(self, first=0, count=None) -> List[np.ndarray]:
+        b, _, _, tot = self.shape()
+        count = b - first if count is None else count
+        out = np.empty(max(1, count * tot), dtype=np.float64)
+        _check(lib().ttr_batch_download(self.ctx._h, self._h, C.c_int64(first), C.c_int64(count), _dptr(out)))
+        return [out[q * tot:(q + 1) * tot].copy() for q in range(count)]
+
+
+def round_fixed_krp_batched(batch: TTBatch, target_ranks: Sequence[int], seed: int) -> TTBatch:
+    """Tensor b rounded as round_fixed_krp(Y_b, target_ranks, derive_seed(seed, b)) (Philox)."""
+    out = C.c_void_p()
+    _check(lib().ttr_round_fixed_krp_batched(batch.ctx._h, batch._h, _i64(target_ranks), C.c_int64(len(target_ranks)),
+                                             C.c_uint64(seed), C.byref(out)))
+    return TTBatch(out, batch.ctx)
+
+
 @dataclass
 class AdaptiveConfig:
     """ttround::AdaptiveConfig (round_rand.hpp:18-25)."""

@@ -424,6 +424,85 @@ ttr_status ttr_ctx_phase_times(ttr_ctx* ctx, double* ms_out, uint64_t* count_out
     });
 }
 
+// ---- batches of independent tensors (config 5a) ----
+ttr_status ttr_batch_upload(ttr_ctx* ctx, int64_t batch, int64_t d, const int64_t* n, const int64_t* r,
+                            const double* host, ttr_batch** out) {
+    return guard([&] {
+        need(ctx && out && n && r && host, "null argument");
+        if (d < 1) fail(Errc::EmptyCoreList, "TT tensor needs at least one core");
+        auto t = std::make_unique<TTBatch>(ctx->c, batch, vec(n, d), vec(r, d + 1));
+        const i64 tot = t->total();
+        for (i64 b = 0; b < batch; ++b) {
+            i64 o = 0;
+            for (i64 k = 0; k < d; ++k) {
+                TTR_CUDA(cudaMemcpyAsync(t->core(b, k), host + b * tot + o, sizeof(double) * t->core_size(k),
+                                         cudaMemcpyHostToDevice, ctx->c.stream));
+                o += t->core_size(k);
+            }
+        }
+        TTR_CUDA(cudaStreamSynchronize(ctx->c.stream));
+        auto* o = new ttr_batch;
+        o->t = std::move(t);
+        *out = o;
+    });
+}
+
+ttr_status ttr_batch_two_part_philox(ttr_ctx* ctx, int64_t batch, int64_t d, int64_t n, int64_t rx, int64_t rz,
+                                     double eps, uint64_t seed, ttr_batch** out) {
+    return guard([&] {
+        need(ctx && out, "null argument");
+        need(batch >= 1 && d >= 2 && n >= 1 && rx >= 1 && rz >= 1, "bad batch shape");
+        auto* o = new ttr_batch;
+        o->t = batch_two_part_philox(ctx->c, batch, d, n, rx, rz, eps, seed);
+        *out = o;
+    });
+}
+
+ttr_status ttr_batch_shape(const ttr_batch* b, int64_t* batch, int64_t* d, int64_t* n, int64_t* r, int64_t* total) {
+    return guard([&] {
+        need(b && b->t, "null batch");
+        const TTBatch& t = *b->t;
+        if (batch) *batch = t.batch;
+        if (d) *d = t.d();
+        if (n) for (i64 k = 0; k < t.d(); ++k) n[k] = t.n[k];
+        if (r) for (i64 k = 0; k <= t.d(); ++k) r[k] = t.r[k];
+        if (total) *total = t.total();
+    });
+}
+
+ttr_status ttr_batch_download(ttr_ctx* ctx, const ttr_batch* b, int64_t first, int64_t count, double* host) {
+    return guard([&] {
+        need(ctx && b && b->t && host, "null argument");
+        const TTBatch& t = *b->t;
+        if (first < 0 || count < 0 || first + count > t.batch) fail(Errc::IndexOutOfRange, "batch range out of range");
+        const i64 tot = t.total();
+        for (i64 q = 0; q < count; ++q) {
+            i64 o = 0;
+            for (i64 k = 0; k < t.d(); ++k) {
+                TTR_CUDA(cudaMemcpyAsync(host + q * tot + o, t.core(first + q, k), sizeof(double) * t.core_size(k),
+                                         cudaMemcpyDeviceToHost, ctx->c.stream));
+                o += t.core_size(k);
+            }
+        }
+        TTR_CUDA(cudaStreamSynchronize(ctx->c.stream));
+    });
+}
+
+ttr_status ttr_batch_destroy(ttr_batch* b) {
+    return guard([&] { delete b; });
+}
+
+ttr_status ttr_round_fixed_krp_batched(ttr_ctx* ctx, const ttr_batch* b, const int64_t* ranks, int64_t count,
+                                       uint64_t seed, ttr_batch** out) {
+    return guard([&] {
+        need(ctx && b && b->t && out, "null argument");
+        if (count < 0 || (count > 0 && !ranks)) fail(Errc::InvalidRanks, "expected d-1 target ranks");
+        auto* o = new ttr_batch;
+        o->t = round_fixed_krp_batched(ctx->c, *b->t, vec(ranks, count), seed);
+        *out = o;
+    });
+}
+
 ttr_status ttr_counters(ttr_ctx* ctx, ttr_counts* out) {
     return guard([&] {
         need(ctx && out, "null argument");

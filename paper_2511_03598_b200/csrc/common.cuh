@@ -141,6 +141,20 @@ void krp_step(Ctx& c, i64 r_left, i64 n, i64 r_right, i64 N, const double* X, co
               i64 ldo, const double* Wt, i64 ldwt, double* W_out, i64 ldw, double* Wt_out, i64 ldwt_out,
               bool last_core);
 
+// Strided batches of independent problems (config 5a): problem b reads
+// A + b*sA, B + b*sB (Omega + b*sO, Wt + b*sWt) and writes C + b*sC.
+void gemm_batched(Ctx& c, bool trans_a, i64 M, i64 N, i64 K, double alpha, const double* A, i64 lda, i64 sA,
+                  const double* B, i64 ldb, i64 sB, double beta, double* C, i64 ldc, i64 sC, i64 batch,
+                  bool count = true);
+void krp_step_batched(Ctx& c, i64 r_left, i64 n, i64 r_right, i64 N, const double* X, i64 sX, const double* Omega,
+                      i64 ldo, i64 sO, const double* Wt, i64 ldwt, i64 sWt, double* W_out, i64 ldw, i64 sW,
+                      double* Wt_out, i64 ldwt_out, i64 sWto, i64 batch, bool last_core);
+void qr_small_batched(Ctx& c, i64 m, i64 n, const double* A, i64 lda, i64 sA, double* Q, i64 ldq, i64 sQ, double* R,
+                      i64 ldr, i64 sR, i64 batch);
+// Omega for a batch: tensor b uses seed derive_seed(seed, b).
+void philox_factor_batched(Ctx& c, std::uint64_t seed, i64 mode, i64 rows, i64 cols, double* out, i64 ld, i64 stride,
+                           i64 batch);
+
 // ---- kernels (dense_ops.cu) -------------------------------------------------
 void philox_factor(Ctx& c, std::uint64_t seed, i64 mode, i64 rows, i64 cols, i64 col0, double* out, i64 ld);
 void fill(Ctx& c, double* p, std::size_t count, double v);

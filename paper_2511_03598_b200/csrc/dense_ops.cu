@@ -38,6 +38,35 @@ __global__ void philox_factor_kernel(std::uint64_t seed, std::uint32_t mode, int
     }
 }
 
+// derive_seed (proj/core/src/rng.cpp:75-78) on the device
+__device__ __forceinline__ std::uint64_t dev_derive_seed(std::uint64_t seed, std::uint64_t tag) {
+    std::uint64_t x = seed ^ (0xd1342543de82ef95ULL * (tag + 1));
+    x += 0x9e3779b97f4a7c15ULL;
+    std::uint64_t z = x;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+}
+
+// Omega_mode for every tensor b of a batch (tensor b: seed derive_seed(seed, b)).
+__global__ void philox_factor_batched_kernel(std::uint64_t seed, std::uint32_t mode, int rows, int cols, double* out,
+                                             i64 ld, i64 stride, int batch) {
+    const int pairs = (rows + 1) / 2;
+    const i64 per = static_cast<i64>(pairs) * cols, total = per * batch;
+    for (i64 idx = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; idx < total;
+         idx += static_cast<i64>(gridDim.x) * blockDim.x) {
+        const int b = static_cast<int>(idx / per);
+        const i64 r = idx % per;
+        const int p = static_cast<int>(r % pairs), c = static_cast<int>(r / pairs);
+        double e, o;
+        ttr_philox_gauss_pair(dev_derive_seed(seed, static_cast<std::uint64_t>(b)), mode, static_cast<std::uint32_t>(c),
+                              static_cast<std::uint32_t>(p), TTR_PHILOX_TAG_KRP, &e, &o);
+        double* dst = out + b * stride + static_cast<i64>(c) * ld + 2 * p;
+        dst[0] = e;
+        if (2 * p + 1 < rows) dst[1] = o;
+    }
+}
+
 // i.i.d. sigma * N(0,1) fill for device-side test/bench inputs (Philox with
 // tag = stream_tag, counter = element pair index).
 __global__ void random_normal_kernel(std::uint64_t seed, std::uint32_t tag, double* out, i64 count, double sigma) {
@@ -155,6 +184,17 @@ void philox_factor(Ctx& c, std::uint64_t seed, i64 mode, i64 rows, i64 cols, i64
     c.counts.rng += static_cast<std::uint64_t>(rows * cols);
     philox_factor_kernel<<<grid_for(c, static_cast<std::size_t>((rows + 1) / 2 * cols)), kThreads, 0, c.stream>>>(
         seed, static_cast<std::uint32_t>(mode), static_cast<int>(rows), static_cast<int>(cols), col0, out, ld);
+    TTR_CUDA(cudaGetLastError());
+    c.launched();
+}
+
+void philox_factor_batched(Ctx& c, std::uint64_t seed, i64 mode, i64 rows, i64 cols, double* out, i64 ld, i64 stride,
+                           i64 batch) {
+    if (rows <= 0 || cols <= 0 || batch <= 0) return;
+    c.counts.rng += static_cast<std::uint64_t>(rows * cols * batch);
+    philox_factor_batched_kernel<<<grid_for(c, static_cast<std::size_t>((rows + 1) / 2 * cols * batch)), kThreads, 0,
+                                   c.stream>>>(seed, static_cast<std::uint32_t>(mode), static_cast<int>(rows),
+                                               static_cast<int>(cols), out, ld, stride, static_cast<int>(batch));
     TTR_CUDA(cudaGetLastError());
     c.launched();
 }

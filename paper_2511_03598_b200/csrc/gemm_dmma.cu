@@ -43,6 +43,9 @@ struct GemmArgs {
     double alpha, beta;
     double* work;  // split-K partials [split][N][M] (ld M)
     int ktiles_per_split;
+    // strided batch (blockIdx.z = batch index; no split-K when batch > 1)
+    int batch;
+    i64 sA, sB, sC, sW;
 };
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
@@ -96,8 +99,15 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32)
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int wm0 = (warp % C_::kWarpsM) * WM, wn0 = (warp / C_::kWarpsM) * WN;
     const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
+    const bool batched = p.batch > 1;
+    const int zsplit = batched ? 0 : static_cast<int>(blockIdx.z);
+    const i64 bz = batched ? static_cast<i64>(blockIdx.z) : 0;
+    const double* __restrict__ Ap = p.A + bz * p.sA;
+    const double* __restrict__ Bp = p.B + bz * p.sB;
+    const double* __restrict__ Wp = p.Wt + bz * p.sW;
+    double* Cp = p.C + bz * p.sC;
     const int total_kt = (p.K + BK - 1) / BK;
-    const int kt_begin = blockIdx.z * p.ktiles_per_split;
+    const int kt_begin = zsplit * p.ktiles_per_split;
     const int kt_end = min(total_kt, kt_begin + p.ktiles_per_split);
     const int nk = max(0, kt_end - kt_begin);
 
@@ -111,10 +121,10 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32)
                 const int kk = idx / CH, r = (idx % CH) * VA;
                 const int gm = m0 + r, gk = k0 + kk;
                 int bytes = 0;
-                const double* src = p.A;
+                const double* src = Ap;
                 if (gk < p.K && gm < p.M) {
                     bytes = 8 * min(VA, p.M - gm);
-                    src = p.A + gm + static_cast<i64>(gk) * p.lda;
+                    src = Ap + gm + static_cast<i64>(gk) * p.lda;
                 }
                 cp_async<VA>(sA + kk * C_::kLdA + r, src, bytes);
             }
@@ -124,10 +134,10 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32)
                 const int m = idx / CH, kk = (idx % CH) * VA;
                 const int gm = m0 + m, gk = k0 + kk;
                 int bytes = 0;
-                const double* src = p.A;
+                const double* src = Ap;
                 if (gm < p.M && gk < p.K) {
                     bytes = 8 * min(VA, p.K - gk);
-                    src = p.A + gk + static_cast<i64>(gm) * p.lda;
+                    src = Ap + gk + static_cast<i64>(gm) * p.lda;
                 }
                 cp_async<VA>(sA + m * C_::kLdA + kk, src, bytes);
             }
@@ -140,10 +150,10 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32)
                 const int n = idx / CH, kk = (idx % CH) * VB;
                 const int gn = n0 + n;
                 int bytes = 0;
-                const double* src = p.B;
+                const double* src = Bp;
                 if (gn < p.N && k0 + kk < p.K) {
                     bytes = 8 * min(VB, p.K - (k0 + kk));
-                    src = p.B + (jbase + kk) + static_cast<i64>(gn) * p.ldb;
+                    src = Bp + (jbase + kk) + static_cast<i64>(gn) * p.ldb;
                 }
                 cp_async<VB>(sB + n * C_::kLdB + kk, src, bytes);
             }
@@ -154,10 +164,10 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32)
             for (int idx = tid; idx < BN / VB; idx += C_::kThreads) {
                 const int n = idx * VB, gn = n0 + n;
                 int bytes = 0;
-                const double* src = p.Wt;
+                const double* src = Wp;
                 if (gn < p.N) {
                     bytes = 8 * min(VB, p.N - gn);
-                    src = p.Wt + gn + static_cast<i64>(g) * p.ldw;
+                    src = Wp + gn + static_cast<i64>(g) * p.ldw;
                 }
                 cp_async<VB>(sW + n, src, bytes);
             }
@@ -169,13 +179,13 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32)
                 const int n = idx / BK, kk = idx % BK;
                 const int gn = n0 + n, gk = k0 + kk;
                 int bytes = 0;
-                const double* so = p.B;
-                const double* sw = p.Wt;
+                const double* so = Bp;
+                const double* sw = Wp;
                 if (gn < p.N && gk < p.K) {
                     bytes = 8;
                     const int g = gk / p.nmode, j = gk - g * p.nmode;
-                    so = p.B + j + static_cast<i64>(gn) * p.ldb;
-                    sw = p.Wt + gn + static_cast<i64>(g) * p.ldw;
+                    so = Bp + j + static_cast<i64>(gn) * p.ldb;
+                    sw = Wp + gn + static_cast<i64>(g) * p.ldw;
                 }
                 cp_async<1>(sB + n * C_::kLdB + kk, so, bytes);
                 cp_async<1>(sW + n * C_::kLdB + kk, sw, bytes);
@@ -236,7 +246,7 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32)
     cp_wait<0>();
 
     // epilogue: fragment (i, j) holds rows wm0+i*8+fr, cols wn0+j*8+2*fc+{0,1}
-    const bool split = gridDim.z > 1;
+    const bool split = !batched && gridDim.z > 1;
     if (!split && p.beta != 0.0) {
         // beta != 0: per fragment row, issue all C loads before the stores
         // (no load->store chains; bounded extra registers)
@@ -249,7 +259,7 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32)
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
                     const int gn = n0 + wn0 + j * 8 + 2 * fc + h;
-                    cv[j][h] = (gm < p.M && gn < p.N) ? __ldcg(p.C + gm + static_cast<i64>(gn) * p.ldc) : 0.0;
+                    cv[j][h] = (gm < p.M && gn < p.N) ? __ldcg(Cp + gm + static_cast<i64>(gn) * p.ldc) : 0.0;
                 }
 #pragma unroll
             for (int j = 0; j < FN; ++j)
@@ -257,7 +267,7 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32)
                 for (int h = 0; h < 2; ++h) {
                     const int gn = n0 + wn0 + j * 8 + 2 * fc + h;
                     if (gm < p.M && gn < p.N)
-                        p.C[gm + static_cast<i64>(gn) * p.ldc] = fma(p.beta, cv[j][h], p.alpha * acc[i][j][h]);
+                        Cp[gm + static_cast<i64>(gn) * p.ldc] = fma(p.beta, cv[j][h], p.alpha * acc[i][j][h]);
                 }
         }
         return;
@@ -273,9 +283,9 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32)
                 const int gn = n0 + wn0 + j * 8 + 2 * fc + h;
                 if (gn >= p.N) continue;
                 if (split) {
-                    p.work[(static_cast<i64>(blockIdx.z) * p.N + gn) * p.M + gm] = acc[i][j][h];
+                    p.work[(static_cast<i64>(zsplit) * p.N + gn) * p.M + gm] = acc[i][j][h];
                 } else {
-                    double* dst = p.C + gm + static_cast<i64>(gn) * p.ldc;
+                    double* dst = Cp + gm + static_cast<i64>(gn) * p.ldc;
                     const double v = p.alpha * acc[i][j][h];
                     *dst = (p.beta == 0.0) ? v : fma(p.beta, *dst, v);
                 }
@@ -300,9 +310,12 @@ __global__ void splitk_reduce(const double* __restrict__ work, int S, int M, int
     }
 }
 
-__global__ void transpose_copy(const double* __restrict__ src, i64 lds, int M, int N, double* dst, i64 ldd) {
+__global__ void transpose_copy(const double* __restrict__ src, i64 lds, int M, int N, double* dst, i64 ldd,
+                               i64 ss = 0, i64 sd = 0) {
     __shared__ double tile[32][33];
     const int bx = blockIdx.x * 32, by = blockIdx.y * 32;
+    src += blockIdx.z * ss;
+    dst += blockIdx.z * sd;
     for (int y = threadIdx.y; y < 32; y += blockDim.y) {
         const int m = bx + threadIdx.x, n = by + y;
         if (m < M && n < N) tile[y][threadIdx.x] = src[m + static_cast<i64>(n) * lds];
@@ -323,7 +336,7 @@ void launch(Ctx& c, GemmArgs& a, int splits) {
         TTR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C_::kSmemBytes));
         configured = true;
     }
-    dim3 grid((a.M + BM - 1) / BM, (a.N + BN - 1) / BN, splits);
+    dim3 grid((a.M + BM - 1) / BM, (a.N + BN - 1) / BN, a.batch > 1 ? a.batch : splits);
     kern<<<grid, C_::kThreads, C_::kSmemBytes, c.stream>>>(a);
     TTR_CUDA(cudaGetLastError());
     c.launched();
@@ -332,6 +345,8 @@ void launch(Ctx& c, GemmArgs& a, int splits) {
 constexpr int kBM = 128, kBN = 64, kWM = 32, kWN = 32, kStages = 4;
 // skinny-M tile (M <= 32: the V^T A products of the blocked QR)
 constexpr int kSkBM = 32, kSkBN = 128;
+// small tile for strided batches of tiny problems (config 5a: 64 x 20 x 1024)
+constexpr int kSmBM = 64, kSmBN = 32;
 
 template <int BM, int BN, bool AT, int KM, int BK>
 void dispatch_vec(Ctx& c, GemmArgs& a, int splits, bool va2, bool vb2) {
@@ -359,11 +374,13 @@ int choose_splits(Ctx& c, i64 tiles, int total_kt) {
 }
 
 void run_gemm(Ctx& c, bool AT, int KM, int BK, GemmArgs& a, bool va2, bool vb2, int splits, double* C, i64 ldc,
-              double alpha, double beta, double* Ct, i64 ldct, bool skinny = false) {
+              double alpha, double beta, double* Ct, i64 ldct, bool skinny = false, i64 sCt = 0) {
+    const bool small = a.batch > 1 && !skinny;
     const int total_kt = (a.K + BK - 1) / BK;
     splits = std::max(1, std::min(splits, total_kt));
     a.ktiles_per_split = (total_kt + splits - 1) / splits;
     splits = (total_kt + a.ktiles_per_split - 1) / a.ktiles_per_split;
+    if (a.batch > 1) splits = 1;
     if (splits > 1) {
         a.work = c.scratch(static_cast<std::size_t>(splits) * a.M * a.N * sizeof(double));
     }
@@ -374,6 +391,12 @@ void run_gemm(Ctx& c, bool AT, int KM, int BK, GemmArgs& a, bool va2, bool vb2, 
     if (skinny && KM == 0) {
         if (AT) dispatch_vec<kSkBM, kSkBN, true, 0, 16>(c, a, splits, va2, vb2);
         else dispatch_vec<kSkBM, kSkBN, false, 0, 16>(c, a, splits, va2, vb2);
+    } else if (small) {
+        if (KM == 0 && AT) dispatch_vec<kSmBM, kSmBN, true, 0, 16>(c, a, splits, va2, vb2);
+        else if (KM == 0) dispatch_vec<kSmBM, kSmBN, false, 0, 16>(c, a, splits, va2, vb2);
+        else if (KM == 1 && BK == 16) dispatch_vec<kSmBM, kSmBN, false, 1, 16>(c, a, splits, va2, vb2);
+        else if (KM == 1 && BK == 4) dispatch_vec<kSmBM, kSmBN, false, 1, 4>(c, a, splits, va2, vb2);
+        else dispatch_vec<kSmBM, kSmBN, false, 2, 16>(c, a, splits, va2, vb2);
     }
     else if (!AT && KM == 0) dispatch_vec<kBM, kBN, false, 0, 16>(c, a, splits, va2, vb2);
     else if (AT && KM == 0) dispatch_vec<kBM, kBN, true, 0, 16>(c, a, splits, va2, vb2);
@@ -388,8 +411,8 @@ void run_gemm(Ctx& c, bool AT, int KM, int BK, GemmArgs& a, bool va2, bool vb2, 
         TTR_CUDA(cudaGetLastError());
         c.launched();
     } else if (Ct) {
-        dim3 grid((a.M + 31) / 32, (a.N + 31) / 32);
-        transpose_copy<<<grid, dim3(32, 8), 0, c.stream>>>(C, ldc, a.M, a.N, Ct, ldct);
+        dim3 grid((a.M + 31) / 32, (a.N + 31) / 32, a.batch > 1 ? a.batch : 1);
+        transpose_copy<<<grid, dim3(32, 8), 0, c.stream>>>(C, ldc, a.M, a.N, Ct, ldct, a.sC, sCt);
         TTR_CUDA(cudaGetLastError());
         c.launched();
     }
@@ -465,6 +488,59 @@ void krp_step(Ctx& c, i64 r_left, i64 n, i64 r_right, i64 N, const double* X, co
         }
     }
     run_gemm(c, false, KM, BK, a, va2, vb2, splits, W_out, ldw, 1.0, 0.0, Wt_out, ldwt_out);
+}
+
+// Strided batches: problem b uses A + b*sA, B + b*sB, C + b*sC (no split-K).
+void gemm_batched(Ctx& c, bool trans_a, i64 M, i64 N, i64 K, double alpha, const double* A, i64 lda, i64 sA,
+                  const double* B, i64 ldb, i64 sB, double beta, double* C, i64 ldc, i64 sC, i64 batch, bool count) {
+    if (M <= 0 || N <= 0 || batch <= 0) return;
+    if (batch == 1) return gemm(c, trans_a, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, count);
+    if (count) c.charge_gemm(2ULL * static_cast<std::uint64_t>(M) * N * K * batch);
+    GemmArgs a{};
+    a.M = static_cast<int>(M);
+    a.N = static_cast<int>(N);
+    a.K = static_cast<int>(K);
+    a.A = A;
+    a.lda = lda;
+    a.B = B;
+    a.ldb = ldb;
+    a.batch = static_cast<int>(batch);
+    a.sA = sA;
+    a.sB = sB;
+    a.sC = sC;
+    const bool va2 = aligned16(A) && lda % 2 == 0 && sA % 2 == 0;
+    const bool vb2 = aligned16(B) && ldb % 2 == 0 && sB % 2 == 0;
+    run_gemm(c, trans_a, 0, 16, a, va2, vb2, 1, C, ldc, alpha, beta, nullptr, 0, M <= kSkBM);
+}
+
+void krp_step_batched(Ctx& c, i64 r_left, i64 n, i64 r_right, i64 N, const double* X, i64 sX, const double* Omega,
+                      i64 ldo, i64 sO, const double* Wt, i64 ldwt, i64 sWt, double* W_out, i64 ldw, i64 sW,
+                      double* Wt_out, i64 ldwt_out, i64 sWto, i64 batch, bool last_core) {
+    if (r_left <= 0 || N <= 0 || batch <= 0) return;
+    const std::uint64_t per = last_core ? 2ULL * r_left * n * N
+                                        : static_cast<std::uint64_t>(N) * (2ULL * r_right * r_left * n + 2ULL * r_left * r_right);
+    c.charge_gemm(per * static_cast<std::uint64_t>(batch));
+    GemmArgs a{};
+    a.M = static_cast<int>(r_left);
+    a.N = static_cast<int>(N);
+    a.K = static_cast<int>(n * r_right);
+    a.A = X;
+    a.lda = r_left;
+    a.B = Omega;
+    a.ldb = ldo;
+    a.Wt = Wt;
+    a.ldw = ldwt;
+    a.nmode = static_cast<int>(n);
+    a.batch = static_cast<int>(batch);
+    a.sA = sX;
+    a.sB = sO;
+    a.sW = sWt;
+    a.sC = sW;
+    const int KM = (n % 4 == 0) ? 1 : 2;
+    const int BK = (KM == 1 && n % 16 != 0) ? 4 : 16;
+    const bool va2 = aligned16(X) && r_left % 2 == 0 && sX % 2 == 0;
+    const bool vb2 = aligned16(Omega) && ldo % 2 == 0 && sO % 2 == 0 && aligned16(Wt) && ldwt % 2 == 0 && sWt % 2 == 0;
+    run_gemm(c, false, KM, BK, a, va2, vb2, 1, W_out, ldw, 1.0, 0.0, Wt_out, ldwt_out, false, sWto);
 }
 
 }  // namespace ttr

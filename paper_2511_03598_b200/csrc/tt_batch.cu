@@ -1,0 +1,156 @@
+// tt_batch.cu — batched fixed-rank KRP rounding of many independent,
+// identically shaped TT tensors (BASELINE config 5a: 4096 tensors, d=8, n=16,
+// formal ranks 64, l=20). One launch per step covers the whole batch: the KRP
+// sketch and every GEMM run as strided batches (grid.z = tensor), the QRs as
+// one-CTA-per-matrix shared-memory Householder QR. Tensor b is rounded exactly
+// as round_fixed_krp(Y_b, targets, derive_seed(seed, b)) in Philox mode.
+#include <algorithm>
+#include <cmath>
+
+#include "common.cuh"
+#include "rng_host.h"
+#include "tt_round.h"
+
+namespace ttr {
+
+TTBatch::TTBatch(Ctx& c, i64 batch_, const std::vector<i64>& n_, const std::vector<i64>& r_)
+    : ctx(&c), n(n_), r(r_), batch(batch_) {
+    const i64 d = static_cast<i64>(n.size());
+    if (d < 1) fail(Errc::EmptyCoreList, "TT tensor needs at least one core");
+    if (static_cast<i64>(r.size()) != d + 1) fail(Errc::InvalidRankChain, "rank chain length must be d+1");
+    if (r.front() != 1 || r.back() != 1) fail(Errc::BoundaryRankNotOne, "boundary TT ranks must be 1");
+    if (batch < 1) fail(Errc::InvalidArgument, "batch must be >= 1");
+    off.resize(d + 1);
+    i64 o = 0;
+    for (i64 k = 0; k < d; ++k) {
+        if (r[k] < 1 || n[k] < 1 || r[k + 1] < 1) fail(Errc::InvalidArgument, "core dimensions must be positive");
+        off[k] = o;
+        o += round_up(r[k] * n[k] * r[k + 1], 32);
+    }
+    off[d] = o;
+    stride = o;
+    buf = DBuf(c, static_cast<std::size_t>(stride * batch));
+}
+
+i64 TTBatch::total() const {
+    i64 t = 0;
+    for (i64 k = 0; k < d(); ++k) t += core_size(k);
+    return t;
+}
+
+// ---------------------------------------------------------------------------
+std::unique_ptr<TTBatch> batch_two_part_philox(Ctx& c, i64 batch, i64 d, i64 n, i64 rx, i64 rz, double eps,
+                                               std::uint64_t seed) {
+    std::vector<i64> modes(d, n), kx(d + 1, rx), kz(d + 1, rz), ky(d + 1, rx + rz);
+    kx.front() = kx.back() = kz.front() = kz.back() = ky.front() = ky.back() = 1;
+    auto out = std::make_unique<TTBatch>(c, batch, modes, ky);
+    for (i64 b = 0; b < batch; ++b) {
+        const std::uint64_t sb = derive_seed(seed, static_cast<std::uint64_t>(b));
+        auto x = random_philox_tt(c, modes, kx, derive_seed(sb, 1));
+        auto z = random_philox_tt(c, modes, kz, derive_seed(sb, 2));
+        scale_tt(c, *x, 1.0 / norm_exact(c, *x));
+        scale_tt(c, *z, eps / norm_exact(c, *z));
+        auto y = formal_sum(c, {x.get(), z.get()});
+        for (i64 k = 0; k < d; ++k)
+            TTR_CUDA(cudaMemcpyAsync(out->core(b, k), y->core(k), sizeof(double) * y->core_size(k),
+                                     cudaMemcpyDeviceToDevice, c.stream));
+    }
+    return out;
+}
+
+std::unique_ptr<TTDev> batch_get(Ctx& c, const TTBatch& t, i64 b) {
+    if (b < 0 || b >= t.batch) fail(Errc::IndexOutOfRange, "batch index out of range");
+    auto out = std::make_unique<TTDev>(c, t.n, t.r);
+    for (i64 k = 0; k < t.d(); ++k)
+        TTR_CUDA(cudaMemcpyAsync(out->core(k), t.core(b, k), sizeof(double) * t.core_size(k), cudaMemcpyDeviceToDevice,
+                                 c.stream));
+    return out;
+}
+
+// ---------------------------------------------------------------------------
+// round_rand.cpp:52-64 (+ rand_orth_sweep :26-44) over a strided batch
+std::unique_ptr<TTBatch> round_fixed_krp_batched(Ctx& c, const TTBatch& t, const std::vector<i64>& targets,
+                                                 std::uint64_t seed) {
+    const i64 d = t.d(), B = t.batch;
+    if (static_cast<i64>(targets.size()) != d - 1) fail(Errc::InvalidRanks, "expected d-1 target ranks");
+    for (i64 l : targets)
+        if (l < 1) fail(Errc::InvalidRanks, "target ranks must be >= 1");
+    if (d == 1) fail(Errc::InvalidArgument, "batched rounding needs d >= 2");
+    const i64 width = *std::max_element(targets.begin(), targets.end());
+    std::vector<i64> r(d + 1, 1);
+    for (i64 k = 1; k < d; ++k) r[k] = std::min({targets[k - 1], r[k - 1] * t.n[k - 1], t.r[k]});
+    auto out = std::make_unique<TTBatch>(c, B, t.n, r);
+
+    // ---- sketch: W_k for k = d..2 (Omega_k drawn per tensor from derive_seed(seed, b)) ----
+    const i64 ldwt = even_ld(width);
+    std::vector<DBuf> W(d + 2), Wt(d + 2);
+    std::vector<i64> ldw(d + 2, 0), sw(d + 2, 0), swt(d + 2, 0);
+    DBuf ones(c, static_cast<std::size_t>(ldwt));
+    fill(c, ones.p, static_cast<std::size_t>(ldwt), 1.0);
+    {
+        PhaseScope ph(c, kPhaseSketch);
+        SketchScope scope(c);
+        for (i64 k = d; k >= 2; --k) {
+            const i64 rl = t.r[k - 1], nk = t.n[k - 1], rr = t.r[k];
+            const i64 ldo = even_ld(nk), so = ldo * width;
+            DBuf om(c, static_cast<std::size_t>(so * B));
+            philox_factor_batched(c, seed, k, nk, width, om.p, ldo, so, B);
+            ldw[k] = even_ld(rl);
+            sw[k] = ldw[k] * width;
+            W[k] = DBuf(c, static_cast<std::size_t>(sw[k] * B));
+            swt[k] = ldwt * rl;
+            if (k >= 3) Wt[k] = DBuf(c, static_cast<std::size_t>(swt[k] * B));
+            const bool last = (k == d);
+            krp_step_batched(c, rl, nk, rr, width, t.core(0, k - 1), t.stride, om.p, ldo, so, last ? ones.p : Wt[k + 1].p,
+                             ldwt, last ? 0 : swt[k + 1], W[k].p, ldw[k], sw[k], k >= 3 ? Wt[k].p : nullptr, ldwt, swt[k],
+                             B, last);
+        }
+    }
+
+    // ---- left-to-right Rand-Orth sweep ----
+    i64 max_work = 0, max_s = 0;
+    for (i64 k = 1; k < d; ++k) {
+        max_work = std::max(max_work, r[k] * t.n[k] * t.r[k + 1]);
+        max_s = std::max(max_s, r[k - 1] * t.n[k - 1] * r[k]);
+    }
+    DBuf work(c, static_cast<std::size_t>(max_work * B));
+    DBuf S(c, static_cast<std::size_t>(max_s * B));
+    DBuf M(c, static_cast<std::size_t>(width * t.max_rank() * B));
+    const double* v = t.core(0, 0);
+    i64 sv = t.stride;
+    for (i64 k = 1; k < d; ++k) {
+        const i64 rows = r[k - 1] * t.n[k - 1], cols = t.r[k], l = r[k];
+        {
+            PhaseScope ph(c, kPhaseGemm);
+            gemm_batched(c, false, rows, l, cols, 1.0, v, rows, sv, W[k + 1].p, ldw[k + 1], sw[k + 1], 0.0, S.p, rows,
+                         rows * l, B);
+        }
+        {
+            PhaseScope ph(c, kPhaseQr);
+            c.charge_qr(4ULL * static_cast<std::uint64_t>(rows) * l * std::min(rows, l) * B);
+            if (rows * l <= 26000) {
+                qr_small_batched(c, rows, l, S.p, rows, rows * l, out->core(0, k - 1), rows, out->stride, nullptr, 1, 0, B);
+            } else {
+                const Counts keep = c.counts;
+                for (i64 b = 0; b < B; ++b)
+                    thin_qr(c, rows, l, S.p + b * rows * l, rows, out->core(b, k - 1), rows, nullptr, 1);
+                c.counts = keep;
+            }
+        }
+        const i64 ncols = t.n[k] * t.r[k + 1];
+        double* dst = (k == d - 1) ? out->core(0, d - 1) : work.p;
+        const i64 sdst = (k == d - 1) ? out->stride : l * ncols;
+        {
+            PhaseScope ph(c, kPhaseGemm);
+            gemm_batched(c, true, l, cols, rows, 1.0, out->core(0, k - 1), rows, out->stride, v, rows, sv, 0.0, M.p, l,
+                         l * cols, B);
+            gemm_batched(c, false, l, ncols, cols, 1.0, M.p, l, l * cols, t.core(0, k), cols, t.stride, 0.0, dst, l, sdst,
+                         B);
+        }
+        v = dst;
+        sv = sdst;
+    }
+    return out;
+}
+
+}  // namespace ttr

@@ -2,6 +2,7 @@
 // (host orchestration in tt_round.cu / tt_det.cu).
 #pragma once
 
+#include <algorithm>
 #include <memory>
 #include <vector>
 
@@ -25,6 +26,25 @@ struct TTDev {
     void upload(const double* host);
     void download(double* host) const;
 };
+
+// Batch of identically shaped TT tensors: tensor b occupies
+// [b*stride, (b+1)*stride) of one allocation, cores laid out as in TTDev.
+struct TTBatch {
+    Ctx* ctx;
+    std::vector<i64> n, r, off;
+    i64 stride = 0, batch = 0;
+    DBuf buf;
+    TTBatch(Ctx& c, i64 batch, const std::vector<i64>& n, const std::vector<i64>& r);
+    i64 d() const { return static_cast<i64>(n.size()); }
+    double* core(i64 b, i64 k) const { return buf.p + b * stride + off[k]; }
+    i64 core_size(i64 k) const { return r[k] * n[k] * r[k + 1]; }
+    i64 total() const;
+    i64 max_rank() const { return *std::max_element(r.begin(), r.end()); }
+};
+std::unique_ptr<TTBatch> batch_two_part_philox(Ctx& c, i64 batch, i64 d, i64 n, i64 rx, i64 rz, double eps,
+                                               std::uint64_t seed);
+std::unique_ptr<TTBatch> round_fixed_krp_batched(Ctx& c, const TTBatch& t, const std::vector<i64>& targets,
+                                                 std::uint64_t seed);
 
 struct AdaptiveCfg {
     double tolerance = 1e-6, f_init = 0.1, f_inc = 0.05;
@@ -83,6 +103,9 @@ struct ttr_tt {
 };
 struct ttr_ctx {
     ttr::Ctx c;
+};
+struct ttr_batch {
+    std::unique_ptr<ttr::TTBatch> t;
 };
 struct ttr_plan {
     std::unique_ptr<ttr::Plan> plan;

@@ -232,3 +232,34 @@ def test_estimate_norm_matches_oracle(P, O):
         ref = O.estimate_norm_krp(x, 64, 7000, rng=rng_mode)
         got = P.estimate_norm_krp(to_device(x), 64, 7000, rng=rng_mode)
         assert abs(got - ref) <= 1e-12 * ref
+
+
+# ---- batched rounding (config 5a) ------------------------------------------------------------
+
+def test_batched_fixed_krp_config5a_parity(P, O):
+    """Config 5a shapes (d=8, n=16, rank 16 + 1e-6 rank 48, l=20): tensor b of the batch equals
+    round_fixed_krp(Y_b, {20}x7, derive_seed(7, b)) of the oracle."""
+    B = 24
+    xs = [O.two_part_tt(8, 16, 16, 48, 1e-6, O.derive_seed(1005, b)) for b in range(B)]
+    n, r, _ = xs[0].shape()
+    batch = P.TTBatch.from_flats(n, r, [x.flat() for x in xs])
+    out = P.round_fixed_krp_batched(batch, [20] * 7, 7)
+    _, on, orr, _ = out.shape()
+    assert orr == [1, 16, 20, 20, 20, 20, 20, 20, 1]
+    flats = out.flats()
+    for b in (0, 5, B - 1):
+        y_ref = O.round_fixed_krp(xs[b], [20] * 7, O.derive_seed(7, b), rng=O.PHILOX)
+        assert y_ref.ranks == orr
+        y_gpu = O.TT.from_flat(len(on), on, orr, flats[b])
+        assert O.relative_error(y_ref, y_gpu) <= 1e-10
+
+
+def test_batched_equals_single(P, O):
+    xs = [O.two_part_tt(5, 20, 6, 10, 1e-4, 40 + b) for b in range(3)]
+    n, r, _ = xs[0].shape()
+    outb = P.round_fixed_krp_batched(P.TTBatch.from_flats(n, r, [x.flat() for x in xs]), [8] * 4, 11)
+    for b, x in enumerate(xs):
+        single = P.round_fixed_krp(to_device(x), [8] * 4, O.derive_seed(11, b))
+        _, on, orr, _ = outb.shape()
+        yb = O.TT.from_flat(len(on), on, orr, outb.flats(b, 1)[0])
+        assert O.relative_error(to_oracle(single), yb) <= 1e-12
