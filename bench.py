@@ -54,7 +54,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="5b", choices=["5b", "3"])
+    ap.add_argument("--config", default="5b", choices=["5b", "3", "5a"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     return ap.parse_args()
@@ -335,11 +335,78 @@ def total_bytes(y):
     return 8 * y.shape()[2]
 
 
+def run_5a(args, world, rank, local):
+    """Config 5a: 4096 independent tensors (d=8, n=16, rank 16 + 1e-6 rank 48 -> 64, l=20), the
+    batch split across ranks (strong scaling, no collective); one step rounds the whole batch."""
+    import torch
+    import paper_2511_03598_b200 as P
+    from paper_2511_03598_b200.seeds import derive_seed
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    torch.cuda.set_device(local)
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    ctx = P.Context(local, stream.cuda_stream)
+    total_batch = 4096
+    nb = total_batch // world + (1 if rank < total_batch % world else 0)
+    batch = P.TTBatch.two_part_philox(nb, 8, 16, 16, 48, 1e-6, derive_seed(1005, 1000 + rank), ctx)
+    ranks = [20] * 7
+    ctx.reset_counters()
+    o = P.round_fixed_krp_batched(batch, ranks, 7)
+    torch.cuda.synchronize()
+    flops = ctx.counters().total()
+    out_ranks = o.shape()[2]
+    del o
+    for _ in range(args.warmup):
+        o = P.round_fixed_krp_batched(batch, ranks, 7)
+        del o
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    l0 = ctx.kernel_launches()
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            o = P.round_fixed_krp_batched(batch, ranks, 7)
+            del o
+        e1.record(stream)
+        torch.cuda.synchronize()
+    launches = ctx.kernel_launches() - l0
+    ms = e0.elapsed_time(e1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    flops_all = flops * world  # per-rank work is (near) equal
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": flops_all / (ms * 1e-3) / 1e12, "unit": "TFLOP/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (device Philox Gaussian cores)",
+            "config": {"workload": "config 5a: 4096 x round_fixed_krp(Y_b, {20}x7, derive_seed(7,b)), batched",
+                       "batch_per_rank": nb, "output_ranks": out_ranks, "flops_per_step_per_rank": flops,
+                       "bytes_per_step": 8 * 4096 * batch.shape()[3],
+                       "l2": "inputs exceed L2 (12.9 GB)"},
+            "hbm_gbs_achieved": 8 * 4096 * batch.shape()[3] / (ms * 1e-3) / 1e9,
+            "clocks": clk.summary(), "gpu_launches": launches,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
 def main():
     args = parse()
     world, rank, local = dist_env()
     if args.impl == "reference":
         run_reference(args, world, rank)
+        return
+    if args.config == "5a":
+        run_5a(args, world, rank, local)
         return
     run_ours(args, world, rank, local)
 
