@@ -205,6 +205,27 @@ class TTTensor:
         return TTTensor._new(ctx, lib().ttr_tt_random_philox, ctx._h, C.c_int64(len(mode_sizes)), _i64(mode_sizes),
                              _i64(ranks), C.c_uint64(seed))
 
+    @staticmethod
+    def kernel_sum(d, n, r, terms, ell, seed, ctx: Optional[Context] = None) -> "TTTensor":
+        """BASELINE config 4 input (smooth exp(-|t - c_ab|/ell) cores, weights 2^-t), built on the device."""
+        ctx = ctx or default_context()
+        return TTTensor._new(ctx, lib().ttr_tt_kernel_sum, ctx._h, C.c_int64(d), C.c_int64(n), C.c_int64(r),
+                             C.c_int64(terms), C.c_double(ell), C.c_uint64(seed))
+
+    @staticmethod
+    def two_part_philox(d, n, rx, rz, eps, seed, ctx: Optional[Context] = None) -> "TTTensor":
+        """X/||X|| + eps Z/||Z|| with Gaussian X (ranks rx) and Z (ranks rz) drawn on the device
+        from derive_seed(seed, 1) and derive_seed(seed, 2) (BASELINE configs 1, 2, 3, 5b)."""
+        from .seeds import derive_seed
+        ctx = ctx or default_context()
+        kx = [1] + [rx] * (d - 1) + [1]
+        kz = [1] + [rz] * (d - 1) + [1]
+        x = TTTensor.random_philox([n] * d, kx, derive_seed(seed, 1), ctx)
+        z = TTTensor.random_philox([n] * d, kz, derive_seed(seed, 2), ctx)
+        x = scaled(x, 1.0 / norm_exact(x))
+        z = scaled(z, eps / norm_exact(z))
+        return formal_sum([x, z])
+
     # -- shape / data ---------------------------------------------------
     def shape(self):
         d = C.c_int64()

@@ -196,6 +196,15 @@ ttr_status ttr_tt_random_philox(ttr_ctx* ctx, int64_t d, const int64_t* n, const
     });
 }
 
+ttr_status ttr_tt_kernel_sum(ttr_ctx* ctx, int64_t d, int64_t n, int64_t r, int64_t terms, double ell, uint64_t seed,
+                             ttr_tt** out) {
+    return guard([&] {
+        need(ctx && out, "null argument");
+        need(d >= 1 && n >= 1 && r >= 1 && terms >= 1 && ell > 0.0, "bad kernel-sum parameters");
+        *out = wrap(kernel_sum_tt(ctx->c, d, n, r, terms, ell, seed));
+    });
+}
+
 ttr_status ttr_tt_formal_sum(ttr_ctx* ctx, const ttr_tt* const* terms, int count, ttr_tt** out) {
     return guard([&] {
         need(ctx && out, "null argument");

@@ -168,6 +168,8 @@ double frob_norm(Ctx& c, i64 rows, i64 cols, const double* a, i64 lda);
 void random_normal(Ctx& c, std::uint64_t seed, std::uint32_t stream_tag, double* out, std::size_t count, double sigma);
 // out[row_off + i, j, col_off + g] = src(i, j, g) (formal-sum block placement)
 void place_block(Ctx& c, const double* src, i64 rl, i64 n, i64 rr, double* dst, i64 RL, i64 RR, i64 row_off, i64 col_off);
+// core(a, j, b) = exp(-|j/(n-1) - cab[a + b*rl]| / ell) (config-4 smooth cores)
+void exp_core(Ctx& c, const double* cab, i64 rl, i64 n, i64 rr, double ell, double* out);
 // columns j of V-unfolding from H (k-th slab etc.)
 void scale_rows_cols(Ctx& c, double* a, i64 rows, i64 cols, i64 lda, const double* row_scale, const double* col_scale);
 

@@ -155,6 +155,18 @@ __global__ void sum_partials(const double* partial, int n, double* out) {
     if (threadIdx.x == 0) out[0] = red[0];
 }
 
+// core(a, j, b) = exp(-|t_j - c[a + b*rl]| / ell), t_j = j / (n - 1)
+__global__ void exp_core_kernel(const double* __restrict__ cab, int rl, int n, int rr, double ell, double* out) {
+    const i64 total = static_cast<i64>(rl) * n * rr;
+    for (i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; i < total; i += static_cast<i64>(gridDim.x) * blockDim.x) {
+        const int a = static_cast<int>(i % rl);
+        const i64 rest = i / rl;
+        const int j = static_cast<int>(rest % n), b = static_cast<int>(rest / n);
+        const double tj = n > 1 ? static_cast<double>(j) / static_cast<double>(n - 1) : 0.0;
+        out[i] = exp(-fabs(tj - cab[a + static_cast<i64>(b) * rl]) / ell);
+    }
+}
+
 __global__ void place_block_kernel(const double* __restrict__ src, int rl, int n, int rr, double* dst, i64 RL, i64 RR,
                                    i64 row_off, i64 col_off) {
     const i64 total = static_cast<i64>(rl) * n * rr;
@@ -274,6 +286,15 @@ void place_block(Ctx& c, const double* src, i64 rl, i64 n, i64 rr, double* dst, 
     if (!total) return;
     place_block_kernel<<<grid_for(c, total), kThreads, 0, c.stream>>>(src, static_cast<int>(rl), static_cast<int>(n),
                                                                       static_cast<int>(rr), dst, RL, RR, row_off, col_off);
+    TTR_CUDA(cudaGetLastError());
+    c.launched();
+}
+
+void exp_core(Ctx& c, const double* cab, i64 rl, i64 n, i64 rr, double ell, double* out) {
+    const std::size_t total = static_cast<std::size_t>(rl * n * rr);
+    if (!total) return;
+    exp_core_kernel<<<grid_for(c, total), kThreads, 0, c.stream>>>(cab, static_cast<int>(rl), static_cast<int>(n),
+                                                                   static_cast<int>(rr), ell, out);
     TTR_CUDA(cudaGetLastError());
     c.launched();
 }

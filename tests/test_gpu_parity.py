@@ -263,3 +263,21 @@ def test_batched_equals_single(P, O):
         _, on, orr, _ = outb.shape()
         yb = O.TT.from_flat(len(on), on, orr, outb.flats(b, 1)[0])
         assert O.relative_error(to_oracle(single), yb) <= 1e-12
+
+
+def test_device_kernel_sum_input_matches_oracle(P, O):
+    """The device generator of the config-4 input equals the oracle's (exp differs by <= ulps)."""
+    dev = P.TTTensor.kernel_sum(3, 16, 4, 3, 0.3, 1004)
+    ref = O.kernel_sum_tt(3, 16, 4, 3, 0.3, 1004)
+    assert dev.ranks() == ref.ranks
+    a, b = dev.flat(), ref.flat()
+    assert np.max(np.abs(a - b)) <= 1e-15 * np.max(np.abs(b))
+
+
+def test_adaptive_config4_small_parity(P, O):
+    """Config 4 structure at reduced size (d=5, n=32, 6 terms of rank 5): identical ranks."""
+    x = O.kernel_sum_tt(5, 32, 5, 6, 0.3, 1004)
+    y_ref = O.round_adaptive_krp(x, tolerance=1e-6, f_init=0.1, f_inc=0.04, seed=7, rng=O.PHILOX)
+    y_gpu = P.round_adaptive_krp(to_device(x), P.AdaptiveConfig(tolerance=1e-6, f_init=0.1, f_inc=0.04, seed=7))
+    assert y_gpu.ranks() == y_ref.ranks
+    assert rel_err_vs_ref(y_ref, y_gpu) <= 1e-10
