@@ -57,6 +57,9 @@ def parse():
     ap.add_argument("--config", default="5b", choices=["5b", "3", "5a"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--sharding", default="tensors", choices=["tensors", "columns"],
+                    help="N>1 on config 5b: independent tensor per rank (weak) or one tensor with "
+                         "column-sharded KRP sketch + NCCL all-gather (strong)")
     return ap.parse_args()
 
 
@@ -335,6 +338,73 @@ def total_bytes(y):
     return 8 * y.shape()[2]
 
 
+def run_columns(args, world, rank, local):
+    """Config 5b, ONE tensor over N GPUs: column-sharded KRP sketch, NCCL all-gather of the W
+    slices, Rand-Orth sweep (replicated). Strong scaling; time = max over ranks."""
+    import torch
+    import paper_2511_03598_b200 as P
+    from paper_2511_03598_b200.distributed import round_fixed_krp_column_sharded
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    torch.cuda.set_device(local)
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    ctx = P.Context(local, stream.cuda_stream)
+    cfg = dict(CFG5B)
+    y = build_input(P, ctx, cfg)  # identical replica on every rank
+    ranks = [cfg["ell"]] * (cfg["d"] - 1)
+    ctx.reset_counters()
+    out, info = round_fixed_krp_column_sharded(y, ranks, 7)
+    torch.cuda.synchronize()
+    cnt = ctx.counters()
+    flops_rank = cnt.total()
+    # algorithmic work of the job: every rank's sketch slice + ONE sweep (the replicas are redundant)
+    sk = torch.tensor([float(cnt.sketch)], device="cuda", dtype=torch.float64)
+    if world > 1:
+        torch.distributed.all_reduce(sk)
+    flops_job = float(sk.item()) + (cnt.total() - cnt.sketch)
+    out_ranks = out.ranks()
+    del out
+    for _ in range(args.warmup):
+        o, _ = round_fixed_krp_column_sharded(y, ranks, 7)
+        del o
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    l0 = ctx.kernel_launches()
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            o, _ = round_fixed_krp_column_sharded(y, ranks, 7)
+            del o
+        e1.record(stream)
+        torch.cuda.synchronize()
+    launches = ctx.kernel_launches() - l0
+    ms = e0.elapsed_time(e1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": flops_job / (ms * 1e-3) / 1e12, "unit": "TFLOP/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (device Philox Gaussian cores)",
+            "config": {"workload": "config 5b, one tensor: column-sharded KRP sketch + NCCL all-gather + "
+                                   "replicated Rand-Orth sweep",
+                       "column_bounds": info["bounds"], "output_ranks": out_ranks,
+                       "flops_per_rank": flops_rank, "l2": "inputs exceed L2"},
+            "clocks": clk.summary(), "gpu_launches": launches,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
 def run_5a(args, world, rank, local):
     """Config 5a: 4096 independent tensors (d=8, n=16, rank 16 + 1e-6 rank 48 -> 64, l=20), the
     batch split across ranks (strong scaling, no collective); one step rounds the whole batch."""
@@ -407,6 +477,9 @@ def main():
         return
     if args.config == "5a":
         run_5a(args, world, rank, local)
+        return
+    if args.sharding == "columns":
+        run_columns(args, world, rank, local)
         return
     run_ours(args, world, rank, local)
 

@@ -187,6 +187,20 @@ ttr_status ttr_gemm(ttr_ctx* ctx, int trans_a, int64_t m, int64_t n, int64_t k, 
 ttr_status ttr_ctx_enable_timing(ttr_ctx* ctx, int on);
 ttr_status ttr_ctx_phase_times(ttr_ctx* ctx, double* ms_out /*4*/, uint64_t* count_out /*4*/);
 
+/* ---- column-sharded sketch (multi-GPU config 5b) --------------------------
+ * ttr_krp_sketch_into writes columns [col0, col0+ncols) of the partial
+ * contractions W_2..W_d (Philox factors for those GLOBAL columns) into
+ * caller-owned device buffers W_dev[k-2] (r_{k-1} x width, leading dim
+ * ldw[k-2]); slices are bitwise equal to the matching columns of a one-shot
+ * contraction, so ranks can each compute a slice and all-gather them.
+ * ttr_round_fixed_krp_from_sketch then runs the left-to-right Rand-Orth sweep
+ * (round_rand.cpp:26-44) from the gathered W. */
+ttr_status ttr_krp_sketch_into(ttr_ctx* ctx, const ttr_tt* tt, int64_t col0, int64_t ncols, uint64_t seed,
+                               double* const* W_dev, const int64_t* ldw);
+ttr_status ttr_round_fixed_krp_from_sketch(ttr_ctx* ctx, const ttr_tt* tt, const int64_t* target_ranks,
+                                           int64_t count, const double* const* W_dev, const int64_t* ldw,
+                                           int64_t width, ttr_tt** out);
+
 /* ---- batches of independent, identically shaped tensors (config 5a) ------
  * Tensor b of a batch is rounded exactly as
  *   round_fixed_krp(Y_b, target_ranks, derive_seed(seed, b))   (Philox mode)

@@ -433,6 +433,45 @@ ttr_status ttr_ctx_phase_times(ttr_ctx* ctx, double* ms_out, uint64_t* count_out
     });
 }
 
+// ---- column-sharded sketch (multi-GPU config 5b) ----
+ttr_status ttr_krp_sketch_into(ttr_ctx* ctx, const ttr_tt* tt, int64_t col0, int64_t ncols, uint64_t seed,
+                               double* const* W_dev, const int64_t* ldw) {
+    return guard([&] {
+        check_same_ctx(ctx, tt);
+        need(W_dev && ldw, "null argument");
+        const i64 d = tt->t->d();
+        std::vector<double*> W(d + 2, nullptr);
+        std::vector<i64> ld(d + 2, 0);
+        for (i64 k = 2; k <= d; ++k) {
+            W[k] = W_dev[k - 2];
+            ld[k] = ldw[k - 2];
+            need(W[k] && ld[k] >= tt->t->r[k - 1], "bad W buffer");
+        }
+        krp_sketch_into(ctx->c, *tt->t, col0, ncols, seed, W, ld);
+    });
+}
+
+ttr_status ttr_round_fixed_krp_from_sketch(ttr_ctx* ctx, const ttr_tt* tt, const int64_t* ranks, int64_t count,
+                                           const double* const* W_dev, const int64_t* ldw, int64_t width, ttr_tt** out) {
+    return guard([&] {
+        check_same_ctx(ctx, tt);
+        need(out && W_dev && ldw, "null argument");
+        if (count < 0 || (count > 0 && !ranks)) fail(Errc::InvalidRanks, "expected d-1 target ranks");
+        auto r = fixed_krp_ranks(*tt->t, vec(ranks, count));
+        const i64 d = tt->t->d();
+        for (i64 k = 1; k < d; ++k) need(r[k] <= width, "sketch narrower than the target ranks");
+        std::vector<const double*> W(d + 2, nullptr);
+        std::vector<i64> ld(d + 2, 0);
+        for (i64 k = 2; k <= d; ++k) {
+            W[k] = W_dev[k - 2];
+            ld[k] = ldw[k - 2];
+        }
+        auto o = std::make_unique<TTDev>(ctx->c, tt->t->n, r);
+        rand_orth_sweep(ctx->c, *tt->t, width, W, ld, *o);
+        *out = wrap(std::move(o));
+    });
+}
+
 // ---- batches of independent tensors (config 5a) ----
 ttr_status ttr_batch_upload(ttr_ctx* ctx, int64_t batch, int64_t d, const int64_t* n, const int64_t* r,
                             const double* host, ttr_batch** out) {

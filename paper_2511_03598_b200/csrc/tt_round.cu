@@ -347,6 +347,33 @@ void krp_partial_contractions(Ctx& c, const TTDev& t, i64 start, i64 cols, const
     TTR_CUDA(cudaStreamSynchronize(c.stream));
 }
 
+// Columns [col0, col0 + ncols) of the partial contractions W_2..W_d written
+// into caller-owned device buffers W[k] (r_{k-1} x total width, leading dim
+// ldw[k]): the unit of work one GPU does in the column-sharded sketch. Philox
+// draws are keyed by the global column and the split-K count of the contraction
+// does not depend on the column count, so slices computed on different GPUs
+// are bitwise equal to the corresponding columns of a one-shot contraction.
+void krp_sketch_into(Ctx& c, const TTDev& t, i64 col0, i64 ncols, std::uint64_t seed,
+                     const std::vector<double*>& W, const std::vector<i64>& ldw) {
+    const i64 d = t.d();
+    if (d < 2) fail(Errc::InvalidArgument, "sketch needs d >= 2");
+    if (ncols < 1 || col0 < 0) fail(Errc::InvalidArgument, "bad column range");
+    const i64 ldwt = even_ld(ncols);
+    std::vector<DBuf> Wt(d + 2);
+    DBuf ones(c, static_cast<std::size_t>(ldwt));
+    fill(c, ones.p, static_cast<std::size_t>(ldwt), 1.0);
+    SketchScope scope(c);
+    for (i64 k = d; k >= 2; --k) {
+        const i64 rl = t.r[k - 1], nk = t.n[k - 1], rr = t.r[k];
+        const i64 ldo = even_ld(nk);
+        DBuf om(c, static_cast<std::size_t>(ldo * ncols));
+        philox_factor(c, seed, k, nk, ncols, col0, om.p, ldo);
+        if (k >= 3) Wt[k] = DBuf(c, static_cast<std::size_t>(ldwt * rl));
+        krp_step(c, rl, nk, rr, ncols, t.core(k - 1), om.p, ldo, k == d ? ones.p : Wt[k + 1].p, ldwt,
+                 W[k] + col0 * ldw[k], ldw[k], k >= 3 ? Wt[k].p : nullptr, ldwt, k == d);
+    }
+}
+
 // ---------------------------------------------------------------------------
 // Fixed-rank KRP rounding — round_rand.cpp:52-64 with rand_orth_sweep :26-44
 static std::vector<i64> checked_targets(const TTDev& t, const std::vector<i64>& targets) {  // round_rand.cpp:14-20
@@ -387,6 +414,21 @@ void round_fixed_krp_into(Ctx& c, const TTDev& t, const std::vector<i64>& target
         PhaseScope ph(c, kPhaseSketch);
         sk.append(2, width);
     }
+    std::vector<const double*> W(d + 2, nullptr);
+    std::vector<i64> ldw(d + 2, 0);
+    for (i64 k = 2; k <= d; ++k) {
+        W[k] = sk.W[k].p;
+        ldw[k] = sk.ldw[k];
+    }
+    rand_orth_sweep(c, t, width, W, ldw, out_tt);
+}
+
+// rand_orth_sweep (round_rand.cpp:26-44) given the partial contractions
+// W[k] (r_{k-1} x width, leading dim ldw[k], k = 2..d) and an output tensor
+// whose ranks are the l_eff caps.
+void rand_orth_sweep(Ctx& c, const TTDev& t, i64 width, const std::vector<const double*>& Wk,
+                     const std::vector<i64>& ldwk, TTDev& out_tt) {
+    const i64 d = t.d();
     const std::vector<i64>& r = out_tt.r;
     TTDev* out = &out_tt;
 
@@ -406,7 +448,7 @@ void round_fixed_krp_into(Ctx& c, const TTDev& t, const std::vector<i64>& target
         // S = V(Y_k) W_{k+1}(:, 1:l)
         {
             PhaseScope ph(c, kPhaseGemm);
-            gemm(c, false, rows, l, cols, 1.0, v, rows, sk.W[k + 1].p, sk.ldw[k + 1], 0.0, S.p, rows);
+            gemm(c, false, rows, l, cols, 1.0, v, rows, Wk[k + 1], ldwk[k + 1], 0.0, S.p, rows);
         }
         // Q = thin_qr_q(S) -> output core k
         {

@@ -69,6 +69,10 @@ std::unique_ptr<TTDev> round_fixed_krp(Ctx& c, const TTDev& t, const std::vector
 std::vector<i64> fixed_krp_ranks(const TTDev& t, const std::vector<i64>& target_ranks);
 void round_fixed_krp_into(Ctx& c, const TTDev& t, const std::vector<i64>& target_ranks, std::uint64_t seed,
                           int rng_mode, TTDev& out);
+void rand_orth_sweep(Ctx& c, const TTDev& t, i64 width, const std::vector<const double*>& W,
+                     const std::vector<i64>& ldw, TTDev& out);
+void krp_sketch_into(Ctx& c, const TTDev& t, i64 col0, i64 ncols, std::uint64_t seed, const std::vector<double*>& W,
+                     const std::vector<i64>& ldw);
 
 // Captured CUDA graph of round_fixed_krp for a fixed input buffer (contents
 // may change between executions) writing into an owned output tensor.
