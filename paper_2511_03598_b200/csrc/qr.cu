@@ -11,19 +11,21 @@
 //  * qr_small_kernel — the whole m x n matrix lives in one CTA's shared
 //    memory (m*n <= ~26k doubles); factor + in-place dorg2r-style backward
 //    accumulation of Q; warp-shuffle column reductions. Batched over a
-//    strided set of matrices (one CTA each), which covers the 5a batch and
-//    every mode of the small configs.
+//    strided set of matrices (one CTA each) for the 5a batch.
 //  * blocked right-looking Householder for tall matrices: panels of width
-//    kPanel factored by ONE cooperative kernel (each CTA keeps its row block
-//    of the panel in shared memory, one grid-wide barrier per column, partial
-//    dot products reduced in fixed CTA order -> deterministic), then the
-//    compact-WY trailing update and the explicit-Q backward accumulation run
-//    on the DMMA GEMM (gemm_dmma.cu).
+//    kPanel factored by panel_col_kernel (qr_panel.cuh: lane = column, warp =
+//    row block, registers only; CTAs combined through one thread-block
+//    cluster's distributed shared memory or a cooperative grid barrier, sums
+//    in fixed order -> deterministic), which also emits V and the compact-WY
+//    T; the trailing update and the explicit-Q backward accumulation run on
+//    the DMMA GEMM (gemm_dmma.cu). <= 32 columns: one launch yields Q and R.
+//    Very tall R-only requests (norm_exact) take a TSQR split first.
 #include <cooperative_groups.h>
 
 #include <algorithm>
 #include <cfloat>
 #include <cmath>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -152,21 +154,9 @@ __global__ void __launch_bounds__(kQrThreads) qr_small_kernel(int m, int n, cons
 }
 
 // ---------------------------------------------------------------------------
-// Register-resident Householder panel (b <= 32 columns). Every thread keeps
-// R rows x 32 columns of the panel in registers, so a column step touches no
-// shared memory except the reductions: per-column dot products are formed in
-// registers, reduced across the warp with a 31-shuffle transpose-reduce
-// (lane l ends up holding column l), across warps through an 8x32 shared
-// tile, and across CTAs either through distributed shared memory inside ONE
-// thread-block cluster (CL = true: <= 16 CTAs, cluster barriers ~0.24 us) or
-// through global memory and a grid barrier (CL = false: cooperative launch,
-// up to one CTA per SM, ~1.2 us). Every reduction runs in a fixed order, so
-// the factorization is deterministic. Optional outputs: the factored panel
-// (reflector tails + R), R, the explicit unit-lower V, the compact-WY T
-// (cluster mode) and — when the panel is the whole matrix — the explicit thin
-// Q (in-register dorg2r backward accumulation).
-constexpr int kRegThreads = 256;
-
+// Arguments of the Householder panel kernel (qr_panel.cuh). Optional outputs:
+// the factored panel (reflector tails + R), R, the explicit unit-lower V, the
+// compact-WY T and — when the panel is the whole matrix — the explicit thin Q.
 struct RegQrArgs {
     int rows, b, rpc;
     const double* Pin;
@@ -185,281 +175,76 @@ struct RegQrArgs {
     double* diag;      // grid mode: [2][32]
 };
 
-// lane l returns the warp sum of a[l] (a is destroyed); 31 shuffles.
-__device__ __forceinline__ double transpose_reduce32(double (&a)[32]) {
-    const int lane = threadIdx.x & 31;
-#pragma unroll
-    for (int s = 16; s >= 1; s >>= 1) {
-        const bool up = (lane & s) != 0;
-#pragma unroll
-        for (int k = 0; k < s; ++k) {
-            const double send = up ? a[k] : a[k + s];
-            const double keep = up ? a[k + s] : a[k];
-            a[k] = keep + __shfl_xor_sync(0xffffffffu, send, s);
-        }
-    }
-    return a[0];
-}
+#include "qr_panel.cuh"
 
-// register-array element i for a runtime i (keeps the array in registers)
-__device__ __forceinline__ double reg_pick(const double (&row)[32], int i) {
-    double v = 0.0;
-#pragma unroll
-    for (int l = 0; l < 32; ++l) v = (l == i) ? row[l] : v;
-    return v;
-}
-__device__ __forceinline__ void reg_set(double (&row)[32], int i, double v) {
-#pragma unroll
-    for (int l = 0; l < 32; ++l) row[l] = (l == i) ? v : row[l];
-}
-
-// this CTA's sums of x(r,i) * x(r,l) over its rows r with global index > i
-// (column l in lane l of threads 0..31); wsum is an 8x32 scratch tile.
-template <int R>
-__device__ __forceinline__ double reg_col_dots(const double (&x)[R][32], const int i, int r0, int nr, double* wsum) {
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    double a[32];
-#pragma unroll
-    for (int l = 0; l < 32; ++l) a[l] = 0.0;
-#pragma unroll
-    for (int j = 0; j < R; ++j) {
-        const int rr = tid + j * kRegThreads;
-        const double xi = (rr < nr && r0 + rr > i) ? reg_pick(x[j], i) : 0.0;
-#pragma unroll
-        for (int l = 0; l < 32; ++l) a[l] = fma(xi, x[j][l], a[l]);
-    }
-    wsum[warp * 32 + lane] = transpose_reduce32(a);
-    __syncthreads();
-    double s = 0.0;
-    if (tid < 32) {
-#pragma unroll
-        for (int w = 0; w < 8; ++w) s += wsum[w * 32 + tid];
-    }
-    __syncthreads();
-    return s;
-}
-
-// the thread holding local row orr copies its 32 values to dst
-template <int R>
-__device__ __forceinline__ void reg_publish_row(const double (&x)[R][32], int orr, int nr, double* dst) {
-    if (orr < 0 || orr >= nr || threadIdx.x != (orr % kRegThreads)) return;
-    const int jo = orr / kRegThreads;
-#pragma unroll
-    for (int j = 0; j < R; ++j)
-        if (j == jo)
-#pragma unroll
-            for (int l = 0; l < 32; ++l) dst[l] = x[j][l];
-}
-
-template <int R, bool CL>
-__global__ void __launch_bounds__(kRegThreads, 1) panel_reg_kernel(RegQrArgs p) {
-    __shared__ double wsum[8 * 32];
-    __shared__ double part_s[2 * 32];
-    __shared__ double dg_s[2 * 32];
-    __shared__ double red[32], wv[32], ts[32], dgv[32], sc[4], gcol[32];
-    __shared__ double tb[32 * 32];  // compact-WY T, built column by column
-    for (int e = threadIdx.x; e < 32 * 32; e += blockDim.x) tb[e] = 0.0;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    int rank, G;
+template <int RPT, int WARPS, bool CL>
+void launch_col(Ctx& c, const RegQrArgs& a, i64 grid) {
+    auto kern = panel_col_kernel<RPT, WARPS, CL>;
     if constexpr (CL) {
-        cg::cluster_group cl = cg::this_cluster();
-        rank = static_cast<int>(cl.block_rank());
-        G = static_cast<int>(cl.num_blocks());
+        static bool configured = false;
+        if (!configured) {
+            TTR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+            configured = true;
+        }
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(static_cast<unsigned>(grid));
+        cfg.blockDim = dim3(WARPS * 32);
+        cfg.dynamicSmemBytes = 0;
+        cfg.stream = c.stream;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = static_cast<unsigned>(grid);
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        TTR_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
     } else {
-        rank = blockIdx.x;
-        G = gridDim.x;
+        RegQrArgs copy = a;
+        void* args[] = {&copy};
+        TTR_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(kern), dim3(static_cast<unsigned>(grid)),
+                                             dim3(WARPS * 32), args, 0, c.stream));
     }
-    const int b = p.b, rpc = p.rpc;
-    const int r0 = rank * rpc, nr = max(0, min(p.rows, r0 + rpc) - r0);
-    const int kk = min(b, p.rows);
-    int xc = 0;  // exchange counter: double-buffer parity
+    c.launched();
+}
 
-    double x[R][32];
-#pragma unroll
-    for (int j = 0; j < R; ++j) {
-        const int rr = tid + j * kRegThreads;
-#pragma unroll
-        for (int l = 0; l < 32; ++l)
-            x[j][l] = (rr < nr && l < b) ? p.Pin[(r0 + rr) + static_cast<i64>(l) * p.ldin] : 0.0;
-    }
-
-    // Cross-CTA: red[l] = sum over CTAs of `mine` (column tid, valid in tid < 32)
-    // in fixed CTA order; dgv[l] = row `orow` of the panel (from its owner).
-    // (the owner of row `orow` has already published it with reg_publish_row
-    // into row_slot(): dg_s[buf] in cluster mode, p.diag[buf] in grid mode)
-    auto row_slot = [&]() { return CL ? dg_s + (xc & 1) * 32 : p.diag + (xc & 1) * 32; };
-    auto exchange = [&](double mine, int orow) {
-        const int buf = xc & 1;
-        ++xc;
-        if constexpr (CL) {
-            cg::cluster_group cl = cg::this_cluster();
-            if (tid < 32) part_s[buf * 32 + tid] = mine;
-            cl.sync();
-            const int g = tid >> 5;
-            const double a0 = (g < G) ? cl.map_shared_rank(part_s, g)[buf * 32 + lane] : 0.0;
-            const double a1 = (g + 8 < G) ? cl.map_shared_rank(part_s, g + 8)[buf * 32 + lane] : 0.0;
-            wsum[g * 32 + lane] = a0 + a1;
-            if (g == 0) dgv[lane] = cl.map_shared_rank(dg_s, orow / rpc)[buf * 32 + lane];
-        } else {
-            cg::grid_group gg = cg::this_grid();
-            double* part = p.partials + static_cast<i64>(buf) * G * 32;
-            if (tid < 32) part[rank * 32 + tid] = mine;
-            gg.sync();
-            constexpr int kMaxLoads = 20;  // G <= 160
-            const int g = tid >> 5;
-            double v[kMaxLoads];
-#pragma unroll
-            for (int q = 0; q < kMaxLoads; ++q) {
-                const int c = g + 8 * q;
-                v[q] = (c < G) ? __ldcg(part + c * 32 + lane) : 0.0;
-            }
-            double s = 0.0;
-#pragma unroll
-            for (int q = 0; q < kMaxLoads; ++q) s += v[q];
-            wsum[g * 32 + lane] = s;
-            if (g == 0) dgv[lane] = __ldcg(p.diag + buf * 32 + lane);
-        }
-        __syncthreads();
-        if (tid < 32) {
-            double s = 0.0;
-#pragma unroll
-            for (int w = 0; w < 8; ++w) s += wsum[w * 32 + tid];
-            red[tid] = s;
-        }
-        __syncthreads();
+// Geometry + template dispatch for panel_col_kernel. a.partials/a.diag must be set.
+bool launch_panel_col(Ctx& c, RegQrArgs a) {
+    const i64 rows = a.rows;
+    constexpr int kClW = 16, kGrW = 8;
+    auto cl_try = [&](auto rpt_tag) -> bool {
+        constexpr int RPT = decltype(rpt_tag)::value;
+        const i64 per = static_cast<i64>(kClW) * RPT;
+        if (rows > 16 * per) return false;
+        const i64 grid = std::max<i64>(1, (rows + per - 1) / per);
+        a.rpc = static_cast<int>(per);
+        launch_col<RPT, kClW, true>(c, a, grid);
+        return true;
     };
-
-    // ---- factorization (runtime column loop; registers are indexed only by
-    // compile-time l, the active column is selected with predicates) ----
-    for (int i = 0; i < kk; ++i) {
-        {
-            const double mine = reg_col_dots<R>(x, i, r0, nr, wsum);
-            reg_publish_row<R>(x, i - r0, nr, row_slot());
-            exchange(mine, i);
-            if (tid == 0) {
-                const double alpha = dgv[i], tail = red[i];
-                double tj, beta, inv;
-                if (tail <= DBL_MIN) {
-                    tj = 0.0;
-                    beta = alpha;
-                    inv = 0.0;
-                } else {
-                    beta = sqrt(alpha * alpha + tail);
-                    if (alpha >= 0.0) beta = -beta;
-                    inv = 1.0 / (alpha - beta);
-                    tj = (beta - alpha) / beta;
-                }
-                ts[i] = tj;
-                sc[0] = beta;
-                sc[1] = inv;
-            }
-            __syncthreads();
-            if (tid < 32) {
-                // update weights (l > i) and, for l < i, the Gram entries
-                // v_l^T v_i = v_l(i) + inv * sum_{r>i} v_l(r) x_i(r), which the
-                // same reduction produced: column i of the compact-WY T follows
-                // (T(0:i,i) = -tau_i T(0:i,0:i) G(0:i,i)) with no extra pass.
-                wv[tid] = (tid > i && tid < b) ? ts[i] * (dgv[tid] + red[tid] * sc[1]) : 0.0;
-                if (tid < i) gcol[tid] = dgv[tid] + sc[1] * red[tid];
-            }
-            __syncthreads();
-            if (p.T && tid <= i) {
-                double s = 0.0;
-                for (int q = tid; q < i; ++q) s = fma(tb[tid + q * 32], gcol[q], s);
-                tb[tid + i * 32] = (tid == i) ? ts[i] : -ts[i] * s;
-            }
-            const double beta = sc[0], inv = sc[1];
-            double vj[R];
-#pragma unroll
-            for (int j = 0; j < R; ++j) {
-                const int rr = tid + j * kRegThreads, gr = r0 + rr;
-                const double xi = reg_pick(x[j], i);
-                vj[j] = (rr < nr && gr > i) ? xi * inv : 0.0;
-                if (rr < nr && gr >= i) reg_set(x[j], i, gr > i ? vj[j] : beta);
-            }
-#pragma unroll
-            for (int l = 0; l < 32; ++l) {
-                if (l > i) {
-                    const double wl = wv[l];
-#pragma unroll
-                    for (int j = 0; j < R; ++j) {
-                        const int rr = tid + j * kRegThreads, gr = r0 + rr;
-                        if (rr < nr) x[j][l] = (gr == i) ? x[j][l] - wl : fma(-wl, vj[j], x[j][l]);
-                    }
-                }
-            }
-        }
-    }
-    if (tid < 32) {
-        if (tid >= kk) ts[tid] = 0.0;
-        if (rank == 0 && tid < kk) p.tau[tid] = ts[tid];
-    }
-    __syncthreads();
-
-    // ---- factored panel / R / V ----
-#pragma unroll
-    for (int j = 0; j < R; ++j) {
-        const int rr = tid + j * kRegThreads, gr = r0 + rr;
-        if (rr < nr) {
-#pragma unroll
-            for (int l = 0; l < 32; ++l) {
-                if (l < b) {
-                    if (p.Pout) p.Pout[gr + static_cast<i64>(l) * p.ldout] = x[j][l];
-                    if (p.R && gr < kk) p.R[gr + static_cast<i64>(l) * p.ldr] = (gr <= l) ? x[j][l] : 0.0;
-                    if (p.V) p.V[gr + static_cast<i64>(l) * p.ldv] = gr > l ? x[j][l] : (gr == l ? 1.0 : 0.0);
-                }
-            }
-        }
-    }
-
-    // ---- compact-WY T (identical in every CTA; rank 0 writes it) ----
-    if (p.T && rank == 0)
-        for (int e = tid; e < 32 * 32; e += kRegThreads) p.T[e] = tb[e];
-
-    // ---- explicit thin Q of the whole (single-panel) matrix ----
-    if (p.Q) {
-        for (int i = kk - 1; i >= 0; --i) {
-            {
-                const double ti = ts[i];
-                if (i < kk - 1 && ti != 0.0) {
-                    const double mine = reg_col_dots<R>(x, i, r0, nr, wsum);
-                    reg_publish_row<R>(x, i - r0, nr, row_slot());
-                    exchange(mine, i);
-                    if (tid < 32) wv[tid] = (tid > i && tid < kk) ? ti * (dgv[tid] + red[tid]) : 0.0;
-                    __syncthreads();
-                    double vi[R];
-#pragma unroll
-                    for (int j = 0; j < R; ++j) vi[j] = reg_pick(x[j], i);
-#pragma unroll
-                    for (int l = 0; l < 32; ++l) {
-                        if (l > i) {
-                            const double wl = wv[l];
-#pragma unroll
-                            for (int j = 0; j < R; ++j) {
-                                const int rr = tid + j * kRegThreads, gr = r0 + rr;
-                                if (rr < nr && gr >= i) x[j][l] = (gr == i) ? x[j][l] - wl : fma(-wl, vi[j], x[j][l]);
-                            }
-                        }
-                    }
-                }
-#pragma unroll
-                for (int j = 0; j < R; ++j) {
-                    const int gr = r0 + tid + j * kRegThreads;
-                    const double xi = reg_pick(x[j], i);
-                    reg_set(x[j], i, gr > i ? -ti * xi : (gr == i ? 1.0 - ti : 0.0));
-                }
-            }
-        }
-#pragma unroll
-        for (int j = 0; j < R; ++j) {
-            const int rr = tid + j * kRegThreads;
-            if (rr < nr)
-#pragma unroll
-                for (int l = 0; l < 32; ++l)
-                    if (l < kk) p.Q[(r0 + rr) + static_cast<i64>(l) * p.ldq] = x[j][l];
-        }
-    }
-    if constexpr (CL) cg::this_cluster().sync();  // peers may still read this CTA's shared memory
+    auto gr_try = [&](auto rpt_tag) -> bool {
+        constexpr int RPT = decltype(rpt_tag)::value;
+        const i64 per = static_cast<i64>(kGrW) * RPT;
+        if (rows > static_cast<i64>(c.sm_count) * per) return false;
+        const i64 grid = std::max<i64>(1, (rows + per - 1) / per);
+        a.rpc = static_cast<int>(per);
+        launch_col<RPT, kGrW, false>(c, a, grid);
+        return true;
+    };
+    static const int mode = [] {
+        const char* e = std::getenv("TTR_QR_PANEL_MODE");  // experiments: "grid" forces the cooperative grid
+        return (e && e[0] == 'g') ? 1 : 0;
+    }();
+    // Measured (tools/qr_bench.py): the cluster wins while a warp owns <= 8
+    // rows (<= 2048-row panels); beyond that spreading the panel over up to
+    // one CTA per SM beats the cheaper cluster barrier.
+    if (mode == 0 && (cl_try(std::integral_constant<int, 4>{}) || cl_try(std::integral_constant<int, 8>{})))
+        return true;
+    if (gr_try(std::integral_constant<int, 4>{}) || gr_try(std::integral_constant<int, 8>{}) ||
+        gr_try(std::integral_constant<int, 16>{}) || gr_try(std::integral_constant<int, 24>{}) ||
+        gr_try(std::integral_constant<int, 32>{}) || gr_try(std::integral_constant<int, 40>{}) ||
+        gr_try(std::integral_constant<int, 48>{}))
+        return false;
+    throw Error(TTR_ERR_INTERNAL, "qr panel taller than the device panel limit");
 }
 
 __global__ void init_thin_identity(int m, int k, double* Q, i64 ldq) {
@@ -512,7 +297,7 @@ void thin_qr(Ctx& c, i64 m, i64 n, const double* A, i64 lda, double* Q, i64 ldq,
     // Panels hold at most 2 rows x 32 columns per thread in registers (one CTA
     // per SM): taller R-only factorizations (norm_exact of very tall cores)
     // go through a TSQR split — R of each row block, then R of the stacked Rs.
-    const i64 max_rows = 2LL * kRegThreads * c.sm_count;
+    const i64 max_rows = 8LL * 48 * c.sm_count;  // panel_col_kernel grid limit (8 warps x 48 rows per SM)
     if (m > max_rows) {
         if (Q != nullptr) throw Error(TTR_ERR_INTERNAL, "thin_qr with Q: matrix taller than the device panel limit");
         const i64 chunk = std::max<i64>(k, max_rows / 2);
@@ -531,59 +316,16 @@ void thin_qr(Ctx& c, i64 m, i64 n, const double* A, i64 lda, double* Q, i64 ldq,
         thin_qr(c, lds, n, stack.p, lds, nullptr, 1, R, ldr);
         return;
     }
-    static bool configured = false;
-    if (!configured) {
-        TTR_CUDA(cudaFuncSetAttribute(panel_reg_kernel<1, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-        TTR_CUDA(cudaFuncSetAttribute(panel_reg_kernel<2, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-        configured = true;
-    }
-    // Launch the register-resident panel kernel on a rows x b panel (b <= 32):
-    // one cluster of <= 16 CTAs when rows <= 16 * 512, else a cooperative grid
-    // of <= one CTA per SM. Returns true if the cluster mode was used.
+    // Launch the column-per-lane panel kernel on a rows x b panel (b <= 32):
+    // one cluster of <= 16 CTAs (16 warps each) when the rows fit, else a
+    // cooperative grid of <= one CTA (8 warps) per SM. Returns true for the
+    // cluster mode.
     DBuf partials(c, static_cast<std::size_t>(2 * 160 * 32));
     DBuf diag(c, 2 * 32);
     auto launch_panel = [&](RegQrArgs a) {
-        const i64 rows = a.rows;
-        const bool cl = rows <= 16 * 2 * kRegThreads;
-        i64 grid;
-        if (cl) {
-            grid = std::max<i64>(1, std::min<i64>(16, (rows + kRegThreads - 1) / kRegThreads));
-        } else {
-            grid = std::min<i64>(c.sm_count, (rows + 2 * kRegThreads - 1) / (2 * kRegThreads) * 2);
-            grid = std::max<i64>(grid, (rows + 2 * kRegThreads - 1) / (2 * kRegThreads));
-            grid = std::min<i64>(grid, c.sm_count);
-        }
-        const i64 rpc = (rows + grid - 1) / grid;
-        if (rpc > 2 * kRegThreads) throw Error(TTR_ERR_INTERNAL, "qr panel too tall for the device");
-        grid = (rows + rpc - 1) / rpc;
-        a.rpc = static_cast<int>(rpc);
         a.partials = partials.p;
         a.diag = diag.p;
-        const bool two = rpc > kRegThreads;
-        if (cl) {
-            cudaLaunchConfig_t cfg = {};
-            cfg.gridDim = dim3(static_cast<unsigned>(grid));
-            cfg.blockDim = dim3(kRegThreads);
-            cfg.dynamicSmemBytes = 0;
-            cfg.stream = c.stream;
-            cudaLaunchAttribute attr[1];
-            attr[0].id = cudaLaunchAttributeClusterDimension;
-            attr[0].val.clusterDim.x = static_cast<unsigned>(grid);
-            attr[0].val.clusterDim.y = 1;
-            attr[0].val.clusterDim.z = 1;
-            cfg.attrs = attr;
-            cfg.numAttrs = 1;
-            if (two) TTR_CUDA(cudaLaunchKernelEx(&cfg, panel_reg_kernel<2, true>, a));
-            else TTR_CUDA(cudaLaunchKernelEx(&cfg, panel_reg_kernel<1, true>, a));
-        } else {
-            void* args[] = {&a};
-            void* fn = two ? reinterpret_cast<void*>(panel_reg_kernel<2, false>)
-                           : reinterpret_cast<void*>(panel_reg_kernel<1, false>);
-            TTR_CUDA(cudaLaunchCooperativeKernel(fn, dim3(static_cast<unsigned>(grid)), dim3(kRegThreads), args, 0,
-                                                 c.stream));
-        }
-        c.launched();
-        return cl;
+        return launch_panel_col(c, a);
     };
 
     // ---- <= 32 columns: factorization and explicit Q in one launch ----
