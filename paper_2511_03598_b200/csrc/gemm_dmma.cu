@@ -348,16 +348,20 @@ constexpr int kSkBM = 32, kSkBN = 128;
 // small tile for strided batches of tiny problems (config 5a: 64 x 20 x 1024)
 constexpr int kSmBM = 64, kSmBN = 32;
 
-template <int BM, int BN, bool AT, int KM, int BK>
+// medium tile: M <= ~384 with long N (M H(X), Q^T V) — no padding of M = 320
+// (tools/gemm_tune.cu: 30.9 vs 26.4 TF/s on 320 x 128000 x 1000)
+constexpr int kMdBM = 64, kMdBN = 64;
+
+template <int BM, int BN, bool AT, int KM, int BK, int ST = kStages>
 void dispatch_vec(Ctx& c, GemmArgs& a, int splits, bool va2, bool vb2) {
     if constexpr (KM == 2) {  // element-wise B staging: only the A vector width matters
-        if (va2) launch<BM, BN, BK, kWM, kWN, kStages, AT, KM, 2, 1>(c, a, splits);
-        else launch<BM, BN, BK, kWM, kWN, kStages, AT, KM, 1, 1>(c, a, splits);
+        if (va2) launch<BM, BN, BK, kWM, kWN, ST, AT, KM, 2, 1>(c, a, splits);
+        else launch<BM, BN, BK, kWM, kWN, ST, AT, KM, 1, 1>(c, a, splits);
     } else {
-        if (va2 && vb2) launch<BM, BN, BK, kWM, kWN, kStages, AT, KM, 2, 2>(c, a, splits);
-        else if (va2) launch<BM, BN, BK, kWM, kWN, kStages, AT, KM, 2, 1>(c, a, splits);
-        else if (vb2) launch<BM, BN, BK, kWM, kWN, kStages, AT, KM, 1, 2>(c, a, splits);
-        else launch<BM, BN, BK, kWM, kWN, kStages, AT, KM, 1, 1>(c, a, splits);
+        if (va2 && vb2) launch<BM, BN, BK, kWM, kWN, ST, AT, KM, 2, 2>(c, a, splits);
+        else if (va2) launch<BM, BN, BK, kWM, kWN, ST, AT, KM, 2, 1>(c, a, splits);
+        else if (vb2) launch<BM, BN, BK, kWM, kWN, ST, AT, KM, 1, 2>(c, a, splits);
+        else launch<BM, BN, BK, kWM, kWN, ST, AT, KM, 1, 1>(c, a, splits);
     }
 }
 
@@ -374,7 +378,7 @@ int choose_splits(Ctx& c, i64 tiles, int total_kt) {
 }
 
 void run_gemm(Ctx& c, bool AT, int KM, int BK, GemmArgs& a, bool va2, bool vb2, int splits, double* C, i64 ldc,
-              double alpha, double beta, double* Ct, i64 ldct, bool skinny = false, i64 sCt = 0) {
+              double alpha, double beta, double* Ct, i64 ldct, bool skinny = false, i64 sCt = 0, bool medium = false) {
     const bool small = a.batch > 1 && !skinny;
     const int total_kt = (a.K + BK - 1) / BK;
     splits = std::max(1, std::min(splits, total_kt));
@@ -398,6 +402,8 @@ void run_gemm(Ctx& c, bool AT, int KM, int BK, GemmArgs& a, bool va2, bool vb2, 
         else if (KM == 1 && BK == 4) dispatch_vec<kSmBM, kSmBN, false, 1, 4>(c, a, splits, va2, vb2);
         else dispatch_vec<kSmBM, kSmBN, false, 2, 16>(c, a, splits, va2, vb2);
     }
+    else if (medium && !AT && KM == 0) dispatch_vec<kMdBM, kMdBN, false, 0, 16, 4>(c, a, splits, va2, vb2);
+    else if (medium && AT && KM == 0) dispatch_vec<kMdBM, kMdBN, true, 0, 16, 3>(c, a, splits, va2, vb2);
     else if (!AT && KM == 0) dispatch_vec<kBM, kBN, false, 0, 16>(c, a, splits, va2, vb2);
     else if (AT && KM == 0) dispatch_vec<kBM, kBN, true, 0, 16>(c, a, splits, va2, vb2);
     else if (!AT && KM == 1 && BK == 16) dispatch_vec<kBM, kBN, false, 1, 16>(c, a, splits, va2, vb2);
@@ -443,11 +449,14 @@ void gemm(Ctx& c, bool trans_a, i64 M, i64 N, i64 K, double alpha, const double*
     const bool va2 = aligned16(A) && (lda % 2 == 0);
     const bool vb2 = aligned16(B) && (ldb % 2 == 0);
     const bool skinny = M <= kSkBM;
-    const i64 bm = skinny ? kSkBM : kBM, bn = skinny ? kSkBN : kBN;
+    // 64 x 64 tiles when 128-row tiles would pad M noticeably (M = 320: 384)
+    const i64 pad128 = (M + kBM - 1) / kBM * kBM, pad64 = (M + kMdBM - 1) / kMdBM * kMdBM;
+    const bool medium = !skinny && pad128 * 20 > pad64 * 21;
+    const i64 bm = skinny ? kSkBM : (medium ? kMdBM : kBM), bn = skinny ? kSkBN : (medium ? kMdBN : kBN);
     const i64 tiles = ((M + bm - 1) / bm) * ((N + bn - 1) / bn);
     const int total_kt = static_cast<int>((K + 15) / 16);
     const int splits = choose_splits(c, tiles, total_kt);
-    run_gemm(c, trans_a, 0, 16, a, va2, vb2, splits, C, ldc, alpha, beta, nullptr, 0, skinny);
+    run_gemm(c, trans_a, 0, 16, a, va2, vb2, splits, C, ldc, alpha, beta, nullptr, 0, skinny, 0, medium);
 }
 
 void krp_step(Ctx& c, i64 r_left, i64 n, i64 r_right, i64 N, const double* X, const double* Omega, i64 ldo,

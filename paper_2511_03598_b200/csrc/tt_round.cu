@@ -440,7 +440,6 @@ void rand_orth_sweep(Ctx& c, const TTDev& t, i64 width, const std::vector<const 
     DBuf work(c, static_cast<std::size_t>(max_work));
     DBuf S(c, static_cast<std::size_t>(max_s));
     DBuf M(c, static_cast<std::size_t>(width * t.max_rank()));
-    DBuf Qt(c, static_cast<std::size_t>(max_s));
 
     const double* v = t.core(0);
     for (i64 k = 1; k < d; ++k) {
@@ -459,11 +458,8 @@ void rand_orth_sweep(Ctx& c, const TTDev& t, i64 width, const std::vector<const 
         double* dst = (k == d - 1) ? out->core(d - 1) : work.p;
         {
             PhaseScope ph(c, kPhaseGemm);
-            // M = Q^T V  (l x r_k)
-            // (as Q^T then a plain GEMM: the column-major A-tile path streams
-            // 1 KB runs of HBM; the transposed-A path only 128 B ones)
-            transpose(c, rows, l, out->core(k - 1), rows, Qt.p, l);
-            gemm(c, false, l, cols, rows, 1.0, Qt.p, l, v, rows, 0.0, M.p, l);
+            // M = Q^T V  (l x r_k), transposed-A GEMM (64 x 64 tiles, split-K)
+            gemm(c, true, l, cols, rows, 1.0, out->core(k - 1), rows, v, rows, 0.0, M.p, l);
             // H(Y_{k+1}) = M H(X_{k+1})  (contract_first, internal.hpp:10-12)
             gemm(c, false, l, ncols, cols, 1.0, M.p, l, t.core(k), cols, 0.0, dst, l);
         }

@@ -1,6 +1,7 @@
 // Tile-configuration sweep for the fp64 DMMA GEMM (measurement tool).
 // Includes the library's kernel source and times instantiations on the
-// shapes of config 5b. Build: see tools/Makefile.tune
+// shapes of config 5b. Build:
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -Iinclude -o tools/gemm_tune tools/gemm_tune.cu
 #include <cstdio>
 #include <vector>
 
@@ -61,11 +62,11 @@ int main() {
     const size_t big = 1000ull * 128000;  // 1 G doubles? no: 128M doubles = 1 GB
     double *A, *B, *Cm, *Wt;
     cudaMalloc(&A, big * 8);
-    cudaMalloc(&B, 64ull * 1024 * 1024 * 8);
+    cudaMalloc(&B, 128ull * 1024 * 1024 * 8);
     cudaMalloc(&Cm, 64ull * 1024 * 1024 * 8);
     cudaMalloc(&Wt, 4ull * 1024 * 1024 * 8);
     cudaMemset(A, 0, big * 8);
-    cudaMemset(B, 0, 64ull * 1024 * 1024 * 8);
+    cudaMemset(B, 0, 128ull * 1024 * 1024 * 8);
     cudaMemset(Wt, 0, 4ull * 1024 * 1024 * 8);
 
     struct Shape { const char* name; int M, N, K; bool at; int km; int splits; };
@@ -95,14 +96,12 @@ int main() {
         }
         RUN(128, 64, 16, 32, 32, 4)
         RUN(128, 64, 16, 32, 32, 3)
-        RUN(64, 128, 16, 32, 32, 4)
-        RUN(128, 128, 16, 64, 32, 3)
-        RUN(128, 128, 16, 32, 64, 3)
-        RUN(128, 128, 16, 64, 64, 3)
         RUN(64, 64, 16, 32, 32, 4)
-        RUN(128, 64, 32, 32, 32, 3)
-        RUN(256, 64, 16, 64, 32, 3)
-        RUN(128, 32, 16, 32, 32, 4)
+        RUN(64, 64, 16, 32, 32, 3)
+        RUN(160, 64, 16, 32, 32, 3)
+        RUN(160, 64, 16, 32, 32, 4)
+        RUN(96, 64, 16, 32, 32, 4)
+        RUN(64, 32, 16, 32, 32, 4)
     }
     return 0;
 }
