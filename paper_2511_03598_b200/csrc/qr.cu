@@ -211,7 +211,7 @@ void launch_col(Ctx& c, const RegQrArgs& a, i64 grid) {
 // Geometry + template dispatch for panel_col_kernel. a.partials/a.diag must be set.
 bool launch_panel_col(Ctx& c, RegQrArgs a) {
     const i64 rows = a.rows;
-    constexpr int kClW = 16, kGrW = 8;
+    constexpr int kClW = 16;
     auto cl_try = [&](auto rpt_tag) -> bool {
         constexpr int RPT = decltype(rpt_tag)::value;
         const i64 per = static_cast<i64>(kClW) * RPT;
@@ -221,13 +221,14 @@ bool launch_panel_col(Ctx& c, RegQrArgs a) {
         launch_col<RPT, kClW, true>(c, a, grid);
         return true;
     };
-    auto gr_try = [&](auto rpt_tag) -> bool {
-        constexpr int RPT = decltype(rpt_tag)::value;
-        const i64 per = static_cast<i64>(kGrW) * RPT;
+    // grid: 16 warps while x[RPT] leaves room in 128 registers, then 8 warps
+    auto gr_try = [&](auto rpt_tag, auto warps_tag) -> bool {
+        constexpr int RPT = decltype(rpt_tag)::value, W = decltype(warps_tag)::value;
+        const i64 per = static_cast<i64>(W) * RPT;
         if (rows > static_cast<i64>(c.sm_count) * per) return false;
         const i64 grid = std::max<i64>(1, (rows + per - 1) / per);
         a.rpc = static_cast<int>(per);
-        launch_col<RPT, kGrW, false>(c, a, grid);
+        launch_col<RPT, W, false>(c, a, grid);
         return true;
     };
     static const int mode = [] {
@@ -239,10 +240,12 @@ bool launch_panel_col(Ctx& c, RegQrArgs a) {
     // one CTA per SM beats the cheaper cluster barrier.
     if (mode == 0 && (cl_try(std::integral_constant<int, 4>{}) || cl_try(std::integral_constant<int, 8>{})))
         return true;
-    if (gr_try(std::integral_constant<int, 4>{}) || gr_try(std::integral_constant<int, 8>{}) ||
-        gr_try(std::integral_constant<int, 16>{}) || gr_try(std::integral_constant<int, 24>{}) ||
-        gr_try(std::integral_constant<int, 32>{}) || gr_try(std::integral_constant<int, 40>{}) ||
-        gr_try(std::integral_constant<int, 48>{}))
+    using I16 = std::integral_constant<int, 16>;
+    using I8 = std::integral_constant<int, 8>;
+    if (gr_try(std::integral_constant<int, 4>{}, I16{}) || gr_try(std::integral_constant<int, 8>{}, I16{}) ||
+        gr_try(std::integral_constant<int, 12>{}, I16{}) || gr_try(std::integral_constant<int, 16>{}, I16{}) ||
+        gr_try(std::integral_constant<int, 20>{}, I16{}) || gr_try(std::integral_constant<int, 24>{}, I16{}) ||
+        gr_try(std::integral_constant<int, 56>{}, I8{}) || gr_try(std::integral_constant<int, 64>{}, I8{}))
         return false;
     throw Error(TTR_ERR_INTERNAL, "qr panel taller than the device panel limit");
 }
