@@ -84,6 +84,7 @@ ttr_status ttr_ctx_destroy(ttr_ctx* ctx) {
         cudaSetDevice(ctx->c.device);
         if (ctx->c.work) cudaFreeAsync(ctx->c.work, ctx->c.stream);
         cudaStreamSynchronize(ctx->c.stream);
+        if (ctx->c.qr_xchg) cudaFree(ctx->c.qr_xchg);
         if (ctx->c.host_scalars) cudaFreeHost(ctx->c.host_scalars);
         if (ctx->c.own_stream) cudaStreamDestroy(ctx->c.stream);
         delete ctx;

@@ -47,6 +47,11 @@ struct Counts {
 // Phase timing (CUDA events on the context stream), for bench.py's roofline.
 enum Phase { kPhaseSketch = 0, kPhaseQr = 1, kPhaseGemm = 2, kPhaseOther = 3, kNumPhases = 4 };
 
+// QR panel grid-exchange workspace (qr_panel.cuh): 2 header words, then
+// [2][160][32] CTA partials and [2][32] published-row slots (sized for the
+// former tagged layout, two words per value)
+constexpr std::size_t kQrXchgWords = 2 + 2 * 160 * 32 * 2 + 2 * 32 * 2;
+
 struct Ctx {
     int device = 0;
     bool timing = false;
@@ -62,6 +67,9 @@ struct Ctx {
     std::size_t work_bytes = 0;
     // small pinned host staging buffer for scalars
     double* host_scalars = nullptr;
+    // persistent workspace of the QR panel's grid exchange (qr_panel.cuh)
+    unsigned long long* qr_xchg = nullptr;
+    unsigned long long* qr_exchange();
 
     void charge_gemm(std::uint64_t f) { counts.gemm += f; if (sketch_depth) counts.sketch += f; }
     void charge_qr(std::uint64_t f) { counts.qr += f; if (sketch_depth) counts.sketch += f; }

@@ -25,6 +25,7 @@
 #include <algorithm>
 #include <cfloat>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -171,16 +172,16 @@ struct RegQrArgs {
     i64 ldq;
     double* R;
     i64 ldr;
-    double* partials;  // grid mode: [2][gridDim][32]
-    double* diag;      // grid mode: [2][32]
+    unsigned long long* xchg;  // grid mode: Ctx::qr_exchange() ([2][160][32] partials + [2][32] row)
+    long long* trace;  // optional (TTR_QR_TRACE): clock64 per phase of CTA 0 / thread 0
 };
 
 #include "qr_panel.cuh"
 
-template <int RPT, int WARPS, bool CL>
+template <int RPT, int WARPS, int MODE>
 void launch_col(Ctx& c, const RegQrArgs& a, i64 grid) {
-    auto kern = panel_col_kernel<RPT, WARPS, CL>;
-    if constexpr (CL) {
+    auto kern = panel_col_kernel<RPT, WARPS, MODE>;
+    if constexpr (MODE == 0) {
         static bool configured = false;
         if (!configured) {
             TTR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
@@ -206,11 +207,33 @@ void launch_col(Ctx& c, const RegQrArgs& a, i64 grid) {
                                              dim3(WARPS * 32), args, 0, c.stream));
     }
     c.launched();
+    if (a.trace) {  // TTR_QR_TRACE: per-phase cycles of CTA 0, averaged over the panel's columns
+        long long h[32 * 8];
+        TTR_CUDA(cudaMemcpyAsync(h, a.trace, sizeof(h), cudaMemcpyDeviceToHost, c.stream));
+        TTR_CUDA(cudaStreamSynchronize(c.stream));
+        const int nc = std::min(a.b, a.rows);
+        double acc[8] = {};
+        for (int i = 0; i < nc; ++i) {
+            const long long* t = h + i * 8;
+            const long long seq[8] = {t[0], t[1], t[6], t[7], t[2], t[3], t[4], t[5]};
+            for (int k = 1; k < 8; ++k) acc[k] += static_cast<double>(seq[k] - seq[k - 1]) / nc;
+            acc[0] += static_cast<double>(t[5] - t[0]) / nc;
+        }
+        std::fprintf(stderr,
+                     "panel<%d,%d,mode %d> grid %lld rows %d: cycles/col %.0f | dots %.0f bar %.0f xchg %.0f gather %.0f "
+                     "scalar %.0f bar %.0f update %.0f\n",
+                     RPT, WARPS, MODE, static_cast<long long>(grid), a.rows, acc[0], acc[1], acc[2], acc[3], acc[4],
+                     acc[5], acc[6], acc[7]);
+    }
 }
 
-// Geometry + template dispatch for panel_col_kernel. a.partials/a.diag must be set.
+// Geometry + template dispatch for panel_col_kernel. a.xchg must be set.
 bool launch_panel_col(Ctx& c, RegQrArgs a) {
     const i64 rows = a.rows;
+    static const bool tracing = std::getenv("TTR_QR_TRACE") != nullptr;  // diagnostics only
+    static long long* trace_buf = nullptr;
+    if (tracing && !trace_buf) TTR_CUDA(cudaMalloc(reinterpret_cast<void**>(&trace_buf), 32 * 8 * sizeof(long long)));
+    a.trace = tracing ? trace_buf : nullptr;
     constexpr int kClW = 16;
     auto cl_try = [&](auto rpt_tag) -> bool {
         constexpr int RPT = decltype(rpt_tag)::value;
@@ -218,34 +241,42 @@ bool launch_panel_col(Ctx& c, RegQrArgs a) {
         if (rows > 16 * per) return false;
         const i64 grid = std::max<i64>(1, (rows + per - 1) / per);
         a.rpc = static_cast<int>(per);
-        launch_col<RPT, kClW, true>(c, a, grid);
+        launch_col<RPT, kClW, 0>(c, a, grid);
         return true;
     };
     // grid: 16 warps while x[RPT] leaves room in 128 registers, then 8 warps
-    auto gr_try = [&](auto rpt_tag, auto warps_tag) -> bool {
+    auto gr_try = [&](auto rpt_tag, auto warps_tag, auto mode_tag, i64 max_grid) -> bool {
         constexpr int RPT = decltype(rpt_tag)::value, W = decltype(warps_tag)::value;
+        constexpr int MODE = decltype(mode_tag)::value;
         const i64 per = static_cast<i64>(W) * RPT;
-        if (rows > static_cast<i64>(c.sm_count) * per) return false;
+        if (rows > max_grid * per) return false;
         const i64 grid = std::max<i64>(1, (rows + per - 1) / per);
         a.rpc = static_cast<int>(per);
-        launch_col<RPT, W, false>(c, a, grid);
+        launch_col<RPT, W, MODE>(c, a, grid);
         return true;
     };
-    static const int mode = [] {
-        const char* e = std::getenv("TTR_QR_PANEL_MODE");  // experiments: "grid" forces the cooperative grid
-        return (e && e[0] == 'g') ? 1 : 0;
+    // experiments: TTR_QR_PANEL_MODE = grid forces the cooperative grid
+    static const int forced = [] {
+        const char* e = std::getenv("TTR_QR_PANEL_MODE");
+        return (e && e[0] == 'g') ? 1 : -1;
     }();
-    // Measured (tools/qr_bench.py): the cluster wins while a warp owns <= 8
-    // rows (<= 2048-row panels); beyond that spreading the panel over up to
-    // one CTA per SM beats the cheaper cluster barrier.
-    if (mode == 0 && (cl_try(std::integral_constant<int, 4>{}) || cl_try(std::integral_constant<int, 8>{})))
-        return true;
     using I16 = std::integral_constant<int, 16>;
     using I8 = std::integral_constant<int, 8>;
-    if (gr_try(std::integral_constant<int, 4>{}, I16{}) || gr_try(std::integral_constant<int, 8>{}, I16{}) ||
-        gr_try(std::integral_constant<int, 12>{}, I16{}) || gr_try(std::integral_constant<int, 16>{}, I16{}) ||
-        gr_try(std::integral_constant<int, 20>{}, I16{}) || gr_try(std::integral_constant<int, 24>{}, I16{}) ||
-        gr_try(std::integral_constant<int, 56>{}, I8{}) || gr_try(std::integral_constant<int, 64>{}, I8{}))
+    using Gb = std::integral_constant<int, 1>;
+    // Measured (tools/qr_bench.py, tools/probe/exchange_cost.cu): the cluster
+    // wins while a warp owns <= 8 rows (<= 2048-row panels); beyond that the
+    // cooperative grid (up to one CTA per SM) wins.
+    if ((forced < 0 || forced == 0) &&
+        (cl_try(std::integral_constant<int, 4>{}) || cl_try(std::integral_constant<int, 8>{})))
+        return true;
+    const i64 g = c.sm_count;
+    if (gr_try(std::integral_constant<int, 4>{}, I16{}, Gb{}, g) ||
+        gr_try(std::integral_constant<int, 8>{}, I16{}, Gb{}, g) ||
+        gr_try(std::integral_constant<int, 12>{}, I16{}, Gb{}, g) ||
+        gr_try(std::integral_constant<int, 16>{}, I16{}, Gb{}, g) ||
+        gr_try(std::integral_constant<int, 20>{}, I16{}, Gb{}, g) ||
+        gr_try(std::integral_constant<int, 24>{}, I16{}, Gb{}, g) ||
+        gr_try(std::integral_constant<int, 56>{}, I8{}, Gb{}, g) || gr_try(std::integral_constant<int, 64>{}, I8{}, Gb{}, g))
         return false;
     throw Error(TTR_ERR_INTERNAL, "qr panel taller than the device panel limit");
 }
@@ -323,11 +354,9 @@ void thin_qr(Ctx& c, i64 m, i64 n, const double* A, i64 lda, double* Q, i64 ldq,
     // one cluster of <= 16 CTAs (16 warps each) when the rows fit, else a
     // cooperative grid of <= one CTA (8 warps) per SM. Returns true for the
     // cluster mode.
-    DBuf partials(c, static_cast<std::size_t>(2 * 160 * 32));
-    DBuf diag(c, 2 * 32);
+    unsigned long long* xchg = c.qr_exchange();
     auto launch_panel = [&](RegQrArgs a) {
-        a.partials = partials.p;
-        a.diag = diag.p;
+        a.xchg = xchg;
         return launch_panel_col(c, a);
     };
 

@@ -7,9 +7,11 @@
 //   * dots: the active column is broadcast row by row from lane i (shuffle)
 //     and lane l accumulates x(r,i)*x(r,l) over its rows with r > i,
 //   * the warp partials are summed in shared memory, the CTA partials through
-//     distributed shared memory inside ONE thread-block cluster (CL = true:
-//     <= 16 CTAs) or through global memory and one grid barrier (CL = false:
-//     cooperative launch, <= one CTA per SM); fixed order -> deterministic,
+//     distributed shared memory inside ONE thread-block cluster (MODE 0:
+//     <= 16 CTAs) or through global memory (cooperative launch, <= one CTA
+//     per SM) behind a grid barrier (MODE 1); fixed summation order ->
+//     deterministic. (Flag- or tag-polling exchanges without the barrier were
+//     measured slower inside the kernel: tools/probe/exchange_cost.cu.)
 //   * warp 0 turns the sums into the reflector (every lane computes the same
 //     beta/tau, so nothing is broadcast) and the per-column update weights,
 //   * update: ONE fma per owned entry, x(r,l) += c_l * x(r,i).
@@ -22,16 +24,17 @@
 // backward accumulation (LAPACK dorg2r order) with the same machinery.
 #pragma once
 
-template <int RPT, int WARPS, bool CL>
+template <int RPT, int WARPS, int MODE>
 __global__ void __launch_bounds__(WARPS * 32, 1) panel_col_kernel(RegQrArgs p) {
+    constexpr bool CL = MODE == 0;
     constexpr int NT = WARPS * 32;
     __shared__ double wsum[WARPS * 32];
     __shared__ double part_s[2 * 32];
     __shared__ double dg_s[2 * 32];
-    constexpr int LW = WARPS >= 16 ? 16 : 8;  // warps that gather CTA partials
-    __shared__ double xs[LW * 32];
     __shared__ double ts[32], invs[32], cas[32], wls[32], sc[2];
-    __shared__ double tb[32 * 32];
+    constexpr int LW = WARPS >= 16 ? 16 : 8;  // grid mode: warps gathering CTA partials
+    __shared__ double xs[LW * 32];
+    __shared__ double gm[32 * 32];  // Gram entries v_k^T v_m (k < m), column m
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     int rank, G;
     if constexpr (CL) {
@@ -48,7 +51,8 @@ __global__ void __launch_bounds__(WARPS * 32, 1) panel_col_kernel(RegQrArgs p) {
     const int g0 = r0 + wr0;     // ... and its global index
     const int kk = min(b, p.rows);
     int xc = 0;
-    for (int e = tid; e < 32 * 32; e += NT) tb[e] = 0.0;
+    if (p.T)
+        for (int e = tid; e < 32 * 32; e += NT) gm[e] = 0.0;
 
     // rows beyond the panel are zero and stay zero (every update is x += c*x_i)
     double x[RPT];
@@ -80,68 +84,105 @@ __global__ void __launch_bounds__(WARPS * 32, 1) panel_col_kernel(RegQrArgs p) {
         return s0 + s1;
     };
     // the warp holding global row `grow` copies that row (lane = column) to dst
-    auto publish_row = [&](int grow, double* dst) {
+    auto publish_row = [&](int grow) {
         const int li = grow - r0;
         if (li < 0 || li >= nr || li / RPT != warp) return;
         const int qi = li - wr0;
         double v = 0.0;
 #pragma unroll
         for (int q = 0; q < RPT; ++q) v = (q == qi) ? x[q] : v;
-        dst[lane] = v;
+        const int buf = xc & 1;
+        if constexpr (CL) dg_s[buf * 32 + lane] = v;
+        else p.xchg[2 + 2 * 160 * 32 * 2 + buf * 32 + lane] = __double_as_longlong(v);
     };
     // Sum `mine` over the whole panel. Warp 0 returns (red, dg): red = the
     // column-`lane` sum, dg = row `orow` entry of column `lane` (published
-    // before the call by its owner). Other warps return garbage.
+    // before the call by its owner). Other warps return garbage. Warp 0 alone
+    // gathers the CTA partials (fixed order), so no barrier follows the
+    // cluster/grid synchronisation.
+    long long* trace_ts = nullptr;  // phases 6/7 of the current column (tracing only)
     auto reduce = [&](double mine, int orow, double& red, double& dg) {
         const int buf = xc & 1;
         ++xc;
         wsum[warp * 32 + lane] = mine;
         __syncthreads();
+        if (trace_ts) trace_ts[0] = clock64();
         if (warp == 0) {
-            double t = 0.0;
+            double t0 = 0.0, t1 = 0.0;
 #pragma unroll
-            for (int w = 0; w < WARPS; ++w) t += wsum[w * 32 + lane];
-            if constexpr (CL) part_s[buf * 32 + lane] = t;
-            else p.partials[static_cast<i64>(buf) * G * 32 + rank * 32 + lane] = t;
+            for (int w = 0; w < WARPS; w += 2) {
+                t0 += wsum[w * 32 + lane];
+                t1 += wsum[(w + 1) * 32 + lane];
+            }
+            if constexpr (CL) part_s[buf * 32 + lane] = t0 + t1;
+            else p.xchg[2 + (buf * 160 + rank) * 32 + lane] = __double_as_longlong(t0 + t1);
         }
         if constexpr (CL) {
             cg::cluster_group cl = cg::this_cluster();
             cl.sync();
-            if (warp < LW) {
-                double a = 0.0;
-                for (int g = warp; g < G; g += LW) a += cl.map_shared_rank(part_s, g)[buf * 32 + lane];
-                xs[warp * 32 + lane] = a;
-                if (warp == 0) dg = cl.map_shared_rank(dg_s, orow / rpc)[buf * 32 + lane];
+            if (trace_ts) trace_ts[1] = clock64();
+            if (warp == 0) {
+                // all remote loads in flight at once (ranks >= G alias rank 0, masked)
+                double v[16];
+#pragma unroll
+                for (int g = 0; g < 16; ++g) v[g] = cl.map_shared_rank(part_s, g < G ? g : 0)[buf * 32 + lane];
+                dg = cl.map_shared_rank(dg_s, orow / rpc)[buf * 32 + lane];
+                double a[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+                for (int g = 0; g < 16; ++g) a[g & 3] += (g < G) ? v[g] : 0.0;
+                red = (a[0] + a[1]) + (a[2] + a[3]);
             }
         } else {
-            cg::grid_group gg = cg::this_grid();
-            const double* part = p.partials + static_cast<i64>(buf) * G * 32;
-            gg.sync();
+            cg::this_grid().sync();
+            if (trace_ts) trace_ts[1] = clock64();
             if (warp < LW) {
-                double s = 0.0;
-#pragma unroll 5
-                for (int c = warp; c < G; c += LW) s += __ldcg(part + c * 32 + lane);
-                xs[warp * 32 + lane] = s;
-                if (warp == 0) dg = __ldcg(p.diag + buf * 32 + lane);
+                constexpr int kLoads = (160 + LW - 1) / LW;  // G <= 160
+                const double* part = reinterpret_cast<const double*>(p.xchg + 2) + buf * 160 * 32 + lane;
+                double v[kLoads];
+#pragma unroll
+                for (int u = 0; u < kLoads; ++u) {
+                    const int c = warp + LW * u;
+                    v[u] = (c < G) ? __ldcg(part + c * 32) : 0.0;
+                }
+                double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+                for (int u = 0; u < kLoads; u += 2) {
+                    a0 += v[u];
+                    if (u + 1 < kLoads) a1 += v[u + 1];
+                }
+                xs[warp * 32 + lane] = a0 + a1;
+                if (warp == 0)
+                    dg = __ldcg(reinterpret_cast<const double*>(p.xchg + 2 + 2 * 160 * 32 * 2) + buf * 32 + lane);
             }
         }
-        __syncthreads();
-        if (warp == 0) {
-            double s = 0.0;
+        if constexpr (!CL) {
+            __syncthreads();
+            if (warp == 0) {
+                double a0 = 0.0, a1 = 0.0;
 #pragma unroll
-            for (int w = 0; w < LW; ++w) s += xs[w * 32 + lane];
-            red = s;
+                for (int w = 0; w < LW; w += 2) {
+                    a0 += xs[w * 32 + lane];
+                    a1 += xs[(w + 1) * 32 + lane];
+                }
+                red = a0 + a1;
+            }
         }
     };
-    auto row_slot = [&]() { return CL ? dg_s + (xc & 1) * 32 : p.diag + (xc & 1) * 32; };
 
     // ---- factorization ----
+    const bool trace = p.trace && rank == 0 && tid == 0;
+#define TTR_TRACE(ph) \
+    if (trace) p.trace[i * 8 + (ph)] = clock64()
     double my_inv = 0.0;  // inv of the reflector of column `lane`
     for (int i = 0; i < kk; ++i) {
+        TTR_TRACE(0);
         const double mine = dots(i);
-        publish_row(i, row_slot());
+        publish_row(i);
+        TTR_TRACE(1);
+        if (trace) trace_ts = p.trace + i * 8 + 6;
         double red = 0.0, dg = 0.0;
         reduce(mine, i, red, dg);
+        TTR_TRACE(2);
         if (warp == 0) {
             // every lane derives the same reflector (Eigen makeHouseholder)
             const double alpha = __shfl_sync(0xffffffffu, dg, i), tail = __shfl_sync(0xffffffffu, red, i);
@@ -166,23 +207,12 @@ __global__ void __launch_bounds__(WARPS * 32, 1) panel_col_kernel(RegQrArgs p) {
                 sc[0] = beta;
                 sc[1] = inv;
             }
-            if (p.T) {
-                // Gram entries v_l^T v_i = inv_l (x(i,l) + inv * sum_{r>i} x(r,l) x(r,i)), l < i
-                const double gl = (lane < i) ? invs[lane] * fma(inv, red, dg) : 0.0;
-                // T(0:i,i) = -tau_i T(0:i,0:i) g ; lane j owns row j
-                double s0 = 0.0, s1 = 0.0;
-#pragma unroll 4
-                for (int q = 0; q < 32; ++q) {
-                    const double gq = __shfl_sync(0xffffffffu, gl, q);
-                    const double tq = (q < i) ? tb[lane + q * 32] : 0.0;
-                    if (q & 1) s1 = fma(tq, gq, s1);
-                    else s0 = fma(tq, gq, s0);
-                }
-                if (lane < i) tb[lane + i * 32] = -tj * (s0 + s1);
-                if (lane == i) tb[i + i * 32] = tj;
-            }
+            // Gram entries v_l^T v_i = inv_l (x(i,l) + inv * sum_{r>i} x(r,l) x(r,i)), l < i
+            if (p.T) gm[lane + i * 32] = (lane < i) ? invs[lane] * fma(inv, red, dg) : 0.0;
         }
+        TTR_TRACE(3);
         __syncthreads();
+        TTR_TRACE(4);
         const double ca = cas[lane];
         if (g0 > i) {
 #pragma unroll
@@ -191,16 +221,22 @@ __global__ void __launch_bounds__(WARPS * 32, 1) panel_col_kernel(RegQrArgs p) {
                 x[q] = fma(ca, xi, x[q]);
             }
         } else {
-            const double wl = wls[lane], beta = sc[0];
+            // rows <= i: only row i changes (x(i,l) -= w_l; x(i,i) = beta)
+            const double wl = wls[lane], diag = (lane == i) ? sc[0] : 0.0;
+            const bool me = (lane == i);
 #pragma unroll
             for (int q = 0; q < RPT; ++q) {
                 const double xi = __shfl_sync(0xffffffffu, x[q], i);
                 const int g = g0 + q;
-                if (g > i) x[q] = fma(ca, xi, x[q]);
-                else if (g == i) x[q] = (lane == i) ? beta : x[q] - wl;
+                const double below = fma(ca, xi, x[q]);
+                const double atrow = me ? diag : x[q] - wl;
+                x[q] = (g > i) ? below : ((g == i) ? atrow : x[q]);
             }
         }
+        TTR_TRACE(5);
     }
+    trace_ts = nullptr;
+#undef TTR_TRACE
     if (tid < 32) {
         if (tid >= kk) ts[tid] = 0.0;
         if (tid >= kk) invs[tid] = 0.0;
@@ -223,8 +259,21 @@ __global__ void __launch_bounds__(WARPS * 32, 1) panel_col_kernel(RegQrArgs p) {
             if (p.V) p.V[g + static_cast<i64>(lane) * p.ldv] = g > lane ? x[q] : (g == lane ? 1.0 : 0.0);
         }
     }
-    if (p.T && rank == 0)
-        for (int e = tid; e < 32 * 32; e += NT) p.T[e] = tb[e];
+    // compact-WY T = (diag(1/tau) + striu(V^T V))^{-1}: lane j solves for
+    // column j by back substitution, x_k = tau_k (delta_kj - sum_{m>k} G(k,m) x_m),
+    // which also gives zero rows/columns for tau = 0 (identity reflectors).
+    if (p.T && rank == 0 && warp == 0) {
+        double acc[32];
+#pragma unroll
+        for (int k = 0; k < 32; ++k) acc[k] = 0.0;
+#pragma unroll
+        for (int m = 31; m >= 0; --m) {
+            const double xm = (m > lane) ? 0.0 : ((m == lane) ? ts[m] : -ts[m] * acc[m]);
+            p.T[m + lane * 32] = xm;
+#pragma unroll
+            for (int k = 0; k < m; ++k) acc[k] = fma(gm[k + m * 32], xm, acc[k]);
+        }
+    }
 
     // ---- explicit thin Q of a single-panel matrix (backward accumulation) ----
     if (p.Q) {
@@ -233,7 +282,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) panel_col_kernel(RegQrArgs p) {
             // columns l > i hold Q(:,l) so far, column i holds v_i (tail)
             if (i < kk - 1 && ti != 0.0) {  // uniform across CTAs (identical ts)
                 const double mine = dots(i);
-                publish_row(i, row_slot());
+                publish_row(i);
                 double red = 0.0, dg = 0.0;
                 reduce(mine, i, red, dg);
                 if (warp == 0) {
@@ -257,13 +306,15 @@ __global__ void __launch_bounds__(WARPS * 32, 1) panel_col_kernel(RegQrArgs p) {
                 }
             } else {
                 const double wl = wls[lane];
+                const bool me = (lane == i);
 #pragma unroll
                 for (int q = 0; q < RPT; ++q) {
                     const double xi = __shfl_sync(0xffffffffu, x[q], i);
                     const int g = g0 + q;
-                    if (g > i) x[q] = fma(ca, xi, x[q]);
-                    else if (g == i) x[q] = (lane == i) ? 1.0 - ti : x[q] - wl;
-                    else if (lane == i) x[q] = 0.0;
+                    const double below = fma(ca, xi, x[q]);
+                    const double atrow = me ? 1.0 - ti : x[q] - wl;
+                    const double above = me ? 0.0 : x[q];
+                    x[q] = (g > i) ? below : ((g == i) ? atrow : above);
                 }
             }
             __syncthreads();  // cas/wls are rewritten by the next step
@@ -274,5 +325,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) panel_col_kernel(RegQrArgs p) {
             if (rr < nr && lane < kk) p.Q[(r0 + rr) + static_cast<i64>(lane) * p.ldq] = x[q];
         }
     }
-    if constexpr (CL) cg::this_cluster().sync();  // peers may still read this CTA's shared memory
+    if constexpr (CL) {
+        cg::this_cluster().sync();  // peers may still read this CTA's shared memory
+    }
 }

@@ -50,6 +50,15 @@ double* Ctx::scratch(std::size_t bytes) {
     return work;
 }
 
+unsigned long long* Ctx::qr_exchange() {
+    if (!qr_xchg) {
+        constexpr std::size_t words = kQrXchgWords;
+        TTR_CUDA(cudaMalloc(reinterpret_cast<void**>(&qr_xchg), words * sizeof(unsigned long long)));
+        TTR_CUDA(cudaMemsetAsync(qr_xchg, 0, words * sizeof(unsigned long long), stream));
+    }
+    return qr_xchg;
+}
+
 // ---------------------------------------------------------------------------
 // TT container
 TTDev::TTDev(Ctx& c, const std::vector<i64>& n_, const std::vector<i64>& r_) : ctx(&c), n(n_), r(r_) {
