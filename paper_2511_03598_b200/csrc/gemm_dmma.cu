@@ -293,6 +293,40 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32)
     }
 }
 
+// Many splits (the V^T A products of the blocked QR, the KRP sketch):
+// block = 32 consecutive elements x 8 warps; warp w sums splits w, w+8, ...
+// and the 8 partials are combined in fixed order -> deterministic.
+__global__ void __launch_bounds__(256) splitk_reduce_wide(const double* __restrict__ work, int S, int M, int N,
+                                                          double alpha, double beta, double* C, i64 ldc, double* Ct,
+                                                          i64 ldct) {
+    __shared__ double red[8][33];
+    const i64 total = static_cast<i64>(M) * N;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const i64 idx = static_cast<i64>(blockIdx.x) * 32 + lane;
+    double s0 = 0.0, s1 = 0.0;
+    if (idx < total) {
+        int z = warp;
+        for (; z + 8 < S; z += 16) {
+            s0 += work[static_cast<i64>(z) * total + idx];
+            s1 += work[static_cast<i64>(z + 8) * total + idx];
+        }
+        if (z < S) s0 += work[static_cast<i64>(z) * total + idx];
+    }
+    red[warp][lane] = s0 + s1;
+    __syncthreads();
+    if (warp == 0 && idx < total) {
+        double s = 0.0;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) s += red[w][lane];
+        const int m = static_cast<int>(idx % M), n = static_cast<int>(idx / M);
+        double v = alpha * s;
+        double* dst = C + m + static_cast<i64>(n) * ldc;
+        if (beta != 0.0) v = fma(beta, *dst, v);
+        *dst = v;
+        if (Ct) Ct[n + static_cast<i64>(m) * ldct] = v;
+    }
+}
+
 // C = alpha * sum_s work[s] + beta * C (split order fixed); optional C^T copy.
 __global__ void splitk_reduce(const double* __restrict__ work, int S, int M, int N, double alpha, double beta,
                               double* C, i64 ldc, double* Ct, i64 ldct) {
@@ -412,8 +446,15 @@ void run_gemm(Ctx& c, bool AT, int KM, int BK, GemmArgs& a, bool va2, bool vb2, 
     else throw Error(TTR_ERR_INTERNAL, "unsupported gemm configuration");
     if (splits > 1) {
         const i64 total = static_cast<i64>(a.M) * a.N;
-        const int blocks = static_cast<int>(std::min<i64>((total + 255) / 256, 4LL * c.sm_count));
-        splitk_reduce<<<blocks, 256, 0, c.stream>>>(a.work, splits, a.M, a.N, alpha, beta, C, ldc, Ct, ldct);
+        // choice by split count only: a column's bits must not depend on N
+        // (KRP append == one-shot)
+        if (splits >= 16) {
+            splitk_reduce_wide<<<static_cast<unsigned>((total + 31) / 32), 256, 0, c.stream>>>(
+                a.work, splits, a.M, a.N, alpha, beta, C, ldc, Ct, ldct);
+        } else {
+            const int blocks = static_cast<int>(std::min<i64>((total + 255) / 256, 4LL * c.sm_count));
+            splitk_reduce<<<blocks, 256, 0, c.stream>>>(a.work, splits, a.M, a.N, alpha, beta, C, ldc, Ct, ldct);
+        }
         TTR_CUDA(cudaGetLastError());
         c.launched();
     } else if (Ct) {
