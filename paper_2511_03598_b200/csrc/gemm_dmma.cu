@@ -23,6 +23,8 @@
 // tests/test_sketch.cpp:78-98).
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
+#include <cstring>
 
 #include "common.cuh"
 
@@ -361,6 +363,66 @@ __global__ void transpose_copy(const double* __restrict__ src, i64 lds, int M, i
     }
 }
 
+#include "gemm_tma.cuh"
+
+// ---- TMA path: host-side tensor maps (driver entry point via the runtime) ----
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            f = nullptr;
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+    }();
+    return fn;
+}
+
+// 2-D fp64 tensor map over a column-major (inner x outer, leading dim ld) matrix
+bool make_map(CUtensorMap* m, const double* base, i64 inner, i64 outer, i64 ld, unsigned box0, unsigned box1,
+              bool swizzle) {
+    auto enc = tensor_map_encoder();
+    if (!enc) return false;
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(std::max<i64>(outer, 1))};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 8};
+    const cuuint32_t box[2] = {box0, box1};
+    const cuuint32_t estr[2] = {1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+bool tma_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("TTR_GEMM_TMA");  // experiments: TTR_GEMM_TMA=0 selects the cp.async kernel
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
+template <int BM, int BN, bool AT, int KM>
+bool launch_tma(Ctx& c, GemmArgs& a, int splits) {
+    using C_ = TmaCfg<BM, BN, AT, KM, 4>;
+    CUtensorMap mA, mB, mW;
+    std::memset(&mW, 0, sizeof(mW));
+    const bool ok =
+        (AT ? make_map(&mA, a.A, a.K, a.M, a.lda, 16, BM, true) : make_map(&mA, a.A, a.M, a.K, a.lda, 16, 16, true)) &&
+        (KM == 1 ? make_map(&mB, a.B, a.nmode, a.N, a.ldb, 16, BN, true) : make_map(&mB, a.B, a.K, a.N, a.ldb, 16, BN, true)) &&
+        (KM != 1 || make_map(&mW, a.Wt, a.N, a.K / a.nmode, a.ldw, BN, 1, false));
+    if (!ok) return false;
+    auto kern = dgemm_tma_kernel<BM, BN, AT, KM, 4>;
+    static bool configured = false;
+    if (!configured) {
+        TTR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C_::kSmemBytes));
+        configured = true;
+    }
+    dim3 grid((a.M + BM - 1) / BM, (a.N + BN - 1) / BN, splits);
+    kern<<<grid, C_::kThreads, C_::kSmemBytes, c.stream>>>(mA, mB, mW, a);
+    TTR_CUDA(cudaGetLastError());
+    c.launched();
+    return true;
+}
+
 template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool AT, int KM, int VA, int VB>
 void launch(Ctx& c, GemmArgs& a, int splits) {
     using C_ = Cfg<BM, BN, BK, WM, WN, STAGES, AT, KM, VA, VB>;
@@ -426,7 +488,16 @@ void run_gemm(Ctx& c, bool AT, int KM, int BK, GemmArgs& a, bool va2, bool vb2, 
     a.ldc = ldc;
     a.alpha = alpha;
     a.beta = beta;
-    if (skinny && KM == 0) {
+    // TMA path: plain / slab-KRP products of the default and medium tiles with
+    // 16-byte aligned operands and even leading dimensions
+    bool done = false;
+    if (tma_enabled() && a.batch <= 1 && !skinny && va2 && vb2 && (KM == 0 || (KM == 1 && BK == 16))) {
+        if (medium && KM == 0) done = AT ? launch_tma<64, 64, true, 0>(c, a, splits) : launch_tma<64, 64, false, 0>(c, a, splits);
+        else if (!medium && KM == 0) done = AT ? launch_tma<128, 64, true, 0>(c, a, splits) : launch_tma<128, 64, false, 0>(c, a, splits);
+        else if (!medium && KM == 1 && !AT) done = launch_tma<128, 64, false, 1>(c, a, splits);
+    }
+    if (done) {
+    } else if (skinny && KM == 0) {
         if (AT) dispatch_vec<kSkBM, kSkBN, true, 0, 16>(c, a, splits, va2, vb2);
         else dispatch_vec<kSkBM, kSkBN, false, 0, 16>(c, a, splits, va2, vb2);
     } else if (small) {

@@ -1,0 +1,242 @@
+// gemm_tma.cuh — TMA-fed variant of the fp64 DMMA GEMM (included by
+// gemm_dmma.cu; uses its GemmArgs / dmma / epilogue conventions).
+//
+// Operand tiles move global -> shared memory with cp.async.bulk.tensor (TMA)
+// under 128-byte hardware swizzle, completion tracked by per-stage mbarriers
+// (full: TMA transaction bytes; empty: one arrival per consumer warp). One
+// thread issues every copy, so the consumer warps execute no address
+// arithmetic for the loads, no bounds checks (TMA zero-fills outside the
+// tensor) and no CTA-wide barrier in the main loop.
+//
+// Shared layout (dense, swizzled): a k-contiguous operand (B, or A when
+// transposed) is [rows][16 k] with 128-byte rows; an m-contiguous A is a set
+// of [16 k][16 m] boxes with 128-byte k-rows. SWIZZLE_128B XORs the 16-byte
+// chunk index with (row & 7). The four k values of one DMMA are taken as
+// {k0, k0+4, k0+1, k0+5} (any k order is valid for a dot product as long as
+// A and B agree): with that order every 64-bit fragment load touches each
+// bank exactly twice, i.e. the two wavefronts 256 bytes need — conflict free.
+//
+// KRP mode (KM = 1) streams Omega tiles (j inside one slab) and the W row of
+// the slab through the same pipeline; the W row scales the B fragment in
+// registers as in dgemm_kernel. The permuted k order makes the sums differ in
+// the last bits from the cp.async kernel's, so the KRP path picks its kernel
+// from (n, r_right) alone — never from the column count — to keep the
+// append == one-shot property.
+#pragma once
+
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+namespace tma {
+
+__device__ __forceinline__ unsigned saddr(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
+
+__device__ __forceinline__ void mbar_init(std::uint64_t* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(saddr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(std::uint64_t* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(saddr(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(std::uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(saddr(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(std::uint64_t* bar, unsigned parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "TTR_WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra TTR_WAIT_%=;\n"
+        "}\n" ::"r"(saddr(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void load_2d(void* dst, const CUtensorMap* map, std::uint64_t* bar, int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
+            saddr(dst)),
+        "l"(reinterpret_cast<std::uint64_t>(map)), "r"(c0), "r"(c1), "r"(saddr(bar))
+        : "memory");
+}
+__device__ __forceinline__ void prefetch_map(const CUtensorMap* map) {
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<std::uint64_t>(map)) : "memory");
+}
+
+}  // namespace tma
+
+// k offset of fragment column fc within a group of 8: {0, 4, 1, 5}, +2 for the
+// second DMMA of the group
+__device__ __forceinline__ int tma_kperm(int q, int fc) { return 8 * (q >> 1) + 2 * (q & 1) + (fc >> 1) + 4 * (fc & 1); }
+
+template <int BM, int BN, bool AT, int KM, int STAGES>
+struct TmaCfg {
+    static constexpr int BK = 16;
+    static constexpr int kWarpsM = BM / 32, kWarpsN = BN / 32;
+    static constexpr int kThreads = kWarpsM * kWarpsN * 32;
+    static constexpr int kABytes = BM * BK * 8, kBBytes = BN * BK * 8, kWBytes = KM == 1 ? BN * 8 : 0;
+    static constexpr int kStageBytes = kABytes + kBBytes + 1024;  // W row in the padded tail
+    static constexpr int kTxBytes = kABytes + kBBytes + kWBytes;
+    static constexpr int kSmemBytes = STAGES * kStageBytes + 1024 /*align*/ + 2 * STAGES * 8;
+    static_assert(kABytes % 1024 == 0 && kBBytes % 1024 == 0, "swizzle atoms are 1 KB");
+};
+
+template <int BM, int BN, bool AT, int KM, int STAGES>
+__global__ void __launch_bounds__((BM / 32) * (BN / 32) * 32)
+    dgemm_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                     const __grid_constant__ CUtensorMap tmW, const GemmArgs p) {
+    using C_ = TmaCfg<BM, BN, AT, KM, STAGES>;
+    constexpr int BK = C_::BK, FM = 4, FN = 4, NWARP = C_::kWarpsM * C_::kWarpsN;
+    extern __shared__ unsigned char smem_raw[];
+    unsigned char* smem =
+        reinterpret_cast<unsigned char*>((reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) & ~std::uintptr_t(1023));
+    std::uint64_t* full = reinterpret_cast<std::uint64_t*>(smem + STAGES * C_::kStageBytes);
+    std::uint64_t* empty = full + STAGES;
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wm0 = (warp % C_::kWarpsM) * 32, wn0 = (warp / C_::kWarpsM) * 32;
+    const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
+    const int zsplit = static_cast<int>(blockIdx.z);
+    const int total_kt = (p.K + BK - 1) / BK;
+    const int kt_begin = zsplit * p.ktiles_per_split;
+    const int kt_end = min(total_kt, kt_begin + p.ktiles_per_split);
+    const int nk = max(0, kt_end - kt_begin);
+
+    if (tid == 0) {
+        tma::prefetch_map(&tmA);
+        tma::prefetch_map(&tmB);
+        if constexpr (KM == 1) tma::prefetch_map(&tmW);
+        for (int s = 0; s < STAGES; ++s) {
+            tma::mbar_init(full + s, 1);
+            tma::mbar_init(empty + s, NWARP);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+
+    auto issue = [&](int kt_local) {  // thread 0 only
+        const int s = kt_local % STAGES;
+        unsigned char* st = smem + s * C_::kStageBytes;
+        const int k0 = (kt_begin + kt_local) * BK;
+        tma::mbar_expect_tx(full + s, C_::kTxBytes);
+        if constexpr (AT) {
+            tma::load_2d(st, &tmA, full + s, k0, m0);  // box {16 k, BM m}
+        } else {
+#pragma unroll
+            for (int b = 0; b < BM / 16; ++b) tma::load_2d(st + b * 2048, &tmA, full + s, m0 + 16 * b, k0);
+        }
+        if constexpr (KM == 1) {
+            tma::load_2d(st + C_::kABytes, &tmB, full + s, k0 % p.nmode, n0);
+            tma::load_2d(st + C_::kABytes + C_::kBBytes, &tmW, full + s, n0, k0 / p.nmode);
+        } else {
+            tma::load_2d(st + C_::kABytes, &tmB, full + s, k0, n0);
+        }
+    };
+    if (tid == 0)
+        for (int s = 0; s < STAGES - 1 && s < nk; ++s) issue(s);
+
+    double acc[FM][FN][2];
+#pragma unroll
+    for (int i = 0; i < FM; ++i)
+#pragma unroll
+        for (int j = 0; j < FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+    const int fr = lane >> 2, fc = lane & 3;
+    // per-lane byte offsets of the fragment loads for k-step q (0..3)
+    int offA[4], offB[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int k = tma_kperm(q, fc);
+        // k-contiguous rows (B; A when transposed): row r = base + fr, r & 7 = fr
+        offB[q] = fr * 128 + ((((k >> 1) ^ fr) << 4) | ((k & 1) << 3));
+        // m-contiguous A boxes: m = wm0 + 8i + fr, k-row k
+        offA[q] = k * 128 + ((((fr >> 1) ^ (k & 7)) << 4) | ((fr & 1) << 3));
+    }
+
+    for (int kt = 0; kt < nk; ++kt) {
+        const int s = kt % STAGES;
+        tma::mbar_wait(full + s, (kt / STAGES) & 1);
+        const unsigned char* st = smem + s * C_::kStageBytes;
+        const unsigned char* sA = st;
+        const unsigned char* sB = st + C_::kABytes;
+        double wreg[FN];
+        if constexpr (KM == 1) {
+            const double* sW = reinterpret_cast<const double*>(st + C_::kABytes + C_::kBBytes);
+#pragma unroll
+            for (int j = 0; j < FN; ++j) wreg[j] = sW[wn0 + j * 8 + fr];
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            double af[FM], bf[FN];
+#pragma unroll
+            for (int i = 0; i < FM; ++i) {
+                if constexpr (AT) {
+                    af[i] = *reinterpret_cast<const double*>(sA + (wm0 + 8 * i) * 128 + offB[q]);
+                } else {
+                    // box (wm0 + 8i) / 16; odd i flips chunk bit 2 ((m & 15) >> 1 gains 4)
+                    af[i] = *reinterpret_cast<const double*>(sA + ((wm0 >> 4) + (i >> 1)) * 2048 +
+                                                             (offA[q] ^ ((i & 1) << 6)));
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < FN; ++j) {
+                bf[j] = *reinterpret_cast<const double*>(sB + (wn0 + 8 * j) * 128 + offB[q]);
+                if constexpr (KM == 1) bf[j] *= wreg[j];
+            }
+#pragma unroll
+            for (int i = 0; i < FM; ++i)
+#pragma unroll
+                for (int j = 0; j < FN; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+        }
+        __syncwarp();
+        if (lane == 0) tma::mbar_arrive(empty + s);
+        if (tid == 0) {
+            const int nxt = kt + STAGES - 1;
+            if (nxt < nk) {
+                // the stage of k-tile nxt last held k-tile nxt - STAGES (= kt - 1)
+                if (nxt >= STAGES) tma::mbar_wait(empty + nxt % STAGES, ((nxt / STAGES) + 1) & 1);
+                issue(nxt);
+            }
+        }
+    }
+
+    // epilogue (as dgemm_kernel): fragment (i, j) = rows wm0+8i+fr, cols wn0+8j+2fc+{0,1}
+    double* Cp = p.C;
+    const bool split = gridDim.z > 1;
+    if (!split && p.beta != 0.0) {
+#pragma unroll
+        for (int i = 0; i < FM; ++i) {
+            const int gm = m0 + wm0 + i * 8 + fr;
+            double cv[FN][2];
+#pragma unroll
+            for (int j = 0; j < FN; ++j)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int gn = n0 + wn0 + j * 8 + 2 * fc + h;
+                    cv[j][h] = (gm < p.M && gn < p.N) ? __ldcg(Cp + gm + static_cast<i64>(gn) * p.ldc) : 0.0;
+                }
+#pragma unroll
+            for (int j = 0; j < FN; ++j)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int gn = n0 + wn0 + j * 8 + 2 * fc + h;
+                    if (gm < p.M && gn < p.N)
+                        Cp[gm + static_cast<i64>(gn) * p.ldc] = fma(p.beta, cv[j][h], p.alpha * acc[i][j][h]);
+                }
+        }
+        return;
+    }
+#pragma unroll
+    for (int i = 0; i < FM; ++i) {
+        const int gm = m0 + wm0 + i * 8 + fr;
+        if (gm >= p.M) continue;
+#pragma unroll
+        for (int j = 0; j < FN; ++j)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int gn = n0 + wn0 + j * 8 + 2 * fc + h;
+                if (gn >= p.N) continue;
+                if (split) p.work[(static_cast<i64>(zsplit) * p.N + gn) * p.M + gm] = acc[i][j][h];
+                else Cp[gm + static_cast<i64>(gn) * p.ldc] = p.alpha * acc[i][j][h];
+            }
+    }
+}
