@@ -17,8 +17,10 @@
 // bank exactly twice, i.e. the two wavefronts 256 bytes need — conflict free.
 //
 // KRP mode (KM = 1) streams Omega tiles (j inside one slab) and the W row of
-// the slab through the same pipeline; the W row scales the B fragment in
-// registers as in dgemm_kernel. The permuted k order makes the sums differ in
+// the slab through the same pipeline; the consumer warps scale the staged
+// Omega tile by the W row in shared memory once per CTA (one named barrier per
+// k-tile) — 4x fewer fp64 multiplies than scaling every B fragment, which
+// competes with DMMA for the fp64 pipe. The permuted k order makes the sums differ in
 // the last bits from the cp.async kernel's, so the KRP path picks its kernel
 // from (n, r_right) alone — never from the column count — to keep the
 // append == one-shot property.
@@ -58,6 +60,11 @@ __device__ __forceinline__ void load_2d(void* dst, const CUtensorMap* map, std::
         "l"(reinterpret_cast<std::uint64_t>(map)), "r"(c0), "r"(c1), "r"(saddr(bar))
         : "memory");
 }
+__device__ __forceinline__ double lds64(unsigned addr) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];\n" : "=d"(v) : "r"(addr));
+    return v;
+}
 __device__ __forceinline__ void prefetch_map(const CUtensorMap* map) {
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<std::uint64_t>(map)) : "memory");
 }
@@ -89,6 +96,7 @@ __global__ void __launch_bounds__((BM / 32) * (BN / 32) * 32)
     extern __shared__ unsigned char smem_raw[];
     unsigned char* smem =
         reinterpret_cast<unsigned char*>((reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) & ~std::uintptr_t(1023));
+    const unsigned smem_s = tma::saddr(smem);
     std::uint64_t* full = reinterpret_cast<std::uint64_t*>(smem + STAGES * C_::kStageBytes);
     std::uint64_t* empty = full + STAGES;
 
@@ -155,14 +163,24 @@ __global__ void __launch_bounds__((BM / 32) * (BN / 32) * 32)
     for (int kt = 0; kt < nk; ++kt) {
         const int s = kt % STAGES;
         tma::mbar_wait(full + s, (kt / STAGES) & 1);
-        const unsigned char* st = smem + s * C_::kStageBytes;
-        const unsigned char* sA = st;
-        const unsigned char* sB = st + C_::kABytes;
-        double wreg[FN];
+        // shared-space addresses (32-bit) so the fragment loads are LDS
+        const unsigned sA = smem_s + s * C_::kStageBytes;
+        const unsigned sB = sA + C_::kABytes;
         if constexpr (KM == 1) {
-            const double* sW = reinterpret_cast<const double*>(st + C_::kABytes + C_::kBBytes);
-#pragma unroll
-            for (int j = 0; j < FN; ++j) wreg[j] = sW[wn0 + j * 8 + fr];
+            // scale the Omega tile by the slab's W row once per CTA (each of
+            // the BN rows is one column n: 128 bytes, all multiplied by W(n))
+            // instead of once per consumer warp and fragment
+            constexpr int kRowsPerWarp = BN / NWARP;  // 8 (128x64) rows, 4 lanes x 32 B per row
+            static_assert(kRowsPerWarp * 4 == 32, "one 32-byte piece per lane");
+            const int n = warp * kRowsPerWarp + (lane >> 2);
+            const double wn = tma::lds64(sB + C_::kBBytes + n * 8);
+            const unsigned a = sB + n * 128 + (lane & 3) * 32;
+            double v0, v1, v2, v3;
+            asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n" : "=d"(v0), "=d"(v1) : "r"(a));
+            asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n" : "=d"(v2), "=d"(v3) : "r"(a + 16));
+            asm volatile("st.shared.v2.f64 [%0], {%1, %2};\n" ::"r"(a), "d"(v0 * wn), "d"(v1 * wn) : "memory");
+            asm volatile("st.shared.v2.f64 [%0], {%1, %2};\n" ::"r"(a + 16), "d"(v2 * wn), "d"(v3 * wn) : "memory");
+            asm volatile("bar.sync 1, %0;\n" ::"n"(C_::kThreads) : "memory");
         }
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
@@ -170,17 +188,15 @@ __global__ void __launch_bounds__((BM / 32) * (BN / 32) * 32)
 #pragma unroll
             for (int i = 0; i < FM; ++i) {
                 if constexpr (AT) {
-                    af[i] = *reinterpret_cast<const double*>(sA + (wm0 + 8 * i) * 128 + offB[q]);
+                    af[i] = tma::lds64(sA + (wm0 + 8 * i) * 128 + offB[q]);
                 } else {
                     // box (wm0 + 8i) / 16; odd i flips chunk bit 2 ((m & 15) >> 1 gains 4)
-                    af[i] = *reinterpret_cast<const double*>(sA + ((wm0 >> 4) + (i >> 1)) * 2048 +
-                                                             (offA[q] ^ ((i & 1) << 6)));
+                    af[i] = tma::lds64(sA + ((wm0 >> 4) + (i >> 1)) * 2048 + (offA[q] ^ ((i & 1) << 6)));
                 }
             }
 #pragma unroll
             for (int j = 0; j < FN; ++j) {
-                bf[j] = *reinterpret_cast<const double*>(sB + (wn0 + 8 * j) * 128 + offB[q]);
-                if constexpr (KM == 1) bf[j] *= wreg[j];
+                bf[j] = tma::lds64(sB + (wn0 + 8 * j) * 128 + offB[q]);
             }
 #pragma unroll
             for (int i = 0; i < FM; ++i)

@@ -54,6 +54,34 @@ float run_cfg(Ctx& c, GemmArgs a, int splits, int reps) {
     return ms / reps;
 }
 
+template <int BM, int BN, bool AT, int KM>
+float run_tma(Ctx& c, GemmArgs a, int splits, int reps) {
+    const int total_kt = (a.K + 15) / 16;
+    a.ktiles_per_split = (total_kt + splits - 1) / splits;
+    splits = (total_kt + a.ktiles_per_split - 1) / a.ktiles_per_split;
+    if (splits > 1) a.work = c.scratch(static_cast<std::size_t>(splits) * a.M * a.N * 8);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    for (int w = 0; w < 2; ++w) launch_tma<BM, BN, AT, KM>(c, a, splits);
+    cudaEventRecord(e0, c.stream);
+    for (int r = 0; r < reps; ++r) {
+        launch_tma<BM, BN, AT, KM>(c, a, splits);
+        if (splits > 1) {
+            const i64 total = static_cast<i64>(a.M) * a.N;
+            splitk_reduce_wide<<<(total + 31) / 32, 256, 0, c.stream>>>(a.work, splits, a.M, a.N, 1.0, 0.0, a.C, a.ldc,
+                                                                       nullptr, 0);
+        }
+    }
+    cudaEventRecord(e1, c.stream);
+    cudaEventSynchronize(e1);
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaError_t err = cudaGetLastError();
+    if (err != cudaSuccess) std::printf("  error %s\n", cudaGetErrorString(err));
+    return ms / reps;
+}
+
 int main() {
     Ctx c;
     c.stream = 0;
@@ -71,7 +99,10 @@ int main() {
 
     struct Shape { const char* name; int M, N, K; bool at; int km; int splits; };
     std::vector<Shape> shapes = {
-        {"sketch 1000x320x128000 (KRP)", 1000, 320, 128000, false, 1, 37},
+        {"sketch 1000x320x128000 (KRP) s74", 1000, 320, 128000, false, 1, 74},
+        {"sketch 1000x320x128000 (KRP) s37", 1000, 320, 128000, false, 1, 37},
+        {"sketch 1000x320x128000 (KRP) s19", 1000, 320, 128000, false, 1, 19},
+        {"plain 1000x320x128000 s37", 1000, 320, 128000, false, 0, 37},
         {"S=V*W 40960x320x1000", 40960, 320, 1000, false, 0, 1},
         {"M=Q^T V 320x1000x40960", 320, 1000, 40960, true, 0, 8},
         {"next=M*H 320x128000x1000", 320, 128000, 1000, false, 0, 1},
@@ -94,14 +125,20 @@ int main() {
             std::printf("  %3dx%-3d bk%-2d w%dx%d st%d : %8.3f ms %6.2f TF/s\n", BM, BN, BK, WM, WN, ST, ms, \
                         gf / ms);                                                                        \
         }
+        {
+            float ms;
+            if (s.km == 1) ms = run_tma<128, 64, false, 1>(c, a, s.splits, 5);
+            else if (s.at) ms = run_tma<128, 64, true, 0>(c, a, s.splits, 5);
+            else ms = run_tma<128, 64, false, 0>(c, a, s.splits, 5);
+            std::printf("  TMA 128x64        : %8.3f ms %6.2f TF/s\n", ms, gf / ms);
+            if (s.km == 0) {
+                ms = s.at ? run_tma<64, 64, true, 0>(c, a, s.splits, 5) : run_tma<64, 64, false, 0>(c, a, s.splits, 5);
+                std::printf("  TMA 64x64         : %8.3f ms %6.2f TF/s\n", ms, gf / ms);
+            }
+        }
         RUN(128, 64, 16, 32, 32, 4)
-        RUN(128, 64, 16, 32, 32, 3)
         RUN(64, 64, 16, 32, 32, 4)
         RUN(64, 64, 16, 32, 32, 3)
-        RUN(160, 64, 16, 32, 32, 3)
-        RUN(160, 64, 16, 32, 32, 4)
-        RUN(96, 64, 16, 32, 32, 4)
-        RUN(64, 32, 16, 32, 32, 4)
     }
     return 0;
 }
