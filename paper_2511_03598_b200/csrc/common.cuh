@@ -191,7 +191,9 @@ void thin_qr(Ctx& c, i64 m, i64 n, const double* A, i64 lda, double* Q, i64 ldq,
 // Thin SVD of a small m x n matrix (m, n <= ~1024) by one-sided Jacobi on the
 // device: U (m x k), s (k, descending), V (n x k), k = min(m, n). Host copies of
 // s are returned (needed for truncation decisions).
-void svd_small(Ctx& c, i64 m, i64 n, const double* A, i64 lda, double* U, i64 ldu, double* V, i64 ldv,
-               std::vector<double>& s_host, double* d_s);
+// Left singular vectors U (m x min(m,n), sorted descending) and singular
+// values of A; Sigma V^T is U^T A (svd.cu).
+void svd_left(Ctx& c, i64 m, i64 n, const double* A, i64 lda, double* U, i64 ldu, std::vector<double>& s_host,
+              double* d_s);
 
 }  // namespace ttr

@@ -49,21 +49,18 @@ std::unique_ptr<TTDev> compress_sweep(Ctx& c, const TTDev& right_orth, bool tol_
     DBuf Q(c, static_cast<std::size_t>(max_core));
     DBuf R(c, static_cast<std::size_t>(maxr * maxr));
     DBuf U(c, static_cast<std::size_t>(maxr * maxr));
-    DBuf Vs(c, static_cast<std::size_t>(maxr * maxr));
     DBuf SV(c, static_cast<std::size_t>(maxr * maxr));
-    DBuf ds(c, static_cast<std::size_t>(maxr));
     std::vector<double> s;
     for (i64 k = 0; k + 1 < d; ++k) {
         const i64 rl = r[k], rows = rl * n[k], rr = r[k + 1], kk = std::min(rows, rr);
         thin_qr(c, rows, rr, cur.p, rows, Q.p, rows, R.p, kk);
-        svd_small(c, kk, rr, R.p, kk, U.p, kk, Vs.p, rr, s, ds.p);
+        svd_left(c, kk, rr, R.p, kk, U.p, kk, s, nullptr);
         const i64 keep = truncation_rank(s, kk, rr, tol_rule, tau, ranks ? (*ranks)[k] : 0);
         // core k = Q U(:, 1:keep)
         cores[k] = DBuf(c, static_cast<std::size_t>(rows * keep));
         gemm(c, false, rows, keep, kk, 1.0, Q.p, rows, U.p, kk, 0.0, cores[k].p, rows);
-        // SV = diag(s) V^T (keep x rr); next core = SV H(core_{k+1})
-        transpose(c, rr, keep, Vs.p, rr, SV.p, keep);
-        scale_rows_cols(c, SV.p, keep, rr, keep, ds.p, nullptr);
+        // SV = diag(s) V^T (keep x rr) = U(:, 1:keep)^T R; next core = SV H(core_{k+1})
+        gemm(c, true, keep, rr, kk, 1.0, U.p, kk, R.p, kk, 0.0, SV.p, keep);
         const i64 ncols = n[k + 1] * r[k + 2];
         gemm(c, false, keep, ncols, rr, 1.0, SV.p, keep, right_orth.core(k + 1), rr, 0.0, cur.p, keep);
         r[k + 1] = keep;
