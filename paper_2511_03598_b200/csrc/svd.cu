@@ -77,7 +77,8 @@ __device__ __forceinline__ bool jacobi_rotate(double* ap, double* aq, int M, int
         ga = fma(x, y, ga);
     }
     warp_sum3(al, be, ga);
-    if (ga == 0.0 || fabs(ga) <= DBL_EPSILON * sqrt(al * be)) return false;
+    // convergence threshold of LAPACK dgesvj: sqrt(M) * eps relative to the pair
+    if (ga == 0.0 || fabs(ga) <= sqrt(static_cast<double>(M)) * DBL_EPSILON * sqrt(al * be)) return false;
     const double zeta = (be - al) / (2.0 * ga);
     const double t = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
     const double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
@@ -357,22 +358,25 @@ void svd_left(Ctx& c, i64 m, i64 n, const double* A_in, i64 lda_in, double* U, i
               double* d_s) {
     const i64 k = std::min(m, n);
     c.charge_svd(14ULL * m * n * k + 8ULL * k * k * k);
-    // wide: the triangle L (m x m) of A = L Q' has A's singular values and left vectors
+    // wide A: A = L Q' with L = R'^T from the QR of A^T (m x m lower
+    // triangular) has A's singular values and left vectors. (As a QR
+    // preconditioner for square inputs, without column pivoting, it did not
+    // reduce the sweep count measurably: tools/det_trace.py.)
     DBuf L;
     const double* src = A_in;
     i64 lds = lda_in, N = n;
     if (m < n) {
         DBuf At(c, static_cast<std::size_t>(n * m));
         transpose(c, m, n, A_in, lda_in, At.p, n);
-        L = DBuf(c, static_cast<std::size_t>(m * m));
-        DBuf Rt(c, static_cast<std::size_t>(m * m));
+        L = DBuf(c, static_cast<std::size_t>(m * k));
+        DBuf Rt(c, static_cast<std::size_t>(k * m));
         const std::uint64_t saved = c.counts.qr;
-        thin_qr(c, n, m, At.p, n, nullptr, 1, Rt.p, m);  // A^T = Q' R'  ->  A = R'^T Q'^T
+        thin_qr(c, n, m, At.p, n, nullptr, 1, Rt.p, k);  // A^T = Q' R' (R' k x m)  ->  A = R'^T Q'^T
         c.counts.qr = saved;                              // charged as part of the SVD
-        transpose(c, m, m, Rt.p, m, L.p, m);
+        transpose(c, k, m, Rt.p, k, L.p, m);
         src = L.p;
         lds = m;
-        N = m;
+        N = k;
     }
     DBuf A(c, static_cast<std::size_t>(m * N));
     copy_matrix(c, m, N, src, lds, A.p, m);
