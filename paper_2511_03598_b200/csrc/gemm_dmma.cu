@@ -400,9 +400,9 @@ bool tma_enabled() {
     return on;
 }
 
-template <int BM, int BN, bool AT, int KM>
+template <int BM, int BN, bool AT, int KM, int ST = 4>
 bool launch_tma(Ctx& c, GemmArgs& a, int splits) {
-    using C_ = TmaCfg<BM, BN, AT, KM, 4>;
+    using C_ = TmaCfg<BM, BN, AT, KM, ST>;
     CUtensorMap mA, mB, mW;
     std::memset(&mW, 0, sizeof(mW));
     const bool ok =
@@ -410,7 +410,7 @@ bool launch_tma(Ctx& c, GemmArgs& a, int splits) {
         (KM == 1 ? make_map(&mB, a.B, a.nmode, a.N, a.ldb, 16, BN, true) : make_map(&mB, a.B, a.K, a.N, a.ldb, 16, BN, true)) &&
         (KM != 1 || make_map(&mW, a.Wt, a.N, a.K / a.nmode, a.ldw, BN, 1, false));
     if (!ok) return false;
-    auto kern = dgemm_tma_kernel<BM, BN, AT, KM, 4>;
+    auto kern = dgemm_tma_kernel<BM, BN, AT, KM, ST>;
     static bool configured = false;
     if (!configured) {
         TTR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C_::kSmemBytes));
@@ -491,9 +491,15 @@ void run_gemm(Ctx& c, bool AT, int KM, int BK, GemmArgs& a, bool va2, bool vb2, 
     // TMA path: plain / slab-KRP products of the default and medium tiles with
     // 16-byte aligned operands and even leading dimensions
     bool done = false;
-    if (tma_enabled() && a.batch <= 1 && !skinny && va2 && vb2 && (KM == 0 || (KM == 1 && BK == 16))) {
-        if (medium && KM == 0) done = AT ? launch_tma<64, 64, true, 0>(c, a, splits) : launch_tma<64, 64, false, 0>(c, a, splits);
-        else if (!medium && KM == 0) done = AT ? launch_tma<128, 64, true, 0>(c, a, splits) : launch_tma<128, 64, false, 0>(c, a, splits);
+    if (tma_enabled() && a.batch <= 1 && va2 && vb2 && (KM == 0 || (KM == 1 && BK == 16))) {
+        // (tools/gemm_tune.cu) skinny M <= 32: 32x64 tiles; short K (<= 64,
+        // the blocked-QR updates, memory-bound): 64x64 tiles, 2 stages, 4 CTAs/SM
+        const bool short_k = a.K <= 64;
+        if (skinny && KM == 0) done = AT ? launch_tma<32, 64, true, 0>(c, a, splits) : launch_tma<32, 64, false, 0>(c, a, splits);
+        else if ((medium || short_k) && KM == 0 && short_k)
+            done = AT ? launch_tma<64, 64, true, 0, 2>(c, a, splits) : launch_tma<64, 64, false, 0, 2>(c, a, splits);
+        else if (medium && KM == 0) done = AT ? launch_tma<64, 64, true, 0>(c, a, splits) : launch_tma<64, 64, false, 0>(c, a, splits);
+        else if (KM == 0) done = AT ? launch_tma<128, 64, true, 0>(c, a, splits) : launch_tma<128, 64, false, 0>(c, a, splits);
         else if (!medium && KM == 1 && !AT) done = launch_tma<128, 64, false, 1>(c, a, splits);
     }
     if (done) {
@@ -564,7 +570,9 @@ void gemm(Ctx& c, bool trans_a, i64 M, i64 N, i64 K, double alpha, const double*
     // 64 x 64 tiles when 128-row tiles would pad M noticeably (M = 320: 384)
     const i64 pad128 = (M + kBM - 1) / kBM * kBM, pad64 = (M + kMdBM - 1) / kMdBM * kMdBM;
     const bool medium = !skinny && pad128 * 20 > pad64 * 21;
-    const i64 bm = skinny ? kSkBM : (medium ? kMdBM : kBM), bn = skinny ? kSkBN : (medium ? kMdBN : kBN);
+    const bool tma_tiles = tma_enabled() && aligned16(A) && (lda % 2 == 0) && aligned16(B) && (ldb % 2 == 0);
+    const i64 bm = skinny ? kSkBM : ((medium || (tma_tiles && K <= 64)) ? kMdBM : kBM);
+    const i64 bn = skinny ? (tma_tiles ? 64 : kSkBN) : ((medium || (tma_tiles && K <= 64)) ? kMdBN : kBN);
     const i64 tiles = ((M + bm - 1) / bm) * ((N + bn - 1) / bn);
     const int total_kt = static_cast<int>((K + 15) / 16);
     const int splits = choose_splits(c, tiles, total_kt);

@@ -54,7 +54,7 @@ float run_cfg(Ctx& c, GemmArgs a, int splits, int reps) {
     return ms / reps;
 }
 
-template <int BM, int BN, bool AT, int KM>
+template <int BM, int BN, bool AT, int KM, int ST = 4>
 float run_tma(Ctx& c, GemmArgs a, int splits, int reps) {
     const int total_kt = (a.K + 15) / 16;
     a.ktiles_per_split = (total_kt + splits - 1) / splits;
@@ -63,10 +63,10 @@ float run_tma(Ctx& c, GemmArgs a, int splits, int reps) {
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
-    for (int w = 0; w < 2; ++w) launch_tma<BM, BN, AT, KM>(c, a, splits);
+    for (int w = 0; w < 2; ++w) launch_tma<BM, BN, AT, KM, ST>(c, a, splits);
     cudaEventRecord(e0, c.stream);
     for (int r = 0; r < reps; ++r) {
-        launch_tma<BM, BN, AT, KM>(c, a, splits);
+        launch_tma<BM, BN, AT, KM, ST>(c, a, splits);
         if (splits > 1) {
             const i64 total = static_cast<i64>(a.M) * a.N;
             splitk_reduce_wide<<<(total + 31) / 32, 256, 0, c.stream>>>(a.work, splits, a.M, a.N, 1.0, 0.0, a.C, a.ldc,
@@ -131,6 +131,10 @@ int main() {
             else if (s.at) ms = run_tma<128, 64, true, 0>(c, a, s.splits, 5);
             else ms = run_tma<128, 64, false, 0>(c, a, s.splits, 5);
             std::printf("  TMA 128x64        : %8.3f ms %6.2f TF/s\n", ms, gf / ms);
+            if (s.km == 1) ms = run_tma<128, 64, false, 1, 6>(c, a, s.splits, 5);
+            else if (s.at) ms = run_tma<128, 64, true, 0, 6>(c, a, s.splits, 5);
+            else ms = run_tma<128, 64, false, 0, 6>(c, a, s.splits, 5);
+            std::printf("  TMA 128x64 st6    : %8.3f ms %6.2f TF/s\n", ms, gf / ms);
             if (s.km == 0) {
                 ms = s.at ? run_tma<64, 64, true, 0>(c, a, s.splits, 5) : run_tma<64, 64, false, 0>(c, a, s.splits, 5);
                 std::printf("  TMA 64x64         : %8.3f ms %6.2f TF/s\n", ms, gf / ms);
@@ -139,6 +143,37 @@ int main() {
         RUN(128, 64, 16, 32, 32, 4)
         RUN(64, 64, 16, 32, 32, 4)
         RUN(64, 64, 16, 32, 32, 3)
+    }
+    // ---- blocked-QR shapes (memory-bound): trailing update and V^T A ----
+    {
+        GemmArgs a{};
+        a.M = 40960; a.N = 288; a.K = 32;
+        a.A = A; a.lda = 40960; a.B = B; a.ldb = 32; a.C = Cm; a.ldc = 40960; a.alpha = -1.0; a.beta = 1.0;
+        const double gb = (2.0 * 40960 * 288 + 40960 * 32) * 8 / 1e9;
+        std::printf("update A -= V W2 40960x288x32 beta=1 (%.0f MB min traffic)\n", gb * 1e3);
+        auto pr = [&](const char* nm, float ms) { std::printf("  %-22s: %8.4f ms %7.0f GB/s\n", nm, ms, gb / ms * 1e3); };
+        pr("TMA 128x64 st4", run_tma<128, 64, false, 0, 4>(c, a, 1, 10));
+        pr("TMA 128x64 st2", run_tma<128, 64, false, 0, 2>(c, a, 1, 10));
+        pr("TMA 64x64 st2", run_tma<64, 64, false, 0, 2>(c, a, 1, 10));
+        pr("TMA 64x64 st4", run_tma<64, 64, false, 0, 4>(c, a, 1, 10));
+        pr("cp.async 128x64", run_cfg<128, 64, 16, 32, 32, 4, false, 0>(c, a, 1, 10));
+    }
+    {
+        GemmArgs a{};
+        a.M = 32; a.N = 288; a.K = 40960;
+        a.A = A; a.lda = 40960; a.B = B; a.ldb = 40960; a.C = Cm; a.ldc = 32; a.alpha = 1.0; a.beta = 0.0;
+        const double gb = (40960.0 * 288 + 40960 * 32) * 8 / 1e9;
+        std::printf("V^T A 32x288x40960 (%.0f MB min traffic)\n", gb * 1e3);
+        auto pr = [&](const char* nm, float ms) { std::printf("  %-22s: %8.4f ms %7.0f GB/s\n", nm, ms, gb / ms * 1e3); };
+        for (int sp : {142, 74, 37}) {
+            char nm[64];
+            std::snprintf(nm, sizeof nm, "cp.async 32x128 s%d", sp);
+            pr(nm, run_cfg<32, 128, 16, 32, 32, 4, true, 0>(c, a, sp, 10));
+            std::snprintf(nm, sizeof nm, "TMA 32x128 s%d", sp);
+            pr(nm, run_tma<32, 128, true, 0, 4>(c, a, sp, 10));
+            std::snprintf(nm, sizeof nm, "TMA 32x64 s%d", sp);
+            pr(nm, run_tma<32, 64, true, 0, 4>(c, a, sp, 10));
+        }
     }
     return 0;
 }
