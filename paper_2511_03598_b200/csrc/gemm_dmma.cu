@@ -465,8 +465,8 @@ bool aligned16(const void* p) { return (reinterpret_cast<std::uintptr_t>(p) & 15
 
 // Grid shaping: enough CTAs to cover 2 waves of 148 SMs when the MxN tile
 // grid alone does not.
-int choose_splits(Ctx& c, i64 tiles, int total_kt) {
-    const i64 target = 2LL * c.sm_count;
+int choose_splits(Ctx& c, i64 tiles, int total_kt, int ctas_per_sm = 2) {
+    const i64 target = static_cast<i64>(ctas_per_sm) * c.sm_count;
     if (tiles >= target || total_kt < 8) return 1;
     i64 s = (target + tiles - 1) / tiles;
     s = std::min<i64>(s, std::max(1, total_kt / 4));
@@ -575,7 +575,9 @@ void gemm(Ctx& c, bool trans_a, i64 M, i64 N, i64 K, double alpha, const double*
     const i64 bn = skinny ? (tma_tiles ? 64 : kSkBN) : ((medium || (tma_tiles && K <= 64)) ? kMdBN : kBN);
     const i64 tiles = ((M + bm - 1) / bm) * ((N + bn - 1) / bn);
     const int total_kt = static_cast<int>((K + 15) / 16);
-    const int splits = choose_splits(c, tiles, total_kt);
+    // resident CTAs per SM grow as the tile (warp count) shrinks
+    const int per_sm = (bm * bn >= 128 * 64) ? 2 : (bm * bn >= 64 * 64 ? 4 : 8);
+    const int splits = choose_splits(c, tiles, total_kt, tma_tiles ? per_sm : 2);
     run_gemm(c, trans_a, 0, 16, a, va2, vb2, splits, C, ldc, alpha, beta, nullptr, 0, skinny, 0, medium);
 }
 

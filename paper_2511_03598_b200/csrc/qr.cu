@@ -299,6 +299,62 @@ __global__ void copy_upper(int k, int n, const double* A, i64 lda, double* R, i6
     }
 }
 
+// Aggregated compact-WY factor of all panels: T = U^{-1}, U = diag(1/tau) +
+// striu(V^T V), by block back substitution with the panel factors T_i
+// (= U_ii^{-1}, zero rows/columns for tau = 0): X_jj = T_j,
+// X_ij = -T_i sum_{l=i+1..j} G_il X_lj. One CTA per block column j; the
+// column X(:, j-block) stays in shared memory. k x k in/out, ld k, blocks of 32
+// (zero padded past k).
+constexpr int kTaggThreads = 256;
+__global__ void __launch_bounds__(kTaggThreads) t_aggregate_kernel(int k, const double* __restrict__ G,
+                                                                   const double* __restrict__ Ts, double* T) {
+    extern __shared__ double xs[];  // X(:, j-block): [nb * 32][32]; then G row block [(nb-1)*32][33]
+    __shared__ double acc_s[32 * 33];
+    __shared__ double ti_s[32 * 33];
+    const int j = blockIdx.x, nb = (k + 31) / 32, tid = threadIdx.x;
+    double* gs = xs + static_cast<i64>(nb) * 32 * 32;
+    const int r = tid & 31, c0 = tid >> 5;  // thread owns (r, c0 + 8q), q = 0..3
+    // X_jj = T_j
+    for (int q = 0; q < 4; ++q) xs[(j * 32 + r) * 32 + c0 + 8 * q] = Ts[static_cast<i64>(j) * 1024 + r + (c0 + 8 * q) * 32];
+    for (int i = j - 1; i >= 0; --i) {
+        // stage G(i-block, (i+1)..j blocks) (coalesced: 32 rows of one column per warp) and T_i
+        const int ncols = (j - i) * 32;
+        for (int e = tid; e < ncols * 32; e += kTaggThreads) {
+            const int rr = e & 31, cc = e >> 5, row = i * 32 + rr, col = (i + 1) * 32 + cc;
+            gs[cc * 33 + rr] = (row < k && col < k) ? G[row + static_cast<i64>(col) * k] : 0.0;
+        }
+        for (int e = tid; e < 1024; e += kTaggThreads) ti_s[(e & 31) * 33 + (e >> 5)] = Ts[static_cast<i64>(i) * 1024 + e];
+        __syncthreads();
+        double a[4] = {0.0, 0.0, 0.0, 0.0};
+        for (int t = 0; t < ncols; ++t) {
+            const double g = gs[t * 33 + r];
+            const double* xr = xs + ((i + 1) * 32 + t) * 32 + c0;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) a[q] = fma(g, xr[8 * q], a[q]);
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc_s[r * 33 + c0 + 8 * q] = a[q];
+        __syncthreads();
+        double x[4] = {0.0, 0.0, 0.0, 0.0};
+        for (int t = 0; t < 32; ++t) {
+            const double tv = ti_s[r * 33 + t];  // T_i(r, t)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) x[q] = fma(tv, acc_s[t * 33 + c0 + 8 * q], x[q]);
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) xs[(i * 32 + r) * 32 + c0 + 8 * q] = -x[q];
+        __syncthreads();
+    }
+    __syncthreads();
+    // write column block j (rows below the diagonal block are zero)
+    for (int e = tid; e < k * 32; e += kTaggThreads) {
+        const int row = e % k, cc = e / k, col = j * 32 + cc;
+        if (col >= k) continue;
+        const int bi = row / 32;
+        T[row + static_cast<i64>(col) * k] = bi <= j ? xs[(bi * 32 + row % 32) * 32 + cc] : 0.0;
+    }
+}
+
 int blocks_for(Ctx& c, i64 work) {
     return static_cast<int>(std::max<i64>(1, std::min<i64>((work + 255) / 256, 4LL * c.sm_count)));
 }
@@ -384,6 +440,7 @@ void thin_qr(Ctx& c, i64 m, i64 n, const double* A, i64 lda, double* Q, i64 ldq,
     const i64 npanels = (k + kPanel - 1) / kPanel;
     DBuf tau(c, static_cast<std::size_t>(k));
     DBuf Vall(c, static_cast<std::size_t>(ldw * k));  // explicit V of every panel (rows j0.. of column block)
+    if (Q) TTR_CUDA(cudaMemsetAsync(Vall.p, 0, sizeof(double) * ldw * k, c.stream));  // zeros above each panel
     DBuf Ts(c, static_cast<std::size_t>(npanels * kPanel * kPanel));
     DBuf Wb(c, static_cast<std::size_t>(kPanel * std::max<i64>(n, 1)));
     DBuf Wb2(c, static_cast<std::size_t>(kPanel * std::max<i64>(n, 1)));
@@ -418,7 +475,34 @@ void thin_qr(Ctx& c, i64 m, i64 n, const double* A, i64 lda, double* Q, i64 ldq,
         c.launched();
     }
     if (Q == nullptr) return;
-    // explicit Q = H_0 ... H_{k-1} [I_k; 0], panels applied last to first
+    // explicit Q = H_0 ... H_{k-1} [I_k; 0] = [I_k; 0] - V T V_1^T with the
+    // aggregated T of all panels (V_1 = top k x k block of V): two full-size
+    // GEMMs (V^T V and V Y) instead of three skinny ones per panel
+    if (k <= 384) {
+        DBuf Gm(c, static_cast<std::size_t>(k * k));
+        DBuf Tf(c, static_cast<std::size_t>(k * k));
+        DBuf V1t(c, static_cast<std::size_t>(k * k));
+        DBuf Y(c, static_cast<std::size_t>(k * k));
+        gemm(c, true, k, k, m, 1.0, Vall.p, ldw, Vall.p, ldw, 0.0, Gm.p, k, false);  // G = V^T V
+        const std::size_t smem = (static_cast<std::size_t>(npanels) * 32 * 32 + (npanels - 1) * 32 * 33) * sizeof(double);
+        static bool configured = false;
+        if (!configured) {
+            TTR_CUDA(cudaFuncSetAttribute(t_aggregate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+            configured = true;
+        }
+        t_aggregate_kernel<<<static_cast<unsigned>(npanels), kTaggThreads, smem, c.stream>>>(static_cast<int>(k), Gm.p,
+                                                                                             Ts.p, Tf.p);
+        TTR_CUDA(cudaGetLastError());
+        c.launched();
+        transpose(c, k, k, Vall.p, ldw, V1t.p, k);                                        // V_1^T
+        gemm(c, false, k, k, k, 1.0, Tf.p, k, V1t.p, k, 0.0, Y.p, k, false);              // Y = T V_1^T
+        init_thin_identity<<<blocks_for(c, m * k), 256, 0, c.stream>>>(static_cast<int>(m), static_cast<int>(k), Q, ldq);
+        TTR_CUDA(cudaGetLastError());
+        c.launched();
+        gemm(c, false, m, k, k, -1.0, Vall.p, ldw, Y.p, k, 1.0, Q, ldq, false);           // Q = [I;0] - V Y
+        return;
+    }
+    // very wide: panels applied last to first (backward accumulation)
     init_thin_identity<<<blocks_for(c, m * k), 256, 0, c.stream>>>(static_cast<int>(m), static_cast<int>(k), Q, ldq);
     TTR_CUDA(cudaGetLastError());
     c.launched();
