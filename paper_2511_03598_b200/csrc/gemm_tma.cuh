@@ -11,10 +11,9 @@
 // Shared layout (dense, swizzled): a k-contiguous operand (B, or A when
 // transposed) is [rows][16 k] with 128-byte rows; an m-contiguous A is a set
 // of [16 k][16 m] boxes with 128-byte k-rows. SWIZZLE_128B XORs the 16-byte
-// chunk index with (row & 7). The four k values of one DMMA are taken as
-// {k0, k0+4, k0+1, k0+5} (any k order is valid for a dot product as long as
-// A and B agree): with that order every 64-bit fragment load touches each
-// bank exactly twice, i.e. the two wavefronts 256 bytes need — conflict free.
+// chunk index with (row & 7). The four k values of one DMMA are a permuted
+// set (tma_kperm; any k order is valid for a dot product as long as A and B
+// agree) chosen so that every 64-bit fragment load is conflict free.
 //
 // KRP mode (KM = 1) streams Omega tiles (j inside one slab) and the W row of
 // the slab through the same pipeline; the consumer warps scale the staged
@@ -71,9 +70,17 @@ __device__ __forceinline__ void prefetch_map(const CUtensorMap* map) {
 
 }  // namespace tma
 
-// k offset of fragment column fc within a group of 8: {0, 4, 1, 5}, +2 for the
-// second DMMA of the group
-__device__ __forceinline__ int tma_kperm(int q, int fc) { return 8 * (q >> 1) + 2 * (q & 1) + (fc >> 1) + 4 * (fc & 1); }
+// k of fragment column fc in DMMA q of a 16-k tile. 64-bit shared loads are
+// served per half-warp (16 lanes = 4 fragment rows x 4 k); with 128-byte
+// swizzle (chunk ^= row & 7) these sets put the 16 lanes of every half-warp on
+// 16 distinct 8-byte bank slots both for k-contiguous rows (B, transposed A:
+// even and odd k pairs whose chunk indices differ in bit 2) and for
+// m-contiguous k-rows (A: distinct (k & 7) >> 1) — conflict free:
+//   q0 {0,10,5,15}  q1 {2,8,7,13}  q2 {4,14,1,11}  q3 {6,12,3,9}
+__device__ __forceinline__ int tma_kperm(int q, int fc) {
+    constexpr unsigned long long kTab = 0x93C6B1E4D7825AF0ull;  // nibble (4q + fc)
+    return static_cast<int>((kTab >> (4 * (4 * q + fc))) & 0xF);
+}
 
 template <int BM, int BN, bool AT, int KM, int STAGES>
 struct TmaCfg {
@@ -170,16 +177,19 @@ __global__ void __launch_bounds__((BM / 32) * (BN / 32) * 32)
             // scale the Omega tile by the slab's W row once per CTA (each of
             // the BN rows is one column n: 128 bytes, all multiplied by W(n))
             // instead of once per consumer warp and fragment
-            constexpr int kRowsPerWarp = BN / NWARP;  // 8 (128x64) rows, 4 lanes x 32 B per row
-            static_assert(kRowsPerWarp * 4 == 32, "one 32-byte piece per lane");
-            const int n = warp * kRowsPerWarp + (lane >> 2);
-            const double wn = tma::lds64(sB + C_::kBBytes + n * 8);
-            const unsigned a = sB + n * 128 + (lane & 3) * 32;
+            // lane: 16-byte chunk (lane & 7) of rows n and n + 4 — each quarter-warp
+            // covers one whole 128-byte row (conflict-free 128-bit accesses)
+            constexpr int kRowsPerWarp = BN / NWARP;  // 8 (128x64)
+            static_assert(kRowsPerWarp == 8, "two rows of 8 chunks per lane group");
+            const int n = warp * kRowsPerWarp + (lane >> 3);
+            const double w0 = tma::lds64(sB + C_::kBBytes + n * 8);
+            const double w1 = tma::lds64(sB + C_::kBBytes + (n + 4) * 8);
+            const unsigned a = sB + n * 128 + (lane & 7) * 16;
             double v0, v1, v2, v3;
             asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n" : "=d"(v0), "=d"(v1) : "r"(a));
-            asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n" : "=d"(v2), "=d"(v3) : "r"(a + 16));
-            asm volatile("st.shared.v2.f64 [%0], {%1, %2};\n" ::"r"(a), "d"(v0 * wn), "d"(v1 * wn) : "memory");
-            asm volatile("st.shared.v2.f64 [%0], {%1, %2};\n" ::"r"(a + 16), "d"(v2 * wn), "d"(v3 * wn) : "memory");
+            asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n" : "=d"(v2), "=d"(v3) : "r"(a + 512));
+            asm volatile("st.shared.v2.f64 [%0], {%1, %2};\n" ::"r"(a), "d"(v0 * w0), "d"(v1 * w0) : "memory");
+            asm volatile("st.shared.v2.f64 [%0], {%1, %2};\n" ::"r"(a + 512), "d"(v2 * w1), "d"(v3 * w1) : "memory");
             asm volatile("bar.sync 1, %0;\n" ::"n"(C_::kThreads) : "memory");
         }
 #pragma unroll
