@@ -143,6 +143,14 @@ ttr_status ttr_round_fixed_krp(ttr_ctx* ctx, const ttr_tt* tt, const int64_t* ta
 typedef struct ttr_plan ttr_plan;
 ttr_status ttr_plan_fixed_krp(ttr_ctx* ctx, const ttr_tt* tt, const int64_t* target_ranks,
                               int64_t count, uint64_t seed, int rng_mode, ttr_plan** out);
+/* Host-streaming plan: host_in (the input's cores, flat and concatenated) is
+ * copied into `tt` and the result into host_out (flat) INSIDE the graph, on a
+ * copy stream overlapped with the sweep (cores arrive in the order the
+ * right-to-left sketch consumes them; output cores leave as soon as they are
+ * final). Both host buffers must be pinned and outlive the plan; execute +
+ * ttr_ctx_synchronize is one end-to-end host-to-host rounding. */
+ttr_status ttr_plan_fixed_krp_host(ttr_ctx* ctx, ttr_tt* tt, const int64_t* target_ranks, int64_t count,
+                                   uint64_t seed, const double* host_in, double* host_out, ttr_plan** out);
 ttr_status ttr_plan_execute(ttr_plan* plan);
 ttr_status ttr_plan_output(ttr_plan* plan, const ttr_tt** out);
 ttr_status ttr_plan_destroy(ttr_plan* plan);

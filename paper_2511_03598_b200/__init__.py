@@ -306,17 +306,38 @@ def round_fixed_krp(tt: TTTensor, target_ranks: Sequence[int], seed: int, rng: i
                          C.c_int64(len(target_ranks)), C.c_uint64(seed), C.c_int(rng))
 
 
+def _host_ptr(buf) -> int:
+    if hasattr(buf, "data_ptr"):
+        return buf.data_ptr()
+    if isinstance(buf, np.ndarray):
+        return buf.ctypes.data
+    raise TypeError("host buffer must be a torch tensor or numpy array")
+
+
 class FixedKrpPlan:
     """CUDA-graph plan of round_fixed_krp for one input buffer (ttr_plan):
     `execute()` replays the captured sweep; `output` is the plan-owned result
     (valid until the plan is closed)."""
 
-    def __init__(self, tt: TTTensor, target_ranks: Sequence[int], seed: int, rng: int = RNG_PHILOX):
+    def __init__(self, tt: TTTensor, target_ranks: Sequence[int], seed: int, rng: int = RNG_PHILOX,
+                 host_in=None, host_out=None):
+        """host_in/host_out (pinned host buffers with the flat input cores / room for
+        the flat result; e.g. torch tensors with pin_memory()): the plan also
+        streams the input in and the result out, overlapped with the sweep
+        (ttr_plan_fixed_krp_host)."""
         self.ctx = tt.ctx
         self.input = tt
         self._h = C.c_void_p()
-        _check(lib().ttr_plan_fixed_krp(tt.ctx._h, tt._h, _i64(target_ranks), C.c_int64(len(target_ranks)),
-                                        C.c_uint64(seed), C.c_int(rng), C.byref(self._h)))
+        self._host = (host_in, host_out)  # keep alive
+        if host_in is not None or host_out is not None:
+            if host_in is None or host_out is None or rng != RNG_PHILOX:
+                raise ValueError("host streaming needs both host buffers and the Philox generator")
+            _check(lib().ttr_plan_fixed_krp_host(tt.ctx._h, tt._h, _i64(target_ranks), C.c_int64(len(target_ranks)),
+                                                 C.c_uint64(seed), C.c_void_p(_host_ptr(host_in)),
+                                                 C.c_void_p(_host_ptr(host_out)), C.byref(self._h)))
+        else:
+            _check(lib().ttr_plan_fixed_krp(tt.ctx._h, tt._h, _i64(target_ranks), C.c_int64(len(target_ranks)),
+                                            C.c_uint64(seed), C.c_int(rng), C.byref(self._h)))
         out = C.c_void_p()
         _check(lib().ttr_plan_output(self._h, C.byref(out)))
         self.output = _BorrowedTT(out, tt.ctx, self)

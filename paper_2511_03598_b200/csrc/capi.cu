@@ -273,6 +273,25 @@ ttr_status ttr_plan_fixed_krp(ttr_ctx* ctx, const ttr_tt* tt, const int64_t* ran
     });
 }
 
+ttr_status ttr_plan_fixed_krp_host(ttr_ctx* ctx, ttr_tt* tt, const int64_t* ranks, int64_t count, uint64_t seed,
+                                   const double* host_in, double* host_out, ttr_plan** out) {
+    return guard([&] {
+        check_same_ctx(ctx, tt);
+        need(out != nullptr && host_in != nullptr && host_out != nullptr, "null argument");
+        if (count < 0 || (count > 0 && !ranks)) fail(Errc::InvalidRanks, "expected d-1 target ranks");
+        auto* p = new ttr_plan;
+        try {
+            p->plan = std::make_unique<Plan>(ctx->c, *tt->t, vec(ranks, count), seed, TTR_RNG_PHILOX, host_in, host_out);
+        } catch (...) {
+            delete p;
+            throw;
+        }
+        p->out.t = std::move(p->plan->out);
+        p->ctx = ctx;
+        *out = p;
+    });
+}
+
 ttr_status ttr_plan_execute(ttr_plan* plan) {
     return guard([&] {
         need(plan && plan->plan, "null plan");

@@ -52,8 +52,27 @@ enum Phase { kPhaseSketch = 0, kPhaseQr = 1, kPhaseGemm = 2, kPhaseOther = 3, kN
 // former tagged layout, two words per value)
 constexpr std::size_t kQrXchgWords = 2 + 2 * 160 * 32 * 2 + 2 * 32 * 2;
 
+// Host-streaming hooks of a plan with host buffers (tt_round.cu): the input
+// cores arrive by H2D on a copy stream (events per core), output cores leave
+// by D2H as soon as they are final, overlapping the PCIe traffic with the
+// sweep. Null outside such a plan.
+struct HostIO {
+    cudaStream_t copy = nullptr;
+    std::vector<cudaEvent_t> in_ready, out_ready;
+    std::vector<double*> out_host;           // destination of each output core
+    std::vector<const double*> out_dev;      // output core device pointers
+    std::vector<std::size_t> out_bytes;
+    void wait_in(cudaStream_t s, std::size_t k) const { cudaStreamWaitEvent(s, in_ready[k], 0); }
+    void out_done(cudaStream_t s, std::size_t k) const {
+        cudaEventRecord(out_ready[k], s);
+        cudaStreamWaitEvent(copy, out_ready[k], 0);
+        cudaMemcpyAsync(out_host[k], out_dev[k], out_bytes[k], cudaMemcpyDeviceToHost, copy);
+    }
+};
+
 struct Ctx {
     int device = 0;
+    HostIO* io = nullptr;
     bool timing = false;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> phase_events[kNumPhases];
     cudaStream_t stream = nullptr;

@@ -300,6 +300,7 @@ struct Sketch {
         SketchScope scope(c);
         for (i64 k = d; k >= start; --k) {
             const i64 rl = t.r[k - 1], nk = t.n[k - 1], rr = t.r[k];
+            if (c.io) c.io->wait_in(c.stream, static_cast<std::size_t>(k - 1));  // core k-1 arrived (H2D)
             const double* wt_next = (k == d) ? ones.p : Wt[k + 1].p + col0;
             const i64 ld_next = ldwt;
             double* wt_out = (k >= 3) ? Wt[k].p + col0 : nullptr;
@@ -451,6 +452,7 @@ void rand_orth_sweep(Ctx& c, const TTDev& t, i64 width, const std::vector<const 
     DBuf M(c, static_cast<std::size_t>(width * t.max_rank()));
 
     const double* v = t.core(0);
+    if (c.io) c.io->wait_in(c.stream, 0);
     for (i64 k = 1; k < d; ++k) {
         const i64 rows = r[k - 1] * t.n[k - 1], cols = t.r[k], l = r[k];
         // S = V(Y_k) W_{k+1}(:, 1:l)
@@ -463,6 +465,7 @@ void rand_orth_sweep(Ctx& c, const TTDev& t, i64 width, const std::vector<const 
             PhaseScope ph(c, kPhaseQr);
             thin_qr(c, rows, l, S.p, rows, out->core(k - 1), rows, nullptr, 1);
         }
+        if (c.io) c.io->out_done(c.stream, static_cast<std::size_t>(k - 1));  // output core k-1 final: D2H
         const i64 ncols = t.n[k] * t.r[k + 1];
         double* dst = (k == d - 1) ? out->core(d - 1) : work.p;
         {
@@ -474,13 +477,15 @@ void rand_orth_sweep(Ctx& c, const TTDev& t, i64 width, const std::vector<const 
         }
         v = dst;  // stream order: this iteration's reads of the old V precede the write
     }
+    if (c.io) c.io->out_done(c.stream, static_cast<std::size_t>(d - 1));
 }
 
 // ---------------------------------------------------------------------------
 // CUDA-graph plan for fixed-rank KRP rounding: one eager run sizes every
 // workspace (and the split-K scratch), then the whole sweep — ~2,400 launches
 // for config 5b — is captured once and replayed with a single graph launch.
-Plan::Plan(Ctx& cc, const TTDev& in_, const std::vector<i64>& ranks_, std::uint64_t seed_, int rng)
+Plan::Plan(Ctx& cc, const TTDev& in_, const std::vector<i64>& ranks_, std::uint64_t seed_, int rng,
+           const double* host_in, double* host_out)
     : c(cc), in(in_), ranks(ranks_), seed(seed_), rng_mode(rng) {
     if (rng_mode != TTR_RNG_PHILOX) fail(Errc::InvalidArgument, "plans need the device (Philox) generator");
     auto r = fixed_krp_ranks(in, ranks);
@@ -492,10 +497,51 @@ Plan::Plan(Ctx& cc, const TTDev& in_, const std::vector<i64>& ranks_, std::uint6
     c.timing = false;
     const Counts saved = c.counts;
     const std::uint64_t l0 = c.launches;
+    const bool host = host_in != nullptr && host_out != nullptr;
+    const i64 d = in.d();
+    if (host) {
+        // host streaming: H2D of core 0 (first needed by the sweep, tiny) then
+        // cores d-1 .. 1 in the order the right-to-left sketch consumes them;
+        // each output core leaves by D2H as soon as it is final
+        TTR_CUDA(cudaStreamCreateWithFlags(&io.copy, cudaStreamNonBlocking));
+        io.in_ready.resize(static_cast<std::size_t>(d));
+        io.out_ready.resize(static_cast<std::size_t>(d));
+        for (auto& e : io.in_ready) TTR_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        for (auto& e : io.out_ready) TTR_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        TTR_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+        TTR_CUDA(cudaEventCreateWithFlags(&join, cudaEventDisableTiming));
+        std::size_t o = 0;
+        for (i64 k = 0; k < d; ++k) {
+            io.out_host.push_back(host_out + o);
+            io.out_dev.push_back(out->core(k));
+            io.out_bytes.push_back(sizeof(double) * static_cast<std::size_t>(out->core_size(k)));
+            o += static_cast<std::size_t>(out->core_size(k));
+        }
+    }
     TTR_CUDA(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal));
     try {
+        if (host) {
+            TTR_CUDA(cudaEventRecord(fork, c.stream));
+            TTR_CUDA(cudaStreamWaitEvent(io.copy, fork, 0));  // the copy stream joins the capture
+            std::vector<std::size_t> offs(static_cast<std::size_t>(d) + 1, 0);
+            for (i64 k = 0; k < d; ++k) offs[k + 1] = offs[k] + static_cast<std::size_t>(in.core_size(k));
+            std::vector<i64> order{0};
+            for (i64 k = d - 1; k >= 1; --k) order.push_back(k);
+            for (i64 k : order) {
+                TTR_CUDA(cudaMemcpyAsync(in.core(k), host_in + offs[k], sizeof(double) * in.core_size(k),
+                                         cudaMemcpyHostToDevice, io.copy));
+                TTR_CUDA(cudaEventRecord(io.in_ready[k], io.copy));
+            }
+            c.io = &io;
+        }
         round_fixed_krp_into(c, in, ranks, seed, rng_mode, *out);
+        if (host) {
+            c.io = nullptr;
+            TTR_CUDA(cudaEventRecord(join, io.copy));
+            TTR_CUDA(cudaStreamWaitEvent(c.stream, join, 0));  // D2H of the last core done
+        }
     } catch (...) {
+        c.io = nullptr;
         cudaGraph_t g;
         cudaStreamEndCapture(c.stream, &g);
         if (g) cudaGraphDestroy(g);
@@ -529,6 +575,11 @@ void Plan::execute() {
 Plan::~Plan() {
     if (exec) cudaGraphExecDestroy(exec);
     if (graph) cudaGraphDestroy(graph);
+    for (auto e : io.in_ready) cudaEventDestroy(e);
+    for (auto e : io.out_ready) cudaEventDestroy(e);
+    if (fork) cudaEventDestroy(fork);
+    if (join) cudaEventDestroy(join);
+    if (io.copy) cudaStreamDestroy(io.copy);
 }
 
 // ---------------------------------------------------------------------------

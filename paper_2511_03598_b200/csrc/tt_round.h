@@ -87,7 +87,12 @@ struct Plan {
     cudaGraphExec_t exec = nullptr;
     std::uint64_t launches_per_run = 0;
     Counts flops;
-    Plan(Ctx& c, const TTDev& in, const std::vector<i64>& ranks, std::uint64_t seed, int rng_mode);
+    HostIO io;  // host-streaming plans only
+    cudaEvent_t fork = nullptr, join = nullptr;
+    // host_in/host_out (pinned, flat cores): the graph also streams the input
+    // in and the result out, overlapped with the sweep
+    Plan(Ctx& c, const TTDev& in, const std::vector<i64>& ranks, std::uint64_t seed, int rng_mode,
+         const double* host_in = nullptr, double* host_out = nullptr);
     ~Plan();
     void execute();
 };

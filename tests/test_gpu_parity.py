@@ -190,6 +190,43 @@ def test_fixed_krp_config3_shape_parity(P, O):
     assert rel_err_vs_ref(y_ref, y_gpu) <= 1e-10
 
 
+def test_plan_replays_bitwise(P, O):
+    """The CUDA-graph plan reproduces the eager call bit for bit, also after the
+    input buffer is refilled with other data."""
+    x1 = O.two_part_tt(5, 24, 12, 36, 1e-6, 2001)
+    x2 = O.two_part_tt(5, 24, 12, 36, 1e-6, 2002)
+    t = to_device(x1)
+    plan = P.FixedKrpPlan(t, [20] * 4, 7)
+    plan.execute()
+    assert np.array_equal(plan.output.flat(), P.round_fixed_krp(to_device(x1), [20] * 4, 7).flat())
+    P.copy_from_host(t, x2.flat())
+    plan.execute()
+    y2 = P.round_fixed_krp(to_device(x2), [20] * 4, 7)
+    assert np.array_equal(plan.output.flat(), y2.flat())
+    assert rel_err_vs_ref(O.round_fixed_krp(x2, [20] * 4, 7, rng=O.PHILOX), y2) <= 1e-10
+    plan.close()
+
+
+def test_host_streaming_plan(P, O):
+    """ttr_plan_fixed_krp_host: H2D of the input and D2H of the result inside the
+    graph (copy stream, per-core events) give the eager result bitwise."""
+    import torch
+    x = O.two_part_tt(6, 32, 20, 60, 1e-6, 2003)
+    y_eager = P.round_fixed_krp(to_device(x), [25] * 5, 7)
+    t = to_device(O.two_part_tt(6, 32, 20, 60, 1e-6, 2004))  # staging buffer, other contents
+    host_in = torch.from_numpy(np.ascontiguousarray(x.flat())).pin_memory()
+    y_flat = y_eager.flat()
+    out_len = y_flat.size
+    host_out = torch.zeros(out_len, dtype=torch.float64).pin_memory()
+    plan = P.FixedKrpPlan(t, [25] * 5, 7, host_in=host_in, host_out=host_out)
+    for _ in range(2):
+        host_out.zero_()
+        plan.execute()
+        t.ctx.synchronize()
+        assert np.array_equal(host_out.numpy(), y_flat)
+    plan.close()
+
+
 # ---- adaptive KRP rounding -------------------------------------------------------------------
 
 @pytest.mark.parametrize("rng_mode", [0, 1])
