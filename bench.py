@@ -58,9 +58,10 @@ def parse():
     ap.add_argument("--config", default="5b", choices=["5b", "3", "5a"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--sharding", default="tensors", choices=["tensors", "columns"],
-                    help="N>1 on config 5b: independent tensor per rank (weak) or one tensor with "
-                         "column-sharded KRP sketch + NCCL all-gather (strong)")
+    ap.add_argument("--sharding", default="tensors", choices=["tensors", "columns", "rows"],
+                    help="N>1 on config 5b: independent tensor per rank (weak), or one tensor with "
+                         "column-sharded KRP sketch + NCCL all-gather and a replicated (columns) or "
+                         "row-sharded TSQR (rows) Rand-Orth sweep (strong)")
     return ap.parse_args()
 
 
@@ -390,7 +391,8 @@ def run_columns(args, world, rank, local):
     slices, Rand-Orth sweep (replicated). Strong scaling; time = max over ranks."""
     import torch
     import paper_2511_03598_b200 as P
-    from paper_2511_03598_b200.distributed import round_fixed_krp_column_sharded
+    from paper_2511_03598_b200.distributed import round_fixed_krp_column_sharded, round_fixed_krp_row_sharded
+    rows_mode = args.sharding == "rows"
     if world > 1:
         import torch.distributed as dist
         torch.cuda.set_device(local)
@@ -402,20 +404,34 @@ def run_columns(args, world, rank, local):
     cfg = dict(CFG5B)
     y = build_input(P, ctx, cfg)  # identical replica on every rank
     ranks = [cfg["ell"]] * (cfg["d"] - 1)
+
+    def step():
+        if rows_mode:
+            return round_fixed_krp_row_sharded(y, ranks, 7), {"bounds": None}
+        return round_fixed_krp_column_sharded(y, ranks, 7)
+
+    if rows_mode:
+        # algorithmic work of the job = one round_fixed_krp (the reference charges)
+        ctx.reset_counters()
+        o = P.round_fixed_krp(y, ranks, 7)
+        torch.cuda.synchronize()
+        flops_job = ctx.counters().total()
+        del o
     ctx.reset_counters()
-    out, info = round_fixed_krp_column_sharded(y, ranks, 7)
+    out, info = step()
     torch.cuda.synchronize()
     cnt = ctx.counters()
     flops_rank = cnt.total()
-    # algorithmic work of the job: every rank's sketch slice + ONE sweep (the replicas are redundant)
-    sk = torch.tensor([float(cnt.sketch)], device="cuda", dtype=torch.float64)
-    if world > 1:
-        torch.distributed.all_reduce(sk)
-    flops_job = float(sk.item()) + (cnt.total() - cnt.sketch)
+    if not rows_mode:
+        # every rank's sketch slice + ONE sweep (the replicas are redundant)
+        sk = torch.tensor([float(cnt.sketch)], device="cuda", dtype=torch.float64)
+        if world > 1:
+            torch.distributed.all_reduce(sk)
+        flops_job = float(sk.item()) + (cnt.total() - cnt.sketch)
     out_ranks = out.ranks()
     del out
     for _ in range(args.warmup):
-        o, _ = round_fixed_krp_column_sharded(y, ranks, 7)
+        o, _ = step()
         del o
     torch.cuda.synchronize()
     if world > 1:
@@ -426,7 +442,7 @@ def run_columns(args, world, rank, local):
     with ClockSampler(local) as clk:
         e0.record(stream)
         for _ in range(args.steps):
-            o, _ = round_fixed_krp_column_sharded(y, ranks, 7)
+            o, _ = step()
             del o
         e1.record(stream)
         torch.cuda.synchronize()
@@ -441,8 +457,10 @@ def run_columns(args, world, rank, local):
             "metric": METRIC, "value": flops_job / (ms * 1e-3) / 1e12, "unit": "TFLOP/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (device Philox Gaussian cores)",
-            "config": {"workload": "config 5b, one tensor: column-sharded KRP sketch + NCCL all-gather + "
-                                   "replicated Rand-Orth sweep",
+            "config": {"workload": ("config 5b, one tensor: column-sharded KRP sketch + NCCL all-gather + "
+                                    "row-sharded Rand-Orth sweep with NVLink TSQR") if rows_mode else
+                                   ("config 5b, one tensor: column-sharded KRP sketch + NCCL all-gather + "
+                                    "replicated Rand-Orth sweep"),
                        "column_bounds": info["bounds"], "output_ranks": out_ranks,
                        "flops_per_rank": flops_rank, "l2": "inputs exceed L2"},
             "clocks": clk.summary(), "gpu_launches": launches,
@@ -527,7 +545,7 @@ def main():
     if args.config == "5a":
         run_5a(args, world, rank, local)
         return
-    if args.sharding == "columns":
+    if args.sharding in ("columns", "rows"):
         run_columns(args, world, rank, local)
         return
     run_ours(args, world, rank, local)

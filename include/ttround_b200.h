@@ -184,6 +184,10 @@ ttr_status ttr_dev_thin_qr(ttr_ctx* ctx, int64_t m, int64_t n, const double* dA,
 ttr_status ttr_dev_gemm(ttr_ctx* ctx, int trans_a, int64_t m, int64_t n, int64_t k, double alpha,
                         const double* dA, int64_t lda, const double* dB, int64_t ldb, double beta,
                         double* dC, int64_t ldc);
+/* Strided batch: C_b = alpha op(A_b) B_b + beta C_b with X_b = X + b*sX. */
+ttr_status ttr_dev_gemm_batched(ttr_ctx* ctx, int trans_a, int64_t m, int64_t n, int64_t k, double alpha,
+                                const double* dA, int64_t lda, int64_t sA, const double* dB, int64_t ldb,
+                                int64_t sB, double beta, double* dC, int64_t ldc, int64_t sC, int64_t batch);
 /* C = op(A) B on the device through the library's DMMA GEMM (for tests). */
 ttr_status ttr_gemm(ttr_ctx* ctx, int trans_a, int64_t m, int64_t n, int64_t k, const double* host_a,
                     const double* host_b, double* host_c);

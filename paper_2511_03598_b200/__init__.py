@@ -112,6 +112,7 @@ class Context:
         self._h = C.c_void_p()
         _check(lib().ttr_ctx_create(C.c_int(device), C.c_void_p(stream) if stream else None, C.byref(self._h)))
         self.device = device
+        self.stream = stream  # caller stream handle, or None (library-owned stream)
 
     def close(self):
         if getattr(self, "_h", None) and self._h.value and _lib is not None:
@@ -123,6 +124,7 @@ class Context:
 
     def set_stream(self, stream: Optional[int]):
         _check(lib().ttr_ctx_set_stream(self._h, C.c_void_p(stream) if stream else None))
+        self.stream = stream
 
     def synchronize(self):
         _check(lib().ttr_ctx_synchronize(self._h))

@@ -411,6 +411,16 @@ ttr_status ttr_dev_gemm(ttr_ctx* ctx, int trans_a, int64_t m, int64_t n, int64_t
     });
 }
 
+ttr_status ttr_dev_gemm_batched(ttr_ctx* ctx, int trans_a, int64_t m, int64_t n, int64_t k, double alpha,
+                                const double* dA, int64_t lda, int64_t sA, const double* dB, int64_t ldb, int64_t sB,
+                                double beta, double* dC, int64_t ldc, int64_t sC, int64_t batch) {
+    return guard([&] {
+        need(ctx && dA && dB && dC, "null argument");
+        need(batch >= 0, "negative batch");
+        gemm_batched(ctx->c, trans_a != 0, m, n, k, alpha, dA, lda, sA, dB, ldb, sB, beta, dC, ldc, sC, batch);
+    });
+}
+
 ttr_status ttr_gemm(ttr_ctx* ctx, int trans_a, int64_t m, int64_t n, int64_t k, const double* host_a, const double* host_b,
                     double* host_c) {
     return guard([&] {

@@ -96,3 +96,142 @@ def test_column_sharded_path_matches_single_gpu_bitwise():
     torch.cuda.synchronize()
     assert sharded.ranks() == single.ranks()
     assert np.array_equal(sharded.flat(), single.flat())
+
+
+# ---- row-sharded Rand-Orth sweep (NVLink TSQR), CPU stand-in backend -----------------
+
+class NumpyOps:
+    """CPU backend for rand_orth_row_sharded: numpy GEMMs, the oracle's
+    Householder QR, gloo collectives — the same orchestration the GPU runs."""
+
+    def __init__(self, O, group=None):
+        self.O, self.group = O, group
+
+    def alloc(self, rows, cols):
+        from paper_2511_03598_b200.distributed import View
+        return View(np.zeros(max(1, rows * cols)), 0, max(1, rows), rows, cols)
+
+    @staticmethod
+    def mat(v):
+        return np.lib.stride_tricks.as_strided(v.base[v.off:], shape=(v.rows, v.cols), strides=(8, 8 * v.ld))
+
+    def gemm(self, ta, alpha, A, B, beta, Cm):
+        a = self.mat(A).T if ta else self.mat(A)
+        c = self.mat(Cm)
+        c[...] = alpha * (a @ self.mat(B)) + (beta * c if beta != 0.0 else 0.0)
+
+    def gemm_batched(self, alpha, A, sA, B, sB, beta, Cv, sC, batch):
+        from paper_2511_03598_b200.distributed import View
+        for b in range(batch):
+            self.gemm(False, alpha, View(A.base, A.off + b * sA, A.ld, A.rows, A.cols),
+                      View(B.base, B.off + b * sB, B.ld, B.rows, B.cols), beta,
+                      View(Cv.base, Cv.off + b * sC, Cv.ld, Cv.rows, Cv.cols))
+
+    def qr(self, A):
+        q, r = self.O.thin_qr(np.array(self.mat(A)))
+        Q, R = self.alloc(*q.shape), self.alloc(*r.shape)
+        self.mat(Q)[...] = q
+        self.mat(R)[...] = r
+        return Q, R
+
+    def contiguous(self, v):
+        out = self.alloc(v.rows, v.cols)
+        self.mat(out)[...] = self.mat(v)
+        return out
+
+    def all_gather_blocks(self, block, world):
+        from paper_2511_03598_b200.distributed import View
+        b, c = block.rows, block.cols
+        mine = torch.from_numpy(np.ascontiguousarray(self.mat(block).T).reshape(-1))  # column-major
+        parts = [torch.empty_like(mine) for _ in range(world)]
+        dist.all_gather(parts, mine, group=self.group)
+        st = np.concatenate([p.numpy().reshape(c, b) for p in parts], axis=1).reshape(-1)  # (c, world*b)
+        return View(st, 0, world * b, world * b, c)
+
+    def all_reduce(self, v, world):
+        t = torch.from_numpy(v.base)
+        dist.all_reduce(t, group=self.group)
+
+    def gather_rows(self, local, counts, world):
+        from paper_2511_03598_b200.distributed import View
+        c = local.cols
+        mx = max(counts)
+        pad = np.zeros((c, mx))
+        pad[:, :local.rows] = self.mat(local).T
+        parts = [torch.empty(c * mx, dtype=torch.float64) for _ in range(world)]
+        dist.all_gather(parts, torch.from_numpy(pad.reshape(-1)), group=self.group)
+        full = np.concatenate([p.numpy().reshape(c, mx)[:, :counts[q]] for q, p in enumerate(parts)], axis=1)
+        return View(np.ascontiguousarray(full).reshape(-1), 0, sum(counts), sum(counts), c)
+
+
+def _row_worker(rank, world, port, result_q):
+    import sys
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import py_oracle as O
+    from paper_2511_03598_b200.distributed import View, fixed_krp_output_ranks, rand_orth_row_sharded
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    x = O.two_part_tt(5, 8, 6, 10, 1e-6, 31)
+    n, r_in, _ = x.shape()
+    targets, seed = [12] * 4, 7
+    width = max(targets)
+    fac = [O.philox_factor(seed, k, n[k - 1], width, 0) for k in range(2, len(n) + 1)]
+    w = O.krp_contractions(x, fac)
+    W = {k: View(np.asfortranarray(wk).reshape(-1, order="F"), 0, wk.shape[0], wk.shape[0], width)
+         for k, wk in zip(range(2, len(n) + 1), w)}
+    flat = x.flat()
+    offs = np.cumsum([0] + [r_in[k] * n[k] * r_in[k + 1] for k in range(len(n))])
+
+    def core(k):
+        rows = r_in[k] * n[k]
+        return View(flat, int(offs[k]), rows, rows, r_in[k + 1])
+
+    r_out = fixed_krp_output_ranks(n, r_in, targets)
+    cores = rand_orth_row_sharded(NumpyOps(O), n, r_in, r_out, W, core, rank, world)
+    y_flat = np.concatenate([NumpyOps.mat(v).reshape(-1, order="F") for v in cores])
+    y = O.TT.from_flat(len(n), n, r_out, y_flat)
+    ref = O.round_fixed_krp(x, targets, seed, rng=O.PHILOX)
+    err = O.relative_error(ref, y)
+    gathered = [None] * world
+    dist.all_gather_object(gathered, y_flat.tobytes())
+    if rank == 0:
+        result_q.put((err, r_out == ref.ranks, all(g == gathered[0] for g in gathered)))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_row_sharded_sweep_gloo_world2():
+    """The TSQR row-sharded sweep (mode 1 replicated, modes >= 2 sharded) on 2
+    CPU ranks reproduces the oracle's round_fixed_krp to 1e-10 with identical
+    ranks, and every rank ends with the same tensor."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_row_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    err, ranks_ok, same = q.get(timeout=240)
+    for p in procs:
+        p.join(timeout=60)
+    assert ranks_ok
+    assert same
+    assert err <= 1e-10, err
+    assert all(p.exitcode == 0 for p in procs)
+
+
+@pytest.mark.gpu
+def test_row_sharded_path_single_gpu():
+    """The device row-sharded driver at world size 1 (replicated modes, TSQR of
+    one block) matches round_fixed_krp to 1e-10."""
+    import sys
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import py_oracle as O
+    from helpers import rel_err_vs_ref, to_device
+    import paper_2511_03598_b200 as P
+    from paper_2511_03598_b200.distributed import round_fixed_krp_row_sharded
+    x = O.two_part_tt(6, 16, 10, 30, 1e-6, 41)
+    y = round_fixed_krp_row_sharded(to_device(x), [24] * 5, 7, world=1, rank=0)
+    ref = O.round_fixed_krp(x, [24] * 5, 7, rng=O.PHILOX)
+    assert y.ranks() == ref.ranks
+    assert rel_err_vs_ref(ref, y) <= 1e-10
