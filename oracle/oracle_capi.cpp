@@ -184,6 +184,15 @@ int ttro_round_adaptive_krp(const ttro_tt* t, double tol, double f_init, double 
         if (tau_out) *tau_out = tr.tau;
     });
 }
+int ttro_round_sum_adaptive_krp(const ttro_tt* const* terms, int count, double eps, double f_inc, std::uint64_t seed,
+                                int rng_mode, ttro_tt** out) {
+    return guard([&] {
+        std::vector<TT> ts;
+        for (int i = 0; i < count; ++i) ts.push_back(terms[i]->tt);
+        *out = wrap(round_sum_adaptive_krp(ts, eps, f_inc, seed, static_cast<RngMode>(rng_mode)));
+    });
+}
+
 int ttro_compression_pass(const ttro_tt* t, double tau, ttro_tt** out) {
     return guard([&] { *out = wrap(compression_pass(t->tt, tau)); });
 }

@@ -237,6 +237,13 @@ def round_adaptive_krp(t: TT, tolerance=1e-6, f_init=0.1, f_inc=0.05, seed=0, rn
     return TT(out)
 
 
+def round_sum_adaptive_krp(terms: Sequence[TT], eps: float, f_inc: float, seed: int, rng=XOSHIRO) -> TT:
+    """sum_round.cpp:52-173 — adaptive rounding of sum(terms) without the formal sum."""
+    arr = (C.c_void_p * max(1, len(terms)))(*[t._h.value for t in terms])
+    return TT._new(lib().ttro_round_sum_adaptive_krp, arr, C.c_int(len(terms)), C.c_double(eps), C.c_double(f_inc),
+                   C.c_uint64(seed), C.c_int(rng))
+
+
 def compression_pass(t: TT, tau: float) -> TT:
     return TT._new(lib().ttro_compression_pass, t._h, C.c_double(tau))
 

@@ -1009,6 +1009,141 @@ TT compression_pass(const TT& left, double tau) {  // round_rand.cpp:155-179
 }
 
 // ---------------------------------------------------------------------------
+// adaptive rounding of a sum of TT tensors — proj/core/src/sum_round.cpp
+void validate_sum(const std::vector<TT>& terms) {  // sum_round.cpp:11-19
+    if (terms.empty()) fail(Errc::EmptyTermList, "sum of no TT terms");
+    const auto modes = terms.front().mode_sizes();
+    for (const auto& t : terms)
+        if (t.mode_sizes() != modes) fail(Errc::ModeSizeMismatch, "sum terms mode sizes differ");
+}
+
+Matrix residual_sketch_sum(const std::vector<TT>& terms, const Matrix& z, const Matrix& q,
+                           std::vector<ContractionSet>& w, Index k, Index b, FactorRng& rng) {  // sum_round.cpp:21-50
+    if (terms.empty()) fail(Errc::EmptyTermList, "residual sketch of no terms");
+    if (b < 1) fail(Errc::InvalidArgument, "sketch block size must be >= 1");
+    if (k < 1 || k >= terms.front().order()) fail(Errc::InvalidArgument, "core index out of range");
+    const Index used = q.cols;
+    const Index have = w.front().at_mode(k + 1).cols;
+    if (have < used + b) {
+        // one shared fresh draw: the sketch of the sum stays the sum of the sketches
+        auto fresh = draw_gaussian_factors(terms.front(), k + 1, used + b - have, rng, have);
+        for (std::size_t i = 0; i < terms.size(); ++i) append_krp_contractions(w[i], terms[i], fresh);
+    }
+    Index expected = 0;
+    for (const auto& t : terms) expected += t.rank(k);
+    if (z.cols != expected) fail(Errc::ModeSizeMismatch, "working unfolding width mismatch");
+    Matrix s(z.rows, b);
+    Index col = 0;
+    for (std::size_t i = 0; i < terms.size(); ++i) {
+        const Index rk = terms[i].rank(k);
+        Matrix si = linalg::mul(z.middle_cols(col, rk), w[i].at_mode(k + 1).middle_cols(used, b));
+        for (std::size_t e = 0; e < s.a.size(); ++e) s.a[e] += si.a[e];
+        col += rk;
+    }
+    if (used > 0) {
+        Matrix p = linalg::mul(q, linalg::tmul(q, s));
+        for (std::size_t e = 0; e < s.a.size(); ++e) s.a[e] -= p.a[e];
+    }
+    return s;
+}
+
+TT round_sum_adaptive_krp(const std::vector<TT>& terms, double eps, double f_inc, std::uint64_t seed,
+                          RngMode mode) {  // sum_round.cpp:52-173
+    if (terms.empty()) fail(Errc::EmptyTermList, "sum of no TT terms");
+    validate_sum(terms);
+    if (!(eps > 0.0)) fail(Errc::InvalidArgument, "tolerance must be > 0");
+    if (!(f_inc > 0.0 && f_inc < 1.0)) fail(Errc::InvalidArgument, "f_inc must lie in (0,1)");
+    const Index s_count = static_cast<Index>(terms.size());
+    const Index d = terms.front().order();
+    const auto modes = terms.front().mode_sizes();
+    if (d == 1) {  // the sum is exact at rank one
+        Core c(1, modes[0], 1);
+        for (const auto& t : terms)
+            for (Index j = 0; j < modes[0]; ++j) c(0, j, 0) += t.core(0)(0, j, 0);
+        return TT({std::move(c)});
+    }
+    FactorRng rng(mode, seed);
+    Index width = 1;
+    for (const auto& t : terms) width = std::max(width, t.max_rank());
+    auto factors = draw_gaussian_factors(terms.front(), 2, width, rng);
+    std::vector<ContractionSet> w;
+    for (const auto& t : terms) w.push_back(krp_partial_contractions_rl(t, factors));
+    // sketch-based norm estimate of the sum; per-term estimates feed the cancellation guard
+    Matrix s0(modes[0], width);
+    double max_term = 0.0;
+    for (Index i = 0; i < s_count; ++i) {
+        Matrix si = linalg::mul(terms[static_cast<std::size_t>(i)].core(0).vertical(),
+                                w[static_cast<std::size_t>(i)].at_mode(2));
+        max_term = std::max(max_term, si.norm() / std::sqrt(static_cast<double>(width)));
+        for (std::size_t e = 0; e < s0.a.size(); ++e) s0.a[e] += si.a[e];
+    }
+    const double nrm = s0.norm() / std::sqrt(static_cast<double>(width));
+    if (nrm < 1e3 * std::numeric_limits<double>::epsilon() * max_term) return TT::zero(modes);
+    const double tau = eps * nrm / std::sqrt(static_cast<double>(d - 1));
+    // working state: vertical unfolding of the projected formal-sum core, one
+    // column block of width r_k^(i) per term
+    Matrix v(modes[0], 0);
+    for (const auto& t : terms) v = hcat(v, t.core(0).vertical());
+    std::vector<Core> out;
+    Index l_prev = 1;
+    for (Index k = 1; k < d; ++k) {
+        const Index rbar = std::min(v.rows, v.cols);
+        Index b_init = 1;
+        for (const auto& t : terms) b_init = std::max(b_init, t.rank(k));
+        b_init = std::min(b_init, rbar);
+        Matrix s(v.rows, b_init);
+        Index col = 0;
+        for (Index i = 0; i < s_count; ++i) {
+            const Index rk = terms[static_cast<std::size_t>(i)].rank(k);
+            Matrix si = linalg::mul(v.middle_cols(col, rk), w[static_cast<std::size_t>(i)].at_mode(k + 1).left_cols(b_init));
+            for (std::size_t e = 0; e < s.a.size(); ++e) s.a[e] += si.a[e];
+            col += rk;
+        }
+        Matrix q = linalg::thin_qr_q(s);
+        Matrix m = linalg::tmul(q, v);
+        const Index b_inc = ceil_fraction(f_inc, rbar);
+        while (q.cols < rbar) {
+            Matrix sk = residual_sketch_sum(terms, v, q, w, k, b_inc, rng);
+            if (residual_norm_estimate(sk, b_inc) <= tau) break;
+            const Index grow = std::min(b_inc, rbar - q.cols);
+            Matrix q_new = linalg::thin_qr_q(sk.left_cols(grow));
+            Matrix proj = linalg::mul(q, linalg::tmul(q, q_new));
+            for (std::size_t e = 0; e < q_new.a.size(); ++e) q_new.a[e] -= proj.a[e];
+            q_new = linalg::thin_qr_q(q_new);
+            m = vcat(m, linalg::tmul(q_new, v));
+            q = hcat(q, q_new);
+        }
+        out.push_back(Core::from_vertical(l_prev, modes[static_cast<std::size_t>(k - 1)], q));
+        l_prev = q.cols;
+        if (k == d - 1) {  // right boundary: the per-term projections add up
+            Matrix h_last(l_prev, modes[static_cast<std::size_t>(k)]);
+            Index c0 = 0;
+            for (Index i = 0; i < s_count; ++i) {
+                const auto& t = terms[static_cast<std::size_t>(i)];
+                Matrix hi = linalg::mul(m.middle_cols(c0, t.rank(k)), t.core(k).horizontal());
+                for (std::size_t e = 0; e < h_last.a.size(); ++e) h_last.a[e] += hi.a[e];
+                c0 += t.rank(k);
+            }
+            out.push_back(Core::from_horizontal(modes[static_cast<std::size_t>(k)], 1, h_last));
+        } else {
+            Matrix v_next(l_prev * modes[static_cast<std::size_t>(k)], 0);
+            Index c0 = 0;
+            for (Index i = 0; i < s_count; ++i) {
+                const auto& t = terms[static_cast<std::size_t>(i)];
+                Matrix hi = linalg::mul(m.middle_cols(c0, t.rank(k)), t.core(k).horizontal());
+                // the horizontal product buffer doubles as the next vertical block
+                Matrix blk(l_prev * t.core(k).n(), t.rank(k + 1));
+                blk.a = hi.a;
+                v_next = hcat(v_next, blk);
+                c0 += t.rank(k);
+            }
+            v = std::move(v_next);
+        }
+    }
+    return TT(std::move(out));
+}
+
+// ---------------------------------------------------------------------------
 // synthetic inputs — proj/core/src/synthetic.cpp:8-26
 Synthetic synthetic_perturbed_tt(const std::vector<Index>& modes, const std::vector<Index>& ranks,
                                  double eps_pert, std::uint64_t seed) {

@@ -238,6 +238,17 @@ Matrix generate_residual_sketch(const TT& tt, const Matrix& z, const Matrix& q, 
 TT round_adaptive_krp(const TT& tt, const AdaptiveConfig& cfg, AdaptiveTrace* trace = nullptr);
 TT compression_pass(const TT& left_orthogonal, double tau);
 
+// ---- sum of TT tensors without the formal sum: proj/core/src/sum_round.cpp --
+//! sum_round.cpp:11-19 (TTSum::of validation)
+void validate_sum(const std::vector<TT>& terms);
+//! sum_round.cpp:21-50: stacked residual sketch of the terms against the
+//! concatenated working unfolding z (one column block of width r_k^(i) per term)
+Matrix residual_sketch_sum(const std::vector<TT>& terms, const Matrix& z, const Matrix& q,
+                           std::vector<ContractionSet>& w, Index k, Index b, FactorRng& rng);
+//! sum_round.cpp:52-173
+TT round_sum_adaptive_krp(const std::vector<TT>& terms, double eps, double f_inc, std::uint64_t seed,
+                          RngMode mode = RngMode::Xoshiro);
+
 // ---- synthetic inputs: proj/core/src/synthetic.cpp:8-26 + BASELINE configs --
 struct Synthetic { TT x, y, z; };
 Synthetic synthetic_perturbed_tt(const std::vector<Index>& modes, const std::vector<Index>& ranks,

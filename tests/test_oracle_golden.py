@@ -59,6 +59,45 @@ def test_criterion7_flop_ratios_golden(oracle):
     assert f"{d / c:.3g}" == "3.94"
 
 
+def test_criterion6_sum_round_flop_ratio_golden(oracle):
+    """acceptance.cpp:283-296 -> 's=8/s=1 contraction flops ratio 8.68' (test_output.txt:32):
+    adaptive sum rounding of scaled copies; depends on the adaptive loop and the charges."""
+    O = oracle
+    base = O.random_gaussian_tt([8] * 5, [1, 8, 8, 8, 8, 1], 31337)
+
+    def sketch_flops(s):
+        O.flops_reset()
+        O.round_sum_adaptive_krp([O.scaled(base, 1.0 + 0.1 * i) for i in range(s)], 0.5, 0.01, 5)
+        return O.flops_get()["sketch"]
+    ratio = sketch_flops(8) / sketch_flops(1)
+    assert f"{ratio:.3g}" == "8.68"
+
+
+def test_sum_round_properties(oracle):
+    """test_sum_round.cpp:99-152 / acceptance.cpp:270-281: 8 random terms meet
+    1.5 eps against the dense sum in >= 9/10 seeds; opposite terms cancel to the
+    zero tensor; one term behaves like the single-tensor algorithm; validation."""
+    O = oracle
+    eps = 1e-6
+    terms = [O.random_gaussian_tt([8] * 4, [1, 3, 3, 3, 1], O.derive_seed(99, i)) for i in range(8)]
+    ref = O.formal_sum(terms).dense()
+    hits = 0
+    for seed in range(10):
+        y = O.round_sum_adaptive_krp(terms, eps, 0.05, seed)
+        hits += np.linalg.norm(y.dense() - ref) / np.linalg.norm(ref) <= 1.5 * eps
+    assert hits >= 9
+    x = O.random_gaussian_tt([5, 4, 5], [1, 3, 3, 1], 37)
+    z = O.round_sum_adaptive_krp([x, O.scaled(x, -1.0)], 1e-6, 0.05, 4)
+    assert max(z.ranks) == 1 and O.norm_exact(z) <= 1e-10 * O.norm_exact(x)
+    x = O.random_gaussian_tt([6, 5, 6], [1, 4, 4, 1], 52)
+    assert O.relative_error(x, O.round_sum_adaptive_krp([x], 1e-10, 0.05, 8)) <= 1e-9
+    with pytest.raises(O.OracleError, match="EmptyTermList"):
+        O.round_sum_adaptive_krp([], 1e-6, 0.05, 1)
+    with pytest.raises(O.OracleError, match="ModeSizeMismatch"):
+        O.round_sum_adaptive_krp([O.random_gaussian_tt([4, 4], [1, 2, 1], 3),
+                                  O.random_gaussian_tt([4, 5], [1, 2, 1], 3)], 1e-6, 0.05, 1)
+
+
 # ---- hand KATs ---------------------------------------------------------------------------
 
 def test_tiny_rank1_kats(oracle):
