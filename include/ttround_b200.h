@@ -157,6 +157,12 @@ ttr_status ttr_plan_destroy(ttr_plan* plan);
 
 ttr_status ttr_round_adaptive_krp(ttr_ctx* ctx, const ttr_tt* tt, const ttr_adaptive_cfg* cfg,
                                   ttr_tt** out);
+/* Adaptive rounding of sum(terms) WITHOUT forming the formal sum
+ * (round_sum_adaptive_krp, sum_round.hpp:29 / sum_round.cpp:52-173): one
+ * shared factor draw, one KRP sketch per term; eps > 0, f_inc in (0,1). An
+ * empty list is EmptyTermList, differing mode sizes ModeSizeMismatch. */
+ttr_status ttr_round_sum_adaptive_krp(ttr_ctx* ctx, const ttr_tt* const* terms, int64_t count, double eps,
+                                      double f_inc, uint64_t seed, int rng_mode, ttr_tt** out);
 ttr_status ttr_round_deterministic_tol(ttr_ctx* ctx, const ttr_tt* tt, double eps, ttr_tt** out);
 ttr_status ttr_round_deterministic_ranks(ttr_ctx* ctx, const ttr_tt* tt, const int64_t* target_ranks,
                                          int64_t count, ttr_tt** out);

@@ -8,6 +8,7 @@
 //   ttround::TTTensor (device resident)     tensor.hpp:124-149
 //   round_fixed_krp                         round_rand.hpp:14-15
 //   AdaptiveConfig / round_adaptive_krp     round_rand.hpp:18-31
+//   TTSum / round_sum_adaptive_krp          sum_round.hpp:11-29
 //   round_deterministic (tolerance / ranks) orthogonalize.hpp:50,54
 //   estimate_norm_krp                       sketch.hpp:63
 //   norm_exact / relative_error / formal_sum / scaled   tensor.hpp:172-191
@@ -162,6 +163,29 @@ inline TTTensor round_adaptive_krp(const TTTensor& tt, const AdaptiveConfig& cfg
     ttr_tt* out = nullptr;
     check(ttr_round_adaptive_krp(tt.context().get(), tt.get(), &c, &out));
     return TTTensor(out, tt.context());
+}
+
+//! A sum of TT tensors kept as its list of summands (sum_round.hpp:11-21).
+struct TTSum {
+    std::vector<TTTensor> terms;
+    static TTSum of(std::vector<TTTensor> terms) {
+        if (terms.empty()) throw Error(Errc::EmptyTermList, "sum of no TT terms");
+        TTSum s;
+        s.terms = std::move(terms);
+        return s;
+    }
+};
+
+//! Adaptive rounding of a sum without the formal sum (sum_round.hpp:29).
+inline TTTensor round_sum_adaptive_krp(const TTSum& sum, double eps, double f_inc, std::uint64_t seed,
+                                       RngMode rng = RngMode::Philox) {
+    std::vector<const ttr_tt*> hs;
+    for (const auto& t : sum.terms) hs.push_back(t.get());
+    ttr_tt* out = nullptr;
+    Context& ctx = sum.terms.front().context();
+    check(ttr_round_sum_adaptive_krp(ctx.get(), hs.data(), static_cast<int64_t>(hs.size()), eps, f_inc, seed,
+                                     static_cast<int>(rng), &out));
+    return TTTensor(out, ctx);
 }
 
 inline TTTensor round_deterministic(const TTTensor& tt, double eps) {

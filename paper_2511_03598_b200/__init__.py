@@ -450,6 +450,18 @@ def round_adaptive_krp(tt: TTTensor, cfg: AdaptiveConfig) -> TTTensor:
     return TTTensor._new(tt.ctx, lib().ttr_round_adaptive_krp, tt.ctx._h, tt._h, C.byref(c))
 
 
+def round_sum_adaptive_krp(terms: Sequence[TTTensor], eps: float, f_inc: float = 0.05, seed: int = 0,
+                           rng: int = RNG_PHILOX) -> TTTensor:
+    """Adaptive rounding of sum(terms) without forming the formal sum
+    (ttr_round_sum_adaptive_krp; sum_round.cpp:52-173)."""
+    if len(terms) == 0:
+        raise TTRoundError(7, "EmptyTermList: sum of no TT terms")
+    ctx = terms[0].ctx
+    arr = (C.c_void_p * len(terms))(*[t._h.value for t in terms])
+    return TTTensor._new(ctx, lib().ttr_round_sum_adaptive_krp, ctx._h, arr, C.c_int64(len(terms)), C.c_double(eps),
+                         C.c_double(f_inc), C.c_uint64(seed), C.c_int(rng))
+
+
 def round_deterministic(tt: TTTensor, eps: Optional[float] = None,
                         target_ranks: Optional[Sequence[int]] = None) -> TTTensor:
     if target_ranks is not None:

@@ -333,6 +333,21 @@ ttr_status ttr_round_adaptive_krp(ttr_ctx* ctx, const ttr_tt* tt, const ttr_adap
     });
 }
 
+ttr_status ttr_round_sum_adaptive_krp(ttr_ctx* ctx, const ttr_tt* const* terms, int64_t count, double eps, double f_inc,
+                                      uint64_t seed, int rng_mode, ttr_tt** out) {
+    return guard([&] {
+        need(ctx && out, "null argument");
+        if (count < 1 || !terms) fail(Errc::EmptyTermList, "sum of no TT terms");
+        std::vector<const TTDev*> ts;
+        for (int64_t i = 0; i < count; ++i) {
+            check_same_ctx(ctx, terms[i]);
+            ts.push_back(terms[i]->t.get());
+        }
+        need(rng_mode == TTR_RNG_PHILOX || rng_mode == TTR_RNG_XOSHIRO, "unknown rng mode");
+        *out = wrap(round_sum_adaptive_krp(ctx->c, ts, eps, f_inc, seed, rng_mode));
+    });
+}
+
 ttr_status ttr_round_deterministic_tol(ttr_ctx* ctx, const ttr_tt* tt, double eps, ttr_tt** out) {
     return guard([&] {
         check_same_ctx(ctx, tt);

@@ -12,6 +12,7 @@
 #include "common.cuh"
 #include "rng_host.h"
 #include "tt_round.h"
+#include "sketch.cuh"
 
 namespace ttr {
 
@@ -236,80 +237,6 @@ double relative_error(Ctx& c, const TTDev& a, const TTDev& b) {  // tensor.cpp:2
     return na == 0.0 ? nd : nd / na;
 }
 
-// ---------------------------------------------------------------------------
-// KRP sketch state — sketch.cpp:44-92. Factors and contractions of modes
-// start..d with a column capacity so that adaptive appends are in place.
-struct Sketch {
-    Ctx& c;
-    const TTDev& t;
-    i64 cap, cols = 0;
-    std::vector<DBuf> omega;  // index k (1-based mode), n_k x cap, ld ldo[k]
-    std::vector<i64> ldo;
-    std::vector<DBuf> W;      // r_{k-1} x cap, ld ldw[k]
-    std::vector<i64> ldw;
-    std::vector<DBuf> Wt;     // cap x r_{k-1}, ld cap_even
-    i64 ldwt;
-    DBuf ones;
-    std::vector<i64> width;   // current column count per mode
-    int rng_mode;
-    std::uint64_t seed;
-    XoshiroGauss xo;
-
-    Sketch(Ctx& cc, const TTDev& tt, i64 capacity, int mode, std::uint64_t s)
-        : c(cc), t(tt), cap(capacity), rng_mode(mode), seed(s), xo(s) {
-        const i64 d = t.d();
-        omega.resize(d + 1);
-        W.resize(d + 1);
-        Wt.resize(d + 2);
-        ldo.assign(d + 1, 0);
-        ldw.assign(d + 1, 0);
-        width.assign(d + 2, 0);
-        ldwt = even_ld(cap);
-        for (i64 k = 2; k <= d; ++k) {
-            ldo[k] = even_ld(t.n[k - 1]);
-            omega[k] = DBuf(c, static_cast<std::size_t>(ldo[k] * cap));
-            ldw[k] = even_ld(t.r[k - 1]);
-            W[k] = DBuf(c, static_cast<std::size_t>(ldw[k] * cap));
-            if (k >= 3) Wt[k] = DBuf(c, static_cast<std::size_t>(ldwt * t.r[k - 1]));
-        }
-        ones = DBuf(c, static_cast<std::size_t>(ldwt));
-        fill(c, ones.p, static_cast<std::size_t>(ldwt), 1.0);
-    }
-
-    // Draw `extra` fresh columns for modes start..d (draw_gaussian_factors,
-    // sketch.cpp:44-56, in the reference's order) and contract them
-    // (contract_tail, sketch.cpp:29-40), appending to W_start..W_d.
-    void append(i64 start, i64 extra) {
-        const i64 d = t.d();
-        const i64 col0 = width[d];
-        if (col0 + extra > cap) throw Error(TTR_ERR_INTERNAL, "sketch capacity exceeded");
-        for (i64 k = start; k <= d; ++k) {
-            const i64 nk = t.n[k - 1];
-            double* dst = omega[k].p + col0 * ldo[k];
-            if (rng_mode == TTR_RNG_PHILOX) {
-                philox_factor(c, seed, k, nk, extra, col0, dst, ldo[k]);
-            } else {
-                auto host = xo.matrix(nk, extra);
-                c.counts.rng += static_cast<std::uint64_t>(nk * extra);
-                for (i64 j = 0; j < extra; ++j)
-                    TTR_CUDA(cudaMemcpyAsync(dst + j * ldo[k], host.data() + j * nk, sizeof(double) * nk,
-                                             cudaMemcpyHostToDevice, c.stream));
-                TTR_CUDA(cudaStreamSynchronize(c.stream));  // host staging buffer lifetime
-            }
-        }
-        SketchScope scope(c);
-        for (i64 k = d; k >= start; --k) {
-            const i64 rl = t.r[k - 1], nk = t.n[k - 1], rr = t.r[k];
-            if (c.io) c.io->wait_in(c.stream, static_cast<std::size_t>(k - 1));  // core k-1 arrived (H2D)
-            const double* wt_next = (k == d) ? ones.p : Wt[k + 1].p + col0;
-            const i64 ld_next = ldwt;
-            double* wt_out = (k >= 3) ? Wt[k].p + col0 : nullptr;
-            krp_step(c, rl, nk, rr, extra, t.core(k - 1), omega[k].p + col0 * ldo[k], ldo[k], k == d ? ones.p : wt_next,
-                     ld_next, W[k].p + col0 * ldw[k], ldw[k], wt_out, ldwt, k == d);
-            width[k] = col0 + extra;
-        }
-    }
-};
 
 // krp_partial_contractions_rl (sketch.cpp:67-78) for caller-supplied factors
 // (host_factors = Omega_start..Omega_d, n_k x cols each) or, when NULL,

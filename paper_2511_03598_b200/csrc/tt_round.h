@@ -98,6 +98,9 @@ struct Plan {
 };
 
 std::unique_ptr<TTDev> round_adaptive_krp(Ctx& c, const TTDev& t, const AdaptiveCfg& cfg, std::vector<double>* trace);
+// sum_round.cpp:52-173 — adaptive rounding of sum(terms) without the formal sum (tt_sum.cu)
+std::unique_ptr<TTDev> round_sum_adaptive_krp(Ctx& c, const std::vector<const TTDev*>& terms, double eps, double f_inc,
+                                              std::uint64_t seed, int rng_mode);
 double estimate_norm_krp(Ctx& c, const TTDev& t, i64 width, std::uint64_t seed, int rng_mode);
 std::unique_ptr<TTDev> round_deterministic_tol(Ctx& c, const TTDev& t, double eps);
 std::unique_ptr<TTDev> round_deterministic_ranks(Ctx& c, const TTDev& t, const std::vector<i64>& ranks);

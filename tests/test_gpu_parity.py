@@ -227,6 +227,50 @@ def test_host_streaming_plan(P, O):
     plan.close()
 
 
+# ---- sum of TT tensors without the formal sum (sum_round.cpp) ----------------------------------
+
+@pytest.mark.parametrize("rng_mode", [0, 1])
+def test_sum_round_parity(P, O, rng_mode):
+    """Eight random terms (test_sum_round.cpp:100-126 shapes): identical ranks and
+    <= 1e-10 against the oracle's round_sum_adaptive_krp, both generators."""
+    terms = [O.random_gaussian_tt([8] * 4, [1, 3, 3, 3, 1], O.derive_seed(99, i)) for i in range(8)]
+    for seed in (0, 3):
+        ref = O.round_sum_adaptive_krp(terms, 1e-6, 0.05, seed, rng=rng_mode)
+        y = P.round_sum_adaptive_krp([to_device(t) for t in terms], 1e-6, 0.05, seed, rng=rng_mode)
+        assert y.ranks() == ref.ranks
+        assert rel_err_vs_ref(ref, y) <= 1e-10
+
+
+def test_sum_round_two_part_parity(P, O):
+    """The structure of every config input (X + eps Z) rounded as a 2-term sum:
+    ranks and values match the oracle; the sum sketch never touches the formal
+    sum's zero blocks."""
+    x = O.random_gaussian_tt([16] * 6, [1] + [20] * 5 + [1], 5)
+    z = O.random_gaussian_tt([16] * 6, [1] + [40] * 5 + [1], 6)
+    x = O.scaled(x, 1.0 / O.norm_exact(x))
+    z = O.scaled(z, 1e-6 / O.norm_exact(z))
+    ref = O.round_sum_adaptive_krp([x, z], 1e-4, 0.05, 7, rng=O.PHILOX)
+    y = P.round_sum_adaptive_krp([to_device(x), to_device(z)], 1e-4, 0.05, 7)
+    assert y.ranks() == ref.ranks
+    assert rel_err_vs_ref(ref, y) <= 1e-10
+
+
+def test_sum_round_edge_cases(P, O):
+    x = O.random_gaussian_tt([5, 4, 5], [1, 3, 3, 1], 37)
+    y = P.round_sum_adaptive_krp([to_device(x), to_device(O.scaled(x, -1.0))], 1e-6, 0.05, 4)
+    assert max(y.ranks()) == 1 and P.norm_exact(y) <= 1e-10 * O.norm_exact(x)
+    x = O.random_gaussian_tt([6, 5, 6], [1, 4, 4, 1], 52)
+    y = P.round_sum_adaptive_krp([to_device(x)], 1e-10, 0.05, 8)
+    assert rel_err_vs_ref(x, y) <= 1e-9
+    with pytest.raises(P.TTRoundError) as e:
+        P.round_sum_adaptive_krp([to_device(O.random_gaussian_tt([4, 4], [1, 2, 1], 3)),
+                                  to_device(O.random_gaussian_tt([4, 5], [1, 2, 1], 3))], 1e-6, 0.05, 1)
+    assert e.value.code == "ModeSizeMismatch"
+    with pytest.raises(P.TTRoundError) as e:
+        P.round_sum_adaptive_krp([to_device(x)], 0.0, 0.05, 1)
+    assert e.value.code == "InvalidArgument"
+
+
 # ---- adaptive KRP rounding -------------------------------------------------------------------
 
 @pytest.mark.parametrize("rng_mode", [0, 1])
