@@ -128,6 +128,9 @@ ttr_status ttr_tt_formal_sum(ttr_ctx* ctx, const ttr_tt* const* terms, int count
  * exp(-|j/(n-1) - c_ab| / ell), c_ab ~ U(0,1) from splitmix64(derive_seed(seed, 100+t)). */
 ttr_status ttr_tt_kernel_sum(ttr_ctx* ctx, int64_t d, int64_t n, int64_t r, int64_t terms, double ell,
                              uint64_t seed, ttr_tt** out);
+/* Term t of that sum alone (already weighted by 2^-t): config 4 as a TT sum. */
+ttr_status ttr_tt_kernel_term(ttr_ctx* ctx, int64_t d, int64_t n, int64_t r, int64_t term, double ell,
+                              uint64_t seed, ttr_tt** out);
 ttr_status ttr_tt_scale(ttr_ctx* ctx, ttr_tt* tt, double alpha);
 ttr_status ttr_norm_exact(ttr_ctx* ctx, const ttr_tt* tt, double* out);
 ttr_status ttr_relative_error(ttr_ctx* ctx, const ttr_tt* a, const ttr_tt* b, double* out);

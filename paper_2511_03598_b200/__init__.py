@@ -215,6 +215,13 @@ class TTTensor:
                              C.c_int64(terms), C.c_double(ell), C.c_uint64(seed))
 
     @staticmethod
+    def kernel_term(d, n, r, term, ell, seed, ctx: Optional[Context] = None) -> "TTTensor":
+        """Term `term` of kernel_sum alone (weight 2^-term): config 4 kept as a TT sum."""
+        ctx = ctx or default_context()
+        return TTTensor._new(ctx, lib().ttr_tt_kernel_term, ctx._h, C.c_int64(d), C.c_int64(n), C.c_int64(r),
+                             C.c_int64(term), C.c_double(ell), C.c_uint64(seed))
+
+    @staticmethod
     def two_part_philox(d, n, rx, rz, eps, seed, ctx: Optional[Context] = None) -> "TTTensor":
         """X/||X|| + eps Z/||Z|| with Gaussian X (ranks rx) and Z (ranks rz) drawn on the device
         from derive_seed(seed, 1) and derive_seed(seed, 2) (BASELINE configs 1, 2, 3, 5b)."""

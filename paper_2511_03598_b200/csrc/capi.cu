@@ -206,6 +206,15 @@ ttr_status ttr_tt_kernel_sum(ttr_ctx* ctx, int64_t d, int64_t n, int64_t r, int6
     });
 }
 
+ttr_status ttr_tt_kernel_term(ttr_ctx* ctx, int64_t d, int64_t n, int64_t r, int64_t term, double ell, uint64_t seed,
+                             ttr_tt** out) {
+    return guard([&] {
+        need(ctx && out, "null argument");
+        need(d >= 1 && n >= 1 && r >= 1 && term >= 0 && ell > 0.0, "bad kernel-sum parameters");
+        *out = wrap(kernel_term_tt(ctx->c, d, n, r, term, ell, seed));
+    });
+}
+
 ttr_status ttr_tt_formal_sum(ttr_ctx* ctx, const ttr_tt* const* terms, int count, ttr_tt** out) {
     return guard([&] {
         need(ctx && out, "null argument");

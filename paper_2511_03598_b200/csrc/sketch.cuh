@@ -82,4 +82,76 @@ struct Sketch {
     }
 };
 
+// The same state for a batch of identically shaped TT tensors sharing ONE
+// factor draw (sum of TT tensors, tt_sum.cu): the per-term contractions are
+// stored STACKED, W_k = [W_k^(1); ...; W_k^(s)] ((s r_{k-1}) x cap), so the
+// sketch of the sum  sum_i V_i W^(i)  is one GEMM with the concatenated V, and
+// each append is one strided-batch KRP step per mode for all terms.
+struct BatchSketch {
+    Ctx& c;
+    const TTBatch& t;
+    i64 cap, s;
+    std::vector<DBuf> omega;  // n_k x cap, shared by the terms
+    std::vector<i64> ldo;
+    std::vector<DBuf> W;      // (s r_{k-1}) x cap, ld ldw[k] = s r_{k-1}
+    std::vector<i64> ldw;
+    std::vector<DBuf> Wt;     // per term cap x r_{k-1} (ld ldwt), term stride ldwt r_{k-1}
+    i64 ldwt;
+    DBuf ones;
+    std::vector<i64> width;
+    int rng_mode;
+    std::uint64_t seed;
+    XoshiroGauss xo;
+
+    BatchSketch(Ctx& cc, const TTBatch& tt, i64 capacity, int mode, std::uint64_t sd)
+        : c(cc), t(tt), cap(capacity), s(tt.batch), rng_mode(mode), seed(sd), xo(sd) {
+        const i64 d = t.d();
+        omega.resize(d + 1);
+        W.resize(d + 1);
+        Wt.resize(d + 2);
+        ldo.assign(d + 1, 0);
+        ldw.assign(d + 1, 0);
+        width.assign(d + 2, 0);
+        ldwt = even_ld(cap);
+        for (i64 k = 2; k <= d; ++k) {
+            ldo[k] = even_ld(t.n[k - 1]);
+            omega[k] = DBuf(c, static_cast<std::size_t>(ldo[k] * cap));
+            ldw[k] = s * t.r[k - 1];
+            W[k] = DBuf(c, static_cast<std::size_t>(ldw[k] * cap));
+            if (k >= 3) Wt[k] = DBuf(c, static_cast<std::size_t>(ldwt * t.r[k - 1] * s));
+        }
+        ones = DBuf(c, static_cast<std::size_t>(ldwt));
+        fill(c, ones.p, static_cast<std::size_t>(ldwt), 1.0);
+    }
+
+    void append(i64 start, i64 extra) {  // Sketch::append for all terms at once
+        const i64 d = t.d();
+        const i64 col0 = width[d];
+        if (col0 + extra > cap) throw Error(TTR_ERR_INTERNAL, "sketch capacity exceeded");
+        for (i64 k = start; k <= d; ++k) {
+            const i64 nk = t.n[k - 1];
+            double* dst = omega[k].p + col0 * ldo[k];
+            if (rng_mode == TTR_RNG_PHILOX) {
+                philox_factor(c, seed, k, nk, extra, col0, dst, ldo[k]);
+            } else {
+                auto host = xo.matrix(nk, extra);
+                c.counts.rng += static_cast<std::uint64_t>(nk * extra);
+                for (i64 j = 0; j < extra; ++j)
+                    TTR_CUDA(cudaMemcpyAsync(dst + j * ldo[k], host.data() + j * nk, sizeof(double) * nk,
+                                             cudaMemcpyHostToDevice, c.stream));
+                TTR_CUDA(cudaStreamSynchronize(c.stream));
+            }
+        }
+        SketchScope scope(c);
+        for (i64 k = d; k >= start; --k) {
+            const i64 rl = t.r[k - 1], nk = t.n[k - 1], rr = t.r[k];
+            const bool last = (k == d);
+            krp_step_batched(c, rl, nk, rr, extra, t.core(0, k - 1), t.stride, omega[k].p + col0 * ldo[k], ldo[k], 0,
+                             last ? ones.p : Wt[k + 1].p + col0, ldwt, last ? 0 : ldwt * rr, W[k].p + col0 * ldw[k],
+                             ldw[k], rl, k >= 3 ? Wt[k].p + col0 : nullptr, ldwt, ldwt * rl, s, last);
+            width[k] = col0 + extra;
+        }
+    }
+};
+
 }  // namespace ttr

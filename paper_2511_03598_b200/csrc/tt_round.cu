@@ -125,28 +125,32 @@ std::unique_ptr<TTDev> random_philox_tt(Ctx& c, const std::vector<i64>& n, const
 // BASELINE config 4: sum_{t<terms} 2^-t * (rank-r TT with slices
 // X_k(a,:,b) = exp(-|t_j - c_ab| / ell)), c_ab ~ U(0,1) from splitmix64 seeded
 // with derive_seed(seed, 100 + t) (the same definition as oracle/kernel_sum_tt).
-std::unique_ptr<TTDev> kernel_sum_tt(Ctx& c, i64 d, i64 n, i64 r, i64 terms, double ell, std::uint64_t seed) {
-    std::vector<std::unique_ptr<TTDev>> parts;
-    std::vector<const TTDev*> ptrs;
+std::unique_ptr<TTDev> kernel_term_tt(Ctx& c, i64 d, i64 n, i64 r, i64 t, double ell, std::uint64_t seed) {
     std::vector<i64> modes(d, n), ranks(d + 1, r);
     ranks.front() = ranks.back() = 1;
     DBuf cab(c, static_cast<std::size_t>(r * r));
     std::vector<double> host(static_cast<std::size_t>(r * r));
+    std::uint64_t s = derive_seed(seed, 100 + static_cast<std::uint64_t>(t));
+    auto part = std::make_unique<TTDev>(c, modes, ranks);
+    for (i64 k = 0; k < d; ++k) {
+        const i64 rl = ranks[k], rr = ranks[k + 1];
+        for (i64 b = 0; b < rr; ++b)
+            for (i64 a = 0; a < rl; ++a)
+                host[static_cast<std::size_t>(a + b * rl)] = static_cast<double>(splitmix64(s) >> 11) * 0x1.0p-53;
+        TTR_CUDA(cudaMemcpyAsync(cab.p, host.data(), sizeof(double) * rl * rr, cudaMemcpyHostToDevice, c.stream));
+        exp_core(c, cab.p, rl, n, rr, ell, part->core(k));
+        TTR_CUDA(cudaStreamSynchronize(c.stream));  // host staging buffer reuse
+    }
+    scale_tt(c, *part, std::ldexp(1.0, -static_cast<int>(t)));
+    return part;
+}
+
+std::unique_ptr<TTDev> kernel_sum_tt(Ctx& c, i64 d, i64 n, i64 r, i64 terms, double ell, std::uint64_t seed) {
+    std::vector<std::unique_ptr<TTDev>> parts;
+    std::vector<const TTDev*> ptrs;
     for (i64 t = 0; t < terms; ++t) {
-        std::uint64_t s = derive_seed(seed, 100 + static_cast<std::uint64_t>(t));
-        auto part = std::make_unique<TTDev>(c, modes, ranks);
-        for (i64 k = 0; k < d; ++k) {
-            const i64 rl = ranks[k], rr = ranks[k + 1];
-            for (i64 b = 0; b < rr; ++b)
-                for (i64 a = 0; a < rl; ++a)
-                    host[static_cast<std::size_t>(a + b * rl)] = static_cast<double>(splitmix64(s) >> 11) * 0x1.0p-53;
-            TTR_CUDA(cudaMemcpyAsync(cab.p, host.data(), sizeof(double) * rl * rr, cudaMemcpyHostToDevice, c.stream));
-            exp_core(c, cab.p, rl, n, rr, ell, part->core(k));
-            TTR_CUDA(cudaStreamSynchronize(c.stream));  // host staging buffer reuse
-        }
-        scale_tt(c, *part, std::ldexp(1.0, -static_cast<int>(t)));
-        ptrs.push_back(part.get());
-        parts.push_back(std::move(part));
+        parts.push_back(kernel_term_tt(c, d, n, r, t, ell, seed));
+        ptrs.push_back(parts.back().get());
     }
     return formal_sum(c, ptrs);
 }

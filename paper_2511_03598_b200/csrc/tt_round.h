@@ -59,6 +59,7 @@ std::unique_ptr<TTDev> copy_tt(Ctx& c, const TTDev& t);
 std::unique_ptr<TTDev> random_philox_tt(Ctx& c, const std::vector<i64>& n, const std::vector<i64>& r, std::uint64_t seed);
 std::unique_ptr<TTDev> formal_sum(Ctx& c, const std::vector<const TTDev*>& terms);
 std::unique_ptr<TTDev> kernel_sum_tt(Ctx& c, i64 d, i64 n, i64 r, i64 terms, double ell, std::uint64_t seed);
+std::unique_ptr<TTDev> kernel_term_tt(Ctx& c, i64 d, i64 n, i64 r, i64 t, double ell, std::uint64_t seed);
 void scale_tt(Ctx& c, TTDev& t, double alpha);
 std::unique_ptr<TTDev> orthogonalize_rl_public(Ctx& c, const TTDev& t);
 double norm_exact(Ctx& c, const TTDev& t);

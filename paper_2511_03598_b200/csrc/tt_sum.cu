@@ -43,13 +43,34 @@ std::unique_ptr<TTDev> round_sum_adaptive_krp(Ctx& c, const std::vector<const TT
     }
     // column capacity of every term's sketch: rbar <= sum of the term ranks
     const i64 cap = std::max(width, rsum + ceil_frac(f_inc, rsum) + 1);
+    // Identically shaped terms (e.g. the 20 terms of config 4) run batched:
+    // one stacked sketch (BatchSketch), the sketch of the sum as ONE GEMM, the
+    // next working unfolding as one strided-batch GEMM. Otherwise one Sketch
+    // per term (same seed and draw sequence: the shared factor draw).
+    bool same = true;
+    for (const TTDev* t : terms) same = same && t->r == terms.front()->r;
+    std::unique_ptr<TTBatch> tb;
+    std::unique_ptr<BatchSketch> bsk;
     std::vector<std::unique_ptr<Sketch>> sk;
-    for (const TTDev* t : terms) {
-        // same seed and draw sequence for every term: the shared factor draw
-        // (Philox: keyed by (mode, global column); xoshiro: identical streams)
-        sk.push_back(std::make_unique<Sketch>(c, *t, cap, rng_mode, seed));
-        sk.back()->append(2, width);
+    if (same && s_count > 1) {
+        tb = std::make_unique<TTBatch>(c, s_count, modes, terms.front()->r);
+        for (i64 i = 0; i < s_count; ++i)
+            for (i64 k = 0; k < d; ++k)
+                TTR_CUDA(cudaMemcpyAsync(tb->core(i, k), terms[i]->core(k), sizeof(double) * tb->core_size(k),
+                                         cudaMemcpyDeviceToDevice, c.stream));
+        bsk = std::make_unique<BatchSketch>(c, *tb, cap, rng_mode, seed);
+        bsk->append(2, width);
+    } else {
+        for (const TTDev* t : terms) {
+            sk.push_back(std::make_unique<Sketch>(c, *t, cap, rng_mode, seed));
+            sk.back()->append(2, width);
+        }
     }
+    // W_k^(i)(:, col0:) of term i
+    auto w_of = [&](i64 i, i64 k, i64 col0) -> std::pair<const double*, i64> {
+        if (bsk) return {bsk->W[k].p + i * terms[i]->r[k - 1] + col0 * bsk->ldw[k], bsk->ldw[k]};
+        return {sk[i]->W[k].p + col0 * sk[i]->ldw[k], sk[i]->ldw[k]};
+    };
     // norm estimate of the sum from the initial sketches (sum_round.cpp:78-91)
     const i64 n0 = modes[0];
     DBuf S0(c, static_cast<std::size_t>(n0 * width)), Si(c, static_cast<std::size_t>(n0 * width));
@@ -57,7 +78,8 @@ std::unique_ptr<TTDev> round_sum_adaptive_krp(Ctx& c, const std::vector<const TT
     double max_term = 0.0;
     for (i64 i = 0; i < s_count; ++i) {
         const TTDev& t = *terms[i];
-        gemm(c, false, n0, width, t.r[1], 1.0, t.core(0), n0, sk[i]->W[2].p, sk[i]->ldw[2], 0.0, Si.p, n0);
+        auto w2 = w_of(i, 2, 0);
+        gemm(c, false, n0, width, t.r[1], 1.0, t.core(0), n0, w2.first, w2.second, 0.0, Si.p, n0);
         max_term = std::max(max_term, frob_norm(c, n0, width, Si.p, n0) / std::sqrt(static_cast<double>(width)));
         axpy_matrix(c, n0, width, 1.0, Si.p, n0, S0.p, n0);
     }
@@ -117,11 +139,17 @@ std::unique_ptr<TTDev> round_sum_adaptive_krp(Ctx& c, const std::vector<const TT
         b_init = std::min(b_init, rbar);
         // S = sum_i V_i W_{k+1}^(i)(:, cols) — the sketch of the sum
         auto sketch_into = [&](i64 col0, i64 ncols) {
+            if (bsk) {  // V [W^(1); ...; W^(s)]: one GEMM
+                gemm(c, false, rows, ncols, vcols, 1.0, v, rows, bsk->W[k + 1].p + col0 * bsk->ldw[k + 1],
+                     bsk->ldw[k + 1], 0.0, Sb.p, rows);
+                return;
+            }
             i64 c0 = 0;
             for (i64 i = 0; i < s_count; ++i) {
                 const i64 rk = terms[i]->r[k];
-                gemm(c, false, rows, ncols, rk, 1.0, v + c0 * rows, rows, sk[i]->W[k + 1].p + col0 * sk[i]->ldw[k + 1],
-                     sk[i]->ldw[k + 1], i == 0 ? 0.0 : 1.0, Sb.p, rows);
+                auto wk = w_of(i, k + 1, col0);
+                gemm(c, false, rows, ncols, rk, 1.0, v + c0 * rows, rows, wk.first, wk.second, i == 0 ? 0.0 : 1.0,
+                     Sb.p, rows);
                 c0 += rk;
             }
         };
@@ -133,9 +161,14 @@ std::unique_ptr<TTDev> round_sum_adaptive_krp(Ctx& c, const std::vector<const TT
         const i64 b_inc = ceil_frac(f_inc, rbar);
         while (q < rbar) {
             // residual_sketch_sum (sum_round.cpp:21-50): one shared fresh draw
-            for (i64 i = 0; i < s_count; ++i) {
-                const i64 have = sk[i]->width[k + 1];
-                if (have < q + b_inc) sk[i]->append(k + 1, q + b_inc - have);
+            if (bsk) {
+                const i64 have = bsk->width[k + 1];
+                if (have < q + b_inc) bsk->append(k + 1, q + b_inc - have);
+            } else {
+                for (i64 i = 0; i < s_count; ++i) {
+                    const i64 have = sk[i]->width[k + 1];
+                    if (have < q + b_inc) sk[i]->append(k + 1, q + b_inc - have);
+                }
             }
             sketch_into(q, b_inc);
             gemm(c, true, q, b_inc, rows, 1.0, Qb.p, rows, Sb.p, rows, 0.0, P.p, q);
@@ -169,6 +202,13 @@ std::unique_ptr<TTDev> round_sum_adaptive_krp(Ctx& c, const std::vector<const TT
         } else {
             const i64 rows1 = q * nk1;
             i64 c0 = 0, oc = 0;
+            if (tb) {  // M_i H(X_{k+1}^(i)) for all terms: one strided-batch GEMM
+                const i64 rk = tb->r[k], rk1 = tb->r[k + 1];
+                gemm_batched(c, false, q, nk1 * rk1, rk, 1.0, Mb.p, ldm, rk * ldm, tb->core(0, k), rk, tb->stride, 0.0,
+                             vnext.p, q, rows1 * rk1, s_count);
+                std::swap(vbuf, vnext);
+                continue;
+            }
             for (i64 i = 0; i < s_count; ++i) {
                 const TTDev& t = *terms[i];
                 // the horizontal product (q x n r_{k+1}) is the next vertical block (q n x r_{k+1})

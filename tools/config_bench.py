@@ -66,6 +66,41 @@ def main():
             ms, fl, out = timed(ctx, stream, lambda: P.round_adaptive_krp(y, c), 3)
             rec = dict(config="4 adaptive KRP d=12 n=128 kernel-sum 400, tol 1e-6", ms_eager=ms,
                        tflops=fl / ms / 1e9, ranks=out.ranks())
+        elif cfg == "3sum":
+            # config-3 input kept as its two summands: round_sum_adaptive_krp (no formal
+            # sum, one sketch per term) vs round_adaptive_krp of the formal sum, tol 1e-6
+            from paper_2511_03598_b200.seeds import derive_seed
+            modes = [64] * 30
+            x = P.TTTensor.random_philox(modes, [1] + [100] * 29 + [1], derive_seed(1003, 1), ctx)
+            z = P.TTTensor.random_philox(modes, [1] + [300] * 29 + [1], derive_seed(1003, 2), ctx)
+            x = P.scaled(x, 1.0 / P.norm_exact(x))
+            z = P.scaled(z, 1e-8 / P.norm_exact(z))
+            y = P.formal_sum([x, z])
+            ms_s, fl_s, out_s = timed(ctx, stream, lambda: P.round_sum_adaptive_krp([x, z], 1e-6, 0.05, 7), 3)
+            c = P.AdaptiveConfig(tolerance=1e-6, f_init=0.25, f_inc=0.05, seed=7)
+            ms_f, fl_f, out_f = timed(ctx, stream, lambda: P.round_adaptive_krp(y, c), 3)
+            rec = dict(config="3sum adaptive tol 1e-6, d=30 n=64, X(100) + 1e-8 Z(300)", ms_sum=ms_s,
+                       tflops_sum=fl_s / ms_s / 1e9, ranks_sum=out_s.ranks()[:4], ms_formal=ms_f,
+                       tflops_formal=fl_f / ms_f / 1e9, ranks_formal=out_f.ranks()[:4],
+                       sketch_flop_ratio=(100 ** 2 + 300 ** 2) / 400 ** 2,
+                       rel_diff=P.relative_error(out_f, out_s))
+        elif cfg == "4sum":
+            # config 4's input IS a sum of 20 rank-20 terms: round it without the formal
+            # sum (one 20-rank sketch per term) vs the formal-sum adaptive rounding
+            terms = [P.TTTensor.kernel_term(12, 128, 20, t, 0.3, 1004, ctx) for t in range(20)]
+            y = P.formal_sum(terms)
+            ms_s, fl_s, out_s = timed(ctx, stream, lambda: P.round_sum_adaptive_krp(terms, 1e-6, 0.04, 7), 3)
+            c = P.AdaptiveConfig(tolerance=1e-6, f_init=0.1, f_inc=0.04, seed=7)
+            ms_f, fl_f, out_f = timed(ctx, stream, lambda: P.round_adaptive_krp(y, c), 3)
+            ctx.reset_counters()
+            P.round_sum_adaptive_krp(terms, 1e-6, 0.04, 7)
+            sk_sum = ctx.counters().sketch
+            ctx.reset_counters()
+            P.round_adaptive_krp(y, c)
+            sk_formal = ctx.counters().sketch
+            rec = dict(config="4sum: config 4 as 20 terms, adaptive tol 1e-6", ms_sum=ms_s, ranks_sum=out_s.ranks(),
+                       ms_formal=ms_f, ranks_formal=out_f.ranks(), sketch_flops_sum=sk_sum,
+                       sketch_flops_formal=sk_formal, rel_diff=P.relative_error(out_f, out_s))
         else:
             continue
         print(json.dumps(rec), flush=True)
