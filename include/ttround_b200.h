@@ -166,6 +166,10 @@ ttr_status ttr_round_adaptive_krp(ttr_ctx* ctx, const ttr_tt* tt, const ttr_adap
  * empty list is EmptyTermList, differing mode sizes ModeSizeMismatch. */
 ttr_status ttr_round_sum_adaptive_krp(ttr_ctx* ctx, const ttr_tt* const* terms, int64_t count, double eps,
                                       double f_inc, uint64_t seed, int rng_mode, ttr_tt** out);
+/* compression_pass (round_rand.hpp / round_rand.cpp:155-179): right-to-left
+ * QR + tolerance-truncated SVD sweep of a LEFT-ORTHOGONAL tensor (e.g. the
+ * output of ttr_round_adaptive_krp; "Adap-R"). NotLeftOrthogonal otherwise. */
+ttr_status ttr_compression_pass(ttr_ctx* ctx, const ttr_tt* tt, double tau, ttr_tt** out);
 ttr_status ttr_round_deterministic_tol(ttr_ctx* ctx, const ttr_tt* tt, double eps, ttr_tt** out);
 ttr_status ttr_round_deterministic_ranks(ttr_ctx* ctx, const ttr_tt* tt, const int64_t* target_ranks,
                                          int64_t count, ttr_tt** out);

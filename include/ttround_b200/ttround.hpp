@@ -165,6 +165,13 @@ inline TTTensor round_adaptive_krp(const TTTensor& tt, const AdaptiveConfig& cfg
     return TTTensor(out, tt.context());
 }
 
+//! round_rand.hpp compression_pass: right-to-left truncation of a left-orthogonal TT.
+inline TTTensor compression_pass(const TTTensor& left_orthogonal, double tau) {
+    ttr_tt* out = nullptr;
+    check(ttr_compression_pass(left_orthogonal.context().get(), left_orthogonal.get(), tau, &out));
+    return TTTensor(out, left_orthogonal.context());
+}
+
 //! A sum of TT tensors kept as its list of summands (sum_round.hpp:11-21).
 struct TTSum {
     std::vector<TTTensor> terms;

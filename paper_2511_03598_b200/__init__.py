@@ -457,6 +457,12 @@ def round_adaptive_krp(tt: TTTensor, cfg: AdaptiveConfig) -> TTTensor:
     return TTTensor._new(tt.ctx, lib().ttr_round_adaptive_krp, tt.ctx._h, tt._h, C.byref(c))
 
 
+def compression_pass(tt: TTTensor, tau: float) -> TTTensor:
+    """Right-to-left QR + truncated-SVD pass over a left-orthogonal tensor
+    (ttr_compression_pass; round_rand.cpp:155-179, the second pass of Adap-R)."""
+    return TTTensor._new(tt.ctx, lib().ttr_compression_pass, tt.ctx._h, tt._h, C.c_double(tau))
+
+
 def round_sum_adaptive_krp(terms: Sequence[TTTensor], eps: float, f_inc: float = 0.05, seed: int = 0,
                            rng: int = RNG_PHILOX) -> TTTensor:
     """Adaptive rounding of sum(terms) without forming the formal sum

@@ -357,6 +357,14 @@ ttr_status ttr_round_sum_adaptive_krp(ttr_ctx* ctx, const ttr_tt* const* terms, 
     });
 }
 
+ttr_status ttr_compression_pass(ttr_ctx* ctx, const ttr_tt* tt, double tau, ttr_tt** out) {
+    return guard([&] {
+        check_same_ctx(ctx, tt);
+        need(out != nullptr, "null output");
+        *out = wrap(compression_pass(ctx->c, *tt->t, tau));
+    });
+}
+
 ttr_status ttr_round_deterministic_tol(ttr_ctx* ctx, const ttr_tt* tt, double eps, ttr_tt** out) {
     return guard([&] {
         check_same_ctx(ctx, tt);

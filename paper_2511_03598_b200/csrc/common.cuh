@@ -185,6 +185,7 @@ void philox_factor_batched(Ctx& c, std::uint64_t seed, i64 mode, i64 rows, i64 c
 // ---- kernels (dense_ops.cu) -------------------------------------------------
 void philox_factor(Ctx& c, std::uint64_t seed, i64 mode, i64 rows, i64 cols, i64 col0, double* out, i64 ld);
 void fill(Ctx& c, double* p, std::size_t count, double v);
+void add_diagonal(Ctx& c, i64 n, double* a, i64 lda, double v);  // A(i,i) += v
 void copy_matrix(Ctx& c, i64 rows, i64 cols, const double* src, i64 lds, double* dst, i64 ldd);
 void transpose(Ctx& c, i64 rows, i64 cols, const double* src, i64 lds, double* dst, i64 ldd);
 void scale(Ctx& c, double* p, std::size_t count, double alpha);

@@ -86,6 +86,11 @@ __global__ void fill_kernel(double* p, i64 n, double v) {
         p[i] = v;
 }
 
+__global__ void add_diag_kernel(double* a, i64 n, i64 lda, double v) {
+    for (i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; i < n; i += static_cast<i64>(gridDim.x) * blockDim.x)
+        a[i + i * lda] += v;
+}
+
 __global__ void scale_kernel(double* p, i64 n, double a) {
     for (i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; i < n; i += static_cast<i64>(gridDim.x) * blockDim.x)
         p[i] *= a;
@@ -221,6 +226,13 @@ void random_normal(Ctx& c, std::uint64_t seed, std::uint32_t tag, double* out, s
 void fill(Ctx& c, double* p, std::size_t count, double v) {
     if (!count) return;
     fill_kernel<<<grid_for(c, count), kThreads, 0, c.stream>>>(p, static_cast<i64>(count), v);
+    TTR_CUDA(cudaGetLastError());
+    c.launched();
+}
+
+void add_diagonal(Ctx& c, i64 n, double* a, i64 lda, double v) {
+    if (n <= 0) return;
+    add_diag_kernel<<<grid_for(c, static_cast<std::size_t>(n)), kThreads, 0, c.stream>>>(a, n, lda, v);
     TTR_CUDA(cudaGetLastError());
     c.launched();
 }

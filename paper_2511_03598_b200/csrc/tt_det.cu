@@ -94,4 +94,66 @@ std::unique_ptr<TTDev> round_deterministic_ranks(Ctx& c, const TTDev& t, const s
     return compress_sweep(c, *o, false, 0.0, &ranks);
 }
 
+// compression_pass — round_rand.cpp:155-179 (the "Adap-R" second pass): a
+// right-to-left sweep over a left-orthogonal TT; per core the QR of H(Y_k)^T,
+// a tolerance-truncated SVD of the small triangle, the right-orthogonal core
+// (Q V_s)^T kept and U S absorbed into the left neighbour. With R = U_R S V_R^T
+// (svd_left of R), R^T = V_R S U_R^T, so U S = R^T U_R and V = U_R: no
+// division by singular values.
+std::unique_ptr<TTDev> compression_pass(Ctx& c, const TTDev& left, double tau) {
+    if (tau < 0) fail(Errc::InvalidArgument, "compression threshold must be >= 0");
+    const i64 d = left.d();
+    {  // round_rand.cpp:158-163: left-orthogonality defect of cores 0..d-2
+        i64 mx = 1;
+        for (i64 k = 0; k + 1 < d; ++k) mx = std::max(mx, left.r[k + 1]);
+        DBuf G(c, static_cast<std::size_t>(mx * mx));
+        for (i64 k = 0; k + 1 < d; ++k) {
+            const i64 rows = left.r[k] * left.n[k], cols = left.r[k + 1];
+            gemm(c, true, cols, cols, rows, 1.0, left.core(k), rows, left.core(k), rows, 0.0, G.p, cols, false);
+            add_diagonal(c, cols, G.p, cols, -1.0);
+            if (frob_norm(c, cols, cols, G.p, cols) >= 1e-8)
+                fail(Errc::NotLeftOrthogonal, "compression pass requires a left-orthogonal input");
+        }
+    }
+    if (d == 1) return copy_tt(c, left);
+    // working copies of the cores (their ranks shrink as the sweep proceeds)
+    std::vector<DBuf> cores(static_cast<std::size_t>(d));
+    std::vector<i64> r = left.r;
+    for (i64 k = 0; k < d; ++k) {
+        cores[k] = DBuf(c, static_cast<std::size_t>(left.core_size(k)));
+        copy_matrix(c, left.core_size(k), 1, left.core(k), left.core_size(k), cores[k].p, left.core_size(k));
+    }
+    std::vector<double> s;
+    for (i64 k = d - 1; k >= 1; --k) {
+        const i64 rl = r[k], nk = left.n[k], rr = r[k + 1], ncols = nk * rr;
+        const i64 kk = std::min(ncols, rl);
+        // Q R = H(Y_k)^T  (ncols x rl)
+        DBuf Ht(c, static_cast<std::size_t>(ncols * rl)), Q(c, static_cast<std::size_t>(ncols * kk)),
+            R(c, static_cast<std::size_t>(kk * rl)), U(c, static_cast<std::size_t>(kk * kk));
+        transpose(c, rl, ncols, cores[k].p, rl, Ht.p, ncols);
+        thin_qr(c, ncols, rl, Ht.p, ncols, Q.p, ncols, R.p, kk);
+        // truncated SVD of R^T (orthogonalize.cpp:87-115, tolerance rule)
+        svd_left(c, kk, rl, R.p, kk, U.p, kk, s, nullptr);
+        const i64 keep = truncation_rank(s, rl, kk, true, tau, 0);
+        // core k (horizontal, keep x ncols) = (Q U_R(:, 1:keep))^T
+        DBuf P(c, static_cast<std::size_t>(ncols * keep));
+        gemm(c, false, ncols, keep, kk, 1.0, Q.p, ncols, U.p, kk, 0.0, P.p, ncols);
+        DBuf nk_core(c, static_cast<std::size_t>(keep * ncols));
+        transpose(c, ncols, keep, P.p, ncols, nk_core.p, keep);
+        cores[k] = std::move(nk_core);
+        // core k-1 <- V(core k-1) (U S) with U S = R^T U_R(:, 1:keep)
+        DBuf US(c, static_cast<std::size_t>(rl * keep));
+        gemm(c, true, rl, keep, kk, 1.0, R.p, kk, U.p, kk, 0.0, US.p, rl);
+        const i64 rows_prev = r[k - 1] * left.n[k - 1];
+        DBuf prev(c, static_cast<std::size_t>(rows_prev * keep));
+        gemm(c, false, rows_prev, keep, rl, 1.0, cores[k - 1].p, rows_prev, US.p, rl, 0.0, prev.p, rows_prev);
+        cores[k - 1] = std::move(prev);
+        r[k] = keep;
+    }
+    auto out = std::make_unique<TTDev>(c, left.n, r);
+    for (i64 k = 0; k < d; ++k)
+        copy_matrix(c, out->core_size(k), 1, cores[k].p, out->core_size(k), out->core(k), out->core_size(k));
+    return out;
+}
+
 }  // namespace ttr

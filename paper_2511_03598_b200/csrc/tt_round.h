@@ -104,6 +104,8 @@ std::unique_ptr<TTDev> round_sum_adaptive_krp(Ctx& c, const std::vector<const TT
                                               std::uint64_t seed, int rng_mode);
 double estimate_norm_krp(Ctx& c, const TTDev& t, i64 width, std::uint64_t seed, int rng_mode);
 std::unique_ptr<TTDev> round_deterministic_tol(Ctx& c, const TTDev& t, double eps);
+// round_rand.cpp:155-179 — right-to-left truncation pass of a left-orthogonal TT (tt_det.cu)
+std::unique_ptr<TTDev> compression_pass(Ctx& c, const TTDev& left_orthogonal, double tau);
 std::unique_ptr<TTDev> round_deterministic_ranks(Ctx& c, const TTDev& t, const std::vector<i64>& ranks);
 
 // W_start..W_d of the KRP partial contractions for explicit (or Philox) factors.

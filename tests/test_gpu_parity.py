@@ -227,6 +227,26 @@ def test_host_streaming_plan(P, O):
     plan.close()
 
 
+# ---- compression_pass / Adap-R (round_rand.cpp:155-179) ----------------------------------------
+
+def test_compression_pass_parity(P, O):
+    """Adap-R: adaptive rounding then the right-to-left truncation pass, same ranks
+    and <= 1e-10 against the oracle; non-left-orthogonal input is rejected."""
+    x = O.two_part_tt(6, 16, 12, 36, 1e-6, 77)
+    a_ref = O.round_adaptive_krp(x, tolerance=1e-4, f_init=0.1, f_inc=0.05, seed=3, rng=O.PHILOX)
+    a_gpu = P.round_adaptive_krp(to_device(x), P.AdaptiveConfig(tolerance=1e-4, seed=3))
+    assert a_gpu.ranks() == a_ref.ranks
+    nrm = O.norm_exact(a_ref)
+    for tau in (1e-6 * nrm, 1e-3 * nrm):
+        c_ref = O.compression_pass(a_ref, tau)
+        c_gpu = P.compression_pass(to_device(a_ref), tau)
+        assert c_gpu.ranks() == c_ref.ranks
+        assert rel_err_vs_ref(c_ref, c_gpu) <= 1e-10
+    with pytest.raises(P.TTRoundError) as e:
+        P.compression_pass(to_device(x), 1e-6)
+    assert e.value.code == "NotLeftOrthogonal"
+
+
 # ---- sum of TT tensors without the formal sum (sum_round.cpp) ----------------------------------
 
 @pytest.mark.parametrize("rng_mode", [0, 1])
