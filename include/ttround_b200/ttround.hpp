@@ -165,6 +165,14 @@ inline TTTensor round_adaptive_krp(const TTTensor& tt, const AdaptiveConfig& cfg
     return TTTensor(out, tt.context());
 }
 
+//! round_rand.hpp:49 round_rand_orth_tt: Rand-Orth with a Gaussian TT sketch.
+inline TTTensor round_rand_orth_tt(const TTTensor& tt, const std::vector<Index>& target_ranks, std::uint64_t seed) {
+    ttr_tt* out = nullptr;
+    check(ttr_round_rand_orth_tt(tt.context().get(), tt.get(), target_ranks.data(),
+                                 static_cast<int64_t>(target_ranks.size()), seed, &out));
+    return TTTensor(out, tt.context());
+}
+
 //! round_rand.hpp compression_pass: right-to-left truncation of a left-orthogonal TT.
 inline TTTensor compression_pass(const TTTensor& left_orthogonal, double tau) {
     ttr_tt* out = nullptr;

@@ -184,6 +184,22 @@ int ttro_round_adaptive_krp(const ttro_tt* t, double tol, double f_init, double 
         if (tau_out) *tau_out = tr.tau;
     });
 }
+int ttro_round_rand_orth_tt(const ttro_tt* t, const std::int64_t* ranks, std::int64_t count, std::uint64_t seed,
+                            ttro_tt** out) {
+    return guard([&] { *out = wrap(round_rand_orth_tt(t->tt, vec(ranks, count), seed)); });
+}
+
+int ttro_tt_partial_contractions(const ttro_tt* x, const ttro_tt* r, double* out) {
+    return guard([&] {
+        auto w = tt_partial_contractions_rl(x->tt, r->tt);
+        std::size_t o = 0;
+        for (const auto& m : w) {
+            std::copy(m.a.begin(), m.a.end(), out + o);
+            o += m.a.size();
+        }
+    });
+}
+
 int ttro_round_sum_adaptive_krp(const ttro_tt* const* terms, int count, double eps, double f_inc, std::uint64_t seed,
                                 int rng_mode, ttro_tt** out) {
     return guard([&] {

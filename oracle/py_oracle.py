@@ -237,6 +237,27 @@ def round_adaptive_krp(t: TT, tolerance=1e-6, f_init=0.1, f_inc=0.05, seed=0, rn
     return TT(out)
 
 
+def round_rand_orth_tt(t: TT, target_ranks: Sequence[int], seed: int) -> TT:
+    """round_rand.cpp:66-78 — Rand-Orth with a Gaussian TT sketch (reference xoshiro stream)."""
+    return TT._new(lib().ttro_round_rand_orth_tt, t._h, _i64(target_ranks), C.c_int64(len(target_ranks)),
+                   C.c_uint64(seed))
+
+
+def tt_partial_contractions(x: TT, r: TT) -> List[np.ndarray]:
+    """sketch.cpp:94-109: [W_1 .. W_{d-1}] with W_{k-1} = H(X_k x_3 W_k) H(R_k)^T."""
+    _, rx, _ = x.shape()
+    _, rr, _ = r.shape()
+    d = len(rx) - 1
+    shapes = [(rx[k], rr[k]) for k in range(1, d)]
+    out = np.empty(sum(a * b for a, b in shapes), dtype=np.float64)
+    _check(lib().ttro_tt_partial_contractions(x._h, r._h, _dptr(out)))
+    res, o = [], 0
+    for a, b in shapes:
+        res.append(out[o:o + a * b].reshape(b, a).T.copy())
+        o += a * b
+    return res
+
+
 def round_sum_adaptive_krp(terms: Sequence[TT], eps: float, f_inc: float, seed: int, rng=XOSHIRO) -> TT:
     """sum_round.cpp:52-173 — adaptive rounding of sum(terms) without the formal sum."""
     arr = (C.c_void_p * max(1, len(terms)))(*[t._h.value for t in terms])

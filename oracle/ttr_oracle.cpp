@@ -911,6 +911,43 @@ TT round_fixed_krp(const TT& tt, const std::vector<Index>& target_ranks, std::ui
     return TT(std::move(out));
 }
 
+std::vector<Matrix> tt_partial_contractions_rl(const TT& x, const TT& r) {  // sketch.cpp:94-109
+    if (x.mode_sizes() != r.mode_sizes()) fail(Errc::ModeSizeMismatch, "contraction pair mode sizes differ");
+    flops::SketchScope scope;
+    const Index d = x.order();
+    std::vector<Matrix> w(static_cast<std::size_t>(d - 1));
+    w.back() = linalg::mul_nt(x.core(d - 1).horizontal(), r.core(d - 1).horizontal());
+    for (Index k = d - 1; k >= 2; --k) {
+        // Z_k = X_k x_3 W_k, then W_{k-1} = H(Z_k) H(R_k)^T
+        Core z = contract_third(x.core(k - 1), w[static_cast<std::size_t>(k - 1)]);
+        w[static_cast<std::size_t>(k - 2)] = linalg::mul_nt(z.horizontal(), r.core(k - 1).horizontal());
+    }
+    return w;
+}
+
+TT round_rand_orth_tt(const TT& tt, const std::vector<Index>& target_ranks, std::uint64_t seed) {  // round_rand.cpp:66-78
+    auto targets = checked_targets(tt, target_ranks);
+    const Index d = tt.order();
+    if (d == 1) return tt;
+    std::vector<Index> sketch_ranks(targets.size() + 2, 1);
+    for (std::size_t k = 0; k < targets.size(); ++k) sketch_ranks[k + 1] = targets[k];
+    TT r = random_gaussian_tt(tt.mode_sizes(), sketch_ranks, seed);
+    auto w = tt_partial_contractions_rl(tt, r);
+    std::vector<Core> out;
+    Core work = tt.core(0);
+    for (Index k = 1; k < d; ++k) {  // rand_orth_sweep, round_rand.cpp:31-41
+        const Matrix v = work.vertical();
+        const Index l_eff = std::min({targets[static_cast<std::size_t>(k - 1)], v.rows, v.cols});
+        Matrix s = linalg::mul(v, w[static_cast<std::size_t>(k - 1)].left_cols(l_eff));
+        Matrix q = linalg::thin_qr_q(s);
+        Matrix m = linalg::tmul(q, v);
+        out.push_back(Core::from_vertical(work.r_left(), work.n(), q));
+        work = contract_first(tt.core(k), m);
+    }
+    out.push_back(std::move(work));
+    return TT(std::move(out));
+}
+
 Matrix generate_residual_sketch(const TT& tt, const Matrix& z, const Matrix& q, ContractionSet& w,
                                 Index k, Index b, FactorRng& rng) {  // round_rand.cpp:80-94
     if (b < 1) fail(Errc::InvalidArgument, "sketch block size must be >= 1");

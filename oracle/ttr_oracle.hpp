@@ -238,6 +238,12 @@ Matrix generate_residual_sketch(const TT& tt, const Matrix& z, const Matrix& q, 
 TT round_adaptive_krp(const TT& tt, const AdaptiveConfig& cfg, AdaptiveTrace* trace = nullptr);
 TT compression_pass(const TT& left_orthogonal, double tau);
 
+// ---- Rand-Orth with a Gaussian TT sketch (the paper's TT-sketch baseline) ----
+//! sketch.cpp:94-109: W_{k-1} = H(X_k x_3 W_k) H(R_k)^T, right to left; w[k-1] pairs with bond k
+std::vector<Matrix> tt_partial_contractions_rl(const TT& x, const TT& r);
+//! round_rand.cpp:66-78 (reference stream: R = random_gaussian_tt(modes, (1, targets, 1), seed))
+TT round_rand_orth_tt(const TT& tt, const std::vector<Index>& target_ranks, std::uint64_t seed);
+
 // ---- sum of TT tensors without the formal sum: proj/core/src/sum_round.cpp --
 //! sum_round.cpp:11-19 (TTSum::of validation)
 void validate_sum(const std::vector<TT>& terms);

@@ -457,6 +457,12 @@ def round_adaptive_krp(tt: TTTensor, cfg: AdaptiveConfig) -> TTTensor:
     return TTTensor._new(tt.ctx, lib().ttr_round_adaptive_krp, tt.ctx._h, tt._h, C.byref(c))
 
 
+def round_rand_orth_tt(tt: TTTensor, target_ranks: Sequence[int], seed: int) -> TTTensor:
+    """Rand-Orth with a Gaussian TT sketch (ttr_round_rand_orth_tt; round_rand.cpp:66-78)."""
+    return TTTensor._new(tt.ctx, lib().ttr_round_rand_orth_tt, tt.ctx._h, tt._h, _i64(target_ranks),
+                         C.c_int64(len(target_ranks)), C.c_uint64(seed))
+
+
 def compression_pass(tt: TTTensor, tau: float) -> TTTensor:
     """Right-to-left QR + truncated-SVD pass over a left-orthogonal tensor
     (ttr_compression_pass; round_rand.cpp:155-179, the second pass of Adap-R)."""

@@ -357,6 +357,16 @@ ttr_status ttr_round_sum_adaptive_krp(ttr_ctx* ctx, const ttr_tt* const* terms, 
     });
 }
 
+ttr_status ttr_round_rand_orth_tt(ttr_ctx* ctx, const ttr_tt* tt, const int64_t* ranks, int64_t count, uint64_t seed,
+                                  ttr_tt** out) {
+    return guard([&] {
+        check_same_ctx(ctx, tt);
+        need(out != nullptr, "null output");
+        if (count < 0 || (count > 0 && !ranks)) fail(Errc::InvalidRanks, "expected d-1 target ranks");
+        *out = wrap(round_rand_orth_tt(ctx->c, *tt->t, vec(ranks, count), seed));
+    });
+}
+
 ttr_status ttr_compression_pass(ttr_ctx* ctx, const ttr_tt* tt, double tau, ttr_tt** out) {
     return guard([&] {
         check_same_ctx(ctx, tt);

@@ -412,6 +412,62 @@ void rand_orth_sweep(Ctx& c, const TTDev& t, i64 width, const std::vector<const 
 }
 
 // ---------------------------------------------------------------------------
+// Rand-Orth with a Gaussian TT sketch — round_rand.cpp:66-78 (the paper's
+// TT-sketch baseline). R = random_gaussian_tt(modes, (1, targets, 1), seed) is
+// drawn from the reference's xoshiro stream on the host (tensor.cpp:217-242,
+// tiny) and the partial contractions W_k = H(X_k x_3 W_{k+1}) H(R_k)^T
+// (sketch.cpp:94-109) run as two GEMMs per mode; the sweep is the KRP one.
+std::unique_ptr<TTDev> round_rand_orth_tt(Ctx& c, const TTDev& t, const std::vector<i64>& target_ranks,
+                                          std::uint64_t seed) {
+    auto targets = checked_targets(t, target_ranks);
+    const i64 d = t.d();
+    if (d == 1) return copy_tt(c, t);
+    std::vector<i64> sr(static_cast<std::size_t>(d + 1), 1);
+    for (i64 k = 0; k + 1 < d; ++k) sr[k + 1] = targets[k];
+    TTDev R(c, t.n, sr);
+    {
+        XoshiroGauss xo(seed);
+        std::vector<double> host;
+        for (i64 k = 0; k < d; ++k) {
+            const double sigma = 1.0 / std::sqrt(static_cast<double>(sr[k]) * t.n[k] * sr[k + 1]);
+            for (i64 e = 0; e < R.core_size(k); ++e) host.push_back(sigma * xo.next());
+        }
+        R.upload(host.data());
+        TTR_CUDA(cudaStreamSynchronize(c.stream));  // host buffer lifetime
+    }
+    std::vector<DBuf> W(static_cast<std::size_t>(d + 2));
+    std::vector<const double*> Wp(static_cast<std::size_t>(d + 2), nullptr);
+    std::vector<i64> ldw(static_cast<std::size_t>(d + 2), 0);
+    {
+        SketchScope scope(c);
+        // W_d = H(X_d) H(R_d)^T : (r_{d-1} x n_d)(n_d x l_{d-1})
+        const i64 nd = t.n[d - 1];
+        DBuf Rt(c, static_cast<std::size_t>(nd * sr[d - 1]));
+        transpose(c, sr[d - 1], nd, R.core(d - 1), sr[d - 1], Rt.p, nd);
+        W[d] = DBuf(c, static_cast<std::size_t>(t.r[d - 1] * sr[d - 1]));
+        gemm(c, false, t.r[d - 1], sr[d - 1], nd, 1.0, t.core(d - 1), t.r[d - 1], Rt.p, nd, 0.0, W[d].p, t.r[d - 1]);
+        ldw[d] = t.r[d - 1];
+        for (i64 k = d - 1; k >= 2; --k) {
+            const i64 rl = t.r[k - 1], nk = t.n[k - 1], rr = t.r[k], lk = sr[k], lk1 = sr[k - 1];
+            // Z = V(X_k) W_{k+1}  (rl nk x lk)
+            DBuf Z(c, static_cast<std::size_t>(rl * nk * lk));
+            gemm(c, false, rl * nk, lk, rr, 1.0, t.core(k - 1), rl * nk, W[k + 1].p, ldw[k + 1], 0.0, Z.p, rl * nk);
+            // W_k = H(Z) H(R_k)^T : (rl x nk lk)(nk lk x l_{k-1})
+            DBuf Rk(c, static_cast<std::size_t>(nk * lk * lk1));
+            transpose(c, lk1, nk * lk, R.core(k - 1), lk1, Rk.p, nk * lk);
+            W[k] = DBuf(c, static_cast<std::size_t>(rl * lk1));
+            gemm(c, false, rl, lk1, nk * lk, 1.0, Z.p, rl, Rk.p, nk * lk, 0.0, W[k].p, rl);
+            ldw[k] = rl;
+        }
+    }
+    for (i64 k = 2; k <= d; ++k) Wp[k] = W[k].p;
+    const i64 width = *std::max_element(targets.begin(), targets.end());
+    auto out = std::make_unique<TTDev>(c, t.n, fixed_krp_ranks(t, targets));
+    rand_orth_sweep(c, t, width, Wp, ldw, *out);
+    return out;
+}
+
+// ---------------------------------------------------------------------------
 // CUDA-graph plan for fixed-rank KRP rounding: one eager run sizes every
 // workspace (and the split-K scratch), then the whole sweep — ~2,400 launches
 // for config 5b — is captured once and replayed with a single graph launch.

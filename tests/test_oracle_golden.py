@@ -98,6 +98,26 @@ def test_sum_round_properties(oracle):
                                   O.random_gaussian_tt([4, 5], [1, 2, 1], 3)], 1e-6, 0.05, 1)
 
 
+def test_rand_orth_tt_properties(oracle):
+    """test_sketch.cpp:100-128 and test_round_rand.cpp:266-291: TT partial
+    contractions (identity for a right-orthogonal self-contraction, the d=2 step)
+    and Rand-Orth with a TT sketch (full width exact, desk-scale error band)."""
+    O = oracle
+    t = O.orthogonalize(O.random_gaussian_tt([4, 3, 4, 5], [1, 3, 3, 4, 1], 15), right_to_left=True)
+    for m in O.tt_partial_contractions(t, t):
+        assert np.linalg.norm(m - np.eye(*m.shape)) <= 1e-12
+    x = O.random_gaussian_tt([3, 4], [1, 2, 1], 1)
+    r = O.random_gaussian_tt([3, 4], [1, 3, 1], 2)
+    w = O.tt_partial_contractions(x, r)
+    assert np.linalg.norm(w[0] - x.cores()[1][:, :, 0] @ r.cores()[1][:, :, 0].T) <= 1e-13
+    t = O.random_gaussian_tt([5, 4, 5], [1, 4, 3, 1], 77)
+    y = O.round_rand_orth_tt(t, [4, 3], 5)
+    assert np.linalg.norm(t.dense() - y.dense()) / np.linalg.norm(t.dense()) <= 1e-10
+    syn = O.synthetic_perturbed_tt(5, 20, 10, 1e-5, 5150)
+    hits = sum(0.5e-5 <= O.relative_error(syn, O.round_rand_orth_tt(syn, [10] * 4, s)) <= 1e-3 for s in range(10))
+    assert hits >= 9
+
+
 # ---- hand KATs ---------------------------------------------------------------------------
 
 def test_tiny_rank1_kats(oracle):
