@@ -167,10 +167,11 @@ ttr_status ttr_round_adaptive_krp(ttr_ctx* ctx, const ttr_tt* tt, const ttr_adap
 ttr_status ttr_round_sum_adaptive_krp(ttr_ctx* ctx, const ttr_tt* const* terms, int64_t count, double eps,
                                       double f_inc, uint64_t seed, int rng_mode, ttr_tt** out);
 /* Rand-Orth with a Gaussian TT sketch tensor (round_rand_orth_tt,
- * round_rand.hpp:49 / round_rand.cpp:66-78): R drawn from the reference's
- * xoshiro stream (random_gaussian_tt(modes, (1, targets, 1), seed)). */
+ * round_rand.hpp:49 / round_rand.cpp:66-78): R = random_gaussian_tt(modes,
+ * (1, targets, 1), seed) from the reference's xoshiro stream (TTR_RNG_XOSHIRO,
+ * host draws) or drawn on the device (TTR_RNG_PHILOX, tag 3000 + core). */
 ttr_status ttr_round_rand_orth_tt(ttr_ctx* ctx, const ttr_tt* tt, const int64_t* target_ranks, int64_t count,
-                                  uint64_t seed, ttr_tt** out);
+                                  uint64_t seed, int rng_mode, ttr_tt** out);
 /* compression_pass (round_rand.hpp / round_rand.cpp:155-179): right-to-left
  * QR + tolerance-truncated SVD sweep of a LEFT-ORTHOGONAL tensor (e.g. the
  * output of ttr_round_adaptive_krp; "Adap-R"). NotLeftOrthogonal otherwise. */

@@ -166,10 +166,11 @@ inline TTTensor round_adaptive_krp(const TTTensor& tt, const AdaptiveConfig& cfg
 }
 
 //! round_rand.hpp:49 round_rand_orth_tt: Rand-Orth with a Gaussian TT sketch.
-inline TTTensor round_rand_orth_tt(const TTTensor& tt, const std::vector<Index>& target_ranks, std::uint64_t seed) {
+inline TTTensor round_rand_orth_tt(const TTTensor& tt, const std::vector<Index>& target_ranks, std::uint64_t seed,
+                                   RngMode rng = RngMode::Philox) {
     ttr_tt* out = nullptr;
     check(ttr_round_rand_orth_tt(tt.context().get(), tt.get(), target_ranks.data(),
-                                 static_cast<int64_t>(target_ranks.size()), seed, &out));
+                                 static_cast<int64_t>(target_ranks.size()), seed, static_cast<int>(rng), &out));
     return TTTensor(out, tt.context());
 }
 

@@ -185,8 +185,8 @@ int ttro_round_adaptive_krp(const ttro_tt* t, double tol, double f_init, double 
     });
 }
 int ttro_round_rand_orth_tt(const ttro_tt* t, const std::int64_t* ranks, std::int64_t count, std::uint64_t seed,
-                            ttro_tt** out) {
-    return guard([&] { *out = wrap(round_rand_orth_tt(t->tt, vec(ranks, count), seed)); });
+                            int rng_mode, ttro_tt** out) {
+    return guard([&] { *out = wrap(round_rand_orth_tt(t->tt, vec(ranks, count), seed, static_cast<RngMode>(rng_mode))); });
 }
 
 int ttro_tt_partial_contractions(const ttro_tt* x, const ttro_tt* r, double* out) {

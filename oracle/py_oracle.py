@@ -237,10 +237,10 @@ def round_adaptive_krp(t: TT, tolerance=1e-6, f_init=0.1, f_inc=0.05, seed=0, rn
     return TT(out)
 
 
-def round_rand_orth_tt(t: TT, target_ranks: Sequence[int], seed: int) -> TT:
-    """round_rand.cpp:66-78 — Rand-Orth with a Gaussian TT sketch (reference xoshiro stream)."""
+def round_rand_orth_tt(t: TT, target_ranks: Sequence[int], seed: int, rng=XOSHIRO) -> TT:
+    """round_rand.cpp:66-78 — Rand-Orth with a Gaussian TT sketch (xoshiro: the reference stream)."""
     return TT._new(lib().ttro_round_rand_orth_tt, t._h, _i64(target_ranks), C.c_int64(len(target_ranks)),
-                   C.c_uint64(seed))
+                   C.c_uint64(seed), C.c_int(rng))
 
 
 def tt_partial_contractions(x: TT, r: TT) -> List[np.ndarray]:

@@ -925,13 +925,28 @@ std::vector<Matrix> tt_partial_contractions_rl(const TT& x, const TT& r) {  // s
     return w;
 }
 
-TT round_rand_orth_tt(const TT& tt, const std::vector<Index>& target_ranks, std::uint64_t seed) {  // round_rand.cpp:66-78
+TT round_rand_orth_tt(const TT& tt, const std::vector<Index>& target_ranks, std::uint64_t seed,
+                      RngMode mode) {  // round_rand.cpp:66-78
     auto targets = checked_targets(tt, target_ranks);
     const Index d = tt.order();
     if (d == 1) return tt;
     std::vector<Index> sketch_ranks(targets.size() + 2, 1);
     for (std::size_t k = 0; k < targets.size(); ++k) sketch_ranks[k + 1] = targets[k];
-    TT r = random_gaussian_tt(tt.mode_sizes(), sketch_ranks, seed);
+    TT r = [&] {
+        if (mode == RngMode::Xoshiro) return random_gaussian_tt(tt.mode_sizes(), sketch_ranks, seed);
+        // Philox: core k = sigma * philox_factor(seed, 3000 + k, r_k n_k, r_{k+1}) (device counterpart)
+        std::vector<Core> cores;
+        const auto modes = tt.mode_sizes();
+        for (Index k = 0; k < d; ++k) {
+            const Index rl = sketch_ranks[static_cast<std::size_t>(k)], n = modes[static_cast<std::size_t>(k)],
+                        rr = sketch_ranks[static_cast<std::size_t>(k) + 1];
+            Matrix m = philox_factor(seed, 3000 + k, rl * n, rr, 0);
+            const double sigma = 1.0 / std::sqrt(static_cast<double>(rl) * n * rr);
+            for (auto& v : m.a) v *= sigma;
+            cores.push_back(Core::from_vertical(rl, n, m));
+        }
+        return TT(std::move(cores));
+    }();
     auto w = tt_partial_contractions_rl(tt, r);
     std::vector<Core> out;
     Core work = tt.core(0);

@@ -242,7 +242,8 @@ TT compression_pass(const TT& left_orthogonal, double tau);
 //! sketch.cpp:94-109: W_{k-1} = H(X_k x_3 W_k) H(R_k)^T, right to left; w[k-1] pairs with bond k
 std::vector<Matrix> tt_partial_contractions_rl(const TT& x, const TT& r);
 //! round_rand.cpp:66-78 (reference stream: R = random_gaussian_tt(modes, (1, targets, 1), seed))
-TT round_rand_orth_tt(const TT& tt, const std::vector<Index>& target_ranks, std::uint64_t seed);
+TT round_rand_orth_tt(const TT& tt, const std::vector<Index>& target_ranks, std::uint64_t seed,
+                      RngMode mode = RngMode::Xoshiro);
 
 // ---- sum of TT tensors without the formal sum: proj/core/src/sum_round.cpp --
 //! sum_round.cpp:11-19 (TTSum::of validation)

@@ -457,10 +457,10 @@ def round_adaptive_krp(tt: TTTensor, cfg: AdaptiveConfig) -> TTTensor:
     return TTTensor._new(tt.ctx, lib().ttr_round_adaptive_krp, tt.ctx._h, tt._h, C.byref(c))
 
 
-def round_rand_orth_tt(tt: TTTensor, target_ranks: Sequence[int], seed: int) -> TTTensor:
+def round_rand_orth_tt(tt: TTTensor, target_ranks: Sequence[int], seed: int, rng: int = RNG_PHILOX) -> TTTensor:
     """Rand-Orth with a Gaussian TT sketch (ttr_round_rand_orth_tt; round_rand.cpp:66-78)."""
     return TTTensor._new(tt.ctx, lib().ttr_round_rand_orth_tt, tt.ctx._h, tt._h, _i64(target_ranks),
-                         C.c_int64(len(target_ranks)), C.c_uint64(seed))
+                         C.c_int64(len(target_ranks)), C.c_uint64(seed), C.c_int(rng))
 
 
 def compression_pass(tt: TTTensor, tau: float) -> TTTensor:

@@ -358,12 +358,13 @@ ttr_status ttr_round_sum_adaptive_krp(ttr_ctx* ctx, const ttr_tt* const* terms, 
 }
 
 ttr_status ttr_round_rand_orth_tt(ttr_ctx* ctx, const ttr_tt* tt, const int64_t* ranks, int64_t count, uint64_t seed,
-                                  ttr_tt** out) {
+                                  int rng_mode, ttr_tt** out) {
     return guard([&] {
         check_same_ctx(ctx, tt);
         need(out != nullptr, "null output");
         if (count < 0 || (count > 0 && !ranks)) fail(Errc::InvalidRanks, "expected d-1 target ranks");
-        *out = wrap(round_rand_orth_tt(ctx->c, *tt->t, vec(ranks, count), seed));
+        need(rng_mode == TTR_RNG_PHILOX || rng_mode == TTR_RNG_XOSHIRO, "unknown rng mode");
+        *out = wrap(round_rand_orth_tt(ctx->c, *tt->t, vec(ranks, count), seed, rng_mode));
     });
 }
 

@@ -415,17 +415,26 @@ void rand_orth_sweep(Ctx& c, const TTDev& t, i64 width, const std::vector<const 
 // Rand-Orth with a Gaussian TT sketch — round_rand.cpp:66-78 (the paper's
 // TT-sketch baseline). R = random_gaussian_tt(modes, (1, targets, 1), seed) is
 // drawn from the reference's xoshiro stream on the host (tensor.cpp:217-242,
-// tiny) and the partial contractions W_k = H(X_k x_3 W_{k+1}) H(R_k)^T
+// or, in Philox mode, on the device) and the partial contractions W_k = H(X_k x_3 W_{k+1}) H(R_k)^T
 // (sketch.cpp:94-109) run as two GEMMs per mode; the sweep is the KRP one.
 std::unique_ptr<TTDev> round_rand_orth_tt(Ctx& c, const TTDev& t, const std::vector<i64>& target_ranks,
-                                          std::uint64_t seed) {
+                                          std::uint64_t seed, int rng_mode) {
     auto targets = checked_targets(t, target_ranks);
     const i64 d = t.d();
     if (d == 1) return copy_tt(c, t);
     std::vector<i64> sr(static_cast<std::size_t>(d + 1), 1);
     for (i64 k = 0; k + 1 < d; ++k) sr[k + 1] = targets[k];
     TTDev R(c, t.n, sr);
-    {
+    if (rng_mode == TTR_RNG_PHILOX) {
+        // device draw: core k = sigma * Philox Gaussian (rows r_k n_k, cols r_{k+1}, tag 3000 + k),
+        // the same stream as the oracle's Philox mode
+        for (i64 k = 0; k < d; ++k) {
+            const i64 rows = sr[k] * t.n[k];
+            philox_factor(c, seed, 3000 + k, rows, sr[k + 1], 0, R.core(k), rows);
+            scale(c, R.core(k), static_cast<std::size_t>(R.core_size(k)),
+                  1.0 / std::sqrt(static_cast<double>(sr[k]) * t.n[k] * sr[k + 1]));
+        }
+    } else {  // the reference's xoshiro stream (host draws)
         XoshiroGauss xo(seed);
         std::vector<double> host;
         for (i64 k = 0; k < d; ++k) {

@@ -101,7 +101,7 @@ struct Plan {
 std::unique_ptr<TTDev> round_adaptive_krp(Ctx& c, const TTDev& t, const AdaptiveCfg& cfg, std::vector<double>* trace);
 // round_rand.cpp:66-78 — Rand-Orth with a Gaussian TT sketch (reference xoshiro stream for R)
 std::unique_ptr<TTDev> round_rand_orth_tt(Ctx& c, const TTDev& t, const std::vector<i64>& target_ranks,
-                                          std::uint64_t seed);
+                                          std::uint64_t seed, int rng_mode);
 // sum_round.cpp:52-173 — adaptive rounding of sum(terms) without the formal sum (tt_sum.cu)
 std::unique_ptr<TTDev> round_sum_adaptive_krp(Ctx& c, const std::vector<const TTDev*>& terms, double eps, double f_inc,
                                               std::uint64_t seed, int rng_mode);

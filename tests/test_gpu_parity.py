@@ -233,9 +233,9 @@ def test_rand_orth_tt_parity(P, O):
     """Same R (reference xoshiro stream) on both sides: identical ranks, <= 1e-10;
     full width is exact (test_round_rand.cpp:274-277)."""
     x = O.two_part_tt(6, 16, 10, 30, 1e-6, 88)
-    for seed in (0, 5):
-        ref = O.round_rand_orth_tt(x, [14] * 5, seed)
-        y = P.round_rand_orth_tt(to_device(x), [14] * 5, seed)
+    for seed, rng in ((0, 0), (5, 0), (5, 1)):
+        ref = O.round_rand_orth_tt(x, [14] * 5, seed, rng=rng)
+        y = P.round_rand_orth_tt(to_device(x), [14] * 5, seed, rng=rng)
         assert y.ranks() == ref.ranks
         assert rel_err_vs_ref(ref, y) <= 1e-10
     t = O.random_gaussian_tt([5, 4, 5], [1, 4, 3, 1], 77)

@@ -34,7 +34,7 @@ def main():
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
     ctx = P.Context(0, stream.cuda_stream)
-    which = sys.argv[1:] or ["1", "2", "3", "3det", "4"]
+    which = sys.argv[1:] or ["1", "2", "3", "3rot", "3det", "4", "4sum"]
     for cfg in which:
         if cfg == "1":
             y = P.TTTensor.two_part_philox(10, 20, 10, 40, 1e-4, 1001, ctx)
@@ -55,6 +55,15 @@ def main():
             msp, fl, _ = timed(ctx, stream, lambda: plan.execute(), 5)
             rec = dict(config="3 fixed KRP d=30 n=64 400->110", ms_plan=msp, tflops=fl / msp / 1e9,
                        ranks=plan.output.ranks()[:4])
+        elif cfg == "3rot":
+            # the paper's baseline: Rand-Orth with a Gaussian TT sketch, same input and ranks
+            y = P.TTTensor.two_part_philox(30, 64, 100, 300, 1e-8, 1003, ctx)
+            ms, fl, out = timed(ctx, stream, lambda: P.round_rand_orth_tt(y, [110] * 29, 7), 3)
+            ctx.reset_counters()
+            P.round_rand_orth_tt(y, [110] * 29, 7)
+            sk = ctx.counters().sketch
+            rec = dict(config="3 Rand-Orth TT sketch d=30 n=64 400->110", ms_eager=ms, tflops=fl / ms / 1e9,
+                       sketch_flops=sk, ranks=out.ranks()[:4])
         elif cfg == "3det":
             y = P.TTTensor.two_part_philox(30, 64, 100, 300, 1e-8, 1003, ctx)
             ms, fl, out = timed(ctx, stream, lambda: P.round_deterministic(y, target_ranks=[100] * 29), 1, warm=1)
