@@ -397,3 +397,76 @@ def test_adaptive_config4_small_parity(P, O):
     y_gpu = P.round_adaptive_krp(to_device(x), P.AdaptiveConfig(tolerance=1e-6, f_init=0.1, f_inc=0.04, seed=7))
     assert y_gpu.ranks() == y_ref.ranks
     assert rel_err_vs_ref(y_ref, y_gpu) <= 1e-10
+
+
+# ---- edge cases across the entry points ----------------------------------------------------------
+
+def _zero_tt(O, n, r):
+    return O.TT.from_cores([np.zeros((r[k], n[k], r[k + 1])) for k in range(len(n))])
+
+
+@pytest.mark.parametrize("shape", [
+    ([7], [1, 1]),                       # d = 1
+    ([6, 5], [1, 3, 1]),                 # d = 2
+    ([1, 4, 1, 3], [1, 1, 2, 2, 1]),     # unit mode sizes
+    ([3, 2, 3], [1, 3, 3, 1]),           # ranks at their caps (r_k = prod of modes)
+])
+def test_edge_shapes_all_paths(P, O, shape):
+    """Ragged / degenerate shapes through fixed, adaptive, deterministic and
+    Rand-Orth-TT rounding: the device matches the oracle (ranks and values)."""
+    n, r = shape
+    x = O.random_gaussian_tt(n, r, 1234)
+    d = len(n)
+    tx = to_device(x)
+    targets = [5] * (d - 1)  # larger than several caps: l_eff = min(l, rows, cols)
+    ref = O.round_fixed_krp(x, targets, 3, rng=O.PHILOX)
+    y = P.round_fixed_krp(tx, targets, 3)
+    assert y.ranks() == ref.ranks
+    assert rel_err_vs_ref(ref, y) <= 1e-10
+    ref = O.round_adaptive_krp(x, tolerance=1e-8, f_init=0.5, f_inc=0.5, seed=4, rng=O.PHILOX)
+    y = P.round_adaptive_krp(tx, P.AdaptiveConfig(tolerance=1e-8, f_init=0.5, f_inc=0.5, seed=4))
+    assert y.ranks() == ref.ranks
+    assert rel_err_vs_ref(ref, y) <= 1e-10
+    ref = O.round_deterministic(x, eps=1e-12)
+    y = P.round_deterministic(tx, eps=1e-12)
+    assert y.ranks() == ref.ranks
+    assert rel_err_vs_ref(ref, y) <= 1e-10
+    if d > 1:
+        ref = O.round_rand_orth_tt(x, targets, 6, rng=O.PHILOX)
+        y = P.round_rand_orth_tt(tx, targets, 6)
+        assert y.ranks() == ref.ranks
+        assert rel_err_vs_ref(ref, y) <= 1e-10
+
+
+def test_zero_tensor_inputs(P, O):
+    """An all-zero tensor: every sketch is zero, Householder takes tau = 0, the
+    result is the zero tensor with the capped ranks (no NaN anywhere)."""
+    n, r = [4, 5, 4], [1, 3, 3, 1]
+    z = _zero_tt(O, n, r)
+    y = P.round_fixed_krp(to_device(z), [2, 2], 1)
+    ref = O.round_fixed_krp(z, [2, 2], 1, rng=O.PHILOX)
+    assert y.ranks() == ref.ranks
+    f = y.flat()
+    assert np.all(np.isfinite(f))
+    assert P.norm_exact(y) == 0.0
+    yd = P.round_deterministic(to_device(z), target_ranks=[2, 2])
+    assert np.all(np.isfinite(yd.flat())) and P.norm_exact(yd) == 0.0
+
+
+def test_nan_free_rank_deficient_sketch(P, O):
+    """Exactly rank-deficient padded input (true ranks 2 stored as 6): fixed
+    rounding to 6 keeps an orthonormal basis (QR of a rank-2 sketch) and
+    reproduces the tensor (the last bond of configs 3/5 behaves like this)."""
+    x = O.random_gaussian_tt([6, 6, 6, 6], [1, 2, 2, 2, 1], 99)
+    cores = x.cores()
+    pad = [1, 6, 6, 6, 1]
+    padded = []
+    for k, c in enumerate(cores):
+        zc = np.zeros((pad[k], c.shape[1], pad[k + 1]))
+        zc[:c.shape[0], :, :c.shape[2]] = c
+        padded.append(zc)
+    xp = O.TT.from_cores(padded)
+    y = P.round_fixed_krp(to_device(xp), [6, 6, 6], 2)
+    assert np.all(np.isfinite(y.flat()))
+    assert rel_err_vs_ref(xp, y) <= 1e-10
+    assert left_orth_defect(y.cores()) <= 1e-12
