@@ -359,7 +359,6 @@ int blocks_for(Ctx& c, i64 work) {
     return static_cast<int>(std::max<i64>(1, std::min<i64>((work + 255) / 256, 4LL * c.sm_count)));
 }
 
-constexpr i64 kSmallMaxElems = 26000;  // ~203 KB of shared memory
 
 std::size_t small_smem_bytes(i64 m, i64 n) { return sizeof(double) * static_cast<std::size_t>(m * n + n + 32 + 4); }
 
@@ -383,27 +382,39 @@ void thin_qr(Ctx& c, i64 m, i64 n, const double* A, i64 lda, double* Q, i64 ldq,
     const i64 k = std::min(m, n);
     c.charge_qr(4ULL * static_cast<std::uint64_t>(m) * n * k);
     if (m <= 0 || n <= 0) return;
-    (void)kSmallMaxElems;  // the single-CTA smem kernel serves the batched API only
-    // Panels hold at most 2 rows x 32 columns per thread in registers (one CTA
-    // per SM): taller R-only factorizations (norm_exact of very tall cores)
-    // go through a TSQR split — R of each row block, then R of the stacked Rs.
-    const i64 max_rows = 8LL * 48 * c.sm_count;  // panel_col_kernel grid limit (8 warps x 48 rows per SM)
+    // A panel lives in registers of at most one CTA per SM (launch_panel_col:
+    // up to 8 warps x 64 rows per SM). Taller matrices take a TSQR split: QR of
+    // each row block, QR of the stacked R factors, and — when Q is requested —
+    // Q(block q) = Q_q Q_s(q-th block) by one GEMM per block. Charged once, as
+    // one QR of the whole matrix (linalg.cpp:48).
+    const i64 max_rows = 8LL * 64 * c.sm_count;
     if (m > max_rows) {
-        if (Q != nullptr) throw Error(TTR_ERR_INTERNAL, "thin_qr with Q: matrix taller than the device panel limit");
+        const Counts saved = c.counts;
         const i64 chunk = std::max<i64>(k, max_rows / 2);
         const i64 nchunks = (m + chunk - 1) / chunk;
-        DBuf stack(c, static_cast<std::size_t>(nchunks * k * n));
         const i64 lds = nchunks * k;
+        DBuf stack(c, static_cast<std::size_t>(lds * n));
+        TTR_CUDA(cudaMemsetAsync(stack.p, 0, sizeof(double) * lds * n, c.stream));
+        std::vector<DBuf> Qq(static_cast<std::size_t>(Q ? nchunks : 0));
         for (i64 q = 0; q < nchunks; ++q) {
             const i64 r0 = q * chunk, rows = std::min(chunk, m - r0), kq = std::min(rows, n);
             DBuf Rq(c, static_cast<std::size_t>(kq * n));
-            thin_qr(c, rows, n, A + r0, lda, nullptr, 1, Rq.p, kq);
-            if (kq < k)
-                TTR_CUDA(cudaMemset2DAsync(stack.p + q * k, sizeof(double) * lds, 0, sizeof(double) * k, n, c.stream));
+            if (Q) Qq[q] = DBuf(c, static_cast<std::size_t>(rows * kq));
+            thin_qr(c, rows, n, A + r0, lda, Q ? Qq[q].p : nullptr, rows, Rq.p, kq);
             TTR_CUDA(cudaMemcpy2DAsync(stack.p + q * k, sizeof(double) * lds, Rq.p, sizeof(double) * kq,
                                        sizeof(double) * kq, n, cudaMemcpyDeviceToDevice, c.stream));
         }
-        thin_qr(c, lds, n, stack.p, lds, nullptr, 1, R, ldr);
+        if (!Q) {
+            thin_qr(c, lds, n, stack.p, lds, nullptr, 1, R, ldr);
+        } else {
+            DBuf Qs(c, static_cast<std::size_t>(lds * k));
+            thin_qr(c, lds, n, stack.p, lds, Qs.p, lds, R, ldr);
+            for (i64 q = 0; q < nchunks; ++q) {
+                const i64 r0 = q * chunk, rows = std::min(chunk, m - r0), kq = std::min(rows, n);
+                gemm(c, false, rows, k, kq, 1.0, Qq[q].p, rows, Qs.p + q * k, lds, 0.0, Q + r0, ldq, false);
+            }
+        }
+        c.counts = saved;
         return;
     }
     // Launch the column-per-lane panel kernel on a rows x b panel (b <= 32):

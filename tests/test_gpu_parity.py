@@ -36,7 +36,8 @@ def test_gemm_matches_numpy(P, m, n, k, ta):
     assert np.linalg.norm(c - ref) <= 1e-13 * np.sqrt(k) * np.linalg.norm(np.abs(a)) * np.linalg.norm(np.abs(b)) + 1e-300
 
 
-@pytest.mark.parametrize("m,n", [(6, 3), (64, 64), (320, 20), (300, 15), (7040, 110), (2000, 70), (40, 60)])
+@pytest.mark.parametrize("m,n", [(6, 3), (64, 64), (320, 20), (300, 15), (7040, 110), (2000, 70), (40, 60),
+                                 (80000, 8), (160000, 40)])  # the last two exceed one panel grid: TSQR split
 def test_thin_qr(P, m, n):
     rng = np.random.default_rng(m + 13 * n)
     a = rng.standard_normal((m, n))
