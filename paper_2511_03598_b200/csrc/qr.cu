@@ -427,7 +427,7 @@ void thin_qr(Ctx& c, i64 m, i64 n, const double* A, i64 lda, double* Q, i64 ldq,
         return launch_panel_col(c, a);
     };
 
-    // ---- <= 32 columns: factorization and explicit Q in one launch ----
+    // ---- <= 32 columns: one panel launch ----
     if (n <= kPanel) {
         DBuf tau(c, static_cast<std::size_t>(k));
         RegQrArgs a{};
@@ -436,11 +436,31 @@ void thin_qr(Ctx& c, i64 m, i64 n, const double* A, i64 lda, double* Q, i64 ldq,
         a.Pin = A;
         a.ldin = lda;
         a.tau = tau.p;
-        a.Q = Q;
-        a.ldq = ldq;
         a.R = R;
         a.ldr = ldr;
+        // Q in registers costs one more cross-CTA exchange per column; on the
+        // cooperative grid (> 2048 rows, ~3 us per exchange) Q = [I;0] - V (T V_1^T)
+        // from the panel's V and T is cheaper (the adaptive paths' growth QRs)
+        const bool wy = Q != nullptr && m > 2048 && n >= 6;
+        if (!wy) {
+            a.Q = Q;
+            a.ldq = ldq;
+            launch_panel(a);
+            return;
+        }
+        const i64 ldv = even_ld(m);
+        DBuf Vb(c, static_cast<std::size_t>(ldv * n)), Tb(c, static_cast<std::size_t>(kPanel * kPanel)),
+            V1t(c, static_cast<std::size_t>(k * k)), Y(c, static_cast<std::size_t>(k * k));
+        a.V = Vb.p;
+        a.ldv = ldv;
+        a.T = Tb.p;
         launch_panel(a);
+        transpose(c, k, k, Vb.p, ldv, V1t.p, k);                                       // V_1^T
+        gemm(c, false, k, k, k, 1.0, Tb.p, kPanel, V1t.p, k, 0.0, Y.p, k, false);      // Y = T V_1^T
+        init_thin_identity<<<blocks_for(c, m * k), 256, 0, c.stream>>>(static_cast<int>(m), static_cast<int>(k), Q, ldq);
+        TTR_CUDA(cudaGetLastError());
+        c.launched();
+        gemm(c, false, m, k, k, -1.0, Vb.p, ldv, Y.p, k, 1.0, Q, ldq, false);           // Q = [I;0] - V Y
         return;
     }
 
