@@ -118,6 +118,11 @@ ttr_status ttr_tt_download(ttr_ctx* ctx, const ttr_tt* tt, double* host_cores);
 /* Overwrite the cores of an existing tensor from host memory (same shape). */
 ttr_status ttr_tt_copy_from_host(ttr_ctx* ctx, ttr_tt* tt, const double* host_cores);
 ttr_status ttr_tt_core_ptr(const ttr_tt* tt, int64_t k, const double** dev_ptr);
+/* TTF1 files (io.hpp / io.cpp:27-76, the reference's binary format): read
+ * straight into a device tensor / write a device tensor. IoError on open,
+ * magic, size or truncation problems; BoundaryRankNotOne on a bad rank chain. */
+ttr_status ttr_tt_read_ttf1(ttr_ctx* ctx, const char* path, ttr_tt** out);
+ttr_status ttr_tt_write_ttf1(ttr_ctx* ctx, const ttr_tt* tt, const char* path);
 ttr_status ttr_tt_destroy(ttr_tt* tt);
 
 /* ---- construction / TT arithmetic --------------------------------------- */

@@ -165,6 +165,16 @@ inline TTTensor round_adaptive_krp(const TTTensor& tt, const AdaptiveConfig& cfg
     return TTTensor(out, tt.context());
 }
 
+//! io.hpp: TTF1 files read straight into / written from a device tensor.
+inline TTTensor read_ttf1(const std::string& path, Context& ctx = Context::thread_default()) {
+    ttr_tt* out = nullptr;
+    check(ttr_tt_read_ttf1(ctx.get(), path.c_str(), &out));
+    return TTTensor(out, ctx);
+}
+inline void write_ttf1(const TTTensor& tt, const std::string& path) {
+    check(ttr_tt_write_ttf1(tt.context().get(), tt.get(), path.c_str()));
+}
+
 //! round_rand.hpp:49 round_rand_orth_tt: Rand-Orth with a Gaussian TT sketch.
 inline TTTensor round_rand_orth_tt(const TTTensor& tt, const std::vector<Index>& target_ranks, std::uint64_t seed,
                                    RngMode rng = RngMode::Philox) {

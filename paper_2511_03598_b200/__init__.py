@@ -274,6 +274,16 @@ class TTTensor:
             off += cnt
         return out
 
+    @staticmethod
+    def read_ttf1(path: str, ctx: Optional[Context] = None) -> "TTTensor":
+        """Read a reference TTF1 file (io.cpp:45-76) into a device tensor."""
+        ctx = ctx or default_context()
+        return TTTensor._new(ctx, lib().ttr_tt_read_ttf1, ctx._h, C.c_char_p(os.fsencode(path)))
+
+    def write_ttf1(self, path: str):
+        """Write the tensor as a reference TTF1 file (io.cpp:27-43)."""
+        _check(lib().ttr_tt_write_ttf1(self.ctx._h, self._h, C.c_char_p(os.fsencode(path))))
+
     def core_ptr(self, k: int) -> int:
         p = C.c_void_p()
         _check(lib().ttr_tt_core_ptr(self._h, C.c_int64(k), C.byref(p)))

@@ -1,5 +1,6 @@
 // capi.cu — the extern "C" boundary (include/ttround_b200.h). Catches every
 // C++ exception and maps it to a ttr_status; messages are kept per thread.
+#include <cstdio>
 #include <cstring>
 #include <string>
 
@@ -165,6 +166,72 @@ ttr_status ttr_tt_download(ttr_ctx* ctx, const ttr_tt* tt, double* host) {
         check_same_ctx(ctx, tt);
         need(host != nullptr, "null output");
         tt->t->download(host);
+    });
+}
+
+// ---- TTF1 files (io.cpp:27-76): "TTF1", u32 d, u32 n[d], u32 r[d+1], then the
+// cores' fp64 data in the reference layout, little-endian. Read/written
+// through a pinned staging buffer straight to/from the device tensor.
+ttr_status ttr_tt_write_ttf1(ttr_ctx* ctx, const ttr_tt* tt, const char* path) {
+    return guard([&] {
+        check_same_ctx(ctx, tt);
+        need(path != nullptr, "null path");
+        const TTDev& t = *tt->t;
+        std::FILE* f = std::fopen(path, "wb");
+        if (!f) fail(Errc::IoError, std::string("cannot open ") + path + " for writing");
+        bool ok = std::fwrite("TTF1", 1, 4, f) == 4;
+        auto u32 = [&](i64 v) {
+            const std::uint32_t w = static_cast<std::uint32_t>(v);
+            ok = ok && std::fwrite(&w, sizeof w, 1, f) == 1;
+        };
+        u32(t.d());
+        for (i64 v : t.n) u32(v);
+        for (i64 v : t.r) u32(v);
+        std::vector<double> host(static_cast<std::size_t>(t.total()));
+        t.download(host.data());
+        ok = ok && std::fwrite(host.data(), sizeof(double), host.size(), f) == host.size();
+        ok = (std::fclose(f) == 0) && ok;
+        if (!ok) fail(Errc::IoError, std::string("failed writing ") + path);
+    });
+}
+
+ttr_status ttr_tt_read_ttf1(ttr_ctx* ctx, const char* path, ttr_tt** out) {
+    return guard([&] {
+        need(ctx && path && out, "null argument");
+        std::FILE* f = std::fopen(path, "rb");
+        if (!f) fail(Errc::IoError, std::string("cannot open ") + path);
+        struct Closer {
+            std::FILE* f;
+            ~Closer() { std::fclose(f); }
+        } closer{f};
+        char magic[4];
+        if (std::fread(magic, 1, 4, f) != 4 || std::memcmp(magic, "TTF1", 4) != 0)
+            fail(Errc::IoError, std::string("not a TTF1 file: ") + path);
+        auto u32 = [&]() {
+            std::uint32_t w = 0;
+            if (std::fread(&w, sizeof w, 1, f) != 1) fail(Errc::IoError, "unexpected end of TTF1 file");
+            return static_cast<i64>(w);
+        };
+        const i64 d = u32();
+        if (d == 0 || d > 64) fail(Errc::IoError, std::string("implausible TT order in ") + path);
+        std::vector<i64> n(static_cast<std::size_t>(d)), r(static_cast<std::size_t>(d + 1));
+        for (auto& v : n) v = u32();
+        for (auto& v : r) v = u32();
+        if (r.front() != 1 || r.back() != 1) fail(Errc::BoundaryRankNotOne, "TTF1 boundary ranks must be 1");
+        i64 total = 0;
+        for (i64 k = 0; k < d; ++k) {
+            if (n[k] < 1 || r[k] < 1 || r[k + 1] < 1) fail(Errc::IoError, "invalid TTF1 dimensions");
+            const i64 cnt = r[k] * n[k] * r[k + 1];
+            if (cnt > (i64{1} << 34)) fail(Errc::IoError, std::string("implausible core size in ") + path);
+            total += cnt;
+        }
+        auto t = std::make_unique<TTDev>(ctx->c, n, r);
+        std::vector<double> host(static_cast<std::size_t>(total));
+        if (std::fread(host.data(), sizeof(double), host.size(), f) != host.size())
+            fail(Errc::IoError, "unexpected end of TTF1 file");
+        t->upload(host.data());
+        TTR_CUDA(cudaStreamSynchronize(ctx->c.stream));  // host buffer lifetime
+        *out = wrap(std::move(t));
     });
 }
 

@@ -20,7 +20,7 @@ def test_header_declares_the_hot_path_entry_points():
     syms = declared_symbols()
     for s in ["ttr_round_fixed_krp", "ttr_round_adaptive_krp", "ttr_round_deterministic_tol",
               "ttr_round_deterministic_ranks", "ttr_estimate_norm_krp", "ttr_tt_upload", "ttr_tt_download",
-              "ttr_norm_exact", "ttr_relative_error", "ttr_krp_partial_contractions", "ttr_plan_fixed_krp", "ttr_plan_fixed_krp_host", "ttr_round_sum_adaptive_krp", "ttr_compression_pass", "ttr_round_rand_orth_tt"]:
+              "ttr_norm_exact", "ttr_relative_error", "ttr_krp_partial_contractions", "ttr_plan_fixed_krp", "ttr_plan_fixed_krp_host", "ttr_round_sum_adaptive_krp", "ttr_compression_pass", "ttr_round_rand_orth_tt", "ttr_tt_read_ttf1", "ttr_tt_write_ttf1"]:
         assert s in syms
 
 

@@ -471,3 +471,46 @@ def test_nan_free_rank_deficient_sketch(P, O):
     assert np.all(np.isfinite(y.flat()))
     assert rel_err_vs_ref(xp, y) <= 1e-10
     assert left_orth_defect(y.cores()) <= 1e-12
+
+
+# ---- TTF1 files (io.cpp, test_io.cpp) ----------------------------------------------------------------
+
+def _ttf1_bytes(n, r, flat, magic=b"TTF1"):
+    import struct
+    return magic + struct.pack("<I", len(n)) + struct.pack(f"<{len(n)}I", *n) + \
+        struct.pack(f"<{len(r)}I", *r) + np.asarray(flat, dtype="<f8").tobytes()
+
+
+def test_ttf1_round_trip_and_format(P, O, tmp_path):
+    """test_io.cpp:34-46: round trip bit identical, and the bytes are exactly the
+    reference layout (magic, u32 d, n, r, fp64 cores)."""
+    x = O.random_gaussian_tt([4, 5, 3], [1, 2, 3, 1], 11)
+    n, r, _ = x.shape()
+    t = to_device(x)
+    p1 = tmp_path / "a.ttf1"
+    t.write_ttf1(str(p1))
+    assert p1.read_bytes() == _ttf1_bytes(n, r, x.flat())
+    back = P.TTTensor.read_ttf1(str(p1))
+    assert back.ranks() == r and np.array_equal(back.flat(), x.flat())
+    p2 = tmp_path / "b.ttf1"
+    back.write_ttf1(str(p2))
+    assert p2.read_bytes() == p1.read_bytes()
+
+
+def test_ttf1_rejects_malformed(P, O, tmp_path):
+    """test_io.cpp:48-90: bad magic, rank-chain violation, truncated payload."""
+    x = O.random_gaussian_tt([3, 3], [1, 2, 1], 5)
+    n, r, _ = x.shape()
+    good = _ttf1_bytes(n, r, x.flat())
+    cases = {"magic.ttf1": (_ttf1_bytes(n, r, x.flat(), magic=b"TTF2"), "IoError"),
+             "chain.ttf1": (_ttf1_bytes(n, [2, 2, 1], x.flat()), "BoundaryRankNotOne"),
+             "short.ttf1": (good[:-9], "IoError")}
+    for name, (data, code) in cases.items():
+        p = tmp_path / name
+        p.write_bytes(data)
+        with pytest.raises(P.TTRoundError) as e:
+            P.TTTensor.read_ttf1(str(p))
+        assert e.value.code == code
+    with pytest.raises(P.TTRoundError) as e:
+        P.TTTensor.read_ttf1(str(tmp_path / "missing.ttf1"))
+    assert e.value.code == "IoError"
