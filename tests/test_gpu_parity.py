@@ -514,3 +514,35 @@ def test_ttf1_rejects_malformed(P, O, tmp_path):
     with pytest.raises(P.TTRoundError) as e:
         P.TTTensor.read_ttf1(str(tmp_path / "missing.ttf1"))
     assert e.value.code == "IoError"
+
+
+def test_cli_round_matches_api(P, O, tmp_path):
+    """The `round` command (tools/ttround_main.cpp:142-184 mirror): TTF1 in, TTF1
+    out, the reference's JSON record; krp-fix with the reference stream equals the
+    oracle's xoshiro rounding; krp-adapt-r runs the compression pass."""
+    import json
+    import subprocess
+    import sys
+    x = O.two_part_tt(5, 12, 6, 18, 1e-6, 321)
+    inp, out = tmp_path / "x.ttf1", tmp_path / "y.ttf1"
+    to_device(x).write_ttf1(str(inp))
+    cmd = [sys.executable, "-m", "paper_2511_03598_b200.cli", "round", str(inp), str(out), "--algo", "krp-fix",
+           "--ranks", "8", "8", "8", "8", "--seed", "7"]
+    res = subprocess.run(cmd, capture_output=True, text=True, cwd=__import__("os").path.dirname(__import__("os").path.dirname(__file__)))
+    assert res.returncode == 0, res.stderr
+    rec = json.loads(res.stdout.strip().splitlines()[-1])
+    assert set(rec) >= {"algorithm", "mode", "target", "rel_error", "ranks", "wall_seconds", "flops_total", "seed"}
+    y = P.TTTensor.read_ttf1(str(out))
+    ref = O.round_fixed_krp(x, [8] * 4, 7, rng=O.XOSHIRO)
+    assert y.ranks() == ref.ranks == rec["ranks"]
+    assert rel_err_vs_ref(ref, y) <= 1e-10
+    cmd[cmd.index("krp-fix")] = "krp-adapt-r"
+    i = cmd.index("--ranks")
+    del cmd[i:i + 5]
+    cmd += ["--tol", "1e-4"]
+    res = subprocess.run(cmd, capture_output=True, text=True, cwd=__import__("os").path.dirname(__import__("os").path.dirname(__file__)))
+    assert res.returncode == 0, res.stderr
+    assert json.loads(res.stdout.strip().splitlines()[-1])["mode"] == "tolerance"
+    bad = subprocess.run(cmd[:4] + [str(tmp_path / "nope.ttf1"), str(out)], capture_output=True, text=True,
+                         cwd=__import__("os").path.dirname(__import__("os").path.dirname(__file__)))
+    assert bad.returncode == 2 and "IoError" in bad.stderr
