@@ -104,6 +104,12 @@ class _AdaptiveCfg(C.Structure):
                 ("max_rank_cap", C.POINTER(C.c_int64)), ("rng_mode", C.c_int)]
 
 
+def _ctx_alive(obj) -> bool:
+    ctx = getattr(obj, "ctx", None)
+    h = getattr(ctx, "_h", None)
+    return bool(h is not None and h.value)
+
+
 class Context:
     """One CUDA device + stream (ttr_ctx). Pass `stream` (an int handle, e.g.
     torch.cuda.current_stream().cuda_stream) to order work on a caller stream."""
@@ -161,7 +167,9 @@ class TTTensor:
         self.ctx = ctx
 
     def __del__(self):
-        if getattr(self, "_h", None) and self._h.value and _lib is not None:
+        # a tensor outliving its context (garbage-collection order at teardown)
+        # is not destroyed: its device memory went with the context
+        if getattr(self, "_h", None) and self._h.value and _lib is not None and _ctx_alive(self):
             _lib.ttr_tt_destroy(self._h)
             self._h = C.c_void_p()
 
@@ -365,7 +373,7 @@ class FixedKrpPlan:
         _check(lib().ttr_plan_execute(self._h))
 
     def close(self):
-        if getattr(self, "_h", None) and self._h.value and _lib is not None:
+        if getattr(self, "_h", None) and self._h.value and _lib is not None and _ctx_alive(self):
             _lib.ttr_plan_destroy(self._h)
             self._h = C.c_void_p()
 
@@ -398,7 +406,7 @@ class TTBatch:
         self.ctx = ctx
 
     def __del__(self):
-        if getattr(self, "_h", None) and self._h.value and _lib is not None:
+        if getattr(self, "_h", None) and self._h.value and _lib is not None and _ctx_alive(self):
             _lib.ttr_batch_destroy(self._h)
             self._h = C.c_void_p()
 

@@ -546,3 +546,47 @@ def test_cli_round_matches_api(P, O, tmp_path):
     bad = subprocess.run(cmd[:4] + [str(tmp_path / "nope.ttf1"), str(out)], capture_output=True, text=True,
                          cwd=__import__("os").path.dirname(__import__("os").path.dirname(__file__)))
     assert bad.returncode == 2 and "IoError" in bad.stderr
+
+
+# ---- BASELINE full sizes: size-independent properties ------------------------------------------
+
+@pytest.mark.parametrize("cfg", ["3", "5b"])
+def test_full_size_fixed_rank_properties(P, cfg):
+    """Configs 3 and 5b at their full BASELINE sizes (2.3 GB / 18.4 GB of cores):
+    the expected rank vector, left-orthogonal cores, error at the
+    noise level of the input (X + eps Z rounded to a rank >= rank(X)), bitwise
+    determinism, and the CUDA-graph plan == the eager call."""
+    from paper_2511_03598_b200.seeds import derive_seed
+    if cfg == "3":
+        d, n, rx, rz, eps, ell, seed = 30, 64, 100, 300, 1e-8, 110, 1003
+    else:
+        d, n, rx, rz, eps, ell, seed = 20, 128, 300, 700, 1e-8, 320, 1005
+    ctx = P.Context(0)
+    modes = [n] * d
+    x = P.TTTensor.random_philox(modes, [1] + [rx] * (d - 1) + [1], derive_seed(seed, 1), ctx)
+    z = P.TTTensor.random_philox(modes, [1] + [rz] * (d - 1) + [1], derive_seed(seed, 2), ctx)
+    x = P.scaled(x, 1.0 / P.norm_exact(x))
+    z = P.scaled(z, eps / P.norm_exact(z))
+    y = P.formal_sum([x, z])
+    del z
+    out = P.round_fixed_krp(y, [ell] * (d - 1), 7)
+    expect = [1, n] + [ell] * (d - 2) + [1]
+    assert out.ranks() == expect
+    # left-orthogonality of cores 0..d-2 (on the device: ||V^T V - I|| via GEMM)
+    for k in (0, 1, d // 2, d - 2):
+        v = out.cores()[k]
+        rl, nn, rr = v.shape
+        m = v.reshape(rl * nn, rr, order="F")
+        assert np.linalg.norm(m.T @ m - np.eye(rr)) <= 1e-11
+    # randomized rounding error at the noise level: rounding to >= rank(X) keeps X;
+    # the per-bond noise residuals add up over the d-1 bonds (~ eps sqrt(d-1))
+    bound = 3 * eps * np.sqrt(d - 1)
+    err = P.relative_error(y, out)
+    assert err <= bound, err
+    assert P.relative_error(x, out) <= bound
+    again = P.round_fixed_krp(y, [ell] * (d - 1), 7)
+    assert np.array_equal(again.flat(), out.flat())
+    plan = P.FixedKrpPlan(y, [ell] * (d - 1), 7)
+    plan.execute()
+    assert np.array_equal(plan.output.flat(), out.flat())
+    plan.close()
