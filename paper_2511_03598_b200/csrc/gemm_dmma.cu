@@ -500,6 +500,9 @@ void run_gemm(Ctx& c, bool AT, int KM, int BK, GemmArgs& a, bool va2, bool vb2, 
             done = AT ? launch_tma<64, 64, true, 0, 2>(c, a, splits) : launch_tma<64, 64, false, 0, 2>(c, a, splits);
         else if (medium && KM == 0) done = AT ? launch_tma<64, 64, true, 0>(c, a, splits) : launch_tma<64, 64, false, 0>(c, a, splits);
         else if (KM == 0) done = AT ? launch_tma<128, 64, true, 0>(c, a, splits) : launch_tma<128, 64, false, 0>(c, a, splits);
+        // narrow KRP products (adaptive appends, N <= 32): 32-column tiles; the
+        // per-column summation order is the same as with 64 (append == one-shot)
+        else if (!medium && KM == 1 && !AT && a.N <= 32) done = launch_tma<128, 32, false, 1>(c, a, splits);
         else if (!medium && KM == 1 && !AT) done = launch_tma<128, 64, false, 1>(c, a, splits);
     }
     if (done) {

@@ -72,9 +72,12 @@ struct Sketch {
         for (i64 k = d; k >= start; --k) {
             const i64 rl = t.r[k - 1], nk = t.n[k - 1], rr = t.r[k];
             if (c.io) c.io->wait_in(c.stream, static_cast<std::size_t>(k - 1));  // core k-1 arrived (H2D)
-            const double* wt_next = (k == d) ? ones.p : Wt[k + 1].p + col0;
+            // Wt only carries this append's columns to the next mode: it starts
+            // at column 0 so the contraction's W operand is always 16-byte
+            // aligned (TMA-eligible) whatever the append offset
+            const double* wt_next = (k == d) ? ones.p : Wt[k + 1].p;
             const i64 ld_next = ldwt;
-            double* wt_out = (k >= 3) ? Wt[k].p + col0 : nullptr;
+            double* wt_out = (k >= 3) ? Wt[k].p : nullptr;
             krp_step(c, rl, nk, rr, extra, t.core(k - 1), omega[k].p + col0 * ldo[k], ldo[k], k == d ? ones.p : wt_next,
                      ld_next, W[k].p + col0 * ldw[k], ldw[k], wt_out, ldwt, k == d);
             width[k] = col0 + extra;
@@ -147,8 +150,8 @@ struct BatchSketch {
             const i64 rl = t.r[k - 1], nk = t.n[k - 1], rr = t.r[k];
             const bool last = (k == d);
             krp_step_batched(c, rl, nk, rr, extra, t.core(0, k - 1), t.stride, omega[k].p + col0 * ldo[k], ldo[k], 0,
-                             last ? ones.p : Wt[k + 1].p + col0, ldwt, last ? 0 : ldwt * rr, W[k].p + col0 * ldw[k],
-                             ldw[k], rl, k >= 3 ? Wt[k].p + col0 : nullptr, ldwt, ldwt * rl, s, last);
+                             last ? ones.p : Wt[k + 1].p, ldwt, last ? 0 : ldwt * rr, W[k].p + col0 * ldw[k],
+                             ldw[k], rl, k >= 3 ? Wt[k].p : nullptr, ldwt, ldwt * rl, s, last);
             width[k] = col0 + extra;
         }
     }
