@@ -177,6 +177,7 @@ struct RegQrArgs {
 };
 
 #include "qr_panel.cuh"
+#include "qr_batch.cuh"
 
 template <int RPT, int WARPS, int MODE>
 void launch_col(Ctx& c, const RegQrArgs& a, i64 grid) {
@@ -366,6 +367,45 @@ std::size_t small_smem_bytes(i64 m, i64 n) { return sizeof(double) * static_cast
 
 void qr_small_batched(Ctx& c, i64 m, i64 n, const double* A, i64 lda, i64 sA, double* Q, i64 ldq, i64 sQ, double* R,
                       i64 ldr, i64 sR, i64 batch) {
+    // <= 32 columns and <= 512 rows: register-resident column owners
+    // (qr_batch.cuh); otherwise the whole matrix in one CTA's shared memory
+    if (n <= 32 && m <= 512) {
+        const int rt_need = static_cast<int>((m + 31) / 32), cn = static_cast<int>((n + 7) / 8);
+        static const int kRt[] = {1, 2, 4, 6, 8, 10, 12, 16};
+        int rt = 16;
+        for (int v : kRt)
+            if (v >= rt_need) {
+                rt = v;
+                break;
+            }
+        const std::size_t smem = sizeof(double) * static_cast<std::size_t>(2 * 32 * rt + 6 + 32);
+        bool done = false;
+        auto go = [&](auto rt_tag, auto c_tag) {
+            constexpr int RT = decltype(rt_tag)::value, CC = decltype(c_tag)::value;
+            if (rt != RT || cn != CC) return;
+            qr_small_colreg_kernel<RT, CC><<<static_cast<unsigned>(batch), 256, smem, c.stream>>>(
+                static_cast<int>(m), static_cast<int>(n), A, lda, sA, Q, ldq, sQ, R, ldr, sR);
+            done = true;
+        };
+        auto per_c = [&](auto rt_tag) {
+            go(rt_tag, std::integral_constant<int, 1>{});
+            go(rt_tag, std::integral_constant<int, 2>{});
+            go(rt_tag, std::integral_constant<int, 3>{});
+            go(rt_tag, std::integral_constant<int, 4>{});
+        };
+        per_c(std::integral_constant<int, 1>{});
+        per_c(std::integral_constant<int, 2>{});
+        per_c(std::integral_constant<int, 4>{});
+        per_c(std::integral_constant<int, 6>{});
+        per_c(std::integral_constant<int, 8>{});
+        per_c(std::integral_constant<int, 10>{});
+        per_c(std::integral_constant<int, 12>{});
+        per_c(std::integral_constant<int, 16>{});
+        if (!done) throw Error(TTR_ERR_INTERNAL, "qr_small_colreg dispatch");
+        TTR_CUDA(cudaGetLastError());
+        c.launched();
+        return;
+    }
     const std::size_t smem = small_smem_bytes(m, n);
     static bool configured = false;
     if (!configured) {

@@ -371,6 +371,24 @@ def test_batched_fixed_krp_config5a_parity(P, O):
         assert O.relative_error(y_ref, y_gpu) <= 1e-10
 
 
+@pytest.mark.parametrize("d,n,r1,r2,l", [(4, 8, 3, 5, 6), (4, 16, 8, 16, 12), (5, 12, 10, 20, 28),
+                                          (4, 40, 4, 8, 30)])
+def test_batched_shapes_parity(P, O, d, n, r1, r2, l):
+    """Batched QR dispatch (register column owners: 1..4 columns per warp, 1..12 row
+    chunks; > 512 rows: the shared-memory kernel) against the oracle, rank-deficient
+    last bond included."""
+    B = 6
+    xs = [O.two_part_tt(d, n, r1, r2, 1e-6, O.derive_seed(77, b)) for b in range(B)]
+    nn, r, _ = xs[0].shape()
+    out = P.round_fixed_krp_batched(P.TTBatch.from_flats(nn, r, [x.flat() for x in xs]), [l] * (d - 1), 5)
+    _, on, orr, _ = out.shape()
+    flats = out.flats()
+    for b in (0, B - 1):
+        y_ref = O.round_fixed_krp(xs[b], [l] * (d - 1), O.derive_seed(5, b), rng=O.PHILOX)
+        assert y_ref.ranks == orr
+        assert O.relative_error(y_ref, O.TT.from_flat(len(on), on, orr, flats[b])) <= 1e-10
+
+
 def test_batched_equals_single(P, O):
     xs = [O.two_part_tt(5, 20, 6, 10, 1e-4, 40 + b) for b in range(3)]
     n, r, _ = xs[0].shape()
