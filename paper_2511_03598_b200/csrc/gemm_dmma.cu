@@ -80,14 +80,15 @@ struct Cfg {
     static constexpr int kWarpsM = BM / WM, kWarpsN = BN / WN;
     static constexpr int kThreads = kWarpsM * kWarpsN * 32;
     // A tile: normal -> [BK][BM+4] (m contiguous); transposed -> [BM][BK+4]
-    static constexpr int kLdA = AT ? (BK + 4) : (BM + 4);
-    static constexpr int kASize = AT ? BM * (BK + 4) : BK * (BM + 4);
+    // (BM + pad) % 16 == 4 for every BM (24-row tiles pad by 12)
+    static constexpr int kLdA = AT ? (BK + 4) : (BM + (20 - BM % 16) % 16);
+    static constexpr int kASize = AT ? BM * kLdA : BK * kLdA;
     static constexpr int kLdB = BK + 4;  // B tile [BN][BK+4] (k contiguous)
     static constexpr int kBSize = BN * (BK + 4);
     static constexpr int kWSize = KM == 1 ? BN : (KM == 2 ? BN * (BK + 4) : 0);
     static constexpr int kStage = kASize + kBSize + kWSize;
     static constexpr int kSmemBytes = STAGES * kStage * 8;
-    static_assert((BM + 4) % 16 == 4 || AT, "A pad keeps 64-bit fragment loads conflict free");
+    static_assert(kLdA % 16 == 4 || AT, "A pad keeps 64-bit fragment loads conflict free");
     static_assert((BK + 4) % 16 == 4 || BK == 4, "B pad keeps 64-bit fragment loads conflict free");
 };
 
@@ -392,6 +393,22 @@ bool make_map(CUtensorMap* m, const double* base, i64 inner, i64 outer, i64 ld, 
                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+bool narrow_tiles() {
+    static const bool on = [] {
+        const char* e = std::getenv("TTR_GEMM_NARROW");  // experiments: TTR_GEMM_NARROW=0 keeps 32-wide tiles
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
+bool narrow_lr() {
+    static const bool on = [] {
+        const char* e = std::getenv("TTR_GEMM_NARROW_LR");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 bool tma_enabled() {
     static const bool on = [] {
         const char* e = std::getenv("TTR_GEMM_TMA");  // experiments: TTR_GEMM_TMA=0 selects the cp.async kernel
@@ -461,6 +478,15 @@ void dispatch_vec(Ctx& c, GemmArgs& a, int splits, bool va2, bool vb2) {
     }
 }
 
+// explicit warp tile (24-wide tiles for the 20-column products of batched 5a)
+template <int BM, int BN, int WM, int WN, bool AT, int KM, int BK, int ST = kStages>
+void dispatch_vec_w(Ctx& c, GemmArgs& a, int splits, bool va2, bool vb2) {
+    if (va2 && vb2) launch<BM, BN, BK, WM, WN, ST, AT, KM, 2, 2>(c, a, splits);
+    else if (va2) launch<BM, BN, BK, WM, WN, ST, AT, KM, 2, 1>(c, a, splits);
+    else if (vb2) launch<BM, BN, BK, WM, WN, ST, AT, KM, 1, 2>(c, a, splits);
+    else launch<BM, BN, BK, WM, WN, ST, AT, KM, 1, 1>(c, a, splits);
+}
+
 bool aligned16(const void* p) { return (reinterpret_cast<std::uintptr_t>(p) & 15) == 0; }
 
 // Grid shaping: enough CTAs to cover 2 waves of 148 SMs when the MxN tile
@@ -505,7 +531,20 @@ void run_gemm(Ctx& c, bool AT, int KM, int BK, GemmArgs& a, bool va2, bool vb2, 
         else if (!medium && KM == 1 && !AT && a.N <= 32) done = launch_tma<128, 32, false, 1>(c, a, splits);
         else if (!medium && KM == 1 && !AT) done = launch_tma<128, 64, false, 1>(c, a, splits);
     }
+    const bool narrow = a.batch > 1 && narrow_tiles();
     if (done) {
+    } else if (narrow && skinny && KM == 0 && a.M <= 24 && (AT || narrow_lr())) {
+        // batched M <= 24 (5a: M H(X) and Q^T V with l = 20): 24-row tiles, 64 columns when N <= 64
+        if (AT && a.N <= 64) dispatch_vec_w<24, 64, 24, 32, true, 0, 16>(c, a, splits, va2, vb2);
+        else if (AT) dispatch_vec_w<24, 128, 24, 32, true, 0, 16>(c, a, splits, va2, vb2);
+        else if (a.N <= 64) dispatch_vec_w<24, 64, 24, 32, false, 0, 16>(c, a, splits, va2, vb2);
+        else dispatch_vec_w<24, 128, 24, 32, false, 0, 16>(c, a, splits, va2, vb2);
+    } else if (narrow && small && a.N <= 24 && KM != 2) {
+        // batched N <= 24 (5a: the KRP sketch and S = V W with l = 20): 24-column tiles
+        if (KM == 0 && AT) dispatch_vec_w<64, 24, 32, 24, true, 0, 16>(c, a, splits, va2, vb2);
+        else if (KM == 0) dispatch_vec_w<64, 24, 32, 24, false, 0, 16>(c, a, splits, va2, vb2);
+        else if (BK == 16) dispatch_vec_w<64, 24, 32, 24, false, 1, 16>(c, a, splits, va2, vb2);
+        else dispatch_vec_w<64, 24, 32, 24, false, 1, 4>(c, a, splits, va2, vb2);
     } else if (skinny && KM == 0) {
         if (AT) dispatch_vec<kSkBM, kSkBN, true, 0, 16>(c, a, splits, va2, vb2);
         else dispatch_vec<kSkBM, kSkBN, false, 0, 16>(c, a, splits, va2, vb2);
