@@ -4,8 +4,9 @@
 // CTA owns RPT consecutive rows and lane l of every warp owns COLUMN l, so a
 // thread holds its column's entries for its warp's rows in registers (x[RPT],
 // always indexed by compile-time q). One column step i:
-//   * dots: the active column is broadcast row by row from lane i (shuffle)
-//     and lane l accumulates x(r,i)*x(r,l) over its rows with r > i,
+//   * dots: lane i stages the active column of its warp's rows in shared
+//     memory (read back with 16-byte broadcast loads: a 64-bit shuffle is two
+//     SHFLs) and lane l accumulates x(r,i)*x(r,l) over its rows with r > i,
 //   * the warp partials are summed in shared memory, the CTA partials through
 //     distributed shared memory inside ONE thread-block cluster (MODE 0:
 //     <= 16 CTAs) or through global memory (cooperative launch, <= one CTA
@@ -35,6 +36,10 @@ __global__ void __launch_bounds__(WARPS * 32, 1) panel_col_kernel(RegQrArgs p) {
     constexpr int LW = WARPS >= 16 ? 16 : 8;  // grid mode: warps gathering CTA partials
     __shared__ double xs[LW * 32];
     __shared__ double gm[32 * 32];  // Gram entries v_k^T v_m (k < m), column m
+    // the active column of this warp's rows, staged by its lane and read back
+    // with 16-byte broadcast loads (a 64-bit shuffle is two SHFLs)
+    static_assert(RPT % 2 == 0, "RPT even: double2 staging");
+    __shared__ __align__(16) double colst[WARPS][RPT];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     int rank, G;
     if constexpr (CL) {
@@ -62,23 +67,33 @@ __global__ void __launch_bounds__(WARPS * 32, 1) panel_col_kernel(RegQrArgs p) {
         x[q] = (rr < nr && lane < b) ? p.Pin[(r0 + rr) + static_cast<i64>(lane) * p.ldin] : 0.0;
     }
 
+    double* const cw = &colst[warp][0];
+    // lane i stages column i of this warp's rows (pre-update values)
+    auto stage = [&](int i) {
+        __syncwarp();  // previous readers done
+        if (lane == i) {
+#pragma unroll
+            for (int q = 0; q < RPT; q += 2) *reinterpret_cast<double2*>(cw + q) = make_double2(x[q], x[q + 1]);
+        }
+        __syncwarp();
+    };
     // this thread's partial of sum_{r > i} x(r,i) * x(r,lane) over its rows
+    // (column i staged by the caller)
     auto dots = [&](int i) -> double {
         double s0 = 0.0, s1 = 0.0;
         if (g0 > i) {
 #pragma unroll
-            for (int q = 0; q < RPT; ++q) {
-                const double xi = __shfl_sync(0xffffffffu, x[q], i);
-                if (q & 1) s1 = fma(xi, x[q], s1);
-                else s0 = fma(xi, x[q], s0);
+            for (int q = 0; q < RPT; q += 2) {
+                const double2 xi = *reinterpret_cast<const double2*>(cw + q);
+                s0 = fma(xi.x, x[q], s0);
+                s1 = fma(xi.y, x[q + 1], s1);
             }
         } else {
 #pragma unroll
-            for (int q = 0; q < RPT; ++q) {
-                const double xi = __shfl_sync(0xffffffffu, x[q], i);
-                const double xs_ = (g0 + q > i) ? xi : 0.0;
-                if (q & 1) s1 = fma(xs_, x[q], s1);
-                else s0 = fma(xs_, x[q], s0);
+            for (int q = 0; q < RPT; q += 2) {
+                const double2 xi = *reinterpret_cast<const double2*>(cw + q);
+                s0 = fma((g0 + q > i) ? xi.x : 0.0, x[q], s0);
+                s1 = fma((g0 + q + 1 > i) ? xi.y : 0.0, x[q + 1], s1);
             }
         }
         return s0 + s1;
@@ -176,6 +191,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) panel_col_kernel(RegQrArgs p) {
     double my_inv = 0.0;  // inv of the reflector of column `lane`
     for (int i = 0; i < kk; ++i) {
         TTR_TRACE(0);
+        stage(i);
         const double mine = dots(i);
         publish_row(i);
         TTR_TRACE(1);
@@ -216,9 +232,10 @@ __global__ void __launch_bounds__(WARPS * 32, 1) panel_col_kernel(RegQrArgs p) {
         const double ca = cas[lane];
         if (g0 > i) {
 #pragma unroll
-            for (int q = 0; q < RPT; ++q) {
-                const double xi = __shfl_sync(0xffffffffu, x[q], i);
-                x[q] = fma(ca, xi, x[q]);
+            for (int q = 0; q < RPT; q += 2) {
+                const double2 xi = *reinterpret_cast<const double2*>(cw + q);
+                x[q] = fma(ca, xi.x, x[q]);
+                x[q + 1] = fma(ca, xi.y, x[q + 1]);
             }
         } else {
             // rows <= i: only row i changes (x(i,l) -= w_l; x(i,i) = beta)
@@ -226,7 +243,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) panel_col_kernel(RegQrArgs p) {
             const bool me = (lane == i);
 #pragma unroll
             for (int q = 0; q < RPT; ++q) {
-                const double xi = __shfl_sync(0xffffffffu, x[q], i);
+                const double xi = cw[q];
                 const int g = g0 + q;
                 const double below = fma(ca, xi, x[q]);
                 const double atrow = me ? diag : x[q] - wl;
@@ -280,6 +297,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) panel_col_kernel(RegQrArgs p) {
         for (int i = kk - 1; i >= 0; --i) {
             const double ti = ts[i];
             // columns l > i hold Q(:,l) so far, column i holds v_i (tail)
+            stage(i);
             if (i < kk - 1 && ti != 0.0) {  // uniform across CTAs (identical ts)
                 const double mine = dots(i);
                 publish_row(i);
@@ -300,16 +318,17 @@ __global__ void __launch_bounds__(WARPS * 32, 1) panel_col_kernel(RegQrArgs p) {
             const double ca = cas[lane];
             if (g0 > i) {
 #pragma unroll
-                for (int q = 0; q < RPT; ++q) {
-                    const double xi = __shfl_sync(0xffffffffu, x[q], i);
-                    x[q] = fma(ca, xi, x[q]);
+                for (int q = 0; q < RPT; q += 2) {
+                    const double2 xi = *reinterpret_cast<const double2*>(cw + q);
+                    x[q] = fma(ca, xi.x, x[q]);
+                    x[q + 1] = fma(ca, xi.y, x[q + 1]);
                 }
             } else {
                 const double wl = wls[lane];
                 const bool me = (lane == i);
 #pragma unroll
                 for (int q = 0; q < RPT; ++q) {
-                    const double xi = __shfl_sync(0xffffffffu, x[q], i);
+                    const double xi = cw[q];
                     const int g = g0 + q;
                     const double below = fma(ca, xi, x[q]);
                     const double atrow = me ? 1.0 - ti : x[q] - wl;
