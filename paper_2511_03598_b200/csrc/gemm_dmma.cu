@@ -500,7 +500,8 @@ int choose_splits(Ctx& c, i64 tiles, int total_kt, int ctas_per_sm = 2) {
 }
 
 void run_gemm(Ctx& c, bool AT, int KM, int BK, GemmArgs& a, bool va2, bool vb2, int splits, double* C, i64 ldc,
-              double alpha, double beta, double* Ct, i64 ldct, bool skinny = false, i64 sCt = 0, bool medium = false) {
+              double alpha, double beta, double* Ct, i64 ldct, bool skinny = false, i64 sCt = 0, bool medium = false,
+              bool narrow_n = false) {
     const bool small = a.batch > 1 && !skinny;
     const int total_kt = (a.K + BK - 1) / BK;
     splits = std::max(1, std::min(splits, total_kt));
@@ -525,6 +526,8 @@ void run_gemm(Ctx& c, bool AT, int KM, int BK, GemmArgs& a, bool va2, bool vb2, 
         else if ((medium || short_k) && KM == 0 && short_k)
             done = AT ? launch_tma<64, 64, true, 0, 2>(c, a, splits) : launch_tma<64, 64, false, 0, 2>(c, a, splits);
         else if (medium && KM == 0) done = AT ? launch_tma<64, 64, true, 0>(c, a, splits) : launch_tma<64, 64, false, 0>(c, a, splits);
+        // N <= 32 (the adaptive growth blocks, b_inc = 16): 32-column tiles
+        else if (KM == 0 && !AT && narrow_n) done = launch_tma<128, 32, false, 0>(c, a, splits);
         else if (KM == 0) done = AT ? launch_tma<128, 64, true, 0>(c, a, splits) : launch_tma<128, 64, false, 0>(c, a, splits);
         // narrow KRP products (adaptive appends, N <= 32): 32-column tiles; the
         // per-column summation order is the same as with 64 (append == one-shot)
@@ -613,14 +616,16 @@ void gemm(Ctx& c, bool trans_a, i64 M, i64 N, i64 K, double alpha, const double*
     const i64 pad128 = (M + kBM - 1) / kBM * kBM, pad64 = (M + kMdBM - 1) / kMdBM * kMdBM;
     const bool medium = !skinny && pad128 * 20 > pad64 * 21;
     const bool tma_tiles = tma_enabled() && aligned16(A) && (lda % 2 == 0) && aligned16(B) && (ldb % 2 == 0);
+    const bool narrow_n = tma_tiles && !skinny && !medium && !trans_a && N <= 32 && K > 64 && narrow_tiles();
     const i64 bm = skinny ? kSkBM : ((medium || (tma_tiles && K <= 64)) ? kMdBM : kBM);
-    const i64 bn = skinny ? (tma_tiles ? 64 : kSkBN) : ((medium || (tma_tiles && K <= 64)) ? kMdBN : kBN);
+    const i64 bn = skinny ? (tma_tiles ? 64 : kSkBN)
+                          : ((medium || (tma_tiles && K <= 64)) ? kMdBN : (narrow_n ? 32 : kBN));
     const i64 tiles = ((M + bm - 1) / bm) * ((N + bn - 1) / bn);
     const int total_kt = static_cast<int>((K + 15) / 16);
     // resident CTAs per SM grow as the tile (warp count) shrinks
     const int per_sm = (bm * bn >= 128 * 64) ? 2 : (bm * bn >= 64 * 64 ? 4 : 8);
     const int splits = choose_splits(c, tiles, total_kt, tma_tiles ? per_sm : 2);
-    run_gemm(c, trans_a, 0, 16, a, va2, vb2, splits, C, ldc, alpha, beta, nullptr, 0, skinny, 0, medium);
+    run_gemm(c, trans_a, 0, 16, a, va2, vb2, splits, C, ldc, alpha, beta, nullptr, 0, skinny, 0, medium, narrow_n);
 }
 
 void krp_step(Ctx& c, i64 r_left, i64 n, i64 r_right, i64 N, const double* X, const double* Omega, i64 ldo,
