@@ -102,6 +102,9 @@ std::unique_ptr<TTDev> round_adaptive_krp(Ctx& c, const TTDev& t, const Adaptive
 // round_rand.cpp:66-78 — Rand-Orth with a Gaussian TT sketch (reference xoshiro stream for R)
 std::unique_ptr<TTDev> round_rand_orth_tt(Ctx& c, const TTDev& t, const std::vector<i64>& target_ranks,
                                           std::uint64_t seed, int rng_mode);
+// adaptive growth step: Qb(:, q:q+grow) = orthonormal basis of the projected
+// sketch block Sb (rows x grow, ld rows); Qn/P scratch (tt_round.cu)
+void growth_basis(Ctx& c, i64 rows, i64 q, i64 grow, double* Qb, double* Sb, double* Qn, double* P);
 // sum_round.cpp:52-173 — adaptive rounding of sum(terms) without the formal sum (tt_sum.cu)
 std::unique_ptr<TTDev> round_sum_adaptive_krp(Ctx& c, const std::vector<const TTDev*>& terms, double eps, double f_inc,
                                               std::uint64_t seed, int rng_mode);

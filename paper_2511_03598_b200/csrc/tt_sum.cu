@@ -176,10 +176,7 @@ std::unique_ptr<TTDev> round_sum_adaptive_krp(Ctx& c, const std::vector<const TT
             const double est = frob_norm(c, rows, b_inc, Sb.p, rows) / std::sqrt(static_cast<double>(b_inc));
             if (est <= tau) break;
             const i64 grow = std::min(b_inc, rbar - q);
-            thin_qr(c, rows, grow, Sb.p, rows, Qn.p, rows, nullptr, 1);
-            gemm(c, true, q, grow, rows, 1.0, Qb.p, rows, Qn.p, rows, 0.0, P.p, q);
-            gemm(c, false, rows, grow, q, -1.0, Qb.p, rows, P.p, q, 1.0, Qn.p, rows);
-            thin_qr(c, rows, grow, Qn.p, rows, Qb.p + q * rows, rows, nullptr, 1);
+            growth_basis(c, rows, q, grow, Qb.p, Sb.p, Qn.p, P.p);
             gemm(c, true, grow, vcols, rows, 1.0, Qb.p + q * rows, rows, v, rows, 0.0, Mb.p + q, ldm);  // M rows [q, q+grow)
             q += grow;
         }
