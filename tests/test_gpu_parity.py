@@ -37,7 +37,8 @@ def test_gemm_matches_numpy(P, m, n, k, ta):
 
 
 @pytest.mark.parametrize("m,n", [(6, 3), (64, 64), (320, 20), (300, 15), (7040, 110), (2000, 70), (40, 60),
-                                 (80000, 8), (160000, 40)])  # the last two exceed one panel grid: TSQR split
+                                 (80000, 8), (160000, 40),  # these two exceed one panel grid: TSQR split
+                                 (40960, 32), (5000, 20), (2049, 33), (4097, 5), (40960, 320), (9000, 45)])
 def test_thin_qr(P, m, n):
     rng = np.random.default_rng(m + 13 * n)
     a = rng.standard_normal((m, n))
@@ -49,7 +50,8 @@ def test_thin_qr(P, m, n):
     assert np.allclose(np.tril(r, -1), 0.0)
 
 
-@pytest.mark.parametrize("m,n,rank", [(320, 60, 16), (5000, 96, 40), (50, 20, 0)])
+@pytest.mark.parametrize("m,n,rank", [(320, 60, 16), (5000, 96, 40), (50, 20, 0), (40960, 32, 10), (9000, 70, 0),
+                                      (7040, 110, 64), (3000, 20, 19)])
 def test_thin_qr_rank_deficient_is_orthonormal(P, m, n, rank):
     """linalg.hpp:22 — Q is orthonormal even for rank-deficient input."""
     rng = np.random.default_rng(5)
@@ -58,6 +60,19 @@ def test_thin_qr_rank_deficient_is_orthonormal(P, m, n, rank):
     assert np.all(np.isfinite(q))
     assert np.linalg.norm(q.T @ q - np.eye(n)) <= 1e-10
     assert np.linalg.norm(q @ r - a) <= 1e-12 * max(1.0, np.linalg.norm(a))
+
+
+@pytest.mark.parametrize("m,n", [(40960, 64), (7040, 110), (4000, 20)])
+def test_thin_qr_graded_columns(P, m, n):
+    """Sketch-like conditioning (singular values 1 .. 1e-12): Q stays orthonormal
+    to working precision and A = QR holds (tall panels take the TSQR route)."""
+    rng = np.random.default_rng(m + n)
+    u, _ = np.linalg.qr(rng.standard_normal((m, n)))
+    v, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    a = (u * np.logspace(0, -12, n)) @ v.T
+    q, r = P.thin_qr(a)
+    assert np.linalg.norm(q.T @ q - np.eye(n)) <= 1e-12 * np.sqrt(n)
+    assert np.linalg.norm(q @ r - a) <= 1e-13 * np.sqrt(m * n) * np.linalg.norm(a)
 
 
 # ---- K1: Philox factors are bit-identical on host and device ---------------------
@@ -608,3 +623,61 @@ def test_full_size_fixed_rank_properties(P, cfg):
     plan.execute()
     assert np.array_equal(plan.output.flat(), out.flat())
     plan.close()
+
+
+# ---- BASELINE full sizes: oracle parity ----------------------------------------------------------
+
+def _dev_to_oracle(O, y):
+    n, r, _ = y.shape()
+    return O.TT.from_flat(len(n), n, r, y.flat())
+
+
+@pytest.mark.parametrize("cfg", ["2", "3", "4", "5b-d4"])
+def test_full_size_config_oracle_parity(P, O, cfg):
+    """North-star gate at the FULL BASELINE sizes of configs 2 (adaptive, 143 MB),
+    3 (fixed, 2.3 GB) and 4 (adaptive, 1.6 GB), and config 5b at full mode size and
+    ranks (n=128, rank 300 + 1e-8 rank 700, l=320) on a d=4 slice (two full
+    1000 x 128 x 1000 middle cores; the full d=20 oracle run is ~4 TF on the host,
+    the full 5b size is covered by test_full_size_fixed_rank_properties): the device input is downloaded into
+    the oracle, both sides draw the same Philox factors, adaptive runs must select
+    identical rank vectors and ||Y_gpu - Y_ref|| / ||Y_ref|| <= 1e-10 (TT arithmetic)."""
+    ctx = P.Context(0)
+    if cfg == "2":
+        y = P.TTTensor.two_part_philox(16, 32, 30, 170, 1e-6, 1002, ctx)
+        kw = dict(tolerance=1e-4, f_init=0.1, f_inc=0.05, seed=7)
+    elif cfg == "3":
+        y = P.TTTensor.two_part_philox(30, 64, 100, 300, 1e-8, 1003, ctx)
+    elif cfg == "5b-d4":
+        y = P.TTTensor.two_part_philox(4, 128, 300, 700, 1e-8, 1005, ctx)
+    else:
+        y = P.TTTensor.kernel_sum(12, 128, 20, 20, 0.3, 1004, ctx)
+        kw = dict(tolerance=1e-6, f_init=0.1, f_inc=0.04, seed=7)
+    x = _dev_to_oracle(O, y)
+    if cfg in ("3", "5b-d4"):
+        tr = [110] * 29 if cfg == "3" else [320] * 3
+        y_gpu = P.round_fixed_krp(y, tr, 7)
+        y_ref = O.round_fixed_krp(x, tr, 7, rng=O.PHILOX)
+    else:
+        y_gpu = P.round_adaptive_krp(y, P.AdaptiveConfig(**kw))
+        y_ref = O.round_adaptive_krp(x, rng=O.PHILOX, **kw)
+    del y, x
+    assert y_gpu.ranks() == y_ref.ranks
+    assert O.relative_error(y_ref, _dev_to_oracle(O, y_gpu)) <= 1e-10
+
+
+def test_full_batch_config5a_sampled_oracle_parity(P, O):
+    """Config 5a at its full size (4096 tensors, 12.9 GB, generated on the device):
+    sampled tensors of the batched result equal the oracle's round_fixed_krp of the
+    same (downloaded) input with the per-tensor seed derive_seed(7, b)."""
+    from paper_2511_03598_b200.seeds import derive_seed
+    ctx = P.Context(0)
+    batch = P.TTBatch.two_part_philox(4096, 8, 16, 16, 48, 1e-6, derive_seed(1005, 1000), ctx)
+    out = P.round_fixed_krp_batched(batch, [20] * 7, 7)
+    _, n, r, _ = batch.shape()
+    _, on, orr, _ = out.shape()
+    assert orr == [1, 16, 20, 20, 20, 20, 20, 20, 1]
+    for b in (0, 1, 2047, 4095):
+        x = O.TT.from_flat(len(n), n, r, batch.flats(b, 1)[0])
+        y_ref = O.round_fixed_krp(x, [20] * 7, O.derive_seed(7, b), rng=O.PHILOX)
+        assert y_ref.ranks == orr
+        assert O.relative_error(y_ref, O.TT.from_flat(len(on), on, orr, out.flats(b, 1)[0])) <= 1e-10
