@@ -27,8 +27,8 @@ __device__ __forceinline__ double colreg_stage(const double (&x)[C][RT], int cj,
     return warp_sum(s);
 }
 
-// Register-resident column owners (dispatched for m <= 32*RT, n <= 8*C): warp w
-// owns columns l = w + 8c (c < C) and lane holds rows lane + 32t (t < RT) of
+// Register-resident column owners (dispatched for m <= 32*RT, n <= NW*C): warp w
+// owns columns l = w + NW*c (c < C) and lane holds rows lane + 32t (t < RT) of
 // them in registers, so the only shared-memory traffic per step is the active
 // column (staged once by its owner, double-buffered) — the smem-resident
 // kernels above are bound by shared-memory bandwidth (5 accesses per 2 fma).
@@ -36,11 +36,10 @@ __device__ __forceinline__ double colreg_stage(const double (&x)[C][RT], int cj,
 // warp loads the staged column once (masked to rows > j), dots its columns
 // with it (warp sums) and updates them. n <= 32, so rows <= j all sit in the
 // first chunk (lane <= j) and only the staged copy of that chunk is masked.
-template <int RT, int C>
-__global__ void __launch_bounds__(256, 2) qr_small_colreg_kernel(int m, int n, const double* __restrict__ A, i64 lda,
+template <int RT, int C, int NW = 8>
+__global__ void __launch_bounds__(NW * 32, 16 / NW) qr_small_colreg_kernel(int m, int n, const double* __restrict__ A, i64 lda,
                                                                  i64 sA, double* Q, i64 ldq, i64 sQ, double* R,
                                                                  i64 ldr, i64 sR) {
-    constexpr int NW = 8;
     extern __shared__ double sm[];
     double* colb = sm;                 // [2][32*RT] active column
     double* tl = colb + 2 * 32 * RT;   // [2][3] beta, inv, tau of the active reflector

@@ -387,7 +387,7 @@ def test_batched_fixed_krp_config5a_parity(P, O):
 
 
 @pytest.mark.parametrize("d,n,r1,r2,l", [(4, 8, 3, 5, 6), (4, 16, 8, 16, 12), (5, 12, 10, 20, 28),
-                                          (4, 40, 4, 8, 30)])
+                                          (4, 40, 4, 8, 30), (5, 16, 10, 20, 18), (4, 16, 12, 36, 17)])
 def test_batched_shapes_parity(P, O, d, n, r1, r2, l):
     """Batched QR dispatch (register column owners: 1..4 columns per warp, 1..12 row
     chunks; > 512 rows: the shared-memory kernel) against the oracle, rank-deficient
