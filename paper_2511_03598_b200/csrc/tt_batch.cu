@@ -6,12 +6,57 @@
 // as round_fixed_krp(Y_b, targets, derive_seed(seed, b)) in Philox mode.
 #include <algorithm>
 #include <cmath>
+#include <cstdint>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "rng_host.h"
 #include "tt_round.h"
 
 namespace ttr {
+namespace {
+#include "lr_batch.cuh"
+
+// Fused H(Y) = M H(X) + S_next = V(Y) W (lr_batch.cuh) when the shapes fit one
+// CTA per tensor; false = caller takes the two-GEMM path.
+bool lr_fused_batched(Ctx& c, const lrb::LrArgs& a, i64 batch) {
+    if (a.l > 32 || a.l2 > 32 || a.cols > 64 || a.rr > 64 || (a.cols & 1) || a.l < 1 || a.l2 < 1) return false;
+    if ((reinterpret_cast<std::uintptr_t>(a.X) & 15) || (a.sX & 1)) return false;
+    static const bool off = [] {
+        const char* e = std::getenv("TTR_LR_FUSED");  // experiments: 0 = two GEMMs
+        return e && e[0] == '0';
+    }();
+    if (off) return false;
+    const int lt = (a.l + 7) / 8, lt2 = (a.l2 + 7) / 8;
+    bool done = false;
+    auto go = [&](auto t1, auto t2) {
+        constexpr int LT = decltype(t1)::value, LT2 = decltype(t2)::value;
+        if (done || lt != LT || lt2 != LT2) return;
+        auto kern = lrb::lr_fused_kernel<LT, LT2>;
+        constexpr std::size_t smem = lrb::LrSmem<LT>::kBytes;
+        static bool configured = false;
+        if (!configured) {
+            TTR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+            configured = true;
+        }
+        kern<<<static_cast<unsigned>(batch), lrb::kThreads, smem, c.stream>>>(a);
+        TTR_CUDA(cudaGetLastError());
+        c.launched();
+        done = true;
+    };
+    auto row = [&](auto t1) {
+        go(t1, std::integral_constant<int, 1>{});
+        go(t1, std::integral_constant<int, 2>{});
+        go(t1, std::integral_constant<int, 3>{});
+        go(t1, std::integral_constant<int, 4>{});
+    };
+    row(std::integral_constant<int, 1>{});
+    row(std::integral_constant<int, 2>{});
+    row(std::integral_constant<int, 3>{});
+    row(std::integral_constant<int, 4>{});
+    return done;
+}
+}  // namespace
 
 TTBatch::TTBatch(Ctx& c, i64 batch_, const std::vector<i64>& n_, const std::vector<i64>& r_)
     : ctx(&c), n(n_), r(r_), batch(batch_) {
@@ -118,9 +163,10 @@ std::unique_ptr<TTBatch> round_fixed_krp_batched(Ctx& c, const TTBatch& t, const
     DBuf M(c, static_cast<std::size_t>(width * t.max_rank() * B));
     const double* v = t.core(0, 0);
     i64 sv = t.stride;
+    bool s_ready = false;  // S of this step already formed by the previous fused step
     for (i64 k = 1; k < d; ++k) {
         const i64 rows = r[k - 1] * t.n[k - 1], cols = t.r[k], l = r[k];
-        {
+        if (!s_ready) {
             PhaseScope ph(c, kPhaseGemm);
             gemm_batched(c, false, rows, l, cols, 1.0, v, rows, sv, W[k + 1].p, ldw[k + 1], sw[k + 1], 0.0, S.p, rows,
                          rows * l, B);
@@ -144,8 +190,35 @@ std::unique_ptr<TTBatch> round_fixed_krp_batched(Ctx& c, const TTBatch& t, const
             PhaseScope ph(c, kPhaseGemm);
             gemm_batched(c, true, l, cols, rows, 1.0, out->core(0, k - 1), rows, out->stride, v, rows, sv, 0.0, M.p, l,
                          l * cols, B);
-            gemm_batched(c, false, l, ncols, cols, 1.0, M.p, l, l * cols, t.core(0, k), cols, t.stride, 0.0, dst, l, sdst,
-                         B);
+            s_ready = false;
+            if (k < d - 1) {
+                // next step's sketch S = V(Y_{k+1}) W_{k+2} fused with Y_{k+1} = M H(X_{k+1})
+                lrb::LrArgs a{};
+                a.l = static_cast<int>(l);
+                a.cols = static_cast<int>(cols);
+                a.n = static_cast<int>(t.n[k]);
+                a.rr = static_cast<int>(t.r[k + 1]);
+                a.l2 = static_cast<int>(r[k + 1]);
+                a.M = M.p;
+                a.sM = l * cols;
+                a.X = t.core(0, k);
+                a.sX = t.stride;
+                a.W = W[k + 2].p;
+                a.ldw = ldw[k + 2];
+                a.sW = sw[k + 2];
+                a.Y = dst;
+                a.sY = sdst;
+                a.S = S.p;
+                a.sS = l * t.n[k] * r[k + 1];
+                s_ready = lr_fused_batched(c, a, B);
+                if (s_ready) {
+                    c.charge_gemm(2ULL * static_cast<std::uint64_t>(l) * ncols * cols * B);
+                    c.charge_gemm(2ULL * static_cast<std::uint64_t>(l * t.n[k]) * r[k + 1] * t.r[k + 1] * B);
+                }
+            }
+            if (!s_ready)
+                gemm_batched(c, false, l, ncols, cols, 1.0, M.p, l, l * cols, t.core(0, k), cols, t.stride, 0.0, dst, l,
+                             sdst, B);
         }
         v = dst;
         sv = sdst;
