@@ -157,7 +157,8 @@ inline i64 even_ld(i64 rows) { return rows < 1 ? 2 : round_up(rows, 2); }
 // C = alpha * op(A) * B + beta * C, fp64 on the DMMA tensor pipe.
 // op(A) = A (M x K, lda) or A^T (A stored K x M, lda). B is K x N (ldb).
 void gemm(Ctx& c, bool trans_a, i64 M, i64 N, i64 K, double alpha, const double* A, i64 lda,
-          const double* B, i64 ldb, double beta, double* C, i64 ldc, bool count = true);
+          const double* B, i64 ldb, double beta, double* C, i64 ldc, bool count = true,
+          bool upper_tiles = false /* only output tiles touching the upper triangle (Gram matrices) */);
 // KRP sketch step (sketch.cpp:15-40 restated as one GEMM):
 //   W_out(:, c) = sum_{g, j} H(X)(:, g*n + j) * Omega(j, c) * Wt(c, g)
 // X is the r_left x n x r_right core (H unfolding, ld = r_left), Omega is

@@ -48,6 +48,9 @@ struct GemmArgs {
     // strided batch (blockIdx.z = batch index; no split-K when batch > 1)
     int batch;
     i64 sA, sB, sC, sW;
+    // TMA kernels: skip output tiles strictly below the diagonal (their C is
+    // left unspecified; Gram matrices whose consumer reads the upper triangle)
+    int upper;
 };
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
@@ -590,7 +593,7 @@ void run_gemm(Ctx& c, bool AT, int KM, int BK, GemmArgs& a, bool va2, bool vb2, 
 }  // namespace
 
 void gemm(Ctx& c, bool trans_a, i64 M, i64 N, i64 K, double alpha, const double* A, i64 lda, const double* B,
-          i64 ldb, double beta, double* C, i64 ldc, bool count) {
+          i64 ldb, double beta, double* C, i64 ldc, bool count, bool upper_tiles) {
     if (M <= 0 || N <= 0) return;
     if (count) c.charge_gemm(2ULL * static_cast<std::uint64_t>(M) * N * K);
     if (K <= 0) {
@@ -609,6 +612,7 @@ void gemm(Ctx& c, bool trans_a, i64 M, i64 N, i64 K, double alpha, const double*
     a.lda = lda;
     a.B = B;
     a.ldb = ldb;
+    a.upper = upper_tiles ? 1 : 0;
     const bool va2 = aligned16(A) && (lda % 2 == 0);
     const bool vb2 = aligned16(B) && (ldb % 2 == 0);
     const bool skinny = M <= kSkBM;

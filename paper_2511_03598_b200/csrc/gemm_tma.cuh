@@ -110,6 +110,7 @@ __global__ void __launch_bounds__((BM / 32) * (BN / 32) * 32)
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int wm0 = (warp % C_::kWarpsM) * 32, wn0 = (warp / C_::kWarpsM) * 32;
     const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
+    if (p.upper && m0 >= n0 + BN) return;  // tile strictly below the diagonal: not needed
     const int zsplit = static_cast<int>(blockIdx.z);
     const int total_kt = (p.K + BK - 1) / BK;
     const int kt_begin = zsplit * p.ktiles_per_split;

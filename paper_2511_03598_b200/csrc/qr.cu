@@ -567,7 +567,8 @@ void thin_qr(Ctx& c, i64 m, i64 n, const double* A, i64 lda, double* Q, i64 ldq,
         DBuf Tf(c, static_cast<std::size_t>(k * k));
         DBuf V1t(c, static_cast<std::size_t>(k * k));
         DBuf Y(c, static_cast<std::size_t>(k * k));
-        gemm(c, true, k, k, m, 1.0, Vall.p, ldw, Vall.p, ldw, 0.0, Gm.p, k, false);  // G = V^T V
+        // G = V^T V; t_aggregate_kernel reads only its strictly upper 32-blocks
+        gemm(c, true, k, k, m, 1.0, Vall.p, ldw, Vall.p, ldw, 0.0, Gm.p, k, false, true);
         const std::size_t smem = (static_cast<std::size_t>(npanels) * 32 * 32 + (npanels - 1) * 32 * 33) * sizeof(double);
         static bool configured = false;
         if (!configured) {
