@@ -31,6 +31,7 @@ from __future__ import annotations
 import argparse
 import ctypes as C
 import json
+import math
 import os
 import statistics
 import subprocess
@@ -55,7 +56,9 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="5b", choices=["5b", "3", "5a"])
+    ap.add_argument("--config", default="5b", choices=["5b", "1", "2", "3", "4", "5a"],
+                    help="BASELINE config: 5b (default, the headline), 1 and 3 (fixed rank), 2 and 4 "
+                         "(adaptive rank), 5a (batch of 4096 tensors)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--sharding", default="tensors", choices=["tensors", "columns", "rows"],
@@ -195,6 +198,8 @@ def run_ours(args, world, rank, local):
     cfg = dict(CFG5B)
     if args.config == "3":
         cfg.update(d=30, n=64, rx=100, rz=300, eps=1e-8, ell=110, seed=1003)
+    elif args.config == "1":
+        cfg.update(d=10, n=20, rx=10, rz=40, eps=1e-4, ell=15, seed=1001)
     cfg["seed"] = cfg["seed"] + 1000 * rank  # independent tensor per rank
     y = build_input(P, ctx, cfg)
     ranks = [cfg["ell"]] * (cfg["d"] - 1)
@@ -320,10 +325,14 @@ def run_ours(args, world, rank, local):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        res = cpu_sample(1)
-        sec, fl = res[0]
-        cpu = {"value": fl / sec / 1e12, "unit": "TFLOP/s", "cores": cpu_threads(), "kind": "port",
-               "sample": sample_desc(), "seconds": sec}
+        if args.config in ("1", "3"):
+            # the oracle on the full config (seconds on the host cores)
+            cpu = cpu_full_fixed(P, y, ranks, seed)
+        else:
+            res = cpu_sample(1)
+            sec, fl = res[0]
+            cpu = {"value": fl / sec / 1e12, "unit": "TFLOP/s", "cores": cpu_threads(), "kind": "port",
+                   "sample": sample_desc(), "seconds": sec}
 
     if rank == 0:
         line = {
@@ -336,11 +345,13 @@ def run_ours(args, world, rank, local):
                        "flops_per_step": flops, "sketch_flops_per_step": sketch_flops,
                        "api": "FixedKrpPlan (CUDA graph of round_fixed_krp) replayed per step",
                        "eager_ms_per_step": eager_ms,
-                       "l2": "inputs exceed L2 (18 GB vs 126 MB)" if args.config == "5b" else "inputs exceed L2",
+                       "l2": {"5b": "inputs exceed L2 (18 GB vs 126 MB)", "3": "inputs exceed L2 (2.3 GB)",
+                              "1": "3.2 MB input is L2-resident (a step re-reads cores from L2; config 1 is "
+                                   "launch/latency bound)"}[args.config],
                        "parallelism": f"{world} independent tensors (batch sharding)"},
             "tflops_fp64": value, "fraction_of_fp64_peak": value / world / FP64_PEAK_TFLOPS,
             "phase_ms": {"sketch": phase_ms[0], "qr": phase_ms[1], "lr_gemm": phase_ms[2], "other": phase_ms[3]},
-            "roofline": roofline_entry(achieved, cfg),
+            "roofline": roofline_entry(achieved, cfg, sketch_ms / (cfg["d"] - 1) if sketch_ms > 0 else None),
             "clocks": clk.summary(),
             "gpu_launches": launches,
             "gpu_launches_per_step": launches_per_step,
@@ -355,18 +366,32 @@ def run_ours(args, world, rank, local):
 SKETCH_NCU = os.path.join(ROOT, "profiles", "r01_ncu_sketch_tma.json")
 
 
-def roofline_entry(achieved, cfg):
-    """Sketch-kernel roofline: achieved = algorithmic flops of the 19 krp_step launches
+HBM_PEAK_GBS = 6534.5  # MEASURED_PEAKS.json (copy bandwidth of this pool's B200)
+RIDGE = FP64_PEAK_TFLOPS * 1e12 / (HBM_PEAK_GBS * 1e9)  # flop/B
+
+
+def roofline_entry(achieved, cfg, ms_per_launch=None):
+    """Sketch-kernel roofline: achieved = algorithmic flops of the d-1 krp_step launches
     / their CUDA-event time; traffic = DRAM bytes (read + write) of ONE middle-core
-    launch from the committed `ncu --set full` capture at the same shape."""
+    launch from the committed `ncu --set full` capture at the same shape. The sketch's
+    arithmetic intensity is l/4 flop/B: below the ridge (config 1, l = 15) the bound is
+    HBM and `achieved` is the algorithmic bytes (every core read once) per launch time."""
     r = cfg["rx"] + cfg["rz"]
+    abytes = 8 * (r * cfg["n"] * r + r * cfg["ell"] + cfg["n"] * cfg["ell"] + r * cfg["ell"])
+    if cfg["ell"] / 4 < RIDGE and ms_per_launch:
+        gbs = abytes / (ms_per_launch * 1e-3) / 1e9
+        return {"bound": "hbm", "achieved": gbs, "peak": HBM_PEAK_GBS, "unit": "GB/s", "frac": gbs / HBM_PEAK_GBS,
+                "traffic": None, "kernel": "krp_step (KRP sketch contraction, cp.async DMMA kernel)",
+                "peak_source": "MEASURED_PEAKS.json HBM copy bandwidth",
+                "algorithmic_bytes_per_launch": abytes,
+                "note": "average over the d-1 sketch launches (phase time incl. their split-K reduce / transpose "
+                        "launches); at config 1's size (0.4 MB per core) every launch is latency-bound"}
     entry = {"bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
              "frac": (achieved / FP64_PEAK_TFLOPS) if achieved else None, "traffic": None,
              "kernel": "krp_step: dgemm_tma_kernel<128,64,KM=1> (TMA + mbarrier pipeline, fp64 DMMA) + "
                        "splitk_reduce_wide",
              "peak_source": PEAK_SOURCE,
-             "algorithmic_bytes_per_launch": 8 * (r * cfg["n"] * r + r * cfg["ell"] + cfg["n"] * cfg["ell"] +
-                                                  r * cfg["ell"])}
+             "algorithmic_bytes_per_launch": abytes}
     if (cfg["n"], r, cfg["ell"]) != (128, 1000, 320):
         return entry  # the committed capture is at the 5b shape only
     try:
@@ -384,6 +409,174 @@ def roofline_entry(achieved, cfg):
 
 def total_bytes(y):
     return 8 * y.shape()[2]
+
+
+def _oracle():
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import py_oracle as O
+    return O
+
+
+def cpu_full_fixed(P, y, ranks, seed):
+    """The CPU oracle (reference restatement, all host threads) on the FULL config input."""
+    O = _oracle()
+    n, r, _ = y.shape()
+    x = O.TT.from_flat(len(n), n, r, y.flat())
+    sec = C.c_double()
+    fl = C.c_uint64()
+    O._check(O.lib().ttro_time_round_fixed_krp(x._h, O._i64(ranks), C.c_int64(len(ranks)), C.c_uint64(seed),
+                                               C.c_int(O.PHILOX), C.byref(sec), C.byref(fl)))
+    return {"value": fl.value / sec.value / 1e12, "unit": "TFLOP/s", "cores": cpu_threads(), "kind": "port",
+            "sample": "the full config: round_fixed_krp on the same input, CPU oracle, wall clock around the call",
+            "seconds": sec.value, "ms_per_round": sec.value * 1e3}
+
+
+ADAPTIVE = {
+    "2": dict(d=16, n=32, rx=30, rz=170, eps=1e-6, seed=1002, tol=1e-4, f_init=0.1, f_inc=0.05,
+              desc="config 2 adaptive KRP rounding round_adaptive_krp(Y, {tol 1e-4, f_init 0.1, f_inc 0.05, seed 7}); "
+                   "Y = X/|X| + 1e-6 Z/|Z|, d=16, n=32, ranks 30 + 170"),
+    "4": dict(d=12, n=128, terms=20, r=20, ell_k=0.3, seed=1004, tol=1e-6, f_init=0.1, f_inc=0.04,
+              desc="config 4 adaptive KRP rounding round_adaptive_krp(Y, {tol 1e-6, f_init 0.1, f_inc 0.04, seed 7}); "
+                   "Y = sum of 20 rank-20 exp(-|t-c|/0.3) TTs weighted 2^-i, d=12, n=128"),
+}
+
+
+def run_adaptive(args, world, rank, local):
+    """Configs 2 and 4: adaptive-rank KRP rounding (host-driven growth decisions, eager API).
+    One step = one round_adaptive_krp; independent tensor per rank (weak scaling)."""
+    import torch
+    import paper_2511_03598_b200 as P
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    torch.cuda.set_device(local)
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    ctx = P.Context(local, stream.cuda_stream)
+    a = ADAPTIVE[args.config]
+    if args.config == "2":
+        y = P.TTTensor.two_part_philox(a["d"], a["n"], a["rx"], a["rz"], a["eps"], a["seed"] + 1000 * rank, ctx)
+    else:
+        y = P.TTTensor.kernel_sum(a["d"], a["n"], a["r"], a["terms"], a["ell_k"], a["seed"] + 1000 * rank, ctx)
+    cfgA = P.AdaptiveConfig(tolerance=a["tol"], f_init=a["f_init"], f_inc=a["f_inc"], seed=7)
+    ctx.reset_counters()
+    l0 = ctx.kernel_launches()
+    out = P.round_adaptive_krp(y, cfgA)
+    torch.cuda.synchronize()
+    flops = ctx.counters().total()
+    launches_per_step = ctx.kernel_launches() - l0
+    out_ranks = out.ranks()
+    del out
+    for _ in range(args.warmup):
+        del_ = P.round_adaptive_krp(y, cfgA)
+        del del_
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    l0 = ctx.kernel_launches()
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            o = P.round_adaptive_krp(y, cfgA)
+            del o
+        e1.record(stream)
+        torch.cuda.synchronize()
+    launches = ctx.kernel_launches() - l0
+    ms = e0.elapsed_time(e1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+
+    # roofline: the initial KRP sketch contraction (estimate_norm_krp at the initial width:
+    # all d-1 contractions + V(X_1) W_2), CUDA events on the context stream
+    n, r, total = y.shape()
+    w = math.ceil(a["f_init"] * max(r))
+    ctx.reset_counters()
+    P.estimate_norm_krp(y, w, 7)
+    sk_flops = ctx.counters().total()
+    reps = 5
+    e0.record(stream)
+    for _ in range(reps):
+        P.estimate_norm_krp(y, w, 7)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    sk_ms = e0.elapsed_time(e1) / reps
+    sk_bytes = 8 * total  # every core read once
+    ai = sk_flops / sk_bytes
+    if ai < RIDGE:
+        gbs = sk_bytes / (sk_ms * 1e-3) / 1e9
+        roof = {"bound": "hbm", "achieved": gbs, "peak": HBM_PEAK_GBS, "unit": "GB/s", "frac": gbs / HBM_PEAK_GBS,
+                "peak_source": "MEASURED_PEAKS.json HBM copy bandwidth"}
+    else:
+        tf = sk_flops / (sk_ms * 1e-3) / 1e12
+        roof = {"bound": "tensor", "achieved": tf, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                "frac": tf / FP64_PEAK_TFLOPS, "peak_source": PEAK_SOURCE}
+    roof.update({"traffic": None, "kernel": f"initial KRP sketch (estimate_norm_krp, width {w}): d-1 krp_step launches",
+                 "algorithmic_bytes_per_launch": sk_bytes, "algorithmic_flops": sk_flops, "ms": sk_ms,
+                 "arithmetic_intensity": ai})
+
+    # e2e through the API with host buffers: pinned H2D of the cores, the rounding, D2H of the result
+    e2e = None
+    if not args.no_e2e:
+        host_in = torch.empty(total, dtype=torch.float64, pin_memory=True)
+        P.lib().ttr_tt_download(ctx._h, y._h, C.c_void_p(host_in.data_ptr()))
+        times, out_bytes = [], 0
+        for it in range(min(args.steps, 3) + 1):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            P.lib().ttr_tt_copy_from_host(ctx._h, y._h, C.c_void_p(host_in.data_ptr()))
+            o = P.round_adaptive_krp(y, cfgA)
+            _, _, ot = o.shape()
+            host_out = torch.empty(ot, dtype=torch.float64, pin_memory=True) if it == 0 else host_out
+            P.lib().ttr_tt_download(ctx._h, o._h, C.c_void_p(host_out.data_ptr()))
+            dt = time.perf_counter() - t0
+            out_bytes = 8 * ot
+            del o
+            if it > 0:
+                times.append(dt)
+        e2e_ms = sum(times) / len(times) * 1e3
+        if world > 1:
+            t = torch.tensor([e2e_ms], device="cuda")
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            e2e_ms = float(t.item())
+        e2e = {"value": flops * world / (e2e_ms * 1e-3) / 1e12, "unit": "TFLOP/s", "ms_per_step": e2e_ms,
+               "h2d_bytes_per_step": 8 * total, "d2h_bytes_per_step": out_bytes,
+               "timing": "host wall clock: pinned H2D of the cores (ttr_tt_copy_from_host) + round_adaptive_krp + "
+                         "D2H of the result (ttr_tt_download, synchronising)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        O = _oracle()
+        x = O.TT.from_flat(len(n), n, r, y.flat())
+        O.flops_reset()
+        t0 = time.perf_counter()
+        ref = O.round_adaptive_krp(x, tolerance=a["tol"], f_init=a["f_init"], f_inc=a["f_inc"], seed=7, rng=O.PHILOX)
+        sec = time.perf_counter() - t0
+        cfl = sum(v for k, v in O.flops_get().items() if k in ("gemm", "qr", "svd"))
+        cpu = {"value": cfl / sec / 1e12, "unit": "TFLOP/s", "cores": cpu_threads(), "kind": "port",
+               "sample": "the full config: round_adaptive_krp on the same input, CPU oracle, wall clock around the call",
+               "seconds": sec, "ms_per_round": sec * 1e3, "ranks_identical": ref.ranks == out_ranks}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": flops * world / (ms * 1e-3) / 1e12, "unit": "TFLOP/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (device-generated input)",
+            "config": {"workload": a["desc"], "output_ranks": out_ranks, "flops_per_step": flops,
+                       "input_gb": 8 * total / 1e9, "api": "round_adaptive_krp (eager; host-side growth decisions)",
+                       "l2": "inputs exceed L2" if 8 * total > 126e6 else "input fits L2 (126 MB); not flushed",
+                       "parallelism": f"{world} independent tensors"},
+            "roofline": roof, "clocks": clk.summary(), "gpu_launches": launches,
+            "gpu_launches_per_step": launches_per_step, "e2e": e2e, "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
 
 
 def run_columns(args, world, rank, local):
@@ -519,6 +712,96 @@ def run_5a(args, world, rank, local):
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms = float(t.item())
     flops_all = flops * world  # per-rank work is (near) equal
+
+    # roofline: the fused next-core + next-sketch kernel (lr_fused_kernel, the "other"
+    # phase of the batched sweep; d-2 launches per step), CUDA events on the stream
+    _, n_, r_in, _ = batch.shape()
+    rb = out_ranks
+    C_ = P.lib()
+    C_.ttr_ctx_enable_timing(ctx._h, 1)
+    C_.ttr_ctx_phase_times(ctx._h, None, None)
+    o = P.round_fixed_krp_batched(batch, ranks, 7)
+    del o
+    phase_ms = (C.c_double * 4)()
+    phase_n = (C.c_uint64 * 4)()
+    C_.ttr_ctx_phase_times(ctx._h, phase_ms, phase_n)
+    C_.ttr_ctx_enable_timing(ctx._h, 0)
+    d_ = len(n_)
+    fb, ff = 0, 0  # algorithmic bytes / flops of the d-2 fused launches
+    for k in range(1, d_ - 1):
+        l, cols, nk, rr, l2 = rb[k], r_in[k], n_[k], r_in[k + 1], rb[k + 1]
+        fb += 8 * nb * (cols * nk * rr + l * nk * rr + l * nk * l2 + l * cols + rr * l2)
+        ff += nb * (2 * l * nk * rr * cols + 2 * l * nk * l2 * rr)
+    fused_ms = phase_ms[3]
+    roof = None
+    if fused_ms > 0:
+        gbs = fb / (fused_ms * 1e-3) / 1e9
+        roof = {"bound": "hbm", "achieved": gbs, "peak": HBM_PEAK_GBS, "unit": "GB/s", "frac": gbs / HBM_PEAK_GBS,
+                "traffic": None, "kernel": "lr_fused_kernel<3,3> (next core M H(X) + next sketch V(Y) W, one CTA per "
+                                          "tensor, cp.async-streamed X slices, fp64 DMMA)",
+                "peak_source": "MEASURED_PEAKS.json HBM copy bandwidth",
+                "algorithmic_bytes_per_launch": fb / (d_ - 2), "launches": d_ - 2, "ms_all_launches": fused_ms,
+                "arithmetic_intensity": ff / fb, "tflops_achieved": ff / (fused_ms * 1e-3) / 1e12}
+        try:
+            with open(os.path.join(ROOT, "profiles", "r01_ncu_lr_fused.json")) as f:
+                nc = json.load(f)
+            roof["traffic"] = nc["dram_read_bytes"] + nc["dram_write_bytes"]
+            roof["traffic_source"] = "profiles/r01_ncu_lr_fused.json (ncu --set full of one middle-mode launch)"
+            roof["ncu_dmma_pipe_active_pct"] = nc.get("dmma_pipe_active_pct")
+        except (OSError, KeyError, ValueError):
+            pass
+
+    # e2e through the C ABI with host buffers: pinned H2D of the whole batch (ttr_batch_upload),
+    # the batched rounding, D2H of every rounded tensor (ttr_batch_download)
+    e2e = None
+    if not args.no_e2e:
+        tot_in = batch.shape()[3]
+        host_in = torch.empty(nb * tot_in, dtype=torch.float64, pin_memory=True)
+        C_.ttr_batch_download(ctx._h, batch._h, C.c_int64(0), C.c_int64(nb), C.c_void_p(host_in.data_ptr()))
+        host_out = None
+        times = []
+        for it in range(min(args.steps, 3) + 1):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            hb = C.c_void_p()
+            P._check(C_.ttr_batch_upload(ctx._h, C.c_int64(nb), C.c_int64(d_), P._i64(n_), P._i64(r_in),
+                                         C.c_void_p(host_in.data_ptr()), C.byref(hb)))
+            up = P.TTBatch(hb, ctx)
+            o = P.round_fixed_krp_batched(up, ranks, 7)
+            tot_out = o.shape()[3]
+            if host_out is None:
+                host_out = torch.empty(nb * tot_out, dtype=torch.float64, pin_memory=True)
+            C_.ttr_batch_download(ctx._h, o._h, C.c_int64(0), C.c_int64(nb), C.c_void_p(host_out.data_ptr()))
+            dt = time.perf_counter() - t0
+            del o, up
+            if it > 0:
+                times.append(dt)
+        e2e_ms = sum(times) / len(times) * 1e3
+        if world > 1:
+            t = torch.tensor([e2e_ms], device="cuda")
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            e2e_ms = float(t.item())
+        e2e = {"value": flops_all / (e2e_ms * 1e-3) / 1e12, "unit": "TFLOP/s", "ms_per_step": e2e_ms,
+               "h2d_bytes_per_step": 8 * nb * tot_in, "d2h_bytes_per_step": 8 * nb * tot_out,
+               "timing": "host wall clock: ttr_batch_upload (pinned H2D of all tensors) + "
+                         "ttr_round_fixed_krp_batched + ttr_batch_download (synchronising)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        O = _oracle()
+        sample = 128
+        xs = [O.TT.from_flat(d_, n_, r_in, f) for f in batch.flats(0, sample)]
+        O.flops_reset()
+        t0 = time.perf_counter()
+        for b, x in enumerate(xs):
+            O.round_fixed_krp(x, ranks, O.derive_seed(7, b), rng=O.PHILOX)
+        sec = time.perf_counter() - t0
+        fl = O.flops_get()["total"]
+        cpu = {"value": fl / sec / 1e12, "unit": "TFLOP/s", "cores": cpu_threads(), "kind": "port",
+               "sample": f"round_fixed_krp of the first {sample} tensors of the batch (same inputs and per-tensor "
+                         f"seeds), CPU oracle, wall clock around the loop", "seconds": sec,
+               "ms_per_4096_tensors_extrapolated": sec / sample * 4096 * 1e3}
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": flops_all / (ms * 1e-3) / 1e12, "unit": "TFLOP/s", "n_gpus": world,
@@ -529,7 +812,8 @@ def run_5a(args, world, rank, local):
                        "bytes_per_step": 8 * 4096 * batch.shape()[3],
                        "l2": "inputs exceed L2 (12.9 GB)"},
             "hbm_gbs_achieved": 8 * 4096 * batch.shape()[3] / (ms * 1e-3) / 1e9,
-            "clocks": clk.summary(), "gpu_launches": launches,
+            "phase_ms": {"sketch": phase_ms[0], "qr": phase_ms[1], "gemm": phase_ms[2], "fused_sweep": phase_ms[3]},
+            "roofline": roof, "clocks": clk.summary(), "gpu_launches": launches, "e2e": e2e, "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -544,6 +828,9 @@ def main():
         return
     if args.config == "5a":
         run_5a(args, world, rank, local)
+        return
+    if args.config in ADAPTIVE:
+        run_adaptive(args, world, rank, local)
         return
     if args.sharding in ("columns", "rows"):
         run_columns(args, world, rank, local)

@@ -190,8 +190,11 @@ std::unique_ptr<TTBatch> round_fixed_krp_batched(Ctx& c, const TTBatch& t, const
             PhaseScope ph(c, kPhaseGemm);
             gemm_batched(c, true, l, cols, rows, 1.0, out->core(0, k - 1), rows, out->stride, v, rows, sv, 0.0, M.p, l,
                          l * cols, B);
+        }
+        {
             s_ready = false;
             if (k < d - 1) {
+                PhaseScope ph(c, kPhaseOther);  // the fused kernel alone (bench.py roofline)
                 // next step's sketch S = V(Y_{k+1}) W_{k+2} fused with Y_{k+1} = M H(X_{k+1})
                 lrb::LrArgs a{};
                 a.l = static_cast<int>(l);
@@ -216,9 +219,11 @@ std::unique_ptr<TTBatch> round_fixed_krp_batched(Ctx& c, const TTBatch& t, const
                     c.charge_gemm(2ULL * static_cast<std::uint64_t>(l * t.n[k]) * r[k + 1] * t.r[k + 1] * B);
                 }
             }
-            if (!s_ready)
+            if (!s_ready) {
+                PhaseScope ph(c, kPhaseGemm);
                 gemm_batched(c, false, l, ncols, cols, 1.0, M.p, l, l * cols, t.core(0, k), cols, t.stride, 0.0, dst, l,
                              sdst, B);
+            }
         }
         v = dst;
         sv = sdst;
