@@ -1,3 +1,1 @@
-for c in 1 2 4 5a; do
-timeout 600 python bench.py --config $c --steps 5 --warmup 3 > gpurun_out/bench$c.json 2> gpurun_out/bench$c.err; echo "cfg $c rc=$?"; tail -2 gpurun_out/bench$c.err
-done
+TTR_CQR_TRACE=1 python tools/qr_bench.py 40960 32 2>&1 | grep -a -A6 cqr | tail -8
