@@ -51,11 +51,12 @@ def _worker(rank, world, port, result_q):
     dist.destroy_process_group()
 
 
-def test_column_sharded_sketch_gloo_world2():
+@pytest.mark.parametrize("world", [2, 3])
+def test_column_sharded_sketch_gloo(world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()
     ok = q.get(timeout=240)
@@ -200,14 +201,16 @@ def _row_worker(rank, world, port, result_q):
     dist.destroy_process_group()
 
 
-def test_row_sharded_sweep_gloo_world2():
-    """The TSQR row-sharded sweep (mode 1 replicated, modes >= 2 sharded) on 2
-    CPU ranks reproduces the oracle's round_fixed_krp to 1e-10 with identical
-    ranks, and every rank ends with the same tensor."""
+@pytest.mark.parametrize("world", [2, 3])
+def test_row_sharded_sweep_gloo(world):
+    """The TSQR row-sharded sweep (mode 1 replicated, modes >= 2 sharded) on 2 and
+    3 CPU ranks (3 does not divide n = 8: uneven slice ownership) reproduces the
+    oracle's round_fixed_krp to 1e-10 with identical ranks, and every rank ends
+    with the same tensor."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_row_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_row_worker, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()
     err, ranks_ok, same = q.get(timeout=240)
