@@ -22,6 +22,7 @@ struct Sketch {
     i64 ldwt;
     DBuf ones;
     std::vector<i64> width;   // current column count per mode
+    std::vector<i64> charged; // columns per mode the reference's appends would have made (charges)
     int rng_mode;
     std::uint64_t seed;
     XoshiroGauss xo;
@@ -35,6 +36,7 @@ struct Sketch {
         ldo.assign(d + 1, 0);
         ldw.assign(d + 1, 0);
         width.assign(d + 2, 0);
+        charged.assign(d + 2, 0);
         ldwt = even_ld(cap);
         for (i64 k = 2; k <= d; ++k) {
             ldo[k] = even_ld(t.n[k - 1]);
@@ -81,6 +83,40 @@ struct Sketch {
             krp_step(c, rl, nk, rr, extra, t.core(k - 1), omega[k].p + col0 * ldo[k], ldo[k], k == d ? ones.p : wt_next,
                      ld_next, W[k].p + col0 * ldw[k], ldw[k], wt_out, ldwt, k == d);
             width[k] = col0 + extra;
+            charged[k] = width[k];
+        }
+    }
+
+    // Make W_start..W_d hold at least `target` columns (the adaptive residual
+    // sketch, round_rand.cpp:88-91: the reference appends exactly the missing
+    // columns). With the counter-based Philox factors a column does not depend
+    // on when or with which others it is contracted (bitwise: append ==
+    // one-shot), so the device appends at least `chunk` columns at a time —
+    // fewer passes over the cores — while the counters are charged exactly as
+    // the reference's appends would be, when the columns are first used.
+    void ensure(i64 start, i64 target, i64 chunk) {
+        const i64 d = t.d();
+        if (rng_mode != TTR_RNG_PHILOX) {
+            if (width[start] < target) append(start, target - width[start]);
+            return;
+        }
+        if (width[start] < target) {
+            const i64 extra = std::min(std::max(target - width[start], chunk), cap - width[d]);
+            const Counts saved = c.counts;
+            const std::vector<i64> keep = charged;
+            append(start, std::max(extra, target - width[start]));
+            c.counts = saved;  // charged below, as the reference would
+            charged = keep;
+        }
+        for (i64 k = start; k <= d; ++k) {
+            if (charged[k] >= target) continue;
+            const i64 cols = target - charged[k];
+            const std::uint64_t rl = t.r[k - 1], nk = t.n[k - 1], rr = t.r[k];
+            c.counts.rng += nk * static_cast<std::uint64_t>(cols);
+            const std::uint64_t f = (k == d) ? 2ULL * rl * nk * cols : cols * (2ULL * rr * rl * nk + 2ULL * rl * rr);
+            c.counts.gemm += f;
+            c.counts.sketch += f;
+            charged[k] = target;
         }
     }
 };

@@ -4,6 +4,7 @@
 // context's stream; the host only sequences launches and, in the adaptive
 // loop, reads back the one scalar that drives each stopping decision.
 #include <algorithm>
+#include <cstdlib>
 #include <array>
 #include <cmath>
 #include <cstring>
@@ -607,6 +608,15 @@ void growth_basis(Ctx& c, i64 rows, i64 q, i64 grow, double* Qb, double* Sb, dou
     thin_qr(c, rows, grow, Qn, rows, Qb + q * rows, rows, nullptr, 1);
 }
 
+// columns per device append of the adaptive residual sketch (Sketch::ensure)
+static i64 adapt_chunk(i64 b_inc_max) {
+    static const double mult = [] {
+        const char* e = std::getenv("TTR_ADAPT_CHUNK");  // experiments: multiple of the largest b_inc, 0 = exact
+        return e ? std::atof(e) : 4.0;
+    }();
+    return static_cast<i64>(mult * static_cast<double>(b_inc_max));
+}
+
 static i64 ceil_fraction(double f, i64 n) {  // round_rand.cpp:46-48
     return std::max<i64>(1, static_cast<i64>(std::ceil(f * static_cast<double>(n))));
 }
@@ -684,8 +694,7 @@ std::unique_ptr<TTDev> round_adaptive_krp(Ctx& c, const TTDev& t, const Adaptive
         const i64 b_inc = ceil_fraction(cfg.f_inc, rbar);
         while (q < rbar) {
             // generate_residual_sketch (round_rand.cpp:80-94)
-            const i64 have = sk.width[k + 1];
-            if (have < q + b_inc) sk.append(k + 1, q + b_inc - have);
+            sk.ensure(k + 1, q + b_inc, adapt_chunk(ceil_fraction(cfg.f_inc, maxr)));
             gemm(c, false, rows, b_inc, cols, 1.0, v, rows, sk.W[k + 1].p + q * sk.ldw[k + 1], sk.ldw[k + 1], 0.0, Sb.p,
                  rows);
             // S -= Q (Q^T S)

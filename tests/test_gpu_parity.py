@@ -681,3 +681,32 @@ def test_full_batch_config5a_sampled_oracle_parity(P, O):
         y_ref = O.round_fixed_krp(x, [20] * 7, O.derive_seed(7, b), rng=O.PHILOX)
         assert y_ref.ranks == orr
         assert O.relative_error(y_ref, O.TT.from_flat(len(on), on, orr, out.flats(b, 1)[0])) <= 1e-10
+
+
+# ---- flop accounting (flops.hpp:12-37): the device counters charge the reference's formulas ----
+
+@pytest.mark.parametrize("case", ["fixed", "adaptive2", "adaptive4"])
+def test_counters_match_oracle(P, O, case):
+    """The device charges exactly the reference's flop counts — in particular the
+    adaptive sketch, which the device appends in larger chunks (Sketch::ensure)
+    but charges as the reference's column-exact appends when the columns are used."""
+    if case == "fixed":
+        x = O.two_part_tt(6, 16, 8, 20, 1e-4, 1001)
+    elif case == "adaptive2":
+        x = O.two_part_tt(6, 32, 30, 170, 1e-6, 1002)
+    else:
+        x = O.kernel_sum_tt(5, 32, 5, 6, 0.3, 1004)
+    y = to_device(x)
+    ctx = y.ctx
+    ctx.reset_counters()
+    O.flops_reset()
+    if case == "fixed":
+        P.round_fixed_krp(y, [12] * 5, 7)
+        O.round_fixed_krp(x, [12] * 5, 7, rng=O.PHILOX)
+    else:
+        f_inc = 0.05 if case == "adaptive2" else 0.04
+        tol = 1e-4 if case == "adaptive2" else 1e-6
+        P.round_adaptive_krp(y, P.AdaptiveConfig(tolerance=tol, f_init=0.1, f_inc=f_inc, seed=7))
+        O.round_adaptive_krp(x, tolerance=tol, f_init=0.1, f_inc=f_inc, seed=7, rng=O.PHILOX)
+    dev, ref = ctx.counters(), O.flops_get()
+    assert (dev.gemm, dev.qr, dev.svd, dev.sketch) == (ref["gemm"], ref["qr"], ref["svd"], ref["sketch"])

@@ -1,1 +1,1 @@
-TTR_CQR_TRACE=1 python tools/qr_bench.py 40960 32 2>&1 | grep -a -A6 cqr | tail -8
+timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -k counters 2>&1 | tail -15
