@@ -683,14 +683,15 @@ std::unique_ptr<TTDev> round_adaptive_krp(Ctx& c, const TTDev& t, const Adaptive
         if (cfg.max_rank_cap) rbar = std::min<i64>(rbar, cfg.max_rank_cap[k - 1]);
         const i64 b_init = std::min(ceil_fraction(cfg.f_init, rbar), rbar);
         const i64 hcols = t.n[k] * t.r[k + 1];
-        const i64 ldh = std::max<i64>(rbar, 1);
         // Q = qr(V W_{k+1}(:, 1:b_init))
         gemm(c, false, rows, b_init, cols, 1.0, v, rows, sk.W[k + 1].p, sk.ldw[k + 1], 0.0, Sb.p, rows);
         thin_qr(c, rows, b_init, Sb.p, rows, Qb.p, rows, nullptr, 1);
         i64 q = std::min(rows, b_init);
-        // H_next(0:q, :) = (Q^T V) H(X_{k+1})
-        gemm(c, true, q, cols, rows, 1.0, Qb.p, rows, v, rows, 0.0, Mb.p, q);
-        gemm(c, false, q, hcols, cols, 1.0, Mb.p, q, t.core(k), cols, 0.0, Hn.p, ldh);
+        // H_next = (Q^T V) H(X_{k+1}) grows by one row block per accepted basis
+        // block in the reference (round_rand.cpp:141-143); its rows do not depend
+        // on each other and it is not read inside the loop, so it is formed once
+        // for all q rows after the loop (one pass over V and X_{k+1} instead of
+        // one per block; the same flop charges)
         const i64 b_inc = ceil_fraction(cfg.f_inc, rbar);
         while (q < rbar) {
             // generate_residual_sketch (round_rand.cpp:80-94)
@@ -705,9 +706,6 @@ std::unique_ptr<TTDev> round_adaptive_krp(Ctx& c, const TTDev& t, const Adaptive
             if (est <= tau) break;
             const i64 grow = std::min(b_inc, rbar - q);
             growth_basis(c, rows, q, grow, Qb.p, Sb.p, Qn.p, P.p);
-            // H_next rows [q, q+grow) = (Qn^T V) H(X_{k+1})
-            gemm(c, true, grow, cols, rows, 1.0, Qb.p + q * rows, rows, v, rows, 0.0, Mb.p, grow);
-            gemm(c, false, grow, hcols, cols, 1.0, Mb.p, grow, t.core(k), cols, 0.0, Hn.p + q, ldh);
             q += grow;
         }
         // finished core k: Q (rows x q) with shape (rl, nk, q)
@@ -715,8 +713,11 @@ std::unique_ptr<TTDev> round_adaptive_krp(Ctx& c, const TTDev& t, const Adaptive
         copy_matrix(c, rows, q, Qb.p, rows, core.p, rows);
         out_cores.push_back(std::move(core));
         shapes.push_back({rl, nk, q});
-        // next working core = H_next(0:q, :) compacted (ld q)
-        copy_matrix(c, q, hcols, Hn.p, ldh, cur.p, q);
+        // next working core H_next = (Q^T V) H(X_{k+1}) (ld q), written over V
+        // after its last use
+        gemm(c, true, q, cols, rows, 1.0, Qb.p, rows, v, rows, 0.0, Mb.p, q);
+        gemm(c, false, q, hcols, cols, 1.0, Mb.p, q, t.core(k), cols, 0.0, Hn.p, q);
+        std::swap(cur, Hn);
         rl = q;
     }
     std::vector<i64> r(d + 1, 1);
