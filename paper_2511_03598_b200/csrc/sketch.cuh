@@ -138,6 +138,7 @@ struct BatchSketch {
     i64 ldwt;
     DBuf ones;
     std::vector<i64> width;
+    std::vector<i64> charged;  // Sketch::charged
     int rng_mode;
     std::uint64_t seed;
     XoshiroGauss xo;
@@ -151,6 +152,7 @@ struct BatchSketch {
         ldo.assign(d + 1, 0);
         ldw.assign(d + 1, 0);
         width.assign(d + 2, 0);
+        charged.assign(d + 2, 0);
         ldwt = even_ld(cap);
         for (i64 k = 2; k <= d; ++k) {
             ldo[k] = even_ld(t.n[k - 1]);
@@ -189,6 +191,34 @@ struct BatchSketch {
                              last ? ones.p : Wt[k + 1].p, ldwt, last ? 0 : ldwt * rr, W[k].p + col0 * ldw[k],
                              ldw[k], rl, k >= 3 ? Wt[k].p : nullptr, ldwt, ldwt * rl, s, last);
             width[k] = col0 + extra;
+            charged[k] = width[k];
+        }
+    }
+
+    // Sketch::ensure for all terms (one shared factor draw, s contractions per mode)
+    void ensure(i64 start, i64 target, i64 chunk) {
+        const i64 d = t.d();
+        if (rng_mode != TTR_RNG_PHILOX) {
+            if (width[start] < target) append(start, target - width[start]);
+            return;
+        }
+        if (width[start] < target) {
+            const i64 extra = std::min(std::max(target - width[start], chunk), cap - width[d]);
+            const Counts saved = c.counts;
+            const std::vector<i64> keep = charged;
+            append(start, std::max(extra, target - width[start]));
+            c.counts = saved;
+            charged = keep;
+        }
+        for (i64 k = start; k <= d; ++k) {
+            if (charged[k] >= target) continue;
+            const i64 cols = target - charged[k];
+            const std::uint64_t rl = t.r[k - 1], nk = t.n[k - 1], rr = t.r[k];
+            c.counts.rng += nk * static_cast<std::uint64_t>(cols);
+            const std::uint64_t f = (k == d) ? 2ULL * rl * nk * cols : cols * (2ULL * rr * rl * nk + 2ULL * rl * rr);
+            c.counts.gemm += f * static_cast<std::uint64_t>(s);
+            c.counts.sketch += f * static_cast<std::uint64_t>(s);
+            charged[k] = target;
         }
     }
 };

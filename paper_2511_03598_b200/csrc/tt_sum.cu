@@ -156,19 +156,16 @@ std::unique_ptr<TTDev> round_sum_adaptive_krp(Ctx& c, const std::vector<const TT
         sketch_into(0, b_init);
         thin_qr(c, rows, b_init, Sb.p, rows, Qb.p, rows, nullptr, 1);
         i64 q = std::min(rows, b_init);
-        gemm(c, true, q, vcols, rows, 1.0, Qb.p, rows, v, rows, 0.0, Mb.p, rcap + 1);  // M = Q^T V (ld rcap+1)
-        const i64 ldm = rcap + 1;
+        const i64 ldm = rcap + 1;  // M = Q^T V (ld rcap+1), formed once after the growth loop
         const i64 b_inc = ceil_frac(f_inc, rbar);
         while (q < rbar) {
             // residual_sketch_sum (sum_round.cpp:21-50): one shared fresh draw
+            // appends in chunks (Sketch::ensure; charges stay column-exact)
+            const i64 chunk = 4 * ceil_frac(f_inc, rsum);
             if (bsk) {
-                const i64 have = bsk->width[k + 1];
-                if (have < q + b_inc) bsk->append(k + 1, q + b_inc - have);
+                bsk->ensure(k + 1, q + b_inc, chunk);
             } else {
-                for (i64 i = 0; i < s_count; ++i) {
-                    const i64 have = sk[i]->width[k + 1];
-                    if (have < q + b_inc) sk[i]->append(k + 1, q + b_inc - have);
-                }
+                for (i64 i = 0; i < s_count; ++i) sk[i]->ensure(k + 1, q + b_inc, chunk);
             }
             sketch_into(q, b_inc);
             gemm(c, true, q, b_inc, rows, 1.0, Qb.p, rows, Sb.p, rows, 0.0, P.p, q);
@@ -177,9 +174,9 @@ std::unique_ptr<TTDev> round_sum_adaptive_krp(Ctx& c, const std::vector<const TT
             if (est <= tau) break;
             const i64 grow = std::min(b_inc, rbar - q);
             growth_basis(c, rows, q, grow, Qb.p, Sb.p, Qn.p, P.p);
-            gemm(c, true, grow, vcols, rows, 1.0, Qb.p + q * rows, rows, v, rows, 0.0, Mb.p + q, ldm);  // M rows [q, q+grow)
             q += grow;
         }
+        gemm(c, true, q, vcols, rows, 1.0, Qb.p, rows, v, rows, 0.0, Mb.p, ldm);  // M = Q^T V
         DBuf core(c, static_cast<std::size_t>(rows * q));
         copy_matrix(c, rows, q, Qb.p, rows, core.p, rows);
         out_cores.push_back(std::move(core));
