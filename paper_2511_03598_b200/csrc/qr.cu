@@ -480,6 +480,16 @@ void thin_qr(Ctx& c, i64 m, i64 n, const double* A, i64 lda, double* Q, i64 ldq,
         return launch_panel_col(c, a);
     };
 
+    // ---- small (<= 512 x 32): one CTA, register column owners (qr_batch.cuh):
+    //      no cross-CTA exchange per column ----
+    static const bool small_on = [] {
+        const char* e = std::getenv("TTR_QR_SMALL_CTA");  // experiments: 0 = cluster panel
+        return !(e && e[0] == '0');
+    }();
+    if (small_on && n <= kPanel && m <= 512 && m >= n) {
+        qr_small_batched(c, m, n, A, lda, 0, Q, ldq, 0, R, ldr, 0, 1);
+        return;
+    }
     // ---- <= 32 columns: one panel launch ----
     if (n <= kPanel) {
         DBuf tau(c, static_cast<std::size_t>(k));
