@@ -1,2 +1,3 @@
-timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
-for f in 1 0; do for c in 1 2; do echo "small=$f cfg $c"; TTR_QR_SMALL_CTA=$f python bench.py --config $c --steps 20 --warmup 5 --no-e2e --no-cpu-baseline 2>/dev/null | grep -o '"ms_per_step": [0-9.]*'; done; done
+for i in 1 2; do python bench.py --config 2 > gpurun_out/h_bench2.json 2> gpurun_out/h_bench2.err; grep -o '"ms_per_step": [0-9.]*\|"clocks": {[^}]*}' gpurun_out/h_bench2.json | head -2; done
+python bench.py --config 4 > gpurun_out/h_bench4.json 2> gpurun_out/h_bench4.err; grep -o '"ms_per_step": [0-9.]*\|"clocks": {[^}]*}' gpurun_out/h_bench4.json | head -2
+python bench.py > gpurun_out/h_bench5b.json 2> gpurun_out/h_bench5b.err; grep -o '"ms_per_step": [0-9.]*\|"clocks": {[^}]*}' gpurun_out/h_bench5b.json | head -2
