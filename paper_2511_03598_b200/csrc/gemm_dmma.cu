@@ -590,6 +590,8 @@ void run_gemm(Ctx& c, bool AT, int KM, int BK, GemmArgs& a, bool va2, bool vb2, 
     }
 }
 
+#include "krp_batch.cuh"
+
 }  // namespace
 
 void gemm(Ctx& c, bool trans_a, i64 M, i64 N, i64 K, double alpha, const double* A, i64 lda, const double* B,
@@ -702,6 +704,58 @@ void krp_step_batched(Ctx& c, i64 r_left, i64 n, i64 r_right, i64 N, const doubl
     const std::uint64_t per = last_core ? 2ULL * r_left * n * N
                                         : static_cast<std::uint64_t>(N) * (2ULL * r_right * r_left * n + 2ULL * r_left * r_right);
     c.charge_gemm(per * static_cast<std::uint64_t>(batch));
+    // small tensors (r_left <= 64, l <= 24): one CTA per tensor streaming the slabs (krp_batch.cuh)
+    static const bool kb_on = [] {
+        const char* e = std::getenv("TTR_KRP_BATCH");  // experiments: 0 = strided-batch GEMM path
+        return !(e && e[0] == '0');
+    }();
+    if (kb_on && r_left <= 64 && r_left % 2 == 0 && N <= 24 && n % 4 == 0 && n <= 32 && aligned16(X) && sX % 2 == 0) {
+        krpb::Args ka{};
+        ka.rl = static_cast<int>(r_left);
+        ka.n = static_cast<int>(n);
+        ka.rr = static_cast<int>(r_right);
+        ka.N = static_cast<int>(N);
+        ka.X = X;
+        ka.sX = sX;
+        ka.Om = Omega;
+        ka.ldo = ldo;
+        ka.sO = sO;
+        ka.Wt = Wt;
+        ka.ldwt = ldwt;
+        ka.sWt = sWt;
+        ka.W = W_out;
+        ka.ldw = ldw;
+        ka.sW = sW;
+        ka.Wto = Wt_out;
+        ka.ldwto = ldwt_out;
+        ka.sWto = sWto;
+        bool done = false;
+        auto go = [&](auto ks_tag) {
+            constexpr int KS = decltype(ks_tag)::value;
+            if (done || n != 4 * KS) return;
+            const std::size_t smem = krpb::smem_bytes<KS>(static_cast<int>(r_right));
+            if (smem > 200 * 1024) return;
+            static bool configured = false;
+            if (!configured) {
+                TTR_CUDA(cudaFuncSetAttribute(krpb::krp_batch_kernel<KS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              200 * 1024));
+                configured = true;
+            }
+            krpb::krp_batch_kernel<KS><<<static_cast<unsigned>(batch), krpb::kThreads, smem, c.stream>>>(ka);
+            TTR_CUDA(cudaGetLastError());
+            c.launched();
+            done = true;
+        };
+        go(std::integral_constant<int, 1>{});
+        go(std::integral_constant<int, 2>{});
+        go(std::integral_constant<int, 3>{});
+        go(std::integral_constant<int, 4>{});
+        go(std::integral_constant<int, 5>{});
+        go(std::integral_constant<int, 6>{});
+        go(std::integral_constant<int, 7>{});
+        go(std::integral_constant<int, 8>{});
+        if (done) return;
+    }
     GemmArgs a{};
     a.M = static_cast<int>(r_left);
     a.N = static_cast<int>(N);

@@ -1,3 +1,4 @@
-for i in 1 2; do python bench.py --config 2 > gpurun_out/h_bench2.json 2> gpurun_out/h_bench2.err; grep -o '"ms_per_step": [0-9.]*\|"clocks": {[^}]*}' gpurun_out/h_bench2.json | head -2; done
-python bench.py --config 4 > gpurun_out/h_bench4.json 2> gpurun_out/h_bench4.err; grep -o '"ms_per_step": [0-9.]*\|"clocks": {[^}]*}' gpurun_out/h_bench4.json | head -2
-python bench.py > gpurun_out/h_bench5b.json 2> gpurun_out/h_bench5b.err; grep -o '"ms_per_step": [0-9.]*\|"clocks": {[^}]*}' gpurun_out/h_bench5b.json | head -2
+timeout 600 python -m pytest tests/test_gpu_parity.py -x -q -k "batch" 2>&1 | tail -2
+for f in 1 0; do TTR_KRP_BATCH=$f python bench.py --config 5a --steps 5 --warmup 3 --no-e2e --no-cpu-baseline 2>/dev/null | grep -o '"ms_per_step": [0-9.]*'; done
+ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/l5a.csv python bench.py --config 5a --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1
+python tools/launch_table.py gpurun_out/l5a.csv 6
