@@ -90,8 +90,9 @@ struct TmaCfg {
     static constexpr int kABytes = BM * BK * 8, kBBytes = BN * BK * 8, kWBytes = KM == 1 ? BN * 8 : 0;
     static constexpr int kStageBytes = kABytes + kBBytes + 1024;  // W row in the padded tail
     static constexpr int kTxBytes = kABytes + kBBytes + kWBytes;
-    static constexpr int kSmemBytes = STAGES * kStageBytes + 1024 /*align*/ + 2 * STAGES * 8;
+    static constexpr int kSmemBytes = STAGES * kStageBytes + 1024 /*align*/ + 3 * STAGES * 8;
     static_assert(kABytes % 1024 == 0 && kBBytes % 1024 == 0, "swizzle atoms are 1 KB");
+    static_assert(KM != 1 || STAGES >= 3, "KRP scaling runs one k-tile ahead of the consumers");
 };
 
 template <int BM, int BN, bool AT, int KM, int STAGES>
@@ -106,6 +107,7 @@ __global__ void __launch_bounds__((BM / 32) * (BN / 32) * 32)
     const unsigned smem_s = tma::saddr(smem);
     std::uint64_t* full = reinterpret_cast<std::uint64_t*>(smem + STAGES * C_::kStageBytes);
     std::uint64_t* empty = full + STAGES;
+    std::uint64_t* scaled = empty + STAGES;  // KM = 1: Omega tile of the stage scaled by W
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int wm0 = (warp % C_::kWarpsM) * 32, wn0 = (warp / C_::kWarpsM) * 32;
@@ -124,6 +126,7 @@ __global__ void __launch_bounds__((BM / 32) * (BN / 32) * 32)
         for (int s = 0; s < STAGES; ++s) {
             tma::mbar_init(full + s, 1);
             tma::mbar_init(empty + s, NWARP);
+            if constexpr (KM == 1) tma::mbar_init(scaled + s, C_::kThreads);
         }
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
@@ -168,30 +171,46 @@ __global__ void __launch_bounds__((BM / 32) * (BN / 32) * 32)
         offA[q] = k * 128 + ((((fr >> 1) ^ (k & 7)) << 4) | ((fr & 1) << 3));
     }
 
+    // KM = 1: scale the Omega tile of k-tile kt by the slab's W row once per
+    // CTA (each of the BN rows is one column n: 128 bytes, all multiplied by
+    // W(n)) instead of once per consumer warp and fragment. Lane: 16-byte
+    // chunk (lane & 7) of rows n and n + 4 — each quarter-warp covers one
+    // whole 128-byte row (conflict-free 128-bit accesses). Every thread
+    // arrives on scaled[s] after its stores (release), consumers wait on it
+    // (acquire) — no CTA-wide barrier in the main loop.
+    auto scale_stage = [&](int kt_s) {
+        const int ss = kt_s % STAGES;
+        tma::mbar_wait(full + ss, (kt_s / STAGES) & 1);
+        const unsigned sB = smem_s + ss * C_::kStageBytes + C_::kABytes;
+        constexpr int kRowsPerWarp = BN / NWARP;  // 8 (128x64)
+        static_assert(KM != 1 || kRowsPerWarp == 8, "two rows of 8 chunks per lane group");
+        const int n = warp * kRowsPerWarp + (lane >> 3);
+        const double w0 = tma::lds64(sB + C_::kBBytes + n * 8);
+        const double w1 = tma::lds64(sB + C_::kBBytes + (n + 4) * 8);
+        const unsigned a = sB + n * 128 + (lane & 7) * 16;
+        double v0, v1, v2, v3;
+        asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n" : "=d"(v0), "=d"(v1) : "r"(a));
+        asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n" : "=d"(v2), "=d"(v3) : "r"(a + 512));
+        asm volatile("st.shared.v2.f64 [%0], {%1, %2};\n" ::"r"(a), "d"(v0 * w0), "d"(v1 * w0) : "memory");
+        asm volatile("st.shared.v2.f64 [%0], {%1, %2};\n" ::"r"(a + 512), "d"(v2 * w1), "d"(v3 * w1) : "memory");
+        tma::mbar_arrive(scaled + ss);
+    };
+    if constexpr (KM == 1) {
+        if (nk > 0) scale_stage(0);
+    }
+
     for (int kt = 0; kt < nk; ++kt) {
         const int s = kt % STAGES;
-        tma::mbar_wait(full + s, (kt / STAGES) & 1);
         // shared-space addresses (32-bit) so the fragment loads are LDS
         const unsigned sA = smem_s + s * C_::kStageBytes;
         const unsigned sB = sA + C_::kABytes;
         if constexpr (KM == 1) {
-            // scale the Omega tile by the slab's W row once per CTA (each of
-            // the BN rows is one column n: 128 bytes, all multiplied by W(n))
-            // instead of once per consumer warp and fragment
-            // lane: 16-byte chunk (lane & 7) of rows n and n + 4 — each quarter-warp
-            // covers one whole 128-byte row (conflict-free 128-bit accesses)
-            constexpr int kRowsPerWarp = BN / NWARP;  // 8 (128x64)
-            static_assert(kRowsPerWarp == 8, "two rows of 8 chunks per lane group");
-            const int n = warp * kRowsPerWarp + (lane >> 3);
-            const double w0 = tma::lds64(sB + C_::kBBytes + n * 8);
-            const double w1 = tma::lds64(sB + C_::kBBytes + (n + 4) * 8);
-            const unsigned a = sB + n * 128 + (lane & 7) * 16;
-            double v0, v1, v2, v3;
-            asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n" : "=d"(v0), "=d"(v1) : "r"(a));
-            asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n" : "=d"(v2), "=d"(v3) : "r"(a + 512));
-            asm volatile("st.shared.v2.f64 [%0], {%1, %2};\n" ::"r"(a), "d"(v0 * w0), "d"(v1 * w0) : "memory");
-            asm volatile("st.shared.v2.f64 [%0], {%1, %2};\n" ::"r"(a + 512), "d"(v2 * w1), "d"(v3 * w1) : "memory");
-            asm volatile("bar.sync 1, %0;\n" ::"n"(C_::kThreads) : "memory");
+            // scale one k-tile ahead, then wait until every warp has scaled
+            // its rows of this one (split barrier: warps may drift by a tile)
+            if (kt + 1 < nk) scale_stage(kt + 1);
+            tma::mbar_wait(scaled + s, (kt / STAGES) & 1);
+        } else {
+            tma::mbar_wait(full + s, (kt / STAGES) & 1);
         }
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
