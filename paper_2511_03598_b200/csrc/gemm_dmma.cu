@@ -51,6 +51,7 @@ struct GemmArgs {
     // TMA kernels: skip output tiles strictly below the diagonal (their C is
     // left unspecified; Gram matrices whose consumer reads the upper triangle)
     int upper;
+    int prefetch_c;  // 2-stage TMA kernel: load C before the main loop (TTR_GEMM_PREC=0 disables)
 };
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
@@ -423,6 +424,11 @@ bool tma_enabled() {
 template <int BM, int BN, bool AT, int KM, int ST = 4>
 bool launch_tma(Ctx& c, GemmArgs& a, int splits) {
     using C_ = TmaCfg<BM, BN, AT, KM, ST>;
+    static const bool prec = [] {
+        const char* e = std::getenv("TTR_GEMM_PREC");  // experiments: 0 = C read after the main loop
+        return !(e && e[0] == '0');
+    }();
+    a.prefetch_c = prec ? 1 : 0;
     CUtensorMap mA, mB, mW;
     std::memset(&mW, 0, sizeof(mW));
     const bool ok =

@@ -160,6 +160,26 @@ __global__ void __launch_bounds__((BM / 32) * (BN / 32) * 32)
         for (int j = 0; j < FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
     const int fr = lane >> 2, fc = lane & 3;
+    // short-K products (2 stages: the blocked-QR trailing updates A -= V W,
+    // K = 32) read C while the two k-tiles are in flight instead of after them
+    constexpr bool kPreC = STAGES == 2;
+    double cpre[kPreC ? FM : 1][kPreC ? FN : 1][2];
+    const bool pre = kPreC && p.prefetch_c && gridDim.z == 1 && p.beta != 0.0;
+    if constexpr (kPreC) {
+        if (pre) {
+#pragma unroll
+            for (int i = 0; i < FM; ++i) {
+                const int gm = m0 + wm0 + i * 8 + fr;
+#pragma unroll
+                for (int j = 0; j < FN; ++j)
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int gn = n0 + wn0 + j * 8 + 2 * fc + h;
+                        cpre[i][j][h] = (gm < p.M && gn < p.N) ? __ldcg(p.C + gm + static_cast<i64>(gn) * p.ldc) : 0.0;
+                    }
+            }
+        }
+    }
     // per-lane byte offsets of the fragment loads for k-step q (0..3)
     int offA[4], offB[4];
 #pragma unroll
@@ -258,6 +278,12 @@ __global__ void __launch_bounds__((BM / 32) * (BN / 32) * 32)
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
                     const int gn = n0 + wn0 + j * 8 + 2 * fc + h;
+                    if constexpr (kPreC) {
+                        if (pre) {
+                            cv[j][h] = cpre[i][j][h];
+                            continue;
+                        }
+                    }
                     cv[j][h] = (gm < p.M && gn < p.N) ? __ldcg(Cp + gm + static_cast<i64>(gn) * p.ldc) : 0.0;
                 }
 #pragma unroll
