@@ -670,7 +670,11 @@ void krp_step(Ctx& c, i64 r_left, i64 n, i64 r_right, i64 N, const double* X, co
     const int total_kt = static_cast<int>((a.K + BK - 1) / BK);
     int splits = 1;
     {
-        const i64 target = 4LL * c.sm_count;
+        static const int waves = [] {  // experiments: TTR_KRP_SPLIT_CTAS (CTAs per SM the m x split grid targets)
+            const char* e = std::getenv("TTR_KRP_SPLIT_CTAS");
+            return e ? std::max(1, std::atoi(e)) : 2;  // 2: fewer split-K partials (5b sketch 47.2 -> 46.6 ms)
+        }();
+        const i64 target = static_cast<i64>(waves) * c.sm_count;
         if (mtiles < target && total_kt >= 8) {
             i64 s = (target + mtiles - 1) / mtiles;
             s = std::min<i64>(s, std::max(1, total_kt / 8));
