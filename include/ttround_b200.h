@@ -79,7 +79,10 @@ typedef struct ttr_ctx ttr_ctx;
 typedef struct ttr_tt ttr_tt;
 
 /* AdaptiveConfig (round_rand.hpp:18-25). has_known_norm / max_rank_cap
- * (NULL or d-1 entries) stand in for the std::optional members. */
+ * stand in for the std::optional members: max_rank_cap is NULL or points to
+ * max_rank_cap_len entries, which must equal d-1 with every cap >= 1
+ * (TTR_ERR_INVALID_RANKS otherwise; the reference indexes the vector
+ * unchecked, round_rand.cpp:125-126). */
 typedef struct {
     double tolerance; /* relative, in (0,1); reference default 1e-6 */
     double f_init;    /* default 0.1 */
@@ -88,6 +91,7 @@ typedef struct {
     int has_known_norm;
     double known_norm;
     const int64_t* max_rank_cap;
+    int64_t max_rank_cap_len;
     int rng_mode;
 } ttr_adaptive_cfg;
 

@@ -159,6 +159,7 @@ inline TTTensor round_adaptive_krp(const TTTensor& tt, const AdaptiveConfig& cfg
     c.has_known_norm = cfg.known_norm.has_value() ? 1 : 0;
     c.known_norm = cfg.known_norm.value_or(0.0);
     c.max_rank_cap = cfg.max_rank_cap ? cfg.max_rank_cap->data() : nullptr;
+    c.max_rank_cap_len = cfg.max_rank_cap ? static_cast<int64_t>(cfg.max_rank_cap->size()) : 0;
     c.rng_mode = static_cast<int>(cfg.rng);
     ttr_tt* out = nullptr;
     check(ttr_round_adaptive_krp(tt.context().get(), tt.get(), &c, &out));

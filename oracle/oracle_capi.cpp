@@ -286,6 +286,13 @@ int ttro_truncated_svd(std::int64_t rows, std::int64_t cols, const double* a, in
         if (v) std::memcpy(v, t.v.data(), sizeof(double) * t.v.a.size());
     });
 }
+int ttro_set_backend(int backend, int threads) { return guard([&] { linalg::set_backend(backend, threads); }); }
+int ttro_backend() { return linalg::backend(); }
+int ttro_blas_available() { return linalg::blas_available() ? 1 : 0; }
+int ttro_random_philox_tt(std::int64_t d, const std::int64_t* n, const std::int64_t* r, std::uint64_t seed,
+                          ttro_tt** out) {
+    return guard([&] { *out = wrap(random_philox_tt(vec(n, d), vec(r, d + 1), seed)); });
+}
 void ttro_flops_reset() { flops::reset(); }
 void ttro_flops_get(std::uint64_t* out5) {
     const auto& c = flops::counters();

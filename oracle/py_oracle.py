@@ -302,6 +302,41 @@ def krp_contractions(t: TT, factors: Sequence[np.ndarray], start_mode=2) -> List
     return res
 
 
+def set_backend(backend: str = "port", threads: int = 0) -> None:
+    """Dense-kernel backend of the oracle: "port" (plain-loop restatement, the
+    pinned default) or "blas" (the same algorithms on OpenBLAS/LAPACK: dgemm,
+    dgeqrf + dorgqr, dgesvd). threads > 0 sizes both the OpenMP and OpenBLAS pools."""
+    _check(lib().ttro_set_backend(C.c_int({"port": 0, "blas": 1}[backend]), C.c_int(threads)))
+
+
+def backend() -> str:
+    return ["port", "blas"][lib().ttro_backend()]
+
+
+def blas_available() -> bool:
+    return bool(lib().ttro_blas_available())
+
+
+class backend_scope:
+    """with backend_scope("blas", threads): ... — restores the previous backend."""
+
+    def __init__(self, name: str, threads: int = 0):
+        self.name, self.threads = name, threads
+
+    def __enter__(self):
+        self.prev = backend()
+        set_backend(self.name, self.threads)
+        return self
+
+    def __exit__(self, *a):
+        set_backend(self.prev, 0)
+
+
+def random_philox_tt(modes, ranks, seed) -> TT:
+    """Bitwise the device generator ttr_tt_random_philox (Philox tags 1000 + k)."""
+    return TT._new(lib().ttro_random_philox_tt, C.c_int64(len(modes)), _i64(modes), _i64(ranks), C.c_uint64(seed))
+
+
 def gaussian_matrix(rows, cols, seed) -> np.ndarray:
     out = np.empty(rows * cols, dtype=np.float64)
     _check(lib().ttro_gaussian_matrix(C.c_int64(rows), C.c_int64(cols), C.c_uint64(seed), _dptr(out)))

@@ -10,6 +10,8 @@
 #include <limits>
 #include <numeric>
 
+#include <omp.h>
+
 extern "C" {
 #include "../include/ttround_b200/philox_gauss.h"
 }
@@ -164,11 +166,72 @@ Matrix FactorRng::draw(Index mode, Index rows, Index cols, Index col0) {
 // dense kernels — proj/core/src/linalg.cpp:24-69
 namespace linalg {
 
+// ---- backend selection ------------------------------------------------------
+// 0 = the plain-loop restatement below (default; what tests/test_oracle_golden.py
+// pins), 1 = the same algorithms on OpenBLAS/LAPACK (scipy's bundled
+// libscipy_openblas, LP64): dgemm for every product, dgeqrf + dorgqr for the
+// Householder thin QR (LAPACK's dlarfg uses Eigen's reflector convention,
+// beta = -sign(alpha)||x||), dgesvd for the thin SVD. The reference's own
+// arithmetic is Eigen (linalg.cpp:24-69); Eigen is absent here, so this is the
+// optimised stand-in used for the full-size parity checks and the CPU baseline.
+namespace {
+int g_backend = 0;
+}
+#ifdef TTRO_HAVE_OPENBLAS
+extern "C" {
+void scipy_dgemm_(const char* ta, const char* tb, const int* m, const int* n, const int* k, const double* alpha,
+                  const double* a, const int* lda, const double* b, const int* ldb, const double* beta, double* c,
+                  const int* ldc);
+void scipy_dgeqrf_(const int* m, const int* n, double* a, const int* lda, double* tau, double* work,
+                   const int* lwork, int* info);
+void scipy_dorgqr_(const int* m, const int* n, const int* k, double* a, const int* lda, const double* tau,
+                   double* work, const int* lwork, int* info);
+void scipy_dgesvd_(const char* jobu, const char* jobvt, const int* m, const int* n, double* a, const int* lda,
+                   double* s, double* u, const int* ldu, double* vt, const int* ldvt, double* work, const int* lwork,
+                   int* info, std::size_t, std::size_t);
+void scipy_openblas_set_num_threads(int);
+}
+bool blas_available() { return true; }
+#else
+bool blas_available() { return false; }
+#endif
+
+void set_backend(int backend, int threads) {
+    if (backend == 1 && !blas_available()) fail(Errc::InvalidArgument, "oracle built without OpenBLAS");
+    g_backend = backend;
+    if (threads > 0) {
+        omp_set_num_threads(threads);
+#ifdef TTRO_HAVE_OPENBLAS
+        scipy_openblas_set_num_threads(threads);
+#endif
+    }
+}
+int backend() { return g_backend; }
+
+namespace {
+int i32(Index v) {
+    if (v > std::numeric_limits<int>::max()) fail(Errc::InvalidArgument, "dimension exceeds the LP64 BLAS range");
+    return static_cast<int>(v);
+}
+}  // namespace
+
 // C = alpha*op(A)*op(B) + beta*C, column-major. Every output element is
 // produced by one thread in a fixed order (deterministic for any thread count).
 void gemm_raw(Index m, Index n, Index k, const double* a, Index lda, bool ta, const double* b,
               Index ldb, bool tb, double* c, Index ldc, double alpha, double beta) {
     if (m <= 0 || n <= 0) return;
+#ifdef TTRO_HAVE_OPENBLAS
+    if (g_backend == 1) {
+        if (k <= 0) {
+            for (Index j = 0; j < n; ++j)
+                for (Index i = 0; i < m; ++i) c[i + j * ldc] = beta == 0.0 ? 0.0 : beta * c[i + j * ldc];
+            return;
+        }
+        const int M = i32(m), N = i32(n), K = i32(k), LDA = i32(lda), LDB = i32(ldb), LDC = i32(ldc);
+        scipy_dgemm_(ta ? "T" : "N", tb ? "T" : "N", &M, &N, &K, &alpha, a, &LDA, b, &LDB, &beta, c, &LDC);
+        return;
+    }
+#endif
     const Index MC = 256, KC = 256, NC = 8;
     const Index mblocks = (m + MC - 1) / MC, nblocks = (n + NC - 1) / NC;
 #pragma omp parallel for collapse(2) schedule(static) if (m * n * k > 200000)
@@ -255,6 +318,34 @@ std::vector<double> mul_vec(const Matrix& a, const double* x) {  // linalg.cpp:3
 ThinQR thin_qr(const Matrix& m_in) {
     const Index rows = m_in.rows, cols = m_in.cols, k = std::min(rows, cols);
     charge(4 * u64(rows) * u64(cols) * u64(k), &flops::Counts::qr);
+#ifdef TTRO_HAVE_OPENBLAS
+    if (g_backend == 1 && k > 0) {  // dgeqrf + dorgqr (blocked Householder, same reflectors)
+        Matrix a = m_in;
+        const int M = i32(rows), N = i32(cols), K = i32(k), LDA = i32(std::max<Index>(1, rows));
+        std::vector<double> tau(static_cast<std::size_t>(k));
+        int info = 0, lwork = -1;
+        double wq = 0;
+        scipy_dgeqrf_(&M, &N, a.data(), &LDA, tau.data(), &wq, &lwork, &info);
+        lwork = std::max(1, static_cast<int>(wq));
+        std::vector<double> work(static_cast<std::size_t>(lwork));
+        scipy_dgeqrf_(&M, &N, a.data(), &LDA, tau.data(), work.data(), &lwork, &info);
+        if (info != 0) fail(Errc::InvalidArgument, "dgeqrf failed");
+        ThinQR out;
+        out.r = Matrix(k, cols);
+        for (Index j = 0; j < cols; ++j)
+            for (Index i = 0; i <= std::min(j, k - 1); ++i) out.r(i, j) = a(i, j);
+        Matrix q(rows, k);
+        std::memcpy(q.data(), a.data(), sizeof(double) * static_cast<std::size_t>(rows * k));
+        lwork = -1;
+        scipy_dorgqr_(&M, &K, &K, q.data(), &LDA, tau.data(), &wq, &lwork, &info);
+        lwork = std::max(1, static_cast<int>(wq));
+        work.assign(static_cast<std::size_t>(lwork), 0.0);
+        scipy_dorgqr_(&M, &K, &K, q.data(), &LDA, tau.data(), work.data(), &lwork, &info);
+        if (info != 0) fail(Errc::InvalidArgument, "dorgqr failed");
+        out.q = std::move(q);
+        return out;
+    }
+#endif
     Matrix a = m_in;
     std::vector<double> tau(static_cast<std::size_t>(k), 0.0);
     for (Index i = 0; i < k; ++i) {
@@ -321,6 +412,27 @@ Matrix thin_qr_q(const Matrix& m) { return thin_qr(m).q; }
 SVD svd(const Matrix& m) {
     const Index rows = m.rows, cols = m.cols, k = std::min(rows, cols);
     charge(14 * u64(rows) * u64(cols) * u64(k) + 8 * u64(k) * u64(k) * u64(k), &flops::Counts::svd);
+#ifdef TTRO_HAVE_OPENBLAS
+    if (g_backend == 1 && k > 0) {  // dgesvd, thin U and V^T (singular values descending)
+        Matrix a = m;
+        const int M = i32(rows), N = i32(cols), K = i32(k);
+        SVD out;
+        out.s.assign(static_cast<std::size_t>(k), 0.0);
+        out.u = Matrix(rows, k);
+        Matrix vt(k, cols);
+        int info = 0, lwork = -1;
+        double wq = 0;
+        scipy_dgesvd_("S", "S", &M, &N, a.data(), &M, out.s.data(), out.u.data(), &M, vt.data(), &K, &wq, &lwork,
+                      &info, 1, 1);
+        lwork = std::max(1, static_cast<int>(wq));
+        std::vector<double> work(static_cast<std::size_t>(lwork));
+        scipy_dgesvd_("S", "S", &M, &N, a.data(), &M, out.s.data(), out.u.data(), &M, vt.data(), &K, work.data(),
+                      &lwork, &info, 1, 1);
+        if (info != 0) fail(Errc::SVDFailure, "SVD did not converge");
+        out.v = vt.transpose();
+        return out;
+    }
+#endif
     const bool trans = rows < cols;
     Matrix a = trans ? m.transpose() : m;  // a is M x N with M >= N
     const Index M = a.rows, N = a.cols;
@@ -460,9 +572,14 @@ TT::TT(std::vector<Core> cores) : cores_(std::move(cores)) {  // tensor.cpp:66-7
     for (std::size_t k = 0; k + 1 < cores_.size(); ++k)
         if (cores_[k].r_right() != cores_[k + 1].r_left())
             fail(Errc::RankChainMismatch, "adjacent core ranks differ at position " + std::to_string(k + 1));
-    for (const auto& c : cores_)
-        for (double v : c.data())
-            if (!std::isfinite(v)) fail(Errc::InvalidArgument, "core entries must be finite");
+    for (const auto& c : cores_) {
+        const double* p = c.data().data();
+        const Index cnt = c.size();
+        int bad = 0;
+#pragma omp parallel for reduction(| : bad) schedule(static) if (cnt > (Index{1} << 22))
+        for (Index i = 0; i < cnt; ++i) bad |= !std::isfinite(p[i]);
+        if (bad) fail(Errc::InvalidArgument, "core entries must be finite");
+    }
 }
 std::vector<Index> TT::mode_sizes() const {
     std::vector<Index> o;
@@ -609,13 +726,57 @@ TT random_gaussian_tt(const std::vector<Index>& modes, const std::vector<Index>&
     return TT(std::move(cores));
 }
 
+TT random_philox_tt(const std::vector<Index>& modes, const std::vector<Index>& ranks, std::uint64_t seed) {
+    // Bitwise the device generator (paper_2511_03598_b200/csrc/dense_ops.cu
+    // random_normal_kernel): core k, element pair p = (2p, 2p+1) from
+    // ttr_philox_gauss_pair(seed, counter (p_hi, p_lo, 0, 1000 + k)), scaled by
+    // sigma = 1/sqrt(r_{k-1} n_k r_k) as tensor.cpp:236 scales its draws.
+    const Index d = static_cast<Index>(modes.size());
+    if (d < 1 || ranks.size() != modes.size() + 1) fail(Errc::InvalidRankChain, "rank chain length must be d+1");
+    std::vector<Core> cores;
+    for (Index k = 0; k < d; ++k) {
+        const Index rl = ranks[static_cast<std::size_t>(k)], n = modes[static_cast<std::size_t>(k)],
+                    rr = ranks[static_cast<std::size_t>(k) + 1];
+        Core c(rl, n, rr);
+        const double sigma = 1.0 / std::sqrt(static_cast<double>(rl) * n * rr);
+        double* out = c.data().data();
+        const Index count = c.size(), pairs = (count + 1) / 2;
+        const std::uint32_t tag = static_cast<std::uint32_t>(1000 + k);
+#pragma omp parallel for schedule(static) if (pairs > 4096)
+        for (Index p = 0; p < pairs; ++p) {
+            double e, o;
+            ttr_philox_gauss_pair(seed, static_cast<std::uint32_t>(static_cast<std::uint64_t>(p) >> 32),
+                                  static_cast<std::uint32_t>(static_cast<std::uint64_t>(p) & 0xffffffffu), 0u, tag,
+                                  &e, &o);
+            out[2 * p] = sigma * e;
+            if (2 * p + 1 < count) out[2 * p + 1] = sigma * o;
+        }
+        cores.push_back(std::move(c));
+    }
+    return TT(std::move(cores));
+}
+
 namespace {
 // internal.hpp:10-17
+// (the unfoldings are zero-copy views of the core in the reference, tensor.hpp:38-41;
+// the products below read the core buffer in place)
 Core contract_first(const Core& core, const Matrix& m) {
-    return Core::from_horizontal(core.n(), core.r_right(), linalg::mul(m, core.horizontal()));
+    const Index rl = core.r_left(), nr = core.n() * core.r_right();
+    if (m.cols != rl) fail(Errc::InvalidArgument, "contract_first: shape mismatch");
+    charge(2 * u64(m.rows) * u64(rl) * u64(nr), &flops::Counts::gemm);
+    std::vector<double> out(static_cast<std::size_t>(m.rows * nr));
+    linalg::gemm_raw(m.rows, nr, rl, m.data(), std::max<Index>(1, m.rows), false, core.data().data(), rl, false,
+                     out.data(), std::max<Index>(1, m.rows), 1.0, 0.0);
+    return Core(m.rows, core.n(), core.r_right(), std::move(out));
 }
 Core contract_third(const Core& core, const Matrix& m) {
-    return Core::from_vertical(core.r_left(), core.n(), linalg::mul(core.vertical(), m));
+    const Index rows = core.r_left() * core.n(), rr = core.r_right();
+    if (m.rows != rr) fail(Errc::InvalidArgument, "contract_third: shape mismatch");
+    charge(2 * u64(rows) * u64(rr) * u64(m.cols), &flops::Counts::gemm);
+    std::vector<double> out(static_cast<std::size_t>(rows * m.cols));
+    linalg::gemm_raw(rows, m.cols, rr, core.data().data(), rows, false, m.data(), std::max<Index>(1, m.rows), false,
+                     out.data(), rows, 1.0, 0.0);
+    return Core(core.r_left(), core.n(), m.cols, std::move(out));
 }
 
 // orthogonalize.cpp:13-26
@@ -769,6 +930,29 @@ Matrix mttkrp_step(const Core& core, const Matrix& w_next, const Matrix& omega) 
     const Index cols = w_next.cols, rl = core.r_left(), n = core.n(), rr = core.r_right();
     charge(u64(cols) * (u64(rr) * 2 * u64(rl) * u64(n) + 2 * u64(rl) * u64(rr)), &flops::Counts::gemm);
     Matrix out(rl, cols);
+    if (linalg::backend() == 1) {
+        // The same contraction as one product over the horizontal unfolding:
+        // out = H(X_k) B with B(j + n g, c) = omega(j, c) w_next(g, c), the KRP
+        // operand formed in slab chunks of <= 32 MB (summation order differs from
+        // the per-column loop only by rounding; the reference's tolerance is
+        // 1e-12 relative, tests/test_sketch.cpp:54-77).
+        const Index gb = std::max<Index>(1, std::min<Index>(rr, (Index{4} << 20) / std::max<Index>(1, n * cols)));
+        std::vector<double> b(static_cast<std::size_t>(n * gb * cols));
+        for (Index g0 = 0; g0 < rr; g0 += gb) {
+            const Index g1 = std::min(rr, g0 + gb), kk = n * (g1 - g0);
+#pragma omp parallel for schedule(static)
+            for (Index c = 0; c < cols; ++c) {
+                const double* om = omega.col(c);
+                const double* wc = w_next.col(c);
+                double* bc = b.data() + c * kk;
+                for (Index g = g0; g < g1; ++g)
+                    for (Index j = 0; j < n; ++j) bc[j + n * (g - g0)] = om[j] * wc[g];
+            }
+            linalg::gemm_raw(rl, cols, kk, core.data().data() + g0 * rl * n, rl, false, b.data(), kk, false,
+                             out.data(), rl, 1.0, g0 == 0 ? 0.0 : 1.0);
+        }
+        return out;
+    }
 #pragma omp parallel for schedule(dynamic, 1) if (cols > 1 && rl * n * rr > 20000)
     for (Index c = 0; c < cols; ++c) {
         std::vector<double> hits(static_cast<std::size_t>(rl * rr));

@@ -127,6 +127,12 @@ ThinQR thin_qr(const Matrix& m);
 Matrix thin_qr_q(const Matrix& m);
 struct SVD { Matrix u; std::vector<double> s; Matrix v; };
 SVD svd(const Matrix& m);
+//! Dense-kernel backend: 0 = plain-loop restatement (default, pinned by the
+//! golden tests), 1 = OpenBLAS/LAPACK (same algorithms; full-size parity and
+//! the CPU baseline). threads > 0 sets both the OpenMP and the OpenBLAS pools.
+void set_backend(int backend, int threads);
+int backend();
+bool blas_available();
 // uncounted helpers used by the oracle itself
 void gemm_raw(Index m, Index n, Index k, const double* a, Index lda, bool ta, const double* b,
               Index ldb, bool tb, double* c, Index ldc, double alpha, double beta);
@@ -184,6 +190,8 @@ double dense_rel_error(const Dense& a, const Dense& b);
 TT formal_sum(const std::vector<TT>& terms);
 TT random_gaussian_tt(const std::vector<Index>& modes, const std::vector<Index>& ranks,
                       std::uint64_t seed);
+//! Device-identical Philox Gaussian TT (bench inputs; tags 1000 + k).
+TT random_philox_tt(const std::vector<Index>& modes, const std::vector<Index>& ranks, std::uint64_t seed);
 double norm_exact(const TT& tt);
 double dot(const TT& a, const TT& b);
 TT scaled(const TT& tt, double alpha);

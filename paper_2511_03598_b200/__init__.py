@@ -101,7 +101,8 @@ class Counts(C.Structure):
 class _AdaptiveCfg(C.Structure):
     _fields_ = [("tolerance", C.c_double), ("f_init", C.c_double), ("f_inc", C.c_double),
                 ("seed", C.c_uint64), ("has_known_norm", C.c_int), ("known_norm", C.c_double),
-                ("max_rank_cap", C.POINTER(C.c_int64)), ("rng_mode", C.c_int)]
+                ("max_rank_cap", C.POINTER(C.c_int64)), ("max_rank_cap_len", C.c_int64),
+                ("rng_mode", C.c_int)]
 
 
 def _ctx_alive(obj) -> bool:
@@ -471,6 +472,7 @@ def round_adaptive_krp(tt: TTTensor, cfg: AdaptiveConfig) -> TTTensor:
     c.known_norm = cfg.known_norm or 0.0
     cap = _i64(cfg.max_rank_cap) if cfg.max_rank_cap is not None else None
     c.max_rank_cap = C.cast(cap, C.POINTER(C.c_int64)) if cap is not None else None
+    c.max_rank_cap_len = len(cfg.max_rank_cap) if cfg.max_rank_cap is not None else 0
     c.rng_mode = cfg.rng
     return TTTensor._new(tt.ctx, lib().ttr_round_adaptive_krp, tt.ctx._h, tt._h, C.byref(c))
 

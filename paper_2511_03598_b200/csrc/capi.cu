@@ -29,8 +29,25 @@ ttr_status guard(F&& f) {
     }
 }
 
+// Entry points bound to a context run on its device (the caller's current
+// device may be another one, e.g. a second context in the same process).
+template <typename F>
+ttr_status guard_ctx(ttr_ctx* ctx, F&& f);
+
 void need(bool ok, const char* what) {
     if (!ok) throw Error(TTR_ERR_INVALID_ARGUMENT, std::string("InvalidArgument: ") + what);
+}
+
+template <typename F>
+ttr_status guard_ctx(ttr_ctx* ctx, F&& f) {
+    return guard([&] {
+        if (ctx) {
+            int cur = -1;
+            TTR_CUDA(cudaGetDevice(&cur));
+            if (cur != ctx->c.device) TTR_CUDA(cudaSetDevice(ctx->c.device));
+        }
+        f();
+    });
 }
 
 std::vector<i64> vec(const int64_t* p, int64_t n) { return std::vector<i64>(p, p + n); }
@@ -80,10 +97,11 @@ ttr_status ttr_ctx_create(int device, void* stream, ttr_ctx** out) {
 }
 
 ttr_status ttr_ctx_destroy(ttr_ctx* ctx) {
-    return guard([&] {
+    return guard_ctx(ctx, [&] {
         if (!ctx) return;
         cudaSetDevice(ctx->c.device);
         if (ctx->c.work) cudaFreeAsync(ctx->c.work, ctx->c.stream);
+        ctx->c.release_retired();
         cudaStreamSynchronize(ctx->c.stream);
         if (ctx->c.qr_xchg) cudaFree(ctx->c.qr_xchg);
         if (ctx->c.host_scalars) cudaFreeHost(ctx->c.host_scalars);
@@ -93,7 +111,7 @@ ttr_status ttr_ctx_destroy(ttr_ctx* ctx) {
 }
 
 ttr_status ttr_ctx_set_stream(ttr_ctx* ctx, void* stream) {
-    return guard([&] {
+    return guard_ctx(ctx, [&] {
         need(ctx != nullptr, "null context");
         TTR_CUDA(cudaStreamSynchronize(ctx->c.stream));
         if (ctx->c.own_stream) {
@@ -110,21 +128,21 @@ ttr_status ttr_ctx_set_stream(ttr_ctx* ctx, void* stream) {
 }
 
 ttr_status ttr_ctx_synchronize(ttr_ctx* ctx) {
-    return guard([&] {
+    return guard_ctx(ctx, [&] {
         need(ctx != nullptr, "null context");
         TTR_CUDA(cudaStreamSynchronize(ctx->c.stream));
     });
 }
 
 ttr_status ttr_ctx_kernel_launches(ttr_ctx* ctx, uint64_t* out) {
-    return guard([&] {
+    return guard_ctx(ctx, [&] {
         need(ctx && out, "null argument");
         *out = ctx->c.launches;
     });
 }
 
 ttr_status ttr_tt_upload(ttr_ctx* ctx, int64_t d, const int64_t* n, const int64_t* r, const double* host, ttr_tt** out) {
-    return guard([&] {
+    return guard_ctx(ctx, [&] {
         need(ctx && out, "null argument");
         if (d < 1) fail(Errc::EmptyCoreList, "TT tensor needs at least one core");
         need(n && r && host, "null argument");
@@ -136,7 +154,7 @@ ttr_status ttr_tt_upload(ttr_ctx* ctx, int64_t d, const int64_t* n, const int64_
 }
 
 ttr_status ttr_tt_from_device(ttr_ctx* ctx, int64_t d, const int64_t* n, const int64_t* r, const double* dev, ttr_tt** out) {
-    return guard([&] {
+    return guard_ctx(ctx, [&] {
         need(ctx && out && n && r && dev, "null argument");
         if (d < 1) fail(Errc::EmptyCoreList, "TT tensor needs at least one core");
         auto t = std::make_unique<TTDev>(ctx->c, vec(n, d), vec(r, d + 1));
@@ -162,7 +180,7 @@ ttr_status ttr_tt_shape(const ttr_tt* tt, int64_t* d, int64_t* n, int64_t* r, in
 }
 
 ttr_status ttr_tt_download(ttr_ctx* ctx, const ttr_tt* tt, double* host) {
-    return guard([&] {
+    return guard_ctx(ctx, [&] {
         check_same_ctx(ctx, tt);
         need(host != nullptr, "null output");
         tt->t->download(host);
@@ -173,7 +191,7 @@ ttr_status ttr_tt_download(ttr_ctx* ctx, const ttr_tt* tt, double* host) {
 // cores' fp64 data in the reference layout, little-endian. Read/written
 // through a pinned staging buffer straight to/from the device tensor.
 ttr_status ttr_tt_write_ttf1(ttr_ctx* ctx, const ttr_tt* tt, const char* path) {
-    return guard([&] {
+    return guard_ctx(ctx, [&] {
         check_same_ctx(ctx, tt);
         need(path != nullptr, "null path");
         const TTDev& t = *tt->t;
@@ -196,7 +214,7 @@ ttr_status ttr_tt_write_ttf1(ttr_ctx* ctx, const ttr_tt* tt, const char* path) {
 }
 
 ttr_status ttr_tt_read_ttf1(ttr_ctx* ctx, const char* path, ttr_tt** out) {
-    return guard([&] {
+    return guard_ctx(ctx, [&] {
         need(ctx && path && out, "null argument");
         std::FILE* f = std::fopen(path, "rb");
         if (!f) fail(Errc::IoError, std::string("cannot open ") + path);
@@ -236,7 +254,7 @@ ttr_status ttr_tt_read_ttf1(ttr_ctx* ctx, const char* path, ttr_tt** out) {
 }
 
 ttr_status ttr_tt_copy_from_host(ttr_ctx* ctx, ttr_tt* tt, const double* host) {
-    return guard([&] {
+    return guard_ctx(ctx, [&] {
         check_same_ctx(ctx, tt);
         need(host != nullptr, "null input");
         tt->t->upload(host);
@@ -257,7 +275,7 @@ ttr_status ttr_tt_destroy(ttr_tt* tt) {
 }
 
 ttr_status ttr_tt_random_philox(ttr_ctx* ctx, int64_t d, const int64_t* n, const int64_t* r, uint64_t seed, ttr_tt** out) {
-    return guard([&] {
+    return guard_ctx(ctx, [&] {
         need(ctx && out && n && r, "null argument");
         if (d < 1) fail(Errc::InvalidRankChain, "rank chain length must be d+1");
         *out = wrap(random_philox_tt(ctx->c, vec(n, d), vec(r, d + 1), seed));
@@ -266,7 +284,7 @@ ttr_status ttr_tt_random_philox(ttr_ctx* ctx, int64_t d, const int64_t* n, const
 
 ttr_status ttr_tt_kernel_sum(ttr_ctx* ctx, int64_t d, int64_t n, int64_t r, int64_t terms, double ell, uint64_t seed,
                              ttr_tt** out) {
-    return guard([&] {
+    return guard_ctx(ctx, [&] {
         need(ctx && out, "null argument");
         need(d >= 1 && n >= 1 && r >= 1 && terms >= 1 && ell > 0.0, "bad kernel-sum parameters");
         *out = wrap(kernel_sum_tt(ctx->c, d, n, r, terms, ell, seed));
@@ -275,7 +293,7 @@ ttr_status ttr_tt_kernel_sum(ttr_ctx* ctx, int64_t d, int64_t n, int64_t r, int6
 
 ttr_status ttr_tt_kernel_term(ttr_ctx* ctx, int64_t d, int64_t n, int64_t r, int64_t term, double ell, uint64_t seed,
                              ttr_tt** out) {
-    return guard([&] {
+    return guard_ctx(ctx, [&] {
         need(ctx && out, "null argument");
         need(d >= 1 && n >= 1 && r >= 1 && term >= 0 && ell > 0.0, "bad kernel-sum parameters");
         *out = wrap(kernel_term_tt(ctx->c, d, n, r, term, ell, seed));
@@ -283,7 +301,7 @@ ttr_status ttr_tt_kernel_term(ttr_ctx* ctx, int64_t d, int64_t n, int64_t r, int
 }
 
 ttr_status ttr_tt_formal_sum(ttr_ctx* ctx, const ttr_tt* const* terms, int count, ttr_tt** out) {
-    return guard([&] {
+    return guard_ctx(ctx, [&] {
         need(ctx && out, "null argument");
         std::vector<const TTDev*> ts;
         for (int i = 0; i < count; ++i) {
@@ -295,14 +313,14 @@ ttr_status ttr_tt_formal_sum(ttr_ctx* ctx, const ttr_tt* const* terms, int count
 }
 
 ttr_status ttr_tt_scale(ttr_ctx* ctx, ttr_tt* tt, double alpha) {
-    return guard([&] {
+    return guard_ctx(ctx, [&] {
         check_same_ctx(ctx, tt);
         scale_tt(ctx->c, *tt->t, alpha);
     });
 }
 
 ttr_status ttr_norm_exact(ttr_ctx* ctx, const ttr_tt* tt, double* out) {
-    return guard([&] {
+    return guard_ctx(ctx, [&] {
         check_same_ctx(ctx, tt);
         need(out != nullptr, "null output");
         *out = norm_exact(ctx->c, *tt->t);
@@ -310,7 +328,7 @@ ttr_status ttr_norm_exact(ttr_ctx* ctx, const ttr_tt* tt, double* out) {
 }
 
 ttr_status ttr_relative_error(ttr_ctx* ctx, const ttr_tt* a, const ttr_tt* b, double* out) {
-    return guard([&] {
+    return guard_ctx(ctx, [&] {
         check_same_ctx(ctx, a);
         check_same_ctx(ctx, b);
         need(out != nullptr, "null output");
@@ -321,7 +339,7 @@ ttr_status ttr_relative_error(ttr_ctx* ctx, const ttr_tt* a, const ttr_tt* b, do
 
 ttr_status ttr_round_fixed_krp(ttr_ctx* ctx, const ttr_tt* tt, const int64_t* ranks, int64_t count, uint64_t seed,
                                int rng_mode, ttr_tt** out) {
-    return guard([&] {
+    return guard_ctx(ctx, [&] {
         check_same_ctx(ctx, tt);
         need(out != nullptr, "null output");
         need(rng_mode == TTR_RNG_PHILOX || rng_mode == TTR_RNG_XOSHIRO, "unknown rng mode");
@@ -332,7 +350,7 @@ ttr_status ttr_round_fixed_krp(ttr_ctx* ctx, const ttr_tt* tt, const int64_t* ra
 
 ttr_status ttr_plan_fixed_krp(ttr_ctx* ctx, const ttr_tt* tt, const int64_t* ranks, int64_t count, uint64_t seed,
                               int rng_mode, ttr_plan** out) {
-    return guard([&] {
+    return guard_ctx(ctx, [&] {
         check_same_ctx(ctx, tt);
         need(out != nullptr, "null output");
         if (count < 0 || (count > 0 && !ranks)) fail(Errc::InvalidRanks, "expected d-1 target ranks");
@@ -351,7 +369,7 @@ ttr_status ttr_plan_fixed_krp(ttr_ctx* ctx, const ttr_tt* tt, const int64_t* ran
 
 ttr_status ttr_plan_fixed_krp_host(ttr_ctx* ctx, ttr_tt* tt, const int64_t* ranks, int64_t count, uint64_t seed,
                                    const double* host_in, double* host_out, ttr_plan** out) {
-    return guard([&] {
+    return guard_ctx(ctx, [&] {
         check_same_ctx(ctx, tt);
         need(out != nullptr && host_in != nullptr && host_out != nullptr, "null argument");
         if (count < 0 || (count > 0 && !ranks)) fail(Errc::InvalidRanks, "expected d-1 target ranks");
@@ -392,7 +410,7 @@ ttr_status ttr_plan_destroy(ttr_plan* plan) {
 }
 
 ttr_status ttr_round_adaptive_krp(ttr_ctx* ctx, const ttr_tt* tt, const ttr_adaptive_cfg* cfg, ttr_tt** out) {
-    return guard([&] {
+    return guard_ctx(ctx, [&] {
         check_same_ctx(ctx, tt);
         need(cfg && out, "null argument");
         need(cfg->rng_mode == TTR_RNG_PHILOX || cfg->rng_mode == TTR_RNG_XOSHIRO, "unknown rng mode");
@@ -403,6 +421,11 @@ ttr_status ttr_round_adaptive_krp(ttr_ctx* ctx, const ttr_tt* tt, const ttr_adap
         a.seed = cfg->seed;
         a.has_known_norm = cfg->has_known_norm != 0;
         a.known_norm = cfg->known_norm;
+        if (cfg->max_rank_cap) {
+            if (cfg->max_rank_cap_len != tt->t->d() - 1) fail(Errc::InvalidRanks, "max_rank_cap needs d-1 entries");
+            for (int64_t k = 0; k < cfg->max_rank_cap_len; ++k)
+                if (cfg->max_rank_cap[k] < 1) fail(Errc::InvalidRanks, "rank caps must be >= 1");
+        }
         a.max_rank_cap = cfg->max_rank_cap;
         a.rng_mode = cfg->rng_mode;
         *out = wrap(round_adaptive_krp(ctx->c, *tt->t, a, nullptr));
@@ -411,7 +434,7 @@ ttr_status ttr_round_adaptive_krp(ttr_ctx* ctx, const ttr_tt* tt, const ttr_adap
 
 ttr_status ttr_round_sum_adaptive_krp(ttr_ctx* ctx, const ttr_tt* const* terms, int64_t count, double eps, double f_inc,
                                       uint64_t seed, int rng_mode, ttr_tt** out) {
-    return guard([&] {
+    return guard_ctx(ctx, [&] {
         need(ctx && out, "null argument");
         if (count < 1 || !terms) fail(Errc::EmptyTermList, "sum of no TT terms");
         std::vector<const TTDev*> ts;
@@ -426,7 +449,7 @@ ttr_status ttr_round_sum_adaptive_krp(ttr_ctx* ctx, const ttr_tt* const* terms, 
 
 ttr_status ttr_round_rand_orth_tt(ttr_ctx* ctx, const ttr_tt* tt, const int64_t* ranks, int64_t count, uint64_t seed,
                                   int rng_mode, ttr_tt** out) {
-    return guard([&] {
+    return guard_ctx(ctx, [&] {
         check_same_ctx(ctx, tt);
         need(out != nullptr, "null output");
         if (count < 0 || (count > 0 && !ranks)) fail(Errc::InvalidRanks, "expected d-1 target ranks");
@@ -436,7 +459,7 @@ ttr_status ttr_round_rand_orth_tt(ttr_ctx* ctx, const ttr_tt* tt, const int64_t*
 }
 
 ttr_status ttr_compression_pass(ttr_ctx* ctx, const ttr_tt* tt, double tau, ttr_tt** out) {
-    return guard([&] {
+    return guard_ctx(ctx, [&] {
         check_same_ctx(ctx, tt);
         need(out != nullptr, "null output");
         *out = wrap(compression_pass(ctx->c, *tt->t, tau));
@@ -444,7 +467,7 @@ ttr_status ttr_compression_pass(ttr_ctx* ctx, const ttr_tt* tt, double tau, ttr_
 }
 
 ttr_status ttr_round_deterministic_tol(ttr_ctx* ctx, const ttr_tt* tt, double eps, ttr_tt** out) {
-    return guard([&] {
+    return guard_ctx(ctx, [&] {
         check_same_ctx(ctx, tt);
         need(out != nullptr, "null output");
         *out = wrap(round_deterministic_tol(ctx->c, *tt->t, eps));
@@ -452,7 +475,7 @@ ttr_status ttr_round_deterministic_tol(ttr_ctx* ctx, const ttr_tt* tt, double ep
 }
 
 ttr_status ttr_round_deterministic_ranks(ttr_ctx* ctx, const ttr_tt* tt, const int64_t* ranks, int64_t count, ttr_tt** out) {
-    return guard([&] {
+    return guard_ctx(ctx, [&] {
         check_same_ctx(ctx, tt);
         need(out != nullptr, "null output");
         if (count < 0 || (count > 0 && !ranks)) fail(Errc::InvalidRanks, "expected d-1 target ranks");
@@ -461,7 +484,7 @@ ttr_status ttr_round_deterministic_ranks(ttr_ctx* ctx, const ttr_tt* tt, const i
 }
 
 ttr_status ttr_estimate_norm_krp(ttr_ctx* ctx, const ttr_tt* tt, int64_t width, uint64_t seed, int rng_mode, double* out) {
-    return guard([&] {
+    return guard_ctx(ctx, [&] {
         check_same_ctx(ctx, tt);
         need(out != nullptr, "null output");
         *out = estimate_norm_krp(ctx->c, *tt->t, width, seed, rng_mode);
@@ -470,7 +493,7 @@ ttr_status ttr_estimate_norm_krp(ttr_ctx* ctx, const ttr_tt* tt, int64_t width, 
 
 ttr_status ttr_krp_partial_contractions(ttr_ctx* ctx, const ttr_tt* tt, int64_t start_mode, int64_t cols,
                                         const double* host_factors, uint64_t seed, int64_t col0, double* host_w) {
-    return guard([&] {
+    return guard_ctx(ctx, [&] {
         check_same_ctx(ctx, tt);
         need(host_w != nullptr, "null output");
         krp_partial_contractions(ctx->c, *tt->t, start_mode, cols, host_factors, seed, col0, host_w);
@@ -479,7 +502,7 @@ ttr_status ttr_krp_partial_contractions(ttr_ctx* ctx, const ttr_tt* tt, int64_t 
 
 ttr_status ttr_philox_factor(ttr_ctx* ctx, uint64_t seed, int64_t mode, int64_t rows, int64_t cols, int64_t col0,
                              double* host_out) {
-    return guard([&] {
+    return guard_ctx(ctx, [&] {
         need(ctx && host_out, "null argument");
         need(rows >= 1 && cols >= 1, "empty shape");
         DBuf b(ctx->c, static_cast<std::size_t>(rows * cols));
@@ -490,7 +513,7 @@ ttr_status ttr_philox_factor(ttr_ctx* ctx, uint64_t seed, int64_t mode, int64_t 
 }
 
 ttr_status ttr_thin_qr(ttr_ctx* ctx, int64_t m, int64_t n, const double* host_a, double* host_q, double* host_r) {
-    return guard([&] {
+    return guard_ctx(ctx, [&] {
         need(ctx && host_a, "null argument");
         need(m >= 1 && n >= 1, "empty shape");
         const i64 k = std::min(m, n);
@@ -506,7 +529,7 @@ ttr_status ttr_thin_qr(ttr_ctx* ctx, int64_t m, int64_t n, const double* host_a,
 
 ttr_status ttr_dev_thin_qr(ttr_ctx* ctx, int64_t m, int64_t n, const double* dA, int64_t lda, double* dQ, int64_t ldq,
                            double* dR, int64_t ldr) {
-    return guard([&] {
+    return guard_ctx(ctx, [&] {
         need(ctx && dA, "null argument");
         need(m >= 1 && n >= 1 && lda >= m && (!dQ || ldq >= m), "bad shape");
         thin_qr(ctx->c, m, n, dA, lda, dQ, ldq, dR, ldr);
@@ -515,7 +538,7 @@ ttr_status ttr_dev_thin_qr(ttr_ctx* ctx, int64_t m, int64_t n, const double* dA,
 
 ttr_status ttr_dev_gemm(ttr_ctx* ctx, int trans_a, int64_t m, int64_t n, int64_t k, double alpha, const double* dA,
                         int64_t lda, const double* dB, int64_t ldb, double beta, double* dC, int64_t ldc) {
-    return guard([&] {
+    return guard_ctx(ctx, [&] {
         need(ctx && dA && dB && dC, "null argument");
         gemm(ctx->c, trans_a != 0, m, n, k, alpha, dA, lda, dB, ldb, beta, dC, ldc);
     });
@@ -524,7 +547,7 @@ ttr_status ttr_dev_gemm(ttr_ctx* ctx, int trans_a, int64_t m, int64_t n, int64_t
 ttr_status ttr_dev_gemm_batched(ttr_ctx* ctx, int trans_a, int64_t m, int64_t n, int64_t k, double alpha,
                                 const double* dA, int64_t lda, int64_t sA, const double* dB, int64_t ldb, int64_t sB,
                                 double beta, double* dC, int64_t ldc, int64_t sC, int64_t batch) {
-    return guard([&] {
+    return guard_ctx(ctx, [&] {
         need(ctx && dA && dB && dC, "null argument");
         need(batch >= 0, "negative batch");
         gemm_batched(ctx->c, trans_a != 0, m, n, k, alpha, dA, lda, sA, dB, ldb, sB, beta, dC, ldc, sC, batch);
@@ -533,7 +556,7 @@ ttr_status ttr_dev_gemm_batched(ttr_ctx* ctx, int trans_a, int64_t m, int64_t n,
 
 ttr_status ttr_gemm(ttr_ctx* ctx, int trans_a, int64_t m, int64_t n, int64_t k, const double* host_a, const double* host_b,
                     double* host_c) {
-    return guard([&] {
+    return guard_ctx(ctx, [&] {
         need(ctx && host_a && host_b && host_c, "null argument");
         need(m >= 1 && n >= 1 && k >= 1, "empty shape");
         DBuf a(ctx->c, static_cast<std::size_t>(m * k)), b(ctx->c, static_cast<std::size_t>(k * n)),
@@ -547,14 +570,14 @@ ttr_status ttr_gemm(ttr_ctx* ctx, int trans_a, int64_t m, int64_t n, int64_t k, 
 }
 
 ttr_status ttr_ctx_enable_timing(ttr_ctx* ctx, int on) {
-    return guard([&] {
+    return guard_ctx(ctx, [&] {
         need(ctx != nullptr, "null context");
         ctx->c.timing = on != 0;
     });
 }
 
 ttr_status ttr_ctx_phase_times(ttr_ctx* ctx, double* ms_out, uint64_t* count_out) {
-    return guard([&] {
+    return guard_ctx(ctx, [&] {
         need(ctx != nullptr, "null context");
         TTR_CUDA(cudaStreamSynchronize(ctx->c.stream));
         for (int p = 0; p < kNumPhases; ++p) {
@@ -576,7 +599,7 @@ ttr_status ttr_ctx_phase_times(ttr_ctx* ctx, double* ms_out, uint64_t* count_out
 // ---- column-sharded sketch (multi-GPU config 5b) ----
 ttr_status ttr_krp_sketch_into(ttr_ctx* ctx, const ttr_tt* tt, int64_t col0, int64_t ncols, uint64_t seed,
                                double* const* W_dev, const int64_t* ldw) {
-    return guard([&] {
+    return guard_ctx(ctx, [&] {
         check_same_ctx(ctx, tt);
         need(W_dev && ldw, "null argument");
         const i64 d = tt->t->d();
@@ -593,7 +616,7 @@ ttr_status ttr_krp_sketch_into(ttr_ctx* ctx, const ttr_tt* tt, int64_t col0, int
 
 ttr_status ttr_round_fixed_krp_from_sketch(ttr_ctx* ctx, const ttr_tt* tt, const int64_t* ranks, int64_t count,
                                            const double* const* W_dev, const int64_t* ldw, int64_t width, ttr_tt** out) {
-    return guard([&] {
+    return guard_ctx(ctx, [&] {
         check_same_ctx(ctx, tt);
         need(out && W_dev && ldw, "null argument");
         if (count < 0 || (count > 0 && !ranks)) fail(Errc::InvalidRanks, "expected d-1 target ranks");
@@ -615,7 +638,7 @@ ttr_status ttr_round_fixed_krp_from_sketch(ttr_ctx* ctx, const ttr_tt* tt, const
 // ---- batches of independent tensors (config 5a) ----
 ttr_status ttr_batch_upload(ttr_ctx* ctx, int64_t batch, int64_t d, const int64_t* n, const int64_t* r,
                             const double* host, ttr_batch** out) {
-    return guard([&] {
+    return guard_ctx(ctx, [&] {
         need(ctx && out && n && r && host, "null argument");
         if (d < 1) fail(Errc::EmptyCoreList, "TT tensor needs at least one core");
         auto t = std::make_unique<TTBatch>(ctx->c, batch, vec(n, d), vec(r, d + 1));
@@ -637,7 +660,7 @@ ttr_status ttr_batch_upload(ttr_ctx* ctx, int64_t batch, int64_t d, const int64_
 
 ttr_status ttr_batch_two_part_philox(ttr_ctx* ctx, int64_t batch, int64_t d, int64_t n, int64_t rx, int64_t rz,
                                      double eps, uint64_t seed, ttr_batch** out) {
-    return guard([&] {
+    return guard_ctx(ctx, [&] {
         need(ctx && out, "null argument");
         need(batch >= 1 && d >= 2 && n >= 1 && rx >= 1 && rz >= 1, "bad batch shape");
         auto* o = new ttr_batch;
@@ -659,7 +682,7 @@ ttr_status ttr_batch_shape(const ttr_batch* b, int64_t* batch, int64_t* d, int64
 }
 
 ttr_status ttr_batch_download(ttr_ctx* ctx, const ttr_batch* b, int64_t first, int64_t count, double* host) {
-    return guard([&] {
+    return guard_ctx(ctx, [&] {
         need(ctx && b && b->t && host, "null argument");
         const TTBatch& t = *b->t;
         if (first < 0 || count < 0 || first + count > t.batch) fail(Errc::IndexOutOfRange, "batch range out of range");
@@ -682,7 +705,7 @@ ttr_status ttr_batch_destroy(ttr_batch* b) {
 
 ttr_status ttr_round_fixed_krp_batched(ttr_ctx* ctx, const ttr_batch* b, const int64_t* ranks, int64_t count,
                                        uint64_t seed, ttr_batch** out) {
-    return guard([&] {
+    return guard_ctx(ctx, [&] {
         need(ctx && b && b->t && out, "null argument");
         if (count < 0 || (count > 0 && !ranks)) fail(Errc::InvalidRanks, "expected d-1 target ranks");
         auto* o = new ttr_batch;
@@ -692,7 +715,7 @@ ttr_status ttr_round_fixed_krp_batched(ttr_ctx* ctx, const ttr_batch* b, const i
 }
 
 ttr_status ttr_counters(ttr_ctx* ctx, ttr_counts* out) {
-    return guard([&] {
+    return guard_ctx(ctx, [&] {
         need(ctx && out, "null argument");
         out->gemm = ctx->c.counts.gemm;
         out->qr = ctx->c.counts.qr;
@@ -703,7 +726,7 @@ ttr_status ttr_counters(ttr_ctx* ctx, ttr_counts* out) {
 }
 
 ttr_status ttr_counters_reset(ttr_ctx* ctx) {
-    return guard([&] {
+    return guard_ctx(ctx, [&] {
         need(ctx != nullptr, "null context");
         ctx->c.counts = Counts{};
     });

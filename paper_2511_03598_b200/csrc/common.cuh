@@ -4,6 +4,7 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 #include <stdexcept>
 #include <string>
@@ -39,6 +40,15 @@ struct Error : std::runtime_error {
         if (_e != cudaSuccess) ::ttr::cuda_fail(_e, #expr, __FILE__, __LINE__); \
     } while (0)
 
+// One-time per-device kernel attribute setup (cudaFuncSetAttribute applies to
+// the current device only): returns true the first time it is called on a device.
+inline bool first_on_device(std::atomic<std::uint64_t>& mask) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const std::uint64_t bit = std::uint64_t{1} << (dev & 63);
+    return (mask.fetch_or(bit) & bit) == 0;
+}
+
 // Algorithmic flop counters with the reference's charges (linalg.cpp:14-18).
 struct Counts {
     std::uint64_t gemm = 0, qr = 0, svd = 0, sketch = 0, rng = 0;
@@ -50,7 +60,8 @@ enum Phase { kPhaseSketch = 0, kPhaseQr = 1, kPhaseGemm = 2, kPhaseOther = 3, kN
 // QR panel grid-exchange workspace (qr_panel.cuh): 2 header words, then
 // [2][160][32] CTA partials and [2][32] published-row slots (sized for the
 // former tagged layout, two words per value)
-constexpr std::size_t kQrXchgWords = 2 + 2 * 160 * 32 * 2 + 2 * 32 * 2;
+constexpr int kQrMaxGridCtas = 160;  // grid-mode panels launch at most this many CTAs
+constexpr std::size_t kQrXchgWords = 2 + 2 * kQrMaxGridCtas * 32 * 2 + 2 * 32 * 2;
 
 // Host-streaming hooks of a plan with host buffers (tt_round.cu): the input
 // cores arrive by H2D on a copy stream (events per core), output cores leave
@@ -81,9 +92,16 @@ struct Ctx {
     Counts counts;
     int sketch_depth = 0;
     std::uint64_t launches = 0;
-    // scratch for split-K partials, grown on demand (stream-ordered)
+    // scratch for split-K partials, grown on demand (stream-ordered). A live
+    // CUDA-graph plan has the pointer baked into its kernel nodes, so while any
+    // plan is alive a grown-out buffer is retired (kept) instead of freed; the
+    // retired buffers are released when the last plan goes (Plan::~Plan) or
+    // with the context.
     double* work = nullptr;
     std::size_t work_bytes = 0;
+    int live_plans = 0;
+    std::vector<void*> retired;
+    void release_retired();
     // small pinned host staging buffer for scalars
     double* host_scalars = nullptr;
     // persistent workspace of the QR panel's grid exchange (qr_panel.cuh)

@@ -437,10 +437,9 @@ bool launch_tma(Ctx& c, GemmArgs& a, int splits) {
         (KM != 1 || make_map(&mW, a.Wt, a.N, a.K / a.nmode, a.ldw, BN, 1, false));
     if (!ok) return false;
     auto kern = dgemm_tma_kernel<BM, BN, AT, KM, ST>;
-    static bool configured = false;
-    if (!configured) {
+    static std::atomic<std::uint64_t> configured{0};  // bit d: attributes set on device d
+    if (first_on_device(configured)) {
         TTR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C_::kSmemBytes));
-        configured = true;
     }
     dim3 grid((a.M + BM - 1) / BM, (a.N + BN - 1) / BN, splits);
     kern<<<grid, C_::kThreads, C_::kSmemBytes, c.stream>>>(mA, mB, mW, a);
@@ -453,10 +452,9 @@ template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool AT, int KM, i
 void launch(Ctx& c, GemmArgs& a, int splits) {
     using C_ = Cfg<BM, BN, BK, WM, WN, STAGES, AT, KM, VA, VB>;
     auto kern = dgemm_kernel<BM, BN, BK, WM, WN, STAGES, AT, KM, VA, VB>;
-    static bool configured = false;  // per instantiation
-    if (!configured) {
+    static std::atomic<std::uint64_t> configured{0};  // bit d: attributes set on device d
+    if (first_on_device(configured)) {
         TTR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C_::kSmemBytes));
-        configured = true;
     }
     dim3 grid((a.M + BM - 1) / BM, (a.N + BN - 1) / BN, a.batch > 1 ? a.batch : splits);
     kern<<<grid, C_::kThreads, C_::kSmemBytes, c.stream>>>(a);
@@ -745,11 +743,10 @@ void krp_step_batched(Ctx& c, i64 r_left, i64 n, i64 r_right, i64 N, const doubl
             if (done || n != 4 * KS) return;
             const std::size_t smem = krpb::smem_bytes<KS>(static_cast<int>(r_right));
             if (smem > 200 * 1024) return;
-            static bool configured = false;
-            if (!configured) {
+            static std::atomic<std::uint64_t> configured{0};  // bit d: attributes set on device d
+            if (first_on_device(configured)) {
                 TTR_CUDA(cudaFuncSetAttribute(krpb::krp_batch_kernel<KS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                               200 * 1024));
-                configured = true;
             }
             krpb::krp_batch_kernel<KS><<<static_cast<unsigned>(batch), krpb::kThreads, smem, c.stream>>>(ka);
             TTR_CUDA(cudaGetLastError());

@@ -183,10 +183,9 @@ template <int RPT, int WARPS, int MODE>
 void launch_col(Ctx& c, const RegQrArgs& a, i64 grid) {
     auto kern = panel_col_kernel<RPT, WARPS, MODE>;
     if constexpr (MODE == 0) {
-        static bool configured = false;
-        if (!configured) {
+        static std::atomic<std::uint64_t> configured{0};  // bit d: attributes set on device d
+        if (first_on_device(configured)) {
             TTR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-            configured = true;
         }
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(static_cast<unsigned>(grid));
@@ -270,7 +269,7 @@ bool launch_panel_col(Ctx& c, RegQrArgs a) {
     if ((forced < 0 || forced == 0) &&
         (cl_try(std::integral_constant<int, 4>{}) || cl_try(std::integral_constant<int, 8>{})))
         return true;
-    const i64 g = c.sm_count;
+    const i64 g = std::min<i64>(c.sm_count, kQrMaxGridCtas);  // the exchange layout holds 160 CTA slots
     if (gr_try(std::integral_constant<int, 4>{}, I16{}, Gb{}, g) ||
         gr_try(std::integral_constant<int, 8>{}, I16{}, Gb{}, g) ||
         gr_try(std::integral_constant<int, 12>{}, I16{}, Gb{}, g) ||
@@ -420,10 +419,9 @@ void qr_small_batched(Ctx& c, i64 m, i64 n, const double* A, i64 lda, i64 sA, do
         return;
     }
     const std::size_t smem = small_smem_bytes(m, n);
-    static bool configured = false;
-    if (!configured) {
+    static std::atomic<std::uint64_t> configured{0};  // bit d: attributes set on device d
+    if (first_on_device(configured)) {
         TTR_CUDA(cudaFuncSetAttribute(qr_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-        configured = true;
     }
     qr_small_kernel<<<static_cast<unsigned>(batch), kQrThreads, smem, c.stream>>>(
         static_cast<int>(m), static_cast<int>(n), A, lda, sA, Q, ldq, sQ, R, ldr, sR);
@@ -580,10 +578,9 @@ void thin_qr(Ctx& c, i64 m, i64 n, const double* A, i64 lda, double* Q, i64 ldq,
         // G = V^T V; t_aggregate_kernel reads only its strictly upper 32-blocks
         gemm(c, true, k, k, m, 1.0, Vall.p, ldw, Vall.p, ldw, 0.0, Gm.p, k, false, true);
         const std::size_t smem = (static_cast<std::size_t>(npanels) * 32 * 32 + (npanels - 1) * 32 * 33) * sizeof(double);
-        static bool configured = false;
-        if (!configured) {
+        static std::atomic<std::uint64_t> configured{0};  // bit d: attributes set on device d
+        if (first_on_device(configured)) {
             TTR_CUDA(cudaFuncSetAttribute(t_aggregate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-            configured = true;
         }
         t_aggregate_kernel<<<static_cast<unsigned>(npanels), kTaggThreads, smem, c.stream>>>(static_cast<int>(k), Gm.p,
                                                                                              Ts.p, Tf.p);

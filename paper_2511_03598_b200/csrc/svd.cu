@@ -299,11 +299,10 @@ int jacobi_columns(Ctx& c, i64 M, i64 Nn, double* A, i64 lda) {
         if (cluster) {
             const std::size_t smem = static_cast<std::size_t>(2 * b * M * 8);
             auto kern = jacobi_block_kernel;
-            static bool configured = false;
-            if (!configured) {
+            static std::atomic<std::uint64_t> configured{0};  // bit d: attributes set on device d
+            if (first_on_device(configured)) {
                 TTR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
                 TTR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(max_smem)));
-                configured = true;
             }
             cudaLaunchConfig_t cfg = {};
             cfg.gridDim = dim3(static_cast<unsigned>(G));

@@ -34,10 +34,9 @@ bool lr_fused_batched(Ctx& c, const lrb::LrArgs& a, i64 batch) {
         if (done || lt != LT || lt2 != LT2) return;
         auto kern = lrb::lr_fused_kernel<LT, LT2>;
         constexpr std::size_t smem = lrb::LrSmem<LT>::kBytes;
-        static bool configured = false;
-        if (!configured) {
+        static std::atomic<std::uint64_t> configured{0};  // bit d: attributes set on device d
+        if (first_on_device(configured)) {
             TTR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-            configured = true;
         }
         kern<<<static_cast<unsigned>(batch), lrb::kThreads, smem, c.stream>>>(a);
         TTR_CUDA(cudaGetLastError());

@@ -44,12 +44,18 @@ void dfree(Ctx& c, void* p) {
 
 double* Ctx::scratch(std::size_t bytes) {
     if (bytes > work_bytes) {
-        if (work) TTR_CUDA(cudaFreeAsync(work, stream));
+        if (work && live_plans > 0) retired.push_back(work);  // a captured graph may still use it
+        else if (work) TTR_CUDA(cudaFreeAsync(work, stream));
         const std::size_t grow = std::max(bytes, work_bytes * 2);
         TTR_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&work), grow, stream));
         work_bytes = grow;
     }
     return work;
+}
+
+void Ctx::release_retired() {
+    for (void* p : retired) cudaFreeAsync(p, stream);  // ordered after every earlier replay
+    retired.clear();
 }
 
 unsigned long long* Ctx::qr_exchange() {
@@ -515,6 +521,7 @@ Plan::Plan(Ctx& cc, const TTDev& in_, const std::vector<i64>& ranks_, std::uint6
             o += static_cast<std::size_t>(out->core_size(k));
         }
     }
+    ++c.live_plans;  // from here on the scratch captured below is never freed under the graph
     TTR_CUDA(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal));
     try {
         if (host) {
@@ -543,6 +550,7 @@ Plan::Plan(Ctx& cc, const TTDev& in_, const std::vector<i64>& ranks_, std::uint6
         cudaStreamEndCapture(c.stream, &g);
         if (g) cudaGraphDestroy(g);
         c.timing = timing;
+        if (--c.live_plans == 0) c.release_retired();
         throw;
     }
     TTR_CUDA(cudaStreamEndCapture(c.stream, &graph));
@@ -572,6 +580,7 @@ void Plan::execute() {
 Plan::~Plan() {
     if (exec) cudaGraphExecDestroy(exec);
     if (graph) cudaGraphDestroy(graph);
+    if (graph && --c.live_plans == 0) c.release_retired();
     for (auto e : io.in_ready) cudaEventDestroy(e);
     for (auto e : io.out_ready) cudaEventDestroy(e);
     if (fork) cudaEventDestroy(fork);

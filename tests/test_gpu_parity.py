@@ -223,6 +223,45 @@ def test_plan_replays_bitwise(P, O):
     plan.close()
 
 
+def test_random_philox_tt_bitwise(P, O):
+    """The bench inputs are reproducible on the host: the oracle's
+    random_philox_tt equals the device generator bit for bit (so the CPU
+    reference arm rounds the same config input as the GPU arm)."""
+    modes, ranks = [7, 16, 5, 9], [1, 13, 30, 4, 1]
+    dev = P.TTTensor.random_philox(modes, ranks, 123456789, P.Context(0))
+    host = O.random_philox_tt(modes, ranks, 123456789)
+    assert np.array_equal(dev.flat(), host.flat())
+
+
+def test_rank_cap_length_checked(P, O):
+    """max_rank_cap crosses the C ABI with its length: anything but d-1 caps >= 1
+    is InvalidRanks (the reference would index the vector out of bounds)."""
+    x = to_device(O.two_part_tt(4, 8, 3, 5, 1e-6, 2005))
+    for cap in ([3, 3], [3, 3, 3, 3], [3, 0, 3]):
+        with pytest.raises(P.TTRoundError) as e:
+            P.round_adaptive_krp(x, P.AdaptiveConfig(tolerance=1e-6, seed=1, max_rank_cap=cap))
+        assert e.value.code == "InvalidRanks"
+
+
+def test_plan_survives_scratch_growth(P, O):
+    """A plan keeps the split-K scratch it captured: a later call on the same
+    context that needs a larger scratch (a bigger tensor) must not free the
+    buffer under the graph — the replay still equals the eager result bitwise."""
+    ctx = P.Context(0)
+    x = O.two_part_tt(5, 24, 12, 36, 1e-6, 2001)
+    t = to_device(x, ctx)
+    plan = P.FixedKrpPlan(t, [20] * 4, 7)
+    plan.execute()
+    first = plan.output.flat()
+    big = P.TTTensor.two_part_philox(4, 128, 300, 700, 1e-8, 1005, ctx)  # split-K scratch of 1000 x 320 slices
+    big_out = P.round_fixed_krp(big, [320] * 3, 7)
+    del big, big_out
+    for _ in range(2):
+        plan.execute()
+        assert np.array_equal(plan.output.flat(), first)
+    plan.close()
+
+
 def test_host_streaming_plan(P, O):
     """ttr_plan_fixed_krp_host: H2D of the input and D2H of the result inside the
     graph (copy stream, per-core events) give the eager result bitwise."""
@@ -663,6 +702,66 @@ def test_full_size_config_oracle_parity(P, O, cfg):
     del y, x
     assert y_gpu.ranks() == y_ref.ranks
     assert O.relative_error(y_ref, _dev_to_oracle(O, y_gpu)) <= 1e-10
+
+
+@pytest.mark.parametrize("cfg", ["5b", "3-det"])
+def test_full_size_headline_oracle_parity(P, O, cfg):
+    """The north-star gate on the two largest calls at their FULL BASELINE sizes:
+    config 5b round_fixed_krp(Y, {320}x19, 7) at d = 20 (18.4 GB of cores,
+    round_rand.cpp:52-64) and config 3's comparison call
+    round_deterministic(Y, {100}x29) (2.3 GB, orthogonalize.cpp:129-140). The
+    device input is downloaded into the oracle, which runs on its OpenBLAS/LAPACK
+    backend (the same algorithms on all host cores; the plain-loop port would take
+    minutes here). Both sides draw the same Philox factors; the rank vectors must be
+    the expected ones and ||Y_gpu - Y_ref|| / ||Y_ref|| <= 1e-10 in TT
+    arithmetic (the oracle's stable formal-difference relative_error)."""
+    import os
+    ctx = P.Context(0)
+    if cfg == "5b":
+        y = P.TTTensor.two_part_philox(20, 128, 300, 700, 1e-8, 1005, ctx)
+        y_gpu = P.round_fixed_krp(y, [320] * 19, 7)
+        expect = [1, 128] + [320] * 18 + [1]
+    else:
+        y = P.TTTensor.two_part_philox(30, 64, 100, 300, 1e-8, 1003, ctx)
+        y_gpu = P.round_deterministic(y, target_ranks=[100] * 29)
+        expect = [1, 64] + [100] * 27 + [64, 1]
+    assert y_gpu.ranks() == expect
+    with O.backend_scope("blas", os.cpu_count() or 1):
+        x = _dev_to_oracle(O, y)
+        del y
+        if cfg == "5b":
+            y_ref = O.round_fixed_krp(x, [320] * 19, 7, rng=O.PHILOX)
+        else:
+            y_ref = O.round_deterministic(x, ranks=[100] * 29)
+        del x
+        assert y_ref.ranks == expect
+        err = O.relative_error(y_ref, _dev_to_oracle(O, y_gpu))
+    assert err <= 1e-10, err
+
+
+def test_full_batch_config5a_all_tensors_oracle_parity(P, O):
+    """Config 5a at its full size: every one of the 4096 tensors of the batched
+    round (12.9 GB generated on the device) equals the oracle's round_fixed_krp of
+    the same downloaded input with the per-tensor seed derive_seed(7, b): identical
+    ranks and ||Y_gpu - Y_ref|| / ||Y_ref|| <= 1e-10 for each b."""
+    from paper_2511_03598_b200.seeds import derive_seed
+    ctx = P.Context(0)
+    batch = P.TTBatch.two_part_philox(4096, 8, 16, 16, 48, 1e-6, derive_seed(1005, 1000), ctx)
+    out = P.round_fixed_krp_batched(batch, [20] * 7, 7)
+    _, n, r, _ = batch.shape()
+    _, on, orr, _ = out.shape()
+    assert orr == [1, 16, 20, 20, 20, 20, 20, 20, 1]
+    worst = 0.0
+    chunk = 512
+    for b0 in range(0, 4096, chunk):
+        xs = batch.flats(b0, chunk)
+        ys = out.flats(b0, chunk)
+        for i in range(chunk):
+            x = O.TT.from_flat(len(n), n, r, xs[i])
+            y_ref = O.round_fixed_krp(x, [20] * 7, O.derive_seed(7, b0 + i), rng=O.PHILOX)
+            assert y_ref.ranks == orr
+            worst = max(worst, O.relative_error(y_ref, O.TT.from_flat(len(on), on, orr, ys[i])))
+    assert worst <= 1e-10, worst
 
 
 def test_full_batch_config5a_sampled_oracle_parity(P, O):
