@@ -19,12 +19,14 @@ round_fixed_krp call (sketch + left-to-right Rand-Orth sweep).
   roofline: the KRP sketch contraction kernel (krp_step = TMA-fed DMMA GEMM +
            split-K reduce) against the measured fp64 DMMA peak; traffic from
            the committed ncu capture of one launch at the same shape.
-  cpu_baseline: the CPU oracle (restatement of the reference, OpenMP on all host
-           cores) on a bounded sample of the same workload: round_fixed_krp on
-           a d=3 slice (n=128, ranks 1000, l=320: one full middle-core mode).
+  cpu_baseline: the CPU oracle (restatement of the reference on its OpenBLAS/LAPACK
+           backend, all host threads) on the FULL config: one round_fixed_krp of
+           the same input (downloaded from the device), wall clock around the call.
 
---impl reference times that CPU implementation alone (the reference itself
-cannot be built here: Eigen is absent — see DESIGN.md).
+--impl reference times that CPU implementation alone on the same config (input
+rebuilt on the host: the Philox cores are bitwise the device's), one full round
+per step (the reference itself cannot be built here: Eigen is absent — see
+DESIGN.md §4).
 """
 from __future__ import annotations
 
@@ -47,7 +49,8 @@ FP64_PEAK_TFLOPS = 36.9  # measured: DMMA m8n8k4 microbenchmark, profiles/r01_bo
 PEAK_SOURCE = "measured fp64 DMMA (mma.sync m8n8k4) burst peak on this pool's B200, profiles/r01_box_probe.log"
 
 CFG5B = dict(d=20, n=128, rx=300, rz=700, eps=1e-8, ell=320, seed=1005, round_seed=7)
-CPU_SAMPLE = dict(d=3, n=128, r=1000, ell=320, seed=5)
+CFG3 = dict(d=30, n=64, rx=100, rz=300, eps=1e-8, ell=110, seed=1003)
+CFG1 = dict(d=10, n=20, rx=10, rz=40, eps=1e-4, ell=15, seed=1001)
 
 
 def parse():
@@ -60,6 +63,8 @@ def parse():
                     help="BASELINE config: 5b (default, the headline), 1 and 3 (fixed rank), 2 and 4 "
                          "(adaptive rank), 5a (batch of 4096 tensors)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-threads", type=int, default=0,
+                    help="host threads of the CPU reference / cpu_baseline (default: all cores)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--sharding", default="tensors", choices=["tensors", "columns", "rows"],
                     help="N>1 on config 5b: independent tensor per rank (weak), or one tensor with "
@@ -76,50 +81,91 @@ def dist_env():
 
 
 # ---------------------------------------------------------------------------
-# CPU oracle sample (reference restatement) — used by cpu_baseline and --impl reference
+# CPU reference (the oracle restatement of the reference, on its OpenBLAS/LAPACK
+# backend) on the FULL config — used by the cpu_baseline leg and --impl reference
 
-def cpu_sample(runs: int = 1):
+def _oracle():
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import py_oracle as O
-    s = CPU_SAMPLE
-    x = O.random_gaussian_tt([s["n"]] * s["d"], [1] + [s["r"]] * (s["d"] - 1) + [1], s["seed"])
-    out = []
-    for _ in range(runs):
-        sec = C.c_double()
-        fl = C.c_uint64()
-        O._check(O.lib().ttro_time_round_fixed_krp(x._h, O._i64([s["ell"]] * (s["d"] - 1)), C.c_int64(s["d"] - 1),
-                                                   C.c_uint64(7), C.c_int(O.PHILOX), C.byref(sec), C.byref(fl)))
-        out.append((sec.value, fl.value))
-    return out
+    return O
 
 
-def cpu_threads() -> int:
+def cpu_threads(args=None) -> int:
+    if args is not None and getattr(args, "cpu_threads", 0):
+        return args.cpu_threads
     return int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
 
 
-def sample_desc():
-    s = CPU_SAMPLE
-    return (f"round_fixed_krp on a d={s['d']} slice of the workload (n={s['n']}, ranks {s['r']}, l={s['ell']}: "
-            f"one full middle-core sketch + LR mode), CPU oracle (reference restatement), wall clock around the call")
+def cpu_input(O, cfg):
+    """The bench input rebuilt on the host: the Philox cores are bitwise the device's
+    (oracle random_philox_tt == ttr_tt_random_philox), each part scaled to unit norm
+    (sqrt(dot), a GEMM-only pass) and combined by formal_sum."""
+    d, n = cfg["d"], cfg["n"]
+    x = O.random_philox_tt([n] * d, [1] + [cfg["rx"]] * (d - 1) + [1], O.derive_seed(cfg["seed"], 1))
+    x = O.scaled(x, 1.0 / math.sqrt(O.dot(x, x)))
+    z = O.random_philox_tt([n] * d, [1] + [cfg["rz"]] * (d - 1) + [1], O.derive_seed(cfg["seed"], 2))
+    z = O.scaled(z, cfg["eps"] / math.sqrt(O.dot(z, z)))
+    return O.formal_sum([x, z])
+
+
+def cpu_round(O, x, ranks, seed):
+    """One round_fixed_krp on the host, wall clock around the call only
+    (tools/ttround_main.cpp:156-160). Returns (seconds, charged flops)."""
+    sec = C.c_double()
+    fl = C.c_uint64()
+    O._check(O.lib().ttro_time_round_fixed_krp(x._h, O._i64(ranks), C.c_int64(len(ranks)), C.c_uint64(seed),
+                                               C.c_int(O.PHILOX), C.byref(sec), C.byref(fl)))
+    return sec.value, fl.value
+
+
+def cpu_desc(cfg, threads):
+    return (f"the full config: round_fixed_krp(Y, {{{cfg['ell']}}}x{cfg['d'] - 1}, 7) on the same input "
+            f"(d={cfg['d']}, n={cfg['n']}, ranks {cfg['rx']} + {cfg['eps']:g} x {cfg['rz']}), one round per step; "
+            f"CPU oracle (restatement of the reference, OpenBLAS/LAPACK backend: dgemm, dgeqrf+dorgqr) on "
+            f"{threads} host threads, wall clock around the call")
 
 
 def run_reference(args, world, rank):
+    """--impl reference: the reference's CPU implementation of the path (the oracle
+    port — the reference itself cannot be built here) on the host cores,
+    on the same config, metric and unit as the GPU arm. Rank 0 only."""
     if rank != 0:
         return
+    O = _oracle()
+    threads = cpu_threads(args)
+    O.set_backend("blas", threads)
+    cfg = dict(CFG5B)
+    if args.config == "3":
+        cfg.update(CFG3)
+    elif args.config == "1":
+        cfg.update(CFG1)
+    elif args.config != "5b":
+        print(json.dumps({"impl": "reference", "unavailable": f"--impl reference covers configs 5b, 3 and 1 "
+                                                                f"(asked: {args.config})"}), flush=True)
+        return
+    t0 = time.perf_counter()
+    x = cpu_input(O, cfg)
+    gen_s = time.perf_counter() - t0
+    ranks = [cfg["ell"]] * (cfg["d"] - 1)
     for _ in range(args.warmup):
-        cpu_sample(1)
-    res = cpu_sample(args.steps)
+        cpu_round(O, x, ranks, 7)
+    res = [cpu_round(O, x, ranks, 7) for _ in range(args.steps)]
     secs = [r[0] for r in res]
     flops = res[0][1]
-    tot = sum(secs)
-    tflops = flops * len(secs) / tot / 1e12
+    ms = sum(secs) / len(secs) * 1e3
+    tflops = flops / (ms * 1e-3) / 1e12
     line = {
         "impl": "reference", "metric": METRIC, "value": tflops, "unit": "TFLOP/s", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot / len(secs) * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "config 5b fixed-rank KRP rounding, bounded CPU sample", "sample": sample_desc()},
-        "cpu_baseline": {"value": tflops, "unit": "TFLOP/s", "cores": cpu_threads(), "kind": "port",
-                         "sample": sample_desc()},
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (host Philox Gaussian cores, bitwise the device generator)",
+        "config": {"workload": f"config {args.config} fixed-rank KRP rounding round_fixed_krp(Y, "
+                               f"{{{cfg['ell']}}}x{cfg['d'] - 1}, 7)", "d": cfg["d"], "n": cfg["n"],
+                   "formal_rank": cfg["rx"] + cfg["rz"], "l": cfg["ell"], "same_config": True,
+                   "flops_per_step": flops, "input_build_s": gen_s},
+        "step_seconds": secs,
+        "cpu_baseline": {"value": tflops, "unit": "TFLOP/s", "cores": threads, "kind": "port",
+                         "sample": cpu_desc(cfg, threads)},
         "e2e": {"value": tflops, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -222,9 +268,9 @@ def run_ours(args, world, rank, local):
 
     cfg = dict(CFG5B)
     if args.config == "3":
-        cfg.update(d=30, n=64, rx=100, rz=300, eps=1e-8, ell=110, seed=1003)
+        cfg.update(CFG3)
     elif args.config == "1":
-        cfg.update(d=10, n=20, rx=10, rz=40, eps=1e-4, ell=15, seed=1001)
+        cfg.update(CFG1)
     cfg["seed"] = cfg["seed"] + 1000 * rank  # independent tensor per rank
     y = build_input(P, ctx, cfg)
     ranks = [cfg["ell"]] * (cfg["d"] - 1)
@@ -350,14 +396,7 @@ def run_ours(args, world, rank, local):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        if args.config in ("1", "3"):
-            # the oracle on the full config (seconds on the host cores)
-            cpu = cpu_full_fixed(P, y, ranks, seed)
-        else:
-            res = cpu_sample(1)
-            sec, fl = res[0]
-            cpu = {"value": fl / sec / 1e12, "unit": "TFLOP/s", "cores": cpu_threads(), "kind": "port",
-                   "sample": sample_desc(), "seconds": sec}
+        cpu = cpu_full_fixed(P, y, ranks, seed, cfg, args)
 
     if rank == 0:
         line = {
@@ -436,24 +475,17 @@ def total_bytes(y):
     return 8 * y.shape()[2]
 
 
-def _oracle():
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    import py_oracle as O
-    return O
-
-
-def cpu_full_fixed(P, y, ranks, seed):
-    """The CPU oracle (reference restatement, all host threads) on the FULL config input."""
+def cpu_full_fixed(P, y, ranks, seed, cfg, args):
+    """cpu_baseline: the CPU oracle (reference restatement, OpenBLAS backend, all host
+    threads) on the FULL config input (downloaded from the device), one round."""
     O = _oracle()
-    n, r, _ = y.shape()
-    x = O.TT.from_flat(len(n), n, r, y.flat())
-    sec = C.c_double()
-    fl = C.c_uint64()
-    O._check(O.lib().ttro_time_round_fixed_krp(x._h, O._i64(ranks), C.c_int64(len(ranks)), C.c_uint64(seed),
-                                               C.c_int(O.PHILOX), C.byref(sec), C.byref(fl)))
-    return {"value": fl.value / sec.value / 1e12, "unit": "TFLOP/s", "cores": cpu_threads(), "kind": "port",
-            "sample": "the full config: round_fixed_krp on the same input, CPU oracle, wall clock around the call",
-            "seconds": sec.value, "ms_per_round": sec.value * 1e3}
+    threads = cpu_threads(args)
+    with O.backend_scope("blas", threads):
+        n, r, _ = y.shape()
+        x = O.TT.from_flat(len(n), n, r, y.flat())
+        sec, fl = cpu_round(O, x, ranks, seed)
+    return {"value": fl / sec / 1e12, "unit": "TFLOP/s", "cores": threads, "kind": "port",
+            "sample": cpu_desc(cfg, threads), "seconds": sec, "ms_per_round": sec * 1e3, "same_config": True}
 
 
 ADAPTIVE = {

@@ -18,6 +18,16 @@
  *   ttr_krp_partial_contractions              krp_partial_contractions_rl + draw_gaussian_factors
  *                                                                   include/ttround/sketch.hpp:25-26,47-48
  *   ttr_counters / ttr_counters_reset         flops::counters/reset include/ttround/flops.hpp:12-25
+ *   ttr_tt_upload_cores                       TTTensor(std::vector<Core>) include/ttround/tensor.hpp:63 (checks of tensor.cpp:66-79)
+ *   ttr_tt_random_gaussian                    random_gaussian_tt    include/ttround/tensor.hpp:111 (reference stream)
+ *   ttr_dot                                   dot                   include/ttround/tensor.hpp:119
+ *   ttr_stream_*                              GaussianStream        include/ttround/rng.hpp:12-35
+ *   ttr_draw_gaussian_factors                 draw_gaussian_factors include/ttround/sketch.hpp:25-26 (GaussianFactorSet :13-22)
+ *   ttr_append_gaussian_columns               append_gaussian_columns include/ttround/sketch.hpp:29
+ *   ttr_krp_partial_contractions_rl           krp_partial_contractions_rl include/ttround/sketch.hpp:47-48 (PartialContractionSet :35-44)
+ *   ttr_append_krp_contractions               append_krp_contractions include/ttround/sketch.hpp:52-53
+ *   ttr_generate_residual_sketch              generate_residual_sketch include/ttround/round_rand.hpp:37-39
+ *   ttr_residual_norm_estimate                residual_norm_estimate include/ttround/sketch.hpp:67
  *
  * Conventions
  *  - Every function returns ttr_status. 0 = success; 1..15 = the reference's
@@ -129,7 +139,25 @@ ttr_status ttr_tt_read_ttf1(ttr_ctx* ctx, const char* path, ttr_tt** out);
 ttr_status ttr_tt_write_ttf1(ttr_ctx* ctx, const ttr_tt* tt, const char* path);
 ttr_status ttr_tt_destroy(ttr_tt* tt);
 
+/* TTTensor(std::vector<Core>) (tensor.hpp:63): one host buffer per core
+ * (core k: r_left[k] x n[k] x r_right[k], reference layout). Checks in the
+ * reference's order (tensor.cpp:20-30, 66-79): EmptyCoreList (d < 1),
+ * InvalidArgument (a non-positive dimension), BoundaryRankNotOne,
+ * RankChainMismatch, InvalidArgument "core entries must be finite" (a device
+ * scan of every core). ttr_tt_upload, ttr_tt_from_device, ttr_tt_read_ttf1
+ * and ttr_batch_upload run the same finiteness scan. */
+ttr_status ttr_tt_upload_cores(ttr_ctx* ctx, int64_t d, const int64_t* r_left, const int64_t* n,
+                               const int64_t* r_right, const double* const* host_cores, ttr_tt** out);
+
 /* ---- construction / TT arithmetic --------------------------------------- */
+/* random_gaussian_tt (tensor.cpp:217-242): cores i.i.d. N(0, 1/(r_{k-1} n_k r_k))
+ * from the reference's xoshiro256++ stream (bitwise), drawn on the host and
+ * uploaded. InvalidRankChain on a bad chain, as the reference. */
+ttr_status ttr_tt_random_gaussian(ttr_ctx* ctx, int64_t d, const int64_t* n, const int64_t* r, uint64_t seed,
+                                  ttr_tt** out);
+/* dot (tensor.cpp:244-256): <a, b> by the core-contraction sweep (device GEMMs).
+ * ModeSizeMismatch if the mode sizes differ. */
+ttr_status ttr_dot(ttr_ctx* ctx, const ttr_tt* a, const ttr_tt* b, double* out);
 ttr_status ttr_tt_random_philox(ttr_ctx* ctx, int64_t d, const int64_t* n, const int64_t* r,
                                 uint64_t seed, ttr_tt** out);
 ttr_status ttr_tt_formal_sum(ttr_ctx* ctx, const ttr_tt* const* terms, int count, ttr_tt** out);
@@ -197,6 +225,56 @@ ttr_status ttr_estimate_norm_krp(ttr_ctx* ctx, const ttr_tt* tt, int64_t width, 
 ttr_status ttr_krp_partial_contractions(ttr_ctx* ctx, const ttr_tt* tt, int64_t start_mode,
                                         int64_t cols, const double* host_factors, uint64_t seed,
                                         int64_t col0, double* host_w);
+/* ---- the reference's sketch objects (sketch.hpp:13-67) -------------------
+ * ttr_stream = GaussianStream (rng.hpp:12-35). TTR_RNG_XOSHIRO: the
+ * reference's sequential xoshiro256++/Box-Muller stream, bitwise (host state;
+ * factors drawn on the host in the reference's order and uploaded).
+ * TTR_RNG_PHILOX: the counter-based device generator; its state is the next
+ * global KRP column, so a draw of c columns is Omega_k(:, next:next+c) for
+ * every mode k and the stream advances by c.
+ * ttr_factors = GaussianFactorSet (device-resident Omega_start..Omega_d,
+ * n_k x cols each). ttr_contractions = PartialContractionSet (device-resident
+ * W_start..W_d, r_{k-1} x cols_k each; after appends from a later start mode
+ * the lower modes keep their width, sketch.hpp:33-34). Downloads are
+ * column-major host copies. Errors follow the reference: InvalidArgument
+ * (start mode outside [2, d], cols < 1, append before the start mode, block
+ * < 1, k outside [1, d)), ModeSizeMismatch (factor rows != mode sizes). */
+typedef struct ttr_stream ttr_stream;
+typedef struct ttr_factors ttr_factors;
+typedef struct ttr_contractions ttr_contractions;
+ttr_status ttr_stream_create(uint64_t seed, int rng_mode, ttr_stream** out);
+ttr_status ttr_stream_destroy(ttr_stream* stream);
+ttr_status ttr_draw_gaussian_factors(ttr_ctx* ctx, const ttr_tt* tt, int64_t start_mode, int64_t cols,
+                                     ttr_stream* stream, ttr_factors** out);
+ttr_status ttr_append_gaussian_columns(ttr_ctx* ctx, ttr_factors* factors, int64_t extra, ttr_stream* stream);
+/* Factors from host matrices (Omega_start.., rows[q] x cols each, concatenated). */
+ttr_status ttr_factors_upload(ttr_ctx* ctx, int64_t start_mode, int64_t nmodes, const int64_t* rows, int64_t cols,
+                              const double* host, ttr_factors** out);
+ttr_status ttr_factors_shape(const ttr_factors* factors, int64_t* start_mode, int64_t* nmodes, int64_t* cols);
+ttr_status ttr_factors_download(ttr_ctx* ctx, const ttr_factors* factors, int64_t mode, double* host);
+ttr_status ttr_factors_destroy(ttr_factors* factors);
+ttr_status ttr_krp_partial_contractions_rl(ttr_ctx* ctx, const ttr_tt* tt, const ttr_factors* factors,
+                                           ttr_contractions** out);
+ttr_status ttr_append_krp_contractions(ttr_ctx* ctx, ttr_contractions* set, const ttr_tt* tt,
+                                       const ttr_factors* fresh);
+/* start_mode / number of modes of the set; rows and cols of W_mode (may be NULL). */
+ttr_status ttr_contractions_shape(const ttr_contractions* set, int64_t mode, int64_t* start_mode, int64_t* nmodes,
+                                  int64_t* rows, int64_t* cols);
+ttr_status ttr_contractions_download(ttr_ctx* ctx, const ttr_contractions* set, int64_t mode, double* host);
+ttr_status ttr_contractions_destroy(ttr_contractions* set);
+/* generate_residual_sketch (round_rand.cpp:80-94): z is the rows x z_cols
+ * vertical unfolding (z_cols = r_k), q the rows x q_cols current basis; draws
+ * fresh factors for modes k+1..d from `stream` and appends their contractions
+ * to `w` when W_{k+1} lacks q_cols + b columns; returns in host_s (rows x b)
+ * S = z W_{k+1}(:, q_cols : q_cols+b) - q (q^T S). */
+ttr_status ttr_generate_residual_sketch(ttr_ctx* ctx, const ttr_tt* tt, int64_t rows, int64_t z_cols,
+                                        const double* host_z, int64_t q_cols, const double* host_q,
+                                        ttr_contractions* w, int64_t k, int64_t b, ttr_stream* stream,
+                                        double* host_s);
+/* residual_norm_estimate (sketch.cpp:121-124): ||S||_F / sqrt(block). */
+ttr_status ttr_residual_norm_estimate(ttr_ctx* ctx, int64_t rows, int64_t cols, const double* host_s, int64_t block,
+                                      double* out);
+
 /* Omega_mode(:, col0:col0+cols) drawn on the device (Philox mode). */
 ttr_status ttr_philox_factor(ttr_ctx* ctx, uint64_t seed, int64_t mode, int64_t rows, int64_t cols,
                              int64_t col0, double* host_out);

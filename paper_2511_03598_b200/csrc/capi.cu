@@ -6,63 +6,12 @@
 
 #include "common.cuh"
 #include "tt_round.h"
+#include "capi_util.h"
 
 using namespace ttr;
+using namespace ttr::capi;
 
-namespace {
-thread_local std::string g_last_error;
-
-template <typename F>
-ttr_status guard(F&& f) {
-    try {
-        f();
-        return TTR_OK;
-    } catch (const Error& e) {
-        g_last_error = e.what();
-        return e.status;
-    } catch (const std::bad_alloc& e) {
-        g_last_error = std::string("host allocation failed: ") + e.what();
-        return TTR_ERR_OUT_OF_MEMORY;
-    } catch (const std::exception& e) {
-        g_last_error = std::string("internal: ") + e.what();
-        return TTR_ERR_INTERNAL;
-    }
-}
-
-// Entry points bound to a context run on its device (the caller's current
-// device may be another one, e.g. a second context in the same process).
-template <typename F>
-ttr_status guard_ctx(ttr_ctx* ctx, F&& f);
-
-void need(bool ok, const char* what) {
-    if (!ok) throw Error(TTR_ERR_INVALID_ARGUMENT, std::string("InvalidArgument: ") + what);
-}
-
-template <typename F>
-ttr_status guard_ctx(ttr_ctx* ctx, F&& f) {
-    return guard([&] {
-        if (ctx) {
-            int cur = -1;
-            TTR_CUDA(cudaGetDevice(&cur));
-            if (cur != ctx->c.device) TTR_CUDA(cudaSetDevice(ctx->c.device));
-        }
-        f();
-    });
-}
-
-std::vector<i64> vec(const int64_t* p, int64_t n) { return std::vector<i64>(p, p + n); }
-
-ttr_tt* wrap(std::unique_ptr<TTDev> t) {
-    auto* o = new ttr_tt;
-    o->t = std::move(t);
-    return o;
-}
-
-void check_same_ctx(ttr_ctx* ctx, const ttr_tt* t) {
-    need(ctx && t && t->t, "null handle");
-    need(t->t->ctx == &ctx->c, "tensor belongs to another context");
-}
-}  // namespace
+thread_local std::string g_last_error;  // declared in capi_util.h
 
 extern "C" {
 
@@ -148,7 +97,7 @@ ttr_status ttr_tt_upload(ttr_ctx* ctx, int64_t d, const int64_t* n, const int64_
         need(n && r && host, "null argument");
         auto t = std::make_unique<TTDev>(ctx->c, vec(n, d), vec(r, d + 1));
         t->upload(host);
-        TTR_CUDA(cudaStreamSynchronize(ctx->c.stream));
+        check_finite(ctx->c, *t);  // TTTensor ctor scan (tensor.cpp:75-78); synchronises
         *out = wrap(std::move(t));
     });
 }
@@ -164,6 +113,7 @@ ttr_status ttr_tt_from_device(ttr_ctx* ctx, int64_t d, const int64_t* n, const i
                                      ctx->c.stream));
             o += t->core_size(k);
         }
+        check_finite(ctx->c, *t);
         *out = wrap(std::move(t));
     });
 }
@@ -248,7 +198,7 @@ ttr_status ttr_tt_read_ttf1(ttr_ctx* ctx, const char* path, ttr_tt** out) {
         if (std::fread(host.data(), sizeof(double), host.size(), f) != host.size())
             fail(Errc::IoError, "unexpected end of TTF1 file");
         t->upload(host.data());
-        TTR_CUDA(cudaStreamSynchronize(ctx->c.stream));  // host buffer lifetime
+        check_finite(ctx->c, *t);  // synchronises (host buffer lifetime); read_ttf1 builds a TTTensor
         *out = wrap(std::move(t));
     });
 }
@@ -643,6 +593,8 @@ ttr_status ttr_batch_upload(ttr_ctx* ctx, int64_t batch, int64_t d, const int64_
         if (d < 1) fail(Errc::EmptyCoreList, "TT tensor needs at least one core");
         auto t = std::make_unique<TTBatch>(ctx->c, batch, vec(n, d), vec(r, d + 1));
         const i64 tot = t->total();
+        // padding between cores is zeroed so one scan covers the whole batch
+        TTR_CUDA(cudaMemsetAsync(t->buf.p, 0, sizeof(double) * t->stride * batch, ctx->c.stream));
         for (i64 b = 0; b < batch; ++b) {
             i64 o = 0;
             for (i64 k = 0; k < d; ++k) {
@@ -651,7 +603,8 @@ ttr_status ttr_batch_upload(ttr_ctx* ctx, int64_t batch, int64_t d, const int64_
                 o += t->core_size(k);
             }
         }
-        TTR_CUDA(cudaStreamSynchronize(ctx->c.stream));
+        if (!all_finite(ctx->c, {{t->buf.p, static_cast<std::size_t>(t->stride * batch)}}))
+            fail(Errc::InvalidArgument, "core entries must be finite");
         auto* o = new ttr_batch;
         o->t = std::move(t);
         *out = o;

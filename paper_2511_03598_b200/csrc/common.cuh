@@ -212,6 +212,9 @@ void axpy_matrix(Ctx& c, i64 rows, i64 cols, double alpha, const double* x, i64 
 // Deterministic Frobenius norm of a rows x cols matrix; result stays on device.
 void frob_norm_sq(Ctx& c, i64 rows, i64 cols, const double* a, i64 lda, double* d_out);
 double frob_norm(Ctx& c, i64 rows, i64 cols, const double* a, i64 lda);
+// true iff every entry of every (pointer, count) span is finite (one
+// synchronisation; the tensor.cpp:75-78 finiteness scan)
+bool all_finite(Ctx& c, const std::vector<std::pair<const double*, std::size_t>>& spans);
 void random_normal(Ctx& c, std::uint64_t seed, std::uint32_t stream_tag, double* out, std::size_t count, double sigma);
 // out[row_off + i, j, col_off + g] = src(i, j, g) (formal-sum block placement)
 void place_block(Ctx& c, const double* src, i64 rl, i64 n, i64 rr, double* dst, i64 RL, i64 RR, i64 row_off, i64 col_off);

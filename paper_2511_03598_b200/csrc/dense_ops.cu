@@ -3,6 +3,8 @@
 // core generation and formal-sum block placement.
 #include <algorithm>
 
+#include <cstring>
+
 #include "common.cuh"
 
 extern "C" {
@@ -283,6 +285,47 @@ void frob_norm_sq(Ctx& c, i64 rows, i64 cols, const double* a, i64 lda, double* 
     sum_partials<<<1, kThreads, 0, c.stream>>>(partial, kNormBlocks, d_out);
     TTR_CUDA(cudaGetLastError());
     c.launched(2);
+}
+
+// Finiteness scan of the TTTensor constructor (tensor.cpp:75-78): any NaN or
+// +-Inf among count entries sets the flag. HBM-bound, one pass, 16-byte loads.
+__global__ void nonfinite_kernel(const double* p, i64 count, unsigned int* flag) {
+    unsigned int bad = 0;
+    const i64 pairs = count / 2;
+    const double2* p2 = reinterpret_cast<const double2*>(p);
+    for (i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; i < pairs;
+         i += static_cast<i64>(gridDim.x) * blockDim.x) {
+        const double2 v = __ldcs(p2 + i);
+        bad |= !isfinite(v.x) | !isfinite(v.y);
+    }
+    if ((count & 1) && blockIdx.x == 0 && threadIdx.x == 0) bad |= !isfinite(p[count - 1]);
+    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1u);
+}
+
+bool all_finite(Ctx& c, const std::vector<std::pair<const double*, std::size_t>>& spans) {
+    unsigned int* flag = reinterpret_cast<unsigned int*>(dalloc(c, 1));
+    TTR_CUDA(cudaMemsetAsync(flag, 0, sizeof(unsigned int), c.stream));
+    for (const auto& sp : spans) {
+        const double* p = sp.first;
+        std::size_t count = sp.second;
+        if (!count) continue;
+        if (reinterpret_cast<std::uintptr_t>(p) % 16 != 0) {  // scan the first entry alone, the rest aligned
+            nonfinite_kernel<<<1, 32, 0, c.stream>>>(p, 1, flag);
+            c.launched();
+            ++p;
+            --count;
+            if (!count) continue;
+        }
+        nonfinite_kernel<<<grid_for(c, (count + 1) / 2), kThreads, 0, c.stream>>>(p, static_cast<i64>(count), flag);
+        TTR_CUDA(cudaGetLastError());
+        c.launched();
+    }
+    TTR_CUDA(cudaMemcpyAsync(c.host_scalars, flag, sizeof(unsigned int), cudaMemcpyDeviceToHost, c.stream));
+    TTR_CUDA(cudaStreamSynchronize(c.stream));
+    unsigned int h = 0;
+    std::memcpy(&h, c.host_scalars, sizeof(unsigned int));
+    dfree(c, flag);
+    return h == 0;
 }
 
 double frob_norm(Ctx& c, i64 rows, i64 cols, const double* a, i64 lda) {

@@ -56,6 +56,15 @@ struct AdaptiveCfg {
 };
 
 std::unique_ptr<TTDev> copy_tt(Ctx& c, const TTDev& t);
+// TTTensor constructor's finiteness scan (tensor.cpp:75-78): InvalidArgument
+// "core entries must be finite" on any NaN/Inf core entry.
+void check_finite(Ctx& c, const TTDev& t);
+// dot (tensor.cpp:244-256): <a, b> by the core-contraction sweep (DMMA GEMMs).
+double dot(Ctx& c, const TTDev& a, const TTDev& b);
+// random_gaussian_tt (tensor.cpp:217-242) from the reference's xoshiro stream
+// (host draws, bitwise the reference), uploaded.
+std::unique_ptr<TTDev> random_gaussian_tt(Ctx& c, const std::vector<i64>& n, const std::vector<i64>& r,
+                                          std::uint64_t seed);
 std::unique_ptr<TTDev> random_philox_tt(Ctx& c, const std::vector<i64>& n, const std::vector<i64>& r, std::uint64_t seed);
 std::unique_ptr<TTDev> formal_sum(Ctx& c, const std::vector<const TTDev*>& terms);
 std::unique_ptr<TTDev> kernel_sum_tt(Ctx& c, i64 d, i64 n, i64 r, i64 terms, double ell, std::uint64_t seed);
