@@ -132,6 +132,8 @@ ttr_status ttr_tt_download(ttr_ctx* ctx, const ttr_tt* tt, double* host_cores);
 /* Overwrite the cores of an existing tensor from host memory (same shape). */
 ttr_status ttr_tt_copy_from_host(ttr_ctx* ctx, ttr_tt* tt, const double* host_cores);
 ttr_status ttr_tt_core_ptr(const ttr_tt* tt, int64_t k, const double** dev_ptr);
+/* Core k (0-based) copied to the host (r_{k} x n_k x r_{k+1}, reference layout). */
+ttr_status ttr_tt_download_core(ttr_ctx* ctx, const ttr_tt* tt, int64_t k, double* host);
 /* TTF1 files (io.hpp / io.cpp:27-76, the reference's binary format): read
  * straight into a device tensor / write a device tensor. IoError on open,
  * magic, size or truncation problems; BoundaryRankNotOne on a bad rank chain. */

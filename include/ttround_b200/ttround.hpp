@@ -13,13 +13,25 @@
 //   estimate_norm_krp                       sketch.hpp:63
 //   norm_exact / relative_error / formal_sum / scaled   tensor.hpp:172-191
 //   flops::counters / reset                 flops.hpp:12-25
+//   Core / TTTensor(std::vector<Core>)      tensor.hpp:17-63
+//   random_gaussian_tt / dot                tensor.hpp:111,119
+//   GaussianStream                          rng.hpp:12-35
+//   GaussianFactorSet / draw_gaussian_factors / append_gaussian_columns   sketch.hpp:13-29
+//   PartialContractionSet / krp_partial_contractions_rl / append_krp_contractions   sketch.hpp:35-53
+//   generate_residual_sketch                round_rand.hpp:37-39
+//   residual_norm_estimate                  sketch.hpp:67
 //
 // Differences a caller sees: cores live in HBM (construct from host cores,
 // read back with cores()); every call takes an optional Context (default: a
-// per-thread context on device 0); the sketch generator defaults to the
-// counter-based Philox stream (RngMode::Xoshiro reproduces the reference's
-// sequential stream). Errors are rethrown as ttround::Error with the same
-// Errc kinds the reference uses.
+// per-thread context on device 0); matrices are the small column-major
+// ttround::Matrix below instead of Eigen::MatrixXd. The sketch generator
+// defaults to RngMode::Xoshiro, the reference's own sequential stream, so a
+// drop-in call round_fixed_krp(x, ranks, seed) draws exactly the reference's
+// Omega; RngMode::Philox selects the counter-based device generator (no host
+// draws; required by the CUDA-graph plans). Errors are rethrown as
+// ttround::Error with the same Errc kinds the reference uses; failures of the
+// device itself (CUDA, out of memory, NCCL, no device) are ttround::DeviceError
+// (Errc::DeviceFailure, a kind the reference does not have).
 #pragma once
 
 #include <cstdint>
@@ -39,6 +51,7 @@ enum class Errc {
     RankChainMismatch, BoundaryRankNotOne, EmptyCoreList, IndexOutOfRange, DenseTooLarge,
     ModeSizeMismatch, EmptyTermList, InvalidRankChain, SVDFailure, InvalidRanks,
     NotLeftOrthogonal, InvalidGrid, Breakdown, InvalidArgument, IoError,
+    DeviceFailure,  // not in the reference: CUDA / out-of-memory / NCCL / no-device failures
 };
 
 class Error : public std::runtime_error {
@@ -53,16 +66,76 @@ private:
     int status_;
 };
 
+//! A failure of the device rather than of the caller's input: status() is the
+//! raw ttr_status (TTR_ERR_CUDA, _OUT_OF_MEMORY, _NCCL, _INTERNAL, _NO_DEVICE).
+class DeviceError : public Error {
+public:
+    DeviceError(const std::string& what, int status) : Error(Errc::DeviceFailure, what, status) {}
+    bool out_of_memory() const noexcept { return status() == TTR_ERR_OUT_OF_MEMORY; }
+};
+
 [[noreturn]] inline void fail(Errc code, const std::string& what) { throw Error(code, what); }
 
 inline void check(ttr_status s) {
     if (s == TTR_OK) return;
     const std::string msg = ttr_last_error();
     if (s >= 1 && s <= 15) throw Error(static_cast<Errc>(s - 1), msg, s);
-    throw Error(Errc::InvalidArgument, "device failure: " + msg, s);  // CUDA / OOM / no device
+    throw DeviceError(msg, s);
 }
 
 enum class RngMode : int { Xoshiro = TTR_RNG_XOSHIRO, Philox = TTR_RNG_PHILOX };
+
+//! Column-major dense matrix (the reference's Eigen::MatrixXd at this boundary).
+struct Matrix {
+    Index rows_ = 0, cols_ = 0;
+    std::vector<double> a;
+    Matrix() = default;
+    Matrix(Index r, Index c) : rows_(r), cols_(c), a(static_cast<std::size_t>(r * c), 0.0) {}
+    Index rows() const noexcept { return rows_; }
+    Index cols() const noexcept { return cols_; }
+    double& operator()(Index i, Index j) { return a[static_cast<std::size_t>(i + j * rows_)]; }
+    double operator()(Index i, Index j) const { return a[static_cast<std::size_t>(i + j * rows_)]; }
+    double* data() noexcept { return a.data(); }
+    const double* data() const noexcept { return a.data(); }
+};
+
+//! A 3-way TT core r_left x n x r_right on the host, stored as the column-major
+//! vertical unfolding: element (i, j, g) at g*r_left*n + j*r_left + i
+//! (tensor.hpp:11-54). The TTTensor built from cores lives on the device.
+class Core {
+public:
+    Core(Index r_left, Index n, Index r_right)
+        : rl_(r_left), n_(n), rr_(r_right), data_(checked(r_left, n, r_right), 0.0) {}
+    Core(Index r_left, Index n, Index r_right, std::vector<double> entries)
+        : rl_(r_left), n_(n), rr_(r_right), data_(std::move(entries)) {
+        if (static_cast<Index>(data_.size()) != static_cast<Index>(checked(r_left, n, r_right)))
+            fail(Errc::InvalidArgument, "core entry count does not match shape");
+    }
+    static Core from_vertical(Index r_left, Index n, const Matrix& v) {
+        if (v.rows() != r_left * n) fail(Errc::InvalidArgument, "vertical unfolding shape mismatch");
+        return Core(r_left, n, v.cols(), v.a);
+    }
+    static Core from_horizontal(Index n, Index r_right, const Matrix& h) {
+        if (h.cols() != n * r_right) fail(Errc::InvalidArgument, "horizontal unfolding shape mismatch");
+        return Core(h.rows(), n, r_right, h.a);
+    }
+    Index r_left() const noexcept { return rl_; }
+    Index n() const noexcept { return n_; }
+    Index r_right() const noexcept { return rr_; }
+    Index size() const noexcept { return static_cast<Index>(data_.size()); }
+    double operator()(Index i, Index j, Index g) const { return data_[static_cast<std::size_t>(g * rl_ * n_ + j * rl_ + i)]; }
+    double& operator()(Index i, Index j, Index g) { return data_[static_cast<std::size_t>(g * rl_ * n_ + j * rl_ + i)]; }
+    const std::vector<double>& data() const noexcept { return data_; }
+    std::vector<double>& data() noexcept { return data_; }
+
+private:
+    static std::size_t checked(Index rl, Index n, Index rr) {
+        if (rl < 1 || n < 1 || rr < 1) fail(Errc::InvalidArgument, "core dimensions must be positive");
+        return static_cast<std::size_t>(rl * n * rr);
+    }
+    Index rl_, n_, rr_;
+    std::vector<double> data_;
+};
 
 class Context {
 public:
@@ -91,6 +164,22 @@ public:
         ttr_tt* t = nullptr;
         check(ttr_tt_upload(ctx.get(), static_cast<int64_t>(mode_sizes.size()), mode_sizes.data(), ranks.data(),
                             cores_concat.data(), &t));
+        h_.reset(t, &ttr_tt_destroy);
+    }
+    //! TTTensor(std::vector<Core>) (tensor.hpp:63): the constructor's checks
+    //! (tensor.cpp:66-79, incl. the finiteness scan, run on the device).
+    explicit TTTensor(const std::vector<Core>& cores, Context& ctx = Context::thread_default()) : ctx_(&ctx) {
+        std::vector<int64_t> rl, n, rr;
+        std::vector<const double*> ptrs;
+        for (const auto& c : cores) {
+            rl.push_back(c.r_left());
+            n.push_back(c.n());
+            rr.push_back(c.r_right());
+            ptrs.push_back(c.data().data());
+        }
+        ttr_tt* t = nullptr;
+        check(ttr_tt_upload_cores(ctx.get(), static_cast<int64_t>(cores.size()), rl.data(), n.data(), rr.data(),
+                                  ptrs.data(), &t));
         h_.reset(t, &ttr_tt_destroy);
     }
     TTTensor(ttr_tt* owned, Context& ctx) : h_(owned, &ttr_tt_destroy), ctx_(&ctx) {}
@@ -124,6 +213,15 @@ public:
         check(ttr_tt_download(ctx_->get(), h_.get(), out.data()));
         return out;
     }
+    //! Core k copied to the host (Core(k) of the reference, tensor.hpp:70).
+    Core core(Index k) const {
+        const auto n = mode_sizes();
+        const auto r = ranks();
+        if (k < 0 || k >= static_cast<Index>(n.size())) fail(Errc::IndexOutOfRange, "core index out of range");
+        std::vector<double> host(static_cast<std::size_t>(r[k] * n[k] * r[k + 1]));
+        check(ttr_tt_download_core(ctx_->get(), h_.get(), k, host.data()));
+        return Core(r[k], n[k], r[k + 1], std::move(host));
+    }
     ttr_tt* get() const { return h_.get(); }
     Context& context() const { return *ctx_; }
 
@@ -139,11 +237,11 @@ struct AdaptiveConfig {  // round_rand.hpp:18-25
     std::uint64_t seed = 0;
     std::optional<double> known_norm;
     std::optional<std::vector<Index>> max_rank_cap;
-    RngMode rng = RngMode::Philox;
+    RngMode rng = RngMode::Xoshiro;  // the reference's stream (Philox: device generator)
 };
 
 inline TTTensor round_fixed_krp(const TTTensor& tt, const std::vector<Index>& target_ranks, std::uint64_t seed,
-                                RngMode rng = RngMode::Philox) {
+                                RngMode rng = RngMode::Xoshiro) {
     ttr_tt* out = nullptr;
     check(ttr_round_fixed_krp(tt.context().get(), tt.get(), target_ranks.data(),
                               static_cast<int64_t>(target_ranks.size()), seed, static_cast<int>(rng), &out));
@@ -178,7 +276,7 @@ inline void write_ttf1(const TTTensor& tt, const std::string& path) {
 
 //! round_rand.hpp:49 round_rand_orth_tt: Rand-Orth with a Gaussian TT sketch.
 inline TTTensor round_rand_orth_tt(const TTTensor& tt, const std::vector<Index>& target_ranks, std::uint64_t seed,
-                                   RngMode rng = RngMode::Philox) {
+                                   RngMode rng = RngMode::Xoshiro) {
     ttr_tt* out = nullptr;
     check(ttr_round_rand_orth_tt(tt.context().get(), tt.get(), target_ranks.data(),
                                  static_cast<int64_t>(target_ranks.size()), seed, static_cast<int>(rng), &out));
@@ -205,7 +303,7 @@ struct TTSum {
 
 //! Adaptive rounding of a sum without the formal sum (sum_round.hpp:29).
 inline TTTensor round_sum_adaptive_krp(const TTSum& sum, double eps, double f_inc, std::uint64_t seed,
-                                       RngMode rng = RngMode::Philox) {
+                                       RngMode rng = RngMode::Xoshiro) {
     std::vector<const ttr_tt*> hs;
     for (const auto& t : sum.terms) hs.push_back(t.get());
     ttr_tt* out = nullptr;
@@ -228,7 +326,7 @@ inline TTTensor round_deterministic(const TTTensor& tt, const std::vector<Index>
     return TTTensor(out, tt.context());
 }
 
-inline double estimate_norm_krp(const TTTensor& tt, Index width, std::uint64_t seed, RngMode rng = RngMode::Philox) {
+inline double estimate_norm_krp(const TTTensor& tt, Index width, std::uint64_t seed, RngMode rng = RngMode::Xoshiro) {
     double v = 0.0;
     check(ttr_estimate_norm_krp(tt.context().get(), tt.get(), width, seed, static_cast<int>(rng), &v));
     return v;
@@ -259,6 +357,126 @@ inline TTTensor scaled(const TTTensor& tt, double alpha) {
     TTTensor out = formal_sum({tt});
     check(ttr_tt_scale(out.context().get(), out.get(), alpha));
     return out;
+}
+
+//! random_gaussian_tt (tensor.hpp:111): the reference's xoshiro stream, bitwise.
+inline TTTensor random_gaussian_tt(const std::vector<Index>& mode_sizes, const std::vector<Index>& ranks,
+                                   std::uint64_t seed, Context& ctx = Context::thread_default()) {
+    if (ranks.size() != mode_sizes.size() + 1) fail(Errc::InvalidRankChain, "rank chain length must be d+1");
+    ttr_tt* out = nullptr;
+    check(ttr_tt_random_gaussian(ctx.get(), static_cast<int64_t>(mode_sizes.size()), mode_sizes.data(), ranks.data(),
+                                 seed, &out));
+    return TTTensor(out, ctx);
+}
+
+//! dot (tensor.hpp:119): <a, b> by the core-contraction sweep.
+inline double dot(const TTTensor& a, const TTTensor& b) {
+    double v = 0.0;
+    check(ttr_dot(a.context().get(), a.get(), b.get(), &v));
+    return v;
+}
+
+//! GaussianStream (rng.hpp:12-35). Xoshiro: the reference's sequential stream;
+//! Philox: the device generator, whose state is the next global KRP column.
+class GaussianStream {
+public:
+    explicit GaussianStream(std::uint64_t seed, RngMode rng = RngMode::Xoshiro) {
+        ttr_stream* s = nullptr;
+        check(ttr_stream_create(seed, static_cast<int>(rng), &s));
+        h_.reset(s, &ttr_stream_destroy);
+    }
+    ttr_stream* get() const { return h_.get(); }
+
+private:
+    std::shared_ptr<ttr_stream> h_;
+};
+
+//! GaussianFactorSet (sketch.hpp:13-22): Omega_start..Omega_d, device-resident.
+class GaussianFactorSet {
+public:
+    GaussianFactorSet(ttr_factors* owned, Context& ctx) : h_(owned, &ttr_factors_destroy), ctx_(&ctx) {}
+    Index start_mode() const { return shape()[0]; }
+    Index cols() const { return shape()[2]; }
+    Index num_modes() const { return shape()[1]; }
+    //! Omega_k (n_k x cols) copied to the host.
+    Matrix at_mode(Index k, Index n_k) const {
+        Matrix m(n_k, cols());
+        check(ttr_factors_download(ctx_->get(), h_.get(), k, m.data()));
+        return m;
+    }
+    ttr_factors* get() const { return h_.get(); }
+    Context& context() const { return *ctx_; }
+
+private:
+    std::vector<Index> shape() const {
+        int64_t a = 0, b = 0, c = 0;
+        check(ttr_factors_shape(h_.get(), &a, &b, &c));
+        return {a, b, c};
+    }
+    std::shared_ptr<ttr_factors> h_;
+    Context* ctx_;
+};
+
+inline GaussianFactorSet draw_gaussian_factors(const TTTensor& tt, Index start_mode, Index cols,
+                                               GaussianStream& stream) {
+    ttr_factors* out = nullptr;
+    check(ttr_draw_gaussian_factors(tt.context().get(), tt.get(), start_mode, cols, stream.get(), &out));
+    return GaussianFactorSet(out, tt.context());
+}
+
+inline void append_gaussian_columns(GaussianFactorSet& set, Index extra, GaussianStream& stream) {
+    check(ttr_append_gaussian_columns(set.context().get(), set.get(), extra, stream.get()));
+}
+
+//! PartialContractionSet (sketch.hpp:35-44): W_start..W_d, device-resident.
+class PartialContractionSet {
+public:
+    PartialContractionSet(ttr_contractions* owned, Context& ctx) : h_(owned, &ttr_contractions_destroy), ctx_(&ctx) {}
+    Index start_mode() const {
+        int64_t s = 0;
+        check(ttr_contractions_shape(h_.get(), 0, &s, nullptr, nullptr, nullptr));
+        return s;
+    }
+    //! W_k (r_{k-1} x cols_k) copied to the host.
+    Matrix at_mode(Index k) const {
+        int64_t rows = 0, cols = 0;
+        check(ttr_contractions_shape(h_.get(), k, nullptr, nullptr, &rows, &cols));
+        Matrix m(rows, cols);
+        check(ttr_contractions_download(ctx_->get(), h_.get(), k, m.data()));
+        return m;
+    }
+    ttr_contractions* get() const { return h_.get(); }
+    Context& context() const { return *ctx_; }
+
+private:
+    std::shared_ptr<ttr_contractions> h_;
+    Context* ctx_;
+};
+
+inline PartialContractionSet krp_partial_contractions_rl(const TTTensor& tt, const GaussianFactorSet& factors) {
+    ttr_contractions* out = nullptr;
+    check(ttr_krp_partial_contractions_rl(tt.context().get(), tt.get(), factors.get(), &out));
+    return PartialContractionSet(out, tt.context());
+}
+
+inline void append_krp_contractions(PartialContractionSet& set, const TTTensor& tt, const GaussianFactorSet& fresh) {
+    check(ttr_append_krp_contractions(tt.context().get(), set.get(), tt.get(), fresh.get()));
+}
+
+//! generate_residual_sketch (round_rand.hpp:37-39).
+inline Matrix generate_residual_sketch(const TTTensor& tt, const Matrix& z, const Matrix& q, PartialContractionSet& w,
+                                       Index k, Index b, GaussianStream& stream) {
+    Matrix s(z.rows(), b > 0 ? b : 0);
+    check(ttr_generate_residual_sketch(tt.context().get(), tt.get(), z.rows(), z.cols(), z.data(), q.cols(),
+                                       q.cols() ? q.data() : nullptr, w.get(), k, b, stream.get(), s.data()));
+    return s;
+}
+
+//! residual_norm_estimate (sketch.hpp:67): ||S||_F / sqrt(block).
+inline double residual_norm_estimate(const Matrix& s, Index block, Context& ctx = Context::thread_default()) {
+    double v = 0.0;
+    check(ttr_residual_norm_estimate(ctx.get(), s.rows(), s.cols(), s.data(), block, &v));
+    return v;
 }
 
 namespace flops {

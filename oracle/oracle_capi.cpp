@@ -249,6 +249,31 @@ int ttro_krp_contractions(const ttro_tt* t, std::int64_t start_mode, std::int64_
         }
     });
 }
+// generate_residual_sketch (round_rand.cpp:80-94) after an initial contraction of
+// width w0 from mode 2 (the adaptive driver's sequence): S (rows x b) and the
+// widths of W_2..W_d afterwards.
+int ttro_residual_sketch(const ttro_tt* t, std::int64_t w0, std::uint64_t seed, int rng_mode, std::int64_t rows,
+                         std::int64_t zc, const double* z, std::int64_t qc, const double* q, std::int64_t k,
+                         std::int64_t b, double* s_out, std::int64_t* widths) {
+    return guard([&] {
+        FactorRng rng(static_cast<RngMode>(rng_mode), seed);
+        auto f = draw_gaussian_factors(t->tt, 2, w0, rng);
+        auto w = krp_partial_contractions_rl(t->tt, f);
+        Matrix zm(rows, zc), qm(rows, qc);
+        std::memcpy(zm.data(), z, sizeof(double) * static_cast<std::size_t>(rows * zc));
+        if (qc) std::memcpy(qm.data(), q, sizeof(double) * static_cast<std::size_t>(rows * qc));
+        Matrix s = generate_residual_sketch(t->tt, zm, qm, w, k, b, rng);
+        std::memcpy(s_out, s.data(), sizeof(double) * s.a.size());
+        for (std::size_t i = 0; i < w.w.size(); ++i) widths[i] = w.w[i].cols;
+    });
+}
+int ttro_residual_norm_estimate(std::int64_t rows, std::int64_t cols, const double* s, std::int64_t block, double* out) {
+    return guard([&] {
+        Matrix m(rows, cols);
+        if (rows > 0 && cols > 0) std::memcpy(m.data(), s, sizeof(double) * static_cast<std::size_t>(rows * cols));
+        *out = residual_norm_estimate(m, block);
+    });
+}
 int ttro_gaussian_matrix(std::int64_t rows, std::int64_t cols, std::uint64_t seed, double* out) {
     return guard([&] {
         auto m = gaussian_matrix(rows, cols, seed);

@@ -302,6 +302,25 @@ def krp_contractions(t: TT, factors: Sequence[np.ndarray], start_mode=2) -> List
     return res
 
 
+def residual_sketch(t: TT, w0: int, seed: int, rng: int, z: np.ndarray, q: np.ndarray, k: int, b: int):
+    """generate_residual_sketch (round_rand.cpp:80-94) after an initial width-w0
+    contraction from mode 2: returns (S, widths of W_2..W_d afterwards)."""
+    z = np.asfortranarray(z, dtype=np.float64)
+    q = np.asfortranarray(q, dtype=np.float64)
+    s = np.empty((z.shape[0], b), dtype=np.float64, order="F")
+    widths = (C.c_int64 * t.order())()
+    _check(lib().ttro_residual_sketch(t._h, C.c_int64(w0), C.c_uint64(seed), C.c_int(rng), C.c_int64(z.shape[0]),
+                                      C.c_int64(z.shape[1]), _dptr(z), C.c_int64(q.shape[1]),
+                                      _dptr(q) if q.size else None, C.c_int64(k), C.c_int64(b), _dptr(s), widths))
+    return s, list(widths)[:t.order() - 1]
+
+
+def residual_norm_estimate(s: np.ndarray, block: int) -> float:
+    s = np.asfortranarray(s, dtype=np.float64)
+    return _scalar(lib().ttro_residual_norm_estimate, C.c_int64(s.shape[0]), C.c_int64(s.shape[1]),
+                   _dptr(s) if s.size else None, C.c_int64(block))
+
+
 def set_backend(backend: str = "port", threads: int = 0) -> None:
     """Dense-kernel backend of the oracle: "port" (plain-loop restatement, the
     pinned default) or "blas" (the same algorithms on OpenBLAS/LAPACK: dgemm,

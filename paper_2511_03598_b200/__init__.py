@@ -193,20 +193,25 @@ class TTTensor:
 
     @staticmethod
     def from_cores(cores: Sequence[np.ndarray], ctx: Optional[Context] = None) -> "TTTensor":
-        """cores[k] of shape (r_{k-1}, n_k, r_k)."""
-        if len(cores) == 0:
-            raise TTRoundError(3, "EmptyCoreList: TT tensor needs at least one core")
+        """TTTensor(std::vector<Core>) (tensor.hpp:63): cores[k] of shape
+        (r_{k-1}, n_k, r_k); the constructor's checks (tensor.cpp:66-79, incl. the
+        finiteness scan) run in the library (ttr_tt_upload_cores)."""
+        ctx = ctx or default_context()
+        d = len(cores)
+        bufs = [np.ascontiguousarray(np.asarray(c, dtype=np.float64).transpose(2, 1, 0).reshape(-1)) for c in cores]
+        ptrs = (C.POINTER(C.c_double) * max(1, d))(*[_dptr(b) for b in bufs])
+        rl = [c.shape[0] for c in cores]
         n = [c.shape[1] for c in cores]
-        r = [cores[0].shape[0]] + [c.shape[2] for c in cores]
-        if cores[0].shape[0] != 1 or cores[-1].shape[2] != 1:
-            raise TTRoundError(2, "BoundaryRankNotOne: boundary TT ranks must be 1")
-        for k in range(len(cores) - 1):
-            if cores[k].shape[2] != cores[k + 1].shape[0]:
-                raise TTRoundError(1, f"RankChainMismatch: adjacent core ranks differ at position {k + 1}")
-        flat = np.concatenate([np.asarray(c, dtype=np.float64).transpose(2, 1, 0).reshape(-1) for c in cores])
-        if not np.all(np.isfinite(flat)):
-            raise TTRoundError(14, "InvalidArgument: core entries must be finite")
-        return TTTensor.from_flat(n, r, flat, ctx)
+        rr = [c.shape[2] for c in cores]
+        return TTTensor._new(ctx, lib().ttr_tt_upload_cores, ctx._h, C.c_int64(d), _i64(rl), _i64(n), _i64(rr), ptrs)
+
+    @staticmethod
+    def random_gaussian(mode_sizes: Sequence[int], ranks: Sequence[int], seed: int,
+                        ctx: Optional[Context] = None) -> "TTTensor":
+        """random_gaussian_tt (tensor.cpp:217-242): the reference's xoshiro stream, bitwise."""
+        ctx = ctx or default_context()
+        return TTTensor._new(ctx, lib().ttr_tt_random_gaussian, ctx._h, C.c_int64(len(mode_sizes)),
+                             _i64(mode_sizes), _i64(ranks), C.c_uint64(seed))
 
     @staticmethod
     def random_philox(mode_sizes: Sequence[int], ranks: Sequence[int], seed: int,
@@ -516,10 +521,131 @@ def estimate_norm_krp(tt: TTTensor, width: int, seed: int, rng: int = RNG_PHILOX
     return v.value
 
 
-def krp_partial_contractions_rl(tt: TTTensor, cols: int, factors: Optional[Sequence[np.ndarray]] = None,
-                                seed: int = 0, start_mode: int = 2, col0: int = 0) -> List[np.ndarray]:
-    """W_start..W_d (r_{k-1} x cols). `factors` = Omega_start..Omega_d (n_k x cols);
-    None draws Philox factors on the device for global columns col0..col0+cols."""
+def dot(a: TTTensor, b: TTTensor) -> float:
+    """dot (tensor.cpp:244-256) on the device."""
+    v = C.c_double()
+    _check(lib().ttr_dot(a.ctx._h, a._h, b._h, C.byref(v)))
+    return v.value
+
+
+class GaussianStream:
+    """GaussianStream (rng.hpp:12-35): RNG_XOSHIRO = the reference's sequential
+    stream (bitwise); RNG_PHILOX = the device generator (state: next global column)."""
+
+    def __init__(self, seed: int, rng: int = RNG_XOSHIRO):
+        self._h = C.c_void_p()
+        _check(lib().ttr_stream_create(C.c_uint64(seed), C.c_int(rng), C.byref(self._h)))
+
+    def __del__(self):
+        if getattr(self, "_h", None) and self._h.value and _lib is not None:
+            _lib.ttr_stream_destroy(self._h)
+            self._h = C.c_void_p()
+
+
+class GaussianFactorSet:
+    """GaussianFactorSet (sketch.hpp:13-22): device-resident Omega_start..Omega_d."""
+
+    def __init__(self, handle, ctx: Context, mode_sizes: Sequence[int]):
+        self._h, self.ctx, self._n = handle, ctx, list(mode_sizes)
+
+    def __del__(self):
+        if getattr(self, "_h", None) and self._h.value and _lib is not None and _ctx_alive(self):
+            _lib.ttr_factors_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def _shape(self):
+        a, b, c = C.c_int64(), C.c_int64(), C.c_int64()
+        _check(lib().ttr_factors_shape(self._h, C.byref(a), C.byref(b), C.byref(c)))
+        return a.value, b.value, c.value
+
+    @property
+    def start_mode(self) -> int:
+        return self._shape()[0]
+
+    def cols(self) -> int:
+        return self._shape()[2]
+
+    def at_mode(self, k: int) -> np.ndarray:
+        rows = self._n[k - 1]
+        out = np.empty(rows * self.cols(), dtype=np.float64)
+        _check(lib().ttr_factors_download(self.ctx._h, self._h, C.c_int64(k), _dptr(out)))
+        return out.reshape(self.cols(), rows).T.copy()
+
+
+def draw_gaussian_factors(tt: TTTensor, start_mode: int, cols: int, stream: GaussianStream) -> GaussianFactorSet:
+    out = C.c_void_p()
+    _check(lib().ttr_draw_gaussian_factors(tt.ctx._h, tt._h, C.c_int64(start_mode), C.c_int64(cols), stream._h,
+                                           C.byref(out)))
+    return GaussianFactorSet(out, tt.ctx, tt.mode_sizes())
+
+
+def append_gaussian_columns(factors: GaussianFactorSet, extra: int, stream: GaussianStream) -> None:
+    _check(lib().ttr_append_gaussian_columns(factors.ctx._h, factors._h, C.c_int64(extra), stream._h))
+
+
+class PartialContractionSet:
+    """PartialContractionSet (sketch.hpp:35-44): device-resident W_start..W_d."""
+
+    def __init__(self, handle, ctx: Context):
+        self._h, self.ctx = handle, ctx
+
+    def __del__(self):
+        if getattr(self, "_h", None) and self._h.value and _lib is not None and _ctx_alive(self):
+            _lib.ttr_contractions_destroy(self._h)
+            self._h = C.c_void_p()
+
+    @property
+    def start_mode(self) -> int:
+        s = C.c_int64()
+        _check(lib().ttr_contractions_shape(self._h, C.c_int64(0), C.byref(s), None, None, None))
+        return s.value
+
+    def at_mode(self, k: int) -> np.ndarray:
+        rows, cols = C.c_int64(), C.c_int64()
+        _check(lib().ttr_contractions_shape(self._h, C.c_int64(k), None, None, C.byref(rows), C.byref(cols)))
+        out = np.empty(max(1, rows.value * cols.value), dtype=np.float64)
+        _check(lib().ttr_contractions_download(self.ctx._h, self._h, C.c_int64(k), _dptr(out)))
+        return out[:rows.value * cols.value].reshape(cols.value, rows.value).T.copy()
+
+
+def append_krp_contractions(w: PartialContractionSet, tt: TTTensor, fresh: GaussianFactorSet) -> None:
+    _check(lib().ttr_append_krp_contractions(tt.ctx._h, w._h, tt._h, fresh._h))
+
+
+def generate_residual_sketch(tt: TTTensor, z: np.ndarray, q: np.ndarray, w: PartialContractionSet, k: int, b: int,
+                             stream: GaussianStream) -> np.ndarray:
+    """generate_residual_sketch (round_rand.cpp:80-94) on the device; z, q host matrices."""
+    z = np.asfortranarray(z, dtype=np.float64)
+    q = np.asfortranarray(q, dtype=np.float64)
+    rows = z.shape[0]
+    out = np.empty((rows, max(b, 0)), dtype=np.float64, order="F")
+    _check(lib().ttr_generate_residual_sketch(tt.ctx._h, tt._h, C.c_int64(rows), C.c_int64(z.shape[1]), _dptr(z),
+                                              C.c_int64(q.shape[1]), _dptr(q) if q.size else None, w._h,
+                                              C.c_int64(k), C.c_int64(b), stream._h, _dptr(out)))
+    return out
+
+
+def residual_norm_estimate(s: np.ndarray, block: int, ctx: Optional[Context] = None) -> float:
+    """residual_norm_estimate (sketch.cpp:121-124): ||S||_F / sqrt(block), on the device."""
+    ctx = ctx or default_context()
+    s = np.asfortranarray(s, dtype=np.float64)
+    v = C.c_double()
+    _check(lib().ttr_residual_norm_estimate(ctx._h, C.c_int64(s.shape[0]), C.c_int64(s.shape[1]),
+                                            _dptr(s) if s.size else None, C.c_int64(block), C.byref(v)))
+    return v.value
+
+
+def krp_partial_contractions_rl(tt: TTTensor, cols, factors: Optional[Sequence[np.ndarray]] = None,
+                                seed: int = 0, start_mode: int = 2, col0: int = 0):
+    """krp_partial_contractions_rl (sketch.cpp:67-78). With a GaussianFactorSet as the
+    second argument: the reference call, returning a device PartialContractionSet.
+    Otherwise the flat helper: W_start..W_d (r_{k-1} x cols) as host arrays, with
+    `factors` = Omega_start..Omega_d (n_k x cols) or None for device Philox factors of
+    global columns col0..col0+cols."""
+    if isinstance(cols, GaussianFactorSet):
+        out = C.c_void_p()
+        _check(lib().ttr_krp_partial_contractions_rl(tt.ctx._h, tt._h, cols._h, C.byref(out)))
+        return PartialContractionSet(out, tt.ctx)
     n, r, _ = tt.shape()
     d = len(n)
     if factors is not None:

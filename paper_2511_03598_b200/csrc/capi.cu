@@ -212,6 +212,17 @@ ttr_status ttr_tt_copy_from_host(ttr_ctx* ctx, ttr_tt* tt, const double* host) {
     });
 }
 
+ttr_status ttr_tt_download_core(ttr_ctx* ctx, const ttr_tt* tt, int64_t k, double* host) {
+    return guard_ctx(ctx, [&] {
+        check_same_ctx(ctx, tt);
+        need(host != nullptr, "null argument");
+        if (k < 0 || k >= tt->t->d()) fail(Errc::IndexOutOfRange, "core index out of range");
+        TTR_CUDA(cudaMemcpyAsync(host, tt->t->core(k), sizeof(double) * tt->t->core_size(k), cudaMemcpyDeviceToHost,
+                                 ctx->c.stream));
+        TTR_CUDA(cudaStreamSynchronize(ctx->c.stream));
+    });
+}
+
 ttr_status ttr_tt_core_ptr(const ttr_tt* tt, int64_t k, const double** ptr) {
     return guard([&] {
         need(tt && tt->t && ptr, "null argument");

@@ -94,3 +94,34 @@ def test_cpp_wrapper_runs_on_device(tmp_path):
     out = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     assert out.returncode == 0, out.stdout + out.stderr
     assert "wrapper ok" in out.stdout
+
+
+def _build_dropin(tmp_path):
+    import paper_2511_03598_b200 as P
+    exe = str(tmp_path / "dropin_vs_oracle")
+    libdir = os.path.dirname(P.LIB_PATH)
+    odir = os.path.join(ROOT, "oracle", "_build")
+    cmd = ["g++", "-std=c++17", "-O2", "-I", os.path.join(ROOT, "include"),
+           os.path.join(ROOT, "tests", "cpp", "dropin_vs_oracle.cpp"), "-L", libdir, "-lttround_b200",
+           "-L", odir, "-lttr_oracle", f"-Wl,-rpath,{libdir}", f"-Wl,-rpath,{odir}", "-o", exe]
+    subprocess.run(cmd, check=True)
+    return exe
+
+
+def test_dropin_vs_oracle_compiles_and_links(tmp_path):
+    """tests/cpp/dropin_vs_oracle.cpp (every mirrored entry point vs the oracle) builds."""
+    assert os.path.exists(_build_dropin(tmp_path))
+
+
+@pytest.mark.gpu
+def test_dropin_vs_oracle_runs_on_device(tmp_path):
+    """The C++ drop-in layer on the device equals the oracle entry point by entry point:
+    Core/TTTensor(vector<Core>), random_gaussian_tt (bitwise), dot, norm_exact, formal_sum,
+    scaled, GaussianStream/draw_gaussian_factors/append_gaussian_columns (bitwise, reference
+    stream), krp_partial_contractions_rl, append_krp_contractions, generate_residual_sketch,
+    residual_norm_estimate, round_fixed_krp / round_adaptive_krp / round_deterministic /
+    estimate_norm_krp (reference stream), and the constructor's error kinds."""
+    exe = _build_dropin(tmp_path)
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "dropin ok" in out.stdout

@@ -809,3 +809,100 @@ def test_counters_match_oracle(P, O, case):
         O.round_adaptive_krp(x, tolerance=tol, f_init=0.1, f_inc=f_inc, seed=7, rng=O.PHILOX)
     dev, ref = ctx.counters(), O.flops_get()
     assert (dev.gemm, dev.qr, dev.svd, dev.sketch) == (ref["gemm"], ref["qr"], ref["svd"], ref["sketch"])
+
+
+# ---- the reference's sketch-level API at the boundary (sketch.hpp:13-67, round_rand.hpp:37-39) ----
+
+@pytest.mark.parametrize("rng", [0, 1])
+def test_sketch_objects_match_oracle(P, O, rng):
+    """GaussianStream -> draw_gaussian_factors -> append_gaussian_columns (bitwise, both
+    generators: the reference stream continues across the calls, sketch.cpp:44-65; Philox
+    takes the set's next global columns), krp_partial_contractions_rl and
+    append_krp_contractions (1e-12, tests/test_sketch.cpp:54-77; the lower modes keep
+    their width, sketch.hpp:33-34; the kept columns are untouched by the append)."""
+    x = O.two_part_tt(6, 10, 4, 9, 1e-3, 3101)
+    xd = to_device(x)
+    st = P.GaussianStream(17, rng)
+    f = P.draw_gaussian_factors(xd, 2, 6, st)
+    P.append_gaussian_columns(f, 3, st)
+    if rng == 1:
+        first = O.draw_factors(x, 2, 6, 17, rng=rng)
+        extra = O.draw_factors(x, 2, 3, 17, rng=rng, col0=6)
+    else:  # one sequential stream: 5 factors of 10 x 6, then 5 blocks of 10 x 3, column-major
+        seq = O.gaussian_matrix(5 * 10 * 9, 1, 17).ravel()
+        first = [seq[q * 60:(q + 1) * 60].reshape(6, 10).T for q in range(5)]
+        extra = [seq[300 + q * 30:300 + (q + 1) * 30].reshape(3, 10).T for q in range(5)]
+    for k in range(2, 7):
+        assert np.array_equal(f.at_mode(k), np.hstack([first[k - 2], extra[k - 2]]))
+    w = P.krp_partial_contractions_rl(xd, f)
+    wref = O.krp_contractions(x, [f.at_mode(k) for k in range(2, 7)])
+    for k in range(2, 7):
+        assert np.abs(w.at_mode(k) - wref[k - 2]).max() <= 1e-12 * (1 + np.abs(wref[k - 2]).max())
+    before = {k: w.at_mode(k) for k in range(2, 7)}
+    fresh = P.draw_gaussian_factors(xd, 4, 4, st)
+    P.append_krp_contractions(w, xd, fresh)
+    wf = O.krp_contractions(x, [fresh.at_mode(k) for k in range(4, 7)], start_mode=4)
+    for k in range(2, 7):
+        got = w.at_mode(k)
+        assert np.array_equal(got[:, :9], before[k])
+        if k < 4:
+            assert got.shape[1] == 9
+        else:
+            assert got.shape[1] == 13
+            assert np.abs(got[:, 9:] - wf[k - 4]).max() <= 1e-12 * (1 + np.abs(wf[k - 4]).max())
+    with pytest.raises(P.TTRoundError) as e:
+        P.draw_gaussian_factors(xd, 1, 3, st)
+    assert e.value.code == "InvalidArgument"
+
+
+@pytest.mark.parametrize("rng", [0, 1])
+def test_generate_residual_sketch_matches_oracle(P, O, rng):
+    """generate_residual_sketch (round_rand.cpp:80-94): the fresh factors for modes
+    k+1..d come from the same stream position / global columns on both sides; S and the
+    grown widths match, and residual_norm_estimate equals ||S||/sqrt(b)."""
+    x = O.two_part_tt(6, 10, 4, 9, 1e-3, 3102)
+    xd = to_device(x)
+    st = P.GaussianStream(23, rng)
+    w = P.krp_partial_contractions_rl(xd, P.draw_gaussian_factors(xd, 2, 5, st))
+    c1 = x.cores()[1]
+    z = c1.reshape(c1.shape[0] * c1.shape[1], -1, order="F")  # V(X_2): (r_1 n) x r_2
+    w3 = w.at_mode(3)
+    q, _ = np.linalg.qr(z @ w3[:, :2])
+    s = P.generate_residual_sketch(xd, z, q, w, 2, 4, st)
+    s_ref, widths = O.residual_sketch(x, 5, 23, rng, z, q, 2, 4)
+    assert np.abs(s - s_ref).max() <= 1e-12 * (1 + np.abs(s_ref).max())
+    assert [w.at_mode(k).shape[1] for k in range(2, 7)] == widths
+    assert abs(P.residual_norm_estimate(s, 4) - O.residual_norm_estimate(s_ref, 4)) <= 1e-12 * (1 + np.linalg.norm(s))
+    with pytest.raises(P.TTRoundError) as e:
+        P.residual_norm_estimate(s, 0)
+    assert e.value.code == "InvalidArgument"
+
+
+def test_dot_random_gaussian_and_constructor_checks(P, O):
+    """dot (tensor.cpp:244-256) <= 1e-12; random_gaussian_tt from the reference stream is
+    bitwise the oracle's; TTTensor(vector<Core>) checks in the reference's order, including
+    the finiteness scan (tensor.cpp:66-79), also on the flat upload."""
+    modes, ranks = [6, 5, 7, 4], [1, 3, 5, 2, 1]
+    g = P.TTTensor.random_gaussian(modes, ranks, 99)
+    go = O.random_gaussian_tt(modes, ranks, 99)
+    assert np.array_equal(g.flat(), go.flat())
+    h = O.random_gaussian_tt(modes, [1, 2, 4, 3, 1], 5)
+    ref = O.dot(go, h)
+    assert abs(P.dot(g, to_device(h)) - ref) <= 1e-12 * O.norm_exact(go) * O.norm_exact(h)
+    with pytest.raises(P.TTRoundError) as e:
+        P.dot(g, to_device(O.random_gaussian_tt([6, 5, 7, 5], ranks, 1)))
+    assert e.value.code == "ModeSizeMismatch"
+    cases = [([], "EmptyCoreList"), ([np.ones((2, 3, 1))], "BoundaryRankNotOne"),
+             ([np.ones((1, 3, 2)), np.ones((3, 3, 1))], "RankChainMismatch"),
+             ([np.full((1, 3, 1), np.nan)], "InvalidArgument"), ([np.full((1, 3, 1), np.inf)], "InvalidArgument")]
+    for cores, code in cases:
+        with pytest.raises(P.TTRoundError) as e:
+            P.TTTensor.from_cores(cores)
+        assert e.value.code == code
+    flat = go.flat().copy()
+    flat[7] = np.inf
+    with pytest.raises(P.TTRoundError) as e:
+        P.TTTensor.from_flat(modes, ranks, flat)
+    assert e.value.code == "InvalidArgument"
+    ok = P.TTTensor.from_cores([np.ones((1, 2, 2)), np.ones((2, 2, 1))])
+    assert ok.ranks() == [1, 2, 1]
