@@ -308,11 +308,11 @@ def residual_sketch(t: TT, w0: int, seed: int, rng: int, z: np.ndarray, q: np.nd
     z = np.asfortranarray(z, dtype=np.float64)
     q = np.asfortranarray(q, dtype=np.float64)
     s = np.empty((z.shape[0], b), dtype=np.float64, order="F")
-    widths = (C.c_int64 * t.order())()
+    widths = (C.c_int64 * t.order)()
     _check(lib().ttro_residual_sketch(t._h, C.c_int64(w0), C.c_uint64(seed), C.c_int(rng), C.c_int64(z.shape[0]),
                                       C.c_int64(z.shape[1]), _dptr(z), C.c_int64(q.shape[1]),
                                       _dptr(q) if q.size else None, C.c_int64(k), C.c_int64(b), _dptr(s), widths))
-    return s, list(widths)[:t.order() - 1]
+    return s, list(widths)[:t.order - 1]
 
 
 def residual_norm_estimate(s: np.ndarray, block: int) -> float:
