@@ -66,11 +66,28 @@ def parse():
     ap.add_argument("--cpu-threads", type=int, default=0,
                     help="host threads of the CPU reference / cpu_baseline (default: all cores)")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--sharding", default="tensors", choices=["tensors", "columns", "rows"],
-                    help="N>1 on config 5b: independent tensor per rank (weak), or one tensor with "
-                         "column-sharded KRP sketch + NCCL all-gather and a replicated (columns) or "
-                         "row-sharded TSQR (rows) Rand-Orth sweep (strong)")
+    ap.add_argument("--sharding", default="tensor", choices=["tensor", "batch"],
+                    help="N>1 on config 5b: ONE tensor over the N GPUs (default; column-sharded KRP sketch + "
+                         "NCCL all-gather, row-sharded Rand-Orth sweep with an NVLink TSQR per mode; strong "
+                         "scaling), or an independent tensor per rank (batch; weak scaling)")
+    ap.add_argument("--local-ranks", type=int, default=0,
+                    help="run the sharded driver with this many ranks simulated on ONE GPU (same code and "
+                         "kernels as the NCCL run; a functional check, not a multi-GPU timing)")
     return ap.parse_args()
+
+
+def maybe_spawn(args):
+    """`bench.py --gpus N` (N > 1) started without a launcher re-executes itself under
+    torch.distributed.run with one rank per GPU (rendezvous on 127.0.0.1)."""
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "ours":
+        import socket
+        s = socket.socket()
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+        s.close()
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd))
 
 
 def dist_env():
@@ -636,88 +653,125 @@ def run_adaptive(args, world, rank, local):
         torch.distributed.destroy_process_group()
 
 
-def run_columns(args, world, rank, local):
-    """Config 5b, ONE tensor over N GPUs: column-sharded KRP sketch, NCCL all-gather of the W
-    slices, Rand-Orth sweep (replicated). Strong scaling; time = max over ranks."""
+def run_sharded(args, world, rank, local):
+    """Config 5b, ONE tensor over N GPUs (csrc/sharded.cu through
+    ttr_round_fixed_krp_sharded): column-sharded KRP sketch + NCCL all-gather of the
+    W slices, row-sharded Rand-Orth sweep with a TSQR per mode. Every rank holds a
+    replica of the input; the output stays sharded (rank p: the core slices J_p).
+    value = the job's algorithmic flops (one round_fixed_krp, the reference's
+    charges) / max-over-ranks time. Strong scaling."""
     import torch
     import paper_2511_03598_b200 as P
-    from paper_2511_03598_b200.distributed import round_fixed_krp_column_sharded, round_fixed_krp_row_sharded
-    rows_mode = args.sharding == "rows"
-    if world > 1:
-        import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
+    from paper_2511_03598_b200.distributed import Communicator, round_fixed_krp_sharded
+    import torch.distributed as dist
     torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
     ctx = P.Context(local, stream.cuda_stream)
     cfg = dict(CFG5B)
     y = build_input(P, ctx, cfg)  # identical replica on every rank
     ranks = [cfg["ell"]] * (cfg["d"] - 1)
+    seed = cfg["round_seed"]
+    # the job's work = one round_fixed_krp with the reference's charges
+    ctx.reset_counters()
+    o = P.round_fixed_krp(y, ranks, seed)
+    torch.cuda.synchronize()
+    flops_job = ctx.counters().total()
+    out_ranks = o.ranks()
+    del o
+    if args.local_ranks:
+        comm = Communicator.local(ctx, args.local_ranks)
+    elif world > 1:
+        comm = Communicator.from_torch(ctx)
+    else:
+        comm = Communicator.local(ctx, 1)
 
     def step():
-        if rows_mode:
-            return round_fixed_krp_row_sharded(y, ranks, 7), {"bounds": None}
-        return round_fixed_krp_column_sharded(y, ranks, 7)
+        loc, _ = round_fixed_krp_sharded(y, ranks, seed, comm, gather=False)
+        return loc
 
-    if rows_mode:
-        # algorithmic work of the job = one round_fixed_krp (the reference charges)
-        ctx.reset_counters()
-        o = P.round_fixed_krp(y, ranks, 7)
-        torch.cuda.synchronize()
-        flops_job = ctx.counters().total()
-        del o
     ctx.reset_counters()
-    out, info = step()
-    torch.cuda.synchronize()
-    cnt = ctx.counters()
-    flops_rank = cnt.total()
-    if not rows_mode:
-        # every rank's sketch slice + ONE sweep (the replicas are redundant)
-        sk = torch.tensor([float(cnt.sketch)], device="cuda", dtype=torch.float64)
-        if world > 1:
-            torch.distributed.all_reduce(sk)
-        flops_job = float(sk.item()) + (cnt.total() - cnt.sketch)
-    out_ranks = out.ranks()
-    del out
+    l0 = ctx.kernel_launches()
+    step()
+    launches_per_step = ctx.kernel_launches() - l0
+    flops_rank = ctx.counters().total()
     for _ in range(args.warmup):
-        o, _ = step()
-        del o
+        step()
     torch.cuda.synchronize()
     if world > 1:
-        torch.distributed.barrier()
+        dist.barrier()
+    torch.cuda.synchronize()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     l0 = ctx.kernel_launches()
     with ClockSampler(local) as clk:
         e0.record(stream)
         for _ in range(args.steps):
-            o, _ = step()
-            del o
+            step()
         e1.record(stream)
         torch.cuda.synchronize()
     launches = ctx.kernel_launches() - l0
     ms = e0.elapsed_time(e1) / args.steps
     if world > 1:
         t = torch.tensor([ms], device="cuda")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
+    value = flops_job / (ms * 1e-3) / 1e12
+
+    e2e = None
+    if not args.no_e2e:
+        # through the API with host buffers: H2D of this rank's input replica from pinned
+        # memory, the sharded round, D2H of this rank's output shard
+        n_, r_, total = y.shape()
+        host_in = torch.empty(total, dtype=torch.float64, pin_memory=True)
+        P._check(P.lib().ttr_tt_download(ctx._h, y._h, C.c_void_p(host_in.data_ptr())))
+        reps = max(1, min(args.steps, 3))
+        times, d2h = [], 0
+        for it in range(reps + 1):
+            if world > 1:
+                dist.barrier()
+            t0 = time.perf_counter()
+            P._check(P.lib().ttr_tt_copy_from_host(ctx._h, y._h, C.c_void_p(host_in.data_ptr())))
+            loc = step()
+            d2h = 0
+            for lt in loc:
+                if lt is not None:
+                    f = lt.flat()
+                    d2h += 8 * f.size
+            dt = time.perf_counter() - t0
+            if it > 0:
+                times.append(dt)
+        e2e_ms = sum(times) / len(times) * 1e3
+        if world > 1:
+            t = torch.tensor([e2e_ms], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_ms = float(t.item())
+        e2e = {"value": flops_job / (e2e_ms * 1e-3) / 1e12, "unit": "TFLOP/s", "ms_per_step": e2e_ms,
+               "h2d_bytes_per_step": 8 * total, "d2h_bytes_per_step": d2h,
+               "timing": "host wall clock per rank (max over ranks): pinned H2D of the input replica "
+                         "(ttr_tt_copy_from_host), ttr_round_fixed_krp_sharded, D2H of the rank's output shard"}
     if rank == 0:
         line = {
-            "metric": METRIC, "value": flops_job / (ms * 1e-3) / 1e12, "unit": "TFLOP/s",
-            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (device Philox Gaussian cores)",
-            "config": {"workload": ("config 5b, one tensor: column-sharded KRP sketch + NCCL all-gather + "
-                                    "row-sharded Rand-Orth sweep with NVLink TSQR") if rows_mode else
-                                   ("config 5b, one tensor: column-sharded KRP sketch + NCCL all-gather + "
-                                    "replicated Rand-Orth sweep"),
-                       "column_bounds": info["bounds"], "output_ranks": out_ranks,
-                       "flops_per_rank": flops_rank, "l2": "inputs exceed L2"},
-            "clocks": clk.summary(), "gpu_launches": launches,
+            "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (device Philox Gaussian cores)",
+            "config": {"workload": "config 5b, ONE tensor over the GPUs: column-sharded KRP sketch + NCCL "
+                                   "all-gather, row-sharded Rand-Orth sweep with an NVLink TSQR per mode "
+                                   "(ttr_round_fixed_krp_sharded)",
+                       "d": cfg["d"], "n": cfg["n"], "formal_rank": cfg["rx"] + cfg["rz"], "l": cfg["ell"],
+                       "output_ranks": out_ranks, "flops_per_step": flops_job, "flops_per_rank": flops_rank,
+                       "local_ranks": args.local_ranks or None, "l2": "inputs exceed L2 (18 GB vs 126 MB)",
+                       "parallelism": f"{world} GPUs, one tensor (columns of the sketch, rows of the sweep)"},
+            "tflops_fp64": value, "fraction_of_fp64_peak": value / world / FP64_PEAK_TFLOPS,
+            "clocks": clk.summary(), "gpu_launches": launches, "gpu_launches_per_step": launches_per_step,
+            "e2e": e2e, "cpu_baseline": None,
         }
         print(json.dumps(line), flush=True)
+    comm.close()
     if world > 1:
-        torch.distributed.destroy_process_group()
+        dist.destroy_process_group()
 
 
 def run_5a(args, world, rank, local):
@@ -879,6 +933,7 @@ def run_5a(args, world, rank, local):
 
 def main():
     args = parse()
+    maybe_spawn(args)
     world, rank, local = dist_env()
     if args.impl == "reference":
         run_reference(args, world, rank)
@@ -889,8 +944,8 @@ def main():
     if args.config in ADAPTIVE:
         run_adaptive(args, world, rank, local)
         return
-    if args.sharding in ("columns", "rows"):
-        run_columns(args, world, rank, local)
+    if args.config == "5b" and (args.local_ranks or (world > 1 and args.sharding == "tensor")):
+        run_sharded(args, world, rank, local)
         return
     run_ours(args, world, rank, local)
 

@@ -321,6 +321,38 @@ ttr_status ttr_round_fixed_krp_from_sketch(ttr_ctx* ctx, const ttr_tt* tt, const
                                            int64_t count, const double* const* W_dev, const int64_t* ldw,
                                            int64_t width, ttr_tt** out);
 
+/* ---- one tensor over P GPUs (config 5b) -----------------------
+ * One process per GPU. ttr_comm wraps an NCCL communicator (ttr_comm_init:
+ * rank 0 creates the id with ttr_comm_unique_id and the caller broadcasts
+ * its TTR_COMM_ID_BYTES bytes, e.g. with torch.distributed) or simulates P
+ * ranks inside one process on one device (ttr_comm_init_local: the same
+ * code, kernels and fixed-order reductions, rank after rank on the context
+ * stream — the sharded algorithm testable on one GPU, bitwise equal to the
+ * NCCL run). NCCL is loaded at run time (libnccl.so.2); TTR_ERR_NCCL if
+ * absent or failing.
+ * ttr_round_fixed_krp_sharded = round_fixed_krp (round_rand.cpp:52-64) with
+ * the KRP sketch column-sharded (all-gather of the W slices) and the Rand-Orth
+ * sweep row-sharded by the mode index with a TSQR per mode (all-gather of the
+ * l x l R factors, M = sum_p Q_p^T V_p by all-gather + fixed-order sum). Every
+ * rank passes its replica of the same input. local_out (one entry per local
+ * rank, may be NULL) receives rank p's slices Y_k(:, J_p, :) of every core —
+ * the sub-tensor on the index slices J_p (NULL if some mode has fewer slices
+ * than ranks); gather != 0 also all-gathers the full result into *full_out on
+ * every rank. Synchronises the context stream. */
+#define TTR_COMM_ID_BYTES 128
+typedef struct ttr_comm ttr_comm;
+ttr_status ttr_comm_unique_id(uint8_t* id_out /* TTR_COMM_ID_BYTES */);
+ttr_status ttr_comm_init(ttr_ctx* ctx, int nranks, int rank, const uint8_t* id, ttr_comm** out);
+ttr_status ttr_comm_init_local(ttr_ctx* ctx, int nranks, ttr_comm** out);
+ttr_status ttr_comm_destroy(ttr_comm* comm);
+/* recv (nranks * count, device) = the ranks' send buffers in rank order (one
+ * send pointer per local rank). */
+ttr_status ttr_comm_all_gather(ttr_ctx* ctx, ttr_comm* comm, const double* const* dev_send, int64_t count,
+                               double* dev_recv);
+ttr_status ttr_round_fixed_krp_sharded(ttr_ctx* ctx, ttr_comm* comm, const ttr_tt* tt, const int64_t* target_ranks,
+                                       int64_t count, uint64_t seed, int gather, ttr_tt** local_out,
+                                       ttr_tt** full_out);
+
 /* ---- batches of independent, identically shaped tensors (config 5a) ------
  * Tensor b of a batch is rounded exactly as
  *   round_fixed_krp(Y_b, target_ranks, derive_seed(seed, b))   (Philox mode)

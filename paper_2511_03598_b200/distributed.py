@@ -1,16 +1,22 @@
-"""Multi-GPU sharding of the KRP rounding path (one process per GPU,
-torch.distributed over NCCL/NVLink as plumbing).
+"""Multi-GPU sharding of the KRP rounding path (one process per GPU).
 
 * Independent tensors (config 5a) need no collective: each rank rounds its own
   slice of the batch (`round_fixed_krp_batched` on a local TTBatch).
-* One large tensor (config 5b): KRP sketch columns are independent
-  (W_{k-1}(:, c) depends only on W_k(:, c) and Omega_k(:, c), sketch.cpp:19-23),
-  so rank p contracts the global columns [c_p, c_{p+1}) on its replica of the
-  input (ttr_krp_sketch_into; Philox draws keyed by the global column make the
-  slice bitwise equal to those columns of a single-GPU contraction), the slices
-  of every W_k are all-gathered over NCCL, and the left-to-right Rand-Orth sweep
-  runs from the gathered sketch (ttr_round_fixed_krp_from_sketch). The sweep is
-  replicated in this version (each rank ends with the full result).
+* One large tensor (config 5b): `round_fixed_krp_sharded` runs the library's
+  sharded driver (csrc/sharded.cu) over a `Communicator`: the KRP sketch is
+  column-sharded (Philox draws keyed by the global column, so every slice is
+  bitwise the matching columns of a one-GPU contraction) with an NCCL
+  all-gather of the W slices, and the Rand-Orth sweep is row-sharded by the
+  mode index with a TSQR per mode (all-gather of the l x l R factors, a
+  redundant QR of the stack, M = sum_p Q_p^T V_p by all-gather and a
+  fixed-order sum). The whole driver — collectives included — is C++ on one
+  stream; torch.distributed only broadcasts the NCCL unique id.
+  `Communicator.local(ctx, P)` runs P ranks inside this process on one GPU
+  with the same code and kernels (the sharded algorithm on one device).
+* `rand_orth_row_sharded` below is the same sweep written against a generic
+  `ops` backend: the CPU tests run it with numpy/oracle arithmetic over gloo at
+  world sizes 2 and 3 (tests/test_distributed.py) as the host-side model of
+  the device driver.
 """
 from __future__ import annotations
 
@@ -76,29 +82,6 @@ def round_from_sketch(tt: TTTensor, target_ranks: Sequence[int], bufs, lds, widt
     return TTTensor(out, tt.ctx)
 
 
-def round_fixed_krp_column_sharded(tt: TTTensor, target_ranks: Sequence[int], seed: int, group=None,
-                                   rank: Optional[int] = None, world: Optional[int] = None
-                                   ) -> Tuple[TTTensor, dict]:
-    """Config-5b multi-GPU rounding: column-sharded KRP sketch + NCCL all-gather
-    of the W slices + Rand-Orth sweep. Every rank passes its replica of the same
-    input; returns (result, timings-free info)."""
-    import torch.distributed as dist
-    if world is None:
-        world = dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
-    if rank is None:
-        rank = dist.get_rank(group) if world > 1 else 0
-    width = max(target_ranks)
-    bounds = column_bounds(width, world)
-    bufs, lds = sketch_buffers(tt, width)
-    c0, c1 = bounds[rank], bounds[rank + 1]
-    if c1 > c0:
-        sketch_slice_into(tt, bufs, lds, c0, c1 - c0, seed)
-    for b in bufs:
-        gather_columns(b, bounds, rank, world, group)
-    out = round_from_sketch(tt, target_ranks, bufs, lds, width)
-    return out, {"bounds": bounds, "width": width}
-
-
 # ---------------------------------------------------------------------------
 # Row-sharded Rand-Orth sweep with an NVLink TSQR (SURVEY §8e, config 5b at
 # P GPUs). The rows of V(Y_k) are sharded by the mode index j: rank p owns the
@@ -111,9 +94,9 @@ def round_fixed_krp_column_sharded(tt: TTTensor, target_ranks: Sequence[int], se
 #   M = sum_p Q_k(J_p)^T V_p              local GEMM + all-reduce (l x r_k)
 #   V_{p}(Y_{k+1}) = M X_{k+1}(:, j, :)   for j in J_p (strided batch): local
 # Modes whose local blocks would be shorter than l (mode 1: n rows) run
-# replicated. The same orchestration runs over any `ops` backend: DeviceOps
-# (the library's DMMA GEMM / Householder QR through the C ABI on torch CUDA
-# buffers, NCCL collectives) here, a numpy backend in the CPU tests.
+# replicated. The same orchestration as the device driver (csrc/sharded.cu),
+# over a generic `ops` backend: the CPU tests run it with numpy GEMMs, the
+# oracle's Householder QR and gloo collectives.
 
 class View:
     """Column-major matrix view: element (i, j) at base[off + i + j*ld]."""
@@ -129,120 +112,6 @@ class View:
 def slice_bounds(n: int, world: int) -> List[int]:
     """Contiguous slices of the mode index: rank p owns j in [b[p], b[p+1])."""
     return [n * p // world for p in range(world + 1)]
-
-
-class DeviceOps:
-    """Device backend: torch CUDA buffers as storage, the library's kernels for
-    the arithmetic (ttr_dev_gemm / ttr_dev_gemm_batched / ttr_dev_thin_qr on
-    the context stream = torch's current stream), torch.distributed (NCCL) for
-    the collectives."""
-
-    def __init__(self, ctx, group=None):
-        import torch
-        self.ctx, self.group, self.torch = ctx, group, torch
-        self.L = lib()
-
-    def alloc(self, rows: int, cols: int) -> View:
-        t = self.torch.zeros(max(1, rows * cols), dtype=self.torch.float64, device="cuda")
-        return View(t, 0, max(1, rows), rows, cols)
-
-    def ptr(self, v: View) -> int:
-        base = v.base if isinstance(v.base, int) else v.base.data_ptr()
-        return base + 8 * v.off
-
-    def gemm(self, ta: bool, alpha: float, A: View, B: View, beta: float, Cm: View):
-        k = A.rows if ta else A.cols
-        _check(self.L.ttr_dev_gemm(self.ctx._h, C.c_int(int(ta)), C_i64(Cm.rows), C_i64(Cm.cols), C_i64(k),
-                                   C_dbl(alpha), C_vp(self.ptr(A)), C_i64(A.ld), C_vp(self.ptr(B)), C_i64(B.ld),
-                                   C_dbl(beta), C_vp(self.ptr(Cm)), C_i64(Cm.ld)))
-
-    def gemm_batched(self, alpha, A, sA, B, sB, beta, Cv, sC, batch):
-        _check(self.L.ttr_dev_gemm_batched(self.ctx._h, C.c_int(0), C_i64(Cv.rows), C_i64(Cv.cols), C_i64(A.cols), C_dbl(alpha),
-                                           C_vp(self.ptr(A)), C_i64(A.ld), C_i64(sA), C_vp(self.ptr(B)), C_i64(B.ld),
-                                           C_i64(sB), C_dbl(beta), C_vp(self.ptr(Cv)), C_i64(Cv.ld), C_i64(sC),
-                                           C_i64(batch)))
-
-    def qr(self, A: View):
-        m, n = A.rows, A.cols
-        k = min(m, n)
-        Q, R = self.alloc(m, k), self.alloc(k, n)
-        _check(self.L.ttr_dev_thin_qr(self.ctx._h, C_i64(m), C_i64(n), C_vp(self.ptr(A)), C_i64(A.ld),
-                                      C_vp(self.ptr(Q)), C_i64(Q.ld), C_vp(self.ptr(R)), C_i64(R.ld)))
-        return Q, R
-
-    def all_gather_blocks(self, block: View, world: int) -> View:
-        """Stack the ranks' (b x c) blocks row-wise: (world*b x c)."""
-        torch = self.torch
-        b, c = block.rows, block.cols
-        mine = self.contiguous(block)
-        if world == 1:
-            return mine
-        out = torch.empty(world * b * c, dtype=torch.float64, device="cuda")
-        import torch.distributed as dist
-        dist.all_gather_into_tensor(out, mine.base[:b * c], group=self.group)
-        st = out.view(world, c, b).permute(1, 0, 2).contiguous().view(-1)  # column j: block 0 rows, block 1 rows...
-        return View(st, 0, world * b, world * b, c)
-
-    def all_reduce(self, v: View, world: int):
-        if world == 1:
-            return
-        import torch.distributed as dist
-        assert v.off == 0 and v.ld == v.rows
-        dist.all_reduce(v.base[:v.rows * v.cols], group=self.group)
-
-    def contiguous(self, v: View) -> View:
-        if not isinstance(v.base, int) and v.off == 0 and v.ld == v.rows:
-            return v
-        out = self.alloc(v.rows, v.cols)
-        self.copy(v, out)
-        return out
-
-    def copy(self, src: View, dst: View):
-        # 2-D strided copy through torch views of the underlying storage (plumbing)
-        s = self._tview(src)
-        d = self._tview(dst)
-        d.copy_(s)
-
-    def _tview(self, v: View):
-        if isinstance(v.base, int):
-            raise TypeError("raw pointer views are read through the library only")
-        return self.torch.as_strided(v.base, (v.cols, v.rows), (v.ld, 1), v.off)
-
-    def gather_rows(self, local: View, counts: List[int], world: int) -> View:
-        """All-gather row blocks of different heights (counts[p] rows each, same
-        column count) into the full matrix, in rank order."""
-        torch = self.torch
-        c = local.cols
-        full_rows = sum(counts)
-        if world == 1:
-            return self.contiguous(local)
-        import torch.distributed as dist
-        mx = max(counts)
-        pad = self.alloc(mx, c)
-        if local.rows:
-            self.copy(local, pad.sub(0, local.rows, 0, c))
-        out = torch.empty(world * mx * c, dtype=torch.float64, device="cuda")
-        dist.all_gather_into_tensor(out, pad.base[:mx * c], group=self.group)
-        full = self.alloc(full_rows, c)
-        r0 = 0
-        for p in range(world):
-            blk = View(out, p * mx * c, mx, counts[p], c)
-            if counts[p]:
-                self.copy(blk, full.sub(r0, counts[p], 0, c))
-            r0 += counts[p]
-        return full
-
-
-def C_i64(v):
-    return C.c_int64(int(v))
-
-
-def C_dbl(v):
-    return C.c_double(float(v))
-
-
-def C_vp(v):
-    return C.c_void_p(int(v))
 
 
 def rand_orth_row_sharded(ops, n: Sequence[int], r_in: Sequence[int], r_out: Sequence[int], W, core, rank: int,
@@ -283,8 +152,9 @@ def rand_orth_row_sharded(ops, n: Sequence[int], r_in: Sequence[int], r_out: Seq
             Qk, _ = ops.qr(S)
         M = ops.alloc(l, cols)
         ops.gemm(True, 1.0, Qk, Vp, 0.0, M)
-        if sharded:
-            ops.all_reduce(M, world)
+        if sharded:  # M = sum_p parts in rank order (all-gather + fixed-order sum, as the device driver)
+            parts = ops.all_gather_blocks(M, world)  # (world*l x cols)
+            ops.sum_blocks(parts, world, M)
             out[k - 1] = ops.gather_rows(Qk, counts, world)
         else:
             out[k - 1] = Qk
@@ -320,49 +190,55 @@ def fixed_krp_output_ranks(n: Sequence[int], r_in: Sequence[int], targets: Seque
     return r
 
 
-def round_fixed_krp_row_sharded(tt: TTTensor, target_ranks: Sequence[int], seed: int, group=None,
-                                rank: Optional[int] = None, world: Optional[int] = None) -> TTTensor:
-    """Config-5b multi-GPU rounding with BOTH phases sharded: column-sharded KRP
-    sketch + NCCL all-gather of the W slices, then the row-sharded Rand-Orth
-    sweep with the NVLink TSQR (rand_orth_row_sharded). Every rank passes its
-    replica of the same input and receives the full result."""
-    import torch
-    import torch.distributed as dist
-    if world is None:
-        world = dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
-    if rank is None:
-        rank = dist.get_rank(group) if world > 1 else 0
-    n, r_in, _ = tt.shape()
-    d = len(n)
-    width = max(target_ranks)
-    r_out = fixed_krp_output_ranks(n, r_in, target_ranks)
+class Communicator:
+    """ttr_comm: an NCCL communicator over the torch.distributed group (rank 0
+    makes the unique id, torch broadcasts it), or `Communicator.local(ctx, P)`:
+    P ranks simulated in this process on one device."""
 
-    def core(k):
-        rows = r_in[k] * n[k]
-        return View(tt.core_ptr(k), 0, rows, rows, r_in[k + 1])
+    def __init__(self, handle, ctx, world: int, rank: int, nlocal: int):
+        self._h, self.ctx, self.world, self.rank, self.nlocal = handle, ctx, world, rank, nlocal
 
-    # the library and torch (buffers, NCCL) must share one stream
-    cur = torch.cuda.current_stream().cuda_stream
-    prev = tt.ctx.stream
-    if prev != cur:
-        tt.ctx.set_stream(cur)
-    try:
-        bounds = column_bounds(width, world)
-        bufs, lds = sketch_buffers(tt, width)
-        c0, c1 = bounds[rank], bounds[rank + 1]
-        if c1 > c0:
-            sketch_slice_into(tt, bufs, lds, c0, c1 - c0, seed)
-        for b in bufs:
-            gather_columns(b, bounds, rank, world, group)
-        W = {k: View(bufs[k - 2].view(-1), 0, lds[k - 2], r_in[k - 1], width) for k in range(2, d + 1)}
-        ops = DeviceOps(tt.ctx, group)
-        cores = rand_orth_row_sharded(ops, n, r_in, r_out, W, core, rank, world)
-        flat = torch.cat([ops.contiguous(v).base[:v.rows * v.cols] for v in cores])
-        out = C.c_void_p()
-        _check(lib().ttr_tt_from_device(tt.ctx._h, C.c_int64(d), _i64(n), _i64(r_out), C.c_void_p(flat.data_ptr()),
-                                        C.byref(out)))
-        tt.ctx.synchronize()
-    finally:
-        if prev != cur:
-            tt.ctx.set_stream(prev)
-    return TTTensor(out, tt.ctx)
+    @staticmethod
+    def from_torch(ctx, group=None) -> "Communicator":
+        import torch.distributed as dist
+        world = dist.get_world_size(group)
+        rank = dist.get_rank(group)
+        idbuf = (C.c_uint8 * 128)()
+        if rank == 0:
+            _check(lib().ttr_comm_unique_id(idbuf))
+        obj = [bytes(idbuf)]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        idbuf = (C.c_uint8 * 128).from_buffer_copy(obj[0])
+        h = C.c_void_p()
+        _check(lib().ttr_comm_init(ctx._h, C.c_int(world), C.c_int(rank), idbuf, C.byref(h)))
+        return Communicator(h, ctx, world, rank, 1)
+
+    @staticmethod
+    def local(ctx, world: int) -> "Communicator":
+        h = C.c_void_p()
+        _check(lib().ttr_comm_init_local(ctx._h, C.c_int(world), C.byref(h)))
+        return Communicator(h, ctx, world, 0, world)
+
+    def close(self):
+        if getattr(self, "_h", None) and self._h.value and lib() is not None:
+            lib().ttr_comm_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        self.close()
+
+
+def round_fixed_krp_sharded(tt: TTTensor, target_ranks: Sequence[int], seed: int, comm: Communicator,
+                            gather: bool = True):
+    """Config-5b rounding of ONE tensor over comm.world GPUs (ttr_round_fixed_krp_sharded).
+    Every rank passes its replica of the same input. Returns (local, full): local =
+    this process's rank slices Y_k(:, J_p, :) of every core (a list, one per local
+    rank; entries may be None), full = the all-gathered result (gather=True) or None."""
+    n = comm.nlocal
+    loc = (C.c_void_p * n)()
+    full = C.c_void_p()
+    _check(lib().ttr_round_fixed_krp_sharded(tt.ctx._h, comm._h, tt._h, _i64(target_ranks),
+                                             C.c_int64(len(target_ranks)), C.c_uint64(seed), C.c_int(int(gather)),
+                                             loc, C.byref(full) if gather else None))
+    local = [TTTensor(C.c_void_p(loc[q]), tt.ctx) if loc[q] else None for q in range(n)]
+    return local, (TTTensor(full, tt.ctx) if gather else None)

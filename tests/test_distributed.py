@@ -149,9 +149,14 @@ class NumpyOps:
         st = np.concatenate([p.numpy().reshape(c, b) for p in parts], axis=1).reshape(-1)  # (c, world*b)
         return View(st, 0, world * b, world * b, c)
 
-    def all_reduce(self, v, world):
-        t = torch.from_numpy(v.base)
-        dist.all_reduce(t, group=self.group)
+    def sum_blocks(self, stacked, world, out):
+        """out = sum_p stacked[p*b:(p+1)*b, :] in rank order (the device driver's fixed-order sum)."""
+        b = out.rows
+        m = self.mat(stacked)
+        acc = m[0:b].copy()
+        for p in range(1, world):
+            acc = acc + m[p * b:(p + 1) * b]
+        self.mat(out)[...] = acc
 
     def gather_rows(self, local, counts, world):
         from paper_2511_03598_b200.distributed import View
@@ -223,18 +228,66 @@ def test_row_sharded_sweep_gloo(world):
 
 
 @pytest.mark.gpu
-def test_row_sharded_path_single_gpu():
-    """The device row-sharded driver at world size 1 (replicated modes, TSQR of
-    one block) matches round_fixed_krp to 1e-10."""
+@pytest.mark.parametrize("world", [1, 2, 3])
+def test_sharded_library_path_local_ranks(world):
+    """The library's sharded driver (csrc/sharded.cu) with `world` ranks simulated on
+    one GPU (ttr_comm_init_local: the same code, kernels and fixed-order sums as the
+    NCCL run): column-sharded sketch, TSQR row-sharded sweep. The gathered result
+    equals the oracle's round_fixed_krp to 1e-10 with identical ranks (world 3 does
+    not divide n = 16: uneven slices); world 1 is bitwise round_fixed_krp; the local
+    shards are the index slices Y(J_p, ..., J_p) of the gathered tensor; two runs
+    are bitwise equal."""
     import sys
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     import py_oracle as O
     from helpers import rel_err_vs_ref, to_device
     import paper_2511_03598_b200 as P
-    from paper_2511_03598_b200.distributed import round_fixed_krp_row_sharded
+    from paper_2511_03598_b200.distributed import Communicator, round_fixed_krp_sharded, slice_bounds
     x = O.two_part_tt(6, 16, 10, 30, 1e-6, 41)
-    y = round_fixed_krp_row_sharded(to_device(x), [24] * 5, 7, world=1, rank=0)
+    xd = to_device(x)
+    comm = Communicator.local(xd.ctx, world)
+    local, full = round_fixed_krp_sharded(xd, [24] * 5, 7, comm)
     ref = O.round_fixed_krp(x, [24] * 5, 7, rng=O.PHILOX)
-    assert y.ranks() == ref.ranks
-    assert rel_err_vs_ref(ref, y) <= 1e-10
+    assert full.ranks() == ref.ranks
+    assert rel_err_vs_ref(ref, full) <= 1e-10
+    _, again = round_fixed_krp_sharded(xd, [24] * 5, 7, comm)
+    assert np.array_equal(again.flat(), full.flat())
+    if world == 1:
+        assert np.array_equal(full.flat(), P.round_fixed_krp(xd, [24] * 5, 7).flat())
+    cores = full.cores()
+    for p, lt in enumerate(local):
+        for k, c in enumerate(lt.cores()):
+            sb = slice_bounds(cores[k].shape[1], world)
+            assert np.array_equal(c, cores[k][:, sb[p]:sb[p + 1], :])
+    comm.close()
+
+
+@pytest.mark.gpu
+def test_nccl_communicator_world1():
+    """The NCCL communicator loads and runs (world size 1 on this one-GPU box): its
+    all-gather copies, and the sharded driver over it is bitwise round_fixed_krp."""
+    import sys
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import ctypes as C
+    import py_oracle as O
+    from helpers import to_device
+    import paper_2511_03598_b200 as P
+    from paper_2511_03598_b200.distributed import Communicator, round_fixed_krp_sharded
+    if not dist.is_initialized():
+        dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{_free_port()}", rank=0, world_size=1)
+    x = O.two_part_tt(5, 12, 8, 20, 1e-6, 43)
+    xd = to_device(x)
+    comm = Communicator.from_torch(xd.ctx)
+    src = torch.arange(10, dtype=torch.float64, device="cuda")
+    dst = torch.zeros(10, dtype=torch.float64, device="cuda")
+    torch.cuda.synchronize()
+    ptrs = (C.c_void_p * 1)(src.data_ptr())
+    P._check(P.lib().ttr_comm_all_gather(xd.ctx._h, comm._h, ptrs, C.c_int64(10), C.c_void_p(dst.data_ptr())))
+    xd.ctx.synchronize()
+    assert torch.equal(src, dst)
+    _, full = round_fixed_krp_sharded(xd, [16] * 4, 7, comm)
+    assert np.array_equal(full.flat(), P.round_fixed_krp(xd, [16] * 4, 7).flat())
+    comm.close()
+    dist.destroy_process_group()
