@@ -177,6 +177,7 @@ struct RegQrArgs {
 };
 
 #include "qr_panel.cuh"
+#include "qr_cpanel.cuh"
 #include "qr_batch.cuh"
 
 template <int RPT, int WARPS, int MODE>
@@ -269,6 +270,13 @@ bool launch_panel_col(Ctx& c, RegQrArgs a) {
     if ((forced < 0 || forced == 0) &&
         (cl_try(std::integral_constant<int, 4>{}) || cl_try(std::integral_constant<int, 8>{})))
         return true;
+    static const bool force_cluster = [] {  // experiments: TTR_QR_PANEL_MODE=c tries tall cluster panels
+        const char* e = std::getenv("TTR_QR_PANEL_MODE");
+        return e && e[0] == 'c';
+    }();
+    if (force_cluster && (cl_try(std::integral_constant<int, 12>{}) || cl_try(std::integral_constant<int, 16>{}) ||
+                          cl_try(std::integral_constant<int, 20>{}) || cl_try(std::integral_constant<int, 28>{})))
+        return true;
     const i64 g = std::min<i64>(c.sm_count, kQrMaxGridCtas);  // the exchange layout holds 160 CTA slots
     if (gr_try(std::integral_constant<int, 4>{}, I16{}, Gb{}, g) ||
         gr_try(std::integral_constant<int, 8>{}, I16{}, Gb{}, g) ||
@@ -281,7 +289,8 @@ bool launch_panel_col(Ctx& c, RegQrArgs a) {
     throw Error(TTR_ERR_INTERNAL, "qr panel taller than the device panel limit");
 }
 
-__global__ void init_thin_identity(int m, int k, double* Q, i64 ldq) {
+__global__ void init_thin_identity(int m, int k, double* Q, i64 ldq, i64 sQ = 0) {
+    Q += blockIdx.y * sQ;
     const i64 total = static_cast<i64>(m) * k;
     for (i64 idx = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; idx < total;
          idx += static_cast<i64>(gridDim.x) * blockDim.x) {
@@ -290,7 +299,9 @@ __global__ void init_thin_identity(int m, int k, double* Q, i64 ldq) {
     }
 }
 
-__global__ void copy_upper(int k, int n, const double* A, i64 lda, double* R, i64 ldr) {
+__global__ void copy_upper(int k, int n, const double* A, i64 lda, double* R, i64 ldr, i64 sA = 0, i64 sR = 0) {
+    A += blockIdx.y * sA;
+    R += blockIdx.y * sR;
     const i64 total = static_cast<i64>(k) * n;
     for (i64 idx = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; idx < total;
          idx += static_cast<i64>(gridDim.x) * blockDim.x) {
@@ -307,10 +318,14 @@ __global__ void copy_upper(int k, int n, const double* A, i64 lda, double* R, i6
 // (zero padded past k).
 constexpr int kTaggThreads = 256;
 __global__ void __launch_bounds__(kTaggThreads) t_aggregate_kernel(int k, const double* __restrict__ G,
-                                                                   const double* __restrict__ Ts, double* T) {
+                                                                   const double* __restrict__ Ts, double* T,
+                                                                   i64 sG = 0, i64 sTs = 0, i64 sT = 0) {
     extern __shared__ double xs[];  // X(:, j-block): [nb * 32][32]; then G row block [(nb-1)*32][33]
     __shared__ double acc_s[32 * 33];
     __shared__ double ti_s[32 * 33];
+    G += blockIdx.y * sG;  // batch (blockIdx.y): one matrix of a strided set
+    Ts += blockIdx.y * sTs;
+    T += blockIdx.y * sT;
     const int j = blockIdx.x, nb = (k + 31) / 32, tid = threadIdx.x;
     double* gs = xs + static_cast<i64>(nb) * 32 * 32;
     const int r = tid & 31, c0 = tid >> 5;  // thread owns (r, c0 + 8q), q = 0..3
@@ -357,6 +372,236 @@ __global__ void __launch_bounds__(kTaggThreads) t_aggregate_kernel(int k, const 
 
 int blocks_for(Ctx& c, i64 work) {
     return static_cast<int>(std::max<i64>(1, std::min<i64>((work + 255) / 256, 4LL * c.sm_count)));
+}
+
+// rows x cols copies / k x k transposes of a strided batch (blockIdx.y = matrix)
+__global__ void copy_batched_kernel(int rows, int cols, const double* __restrict__ s, i64 lds, i64 ss,
+                                    double* __restrict__ d, i64 ldd, i64 sd) {
+    s += blockIdx.y * ss;
+    d += blockIdx.y * sd;
+    const i64 total = static_cast<i64>(rows) * cols;
+    for (i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<i64>(gridDim.x) * blockDim.x) {
+        const int r = static_cast<int>(i % rows), cc = static_cast<int>(i / rows);
+        d[r + cc * ldd] = s[r + cc * lds];
+    }
+}
+__global__ void transpose_batched_kernel(int k, const double* __restrict__ s, i64 lds, i64 ss, double* __restrict__ d,
+                                         i64 ldd, i64 sd) {
+    s += blockIdx.y * ss;
+    d += blockIdx.y * sd;
+    const i64 total = static_cast<i64>(k) * k;
+    for (i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<i64>(gridDim.x) * blockDim.x) {
+        const int r = static_cast<int>(i % k), cc = static_cast<int>(i / k);
+        d[cc + r * ldd] = s[r + cc * lds];
+    }
+}
+
+// ---- cluster push panels (qr_cpanel.cuh) --------------------------------------
+constexpr int kPushWarps = 16;
+constexpr int kPushMaxRpt = 28;
+constexpr i64 kPushMaxRows = static_cast<i64>(kPushMaxCtas) * kPushWarps * kPushMaxRpt;  // 7,168
+
+template <int RPT>
+void launch_push(Ctx& c, const PushQrArgs& a, int G, i64 batch) {
+    auto kern = panel_push_kernel<RPT, kPushWarps>;
+    static std::atomic<std::uint64_t> configured{0};  // bit d: attributes set on device d
+    if (first_on_device(configured)) {
+        TTR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>(G * batch));
+    cfg.blockDim = dim3(kPushWarps * 32);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = c.stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = static_cast<unsigned>(G);
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    TTR_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
+    c.launched();
+    if (a.trace) {  // TTR_QR_TRACE: per-phase cycles of cluster 0 / CTA 0, averaged over the panel's columns
+        long long h[32 * 8];
+        TTR_CUDA(cudaMemcpyAsync(h, a.trace, sizeof(h), cudaMemcpyDeviceToHost, c.stream));
+        TTR_CUDA(cudaStreamSynchronize(c.stream));
+        const int nc = std::min(a.b, a.rows);
+        double acc[8] = {};
+        for (int i = 0; i < nc; ++i) {
+            const long long* t = h + i * 8;
+            const long long seq[8] = {t[0], t[1], t[6], t[7], t[2], t[3], t[4], t[5]};
+            for (int q = 1; q < 8; ++q) acc[q] += static_cast<double>(seq[q] - seq[q - 1]) / nc;
+            acc[0] += static_cast<double>(t[5] - t[0]) / nc;
+        }
+        std::fprintf(stderr,
+                     "push<%d> cluster %d x %lld rows %d: cycles/col %.0f | dots %.0f bar %.0f xchg %.0f sum %.0f "
+                     "scalar %.0f bar %.0f update %.0f\n",
+                     RPT, G, static_cast<long long>(batch), a.rows, acc[0], acc[1], acc[2], acc[3], acc[4], acc[5],
+                     acc[6], acc[7]);
+    }
+}
+
+// One cluster per matrix: the fewest rows per warp that fit 16 CTAs (more CTAs =
+// less arithmetic per column; the push exchange grows with the cluster size).
+void launch_panel_push(Ctx& c, PushQrArgs a, i64 batch) {
+    static const bool tracing = std::getenv("TTR_QR_TRACE") != nullptr;  // diagnostics only
+    static long long* trace_buf = nullptr;
+    if (tracing && !trace_buf) TTR_CUDA(cudaMalloc(reinterpret_cast<void**>(&trace_buf), 32 * 8 * sizeof(long long)));
+    a.trace = tracing ? trace_buf : nullptr;
+    const i64 rows = a.rows;
+    bool done = false;
+    auto go = [&](auto rpt_tag) {
+        constexpr int RPT = decltype(rpt_tag)::value;
+        const i64 per = static_cast<i64>(kPushWarps) * RPT;
+        if (done || rows > kPushMaxCtas * per) return;
+        a.rpc = static_cast<int>(per);
+        launch_push<RPT>(c, a, static_cast<int>(std::max<i64>(1, (rows + per - 1) / per)), batch);
+        done = true;
+    };
+    go(std::integral_constant<int, 2>{});
+    go(std::integral_constant<int, 4>{});
+    go(std::integral_constant<int, 8>{});
+    go(std::integral_constant<int, 12>{});
+    go(std::integral_constant<int, 16>{});
+    go(std::integral_constant<int, 20>{});
+    go(std::integral_constant<int, 24>{});
+    go(std::integral_constant<int, 28>{});
+    if (!done) throw Error(TTR_ERR_INTERNAL, "push panel taller than one cluster");
+}
+
+// Blocked right-looking Householder QR of a strided batch of m x n matrices
+// (m <= kPushMaxRows): panels of 32 columns on one cluster per matrix
+// (panel_push_kernel), trailing updates and the explicit thin Q as strided-
+// batch DMMA GEMMs. Not charged (the caller charges the reference's 4mnk).
+void qr_blocked_push(Ctx& c, i64 batch, i64 m, i64 n, const double* A, i64 lda, i64 sA, double* Q, i64 ldq, i64 sQ,
+                     double* R, i64 ldr, i64 sR, double* inplace = nullptr) {
+    // inplace: A itself is the (overwritten) work buffer, lda == even_ld(m), sA == lda * n
+    const i64 k = std::min(m, n);
+    const i64 ldw = even_ld(m), sW = ldw * n;
+    DBuf work_buf;
+    double* work = inplace;
+    if (!inplace) {
+        work_buf = DBuf(c, static_cast<std::size_t>(sW * batch));
+        work = work_buf.p;
+        dim3 grid(static_cast<unsigned>(blocks_for(c, m * n)), static_cast<unsigned>(batch));
+        copy_batched_kernel<<<grid, 256, 0, c.stream>>>(static_cast<int>(m), static_cast<int>(n), A, lda, sA, work,
+                                                        ldw, sW);
+        TTR_CUDA(cudaGetLastError());
+        c.launched();
+    }
+    const i64 npanels = (k + kPanel - 1) / kPanel;
+    DBuf tau(c, static_cast<std::size_t>(k * batch));
+    if (n <= kPanel) {  // one panel: R and the explicit Q straight from the cluster kernel
+        PushQrArgs a{};
+        a.rows = static_cast<int>(m);
+        a.b = static_cast<int>(n);
+        a.Pin = work;
+        a.ldin = ldw;
+        a.sin = sW;
+        a.tau = tau.p;
+        a.stau = k;
+        a.Q = Q;
+        a.ldq = ldq;
+        a.sq = sQ;
+        a.R = R;
+        a.ldr = ldr;
+        a.sr = sR;
+        launch_panel_push(c, a, batch);
+        return;
+    }
+    const i64 sV = ldw * k, sTs = npanels * kPanel * kPanel, sWb = kPanel * n;
+    DBuf Vall(c, static_cast<std::size_t>(sV * batch));
+    if (Q) TTR_CUDA(cudaMemsetAsync(Vall.p, 0, sizeof(double) * sV * batch, c.stream));  // zeros above each panel
+    DBuf Ts(c, static_cast<std::size_t>(sTs * batch));
+    DBuf Wb(c, static_cast<std::size_t>(sWb * batch)), Wb2(c, static_cast<std::size_t>(sWb * batch));
+    for (i64 p = 0; p < npanels; ++p) {
+        const i64 j0 = p * kPanel, bb = std::min<i64>(kPanel, k - j0), rows = m - j0;
+        double* V = Vall.p + j0 + j0 * ldw;
+        PushQrArgs a{};
+        a.rows = static_cast<int>(rows);
+        a.b = static_cast<int>(bb);
+        a.Pin = work + j0 + j0 * ldw;
+        a.ldin = ldw;
+        a.sin = sW;
+        a.Pout = work + j0 + j0 * ldw;
+        a.ldout = ldw;
+        a.sout = sW;
+        a.tau = tau.p + j0;
+        a.stau = k;
+        a.V = V;
+        a.ldv = ldw;
+        a.sv = sV;
+        a.T = Ts.p + p * kPanel * kPanel;
+        a.sT = sTs;
+        launch_panel_push(c, a, batch);
+        const i64 ntrail = n - j0 - bb;
+        if (ntrail > 0) {
+            double* At = work + j0 + (j0 + bb) * ldw;
+            const double* T = Ts.p + p * kPanel * kPanel;
+            gemm_batched(c, true, bb, ntrail, rows, 1.0, V, ldw, sV, At, ldw, sW, 0.0, Wb.p, kPanel, sWb, batch,
+                         false);                                                                   // V^T A
+            gemm_batched(c, true, bb, ntrail, bb, 1.0, T, kPanel, sTs, Wb.p, kPanel, sWb, 0.0, Wb2.p, kPanel, sWb,
+                         batch, false);                                                            // T^T (V^T A)
+            gemm_batched(c, false, rows, ntrail, bb, -1.0, V, ldw, sV, Wb2.p, kPanel, sWb, 1.0, At, ldw, sW, batch,
+                         false);                                                                   // A -= V (.)
+        }
+    }
+    if (R) {
+        dim3 grid(static_cast<unsigned>(blocks_for(c, k * n)), static_cast<unsigned>(batch));
+        copy_upper<<<grid, 256, 0, c.stream>>>(static_cast<int>(k), static_cast<int>(n), work, ldw, R, ldr, sW, sR);
+        TTR_CUDA(cudaGetLastError());
+        c.launched();
+    }
+    if (Q == nullptr) return;
+    {
+        dim3 grid(static_cast<unsigned>(blocks_for(c, m * k)), static_cast<unsigned>(batch));
+        init_thin_identity<<<grid, 256, 0, c.stream>>>(static_cast<int>(m), static_cast<int>(k), Q, ldq, sQ);
+        TTR_CUDA(cudaGetLastError());
+        c.launched();
+    }
+    if (k <= 384) {  // Q = [I;0] - V (T V_1^T) with the aggregated T of all panels
+        const i64 kk2 = k * k;
+        DBuf Gm(c, static_cast<std::size_t>(kk2 * batch)), Tf(c, static_cast<std::size_t>(kk2 * batch)),
+            V1t(c, static_cast<std::size_t>(kk2 * batch)), Y(c, static_cast<std::size_t>(kk2 * batch));
+        if (batch == 1)
+            gemm(c, true, k, k, m, 1.0, Vall.p, ldw, Vall.p, ldw, 0.0, Gm.p, k, false, true);  // upper tiles only
+        else
+            gemm_batched(c, true, k, k, m, 1.0, Vall.p, ldw, sV, Vall.p, ldw, sV, 0.0, Gm.p, k, kk2, batch, false);
+        const std::size_t smem = (static_cast<std::size_t>(npanels) * 32 * 32 + (npanels - 1) * 32 * 33) * sizeof(double);
+        static std::atomic<std::uint64_t> configured{0};  // bit d: attributes set on device d
+        if (first_on_device(configured)) {
+            TTR_CUDA(cudaFuncSetAttribute(t_aggregate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        }
+        t_aggregate_kernel<<<dim3(static_cast<unsigned>(npanels), static_cast<unsigned>(batch)), kTaggThreads, smem,
+                             c.stream>>>(static_cast<int>(k), Gm.p, Ts.p, Tf.p, kk2, sTs, kk2);
+        TTR_CUDA(cudaGetLastError());
+        c.launched();
+        {
+            dim3 grid(static_cast<unsigned>(blocks_for(c, kk2)), static_cast<unsigned>(batch));
+            transpose_batched_kernel<<<grid, 256, 0, c.stream>>>(static_cast<int>(k), Vall.p, ldw, sV, V1t.p, k, kk2);
+            TTR_CUDA(cudaGetLastError());
+            c.launched();
+        }
+        gemm_batched(c, false, k, k, k, 1.0, Tf.p, k, kk2, V1t.p, k, kk2, 0.0, Y.p, k, kk2, batch, false);  // T V_1^T
+        gemm_batched(c, false, m, k, k, -1.0, Vall.p, ldw, sV, Y.p, k, kk2, 1.0, Q, ldq, sQ, batch, false);  // Q -= V Y
+        return;
+    }
+    // very wide: panels applied last to first (backward accumulation)
+    const i64 sQw = kPanel * k;
+    DBuf Qw(c, static_cast<std::size_t>(sQw * batch)), Qw2(c, static_cast<std::size_t>(sQw * batch));
+    for (i64 p = npanels - 1; p >= 0; --p) {
+        const i64 j0 = p * kPanel, bb = std::min<i64>(kPanel, k - j0), rows = m - j0, nc = k - j0;
+        const double* V = Vall.p + j0 + j0 * ldw;
+        const double* T = Ts.p + p * kPanel * kPanel;
+        double* Qs = Q + j0 + j0 * ldq;
+        gemm_batched(c, true, bb, nc, rows, 1.0, V, ldw, sV, Qs, ldq, sQ, 0.0, Qw.p, kPanel, sQw, batch, false);
+        gemm_batched(c, false, bb, nc, bb, 1.0, T, kPanel, sTs, Qw.p, kPanel, sQw, 0.0, Qw2.p, kPanel, sQw, batch,
+                     false);
+        gemm_batched(c, false, rows, nc, bb, -1.0, V, ldw, sV, Qw2.p, kPanel, sQw, 1.0, Qs, ldq, sQ, batch, false);
+    }
 }
 
 
@@ -486,6 +731,49 @@ void thin_qr(Ctx& c, i64 m, i64 n, const double* A, i64 lda, double* Q, i64 ldq,
     }();
     if (small_on && n <= kPanel && m <= 512 && m >= n) {
         qr_small_batched(c, m, n, A, lda, 0, Q, ldq, 0, R, ldr, 0, 1);
+        return;
+    }
+    static const bool old_panels = [] {  // experiments: TTR_QR_OLD=1 = cooperative-grid / old cluster panels
+        const char* e = std::getenv("TTR_QR_OLD");
+        return e && e[0] == '1';
+    }();
+    if (!old_panels && n <= kPushMaxRows) {
+        if (m <= kPushMaxRows) {  // one cluster per panel
+            qr_blocked_push(c, 1, m, n, A, lda, 0, Q, ldq, 0, R, ldr, 0);
+            return;
+        }
+        // Taller: TSQR over B cluster-sized row chunks, all factored at once
+        // (one cluster per chunk, strided-batch GEMMs), then the QR of the
+        // stacked R factors and Q(chunk q) = Q_q Q_s(q-th block). The chunks are
+        // padded with zero rows to one height (zero rows leave R unchanged and
+        // get zero rows of Q, never copied out). Charged once, as one QR.
+        const Counts saved = c.counts;
+        const i64 B = (m + kPushMaxRows - 1) / kPushMaxRows;
+        const i64 chunk = even_ld((m + B - 1) / B), kq = std::min(chunk, n), sC = chunk * n;
+        DBuf Ap(c, static_cast<std::size_t>(sC * B));
+        if (chunk * B != m) TTR_CUDA(cudaMemsetAsync(Ap.p, 0, sizeof(double) * sC * B, c.stream));
+        for (i64 q = 0; q < B; ++q) {
+            const i64 rq = std::min(chunk, m - q * chunk);
+            TTR_CUDA(cudaMemcpy2DAsync(Ap.p + q * sC, sizeof(double) * chunk, A + q * chunk, sizeof(double) * lda,
+                                       sizeof(double) * rq, n, cudaMemcpyDeviceToDevice, c.stream));
+        }
+        const i64 ls = B * kq;
+        DBuf Rst(c, static_cast<std::size_t>(ls * n));
+        DBuf Qc(c, static_cast<std::size_t>(Q ? chunk * kq * B : 1));
+        qr_blocked_push(c, B, chunk, n, Ap.p, chunk, sC, Q ? Qc.p : nullptr, chunk, chunk * kq, Rst.p, ls, kq, Ap.p);
+        if (!Q) {
+            thin_qr(c, ls, n, Rst.p, ls, nullptr, 1, R, ldr);
+        } else {
+            DBuf Qs(c, static_cast<std::size_t>(ls * k));
+            thin_qr(c, ls, n, Rst.p, ls, Qs.p, ls, R, ldr);
+            if (B > 1)
+                gemm_batched(c, false, chunk, k, kq, 1.0, Qc.p, chunk, chunk * kq, Qs.p, ls, kq, 0.0, Q, ldq, chunk,
+                             B - 1, false);
+            const i64 last = m - (B - 1) * chunk;
+            gemm(c, false, last, k, kq, 1.0, Qc.p + (B - 1) * chunk * kq, chunk, Qs.p + (B - 1) * kq, ls, 0.0,
+                 Q + (B - 1) * chunk, ldq, false);
+        }
+        c.counts = saved;
         return;
     }
     // ---- <= 32 columns: one panel launch ----

@@ -318,7 +318,9 @@ ShardOut round_fixed_krp_sharded(Ctx& c, const ttr_comm& cm, const TTDev& t, con
             PhaseScope ph(c, kPhaseGemm);
             if (k < d - 1) {
                 Vnext[q] = DBuf(c, static_cast<std::size_t>(std::max<i64>(1, nj * l * r1)));
-                if (nj)
+                if (nj == n1)  // one rank owns every slice: the one-GPU contract_first GEMM, same bits
+                    gemm(c, false, l, n1 * r1, cols, 1.0, M.p, l, X, cols, 0.0, Vnext[q].p, l);
+                else if (nj)
                     gemm_batched(c, false, l, r1, cols, 1.0, M.p, l, 0, X + j0 * cols, cols * n1, cols, 0.0, Vnext[q].p,
                                  nj * l, l, nj);
             } else {  // last core (r_d = 1): l x nj, the local columns of V(Y_d)
