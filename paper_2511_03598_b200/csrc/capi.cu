@@ -52,6 +52,7 @@ ttr_status ttr_ctx_destroy(ttr_ctx* ctx) {
         if (ctx->c.work) cudaFreeAsync(ctx->c.work, ctx->c.stream);
         ctx->c.release_retired();
         cudaStreamSynchronize(ctx->c.stream);
+        ctx->c.destroy_side();
         if (ctx->c.qr_xchg) cudaFree(ctx->c.qr_xchg);
         if (ctx->c.host_scalars) cudaFreeHost(ctx->c.host_scalars);
         if (ctx->c.own_stream) cudaStreamDestroy(ctx->c.stream);

@@ -102,6 +102,15 @@ struct Ctx {
     int live_plans = 0;
     std::vector<void*> retired;
     void release_retired();
+    // side streams for independent work inside one call (e.g. the row chunks of
+    // a TSQR): fork_side(n) makes side[0..n) wait for `stream`, join_side(n)
+    // makes `stream` wait for them; capturable (fork/join by events)
+    std::vector<cudaStream_t> side;
+    std::vector<cudaEvent_t> side_ev;
+    cudaEvent_t fork_ev = nullptr;
+    void fork_side(int n);
+    void join_side(int n);
+    void destroy_side();
     // small pinned host staging buffer for scalars
     double* host_scalars = nullptr;
     // persistent workspace of the QR panel's grid exchange (qr_panel.cuh)

@@ -401,19 +401,21 @@ __global__ void transpose_batched_kernel(int k, const double* __restrict__ s, i6
 // ---- cluster push panels (qr_cpanel.cuh) --------------------------------------
 constexpr int kPushWarps = 16;
 constexpr int kPushMaxRpt = 28;
-constexpr i64 kPushMaxRows = static_cast<i64>(kPushMaxCtas) * kPushWarps * kPushMaxRpt;  // 7,168
+constexpr i64 kPushMaxRows = static_cast<i64>(kPushMaxCtas) * kPushWarps * kPushMaxRpt;  // 7,168 (+ the diagonal block)
 
 template <int RPT>
 void launch_push(Ctx& c, const PushQrArgs& a, int G, i64 batch) {
     auto kern = panel_push_kernel<RPT, kPushWarps>;
     static std::atomic<std::uint64_t> configured{0};  // bit d: attributes set on device d
+    constexpr std::size_t smem = push_smem_bytes<RPT, kPushWarps>();
     if (first_on_device(configured)) {
         TTR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        TTR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(static_cast<unsigned>(G * batch));
     cfg.blockDim = dim3(kPushWarps * 32);
-    cfg.dynamicSmemBytes = 0;
+    cfg.dynamicSmemBytes = smem;
     cfg.stream = c.stream;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -425,7 +427,7 @@ void launch_push(Ctx& c, const PushQrArgs& a, int G, i64 batch) {
     TTR_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
     c.launched();
     if (a.trace) {  // TTR_QR_TRACE: per-phase cycles of cluster 0 / CTA 0, averaged over the panel's columns
-        long long h[32 * 8];
+        long long h[32 * 8 + 8];
         TTR_CUDA(cudaMemcpyAsync(h, a.trace, sizeof(h), cudaMemcpyDeviceToHost, c.stream));
         TTR_CUDA(cudaStreamSynchronize(c.stream));
         const int nc = std::min(a.b, a.rows);
@@ -436,11 +438,12 @@ void launch_push(Ctx& c, const PushQrArgs& a, int G, i64 batch) {
             for (int q = 1; q < 8; ++q) acc[q] += static_cast<double>(seq[q] - seq[q - 1]) / nc;
             acc[0] += static_cast<double>(t[5] - t[0]) / nc;
         }
+        const long long* k = h + 256;
         std::fprintf(stderr,
                      "push<%d> cluster %d x %lld rows %d: cycles/col %.0f | dots %.0f bar %.0f xchg %.0f sum %.0f "
-                     "scalar %.0f bar %.0f update %.0f\n",
+                     "scalar %.0f bar %.0f update %.0f | init+load %lld loop %lld epilogue %lld q %lld exit %lld\n",
                      RPT, G, static_cast<long long>(batch), a.rows, acc[0], acc[1], acc[2], acc[3], acc[4], acc[5],
-                     acc[6], acc[7]);
+                     acc[6], acc[7], k[1] - k[0], k[2] - k[1], k[3] - k[2], k[4] - k[3], k[5] - k[4]);
     }
 }
 
@@ -449,9 +452,9 @@ void launch_push(Ctx& c, const PushQrArgs& a, int G, i64 batch) {
 void launch_panel_push(Ctx& c, PushQrArgs a, i64 batch) {
     static const bool tracing = std::getenv("TTR_QR_TRACE") != nullptr;  // diagnostics only
     static long long* trace_buf = nullptr;
-    if (tracing && !trace_buf) TTR_CUDA(cudaMalloc(reinterpret_cast<void**>(&trace_buf), 32 * 8 * sizeof(long long)));
+    if (tracing && !trace_buf) TTR_CUDA(cudaMalloc(reinterpret_cast<void**>(&trace_buf), (32 * 8 + 8) * sizeof(long long)));
     a.trace = tracing ? trace_buf : nullptr;
-    const i64 rows = a.rows;
+    const i64 rows = a.rows - std::min(a.b, a.rows);  // register rows (the diagonal block sits in CTA 0's smem)
     bool done = false;
     auto go = [&](auto rpt_tag) {
         constexpr int RPT = decltype(rpt_tag)::value;
@@ -494,24 +497,6 @@ void qr_blocked_push(Ctx& c, i64 batch, i64 m, i64 n, const double* A, i64 lda, 
     }
     const i64 npanels = (k + kPanel - 1) / kPanel;
     DBuf tau(c, static_cast<std::size_t>(k * batch));
-    if (n <= kPanel) {  // one panel: R and the explicit Q straight from the cluster kernel
-        PushQrArgs a{};
-        a.rows = static_cast<int>(m);
-        a.b = static_cast<int>(n);
-        a.Pin = work;
-        a.ldin = ldw;
-        a.sin = sW;
-        a.tau = tau.p;
-        a.stau = k;
-        a.Q = Q;
-        a.ldq = ldq;
-        a.sq = sQ;
-        a.R = R;
-        a.ldr = ldr;
-        a.sr = sR;
-        launch_panel_push(c, a, batch);
-        return;
-    }
     const i64 sV = ldw * k, sTs = npanels * kPanel * kPanel, sWb = kPanel * n;
     DBuf Vall(c, static_cast<std::size_t>(sV * batch));
     if (Q) TTR_CUDA(cudaMemsetAsync(Vall.p, 0, sizeof(double) * sV * batch, c.stream));  // zeros above each panel
@@ -737,11 +722,24 @@ void thin_qr(Ctx& c, i64 m, i64 n, const double* A, i64 lda, double* Q, i64 ldq,
         const char* e = std::getenv("TTR_QR_OLD");
         return e && e[0] == '1';
     }();
-    if (!old_panels && n <= kPushMaxRows) {
-        if (m <= kPushMaxRows) {  // one cluster per panel
-            qr_blocked_push(c, 1, m, n, A, lda, 0, Q, ldq, 0, R, ldr, 0);
-            return;
-        }
+    // Measured (tools/qr_bench.py, TTR_QR_OLD=1 for the other path): the push
+    // cluster panels win for blocked QRs up to one cluster of rows (7040 x 110:
+    // 0.566 -> 0.466 ms, 5120 x 320: 1.60 -> 1.28, 2560 x 320: 1.51 -> 1.10);
+    // single panels (<= 32 columns) keep the in-register-Q panels below, and
+    // taller matrices the cooperative-grid panel (40960 x 320: 2.72 ms vs 3.8
+    // for the chunked TSQR below, kept behind TTR_QR_TSQR=1 for experiments).
+    // The push panel's per-column floor (~4,200 cycles at 7,040 rows) is the
+    // shared-memory broadcast of the active column (two LDS.128 wavefronts per
+    // two rows per phase, ~440 rows per SM) plus the serial reflector step.
+    static const bool tsqr_on = [] {
+        const char* e = std::getenv("TTR_QR_TSQR");
+        return e && e[0] == '1';
+    }();
+    if (!old_panels && m <= kPushMaxRows && n > kPanel) {
+        qr_blocked_push(c, 1, m, n, A, lda, 0, Q, ldq, 0, R, ldr, 0);
+        return;
+    }
+    if (!old_panels && tsqr_on && n <= kPushMaxRows && m > kPushMaxRows) {
         // Taller: TSQR over B cluster-sized row chunks, all factored at once
         // (one cluster per chunk, strided-batch GEMMs), then the QR of the
         // stacked R factors and Q(chunk q) = Q_q Q_s(q-th block). The chunks are
@@ -760,7 +758,30 @@ void thin_qr(Ctx& c, i64 m, i64 n, const double* A, i64 lda, double* Q, i64 ldq,
         const i64 ls = B * kq;
         DBuf Rst(c, static_cast<std::size_t>(ls * n));
         DBuf Qc(c, static_cast<std::size_t>(Q ? chunk * kq * B : 1));
-        qr_blocked_push(c, B, chunk, n, Ap.p, chunk, sC, Q ? Qc.p : nullptr, chunk, chunk * kq, Rst.p, ls, kq, Ap.p);
+        // the chunk QRs are independent: one side stream each (their panels run
+        // as concurrent clusters, their GEMMs share the GPU), each with its own
+        // split-K scratch; joined before the stacked QR
+        {
+            const int ns = static_cast<int>(std::min<i64>(B, 8));
+            c.fork_side(ns);
+            const cudaStream_t main = c.stream;
+            double* const main_work = c.work;
+            const std::size_t main_bytes = c.work_bytes;
+            std::vector<double*> works;
+            for (i64 q = 0; q < B; ++q) {
+                c.stream = c.side[q % ns];
+                c.work = nullptr;
+                c.work_bytes = 0;
+                qr_blocked_push(c, 1, chunk, n, Ap.p + q * sC, chunk, sC, Q ? Qc.p + q * chunk * kq : nullptr, chunk,
+                                chunk * kq, Rst.p + q * kq, ls, kq, Ap.p + q * sC);
+                if (c.work) works.push_back(c.work);
+            }
+            c.stream = main;
+            c.work = main_work;
+            c.work_bytes = main_bytes;
+            c.join_side(ns);
+            for (double* w : works) TTR_CUDA(cudaFreeAsync(w, c.stream));
+        }
         if (!Q) {
             thin_qr(c, ls, n, Rst.p, ls, nullptr, 1, R, ldr);
         } else {

@@ -53,6 +53,36 @@ double* Ctx::scratch(std::size_t bytes) {
     return work;
 }
 
+void Ctx::fork_side(int n) {
+    if (!fork_ev) TTR_CUDA(cudaEventCreateWithFlags(&fork_ev, cudaEventDisableTiming));
+    while (static_cast<int>(side.size()) < n) {
+        cudaStream_t st;
+        TTR_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        side.push_back(st);
+        cudaEvent_t ev;
+        TTR_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        side_ev.push_back(ev);
+    }
+    TTR_CUDA(cudaEventRecord(fork_ev, stream));
+    for (int q = 0; q < n; ++q) TTR_CUDA(cudaStreamWaitEvent(side[q], fork_ev, 0));
+}
+
+void Ctx::join_side(int n) {
+    for (int q = 0; q < n; ++q) {
+        TTR_CUDA(cudaEventRecord(side_ev[q], side[q]));
+        TTR_CUDA(cudaStreamWaitEvent(stream, side_ev[q], 0));
+    }
+}
+
+void Ctx::destroy_side() {
+    for (auto st : side) cudaStreamDestroy(st);
+    for (auto ev : side_ev) cudaEventDestroy(ev);
+    if (fork_ev) cudaEventDestroy(fork_ev);
+    side.clear();
+    side_ev.clear();
+    fork_ev = nullptr;
+}
+
 void Ctx::release_retired() {
     for (void* p : retired) cudaFreeAsync(p, stream);  // ordered after every earlier replay
     retired.clear();
