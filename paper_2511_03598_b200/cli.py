@@ -1,10 +1,12 @@
-"""Command-line drop-in for the reference CLI's `round` command
-(tools/ttround_main.cpp:86-184): round a TTF1 file on the B200 and print the
-same JSON record (algorithm, mode, target, rel_error, ranks, wall_seconds,
-flops_total/gemm/qr/svd/sketch, rng_draws, seed).
+"""Command-line drop-in for the reference CLI's `round` and `bench-synthetic`
+commands (tools/ttround_main.cpp:86-210): round a TTF1 file on the B200 and
+print the same JSON record (algorithm, mode, target, rel_error, ranks,
+wall_seconds, flops_total/gemm/qr/svd/sketch, rng_draws, seed), or sweep the
+synthetic benchmark into the same CSV schema.
 
     python -m paper_2511_03598_b200.cli round IN.ttf1 OUT.ttf1 --algo krp-fix --ranks 10 10 10 --seed 7
     python -m paper_2511_03598_b200.cli round IN.ttf1 OUT.ttf1 --algo krp-adapt-r --tol 1e-6
+    python -m paper_2511_03598_b200.cli bench-synthetic --d 5 --n 20 --rank 10 --targets 10,12 --tols 1e-4 --csv b.csv
 
 Algorithms: det, krp-fix, rand-orth, krp-adapt, krp-adapt-r (dispatch_rounding,
 ttround_main.cpp:86-119). `--rng xoshiro` (default) reproduces the reference's
@@ -74,6 +76,83 @@ def cmd_round(args) -> int:  # ttround_main.cpp:142-184
     return 0
 
 
+BENCH_CSV_HEADER = ("algorithm,mode,target,rel_error,ranks,wall_seconds,flops_total,flops_gemm,flops_qr,"
+                    "flops_svd,flops_sketch,rng_draws,seed")  # ttround_main.cpp:75-77
+
+
+def fmt17(v: float) -> str:  # ttround_main.cpp:33-37
+    return "%.17g" % v
+
+
+def run_rounding(ctx, algo, x, targets, tol, seed, rng):  # ttround_main.cpp:121-140
+    ctx.reset_counters()
+    ctx.synchronize()
+    t0 = time.perf_counter()
+    y = dispatch_rounding(algo, x, targets, tol, seed, rng)
+    ctx.synchronize()
+    wall = time.perf_counter() - t0
+    cnt = ctx.counters()
+    return {"algorithm": algo, "mode": "ranks" if targets else "tolerance",
+            "target": float(max(targets)) if targets else tol, "rel_error": relative_error(x, y),
+            "ranks": y.ranks(), "wall_seconds": wall, "counts": cnt, "seed": seed}
+
+
+def csv_row(r) -> str:  # ttround_main.cpp:79-84
+    c = r["counts"]
+    return ",".join([r["algorithm"], r["mode"], fmt17(r["target"]), fmt17(r["rel_error"]),
+                     "x".join(str(v) for v in r["ranks"]), fmt17(r["wall_seconds"]), str(c.total()), str(c.gemm),
+                     str(c.qr), str(c.svd), str(c.sketch), str(c.rng), str(r["seed"])])
+
+
+def synthetic_perturbed_tt(ctx, d, n, r, eps, seed):
+    """synthetic.cpp:8-26 on the device: Y, Z Gaussian TTs (reference stream, shared rank
+    chain) normalised by norm_exact, X = formal_sum(Y, eps Z)."""
+    from . import formal_sum, norm_exact, scaled
+    from .seeds import derive_seed
+    ranks = [1] + [r] * (d - 1) + [1]
+    y = TTTensor.random_gaussian([n] * d, ranks, derive_seed(seed, 1), ctx)
+    z = TTTensor.random_gaussian([n] * d, ranks, derive_seed(seed, 2), ctx)
+    y = scaled(y, 1.0 / norm_exact(y))
+    z = scaled(z, 1.0 / norm_exact(z))
+    return formal_sum([y, scaled(z, eps)])
+
+
+# Orth-Rand (round_orth_rand, round_rand.cpp:181-240) is outside this repo's
+# scope (SURVEY §2 row 8): its rows are not produced.
+OMITTED = ["orth-rand"]
+
+
+def cmd_bench_synthetic(args) -> int:  # ttround_main.cpp:178-210
+    d, n, rank, eps, seeds = args.d, args.n, args.rank, args.eps_pert, args.seeds
+    if d < 2 or n < 1 or rank < 1 or eps < 0 or seeds < 1:
+        raise TTRoundError(14, "InvalidArgument: invalid benchmark parameters")
+    targets = [int(v) for v in args.targets.split(",")] if args.targets else []
+    tols = [float(v) for v in args.tols.split(",")] if args.tols else []
+    if not targets and not tols:
+        raise TTRoundError(14, "InvalidArgument: need --targets or --tols")
+    ctx = Context(args.device)
+    x = synthetic_perturbed_tt(ctx, d, n, rank, eps, args.master_seed)
+    rng = RNG_XOSHIRO if args.rng == "xoshiro" else RNG_PHILOX
+    try:
+        f = open(args.csv, "w")
+    except OSError:
+        raise TTRoundError(15, f"IoError: cannot open {args.csv}")
+    with f:
+        f.write(BENCH_CSV_HEADER + "\n")
+        for target in targets:
+            tr = [target] * (d - 1)
+            for seed in range(seeds):
+                for algo in ("det", "krp-fix", "rand-orth"):
+                    f.write(csv_row(run_rounding(ctx, algo, x, tr, None, seed, rng)) + "\n")
+        for tol in tols:
+            for seed in range(seeds):
+                for algo in ("det", "krp-adapt", "krp-adapt-r"):
+                    f.write(csv_row(run_rounding(ctx, algo, x, None, tol, seed, rng)) + "\n")
+    print(json.dumps({"csv": args.csv, "d": d, "n": n, "rank": rank, "eps_pert": eps, "x_ranks": x.ranks(),
+                      "omitted_algorithms": OMITTED}))
+    return 0
+
+
 def main(argv=None) -> int:
     ap = argparse.ArgumentParser(prog="ttround-b200")
     sub = ap.add_subparsers(dest="cmd", required=True)
@@ -86,8 +165,22 @@ def main(argv=None) -> int:
     r.add_argument("--seed", type=int, default=0)
     r.add_argument("--rng", default="xoshiro", choices=["xoshiro", "philox"])
     r.add_argument("--device", type=int, default=0)
+    b = sub.add_parser("bench-synthetic", help="rounding benchmark on perturbed low-rank tensors")
+    b.add_argument("--d", type=int, default=5)
+    b.add_argument("--n", type=int, default=20)
+    b.add_argument("--rank", type=int, default=10)
+    b.add_argument("--eps-pert", type=float, default=1e-5)
+    b.add_argument("--targets", default="")
+    b.add_argument("--tols", default="")
+    b.add_argument("--seeds", type=int, default=10)
+    b.add_argument("--csv", default="bench.csv")
+    b.add_argument("--master-seed", type=int, default=20250807)
+    b.add_argument("--rng", default="xoshiro", choices=["xoshiro", "philox"])
+    b.add_argument("--device", type=int, default=0)
     args = ap.parse_args(argv)
     try:
+        if args.cmd == "bench-synthetic":
+            return cmd_bench_synthetic(args)
         return cmd_round(args)
     except TTRoundError as e:
         print(f"ttround error: {e}", file=sys.stderr)

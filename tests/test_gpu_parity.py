@@ -620,6 +620,40 @@ def test_cli_round_matches_api(P, O, tmp_path):
     assert bad.returncode == 2 and "IoError" in bad.stderr
 
 
+def test_cli_bench_synthetic(P, O, tmp_path):
+    """`bench-synthetic` (ttround_main.cpp:178-210 mirror): the synthetic instance is
+    the oracle's synthetic_perturbed_tt bit for bit (reference stream), the CSV has the
+    reference header and one row per (target|tol, seed, algorithm) — Orth-Rand rows
+    omitted (out of scope) — and the krp-fix rows equal the oracle's round_fixed_krp
+    of that instance with the same seed."""
+    import csv
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = tmp_path / "b.csv"
+    cmd = [sys.executable, "-m", "paper_2511_03598_b200.cli", "bench-synthetic", "--d", "4", "--n", "10", "--rank",
+           "5", "--eps-pert", "1e-5", "--targets", "5,6", "--tols", "1e-3", "--seeds", "2", "--csv", str(out)]
+    res = subprocess.run(cmd, capture_output=True, text=True, cwd=root)
+    assert res.returncode == 0, res.stderr
+    summ = json.loads(res.stdout.strip().splitlines()[-1])
+    assert summ["x_ranks"] == [1, 10, 10, 10, 1] and summ["omitted_algorithms"] == ["orth-rand"]
+    rows = list(csv.reader(open(out)))
+    assert ",".join(rows[0]) == ("algorithm,mode,target,rel_error,ranks,wall_seconds,flops_total,flops_gemm,"
+                                 "flops_qr,flops_svd,flops_sketch,rng_draws,seed")
+    body = rows[1:]
+    assert len(body) == 2 * 2 * 3 + 1 * 2 * 3
+    syn = O.synthetic_perturbed_tt(4, 10, 5, 1e-5, 20250807)
+    for r in body:
+        if r[0] == "krp-fix":
+            ref = O.round_fixed_krp(syn, [int(float(r[2]))] * 3, int(r[12]), rng=O.XOSHIRO)
+            assert r[4] == "x".join(str(v) for v in ref.ranks)
+            assert abs(float(r[3]) - O.relative_error(syn, ref)) <= 1e-8 * max(1e-12, float(r[3])) + 1e-15
+    bad = subprocess.run(cmd[:4] + ["--d", "1"], capture_output=True, text=True, cwd=root)
+    assert bad.returncode == 2 and "InvalidArgument" in bad.stderr
+
+
 # ---- BASELINE full sizes: size-independent properties ------------------------------------------
 
 @pytest.mark.parametrize("cfg", ["3", "5b"])
