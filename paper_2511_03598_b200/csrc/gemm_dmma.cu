@@ -413,6 +413,14 @@ bool narrow_lr() {
     return on;
 }
 
+bool krp_wide_tiles() {
+    static const bool on = [] {
+        const char* e = std::getenv("TTR_KRP_WIDE");  // experiments: TTR_KRP_WIDE=0 keeps 128 x 64 KRP tiles
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 bool tma_enabled() {
     static const bool on = [] {
         const char* e = std::getenv("TTR_GEMM_TMA");  // experiments: TTR_GEMM_TMA=0 selects the cp.async kernel
@@ -421,9 +429,9 @@ bool tma_enabled() {
     return on;
 }
 
-template <int BM, int BN, bool AT, int KM, int ST = 4>
+template <int BM, int BN, bool AT, int KM, int ST = 4, int WN = 32>
 bool launch_tma(Ctx& c, GemmArgs& a, int splits) {
-    using C_ = TmaCfg<BM, BN, AT, KM, ST>;
+    using C_ = TmaCfg<BM, BN, AT, KM, ST, WN>;
     static const bool prec = [] {
         const char* e = std::getenv("TTR_GEMM_PREC");  // experiments: 0 = C read after the main loop
         return !(e && e[0] == '0');
@@ -436,7 +444,7 @@ bool launch_tma(Ctx& c, GemmArgs& a, int splits) {
         (KM == 1 ? make_map(&mB, a.B, a.nmode, a.N, a.ldb, 16, BN, true) : make_map(&mB, a.B, a.K, a.N, a.ldb, 16, BN, true)) &&
         (KM != 1 || make_map(&mW, a.Wt, a.N, a.K / a.nmode, a.ldw, BN, 1, false));
     if (!ok) return false;
-    auto kern = dgemm_tma_kernel<BM, BN, AT, KM, ST>;
+    auto kern = dgemm_tma_kernel<BM, BN, AT, KM, ST, WN>;
     static std::atomic<std::uint64_t> configured{0};  // bit d: attributes set on device d
     if (first_on_device(configured)) {
         TTR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C_::kSmemBytes));
@@ -539,7 +547,17 @@ void run_gemm(Ctx& c, bool AT, int KM, int BK, GemmArgs& a, bool va2, bool vb2, 
         // narrow KRP products (adaptive appends, N <= 32): 32-column tiles; the
         // per-column summation order is the same as with 64 (append == one-shot)
         else if (!medium && KM == 1 && !AT && a.N <= 32) done = launch_tma<128, 32, false, 1>(c, a, splits);
-        else if (!medium && KM == 1 && !AT) done = launch_tma<128, 64, false, 1>(c, a, splits);
+        else if (!medium && KM == 1 && !AT) {
+            // shape-adaptive KRP tiles: 64 x 112 (warp tiles 32 x 56) when they
+            // pad M x N less than 128 x 64 (config 3: 400 x 110 -> 448 x 112
+            // instead of 512 x 128); the split count is a function of (M, K)
+            // only and the per-column k order is the tile's, so columns stay
+            // bitwise independent of N (append == one-shot)
+            const i64 pad_a = (a.M + 127) / 128 * 128 * ((a.N + 63) / 64 * 64);
+            const i64 pad_b = (a.M + 63) / 64 * 64 * ((a.N + 111) / 112 * 112);
+            if (krp_wide_tiles() && pad_b * 20 < pad_a * 19) done = launch_tma<64, 112, false, 1, 4, 56>(c, a, splits);
+            else done = launch_tma<128, 64, false, 1>(c, a, splits);
+        }
     }
     const bool narrow = a.batch > 1 && narrow_tiles();
     if (done) {

@@ -82,10 +82,11 @@ __device__ __forceinline__ int tma_kperm(int q, int fc) {
     return static_cast<int>((kTab >> (4 * (4 * q + fc))) & 0xF);
 }
 
-template <int BM, int BN, bool AT, int KM, int STAGES>
+template <int BM, int BN, bool AT, int KM, int STAGES, int WN = 32>
 struct TmaCfg {
     static constexpr int BK = 16;
-    static constexpr int kWarpsM = BM / 32, kWarpsN = BN / 32;
+    static constexpr int kWarpsM = BM / 32, kWarpsN = BN / WN;  // warp tile 32 x WN (WN = 32 or 56)
+    static_assert(BN % WN == 0 && WN % 8 == 0, "warp tiles of whole n8 fragments");
     static constexpr int kThreads = kWarpsM * kWarpsN * 32;
     static constexpr int kABytes = BM * BK * 8, kBBytes = BN * BK * 8, kWBytes = KM == 1 ? BN * 8 : 0;
     static constexpr int kStageBytes = kABytes + kBBytes + 1024;  // W row in the padded tail
@@ -95,12 +96,12 @@ struct TmaCfg {
     static_assert(KM != 1 || STAGES >= 3, "KRP scaling runs one k-tile ahead of the consumers");
 };
 
-template <int BM, int BN, bool AT, int KM, int STAGES>
-__global__ void __launch_bounds__((BM / 32) * (BN / 32) * 32)
+template <int BM, int BN, bool AT, int KM, int STAGES, int WN = 32>
+__global__ void __launch_bounds__((BM / 32) * (BN / WN) * 32)
     dgemm_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ CUtensorMap tmW, const GemmArgs p) {
-    using C_ = TmaCfg<BM, BN, AT, KM, STAGES>;
-    constexpr int BK = C_::BK, FM = 4, FN = 4, NWARP = C_::kWarpsM * C_::kWarpsN;
+    using C_ = TmaCfg<BM, BN, AT, KM, STAGES, WN>;
+    constexpr int BK = C_::BK, FM = 4, FN = WN / 8, NWARP = C_::kWarpsM * C_::kWarpsN;
     extern __shared__ unsigned char smem_raw[];
     unsigned char* smem =
         reinterpret_cast<unsigned char*>((reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) & ~std::uintptr_t(1023));
@@ -110,7 +111,7 @@ __global__ void __launch_bounds__((BM / 32) * (BN / 32) * 32)
     std::uint64_t* scaled = empty + STAGES;  // KM = 1: Omega tile of the stage scaled by W
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int wm0 = (warp % C_::kWarpsM) * 32, wn0 = (warp / C_::kWarpsM) * 32;
+    const int wm0 = (warp % C_::kWarpsM) * 32, wn0 = (warp / C_::kWarpsM) * WN;
     const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
     if (p.upper && m0 >= n0 + BN) return;  // tile strictly below the diagonal: not needed
     const int zsplit = static_cast<int>(blockIdx.z);
@@ -202,17 +203,20 @@ __global__ void __launch_bounds__((BM / 32) * (BN / 32) * 32)
         const int ss = kt_s % STAGES;
         tma::mbar_wait(full + ss, (kt_s / STAGES) & 1);
         const unsigned sB = smem_s + ss * C_::kStageBytes + C_::kABytes;
-        constexpr int kRowsPerWarp = BN / NWARP;  // 8 (128x64)
-        static_assert(KM != 1 || kRowsPerWarp == 8, "two rows of 8 chunks per lane group");
-        const int n = warp * kRowsPerWarp + (lane >> 3);
-        const double w0 = tma::lds64(sB + C_::kBBytes + n * 8);
-        const double w1 = tma::lds64(sB + C_::kBBytes + (n + 4) * 8);
-        const unsigned a = sB + n * 128 + (lane & 7) * 16;
-        double v0, v1, v2, v3;
-        asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n" : "=d"(v0), "=d"(v1) : "r"(a));
-        asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n" : "=d"(v2), "=d"(v3) : "r"(a + 512));
-        asm volatile("st.shared.v2.f64 [%0], {%1, %2};\n" ::"r"(a), "d"(v0 * w0), "d"(v1 * w0) : "memory");
-        asm volatile("st.shared.v2.f64 [%0], {%1, %2};\n" ::"r"(a + 512), "d"(v2 * w1), "d"(v3 * w1) : "memory");
+        static_assert(KM != 1 || BN % 8 == 0, "groups of 8 rows (two rows of 8 chunks per lane group)");
+        // each warp scales 8-row groups warp, warp + NWARP, ... (128x64: exactly one)
+#pragma unroll
+        for (int r8 = warp * 8; r8 < BN; r8 += NWARP * 8) {
+            const int n = r8 + (lane >> 3);
+            const double w0 = tma::lds64(sB + C_::kBBytes + n * 8);
+            const double w1 = tma::lds64(sB + C_::kBBytes + (n + 4) * 8);
+            const unsigned a = sB + n * 128 + (lane & 7) * 16;
+            double v0, v1, v2, v3;
+            asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n" : "=d"(v0), "=d"(v1) : "r"(a));
+            asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n" : "=d"(v2), "=d"(v3) : "r"(a + 512));
+            asm volatile("st.shared.v2.f64 [%0], {%1, %2};\n" ::"r"(a), "d"(v0 * w0), "d"(v1 * w0) : "memory");
+            asm volatile("st.shared.v2.f64 [%0], {%1, %2};\n" ::"r"(a + 512), "d"(v2 * w1), "d"(v3 * w1) : "memory");
+        }
         tma::mbar_arrive(scaled + ss);
     };
     if constexpr (KM == 1) {
