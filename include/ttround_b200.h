@@ -284,11 +284,22 @@ ttr_status ttr_philox_factor(ttr_ctx* ctx, uint64_t seed, int64_t mode, int64_t 
  * the device (linalg::thin_qr, linalg.hpp:22-25). q: m x n, r: n x n. */
 ttr_status ttr_thin_qr(ttr_ctx* ctx, int64_t m, int64_t n, const double* host_a, double* host_q,
                        double* host_r);
+/* Shifted Cholesky QR (sCQR3, the sweep's speculative QR; qr_chol.cu) of a
+ * host m x n matrix (m >= n, n <= 416): q m x n, r n x n upper. *breakdown = 1
+ * when a Cholesky factorisation broke down or the third Gram matrix was far
+ * from I (q and r are then unusable; the rounding entry points redo such a
+ * call on the Householder path). No reference counterpart: a test hook. */
+ttr_status ttr_thin_qr_cholesky(ttr_ctx* ctx, int64_t m, int64_t n, const double* host_a, double* host_q,
+                                double* host_r, int* breakdown);
 /* Device-pointer variants (column-major, caller-owned device memory, ordered
  * on the context stream, no synchronisation): thin QR (Q and/or R may be
  * NULL) and C = alpha op(A) B + beta C. */
 ttr_status ttr_dev_thin_qr(ttr_ctx* ctx, int64_t m, int64_t n, const double* dA, int64_t lda, double* dQ,
                            int64_t ldq, double* dR, int64_t ldr);
+/* sCQR3 on device pointers (Q may alias A; R may be NULL); *breakdown is read
+ * after a stream synchronisation. */
+ttr_status ttr_dev_thin_qr_cholesky(ttr_ctx* ctx, int64_t m, int64_t n, const double* dA, int64_t lda, double* dQ,
+                                    int64_t ldq, double* dR, int64_t ldr, int* breakdown);
 ttr_status ttr_dev_gemm(ttr_ctx* ctx, int trans_a, int64_t m, int64_t n, int64_t k, double alpha,
                         const double* dA, int64_t lda, const double* dB, int64_t ldb, double beta,
                         double* dC, int64_t ldc);

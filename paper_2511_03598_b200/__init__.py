@@ -685,6 +685,19 @@ def thin_qr(a: np.ndarray, ctx: Optional[Context] = None):
     return q.reshape(k, m).T.copy(), r.reshape(n, k).T.copy()
 
 
+def thin_qr_cholesky(a: np.ndarray, ctx: Optional[Context] = None):
+    """sCQR3 on the device (qr_chol.cu): (q, r, breakdown)."""
+    ctx = ctx or default_context()
+    m, n = a.shape
+    flat = np.ascontiguousarray(np.asarray(a, dtype=np.float64).T).reshape(-1)
+    q = np.empty(m * n)
+    r = np.empty(n * n)
+    bd = C.c_int(0)
+    _check(lib().ttr_thin_qr_cholesky(ctx._h, C.c_int64(m), C.c_int64(n), _dptr(flat), _dptr(q), _dptr(r),
+                                      C.byref(bd)))
+    return q.reshape(n, m).T.copy(), r.reshape(n, n).T.copy(), bool(bd.value)
+
+
 def gemm(a: np.ndarray, b: np.ndarray, trans_a: bool = False, ctx: Optional[Context] = None) -> np.ndarray:
     ctx = ctx or default_context()
     if trans_a:

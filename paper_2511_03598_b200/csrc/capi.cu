@@ -54,6 +54,7 @@ ttr_status ttr_ctx_destroy(ttr_ctx* ctx) {
         cudaStreamSynchronize(ctx->c.stream);
         ctx->c.destroy_side();
         if (ctx->c.qr_xchg) cudaFree(ctx->c.qr_xchg);
+        if (ctx->c.qr_flag) cudaFree(ctx->c.qr_flag);
         if (ctx->c.host_scalars) cudaFreeHost(ctx->c.host_scalars);
         if (ctx->c.own_stream) cudaStreamDestroy(ctx->c.stream);
         delete ctx;
@@ -486,6 +487,33 @@ ttr_status ttr_thin_qr(ttr_ctx* ctx, int64_t m, int64_t n, const double* host_a,
         if (host_q) TTR_CUDA(cudaMemcpyAsync(host_q, q.p, sizeof(double) * m * k, cudaMemcpyDeviceToHost, ctx->c.stream));
         if (host_r) TTR_CUDA(cudaMemcpyAsync(host_r, r.p, sizeof(double) * k * n, cudaMemcpyDeviceToHost, ctx->c.stream));
         TTR_CUDA(cudaStreamSynchronize(ctx->c.stream));
+    });
+}
+
+ttr_status ttr_thin_qr_cholesky(ttr_ctx* ctx, int64_t m, int64_t n, const double* host_a, double* host_q,
+                                double* host_r, int* breakdown) {
+    return guard_ctx(ctx, [&] {
+        need(ctx && host_a && breakdown, "null argument");
+        need(cholqr_fits(m, n), "shape outside the Cholesky-QR path (m >= n, n <= 416)");
+        DBuf a(ctx->c, static_cast<std::size_t>(m * n)), q(ctx->c, static_cast<std::size_t>(m * n)),
+            r(ctx->c, static_cast<std::size_t>(n * n));
+        TTR_CUDA(cudaMemcpyAsync(a.p, host_a, sizeof(double) * m * n, cudaMemcpyHostToDevice, ctx->c.stream));
+        ctx->c.qr_flag_reset();
+        thin_qr_cholesky(ctx->c, m, n, a.p, m, q.p, m, r.p, n);
+        if (host_q) TTR_CUDA(cudaMemcpyAsync(host_q, q.p, sizeof(double) * m * n, cudaMemcpyDeviceToHost, ctx->c.stream));
+        if (host_r) TTR_CUDA(cudaMemcpyAsync(host_r, r.p, sizeof(double) * n * n, cudaMemcpyDeviceToHost, ctx->c.stream));
+        *breakdown = ctx->c.qr_flag_read() >= 0 ? 1 : 0;
+    });
+}
+
+ttr_status ttr_dev_thin_qr_cholesky(ttr_ctx* ctx, int64_t m, int64_t n, const double* dA, int64_t lda, double* dQ,
+                                    int64_t ldq, double* dR, int64_t ldr, int* breakdown) {
+    return guard_ctx(ctx, [&] {
+        need(ctx && dA && dQ && breakdown, "null argument");
+        need(cholqr_fits(m, n) && lda >= m && ldq >= m && (!dR || ldr >= n), "bad shape");
+        ctx->c.qr_flag_reset();
+        thin_qr_cholesky(ctx->c, m, n, dA, lda, dQ, ldq, dR, ldr);
+        *breakdown = ctx->c.qr_flag_read() >= 0 ? 1 : 0;
     });
 }
 

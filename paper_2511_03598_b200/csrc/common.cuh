@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <climits>
 #include <cstdint>
 #include <stdexcept>
 #include <string>
@@ -116,6 +117,17 @@ struct Ctx {
     // persistent workspace of the QR panel's grid exchange (qr_panel.cuh)
     unsigned long long* qr_xchg = nullptr;
     unsigned long long* qr_exchange();
+    // Cholesky-QR speculation (qr_chol.cu): qr_spec lets the Rand-Orth sweep
+    // take the shifted Cholesky QR for modes < qr_hh_from (set by callers that
+    // check the breakdown flag afterwards, with_qr_speculation);
+    // qr_spec_used records that it did. The flag holds the smallest mode whose
+    // factorisation broke down (kQrNoBreakdown: none).
+    bool qr_spec = false, qr_spec_used = false;
+    i64 qr_hh_from = INT32_MAX;
+    int* qr_flag = nullptr;
+    int* qr_flag_dev();
+    void qr_flag_reset();
+    int qr_flag_read();  // smallest broken-down tag or -1; synchronises the stream
 
     void charge_gemm(std::uint64_t f) { counts.gemm += f; if (sketch_depth) counts.sketch += f; }
     void charge_qr(std::uint64_t f) { counts.qr += f; if (sketch_depth) counts.sketch += f; }
@@ -237,6 +249,16 @@ void scale_rows_cols(Ctx& c, double* a, i64 rows, i64 cols, i64 lda, const doubl
 // callers; for m < n only the first m columns are factored). Q: m x min(m,n)
 // (ldq), R (optional): min(m,n) x n upper trapezoidal (ldr). A is not modified.
 void thin_qr(Ctx& c, i64 m, i64 n, const double* A, i64 lda, double* Q, i64 ldq, double* R, i64 ldr);
+
+// ---- shifted Cholesky QR (qr_chol.cu) ----------------------------------------
+// sCQR3 of a tall m x n matrix (m >= n, n <= kCholQrMaxN): Q (m x n, may alias
+// A) and optionally R (n x n upper). Breakdown sets the context's QR flag
+// (Ctx::qr_flag_read) instead of failing; the caller must check it.
+constexpr i64 kCholQrMaxN = 416;
+constexpr int kQrNoBreakdown = 0x7f7f7f7f;  // flag value after a 0x7f byte memset
+bool cholqr_fits(i64 m, i64 n);
+void thin_qr_cholesky(Ctx& c, i64 m, i64 n, const double* A, i64 lda, double* Q, i64 ldq, double* R, i64 ldr,
+                      int tag = 0);
 
 // ---- SVD (svd.cu) -----------------------------------------------------------
 // Thin SVD of a small m x n matrix (m, n <= ~1024) by one-sided Jacobi on the

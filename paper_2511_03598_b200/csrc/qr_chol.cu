@@ -1,0 +1,509 @@
+// qr_chol.cu — K4c: shifted Cholesky QR (sCQR) for the tall-skinny sketches
+// of the Rand-Orth sweep and the TT-SVD orthogonalisations.
+//
+// linalg::thin_qr_q (proj/core/src/linalg.cpp:44-56) is called by the sweep
+// only for an orthonormal basis of range(S) (round_rand.cpp:33-37); the
+// Householder path (qr.cu) is latency-bound: every column of every panel waits
+// on one cross-CTA exchange (~2.5-4.5 us per column at 7,040-40,960 rows).
+// Shifted CholeskyQR (Fukaya, Kannan, Nakatsukasa, Yamamoto, Yanagisawa, SIAM
+// J. Sci. Comput. 2020) needs no per-column exchange: four passes of
+//   G = A^T A            (DMMA GEMM, upper tiles, split-K — gemm_dmma.cu)
+//   R = chol(G [+ s I])  (chol_kernel: one CTA, blocked right-looking)
+//   Q = A R^{-1}         (trsm_kernel: row tiles, DMMA + substitution)
+// the first two with the shift s = 11 (m n + n (n+1)) u ||A||_F^2 (each pass
+// lowers the condition number by ~sqrt(s)/||A||), the last two (CholeskyQR2) on
+// the previous Q without. For kappa(A) up to ~u^{-1} the result is backward
+// stable with an orthonormal Q (the same guarantees as Householder); Q spans
+// the same space as the Householder Q up to column signs, so the rounded
+// tensor — a product of projections Q Q^T — is the same.
+//
+// Breakdown: a non-positive or non-finite pivot in any of the three Cholesky
+// factorisations, or ||G_4 - I||_F > 1/2 (the earlier passes did not deliver a
+// well-conditioned Q_3), sets the context's QR flag. Callers speculate: they
+// run the whole rounding with sCQR, read the flag once, and redo the call on
+// the Householder path if it is set (tt_round.cu), so exactly rank-deficient
+// sketches still get the reference's behaviour.
+#include <cfloat>
+#include <cmath>
+#include <cstdint>
+
+#include "common.cuh"
+
+namespace ttr {
+namespace {
+
+constexpr int kCholThreads = 256;
+constexpr int kCholSmemMaxN = 144;  // whole matrix in shared memory up to this order
+
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(c0), "+d"(c1)
+                 : "d"(a), "d"(b));
+}
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void cp_async16(double* dst, const double* src, int bytes) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(dst)), "l"(src), "r"(bytes));
+}
+__device__ __forceinline__ void cp_async8(double* dst, const double* src, int bytes) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(smem_u32(dst)), "l"(src), "r"(bytes));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+__host__ __device__ constexpr int chol_ldp(int n) { return ((n + 3) / 4) * 4 + 4; }
+__host__ __device__ constexpr int trsm_ld(int n) { return ((n + 31) / 32) * 32 + 4; }  // % 16 == 4
+
+struct CholArgs {
+    int n;
+    double* G;  // n x n (ld ldg): upper triangle in, R (upper, zeros below) out
+    int ldg;
+    int mode;  // bit 0: add shift_coeff * trace(G) to the diagonal; bit 1: require ||G - I||_F <= 1/2
+    double shift_coeff;
+    int* flag;  // atomicMin(flag, tag) on breakdown
+    int tag;
+    double* Rinv;  // [ceil(n/32)][32 x 32] column-major inverses of the diagonal blocks of R
+};
+
+// Blocked (32) right-looking Cholesky G = R^T R in one CTA. Per block row J
+// the 32 x (n - j0) row panel is copied to shared memory and eliminated in
+// place with deferred scaling (step k: G(i, c) -= G(k, i) G(k, c) / g_kk for
+// the panel rows i > k; one barrier per step, every thread owning columns),
+// which factors the diagonal block and solves the panel rows together; the
+// rows are then scaled by 1/sqrt(g_kk) into R and the trailing upper triangle
+// is updated with 4 x 4 register tiles. Finally the inverses of the 32 x 32
+// diagonal blocks of R are formed (one warp per block, one row per step) for
+// the blocked TRSM. All loops stay rolled: this kernel is latency-bound on one
+// SM, and straight-line code would run from instruction-cache misses.
+// SM: the matrix lives in shared memory (n <= kCholSmemMaxN); otherwise it is
+// updated in place in global memory (L2-resident).
+#ifdef TTR_CHOL_TRACE
+__device__ unsigned long long g_chol_trace[8];
+#define CHOL_T(i) do { __syncthreads(); if (threadIdx.x == 0) { long long t = clock64(); atomicAdd(&g_chol_trace[i], static_cast<unsigned long long>(t - t_last)); t_last = t; } } while (0)
+#else
+#define CHOL_T(i) do { } while (0)
+#endif
+template <bool SM>
+__global__ void __launch_bounds__(kCholThreads) chol_kernel(CholArgs p) {
+#ifdef TTR_CHOL_TRACE
+    long long t_last = clock64();
+#endif
+    extern __shared__ __align__(16) double smem[];
+    __shared__ double dall[kCholQrMaxN + 32];  // 1 / r_kk
+    __shared__ double pv[32];                  // pivots of the current block
+    __shared__ double red[kCholThreads / 32];
+    __shared__ int bad;
+    const int n = p.n, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int ldp = chol_ldp(n);
+    double* RP = smem;  // row panel [32][ldp]: RP[i * ldp + c'] = G(j0 + i, j0 + c')
+    double* A;
+    i64 lda;
+    if constexpr (SM) {
+        A = smem + 32 * ldp;
+        lda = n + 1;
+        for (int cc = warp; cc < n; cc += kCholThreads / 32)
+            for (int r = lane; r <= cc; r += 32) cp_async8(A + r + cc * lda, p.G + r + static_cast<i64>(cc) * p.ldg, 8);
+        cp_commit();
+        cp_wait<0>();
+    } else {
+        A = p.G;
+        lda = p.ldg;
+    }
+    if (tid == 0) bad = 0;
+    __syncthreads();
+    CHOL_T(0);
+    double shift = 0.0;
+    if (p.mode & 3) {
+        double acc = 0.0;
+        if (p.mode & 1) {
+            for (int i = tid; i < n; i += kCholThreads) acc += A[i + i * lda];
+        } else {
+            for (int cc = warp; cc < n; cc += kCholThreads / 32)
+                for (int r = lane; r <= cc; r += 32) {
+                    const double v = A[r + cc * lda] - (r == cc ? 1.0 : 0.0);
+                    acc += (r == cc ? 1.0 : 2.0) * v * v;
+                }
+        }
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) red[warp] = acc;
+        __syncthreads();
+        double total = 0.0;
+        for (int w = 0; w < kCholThreads / 32; ++w) total += red[w];
+        if (p.mode & 1)
+            shift = p.shift_coeff * total;
+        else if (tid == 0 && !(total <= 0.25))
+            bad = 1;
+    }
+    for (int j0 = 0; j0 < n; j0 += 32) {
+        const int b = min(32, n - j0), nt = n - j0;  // panel columns c' in [0, nt)
+        for (int cc = tid; cc < nt; cc += kCholThreads)
+            for (int i = 0; i < 32; ++i)
+                RP[i * ldp + cc] = (i < b && i <= cc) ? A[(j0 + i) + (j0 + cc) * lda] + (i == cc ? shift : 0.0) : 0.0;
+        __syncthreads();
+        CHOL_T(1);
+        for (int k = 0; k < b; ++k) {
+            double piv = RP[k * ldp + k];
+            if (!(piv > 0.0) || !isfinite(piv)) {
+                if (tid == 0) bad = 1;
+                piv = 1.0;  // keep the factor finite; the result is discarded
+            }
+            if (tid == 0) pv[k] = piv;
+            const double invp = 1.0 / piv;
+            const double* rk = RP + k * ldp;
+            for (int cc = k + 1 + tid; cc < nt; cc += kCholThreads) {
+                const double f = rk[cc] * invp;
+                const int iend = min(cc, b - 1);
+                for (int i = k + 1; i <= iend; ++i) RP[i * ldp + cc] = fma(-rk[i], f, RP[i * ldp + cc]);
+            }
+            __syncthreads();
+        }
+        CHOL_T(2);
+        // R rows: R(j0 + k, c) = G(k, c) / sqrt(g_kk) (c > k), R(k, k) = sqrt(g_kk)
+        for (int cc = tid; cc < nt; cc += kCholThreads) {
+            for (int k = 0; k < b && k <= cc; ++k) {
+                const double r = sqrt(pv[k]);
+                const double v = (k == cc) ? r : RP[k * ldp + cc] / r;
+                RP[k * ldp + cc] = v;
+                A[(j0 + k) + (j0 + cc) * lda] = v;
+            }
+            if (cc < b) dall[j0 + cc] = 1.0 / sqrt(pv[cc]);
+        }
+        // zero the panel's padding columns so the 4-wide tiles read zeros
+        for (int e = tid; e < 32 * 4; e += kCholThreads) {
+            const int r = e >> 2, cc = nt + (e & 3);
+            if (cc < ldp) RP[r * ldp + cc] = 0.0;
+        }
+        __syncthreads();
+        CHOL_T(3);
+        // trailing update of the upper triangle: G(i, j) -= sum_r P(r, i) P(r, j)
+        // over the panel columns past the diagonal block, 4 x 4 tiles (ti <= tj)
+        const int c1 = j0 + b, nr = n - c1;
+        const double* Pb = RP + b;
+        const int nt4 = (nr + 3) / 4, ntiles = nt4 * (nt4 + 1) / 2;
+        for (int t = tid; t < ntiles; t += kCholThreads) {
+            int tj = static_cast<int>((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
+            while (tj * (tj + 1) / 2 > t) --tj;
+            while ((tj + 1) * (tj + 2) / 2 <= t) ++tj;
+            const int ti = t - tj * (tj + 1) / 2;
+            double old[4][4];
+#pragma unroll
+            for (int v = 0; v < 4; ++v)
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int i = 4 * ti + u, j = 4 * tj + v;
+                    old[u][v] = (i <= j && j < nr) ? A[(c1 + i) + (c1 + j) * lda] : 0.0;
+                }
+            double acc[4][4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (int v = 0; v < 4; ++v) acc[u][v] = 0.0;
+#pragma unroll 2
+            for (int r = 0; r < b; ++r) {
+                const double2 i01 = *reinterpret_cast<const double2*>(Pb + r * ldp + 4 * ti);
+                const double2 i23 = *reinterpret_cast<const double2*>(Pb + r * ldp + 4 * ti + 2);
+                const double2 j01 = *reinterpret_cast<const double2*>(Pb + r * ldp + 4 * tj);
+                const double2 j23 = *reinterpret_cast<const double2*>(Pb + r * ldp + 4 * tj + 2);
+                const double pi[4] = {i01.x, i01.y, i23.x, i23.y}, pj[4] = {j01.x, j01.y, j23.x, j23.y};
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+#pragma unroll
+                    for (int v = 0; v < 4; ++v) acc[u][v] = fma(pi[u], pj[v], acc[u][v]);
+            }
+#pragma unroll
+            for (int v = 0; v < 4; ++v)
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int i = 4 * ti + u, j = 4 * tj + v;
+                    if (i <= j && j < nr) A[(c1 + i) + (c1 + j) * lda] = old[u][v] - acc[u][v];
+                }
+        }
+        __syncthreads();
+        CHOL_T(4);
+    }
+    // inverses of the diagonal blocks for the blocked TRSM: X = U^{-1} by rows
+    // from the bottom, X(i, c) = (delta_ic - sum_{k > i} U(i, k) X(k, c)) / U(i, i);
+    // one warp per block, lane = column c; X staged in the block's output
+    for (int J = warp; J * 32 < n; J += kCholThreads / 32) {
+        const int j0 = J * 32, b = min(32, n - j0), c = lane;
+        double* X = p.Rinv + static_cast<i64>(J) * 1024;  // column-major 32 x 32
+        for (int i = 31; i >= 0; --i) {
+            double v = 0.0;
+            if (i < b && c < b && i <= c) {
+                v = (i == c) ? 1.0 : 0.0;
+                for (int k = i + 1; k <= c; ++k) v = fma(-A[(j0 + i) + (j0 + k) * lda], X[k + 32 * c], v);
+                v *= dall[j0 + i];
+            }
+            X[i + 32 * c] = v;
+            __syncwarp();
+        }
+    }
+    CHOL_T(5);
+    // R out (upper) with zeros below the diagonal
+    for (int cc = warp; cc < n; cc += kCholThreads / 32)
+        for (int r = lane; r < n; r += 32) {
+            double* g = p.G + r + static_cast<i64>(cc) * p.ldg;
+            if (r > cc)
+                *g = 0.0;
+            else if constexpr (SM)
+                *g = A[r + cc * lda];
+        }
+    if (tid == 0 && bad) atomicMin(p.flag, p.tag);
+}
+
+// Q = A R^{-1} for R upper triangular (n x n), one CTA per BM-row tile (BM/16
+// warps, 16 rows each). The tile lives column-major in shared memory; per
+// 32-column block J each warp forms acc = A(:, J) - Q(:, <J) R(<J, J) on DMMA,
+// with R(<J, J) streamed through shared memory in 32 x 32 chunks (cp.async,
+// double buffered), then Q(:, J) = acc * inv(R_JJ) with the 32 x 32 inverse of
+// the diagonal block written by chol_kernel (blocked TRSM with inverted
+// diagonal blocks). With the two shifted passes every factor here has
+// kappa(R) <= ~||A|| / sqrt(s) ~ 1e4, so the inverted blocks cost at most that
+// factor in the rowwise residual. A and Q may alias (in place).
+constexpr int kRcLd = 36;  // chunk [32 cols][32 k + 4]: conflict-free B fragments
+
+template <int BM>
+__global__ void __launch_bounds__(BM * 2) trsm_kernel(int m, int n, const double* A, i64 lda, const double* R,
+                                                     int ldr, const double* Rinv, double* Q, i64 ldq) {
+    constexpr int kThreads = BM * 2, kLdm = BM + 4;  // kLdm % 16 == 4: conflict-free A fragments
+    extern __shared__ __align__(16) double smem[];
+    const int npad = ((n + 31) / 32) * 32;
+    double* Qs = smem;                    // [npad][kLdm] column-major tile
+    double* Rc = smem + npad * kLdm;      // [2][32][kRcLd] chunks of R(<J, J)
+    double* Ui = Rc + 2 * 32 * kRcLd;     // [32][kRcLd] inv(R_JJ)
+    const i64 row0 = static_cast<i64>(blockIdx.x) * BM;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const bool vec = ((lda & 1) == 0) && ((reinterpret_cast<std::uintptr_t>(A) & 15) == 0);
+    for (int e = tid; e < npad * (BM / 2); e += kThreads) {
+        const int cc = e / (BM / 2), r2 = (e % (BM / 2)) * 2;
+        const i64 gr = row0 + r2;
+        double* dst = Qs + cc * kLdm + r2;
+        const int rows = (cc < n && gr < m) ? static_cast<int>(m - gr < 2 ? m - gr : 2) : 0;
+        const double* src = A + (rows ? gr + cc * lda : 0);
+        if (vec) {
+            cp_async16(dst, src, rows * 8);
+        } else {
+            cp_async8(dst, src, rows >= 1 ? 8 : 0);
+            cp_async8(dst + 1, src + (rows >= 2 ? 1 : 0), rows >= 2 ? 8 : 0);
+        }
+    }
+    cp_commit();
+    const bool rvec = (ldr & 1) == 0;
+    auto load_block = [&](double* dst, const double* base, i64 ld, int k0, int c0, bool v16) {
+        // base(k0:k0+32, c0:c0+32) -> dst[col][k] (zero fill past n)
+        for (int e = tid; e < 32 * 16; e += kThreads) {
+            const int col = e >> 4, kk = (e & 15) * 2;
+            const int gc = c0 + col, gk = k0 + kk;
+            const int cnt = gc < n ? max(0, min(2, n - gk)) : 0;
+            const double* src = base + (cnt ? static_cast<i64>(gc) * ld + gk : 0);
+            double* d = dst + col * kRcLd + kk;
+            if (v16) {
+                cp_async16(d, src, cnt * 8);
+            } else {
+                cp_async8(d, src, cnt >= 1 ? 8 : 0);
+                cp_async8(d + 1, src + (cnt >= 2 ? 1 : 0), cnt >= 2 ? 8 : 0);
+            }
+        }
+    };
+    const int fr = lane >> 2, fc = lane & 3, wr = warp * 16;
+    for (int c0 = 0; c0 < n; c0 += 32) {
+        const int nch = c0 / 32;
+        __syncthreads();  // the previous block's reads of Ui / Rc are done
+        {
+            // inv(R_JJ): stored 32 x 32 column-major per block (ld 32, c0 local)
+            const double* ub = Rinv + static_cast<i64>(c0 / 32) * 1024;
+            for (int e = tid; e < 32 * 16; e += kThreads) {
+                const int col = e >> 4, kk = (e & 15) * 2;
+                cp_async16(Ui + col * kRcLd + kk, ub + col * 32 + kk, 16);
+            }
+        }
+        if (nch > 0) load_block(Rc, R, ldr, 0, c0, rvec);
+        cp_commit();
+        double acc[2][4][2];
+#pragma unroll
+        for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+            for (int t = 0; t < 4; ++t)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) acc[mi][t][h] = 0.0;
+        for (int ch = 0; ch < nch; ++ch) {
+            if (ch + 1 < nch) load_block(Rc + ((ch + 1) & 1) * 32 * kRcLd, R, ldr, (ch + 1) * 32, c0, rvec);
+            cp_commit();
+            cp_wait<1>();
+            __syncthreads();
+            const double* rc = Rc + (ch & 1) * 32 * kRcLd;
+            const double* qa = Qs + (ch * 32) * kLdm + wr + fr;
+#pragma unroll
+            for (int k = 0; k < 32; k += 4) {
+                const double a0 = qa[(k + fc) * kLdm], a1 = qa[(k + fc) * kLdm + 8];
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    const double bv = rc[(t * 8 + fr) * kRcLd + k + fc];
+                    dmma(acc[0][t][0], acc[0][t][1], a0, bv);
+                    dmma(acc[1][t][0], acc[1][t][1], a1, bv);
+                }
+            }
+            __syncthreads();  // buffer (ch & 1) is refilled two chunks later
+        }
+        cp_wait<0>();
+        __syncthreads();
+        // acc_J = A(:, J) - Q(:, <J) R(<J, J) into the tile (own rows only)
+        double* qj = Qs + c0 * kLdm + wr + fr;
+#pragma unroll
+        for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+            for (int t = 0; t < 4; ++t)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    double* d = qj + (t * 8 + 2 * fc + h) * kLdm + mi * 8;
+                    *d = *d - acc[mi][t][h];
+                }
+        __syncwarp();
+        // Q(:, J) = acc_J inv(R_JJ)
+        double x[2][4][2];
+#pragma unroll
+        for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+            for (int t = 0; t < 4; ++t) x[mi][t][0] = x[mi][t][1] = 0.0;
+#pragma unroll
+        for (int k = 0; k < 32; k += 4) {
+            const double a0 = qj[(k + fc) * kLdm], a1 = qj[(k + fc) * kLdm + 8];
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                const double bv = Ui[(t * 8 + fr) * kRcLd + k + fc];
+                dmma(x[0][t][0], x[0][t][1], a0, bv);
+                dmma(x[1][t][0], x[1][t][1], a1, bv);
+            }
+        }
+        __syncwarp();
+#pragma unroll
+        for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+            for (int t = 0; t < 4; ++t)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) qj[(t * 8 + 2 * fc + h) * kLdm + mi * 8] = x[mi][t][h];
+        __syncwarp();
+    }
+    __syncthreads();
+    for (int e = tid; e < n * BM; e += kThreads) {
+        const int cc = e / BM, r = e % BM;
+        const i64 gr = row0 + r;
+        if (gr < m) Q[gr + cc * ldq] = Qs[cc * kLdm + r];
+    }
+}
+
+template <int BM>
+std::size_t trsm_smem(i64 n) {
+    const std::size_t npad = static_cast<std::size_t>((n + 31) / 32) * 32;
+    return sizeof(double) * (npad * (BM + 4) + 3 * 32 * kRcLd);
+}
+
+// opt in to the largest dynamic shared memory the kernel's static usage leaves
+void set_max_dynamic_smem(const void* fn) {
+    cudaFuncAttributes fa{};
+    TTR_CUDA(cudaFuncGetAttributes(&fa, fn));
+    int dev = 0, optin = 0;
+    TTR_CUDA(cudaGetDevice(&dev));
+    TTR_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    TTR_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  optin - static_cast<int>(fa.sharedSizeBytes)));
+}
+
+void launch_chol(Ctx& c, i64 n, double* G, i64 ldg, int mode, double coeff, double* Rinv, int tag) {
+    CholArgs a{static_cast<int>(n), G, static_cast<int>(ldg), mode, coeff, c.qr_flag_dev(), static_cast<int>(tag), Rinv};
+    const std::size_t panel = sizeof(double) * 32 * chol_ldp(static_cast<int>(n));
+    static std::atomic<std::uint64_t> configured{0};
+    if (first_on_device(configured)) {
+        set_max_dynamic_smem(reinterpret_cast<const void*>(chol_kernel<true>));
+        set_max_dynamic_smem(reinterpret_cast<const void*>(chol_kernel<false>));
+    }
+    if (n <= kCholSmemMaxN) {
+        const std::size_t smem = panel + sizeof(double) * static_cast<std::size_t>(n * (n + 1));
+        chol_kernel<true><<<1, kCholThreads, smem, c.stream>>>(a);
+    } else {
+        chol_kernel<false><<<1, kCholThreads, panel, c.stream>>>(a);
+    }
+    TTR_CUDA(cudaGetLastError());
+    c.launched();
+}
+
+void launch_trsm(Ctx& c, i64 m, i64 n, const double* A, i64 lda, const double* R, i64 ldr, const double* Rinv,
+                 double* Q, i64 ldq) {
+    static std::atomic<std::uint64_t> configured{0};
+    if (first_on_device(configured)) {
+        set_max_dynamic_smem(reinterpret_cast<const void*>(trsm_kernel<64>));
+        set_max_dynamic_smem(reinterpret_cast<const void*>(trsm_kernel<32>));
+    }
+    if (trsm_smem<64>(n) <= 220 * 1024) {
+        const unsigned grid = static_cast<unsigned>((m + 63) / 64);
+        trsm_kernel<64><<<grid, 128, trsm_smem<64>(n), c.stream>>>(static_cast<int>(m), static_cast<int>(n), A, lda, R,
+                                                                  static_cast<int>(ldr), Rinv, Q, ldq);
+    } else {
+        const unsigned grid = static_cast<unsigned>((m + 31) / 32);
+        trsm_kernel<32><<<grid, 64, trsm_smem<32>(n), c.stream>>>(static_cast<int>(m), static_cast<int>(n), A, lda, R,
+                                                                 static_cast<int>(ldr), Rinv, Q, ldq);
+    }
+    TTR_CUDA(cudaGetLastError());
+    c.launched();
+}
+
+}  // namespace
+
+// Passes: two shifted (each lowers kappa by ~sqrt(11 (mn + n^2) u), enough for
+// the ~1e10-1e12 condition numbers of the sweep's sketches), then two plain
+// (CholeskyQR2), the last one checking that its Gram matrix is close to I.
+constexpr int kCholQrPasses = 4, kCholQrShifted = 2;
+
+bool cholqr_fits(i64 m, i64 n) { return n >= 1 && n <= kCholQrMaxN && m >= n; }
+
+int* Ctx::qr_flag_dev() {
+    if (!qr_flag) {
+        TTR_CUDA(cudaMalloc(reinterpret_cast<void**>(&qr_flag), sizeof(int)));
+        TTR_CUDA(cudaMemsetAsync(qr_flag, 0x7f, sizeof(int), stream));
+    }
+    return qr_flag;
+}
+
+void Ctx::qr_flag_reset() { TTR_CUDA(cudaMemsetAsync(qr_flag_dev(), 0x7f, sizeof(int), stream)); }
+
+int Ctx::qr_flag_read() {
+    int* hf = reinterpret_cast<int*>(host_scalars + 8);
+    TTR_CUDA(cudaMemcpyAsync(hf, qr_flag_dev(), sizeof(int), cudaMemcpyDeviceToHost, stream));
+    TTR_CUDA(cudaStreamSynchronize(stream));
+    return *hf == kQrNoBreakdown ? -1 : *hf;
+}
+
+void thin_qr_cholesky(Ctx& c, i64 m, i64 n, const double* A, i64 lda, double* Q, i64 ldq, double* R, i64 ldr,
+                      int tag) {
+    if (!cholqr_fits(m, n)) fail(Errc::InvalidArgument, "sCQR: shape outside the Cholesky-QR path");
+    c.charge_qr(4ULL * static_cast<std::uint64_t>(m) * n * n);  // the reference's Householder charge
+    const double u = DBL_EPSILON / 2;
+    const double coeff = 11.0 * (static_cast<double>(m) * n + static_cast<double>(n) * (n + 1)) * u;
+    const std::size_t nn = static_cast<std::size_t>(n * n), ni = static_cast<std::size_t>((n + 31) / 32) * 1024;
+    DBuf Gs(c, nn * (R ? kCholQrPasses : 1)), Ri(c, ni);
+    const double* src = A;
+    i64 lds = lda;
+    for (int it = 0; it < kCholQrPasses; ++it) {
+        double* G = Gs.p + (R ? it * nn : 0);
+        gemm(c, true, n, n, m, 1.0, src, lds, src, lds, 0.0, G, n, false, true);  // upper tiles of src^T src
+        const int mode = it < kCholQrShifted ? 1 : (it == kCholQrPasses - 1 ? 2 : 0);
+        launch_chol(c, n, G, n, mode, coeff, Ri.p, tag);
+        launch_trsm(c, m, n, src, lds, G, n, Ri.p, Q, ldq);
+        src = Q;
+        lds = ldq;
+    }
+    if (R) {  // R = R_p ... R_2 R_1
+        DBuf T(c, nn), T2(c, nn);
+        double* acc = Gs.p + (kCholQrPasses - 1) * nn;
+        for (int it = kCholQrPasses - 2; it >= 0; --it) {
+            double* dst = it == 0 ? R : (acc == T.p ? T2.p : T.p);
+            const i64 ldd = it == 0 ? ldr : n;
+            gemm(c, false, n, n, n, 1.0, acc, n, Gs.p + it * nn, n, 0.0, dst, ldd, false);
+            acc = dst;
+        }
+    }
+}
+
+}  // namespace ttr

@@ -4,6 +4,7 @@
 // context's stream; the host only sequences launches and, in the adaptive
 // loop, reads back the one scalar that drives each stopping decision.
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <array>
 #include <cmath>
@@ -13,6 +14,7 @@
 #include "common.cuh"
 #include "rng_host.h"
 #include "tt_round.h"
+#include <functional>
 #include "sketch.cuh"
 
 namespace ttr {
@@ -376,8 +378,32 @@ std::unique_ptr<TTDev> round_fixed_krp(Ctx& c, const TTDev& t, const std::vector
     auto r = fixed_krp_ranks(t, target_ranks);
     if (t.d() == 1) return copy_tt(c, t);
     auto out = std::make_unique<TTDev>(c, t.n, r);
-    round_fixed_krp_into(c, t, target_ranks, seed, rng_mode, *out);
+    with_qr_speculation(c, [&] { round_fixed_krp_into(c, t, target_ranks, seed, rng_mode, *out); });
     return out;
+}
+
+// Runs `body` (a rounding that ends in rand_orth_sweep) with the sweep allowed
+// to take the shifted Cholesky QR; if any of its factorisations broke down
+// (exactly or numerically rank-deficient sketch), runs it again on the
+// Householder path. One flag read (and stream synchronisation) per call.
+void with_qr_speculation(Ctx& c, const std::function<void()>& body) {
+    struct Restore {
+        Ctx& c;
+        ~Restore() { c.qr_spec = false; }
+    } restore{c};
+    c.qr_spec = true;
+    c.qr_hh_from = INT32_MAX;
+    for (;;) {
+        c.qr_spec_used = false;
+        body();
+        if (!c.qr_spec_used) break;
+        const int failed = c.qr_flag_read();
+        if (failed < 0) break;
+        // modes before `failed` reproduce bitwise on the rerun; from there on
+        // the sweep takes the Householder QR (strictly decreasing: terminates)
+        c.qr_hh_from = failed;
+    }
+    c.qr_spec = false;
 }
 
 // The sweep proper, writing into a preallocated output (used directly by the
@@ -419,6 +445,18 @@ void rand_orth_sweep(Ctx& c, const TTDev& t, i64 width, const std::vector<const 
     DBuf S(c, static_cast<std::size_t>(max_s));
     DBuf M(c, static_cast<std::size_t>(width * t.max_rank()));
 
+    // Structural rank bound of the contractions: W_d = H(X_d) Omega_d has rank
+    // <= min(r_{d-1}, n_d, width), W_k = H(X_k)(W_{k+1} (.) Omega_k) rank <=
+    // min(r_{k-1}, n_k rank(W_{k+1}), width) (the same for a TT sketch,
+    // sketch.cpp:94-109). A sketch S_k = V(Y_k) W_{k+1}(:, 1:l) whose bound is
+    // below l is exactly rank-deficient (e.g. the last bond whenever n_d < l):
+    // it keeps the Householder QR, whose tau = 0 convention handles it.
+    std::vector<i64> wbound(static_cast<std::size_t>(d + 2), 0);
+    wbound[d] = std::min({t.r[d - 1], t.n[d - 1], width});
+    for (i64 k = d - 1; k >= 2; --k)
+        wbound[k] = std::min({t.r[k - 1], width, t.n[k - 1] * wbound[k + 1]});
+    if (c.qr_spec) c.qr_flag_reset();
+
     const double* v = t.core(0);
     if (c.io) c.io->wait_in(c.stream, 0);
     for (i64 k = 1; k < d; ++k) {
@@ -431,7 +469,13 @@ void rand_orth_sweep(Ctx& c, const TTDev& t, i64 width, const std::vector<const 
         // Q = thin_qr_q(S) -> output core k
         {
             PhaseScope ph(c, kPhaseQr);
-            thin_qr(c, rows, l, S.p, rows, out->core(k - 1), rows, nullptr, 1);
+            if (c.qr_spec && k < c.qr_hh_from && l > 32 && rows >= 2 * l && cholqr_fits(rows, l) &&
+                wbound[k + 1] >= l) {
+                thin_qr_cholesky(c, rows, l, S.p, rows, out->core(k - 1), rows, nullptr, 1, static_cast<int>(k));
+                c.qr_spec_used = true;
+            } else {
+                thin_qr(c, rows, l, S.p, rows, out->core(k - 1), rows, nullptr, 1);
+            }
         }
         if (c.io) c.io->out_done(c.stream, static_cast<std::size_t>(k - 1));  // output core k-1 final: D2H
         const i64 ncols = t.n[k] * t.r[k + 1];
@@ -518,18 +562,19 @@ std::unique_ptr<TTDev> round_rand_orth_tt(Ctx& c, const TTDev& t, const std::vec
 // workspace (and the split-K scratch), then the whole sweep — ~2,400 launches
 // for config 5b — is captured once and replayed with a single graph launch.
 Plan::Plan(Ctx& cc, const TTDev& in_, const std::vector<i64>& ranks_, std::uint64_t seed_, int rng,
-           const double* host_in, double* host_out)
-    : c(cc), in(in_), ranks(ranks_), seed(seed_), rng_mode(rng) {
+           const double* host_in_, double* host_out_)
+    : c(cc), in(in_), ranks(ranks_), seed(seed_), rng_mode(rng), host_in(host_in_), host_out(host_out_) {
     if (rng_mode != TTR_RNG_PHILOX) fail(Errc::InvalidArgument, "plans need the device (Philox) generator");
     auto r = fixed_krp_ranks(in, ranks);
     if (in.d() < 2) fail(Errc::InvalidArgument, "plans need d >= 2");
     out = std::make_unique<TTDev>(c, in.n, r);
-    round_fixed_krp_into(c, in, ranks, seed, rng_mode, *out);  // eager run: sizes pools and scratch
+    target = out.get();
+    // eager run: sizes pools and scratch (and the speculative path's buffers)
+    // and finds the first mode whose Cholesky QR breaks down on this input
+    // (the captured graph takes the Householder QR from there on)
+    with_qr_speculation(c, [&] { round_fixed_krp_into(c, in, ranks, seed, rng_mode, *target); });
+    hh_from = c.qr_hh_from;
     TTR_CUDA(cudaStreamSynchronize(c.stream));
-    const bool timing = c.timing;
-    c.timing = false;
-    const Counts saved = c.counts;
-    const std::uint64_t l0 = c.launches;
     const bool host = host_in != nullptr && host_out != nullptr;
     const i64 d = in.d();
     if (host) {
@@ -546,12 +591,32 @@ Plan::Plan(Ctx& cc, const TTDev& in_, const std::vector<i64>& ranks_, std::uint6
         std::size_t o = 0;
         for (i64 k = 0; k < d; ++k) {
             io.out_host.push_back(host_out + o);
-            io.out_dev.push_back(out->core(k));
-            io.out_bytes.push_back(sizeof(double) * static_cast<std::size_t>(out->core_size(k)));
-            o += static_cast<std::size_t>(out->core_size(k));
+            io.out_dev.push_back(target->core(k));
+            io.out_bytes.push_back(sizeof(double) * static_cast<std::size_t>(target->core_size(k)));
+            o += static_cast<std::size_t>(target->core_size(k));
         }
     }
     ++c.live_plans;  // from here on the scratch captured below is never freed under the graph
+    try {
+        speculative = capture(true, graph, exec);
+    } catch (...) {
+        if (--c.live_plans == 0) c.release_retired();
+        throw;
+    }
+}
+
+// Captures one round (optionally with the Cholesky-QR speculation) into a
+// graph; returns whether the captured sweep took the Cholesky path.
+bool Plan::capture(bool spec, cudaGraph_t& g_out, cudaGraphExec_t& e_out) {
+    const bool timing = c.timing;
+    c.timing = false;
+    const Counts saved = c.counts;
+    const std::uint64_t l0 = c.launches;
+    const bool host = host_in != nullptr && host_out != nullptr;
+    const i64 d = in.d();
+    c.qr_spec = spec;
+    c.qr_hh_from = hh_from;
+    c.qr_spec_used = false;
     TTR_CUDA(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal));
     try {
         if (host) {
@@ -568,7 +633,7 @@ Plan::Plan(Ctx& cc, const TTDev& in_, const std::vector<i64>& ranks_, std::uint6
             }
             c.io = &io;
         }
-        round_fixed_krp_into(c, in, ranks, seed, rng_mode, *out);
+        round_fixed_krp_into(c, in, ranks, seed, rng_mode, *target);
         if (host) {
             c.io = nullptr;
             TTR_CUDA(cudaEventRecord(join, io.copy));
@@ -576,14 +641,16 @@ Plan::Plan(Ctx& cc, const TTDev& in_, const std::vector<i64>& ranks_, std::uint6
         }
     } catch (...) {
         c.io = nullptr;
+        c.qr_spec = false;
         cudaGraph_t g;
         cudaStreamEndCapture(c.stream, &g);
         if (g) cudaGraphDestroy(g);
         c.timing = timing;
-        if (--c.live_plans == 0) c.release_retired();
         throw;
     }
-    TTR_CUDA(cudaStreamEndCapture(c.stream, &graph));
+    c.qr_spec = false;
+    const bool used = c.qr_spec_used;
+    TTR_CUDA(cudaStreamEndCapture(c.stream, &g_out));
     launches_per_run = c.launches - l0;
     flops = c.counts;  // counters of one run (captured run)
     flops.gemm -= saved.gemm;
@@ -594,22 +661,34 @@ Plan::Plan(Ctx& cc, const TTDev& in_, const std::vector<i64>& ranks_, std::uint6
     c.counts = saved;
     c.launches = l0;
     c.timing = timing;
-    TTR_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+    TTR_CUDA(cudaGraphInstantiate(&e_out, g_out, 0));
+    return used;
 }
 
+// Replays the graph. A speculative graph (Cholesky QR in the sweep) is
+// followed by one read of the breakdown flag; on breakdown the Householder
+// graph (captured on first need) runs instead, writing the same output.
 void Plan::execute() {
     TTR_CUDA(cudaGraphLaunch(exec, c.stream));
+    std::uint64_t launches = launches_per_run;
+    if (speculative && c.qr_flag_read() >= 0) {
+        if (!exec_safe) capture(false, graph_safe, exec_safe);
+        TTR_CUDA(cudaGraphLaunch(exec_safe, c.stream));
+        launches += launches_per_run;
+    }
     c.counts.gemm += flops.gemm;
     c.counts.qr += flops.qr;
     c.counts.svd += flops.svd;
     c.counts.sketch += flops.sketch;
     c.counts.rng += flops.rng;
-    c.launched(static_cast<int>(launches_per_run));
+    c.launched(static_cast<int>(launches));
 }
 
 Plan::~Plan() {
     if (exec) cudaGraphExecDestroy(exec);
     if (graph) cudaGraphDestroy(graph);
+    if (exec_safe) cudaGraphExecDestroy(exec_safe);
+    if (graph_safe) cudaGraphDestroy(graph_safe);
     if (graph && --c.live_plans == 0) c.release_retired();
     for (auto e : io.in_ready) cudaEventDestroy(e);
     for (auto e : io.out_ready) cudaEventDestroy(e);

@@ -3,6 +3,7 @@
 #pragma once
 
 #include <algorithm>
+#include <functional>
 #include <memory>
 #include <vector>
 
@@ -79,6 +80,9 @@ std::unique_ptr<TTDev> round_fixed_krp(Ctx& c, const TTDev& t, const std::vector
 std::vector<i64> fixed_krp_ranks(const TTDev& t, const std::vector<i64>& target_ranks);
 void round_fixed_krp_into(Ctx& c, const TTDev& t, const std::vector<i64>& target_ranks, std::uint64_t seed,
                           int rng_mode, TTDev& out);
+// Runs a rounding whose sweep may take the Cholesky QR, then checks the
+// breakdown flag once and reruns it on the Householder path if set.
+void with_qr_speculation(Ctx& c, const std::function<void()>& body);
 void rand_orth_sweep(Ctx& c, const TTDev& t, i64 width, const std::vector<const double*>& W,
                      const std::vector<i64>& ldw, TTDev& out);
 void krp_sketch_into(Ctx& c, const TTDev& t, i64 col0, i64 ncols, std::uint64_t seed, const std::vector<double*>& W,
@@ -92,9 +96,14 @@ struct Plan {
     std::vector<i64> ranks;
     std::uint64_t seed;
     int rng_mode;
-    std::unique_ptr<TTDev> out;
-    cudaGraph_t graph = nullptr;
-    cudaGraphExec_t exec = nullptr;
+    const double* host_in = nullptr;
+    double* host_out = nullptr;
+    std::unique_ptr<TTDev> out;  // moved to the C handle after construction
+    TTDev* target = nullptr;     // the output tensor every graph writes
+    cudaGraph_t graph = nullptr, graph_safe = nullptr;
+    cudaGraphExec_t exec = nullptr, exec_safe = nullptr;  // speculative (Cholesky QR) / Householder
+    bool speculative = false;
+    i64 hh_from = INT32_MAX;  // modes >= hh_from take the Householder QR in the speculative graph
     std::uint64_t launches_per_run = 0;
     Counts flops;
     HostIO io;  // host-streaming plans only
@@ -104,6 +113,7 @@ struct Plan {
     Plan(Ctx& c, const TTDev& in, const std::vector<i64>& ranks, std::uint64_t seed, int rng_mode,
          const double* host_in = nullptr, double* host_out = nullptr);
     ~Plan();
+    bool capture(bool spec, cudaGraph_t& g, cudaGraphExec_t& e);
     void execute();
 };
 

@@ -75,6 +75,81 @@ def test_thin_qr_graded_columns(P, m, n):
     assert np.linalg.norm(q @ r - a) <= 1e-13 * np.sqrt(m * n) * np.linalg.norm(a)
 
 
+# ---- K4c: shifted Cholesky QR (the sweep's speculative QR) ---------------------------
+
+@pytest.mark.parametrize("m,n", [(7040, 110), (40960, 320), (25600, 400), (2000, 70), (16384, 320), (300, 33),
+                                 (5000, 144), (5000, 145), (100, 100), (6400, 416)])
+@pytest.mark.parametrize("graded", [False, True])
+def test_thin_qr_cholesky(P, m, n, graded):
+    """sCQR3: orthonormal Q, A = QR, R upper, no breakdown for kappa up to 1e12,
+    and the same basis as the Householder QR up to column signs."""
+    rng = np.random.default_rng(m + 7 * n + graded)
+    if graded:
+        u, _ = np.linalg.qr(rng.standard_normal((m, n)))
+        v, _ = np.linalg.qr(rng.standard_normal((n, n)))
+        a = (u * np.logspace(0, -12, n)) @ v.T
+    else:
+        a = rng.standard_normal((m, n))
+    q, r, breakdown = P.thin_qr_cholesky(a)
+    assert not breakdown
+    assert np.linalg.norm(q.T @ q - np.eye(n)) <= 1e-12 * np.sqrt(n)
+    assert np.linalg.norm(q @ r - a) <= 1e-13 * np.sqrt(m * n) * np.linalg.norm(a)
+    assert np.allclose(np.tril(r, -1), 0.0)
+    if not graded:
+        qh, _ = P.thin_qr(a)
+        signs = np.sign(np.sum(q * qh, axis=0))
+        assert np.all(np.abs(signs) == 1)
+        assert np.linalg.norm(q - qh * signs) <= 1e-11 * np.sqrt(n)
+
+
+@pytest.mark.parametrize("m,n,rank", [(7040, 110, 64), (40960, 320, 128), (500, 40, 0), (3000, 60, 59)])
+def test_thin_qr_cholesky_rank_deficient(P, m, n, rank):
+    """Exactly rank-deficient input: either the breakdown flag is raised (the
+    caller redoes the call with Householder) or the result is still a valid
+    thin QR — orthonormal Q (any completion of the range) and A = QR."""
+    rng = np.random.default_rng(3)
+    a = rng.standard_normal((m, rank)) @ rng.standard_normal((rank, n)) if rank else np.zeros((m, n))
+    q, r, breakdown = P.thin_qr_cholesky(a)
+    if rank == 0:
+        assert breakdown
+    if not breakdown:
+        assert np.linalg.norm(q.T @ q - np.eye(n)) <= 1e-12 * np.sqrt(n)
+        assert np.linalg.norm(q @ r - a) <= 1e-13 * np.sqrt(m * n) * max(1.0, np.linalg.norm(a))
+
+
+def _padded_low_rank(O, modes, true_r, pad_r, seed):
+    x = O.random_gaussian_tt(modes, true_r, seed)
+    out = []
+    for k, c in enumerate(x.cores()):
+        z = np.zeros((pad_r[k], c.shape[1], pad_r[k + 1]))
+        z[:c.shape[0], :, :c.shape[2]] = c
+        out.append(z)
+    return O.TT.from_cores(out)
+
+
+def test_fixed_krp_cholesky_breakdown_falls_back(P, O):
+    """Exactly rank-deficient sketches wider than one panel (true ranks 20
+    stored as 60, l = 40): the speculative sCQR3 breaks down, the call is redone
+    on the Householder path — eager and plan — and still reproduces the tensor."""
+    xp = _padded_low_rank(O, [16] * 5, [1, 20, 20, 20, 20, 1], [1, 60, 60, 60, 60, 1], 17)
+    y = P.round_fixed_krp(to_device(xp), [40] * 4, 3, rng=P.RNG_PHILOX)
+    assert np.all(np.isfinite(y.flat()))
+    assert rel_err_vs_ref(xp, y) <= 1e-10
+    assert left_orth_defect(y.cores()) <= 1e-12
+    t = to_device(xp)
+    plan = P.FixedKrpPlan(t, [40] * 4, 3)
+    plan.execute()
+    assert np.array_equal(plan.output.flat(), y.flat())
+    # refill with a full-rank input of the same shape: the speculative graph is valid again
+    x2 = O.two_part_tt(5, 16, 20, 40, 1e-8, 2203)
+    P.copy_from_host(t, x2.flat())
+    plan.execute()
+    y2 = P.round_fixed_krp(to_device(x2), [40] * 4, 3, rng=P.RNG_PHILOX)
+    assert np.array_equal(plan.output.flat(), y2.flat())
+    assert rel_err_vs_ref(O.round_fixed_krp(x2, [40] * 4, 3, rng=O.PHILOX), y2) <= 1e-10
+    plan.close()
+
+
 # ---- K1: Philox factors are bit-identical on host and device ---------------------
 
 @pytest.mark.parametrize("seed,mode,rows,cols,col0", [(7, 2, 20, 15, 0), (7, 30, 64, 110, 0), (2**40 + 3, 5, 33, 9, 17),

@@ -16,6 +16,33 @@ L.ttr_dev_thin_qr.argtypes = [C.c_void_p, C.c_int64, C.c_int64, C.c_void_p, C.c_
                               C.c_void_p, C.c_int64]
 
 
+L.ttr_dev_thin_qr_cholesky.argtypes = [C.c_void_p, C.c_int64, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p,
+                                       C.c_int64, C.c_void_p, C.c_int64, C.c_void_p]
+
+
+def bench_chol(ctx, m, n, reps=20):
+    a = torch.randn(n, m, dtype=torch.float64, device="cuda")
+    q = torch.empty(n, m, dtype=torch.float64, device="cuda")
+    bd = C.c_int(0)
+    s = torch.cuda.current_stream()
+    for _ in range(2):
+        L.ttr_dev_thin_qr_cholesky(ctx._h, m, n, a.data_ptr(), m, q.data_ptr(), m, None, 1, C.byref(bd))
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(s)
+    for _ in range(reps):  # each call ends with a flag read (one sync)
+        L.ttr_dev_thin_qr_cholesky(ctx._h, m, n, a.data_ptr(), m, q.data_ptr(), m, None, 1, C.byref(bd))
+    e1.record(s)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    qt = q.T
+    orth = torch.linalg.norm(qt.T @ qt - torch.eye(n, dtype=torch.float64, device="cuda")).item()
+    at = a.T
+    res = torch.linalg.norm(qt @ (qt.T @ at) - at).item() / torch.linalg.norm(at).item()
+    print(f"sCQR3 {m}x{n}: {ms:.3f} ms  ({4 * m * n * n / ms / 1e9:.2f} TF/s charged)  orth {orth:.2e} "
+          f"resid {res:.2e} breakdown {bd.value}", flush=True)
+
+
 def bench_qr(ctx, m, n, reps=20):
     a = torch.randn(n, m, dtype=torch.float64, device="cuda")  # column-major m x n
     q = torch.empty(n, m, dtype=torch.float64, device="cuda")
@@ -55,6 +82,8 @@ def main():
         shapes = [(int(sys.argv[i]), int(sys.argv[i + 1])) for i in range(1, len(sys.argv) - 1, 2)]
     for m, n in shapes:
         bench_qr(ctx, m, n)
+        if n <= 416 and m >= n:
+            bench_chol(ctx, m, n)
         a = torch.randn(m, n, dtype=torch.float64, device="cuda")
         torch.cuda.synchronize()
         t = time.perf_counter()
