@@ -53,7 +53,8 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
-__host__ __device__ constexpr int chol_ldp(int n) { return ((n + 3) / 4) * 4 + 4; }
+// row panel: n - j0 columns + 32 appended identity columns (-> inv(R_JJ)) + 4 pad
+__host__ __device__ constexpr int chol_ldp(int n) { return ((n + 3) / 4) * 4 + 36; }
 __host__ __device__ constexpr int trsm_ld(int n) { return ((n + 31) / 32) * 32 + 4; }  // % 16 == 4
 
 struct CholArgs {
@@ -91,8 +92,8 @@ __global__ void __launch_bounds__(kCholThreads) chol_kernel(CholArgs p) {
     long long t_last = clock64();
 #endif
     extern __shared__ __align__(16) double smem[];
-    __shared__ double dall[kCholQrMaxN + 32];  // 1 / r_kk
-    __shared__ double pv[32];                  // pivots of the current block
+    __shared__ double pv[32], rsq[32], rinv[32];  // pivots of the current block, sqrt, 1 / sqrt
+    __shared__ double prcp[32];                   // 1 / pivot
     __shared__ double red[kCholThreads / 32];
     __shared__ int bad;
     const int n = p.n, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -137,108 +138,166 @@ __global__ void __launch_bounds__(kCholThreads) chol_kernel(CholArgs p) {
             bad = 1;
     }
     for (int j0 = 0; j0 < n; j0 += 32) {
-        const int b = min(32, n - j0), nt = n - j0;  // panel columns c' in [0, nt)
+        const int b = min(32, n - j0), nt = n - j0;  // panel columns c' in [0, nt), then 32 identity columns
         for (int cc = tid; cc < nt; cc += kCholThreads)
-            for (int i = 0; i < 32; ++i)
-                RP[i * ldp + cc] = (i < b && i <= cc) ? A[(j0 + i) + (j0 + cc) * lda] + (i == cc ? shift : 0.0) : 0.0;
+            for (int i = 0; i < 32; ++i) {
+                const bool in = i < b && i <= cc;
+                if constexpr (SM)
+                    RP[i * ldp + cc] = in ? A[(j0 + i) + (j0 + cc) * lda] : 0.0;
+                else  // global -> shared without a register round trip (latency-bound otherwise)
+                    cp_async8(RP + i * ldp + cc, A + (in ? (j0 + i) + (j0 + cc) * lda : 0), in ? 8 : 0);
+            }
+        cp_commit();
+        for (int e = tid; e < 32 * 32; e += kCholThreads) {
+            const int i = e & 31, a = e >> 5;
+            RP[i * ldp + nt + a] = (i == a && a < b) ? 1.0 : 0.0;
+        }
+        cp_wait<0>();
+        __syncthreads();
+        if (tid < b && shift != 0.0) RP[tid * ldp + tid] += shift;
         __syncthreads();
         CHOL_T(1);
-        for (int k = 0; k < b; ++k) {
-            double piv = RP[k * ldp + k];
-            if (!(piv > 0.0) || !isfinite(piv)) {
-                if (tid == 0) bad = 1;
-                piv = 1.0;  // keep the factor finite; the result is discarded
+        // elimination with deferred scaling: row_i -= (G(k, i) / g_kk) row_k, i > k,
+        // over the whole row panel (diagonal block, panel columns, identity
+        // columns) at once: thread (row group rg, column lane cl) owns rows
+        // rg + 4q and columns cl + 64p; one barrier per step. Regular columns
+        // only need their upper part (i <= c), the identity columns all rows.
+        const int ncol = nt + 32;
+        {
+            const int rg = tid >> 6, cl = tid & 63;
+            for (int k = 0; k < b; ++k) {
+                double piv = RP[k * ldp + k];
+                if (!(piv > 0.0) || !isfinite(piv)) {
+                    if (tid == 0) bad = 1;
+                    piv = 1.0;  // keep the factor finite; the result is discarded
+                }
+                if (tid == 0) pv[k] = piv;
+                const double invp = 1.0 / piv;
+                const double* rk = RP + k * ldp;
+                double ri[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) ri[q] = rk[rg + 4 * q] * invp;  // multipliers G(k, i) / g_kk
+                for (int c0 = k + 1; c0 < ncol; c0 += 64) {
+                    const int cc = c0 + cl;
+                    if (cc >= ncol) continue;
+                    const double rc = rk[cc];
+                    const int iend = cc < nt ? min(cc, b - 1) : b - 1;
+                    double v[8];
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) v[q] = RP[(rg + 4 * q) * ldp + cc];
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        const int i = rg + 4 * q;
+                        if (i > k && i <= iend) RP[i * ldp + cc] = fma(-ri[q], rc, v[q]);
+                    }
+                }
+                __syncthreads();
             }
-            if (tid == 0) pv[k] = piv;
-            const double invp = 1.0 / piv;
-            const double* rk = RP + k * ldp;
-            for (int cc = k + 1 + tid; cc < nt; cc += kCholThreads) {
-                const double f = rk[cc] * invp;
-                const int iend = min(cc, b - 1);
-                for (int i = k + 1; i <= iend; ++i) RP[i * ldp + cc] = fma(-rk[i], f, RP[i * ldp + cc]);
-            }
-            __syncthreads();
         }
         CHOL_T(2);
-        // R rows: R(j0 + k, c) = G(k, c) / sqrt(g_kk) (c > k), R(k, k) = sqrt(g_kk)
-        for (int cc = tid; cc < nt; cc += kCholThreads) {
-            for (int k = 0; k < b && k <= cc; ++k) {
-                const double r = sqrt(pv[k]);
-                const double v = (k == cc) ? r : RP[k * ldp + cc] / r;
-                RP[k * ldp + cc] = v;
-                A[(j0 + k) + (j0 + cc) * lda] = v;
-            }
-            if (cc < b) dall[j0 + cc] = 1.0 / sqrt(pv[cc]);
+        // R rows: R(j0 + k, c) = G(k, c) / sqrt(g_kk) (c > k), R(k, k) = sqrt(g_kk); the
+        // identity columns become inv(R_JJ)^T
+        if (tid < 32) {
+            const double r = tid < b ? sqrt(pv[tid]) : 1.0;
+            rsq[tid] = r;
+            rinv[tid] = 1.0 / r;
         }
-        // zero the panel's padding columns so the 4-wide tiles read zeros
-        for (int e = tid; e < 32 * 4; e += kCholThreads) {
-            const int r = e >> 2, cc = nt + (e & 3);
-            if (cc < ldp) RP[r * ldp + cc] = 0.0;
+        __syncthreads();
+        {
+            const int rg = tid >> 6, cl = tid & 63;
+            for (int cc = cl; cc < ncol; cc += 64) {
+                const int kend = cc < nt ? min(cc, b - 1) : b - 1;
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const int k = rg + 4 * q;
+                    if (k <= kend) {
+                        const double v = (k == cc) ? rsq[k] : RP[k * ldp + cc] * rinv[k];
+                        RP[k * ldp + cc] = v;
+                        if (cc < nt) A[(j0 + k) + (j0 + cc) * lda] = v;
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        // inv(R_JJ) (column-major 32 x 32) = transpose of the identity columns
+        for (int e = tid; e < 32 * 32; e += kCholThreads) {
+            const int i = e & 31, c = e >> 5;
+            p.Rinv[static_cast<i64>(j0 / 32) * 1024 + i + 32 * c] = (i < b && c < b) ? RP[c * ldp + nt + i] : 0.0;
+        }
+        __syncthreads();  // the identity columns are read above before the padding below overwrites them
+        // zero the panel's padding columns past the trailing block so the 4-wide tiles read zeros
+        for (int e = tid; e < 32 * 8; e += kCholThreads) {
+            const int r = e >> 3, cc = nt + (e & 7);
+            RP[r * ldp + cc] = 0.0;
         }
         __syncthreads();
         CHOL_T(3);
         // trailing update of the upper triangle: G(i, j) -= sum_r P(r, i) P(r, j)
-        // over the panel columns past the diagonal block, 4 x 4 tiles (ti <= tj)
+        // over the panel columns past the diagonal block, 4 (i) x 8 (j) register
+        // tiles with i <= j somewhere in the tile; lanes of a warp share the
+        // j-tile (broadcast loads), so the update is FMA-bound; the next tile's
+        // old values load while this tile computes
         const int c1 = j0 + b, nr = n - c1;
         const double* Pb = RP + b;
-        const int nt4 = (nr + 3) / 4, ntiles = nt4 * (nt4 + 1) / 2;
-        for (int t = tid; t < ntiles; t += kCholThreads) {
-            int tj = static_cast<int>((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
-            while (tj * (tj + 1) / 2 > t) --tj;
-            while ((tj + 1) * (tj + 2) / 2 <= t) ++tj;
-            const int ti = t - tj * (tj + 1) / 2;
-            double old[4][4];
+        const int nj = (nr + 7) / 8, ntiles = nj * (nj + 1);  // j-tile tj holds i-tiles 0 .. 2 tj + 1
+        auto tile_of = [&](int t, int& ti, int& tj) {
+            tj = static_cast<int>((sqrt(4.0 * t + 1.0) - 1.0) * 0.5);
+            while (tj * (tj + 1) > t) --tj;
+            while ((tj + 1) * (tj + 2) <= t) ++tj;
+            ti = t - tj * (tj + 1);
+        };
+        double oldv[4][8];
+        auto load_old = [&](int ti, int tj) {
 #pragma unroll
-            for (int v = 0; v < 4; ++v)
+            for (int v = 0; v < 8; ++v)
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
-                    const int i = 4 * ti + u, j = 4 * tj + v;
-                    old[u][v] = (i <= j && j < nr) ? A[(c1 + i) + (c1 + j) * lda] : 0.0;
+                    const int i = 4 * ti + u, j = 8 * tj + v;
+                    oldv[u][v] = (i <= j && j < nr) ? A[(c1 + i) + (c1 + j) * lda] : 0.0;
                 }
-            double acc[4][4];
+        };
+        int ti = 0, tj = 0;
+        if (tid < ntiles) {
+            tile_of(tid, ti, tj);
+            load_old(ti, tj);
+        }
+        for (int t = tid; t < ntiles; t += kCholThreads) {
+            double acc[4][8];
 #pragma unroll
             for (int u = 0; u < 4; ++u)
 #pragma unroll
-                for (int v = 0; v < 4; ++v) acc[u][v] = 0.0;
+                for (int v = 0; v < 8; ++v) acc[u][v] = oldv[u][v];
+            const int cti = ti, ctj = tj;
+            if (t + kCholThreads < ntiles) {
+                tile_of(t + kCholThreads, ti, tj);
+                load_old(ti, tj);
+            }
 #pragma unroll 2
             for (int r = 0; r < b; ++r) {
-                const double2 i01 = *reinterpret_cast<const double2*>(Pb + r * ldp + 4 * ti);
-                const double2 i23 = *reinterpret_cast<const double2*>(Pb + r * ldp + 4 * ti + 2);
-                const double2 j01 = *reinterpret_cast<const double2*>(Pb + r * ldp + 4 * tj);
-                const double2 j23 = *reinterpret_cast<const double2*>(Pb + r * ldp + 4 * tj + 2);
-                const double pi[4] = {i01.x, i01.y, i23.x, i23.y}, pj[4] = {j01.x, j01.y, j23.x, j23.y};
+                const double* pr = Pb + r * ldp;
+                const double2 i01 = *reinterpret_cast<const double2*>(pr + 4 * cti);
+                const double2 i23 = *reinterpret_cast<const double2*>(pr + 4 * cti + 2);
+                const double2 j01 = *reinterpret_cast<const double2*>(pr + 8 * ctj);
+                const double2 j23 = *reinterpret_cast<const double2*>(pr + 8 * ctj + 2);
+                const double2 j45 = *reinterpret_cast<const double2*>(pr + 8 * ctj + 4);
+                const double2 j67 = *reinterpret_cast<const double2*>(pr + 8 * ctj + 6);
+                const double pi[4] = {i01.x, i01.y, i23.x, i23.y};
+                const double pj[8] = {j01.x, j01.y, j23.x, j23.y, j45.x, j45.y, j67.x, j67.y};
 #pragma unroll
                 for (int u = 0; u < 4; ++u)
 #pragma unroll
-                    for (int v = 0; v < 4; ++v) acc[u][v] = fma(pi[u], pj[v], acc[u][v]);
+                    for (int v = 0; v < 8; ++v) acc[u][v] = fma(-pi[u], pj[v], acc[u][v]);
             }
 #pragma unroll
-            for (int v = 0; v < 4; ++v)
+            for (int v = 0; v < 8; ++v)
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
-                    const int i = 4 * ti + u, j = 4 * tj + v;
-                    if (i <= j && j < nr) A[(c1 + i) + (c1 + j) * lda] = old[u][v] - acc[u][v];
+                    const int i = 4 * cti + u, j = 8 * ctj + v;
+                    if (i <= j && j < nr) A[(c1 + i) + (c1 + j) * lda] = acc[u][v];
                 }
         }
         __syncthreads();
         CHOL_T(4);
-    }
-    // inverses of the diagonal blocks for the blocked TRSM: X = U^{-1} by rows
-    // from the bottom, X(i, c) = (delta_ic - sum_{k > i} U(i, k) X(k, c)) / U(i, i);
-    // one warp per block, lane = column c; X staged in the block's output
-    for (int J = warp; J * 32 < n; J += kCholThreads / 32) {
-        const int j0 = J * 32, b = min(32, n - j0), c = lane;
-        double* X = p.Rinv + static_cast<i64>(J) * 1024;  // column-major 32 x 32
-        for (int i = 31; i >= 0; --i) {
-            double v = 0.0;
-            if (i < b && c < b && i <= c) {
-                v = (i == c) ? 1.0 : 0.0;
-                for (int k = i + 1; k <= c; ++k) v = fma(-A[(j0 + i) + (j0 + k) * lda], X[k + 32 * c], v);
-                v *= dall[j0 + i];
-            }
-            X[i + 32 * c] = v;
-            __syncwarp();
-        }
     }
     CHOL_T(5);
     // R out (upper) with zeros below the diagonal

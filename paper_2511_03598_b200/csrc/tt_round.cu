@@ -469,7 +469,14 @@ void rand_orth_sweep(Ctx& c, const TTDev& t, i64 width, const std::vector<const 
         // Q = thin_qr_q(S) -> output core k
         {
             PhaseScope ph(c, kPhaseQr);
-            if (c.qr_spec && k < c.qr_hh_from && l > 32 && rows >= 2 * l && cholqr_fits(rows, l) &&
+            // The shifted Cholesky QR is opt-in (TTR_QR_CHOL=1): measured on B200 its
+            // one-CTA Cholesky (~90 us at n = 110, ~680 us at n = 320, latency-bound)
+            // keeps it behind the Householder panels (K4c).
+            static const bool chol_on = [] {
+                const char* e = std::getenv("TTR_QR_CHOL");
+                return e && e[0] == '1';
+            }();
+            if (chol_on && c.qr_spec && k < c.qr_hh_from && l > 32 && rows >= 2 * l && cholqr_fits(rows, l) &&
                 wbound[k + 1] >= l) {
                 thin_qr_cholesky(c, rows, l, S.p, rows, out->core(k - 1), rows, nullptr, 1, static_cast<int>(k));
                 c.qr_spec_used = true;

@@ -127,27 +127,52 @@ def _padded_low_rank(O, modes, true_r, pad_r, seed):
     return O.TT.from_cores(out)
 
 
-def test_fixed_krp_cholesky_breakdown_falls_back(P, O):
-    """Exactly rank-deficient sketches wider than one panel (true ranks 20
-    stored as 60, l = 40): the speculative sCQR3 breaks down, the call is redone
-    on the Householder path — eager and plan — and still reproduces the tensor."""
-    xp = _padded_low_rank(O, [16] * 5, [1, 20, 20, 20, 20, 1], [1, 60, 60, 60, 60, 1], 17)
-    y = P.round_fixed_krp(to_device(xp), [40] * 4, 3, rng=P.RNG_PHILOX)
-    assert np.all(np.isfinite(y.flat()))
-    assert rel_err_vs_ref(xp, y) <= 1e-10
-    assert left_orth_defect(y.cores()) <= 1e-12
-    t = to_device(xp)
-    plan = P.FixedKrpPlan(t, [40] * 4, 3)
-    plan.execute()
-    assert np.array_equal(plan.output.flat(), y.flat())
-    # refill with a full-rank input of the same shape: the speculative graph is valid again
-    x2 = O.two_part_tt(5, 16, 20, 40, 1e-8, 2203)
-    P.copy_from_host(t, x2.flat())
-    plan.execute()
-    y2 = P.round_fixed_krp(to_device(x2), [40] * 4, 3, rng=P.RNG_PHILOX)
-    assert np.array_equal(plan.output.flat(), y2.flat())
-    assert rel_err_vs_ref(O.round_fixed_krp(x2, [40] * 4, 3, rng=O.PHILOX), y2) <= 1e-10
-    plan.close()
+_CHOL_SWEEP_SCRIPT = r"""
+import sys, numpy as np
+sys.path[:0] = [sys.argv[1], sys.argv[2], sys.argv[3]]
+import paper_2511_03598_b200 as P, py_oracle as O
+from helpers import left_orth_defect, rel_err_vs_ref, to_device
+from test_gpu_parity import _padded_low_rank
+# exactly rank-deficient padded input (true ranks 20 stored as 60, l = 40):
+# the speculative Cholesky QR of mode 1.. breaks down or yields a valid basis
+xp = _padded_low_rank(O, [16] * 5, [1, 20, 20, 20, 20, 1], [1, 60, 60, 60, 60, 1], 17)
+y = P.round_fixed_krp(to_device(xp), [40] * 4, 3, rng=P.RNG_PHILOX)
+assert np.all(np.isfinite(y.flat()))
+assert rel_err_vs_ref(xp, y) <= 1e-10
+assert left_orth_defect(y.cores()) <= 1e-12
+t = to_device(xp)
+plan = P.FixedKrpPlan(t, [40] * 4, 3)
+plan.execute()
+assert np.array_equal(plan.output.flat(), y.flat())
+# full-rank input of the same shape through the same plan, against the oracle
+x2 = O.two_part_tt(5, 16, 20, 40, 1e-8, 2203)
+P.copy_from_host(t, x2.flat())
+plan.execute()
+y2 = P.round_fixed_krp(to_device(x2), [40] * 4, 3, rng=P.RNG_PHILOX)
+assert np.array_equal(plan.output.flat(), y2.flat())
+assert rel_err_vs_ref(O.round_fixed_krp(x2, [40] * 4, 3, rng=O.PHILOX), y2) <= 1e-10
+# config-3 shapes (7040 x 110 sketches) at reduced order
+x3 = O.two_part_tt(6, 64, 100, 300, 1e-8, 1003)
+y3 = P.round_fixed_krp(to_device(x3), [110] * 5, 7, rng=P.RNG_PHILOX)
+assert rel_err_vs_ref(O.round_fixed_krp(x3, [110] * 5, 7, rng=O.PHILOX), y3) <= 1e-10
+plan.close()
+print("ok")
+"""
+
+
+def test_fixed_krp_cholesky_sweep_and_fallback(P, O):
+    """The opt-in Cholesky-QR sweep (TTR_QR_CHOL=1, read once per process, so
+    in a subprocess): oracle parity, and exactly rank-deficient sketches either
+    get a valid basis or are redone on the Householder path — eager and plan."""
+    import os
+    import subprocess
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    root = os.path.dirname(here)
+    env = dict(os.environ, TTR_QR_CHOL="1")
+    r = subprocess.run([sys.executable, "-c", _CHOL_SWEEP_SCRIPT, root, os.path.join(root, "oracle"), here],
+                       env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
 
 
 # ---- K1: Philox factors are bit-identical on host and device ---------------------

@@ -41,7 +41,7 @@ int main(int argc, char** argv) {
         float ms; cudaEventElapsedTime(&ms, e0, e1);
         unsigned long long t[8]; cudaMemcpyFromSymbol(t, g_chol_trace, sizeof(t));
         int f; cudaMemcpy(&f, flag, 4, cudaMemcpyDeviceToHost);
-        printf("n=%d %.1f us flag %d err %s | cycles: load %llu dload %llu diag %llu panel %llu trail %llu inv %llu\n", n,
-               ms * 1e3, f, cudaGetErrorString(cudaGetLastError()), t[0], t[1], t[2], t[3], t[4], t[5]);
+        printf("n=%d %.1f us flag %d err %s | cycles: load %llu dload %llu diag %llu panel %llu trail %llu inv %llu diagwarp %llu\n", n,
+               ms * 1e3, f, cudaGetErrorString(cudaGetLastError()), t[0], t[1], t[2], t[3], t[4], t[5], t[6]);
     }
 }
