@@ -65,6 +65,89 @@ struct JacobiArgs {
     long long* trace;  // TTR_SVD_TRACE: [3] cycle sums of CTA 0 (intra, cross, move)
 };
 
+__device__ __forceinline__ double lds64(unsigned a) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];\n" : "=d"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void sts64(unsigned a, double v) { asm volatile("st.shared.f64 [%0], %1;\n" ::"r"(a), "d"(v)); }
+
+// Rotation parameters of the pair (al = |a_p|^2, be = |a_q|^2, ga = a_p . a_q);
+// false when the pair is already orthogonal to the dgesvj threshold.
+__device__ __forceinline__ bool jacobi_params(double al, double be, double ga, int M, double& c, double& s) {
+    // convergence threshold of LAPACK dgesvj: |ga| <= sqrt(M) eps sqrt(al be),
+    // squared (no square roots on the skip path)
+    if (ga == 0.0 || ga * ga <= static_cast<double>(M) * (DBL_EPSILON * DBL_EPSILON) * (al * be)) return false;
+    // zeta = (be - al) / (2 ga), t = sign(zeta) / (|zeta| + sqrt(1 + zeta^2)),
+    // scaled by |2 ga|: one sqrt, one division and one rsqrt per rotation
+    // instead of three of each
+    const double h = be - al, g2 = 2.0 * ga;
+    const double sz = ((h >= 0.0) == (g2 >= 0.0)) || h == 0.0 ? 1.0 : -1.0;
+    const double t = sz * fabs(g2) / (fabs(h) + sqrt(fma(h, h, g2 * g2)));
+    c = rsqrt(fma(t, t, 1.0));
+    s = c * t;
+    return true;
+}
+
+// Shared-memory columns of M <= 32 * kRotRows rows: both columns are read once
+// into registers (explicit shared-space loads, all in flight together),
+// rotated there and written back.
+constexpr int kRotRows = 16;
+__device__ __forceinline__ bool jacobi_rotate_smem(double* ap, double* aq, int M, int lane) {
+    const unsigned pa = static_cast<unsigned>(__cvta_generic_to_shared(ap)) + 8u * lane;
+    const unsigned pq = static_cast<unsigned>(__cvta_generic_to_shared(aq)) + 8u * lane;
+    double x[kRotRows], y[kRotRows];
+    double al = 0, be = 0, ga = 0;
+#pragma unroll
+    for (int t = 0; t < kRotRows; ++t) {
+        const bool in = lane + 32 * t < M;
+        x[t] = in ? lds64(pa + 256u * t) : 0.0;
+        y[t] = in ? lds64(pq + 256u * t) : 0.0;
+    }
+#pragma unroll
+    for (int t = 0; t < kRotRows; ++t) {
+        al = fma(x[t], x[t], al);
+        be = fma(y[t], y[t], be);
+        ga = fma(x[t], y[t], ga);
+    }
+    warp_sum3(al, be, ga);
+    double c, s;
+    if (!jacobi_params(al, be, ga, M, c, s)) return false;
+#pragma unroll
+    for (int t = 0; t < kRotRows; ++t) {
+        if (lane + 32 * t < M) {
+            sts64(pa + 256u * t, c * x[t] - s * y[t]);
+            sts64(pq + 256u * t, s * x[t] + c * y[t]);
+        }
+    }
+    return true;
+}
+
+// The same with the first column already in registers (x, rows lane + 32t).
+__device__ __forceinline__ bool jacobi_rotate_reg(double (&x)[kRotRows], double* aq, int M, int lane) {
+    const unsigned pq = static_cast<unsigned>(__cvta_generic_to_shared(aq)) + 8u * lane;
+    double y[kRotRows];
+    double al = 0, be = 0, ga = 0;
+#pragma unroll
+    for (int t = 0; t < kRotRows; ++t) y[t] = lane + 32 * t < M ? lds64(pq + 256u * t) : 0.0;
+#pragma unroll
+    for (int t = 0; t < kRotRows; ++t) {
+        al = fma(x[t], x[t], al);
+        be = fma(y[t], y[t], be);
+        ga = fma(x[t], y[t], ga);
+    }
+    warp_sum3(al, be, ga);
+    double c, s;
+    if (!jacobi_params(al, be, ga, M, c, s)) return false;
+#pragma unroll
+    for (int t = 0; t < kRotRows; ++t) {
+        const double xn = c * x[t] - s * y[t];
+        if (lane + 32 * t < M) sts64(pq + 256u * t, s * x[t] + c * y[t]);
+        x[t] = xn;
+    }
+    return true;
+}
+
 // Orthogonalise columns ap, aq (M rows). Loads run in chunks of 4 rows per
 // lane so each chunk's shared/global loads are in flight together.
 __device__ __forceinline__ bool jacobi_rotate(double* ap, double* aq, int M, int lane) {
@@ -77,11 +160,8 @@ __device__ __forceinline__ bool jacobi_rotate(double* ap, double* aq, int M, int
         ga = fma(x, y, ga);
     }
     warp_sum3(al, be, ga);
-    // convergence threshold of LAPACK dgesvj: sqrt(M) * eps relative to the pair
-    if (ga == 0.0 || fabs(ga) <= sqrt(static_cast<double>(M)) * DBL_EPSILON * sqrt(al * be)) return false;
-    const double zeta = (be - al) / (2.0 * ga);
-    const double t = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-    const double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
+    double c, s;
+    if (!jacobi_params(al, be, ga, M, c, s)) return false;
 #pragma unroll 4
     for (int row = lane; row < M; row += 32) {
         const double x = ap[row], y = aq[row];
@@ -153,6 +233,10 @@ __global__ void __launch_bounds__(kJw * 32, 1) jacobi_block_kernel(JacobiArgs p,
     cl.sync();
     int* flag0 = cl.map_shared_rank(&sweep_flag, 0);
     auto col = [&](int sl, int cc) { return slot[sl] + static_cast<i64>(cc) * M; };
+    const bool reg_rows = M <= 32 * kRotRows;
+    auto rot = [&](double* a, double* b2) {
+        return reg_rows ? jacobi_rotate_smem(a, b2, M, lane) : jacobi_rotate(a, b2, M, lane);
+    };
     // movement sources (position j <- j+1, P-1 <- 1, 0 fixed)
     int src0_cta = -1, src0_slot = 0, src1_cta, src1_slot;
     if (g >= 1) {
@@ -179,7 +263,7 @@ __global__ void __launch_bounds__(kJw * 32, 1) jacobi_block_kernel(JacobiArgs p,
                         int x = pl(i), y = pl(bb - 1 - i);
                         if (x > y) { const int t = x; x = y; y = t; }
                         if (y >= b) continue;
-                        rotated |= jacobi_rotate(col(sl, x), col(sl, y), M, lane);
+                        rotated |= rot(col(sl, x), col(sl, y));
                     }
                     __syncthreads();
                 }
@@ -187,9 +271,29 @@ __global__ void __launch_bounds__(kJw * 32, 1) jacobi_block_kernel(JacobiArgs p,
             const long long t1 = tr ? clock64() : 0;
             if (tr) tsum[0] += t1 - t0;
             // cross pairs (top i, bottom (i + s) mod b)
-            for (int sr = 0; sr < b; ++sr) {
-                for (int i = warp; i < b; i += kJw) rotated |= jacobi_rotate(col(0, i), col(1, (i + sr) % b), M, lane);
+            if (reg_rows && b <= kJw) {
+                // warp i keeps its top column in registers for the whole step (it
+                // meets every bottom column once): half the shared-memory traffic
+                // of the rotations, which is what bounds them
+                double x[kRotRows];
+                const unsigned px = warp < b ? static_cast<unsigned>(__cvta_generic_to_shared(col(0, warp))) + 8u * lane : 0u;
+#pragma unroll
+                for (int t = 0; t < kRotRows; ++t) x[t] = (warp < b && lane + 32 * t < M) ? lds64(px + 256u * t) : 0.0;
+                for (int sr = 0; sr < b; ++sr) {
+                    if (warp < b) rotated |= jacobi_rotate_reg(x, col(1, (warp + sr) % b), M, lane);
+                    __syncthreads();
+                }
+                if (warp < b) {
+#pragma unroll
+                    for (int t = 0; t < kRotRows; ++t)
+                        if (lane + 32 * t < M) sts64(px + 256u * t, x[t]);
+                }
                 __syncthreads();
+            } else {
+                for (int sr = 0; sr < b; ++sr) {
+                    for (int i = warp; i < b; i += kJw) rotated |= rot(col(0, i), col(1, (i + sr) % b));
+                    __syncthreads();
+                }
             }
             if (rotated && lane == 0) *reinterpret_cast<volatile int*>(flag0) = sweep + 1;
             rotated = false;
@@ -378,7 +482,26 @@ void svd_left(Ctx& c, i64 m, i64 n, const double* A_in, i64 lda_in, double* U, i
         N = k;
     }
     DBuf A(c, static_cast<std::size_t>(m * N));
-    copy_matrix(c, m, N, src, lds, A.p, m);
+    static const bool sort_cols = [] {  // experiments: de Rijk-style presort of the columns by norm
+        const char* e = std::getenv("TTR_SVD_SORT");
+        return e && e[0] == '1';
+    }();
+    if (sort_cols && N > 1) {
+        DBuf s0(c, static_cast<std::size_t>(N));
+        col_norms<<<static_cast<unsigned>((N * 32 + 255) / 256), 256, 0, c.stream>>>(static_cast<int>(m), static_cast<int>(N), src, lds, s0.p);
+        TTR_CUDA(cudaGetLastError());
+        std::vector<double> h(static_cast<std::size_t>(N));
+        TTR_CUDA(cudaMemcpyAsync(h.data(), s0.p, sizeof(double) * N, cudaMemcpyDeviceToHost, c.stream));
+        TTR_CUDA(cudaStreamSynchronize(c.stream));
+        std::vector<int> pi(static_cast<std::size_t>(N));
+        std::iota(pi.begin(), pi.end(), 0);
+        std::stable_sort(pi.begin(), pi.end(), [&](int a, int b) { return h[a] > h[b]; });
+        for (i64 j = 0; j < N; ++j)
+            TTR_CUDA(cudaMemcpyAsync(A.p + j * m, src + static_cast<i64>(pi[j]) * lds, sizeof(double) * m,
+                                     cudaMemcpyDeviceToDevice, c.stream));
+    } else {
+        copy_matrix(c, m, N, src, lds, A.p, m);
+    }
     jacobi_columns(c, m, N, A.p, m);
     DBuf s(c, static_cast<std::size_t>(N));
     col_norms<<<static_cast<unsigned>((N * 32 + 255) / 256), 256, 0, c.stream>>>(static_cast<int>(m), static_cast<int>(N), A.p, m, s.p);
