@@ -130,11 +130,20 @@ __device__ __forceinline__ bool jacobi_rotate_reg(double (&x)[kRotRows], double*
     double al = 0, be = 0, ga = 0;
 #pragma unroll
     for (int t = 0; t < kRotRows; ++t) y[t] = lane + 32 * t < M ? lds64(pq + 256u * t) : 0.0;
+    {
+        double al1 = 0, be1 = 0, ga1 = 0;  // two chains each (fma latency)
 #pragma unroll
-    for (int t = 0; t < kRotRows; ++t) {
-        al = fma(x[t], x[t], al);
-        be = fma(y[t], y[t], be);
-        ga = fma(x[t], y[t], ga);
+        for (int t = 0; t < kRotRows; t += 2) {
+            al = fma(x[t], x[t], al);
+            be = fma(y[t], y[t], be);
+            ga = fma(x[t], y[t], ga);
+            al1 = fma(x[t + 1], x[t + 1], al1);
+            be1 = fma(y[t + 1], y[t + 1], be1);
+            ga1 = fma(x[t + 1], y[t + 1], ga1);
+        }
+        al += al1;
+        be += be1;
+        ga += ga1;
     }
     warp_sum3(al, be, ga);
     double c, s;
@@ -210,7 +219,7 @@ __global__ void __launch_bounds__(kSvdThreads) jacobi_kernel(JacobiArgs p) {
 constexpr int kJw = 16;      // warps per CTA
 constexpr int kJStage = 24;  // doubles per thread staged per incoming block
 
-__global__ void __launch_bounds__(kJw * 32, 1) jacobi_block_kernel(JacobiArgs p, int b) {
+__global__ void __launch_bounds__(kJw * 32, 1) jacobi_block_kernel(JacobiArgs p, int b, int dbuf) {
     extern __shared__ double jsm[];
     __shared__ int sweep_flag;
     cg::cluster_group cl = cg::this_cluster();
@@ -219,7 +228,11 @@ __global__ void __launch_bounds__(kJw * 32, 1) jacobi_block_kernel(JacobiArgs p,
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int M = p.m, n = p.n;
     const i64 slot_len = static_cast<i64>(b) * M;
+    // dbuf: four slots (the incoming blocks land in the two spare ones, one
+    // cluster barrier per move); otherwise two, staged through registers
     double* slot[2] = {jsm, jsm + slot_len};
+    double* spare[2] = {jsm + 2 * slot_len, jsm + 3 * slot_len};
+    int mv = 0;  // dbuf: parity of the moves so far (which half holds the moving slots)
     // home: position g (slot 0) holds block g; position P-1-g (slot 1) holds block P-1-g
     auto load_block = [&](double* dst, int blk) {
         for (i64 e = tid; e < slot_len; e += kJw * 32) {
@@ -299,6 +312,41 @@ __global__ void __launch_bounds__(kJw * 32, 1) jacobi_block_kernel(JacobiArgs p,
             rotated = false;
             const long long t2 = tr ? clock64() : 0;
             if (tr) tsum[1] += t2 - t1;
+            if (dbuf) {
+                // move: after one cluster barrier every source block is final;
+                // copy it (16-byte DSMEM loads) into the spare slots and swap
+                cl.sync();
+                // every moving slot swaps in lockstep (parity mv); only CTA 0's
+                // slot 0 (the fixed position) never moves
+                auto cur = [&](int cta, int sl) {
+                    double* base = (cta == 0 && sl == 0) ? jsm : (mv ? jsm + (2 + sl) * slot_len : jsm + sl * slot_len);
+                    return reinterpret_cast<const double2*>(cl.map_shared_rank(base, cta));
+                };
+                const double2* in0 = src0_cta >= 0 ? cur(src0_cta, src0_slot) : nullptr;
+                const double2* in1 = cur(src1_cta, src1_slot);
+                double2* o0 = reinterpret_cast<double2*>(spare[0]);
+                double2* o1 = reinterpret_cast<double2*>(spare[1]);
+                const int half = static_cast<int>(slot_len / 2);
+                for (int e = tid; e < half; e += kJw * 32) {
+                    const double2 v1 = in1[e];
+                    if (in0) o0[e] = in0[e];
+                    o1[e] = v1;
+                }
+                __syncthreads();
+                if (in0) {
+                    double* tmp = slot[0];
+                    slot[0] = spare[0];
+                    spare[0] = tmp;
+                }
+                {
+                    double* tmp = slot[1];
+                    slot[1] = spare[1];
+                    spare[1] = tmp;
+                }
+                mv ^= 1;
+                if (tr) tsum[2] += clock64() - t2;
+                continue;
+            }
             // move: stage the incoming blocks in registers, barrier, write
             cl.sync();
             double st0[kJStage], st1[kJStage];
@@ -388,6 +436,7 @@ int jacobi_columns(Ctx& c, i64 M, i64 Nn, double* A, i64 lda) {
         G = std::max<i64>(1, (Nn + 31) / 32);
         b = (Nn + 2 * G - 1) / (2 * G);
         auto fits = [&] { return 2 * b * M * 8 <= max_smem && b * M <= static_cast<i64>(kJStage) * kJw * 32; };
+        auto fits4 = [&] { return 4 * b * M * 8 <= max_smem && (b * M) % 2 == 0; };
         while (G < 16 && !fits()) {
             ++G;
             b = (Nn + 2 * G - 1) / (2 * G);
@@ -401,7 +450,12 @@ int jacobi_columns(Ctx& c, i64 M, i64 Nn, double* A, i64 lda) {
             cudaEventRecord(t0, c.stream);
         }
         if (cluster) {
-            const std::size_t smem = static_cast<std::size_t>(2 * b * M * 8);
+            static const bool dbuf_off = [] {
+                const char* e = std::getenv("TTR_SVD_DBUF");
+                return e && e[0] == '0';
+            }();
+            const int dbuf = (!dbuf_off && fits4()) ? 1 : 0;
+            const std::size_t smem = static_cast<std::size_t>((dbuf ? 4 : 2) * b * M * 8);
             auto kern = jacobi_block_kernel;
             static std::atomic<std::uint64_t> configured{0};  // bit d: attributes set on device d
             if (first_on_device(configured)) {
@@ -420,7 +474,7 @@ int jacobi_columns(Ctx& c, i64 M, i64 Nn, double* A, i64 lda) {
             attr[0].val.clusterDim.z = 1;
             cfg.attrs = attr;
             cfg.numAttrs = 1;
-            TTR_CUDA(cudaLaunchKernelEx(&cfg, kern, ja, static_cast<int>(b)));
+            TTR_CUDA(cudaLaunchKernelEx(&cfg, kern, ja, static_cast<int>(b), dbuf));
         } else {
             const int warps_needed = ja.N / 2;
             int blocks = (warps_needed * 32 + kSvdThreads - 1) / kSvdThreads;
