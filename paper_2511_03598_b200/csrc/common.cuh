@@ -220,7 +220,7 @@ void qr_small_batched(Ctx& c, i64 m, i64 n, const double* A, i64 lda, i64 sA, do
                       i64 ldr, i64 sR, i64 batch);
 // Omega for a batch: tensor b uses seed derive_seed(seed, b).
 void philox_factor_batched(Ctx& c, std::uint64_t seed, i64 mode, i64 rows, i64 cols, double* out, i64 ld, i64 stride,
-                           i64 batch);
+                           i64 batch, i64 b0 = 0);  // tensor b of the launch is tensor b0 + b of the batch
 
 // ---- kernels (dense_ops.cu) -------------------------------------------------
 void philox_factor(Ctx& c, std::uint64_t seed, i64 mode, i64 rows, i64 cols, i64 col0, double* out, i64 ld);

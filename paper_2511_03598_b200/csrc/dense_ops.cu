@@ -52,7 +52,7 @@ __device__ __forceinline__ std::uint64_t dev_derive_seed(std::uint64_t seed, std
 
 // Omega_mode for every tensor b of a batch (tensor b: seed derive_seed(seed, b)).
 __global__ void philox_factor_batched_kernel(std::uint64_t seed, std::uint32_t mode, int rows, int cols, double* out,
-                                             i64 ld, i64 stride, int batch) {
+                                             i64 ld, i64 stride, int batch, i64 b0) {
     const int pairs = (rows + 1) / 2;
     const i64 per = static_cast<i64>(pairs) * cols, total = per * batch;
     for (i64 idx = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; idx < total;
@@ -61,7 +61,7 @@ __global__ void philox_factor_batched_kernel(std::uint64_t seed, std::uint32_t m
         const i64 r = idx % per;
         const int p = static_cast<int>(r % pairs), c = static_cast<int>(r / pairs);
         double e, o;
-        ttr_philox_gauss_pair(dev_derive_seed(seed, static_cast<std::uint64_t>(b)), mode, static_cast<std::uint32_t>(c),
+        ttr_philox_gauss_pair(dev_derive_seed(seed, static_cast<std::uint64_t>(b0 + b)), mode, static_cast<std::uint32_t>(c),
                               static_cast<std::uint32_t>(p), TTR_PHILOX_TAG_KRP, &e, &o);
         double* dst = out + b * stride + static_cast<i64>(c) * ld + 2 * p;
         dst[0] = e;
@@ -208,12 +208,12 @@ void philox_factor(Ctx& c, std::uint64_t seed, i64 mode, i64 rows, i64 cols, i64
 }
 
 void philox_factor_batched(Ctx& c, std::uint64_t seed, i64 mode, i64 rows, i64 cols, double* out, i64 ld, i64 stride,
-                           i64 batch) {
+                           i64 batch, i64 b0) {
     if (rows <= 0 || cols <= 0 || batch <= 0) return;
     c.counts.rng += static_cast<std::uint64_t>(rows * cols * batch);
     philox_factor_batched_kernel<<<grid_for(c, static_cast<std::size_t>((rows + 1) / 2 * cols * batch)), kThreads, 0,
                                    c.stream>>>(seed, static_cast<std::uint32_t>(mode), static_cast<int>(rows),
-                                               static_cast<int>(cols), out, ld, stride, static_cast<int>(batch));
+                                               static_cast<int>(cols), out, ld, stride, static_cast<int>(batch), b0);
     TTR_CUDA(cudaGetLastError());
     c.launched();
 }

@@ -125,108 +125,154 @@ std::unique_ptr<TTBatch> round_fixed_krp_batched(Ctx& c, const TTBatch& t, const
     for (i64 k = 1; k < d; ++k) r[k] = std::min({targets[k - 1], r[k - 1] * t.n[k - 1], t.r[k]});
     auto out = std::make_unique<TTBatch>(c, B, t.n, r);
 
-    // ---- sketch: W_k for k = d..2 (Omega_k drawn per tensor from derive_seed(seed, b)) ----
-    const i64 ldwt = even_ld(width);
-    std::vector<DBuf> W(d + 2), Wt(d + 2);
-    std::vector<i64> ldw(d + 2, 0), sw(d + 2, 0), swt(d + 2, 0);
-    DBuf ones(c, static_cast<std::size_t>(ldwt));
-    fill(c, ones.p, static_cast<std::size_t>(ldwt), 1.0);
-    {
-        PhaseScope ph(c, kPhaseSketch);
-        SketchScope scope(c);
-        for (i64 k = d; k >= 2; --k) {
-            const i64 rl = t.r[k - 1], nk = t.n[k - 1], rr = t.r[k];
-            const i64 ldo = even_ld(nk), so = ldo * width;
-            DBuf om(c, static_cast<std::size_t>(so * B));
-            philox_factor_batched(c, seed, k, nk, width, om.p, ldo, so, B);
-            ldw[k] = even_ld(rl);
-            sw[k] = ldw[k] * width;
-            W[k] = DBuf(c, static_cast<std::size_t>(sw[k] * B));
-            swt[k] = ldwt * rl;
-            if (k >= 3) Wt[k] = DBuf(c, static_cast<std::size_t>(swt[k] * B));
-            const bool last = (k == d);
-            krp_step_batched(c, rl, nk, rr, width, t.core(0, k - 1), t.stride, om.p, ldo, so, last ? ones.p : Wt[k + 1].p,
-                             ldwt, last ? 0 : swt[k + 1], W[k].p, ldw[k], sw[k], k >= 3 ? Wt[k].p : nullptr, ldwt, swt[k],
-                             B, last);
-        }
-    }
+    // The batch runs as G independent groups of tensors, each on its own side
+    // stream, so that one group's latency-bound QR launches overlap another
+    // group's HBM/DMMA-bound sketch and sweep kernels (results are per tensor,
+    // identical to one group). TTR_BATCH_GROUPS overrides G (1 = one stream).
+    static const int groups_env = [] {
+        const char* e = std::getenv("TTR_BATCH_GROUPS");
+        return e ? std::atoi(e) : 0;
+    }();
+    // (phase timing — bench.py's per-kernel roofline run — needs one stream)
+    const i64 G = c.timing ? 1 : std::max<i64>(1, std::min<i64>(groups_env > 0 ? groups_env : (B >= 1024 ? 2 : 1), B));
+    auto run_group = [&](i64 b0, i64 Bg) {
 
-    // ---- left-to-right Rand-Orth sweep ----
-    i64 max_work = 0, max_s = 0;
-    for (i64 k = 1; k < d; ++k) {
-        max_work = std::max(max_work, r[k] * t.n[k] * t.r[k + 1]);
-        max_s = std::max(max_s, r[k - 1] * t.n[k - 1] * r[k]);
-    }
-    DBuf work(c, static_cast<std::size_t>(max_work * B));
-    DBuf S(c, static_cast<std::size_t>(max_s * B));
-    DBuf M(c, static_cast<std::size_t>(width * t.max_rank() * B));
-    const double* v = t.core(0, 0);
-    i64 sv = t.stride;
-    bool s_ready = false;  // S of this step already formed by the previous fused step
-    for (i64 k = 1; k < d; ++k) {
-        const i64 rows = r[k - 1] * t.n[k - 1], cols = t.r[k], l = r[k];
-        if (!s_ready) {
-            PhaseScope ph(c, kPhaseGemm);
-            gemm_batched(c, false, rows, l, cols, 1.0, v, rows, sv, W[k + 1].p, ldw[k + 1], sw[k + 1], 0.0, S.p, rows,
-                         rows * l, B);
-        }
+        // ---- sketch: W_k for k = d..2 (Omega_k drawn per tensor from derive_seed(seed, b)) ----
+        const i64 ldwt = even_ld(width);
+        std::vector<DBuf> W(d + 2), Wt(d + 2);
+        std::vector<i64> ldw(d + 2, 0), sw(d + 2, 0), swt(d + 2, 0);
+        DBuf ones(c, static_cast<std::size_t>(ldwt));
+        fill(c, ones.p, static_cast<std::size_t>(ldwt), 1.0);
         {
-            PhaseScope ph(c, kPhaseQr);
-            c.charge_qr(4ULL * static_cast<std::uint64_t>(rows) * l * std::min(rows, l) * B);
-            if (rows * l <= 26000) {
-                qr_small_batched(c, rows, l, S.p, rows, rows * l, out->core(0, k - 1), rows, out->stride, nullptr, 1, 0, B);
-            } else {
-                const Counts keep = c.counts;
-                for (i64 b = 0; b < B; ++b)
-                    thin_qr(c, rows, l, S.p + b * rows * l, rows, out->core(b, k - 1), rows, nullptr, 1);
-                c.counts = keep;
+            PhaseScope ph(c, kPhaseSketch);
+            SketchScope scope(c);
+            for (i64 k = d; k >= 2; --k) {
+                const i64 rl = t.r[k - 1], nk = t.n[k - 1], rr = t.r[k];
+                const i64 ldo = even_ld(nk), so = ldo * width;
+                DBuf om(c, static_cast<std::size_t>(so * Bg));
+                philox_factor_batched(c, seed, k, nk, width, om.p, ldo, so, Bg, b0);
+                ldw[k] = even_ld(rl);
+                sw[k] = ldw[k] * width;
+                W[k] = DBuf(c, static_cast<std::size_t>(sw[k] * Bg));
+                swt[k] = ldwt * rl;
+                if (k >= 3) Wt[k] = DBuf(c, static_cast<std::size_t>(swt[k] * Bg));
+                const bool last = (k == d);
+                krp_step_batched(c, rl, nk, rr, width, t.core(b0, k - 1), t.stride, om.p, ldo, so, last ? ones.p : Wt[k + 1].p,
+                                 ldwt, last ? 0 : swt[k + 1], W[k].p, ldw[k], sw[k], k >= 3 ? Wt[k].p : nullptr, ldwt, swt[k],
+                                 Bg, last);
             }
         }
-        const i64 ncols = t.n[k] * t.r[k + 1];
-        double* dst = (k == d - 1) ? out->core(0, d - 1) : work.p;
-        const i64 sdst = (k == d - 1) ? out->stride : l * ncols;
-        {
-            PhaseScope ph(c, kPhaseGemm);
-            gemm_batched(c, true, l, cols, rows, 1.0, out->core(0, k - 1), rows, out->stride, v, rows, sv, 0.0, M.p, l,
-                         l * cols, B);
+
+        // ---- left-to-right Rand-Orth sweep ----
+        i64 max_work = 0, max_s = 0;
+        for (i64 k = 1; k < d; ++k) {
+            max_work = std::max(max_work, r[k] * t.n[k] * t.r[k + 1]);
+            max_s = std::max(max_s, r[k - 1] * t.n[k - 1] * r[k]);
         }
-        {
-            s_ready = false;
-            if (k < d - 1) {
-                PhaseScope ph(c, kPhaseOther);  // the fused kernel alone (bench.py roofline)
-                // next step's sketch S = V(Y_{k+1}) W_{k+2} fused with Y_{k+1} = M H(X_{k+1})
-                lrb::LrArgs a{};
-                a.l = static_cast<int>(l);
-                a.cols = static_cast<int>(cols);
-                a.n = static_cast<int>(t.n[k]);
-                a.rr = static_cast<int>(t.r[k + 1]);
-                a.l2 = static_cast<int>(r[k + 1]);
-                a.M = M.p;
-                a.sM = l * cols;
-                a.X = t.core(0, k);
-                a.sX = t.stride;
-                a.W = W[k + 2].p;
-                a.ldw = ldw[k + 2];
-                a.sW = sw[k + 2];
-                a.Y = dst;
-                a.sY = sdst;
-                a.S = S.p;
-                a.sS = l * t.n[k] * r[k + 1];
-                s_ready = lr_fused_batched(c, a, B);
-                if (s_ready) {
-                    c.charge_gemm(2ULL * static_cast<std::uint64_t>(l) * ncols * cols * B);
-                    c.charge_gemm(2ULL * static_cast<std::uint64_t>(l * t.n[k]) * r[k + 1] * t.r[k + 1] * B);
-                }
-            }
+        DBuf work(c, static_cast<std::size_t>(max_work * Bg));
+        DBuf S(c, static_cast<std::size_t>(max_s * Bg));
+        DBuf M(c, static_cast<std::size_t>(width * t.max_rank() * Bg));
+        const double* v = t.core(b0, 0);
+        i64 sv = t.stride;
+        bool s_ready = false;  // S of this step already formed by the previous fused step
+        for (i64 k = 1; k < d; ++k) {
+            const i64 rows = r[k - 1] * t.n[k - 1], cols = t.r[k], l = r[k];
             if (!s_ready) {
                 PhaseScope ph(c, kPhaseGemm);
-                gemm_batched(c, false, l, ncols, cols, 1.0, M.p, l, l * cols, t.core(0, k), cols, t.stride, 0.0, dst, l,
-                             sdst, B);
+                gemm_batched(c, false, rows, l, cols, 1.0, v, rows, sv, W[k + 1].p, ldw[k + 1], sw[k + 1], 0.0, S.p, rows,
+                             rows * l, Bg);
             }
+            {
+                PhaseScope ph(c, kPhaseQr);
+                c.charge_qr(4ULL * static_cast<std::uint64_t>(rows) * l * std::min(rows, l) * Bg);
+                if (rows * l <= 26000) {
+                    qr_small_batched(c, rows, l, S.p, rows, rows * l, out->core(b0, k - 1), rows, out->stride, nullptr, 1, 0, Bg);
+                } else {
+                    const Counts keep = c.counts;
+                    for (i64 b = 0; b < Bg; ++b)
+                        thin_qr(c, rows, l, S.p + b * rows * l, rows, out->core(b0 + b, k - 1), rows, nullptr, 1);
+                    c.counts = keep;
+                }
+            }
+            const i64 ncols = t.n[k] * t.r[k + 1];
+            double* dst = (k == d - 1) ? out->core(b0, d - 1) : work.p;
+            const i64 sdst = (k == d - 1) ? out->stride : l * ncols;
+            {
+                PhaseScope ph(c, kPhaseGemm);
+                gemm_batched(c, true, l, cols, rows, 1.0, out->core(b0, k - 1), rows, out->stride, v, rows, sv, 0.0, M.p, l,
+                             l * cols, Bg);
+            }
+            {
+                s_ready = false;
+                if (k < d - 1) {
+                    PhaseScope ph(c, kPhaseOther);  // the fused kernel alone (bench.py roofline)
+                    // next step's sketch S = V(Y_{k+1}) W_{k+2} fused with Y_{k+1} = M H(X_{k+1})
+                    lrb::LrArgs a{};
+                    a.l = static_cast<int>(l);
+                    a.cols = static_cast<int>(cols);
+                    a.n = static_cast<int>(t.n[k]);
+                    a.rr = static_cast<int>(t.r[k + 1]);
+                    a.l2 = static_cast<int>(r[k + 1]);
+                    a.M = M.p;
+                    a.sM = l * cols;
+                    a.X = t.core(b0, k);
+                    a.sX = t.stride;
+                    a.W = W[k + 2].p;
+                    a.ldw = ldw[k + 2];
+                    a.sW = sw[k + 2];
+                    a.Y = dst;
+                    a.sY = sdst;
+                    a.S = S.p;
+                    a.sS = l * t.n[k] * r[k + 1];
+                    s_ready = lr_fused_batched(c, a, Bg);
+                    if (s_ready) {
+                        c.charge_gemm(2ULL * static_cast<std::uint64_t>(l) * ncols * cols * Bg);
+                        c.charge_gemm(2ULL * static_cast<std::uint64_t>(l * t.n[k]) * r[k + 1] * t.r[k + 1] * Bg);
+                    }
+                }
+                if (!s_ready) {
+                    PhaseScope ph(c, kPhaseGemm);
+                    gemm_batched(c, false, l, ncols, cols, 1.0, M.p, l, l * cols, t.core(b0, k), cols, t.stride, 0.0, dst, l,
+                                 sdst, Bg);
+                }
+            }
+            v = dst;
+            sv = sdst;
         }
-        v = dst;
-        sv = sdst;
+    };
+    if (G == 1) {
+        run_group(0, B);
+        return out;
     }
+    c.fork_side(static_cast<int>(G));
+    const cudaStream_t main = c.stream;
+    double* const main_work = c.work;
+    const std::size_t main_bytes = c.work_bytes;
+    const bool timing = c.timing;
+    c.timing = false;  // per-phase events would time interleaved streams
+    std::vector<double*> works;
+    auto restore = [&] {
+        c.stream = main;
+        c.work = main_work;
+        c.work_bytes = main_bytes;
+        c.timing = timing;
+    };
+    try {
+        for (i64 g = 0; g < G; ++g) {
+            const i64 b0 = B * g / G, b1 = B * (g + 1) / G;
+            c.stream = c.side[g];
+            c.work = nullptr;
+            c.work_bytes = 0;
+            run_group(b0, b1 - b0);
+            if (c.work) works.push_back(c.work);
+        }
+    } catch (...) {
+        restore();
+        throw;
+    }
+    restore();
+    c.join_side(static_cast<int>(G));
+    for (double* w : works) TTR_CUDA(cudaFreeAsync(w, c.stream));
     return out;
 }
 
