@@ -384,6 +384,44 @@ ttr_status ttr_batch_destroy(ttr_batch* b);
 ttr_status ttr_round_fixed_krp_batched(ttr_ctx* ctx, const ttr_batch* b, const int64_t* target_ranks,
                                        int64_t count, uint64_t seed, ttr_batch** out);
 
+/* ---- TT-GMRES cookie harness (proj/core/include/ttround/solver.hpp) ----
+ * KroneckerSumOperator sum_i A_{i,1} (x) ... (x) A_{i,d} on the device
+ * (solver.hpp:12-21): factors term-major, then mode, each n_k x n_k
+ * column-major. build_cookie_problem (solver.hpp:32-40) gives the parametric
+ * diffusion operator and the rank-1 ones right-hand side; apply_operator
+ * (solver.hpp:42-44) returns the nterms result tensors (a TTSum's terms);
+ * tt_gmres (solver.hpp:80-82) runs TT-GMRES with the configured Sum+Round on
+ * the device. History buffers are caller-owned, capacity max_iterations (the
+ * true-residual one may be NULL when track_true_residual is 0). */
+typedef struct ttr_kron_op ttr_kron_op;
+enum { TTR_GMRES_DETERMINISTIC = 0, TTR_GMRES_RAND_ORTH_TT = 1, TTR_GMRES_ADAPTIVE_KRP_SUM = 2 };
+typedef struct {
+    double rel_tolerance;      /* > 0 */
+    int64_t max_iterations;    /* >= 1 */
+    int strategy;              /* TTR_GMRES_* (RoundingStrategy) */
+    double rounding_tolerance; /* 0: 0.1 * rel_tolerance */
+    uint64_t seed;
+    int track_true_residual;
+    int mean_field_preconditioner;
+    int rng_mode;              /* sketch generator of the randomized strategies (TTR_RNG_*) */
+} ttr_gmres_cfg;
+typedef struct {
+    int64_t iterations;
+    int converged;
+    double rounding_seconds;
+    double* residual_history;      /* [max_iterations] Arnoldi estimates */
+    double* true_residual_history; /* [max_iterations] or NULL */
+    int64_t* max_rank_history;     /* [max_iterations] */
+} ttr_gmres_result;
+ttr_status ttr_kron_op_create(ttr_ctx* ctx, int64_t nterms, int64_t d, const int64_t* n, const double* factors,
+                              ttr_kron_op** out);
+ttr_status ttr_kron_op_destroy(ttr_kron_op* op);
+ttr_status ttr_cookie_problem(ttr_ctx* ctx, int64_t num_param_modes, int64_t grid_size, int64_t num_param_samples,
+                              double rho_min, double rho_max, ttr_kron_op** op, ttr_tt** rhs);
+ttr_status ttr_apply_operator(ttr_ctx* ctx, const ttr_kron_op* op, const ttr_tt* x, ttr_tt** out_terms);
+ttr_status ttr_tt_gmres(ttr_ctx* ctx, const ttr_kron_op* op, const ttr_tt* rhs, const ttr_gmres_cfg* cfg,
+                        ttr_gmres_result* result, ttr_tt** solution);
+
 ttr_status ttr_counters(ttr_ctx* ctx, ttr_counts* out);
 ttr_status ttr_counters_reset(ttr_ctx* ctx);
 

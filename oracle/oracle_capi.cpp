@@ -209,6 +209,71 @@ int ttro_round_sum_adaptive_krp(const ttro_tt* const* terms, int count, double e
     });
 }
 
+// TT-GMRES on the cookie problem (solver.cpp:241-363): config as plain values,
+// histories into caller buffers of capacity max_iterations.
+int ttro_gmres_cookie(std::int64_t p, std::int64_t grid, std::int64_t samples, double rho_min, double rho_max,
+                      double rel_tol, std::int64_t max_it, int strategy, double rounding_tol, std::uint64_t seed,
+                      int track_true, int precond, int rng_mode, std::int64_t* iterations, int* converged,
+                      double* residual_hist, double* true_hist, std::int64_t* rank_hist, ttro_tt** solution) {
+    return guard([&] {
+        CookieProblem prob = build_cookie_problem(p, grid, samples, rho_min, rho_max);
+        GmresConfig cfg;
+        cfg.rel_tolerance = rel_tol;
+        cfg.max_iterations = max_it;
+        cfg.strategy = static_cast<GmresStrategy>(strategy);
+        cfg.rounding_tolerance = rounding_tol;
+        cfg.seed = seed;
+        cfg.track_true_residual = track_true != 0;
+        cfg.mean_field_preconditioner = precond != 0;
+        cfg.rng = static_cast<RngMode>(rng_mode);
+        GmresResult r = tt_gmres(prob.op, prob.rhs, cfg);
+        *iterations = r.iterations;
+        *converged = r.converged ? 1 : 0;
+        for (std::size_t i = 0; i < r.residual_history.size(); ++i) residual_hist[i] = r.residual_history[i];
+        for (std::size_t i = 0; i < r.true_residual_history.size(); ++i) true_hist[i] = r.true_residual_history[i];
+        for (std::size_t i = 0; i < r.max_rank_history.size(); ++i) rank_hist[i] = r.max_rank_history[i];
+        *solution = wrap(std::move(r.solution));
+    });
+}
+
+// The cookie operator's factors A_{i,k} (column-major, term-major then mode)
+// and the right-hand side (build_cookie_problem, solver.cpp:81-135).
+int ttro_cookie_problem(std::int64_t p, std::int64_t grid, std::int64_t samples, double rho_min, double rho_max,
+                        double* factors, ttro_tt** rhs) {
+    return guard([&] {
+        CookieProblem prob = build_cookie_problem(p, grid, samples, rho_min, rho_max);
+        std::int64_t off = 0;
+        for (const auto& term : prob.op.terms)
+            for (const auto& a : term) {
+                std::memcpy(factors + off, a.data(), sizeof(double) * a.a.size());
+                off += static_cast<std::int64_t>(a.a.size());
+            }
+        *rhs = wrap(std::move(prob.rhs));
+    });
+}
+
+// apply_operator of an explicit operator (factors as above, nterms x d) to t:
+// the nterms result terms.
+int ttro_apply_operator(std::int64_t nterms, const double* factors, const ttro_tt* t, ttro_tt** out) {
+    return guard([&] {
+        const auto modes = t->tt.mode_sizes();
+        std::vector<std::vector<Matrix>> terms;
+        std::int64_t off = 0;
+        for (std::int64_t i = 0; i < nterms; ++i) {
+            std::vector<Matrix> term;
+            for (Index n : modes) {
+                Matrix a(n, n);
+                std::memcpy(a.data(), factors + off, sizeof(double) * n * n);
+                off += n * n;
+                term.push_back(std::move(a));
+            }
+            terms.push_back(std::move(term));
+        }
+        auto res = apply_operator(KronOp::of(std::move(terms)), t->tt);
+        for (std::size_t i = 0; i < res.size(); ++i) out[i] = wrap(std::move(res[i]));
+    });
+}
+
 int ttro_compression_pass(const ttro_tt* t, double tau, ttro_tt** out) {
     return guard([&] { *out = wrap(compression_pass(t->tt, tau)); });
 }

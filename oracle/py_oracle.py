@@ -408,3 +408,57 @@ def flops_get() -> dict:
     arr = (C.c_uint64 * 5)()
     lib().ttro_flops_get(arr)
     return dict(gemm=arr[0], qr=arr[1], svd=arr[2], sketch=arr[3], rng=arr[4], total=arr[0] + arr[1] + arr[2])
+
+
+# -- TT-GMRES cookie harness (solver.cpp; ttr_oracle_solver.cpp) ------------------
+
+DETERMINISTIC, RAND_ORTH_TT, ADAPTIVE_KRP_SUM = 0, 1, 2
+
+
+def cookie_problem(p: int, grid: int, samples: int, rho_min: float, rho_max: float):
+    """build_cookie_problem (solver.cpp:81-135): (factors[term][mode] as arrays, rhs TT)."""
+    modes = [grid * grid] + [samples] * p
+    nterms = p + 1
+    tot = nterms * sum(m * m for m in modes)
+    buf = np.empty(tot, dtype=np.float64)
+    h = C.c_void_p()
+    _check(lib().ttro_cookie_problem(C.c_int64(p), C.c_int64(grid), C.c_int64(samples), C.c_double(rho_min),
+                                     C.c_double(rho_max), _dptr(buf), C.byref(h)))
+    terms, off = [], 0
+    for _ in range(nterms):
+        term = []
+        for m in modes:
+            term.append(buf[off:off + m * m].reshape(m, m).T.copy())
+            off += m * m
+        terms.append(term)
+    return terms, TT(h)
+
+
+def apply_operator(terms, t: TT) -> List[TT]:
+    """apply_operator (solver.cpp:137-151) of explicit factors terms[i][k]."""
+    flat = np.concatenate([np.asarray(a, dtype=np.float64).T.reshape(-1) for term in terms for a in term])
+    outs = (C.c_void_p * len(terms))()
+    _check(lib().ttro_apply_operator(C.c_int64(len(terms)), _dptr(flat), t._h, outs))
+    return [TT(C.c_void_p(outs[i])) for i in range(len(terms))]
+
+
+def tt_gmres_cookie(p, grid, samples, rho_min, rho_max, rel_tolerance=1e-8, max_iterations=200,
+                    strategy=DETERMINISTIC, rounding_tolerance=0.0, seed=0, track_true_residual=True,
+                    mean_field_preconditioner=True, rng=XOSHIRO):
+    """tt_gmres on build_cookie_problem(p, grid, samples, rho_min, rho_max) -> dict."""
+    it = C.c_int64()
+    conv = C.c_int()
+    rh = np.zeros(max_iterations)
+    th = np.zeros(max_iterations)
+    kh = np.zeros(max_iterations, dtype=np.int64)
+    h = C.c_void_p()
+    _check(lib().ttro_gmres_cookie(C.c_int64(p), C.c_int64(grid), C.c_int64(samples), C.c_double(rho_min),
+                                   C.c_double(rho_max), C.c_double(rel_tolerance), C.c_int64(max_iterations),
+                                   C.c_int(strategy), C.c_double(rounding_tolerance), C.c_uint64(seed),
+                                   C.c_int(1 if track_true_residual else 0),
+                                   C.c_int(1 if mean_field_preconditioner else 0), C.c_int(rng), C.byref(it),
+                                   C.byref(conv), _dptr(rh), _dptr(th), kh.ctypes.data_as(C.c_void_p), C.byref(h)))
+    n = it.value
+    return {"iterations": n, "converged": bool(conv.value), "residual_history": rh[:n].tolist(),
+            "true_residual_history": th[:n].tolist() if track_true_residual else [],
+            "max_rank_history": kh[:n].tolist(), "solution": TT(h)}

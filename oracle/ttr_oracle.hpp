@@ -25,6 +25,7 @@
 #include <optional>
 #include <stdexcept>
 #include <string>
+#include <memory>
 #include <vector>
 
 namespace ttr_oracle {
@@ -273,5 +274,41 @@ Synthetic synthetic_perturbed_tt(Index d, Index n, Index r, double eps_pert, std
 TT two_part_tt(Index d, Index n, Index rx, Index rz, double eps, std::uint64_t seed);
 //! Config 4: sum_{i<terms} 2^-i * (rank-r TT with slices exp(-|t - c_ab|/ell)).
 TT kernel_sum_tt(Index d, Index n, Index r, Index terms, double ell, std::uint64_t seed);
+
+// ---- TT-GMRES cookie harness: proj/core/include/ttround/solver.hpp (ttr_oracle_solver.cpp) --
+struct KronOp {  // solver.hpp:12-21 (KroneckerSumOperator)
+    std::vector<std::vector<Matrix>> terms;  // terms[i][k-1] = A_{i,k}
+    static KronOp of(std::vector<std::vector<Matrix>> terms);
+    Index num_terms() const { return static_cast<Index>(terms.size()); }
+    Index order() const { return static_cast<Index>(terms.front().size()); }
+    std::vector<Index> mode_sizes() const;
+};
+struct CookieProblem {
+    KronOp op;
+    TT rhs;
+};
+CookieProblem build_cookie_problem(Index num_param_modes, Index grid_size, Index num_param_samples, double rho_min,
+                                   double rho_max);
+std::vector<TT> apply_operator(const KronOp& op, const TT& x);
+enum class GmresStrategy { Deterministic = 0, RandOrthTT = 1, AdaptiveKRPSum = 2 };
+struct GmresConfig {  // solver.hpp:48-64 (+ the sketch generator of the randomized strategies)
+    double rel_tolerance = 1e-8;
+    Index max_iterations = 200;
+    GmresStrategy strategy = GmresStrategy::Deterministic;
+    double rounding_tolerance = 0.0;
+    std::uint64_t seed = 0;
+    bool track_true_residual = true;
+    bool mean_field_preconditioner = true;
+    RngMode rng = RngMode::Xoshiro;
+};
+struct GmresResult {  // solver.hpp:66-78
+    TT solution;
+    std::vector<double> residual_history, true_residual_history, rounding_seconds_history;
+    std::vector<Index> max_rank_history;
+    double rounding_seconds = 0.0;
+    Index iterations = 0;
+    bool converged = false;
+};
+GmresResult tt_gmres(const KronOp& op, const TT& rhs, const GmresConfig& cfg);
 
 }  // namespace ttr_oracle

@@ -711,3 +711,87 @@ def gemm(a: np.ndarray, b: np.ndarray, trans_a: bool = False, ctx: Optional[Cont
     _check(lib().ttr_gemm(ctx._h, C.c_int(1 if trans_a else 0), C.c_int64(m), C.c_int64(n), C.c_int64(k),
                           _dptr(fa), _dptr(fb), _dptr(out)))
     return out.reshape(n, m).T.copy()
+
+
+# ---- TT-GMRES cookie harness (solver.hpp; csrc/tt_gmres.cu) -------------------------
+
+GMRES_DETERMINISTIC, GMRES_RAND_ORTH_TT, GMRES_ADAPTIVE_KRP_SUM = 0, 1, 2
+
+
+class _GmresCfg(C.Structure):
+    _fields_ = [("rel_tolerance", C.c_double), ("max_iterations", C.c_int64), ("strategy", C.c_int),
+                ("rounding_tolerance", C.c_double), ("seed", C.c_uint64), ("track_true_residual", C.c_int),
+                ("mean_field_preconditioner", C.c_int), ("rng_mode", C.c_int)]
+
+
+class _GmresResult(C.Structure):
+    _fields_ = [("iterations", C.c_int64), ("converged", C.c_int), ("rounding_seconds", C.c_double),
+                ("residual_history", C.POINTER(C.c_double)), ("true_residual_history", C.POINTER(C.c_double)),
+                ("max_rank_history", C.POINTER(C.c_int64))]
+
+
+class KronOp:
+    """KroneckerSumOperator on the device (solver.hpp:12-21): terms[i][k] = A_{i,k}."""
+
+    def __init__(self, handle: C.c_void_p, ctx: Context, nterms: int, modes: Sequence[int]):
+        self._h = handle
+        self.ctx = ctx
+        self.nterms = nterms
+        self.modes = list(modes)
+
+    @staticmethod
+    def of(terms, ctx: Optional[Context] = None) -> "KronOp":
+        ctx = ctx or default_context()
+        modes = [np.asarray(a).shape[0] for a in terms[0]]
+        flat = np.concatenate([np.asarray(a, dtype=np.float64).T.reshape(-1) for term in terms for a in term])
+        h = C.c_void_p()
+        _check(lib().ttr_kron_op_create(ctx._h, C.c_int64(len(terms)), C.c_int64(len(modes)), _i64(modes),
+                                        _dptr(flat), C.byref(h)))
+        return KronOp(h, ctx, len(terms), modes)
+
+    def close(self):
+        if getattr(self, "_h", None) and self._h.value:
+            lib().ttr_kron_op_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        self.close()
+
+
+def cookie_problem(num_param_modes: int, grid_size: int, num_param_samples: int, rho_min: float, rho_max: float,
+                   ctx: Optional[Context] = None):
+    """build_cookie_problem (solver.hpp:32-40): (KronOp, rhs TTTensor)."""
+    ctx = ctx or default_context()
+    ho, ht = C.c_void_p(), C.c_void_p()
+    _check(lib().ttr_cookie_problem(ctx._h, C.c_int64(num_param_modes), C.c_int64(grid_size),
+                                    C.c_int64(num_param_samples), C.c_double(rho_min), C.c_double(rho_max),
+                                    C.byref(ho), C.byref(ht)))
+    modes = [grid_size * grid_size] + [num_param_samples] * num_param_modes
+    return KronOp(ho, ctx, num_param_modes + 1, modes), TTTensor(ht, ctx)
+
+
+def apply_operator(op: KronOp, x: TTTensor) -> List[TTTensor]:
+    """apply_operator (solver.hpp:42-44): the terms of the TTSum A x."""
+    outs = (C.c_void_p * op.nterms)()
+    _check(lib().ttr_apply_operator(op.ctx._h, op._h, x._h, outs))
+    return [TTTensor(C.c_void_p(outs[i]), op.ctx) for i in range(op.nterms)]
+
+
+def tt_gmres(op: KronOp, rhs: TTTensor, rel_tolerance: float = 1e-8, max_iterations: int = 200,
+             strategy: int = GMRES_DETERMINISTIC, rounding_tolerance: float = 0.0, seed: int = 0,
+             track_true_residual: bool = True, mean_field_preconditioner: bool = True, rng: int = RNG_XOSHIRO):
+    """tt_gmres (solver.hpp:80-82) on the device -> dict like GMRESResult."""
+    cfg = _GmresCfg(rel_tolerance, max_iterations, strategy, rounding_tolerance, seed, 1 if track_true_residual else 0,
+                    1 if mean_field_preconditioner else 0, rng)
+    rh = np.zeros(max_iterations)
+    th = np.zeros(max_iterations)
+    kh = np.zeros(max_iterations, dtype=np.int64)
+    res = _GmresResult(0, 0, 0.0, rh.ctypes.data_as(C.POINTER(C.c_double)), th.ctypes.data_as(C.POINTER(C.c_double)),
+                       kh.ctypes.data_as(C.POINTER(C.c_int64)))
+    h = C.c_void_p()
+    _check(lib().ttr_tt_gmres(op.ctx._h, op._h, rhs._h, C.byref(cfg), C.byref(res), C.byref(h)))
+    n = res.iterations
+    return {"iterations": n, "converged": bool(res.converged), "residual_history": rh[:n].tolist(),
+            "true_residual_history": th[:n].tolist() if track_true_residual else [],
+            "max_rank_history": kh[:n].tolist(), "rounding_seconds": res.rounding_seconds,
+            "solution": TTTensor(h, op.ctx)}

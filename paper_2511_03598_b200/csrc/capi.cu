@@ -6,6 +6,7 @@
 
 #include "common.cuh"
 #include "tt_round.h"
+#include "tt_gmres.h"
 #include "capi_util.h"
 
 using namespace ttr;
@@ -726,3 +727,66 @@ ttr_status ttr_counters_reset(ttr_ctx* ctx) {
 }
 
 }  // extern "C"
+
+// ---- TT-GMRES cookie harness (tt_gmres.cu) ----
+ttr_status ttr_kron_op_create(ttr_ctx* ctx, int64_t nterms, int64_t d, const int64_t* n, const double* factors,
+                              ttr_kron_op** out) {
+    return guard_ctx(ctx, [&] {
+        need(ctx && n && factors && out, "null argument");
+        need(d >= 1 && nterms >= 1, "operator needs at least one term and one factor");
+        auto* o = new ttr_kron_op;
+        try {
+            o->op = std::make_unique<KronOpDev>(ctx->c, nterms, vec(n, d), factors);
+        } catch (...) {
+            delete o;
+            throw;
+        }
+        *out = o;
+    });
+}
+
+ttr_status ttr_kron_op_destroy(ttr_kron_op* op) {
+    delete op;
+    return TTR_OK;
+}
+
+ttr_status ttr_cookie_problem(ttr_ctx* ctx, int64_t num_param_modes, int64_t grid_size, int64_t num_param_samples,
+                              double rho_min, double rho_max, ttr_kron_op** op, ttr_tt** rhs) {
+    return guard_ctx(ctx, [&] {
+        need(ctx && op && rhs, "null argument");
+        std::unique_ptr<TTDev> b;
+        auto k = cookie_problem(ctx->c, num_param_modes, grid_size, num_param_samples, rho_min, rho_max, &b);
+        auto* o = new ttr_kron_op;
+        o->op = std::move(k);
+        *op = o;
+        *rhs = wrap(std::move(b));
+    });
+}
+
+ttr_status ttr_apply_operator(ttr_ctx* ctx, const ttr_kron_op* op, const ttr_tt* x, ttr_tt** out_terms) {
+    return guard_ctx(ctx, [&] {
+        need(ctx && op && op->op && x && x->t && out_terms, "null argument");
+        auto terms = apply_operator(ctx->c, *op->op, *x->t);
+        for (std::size_t i = 0; i < terms.size(); ++i) out_terms[i] = wrap(std::move(terms[i]));
+    });
+}
+
+ttr_status ttr_tt_gmres(ttr_ctx* ctx, const ttr_kron_op* op, const ttr_tt* rhs, const ttr_gmres_cfg* cfg,
+                        ttr_gmres_result* result, ttr_tt** solution) {
+    return guard_ctx(ctx, [&] {
+        need(ctx && op && op->op && rhs && rhs->t && cfg && result && solution, "null argument");
+        need(result->residual_history && result->max_rank_history, "history buffers are required");
+        need(cfg->strategy >= TTR_GMRES_DETERMINISTIC && cfg->strategy <= TTR_GMRES_ADAPTIVE_KRP_SUM,
+             "unknown rounding strategy");
+        auto r = tt_gmres(ctx->c, *op->op, *rhs->t, *cfg);
+        result->iterations = r.iterations;
+        result->converged = r.converged ? 1 : 0;
+        result->rounding_seconds = r.rounding_seconds;
+        for (std::size_t i = 0; i < r.residual_history.size(); ++i) result->residual_history[i] = r.residual_history[i];
+        for (std::size_t i = 0; i < r.max_rank_history.size(); ++i) result->max_rank_history[i] = r.max_rank_history[i];
+        if (result->true_residual_history)
+            for (std::size_t i = 0; i < r.true_residual_history.size(); ++i)
+                result->true_residual_history[i] = r.true_residual_history[i];
+        *solution = wrap(std::move(r.solution));
+    });
+}

@@ -1040,3 +1040,91 @@ def test_dot_random_gaussian_and_constructor_checks(P, O):
     assert e.value.code == "InvalidArgument"
     ok = P.TTTensor.from_cores([np.ones((1, 2, 2)), np.ones((2, 2, 1))])
     assert ok.ranks() == [1, 2, 1]
+
+
+# ---- TT-GMRES cookie harness (solver.cpp; csrc/tt_gmres.cu) ----------------------------------
+
+def _dense_kron_apply(terms, ot):
+    n, _, _ = ot.shape()
+    x = ot.dense().reshape(tuple(n), order="F")
+    out = np.zeros_like(x)
+    for term in terms:
+        y = x
+        for k, a in enumerate(term):
+            y = np.moveaxis(np.tensordot(a, y, axes=([1], [k])), 0, k)
+        out += y
+    return out
+
+
+def test_cookie_problem_and_apply_match_oracle(P, O):
+    """build_cookie_problem + apply_operator on the device against the oracle's
+    (solver.cpp:81-151): same right-hand side, same operator terms applied to a
+    random TT (strided-batch DMMA GEMMs vs the loop), identities copied."""
+    op, rhs = P.cookie_problem(2, 8, 3, 1.0, 5.0)
+    terms, orhs = O.cookie_problem(2, 8, 3, 1.0, 5.0)
+    assert np.array_equal(rhs.flat(), orhs.flat())
+    x = O.random_gaussian_tt([64, 3, 3], [1, 4, 2, 1], 8)
+    dev = P.apply_operator(op, to_device(x))
+    ref = O.apply_operator(terms, x)
+    assert len(dev) == len(ref) == 3
+    for d, r in zip(dev, ref):
+        assert d.ranks() == r.ranks
+        assert np.linalg.norm(d.flat() - r.flat()) <= 1e-13 * np.linalg.norm(r.flat())
+    # an explicit operator (KronOp.of) and the identity-only case (test_solver.cpp:62-69)
+    eye = P.KronOp.of([[np.eye(4), np.eye(5)]])
+    y = O.random_gaussian_tt([4, 5], [1, 3, 1], 5)
+    assert np.array_equal(P.apply_operator(eye, to_device(y))[0].flat(), y.flat())
+
+
+@pytest.mark.parametrize("strategy", [0, 1, 2])
+def test_gmres_device_matches_oracle(P, O, strategy):
+    """tt_gmres on the device vs the oracle (solver.cpp:241-363), the small cookie
+    problem of test_solver.cpp:109-125 with the reference's xoshiro sketches:
+    same iteration count and rank history, Arnoldi estimates and the solution
+    equal to rounding, dense residual <= 1e-4."""
+    op, rhs = P.cookie_problem(2, 8, 4, 1.0, 10.0)
+    dev = P.tt_gmres(op, rhs, rel_tolerance=1e-5, max_iterations=120, strategy=strategy, seed=4, rng=P.RNG_XOSHIRO)
+    ref = O.tt_gmres_cookie(2, 8, 4, 1.0, 10.0, rel_tolerance=1e-5, max_iterations=120, strategy=strategy, seed=4)
+    assert dev["converged"] and ref["converged"]
+    assert dev["iterations"] == ref["iterations"]
+    assert dev["max_rank_history"] == ref["max_rank_history"]
+    np.testing.assert_allclose(dev["residual_history"], ref["residual_history"], rtol=1e-6)
+    np.testing.assert_allclose(dev["true_residual_history"], ref["true_residual_history"], rtol=1e-5)
+    assert rel_err_vs_ref(ref["solution"], dev["solution"]) <= 1e-8
+    terms, orhs = O.cookie_problem(2, 8, 4, 1.0, 10.0)
+    n, _, _ = orhs.shape()
+    b = orhs.dense().reshape(tuple(n), order="F")
+    x = to_oracle(dev["solution"])
+    assert np.linalg.norm(b - _dense_kron_apply(terms, x)) / np.linalg.norm(b) <= 1e-4
+
+
+def test_gmres_identity_operator_one_iteration(P, O):
+    """test_solver.cpp:96-107."""
+    op = P.KronOp.of([[np.eye(6), np.eye(4)]])
+    b = O.random_gaussian_tt([6, 4], [1, 2, 1], 12)
+    r = P.tt_gmres(op, to_device(b), rel_tolerance=1e-10)
+    assert r["converged"] and r["iterations"] == 1
+    assert rel_err_vs_ref(b, r["solution"]) <= 1e-9
+
+
+def test_gmres_criterion8_on_device(P, O):
+    """The reference's acceptance criterion 8 (acceptance.cpp:335-383, printed in
+    test_output.txt:34) run through the device harness: the deterministic and the
+    three seeded AdaptiveKRPSum runs converge in 17 iterations to the dense
+    residual 4.42e-07; rank histories stay inside the 2x band."""
+    op, rhs = P.cookie_problem(3, 16, 8, 1.0, 10.0)
+    terms, orhs = O.cookie_problem(3, 16, 8, 1.0, 10.0)
+    n, _, _ = orhs.shape()
+    bd = orhs.dense().reshape(tuple(n), order="F")
+    det = P.tt_gmres(op, rhs, rel_tolerance=1e-6, max_iterations=250, strategy=P.GMRES_DETERMINISTIC,
+                     track_true_residual=False)
+    assert det["converged"] and det["iterations"] == 17
+    for seed in (1, 2, 3):
+        r = P.tt_gmres(op, rhs, rel_tolerance=1e-6, max_iterations=250, strategy=P.GMRES_ADAPTIVE_KRP_SUM, seed=seed,
+                       track_true_residual=False, rng=P.RNG_XOSHIRO)
+        assert r["converged"] and r["iterations"] == 17
+        resid = np.linalg.norm(bd - _dense_kron_apply(terms, to_oracle(r["solution"]))) / np.linalg.norm(bd)
+        assert f"{resid:.2g}" == "4.4e-07"
+        c = min(len(r["max_rank_history"]), len(det["max_rank_history"]))
+        ratio = max([1.0] + [max(x / y, y / x) for x, y in zip(r["max_rank_history"][:c], det["max_rank_history"][:c])])
+        assert ratio <= 2.0

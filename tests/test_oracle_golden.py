@@ -252,3 +252,93 @@ def test_det_properties(oracle):
     t = O.random_gaussian_tt([5, 5, 5, 5], [1, 6, 6, 6, 1], 47)
     y = O.round_deterministic(t, ranks=[3, 4, 2])
     assert y.ranks == [1, 3, 4, 2, 1]
+
+
+# ---- TT-GMRES cookie harness (solver.cpp; oracle/ttr_oracle_solver.cpp) -----------
+
+def _dense_kron_apply(terms, t):
+    """tests/support/oracles.hpp dense_kron_sum_apply: sum_i (A_i1 x ... x A_id) x."""
+    n, _, _ = t.shape()
+    x = t.dense().reshape(tuple(n), order="F")
+    out = np.zeros_like(x)
+    for term in terms:
+        y = x
+        for k, a in enumerate(term):
+            y = np.moveaxis(np.tensordot(a, y, axes=([1], [k])), 0, k)
+        out += y
+    return out
+
+
+def test_criterion8_gmres_cookie_golden(oracle):
+    """acceptance.cpp:335-383 -> 'seed 1 resid 4.42e-07, iters 17, rank ratio 1.73; seed 2
+    resid 4.42e-07, iters 17, rank ratio 1.79; seed 3 ...' (test_output.txt:34). The
+    iteration counts and the dense residual reproduce to the printed digits; the rank
+    ratios (a max over iterations of tolerance-truncated ranks, sensitive to the last
+    bit of every SVD) must stay inside the criterion's 2x band."""
+    O = oracle
+    terms, rhs = O.cookie_problem(3, 16, 8, 1.0, 10.0)
+    n, _, _ = rhs.shape()
+    b = rhs.dense().reshape(tuple(n), order="F")
+    det = O.tt_gmres_cookie(3, 16, 8, 1.0, 10.0, rel_tolerance=1e-6, max_iterations=250,
+                            strategy=O.DETERMINISTIC, track_true_residual=False)
+    assert det["converged"] and det["iterations"] == 17
+    for seed in (1, 2, 3):
+        r = O.tt_gmres_cookie(3, 16, 8, 1.0, 10.0, rel_tolerance=1e-6, max_iterations=250,
+                              strategy=O.ADAPTIVE_KRP_SUM, seed=seed, track_true_residual=False)
+        assert r["converged"] and r["iterations"] == 17
+        resid = np.linalg.norm(b - _dense_kron_apply(terms, r["solution"])) / np.linalg.norm(b)
+        assert f"{resid:.3g}" == "4.42e-07"
+        c = min(len(r["max_rank_history"]), len(det["max_rank_history"]))
+        ratio = max([1.0] + [max(x / y, y / x) for x, y in zip(r["max_rank_history"][:c], det["max_rank_history"][:c])])
+        assert 1.5 <= ratio <= 2.0
+
+
+def test_cookie_assembly_and_operator(oracle):
+    """test_solver.cpp:12-99: the degenerate Poisson system, the parameter factors,
+    the symmetric disc operators, and operator application against the dense oracle."""
+    O = oracle
+    terms, rhs = O.cookie_problem(0, 8, 1, 1.0, 10.0)
+    assert len(terms) == 1 and terms[0][0].shape == (64, 64)
+    a = terms[0][0]
+    assert np.linalg.norm(a - a.T) <= 1e-12 * np.linalg.norm(a)
+    h2 = 81.0
+    assert a[3 * 8 + 3, 3 * 8 + 3] == pytest.approx(4 * h2) and a[3 * 8 + 3, 3 * 8 + 4] == pytest.approx(-h2)
+    assert O.norm_exact(rhs) == pytest.approx(8.0)
+    for n in (8, 16):
+        terms, _ = O.cookie_problem(5, 8, n, 1.0, 10.0)
+        assert len(terms) == 6 and [t.shape[0] for t in terms[0]] == [64] + [n] * 5
+        dg = terms[2][2]
+        assert dg[0, 0] == pytest.approx(1.0) and dg[n - 1, n - 1] == pytest.approx(10.0)
+        assert dg[1, 1] - dg[0, 0] == pytest.approx(9.0 / (n - 1))
+        assert np.array_equal(terms[2][1], np.eye(n))
+        for i in range(1, 6):
+            ad = terms[i][0]
+            assert np.linalg.norm(ad) > 0 and np.linalg.norm(ad - ad.T) <= 1e-12 * np.linalg.norm(ad)
+    with pytest.raises(O.OracleError) as e:
+        O.cookie_problem(2, 4, 4, 1.0, 10.0)
+    assert e.value.errc == "InvalidGrid"
+    terms, _ = O.cookie_problem(2, 8, 3, 1.0, 5.0)
+    x = O.random_gaussian_tt([64, 3, 3], [1, 2, 2, 1], 8)
+    got = sum(t.dense() for t in O.apply_operator(terms, x))
+    n = [64, 3, 3]
+    expect = _dense_kron_apply(terms, x).reshape(-1, order="F")
+    assert np.linalg.norm(got - expect) <= 1e-12 * np.linalg.norm(expect)
+
+
+def test_gmres_small_cookie_all_strategies(oracle):
+    """test_solver.cpp:109-125 and :160-176: every strategy converges to a dense
+    residual <= 1e-4; the randomized run is seeded-deterministic; the Arnoldi
+    estimate is monotone."""
+    O = oracle
+    terms, rhs = O.cookie_problem(2, 8, 4, 1.0, 10.0)
+    n, _, _ = rhs.shape()
+    b = rhs.dense().reshape(tuple(n), order="F")
+    for strategy in (O.DETERMINISTIC, O.RAND_ORTH_TT, O.ADAPTIVE_KRP_SUM):
+        r = O.tt_gmres_cookie(2, 8, 4, 1.0, 10.0, rel_tolerance=1e-5, max_iterations=120, strategy=strategy, seed=4)
+        assert r["converged"]
+        assert np.linalg.norm(b - _dense_kron_apply(terms, r["solution"])) / np.linalg.norm(b) <= 1e-4
+        h = r["residual_history"]
+        assert all(h[i] <= h[i - 1] + 1e-15 for i in range(1, len(h)))
+    a = O.tt_gmres_cookie(2, 8, 4, 1.0, 10.0, rel_tolerance=1e-4, max_iterations=80, strategy=O.ADAPTIVE_KRP_SUM, seed=99)
+    b2 = O.tt_gmres_cookie(2, 8, 4, 1.0, 10.0, rel_tolerance=1e-4, max_iterations=80, strategy=O.ADAPTIVE_KRP_SUM, seed=99)
+    assert a["residual_history"] == b2["residual_history"] and a["max_rank_history"] == b2["max_rank_history"]
