@@ -412,6 +412,7 @@ typedef struct {
     double* residual_history;      /* [max_iterations] Arnoldi estimates */
     double* true_residual_history; /* [max_iterations] or NULL */
     int64_t* max_rank_history;     /* [max_iterations] */
+    double* rounding_seconds_history; /* [max_iterations] cumulative Sum+Round seconds, or NULL */
 } ttr_gmres_result;
 ttr_status ttr_kron_op_create(ttr_ctx* ctx, int64_t nterms, int64_t d, const int64_t* n, const double* factors,
                               ttr_kron_op** out);

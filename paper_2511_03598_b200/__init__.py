@@ -727,7 +727,7 @@ class _GmresCfg(C.Structure):
 class _GmresResult(C.Structure):
     _fields_ = [("iterations", C.c_int64), ("converged", C.c_int), ("rounding_seconds", C.c_double),
                 ("residual_history", C.POINTER(C.c_double)), ("true_residual_history", C.POINTER(C.c_double)),
-                ("max_rank_history", C.POINTER(C.c_int64))]
+                ("max_rank_history", C.POINTER(C.c_int64)), ("rounding_seconds_history", C.POINTER(C.c_double))]
 
 
 class KronOp:
@@ -786,12 +786,14 @@ def tt_gmres(op: KronOp, rhs: TTTensor, rel_tolerance: float = 1e-8, max_iterati
     rh = np.zeros(max_iterations)
     th = np.zeros(max_iterations)
     kh = np.zeros(max_iterations, dtype=np.int64)
+    sh = np.zeros(max_iterations)
     res = _GmresResult(0, 0, 0.0, rh.ctypes.data_as(C.POINTER(C.c_double)), th.ctypes.data_as(C.POINTER(C.c_double)),
-                       kh.ctypes.data_as(C.POINTER(C.c_int64)))
+                       kh.ctypes.data_as(C.POINTER(C.c_int64)), sh.ctypes.data_as(C.POINTER(C.c_double)))
     h = C.c_void_p()
     _check(lib().ttr_tt_gmres(op.ctx._h, op._h, rhs._h, C.byref(cfg), C.byref(res), C.byref(h)))
     n = res.iterations
     return {"iterations": n, "converged": bool(res.converged), "residual_history": rh[:n].tolist(),
             "true_residual_history": th[:n].tolist() if track_true_residual else [],
             "max_rank_history": kh[:n].tolist(), "rounding_seconds": res.rounding_seconds,
+            "rounding_seconds_history": sh[:n].tolist(),
             "solution": TTTensor(h, op.ctx)}

@@ -153,6 +153,39 @@ def cmd_bench_synthetic(args) -> int:  # ttround_main.cpp:178-210
     return 0
 
 
+COOKIE_STRATEGIES = {"det": 0, "rand-orth": 1, "krp-adapt-sum": 2}
+
+
+def cmd_cookie(args) -> int:  # ttround_main.cpp:246-296
+    import paper_2511_03598_b200 as P
+    ctx = P.Context(args.device)
+    op, rhs = P.cookie_problem(args.params, args.grid, args.nsamples, args.rho_min, args.rho_max, ctx)
+    track = not args.no_true_residual
+    res = P.tt_gmres(op, rhs, rel_tolerance=args.tol, max_iterations=args.max_iters,
+                     strategy=COOKIE_STRATEGIES[args.strategy], rounding_tolerance=args.round_tol, seed=args.seed,
+                     track_true_residual=track, rng=P.RNG_XOSHIRO if args.rng == "xoshiro" else P.RNG_PHILOX)
+    if args.csv:
+        try:
+            with open(args.csv, "w") as f:
+                f.write("iteration,rel_residual,max_tt_rank,cum_rounding_seconds\n")
+                for i in range(res["iterations"]):
+                    resid = res["true_residual_history"][i] if track else res["residual_history"][i]
+                    f.write(f"{i + 1},{fmt17(resid)},{res['max_rank_history'][i]},"
+                            f"{fmt17(res['rounding_seconds_history'][i])}\n")
+        except OSError:
+            raise TTRoundError(15, f"IoError: cannot open {args.csv}")
+    summary = {"converged": res["converged"], "iterations": res["iterations"], "strategy": args.strategy,
+               "arnoldi_residual": res["residual_history"][-1] if res["residual_history"] else 0.0,
+               "solution_ranks": res["solution"].ranks(), "rounding_seconds": res["rounding_seconds"],
+               "seed": args.seed}
+    if track and res["true_residual_history"]:
+        summary["true_residual"] = res["true_residual_history"][-1]
+    if args.csv:
+        summary["csv"] = args.csv
+    print(json.dumps(summary))
+    return 0
+
+
 def main(argv=None) -> int:
     ap = argparse.ArgumentParser(prog="ttround-b200")
     sub = ap.add_subparsers(dest="cmd", required=True)
@@ -177,10 +210,27 @@ def main(argv=None) -> int:
     b.add_argument("--master-seed", type=int, default=20250807)
     b.add_argument("--rng", default="xoshiro", choices=["xoshiro", "philox"])
     b.add_argument("--device", type=int, default=0)
+    k = sub.add_parser("cookie", help="parametric cookie problem via TT-GMRES")
+    k.add_argument("--params", type=int, default=3)
+    k.add_argument("--grid", type=int, default=16)
+    k.add_argument("--nsamples", type=int, default=8)
+    k.add_argument("--rho-min", type=float, default=1.0)
+    k.add_argument("--rho-max", type=float, default=10.0)
+    k.add_argument("--tol", type=float, default=1e-6)
+    k.add_argument("--strategy", default="krp-adapt-sum", choices=list(COOKIE_STRATEGIES))
+    k.add_argument("--seed", type=int, default=0)
+    k.add_argument("--csv", default="")
+    k.add_argument("--max-iters", type=int, default=250)
+    k.add_argument("--round-tol", type=float, default=0.0)
+    k.add_argument("--no-true-residual", action="store_true")
+    k.add_argument("--rng", default="xoshiro", choices=["xoshiro", "philox"])
+    k.add_argument("--device", type=int, default=0)
     args = ap.parse_args(argv)
     try:
         if args.cmd == "bench-synthetic":
             return cmd_bench_synthetic(args)
+        if args.cmd == "cookie":
+            return cmd_cookie(args)
         return cmd_round(args)
     except TTRoundError as e:
         print(f"ttround error: {e}", file=sys.stderr)

@@ -787,6 +787,9 @@ ttr_status ttr_tt_gmres(ttr_ctx* ctx, const ttr_kron_op* op, const ttr_tt* rhs, 
         if (result->true_residual_history)
             for (std::size_t i = 0; i < r.true_residual_history.size(); ++i)
                 result->true_residual_history[i] = r.true_residual_history[i];
+        if (result->rounding_seconds_history)
+            for (std::size_t i = 0; i < r.rounding_seconds_history.size(); ++i)
+                result->rounding_seconds_history[i] = r.rounding_seconds_history[i];
         *solution = wrap(std::move(r.solution));
     });
 }

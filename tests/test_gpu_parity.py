@@ -1128,3 +1128,32 @@ def test_gmres_criterion8_on_device(P, O):
         c = min(len(r["max_rank_history"]), len(det["max_rank_history"]))
         ratio = max([1.0] + [max(x / y, y / x) for x, y in zip(r["max_rank_history"][:c], det["max_rank_history"][:c])])
         assert ratio <= 2.0
+
+
+def test_cli_cookie(P, O, tmp_path):
+    """`cookie` (ttround_main.cpp:246-296 mirror): JSON summary with the reference's
+    keys and the iteration CSV with its header; the run equals the API call; an
+    unknown strategy is rejected."""
+    import csv
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = tmp_path / "c.csv"
+    cmd = [sys.executable, "-m", "paper_2511_03598_b200.cli", "cookie", "--params", "2", "--grid", "8", "--nsamples",
+           "4", "--tol", "1e-5", "--strategy", "det", "--max-iters", "120", "--csv", str(out)]
+    res = subprocess.run(cmd, capture_output=True, text=True, cwd=root)
+    assert res.returncode == 0, res.stderr
+    summ = json.loads(res.stdout.strip().splitlines()[-1])
+    assert set(summ) >= {"converged", "iterations", "strategy", "arnoldi_residual", "solution_ranks",
+                         "rounding_seconds", "seed", "true_residual", "csv"}
+    assert summ["converged"] and summ["strategy"] == "det"
+    ref = O.tt_gmres_cookie(2, 8, 4, 1.0, 10.0, rel_tolerance=1e-5, max_iterations=120, strategy=O.DETERMINISTIC)
+    assert summ["iterations"] == ref["iterations"] and summ["solution_ranks"] == ref["solution"].ranks
+    rows = list(csv.reader(open(out)))
+    assert ",".join(rows[0]) == "iteration,rel_residual,max_tt_rank,cum_rounding_seconds"
+    assert len(rows) - 1 == summ["iterations"]
+    assert [int(r[2]) for r in rows[1:]] == ref["max_rank_history"]
+    bad = subprocess.run(cmd[:4] + ["--strategy", "nope"], capture_output=True, text=True, cwd=root)
+    assert bad.returncode != 0
