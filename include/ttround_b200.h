@@ -417,6 +417,10 @@ typedef struct {
 ttr_status ttr_kron_op_create(ttr_ctx* ctx, int64_t nterms, int64_t d, const int64_t* n, const double* factors,
                               ttr_kron_op** out);
 ttr_status ttr_kron_op_destroy(ttr_kron_op* op);
+/* Shape (nterms, d, n[d]; n may be NULL) and the factors, laid out as for create
+ * (factors may be NULL). */
+ttr_status ttr_kron_op_shape(const ttr_kron_op* op, int64_t* nterms, int64_t* d, int64_t* n);
+ttr_status ttr_kron_op_factors(const ttr_kron_op* op, double* factors);
 ttr_status ttr_cookie_problem(ttr_ctx* ctx, int64_t num_param_modes, int64_t grid_size, int64_t num_param_samples,
                               double rho_min, double rho_max, ttr_kron_op** op, ttr_tt** rhs);
 ttr_status ttr_apply_operator(ttr_ctx* ctx, const ttr_kron_op* op, const ttr_tt* x, ttr_tt** out_terms);

@@ -9,6 +9,7 @@
 //   round_fixed_krp                         round_rand.hpp:14-15
 //   AdaptiveConfig / round_adaptive_krp     round_rand.hpp:18-31
 //   TTSum / round_sum_adaptive_krp          sum_round.hpp:11-29
+//   KroneckerSumOperator / build_cookie_problem / apply_operator / tt_gmres   solver.hpp:12-82
 //   round_deterministic (tolerance / ranks) orthogonalize.hpp:50,54
 //   estimate_norm_krp                       sketch.hpp:63
 //   norm_exact / relative_error / formal_sum / scaled   tensor.hpp:172-191
@@ -477,6 +478,138 @@ inline double residual_norm_estimate(const Matrix& s, Index block, Context& ctx 
     double v = 0.0;
     check(ttr_residual_norm_estimate(ctx.get(), s.rows(), s.cols(), s.data(), block, &v));
     return v;
+}
+
+// ---- TT-GMRES cookie harness (solver.hpp) ----------------------------------
+
+//! KroneckerSumOperator (solver.hpp:12-21): terms[i][k-1] = A_{i,k}; the
+//! factors are uploaded once (the device operator is kept alongside).
+struct KroneckerSumOperator {
+    std::vector<std::vector<Matrix>> terms;
+    std::shared_ptr<ttr_kron_op> dev;
+    static KroneckerSumOperator of(std::vector<std::vector<Matrix>> terms, Context& ctx = Context::thread_default()) {
+        if (terms.empty()) throw Error(Errc::InvalidArgument, "operator needs at least one term");
+        const std::size_t d = terms.front().size();
+        if (d == 0) throw Error(Errc::InvalidArgument, "operator term needs at least one factor");
+        std::vector<int64_t> n;
+        for (const auto& a : terms.front()) n.push_back(a.rows());
+        std::vector<double> flat;
+        for (const auto& term : terms) {
+            if (term.size() != d) throw Error(Errc::ModeSizeMismatch, "operator terms have unequal order");
+            for (std::size_t k = 0; k < d; ++k) {
+                if (term[k].rows() != term[k].cols() || term[k].rows() != n[k])
+                    throw Error(Errc::ModeSizeMismatch, "operator factors must be square and consistent");
+                flat.insert(flat.end(), term[k].a.begin(), term[k].a.end());
+            }
+        }
+        ttr_kron_op* h = nullptr;
+        check(ttr_kron_op_create(ctx.get(), static_cast<int64_t>(terms.size()), static_cast<int64_t>(d), n.data(),
+                                 flat.data(), &h));
+        KroneckerSumOperator op;
+        op.terms = std::move(terms);
+        op.dev.reset(h, &ttr_kron_op_destroy);
+        return op;
+    }
+    Index num_terms() const { return static_cast<Index>(terms.size()); }
+    Index order() const { return static_cast<Index>(terms.front().size()); }
+    std::vector<Index> mode_sizes() const {
+        std::vector<Index> out;
+        for (const auto& a : terms.front()) out.push_back(a.rows());
+        return out;
+    }
+};
+
+struct CookieProblem {
+    KroneckerSumOperator op;
+    TTTensor rhs;
+};
+
+//! build_cookie_problem (solver.hpp:32-40): assembled on the host and the
+//! device by the same formulas (the host factors stay in op.terms).
+inline CookieProblem build_cookie_problem(Index num_param_modes, Index grid_size, Index num_param_samples,
+                                          double rho_min, double rho_max, Context& ctx = Context::thread_default()) {
+    ttr_kron_op* h = nullptr;
+    ttr_tt* rhs = nullptr;
+    check(ttr_cookie_problem(ctx.get(), num_param_modes, grid_size, num_param_samples, rho_min, rho_max, &h, &rhs));
+    std::shared_ptr<ttr_kron_op> dev(h, &ttr_kron_op_destroy);
+    TTTensor b(rhs, ctx);
+    // host copies of the factors (the reference keeps them in op.terms)
+    int64_t nterms = 0, d = 0;
+    check(ttr_kron_op_shape(h, &nterms, &d, nullptr));
+    std::vector<int64_t> n(static_cast<std::size_t>(d));
+    check(ttr_kron_op_shape(h, &nterms, &d, n.data()));
+    std::size_t tot = 0;
+    for (int64_t k : n) tot += static_cast<std::size_t>(k * k);
+    std::vector<double> flat(tot * static_cast<std::size_t>(nterms));
+    check(ttr_kron_op_factors(h, flat.data()));
+    KroneckerSumOperator op;
+    op.dev = dev;
+    std::size_t off = 0;
+    for (int64_t i = 0; i < nterms; ++i) {
+        std::vector<Matrix> term;
+        for (int64_t k : n) {
+            Matrix a(k, k);
+            std::copy(flat.begin() + static_cast<std::ptrdiff_t>(off), flat.begin() + static_cast<std::ptrdiff_t>(off + k * k),
+                      a.a.begin());
+            off += static_cast<std::size_t>(k * k);
+            term.push_back(std::move(a));
+        }
+        op.terms.push_back(std::move(term));
+    }
+    return CookieProblem{std::move(op), std::move(b)};
+}
+
+//! apply_operator (solver.hpp:42-44): the s-term sum A x.
+inline TTSum apply_operator(const KroneckerSumOperator& op, const TTTensor& x) {
+    std::vector<ttr_tt*> outs(static_cast<std::size_t>(op.num_terms()), nullptr);
+    check(ttr_apply_operator(x.context().get(), op.dev.get(), x.get(), outs.data()));
+    std::vector<TTTensor> terms;
+    for (ttr_tt* t : outs) terms.emplace_back(t, x.context());
+    return TTSum::of(std::move(terms));
+}
+
+enum class RoundingStrategy { Deterministic = TTR_GMRES_DETERMINISTIC, RandOrthTT = TTR_GMRES_RAND_ORTH_TT,
+                              AdaptiveKRPSum = TTR_GMRES_ADAPTIVE_KRP_SUM };
+
+struct GMRESConfig {  // solver.hpp:48-64
+    double rel_tolerance = 1e-8;
+    Index max_iterations = 200;
+    RoundingStrategy strategy = RoundingStrategy::Deterministic;
+    double rounding_tolerance = 0.0;
+    std::uint64_t seed = 0;
+    bool track_true_residual = true;
+    bool mean_field_preconditioner = true;
+    RngMode rng = RngMode::Xoshiro;  //!< sketch generator of the randomized strategies
+};
+
+struct GMRESResult {  // solver.hpp:66-78
+    TTTensor solution;
+    std::vector<double> residual_history, true_residual_history;
+    std::vector<Index> max_rank_history;
+    std::vector<double> rounding_seconds_history;
+    double rounding_seconds = 0.0;
+    Index iterations = 0;
+    bool converged = false;
+};
+
+//! tt_gmres (solver.hpp:80-82) on the device; throws Breakdown as the reference.
+inline GMRESResult tt_gmres(const KroneckerSumOperator& op, const TTTensor& rhs, const GMRESConfig& cfg) {
+    ttr_gmres_cfg c{cfg.rel_tolerance, cfg.max_iterations, static_cast<int>(cfg.strategy), cfg.rounding_tolerance,
+                    cfg.seed, cfg.track_true_residual ? 1 : 0, cfg.mean_field_preconditioner ? 1 : 0,
+                    static_cast<int>(cfg.rng)};
+    const std::size_t m = static_cast<std::size_t>(cfg.max_iterations > 0 ? cfg.max_iterations : 1);
+    std::vector<double> rh(m), th(m), sh(m);
+    std::vector<int64_t> kh(m);
+    ttr_gmres_result r{0, 0, 0.0, rh.data(), th.data(), kh.data(), sh.data()};
+    ttr_tt* sol = nullptr;
+    check(ttr_tt_gmres(rhs.context().get(), op.dev.get(), rhs.get(), &c, &r, &sol));
+    const std::size_t n = static_cast<std::size_t>(r.iterations);
+    GMRESResult out{TTTensor(sol, rhs.context()), {}, {}, {}, {}, r.rounding_seconds, r.iterations, r.converged != 0};
+    out.residual_history.assign(rh.begin(), rh.begin() + n);
+    if (cfg.track_true_residual) out.true_residual_history.assign(th.begin(), th.begin() + n);
+    out.max_rank_history.assign(kh.begin(), kh.begin() + n);
+    out.rounding_seconds_history.assign(sh.begin(), sh.begin() + n);
+    return out;
 }
 
 namespace flops {

@@ -750,6 +750,28 @@ ttr_status ttr_kron_op_destroy(ttr_kron_op* op) {
     return TTR_OK;
 }
 
+ttr_status ttr_kron_op_shape(const ttr_kron_op* op, int64_t* nterms, int64_t* d, int64_t* n) {
+    return guard([&] {
+        need(op && op->op && nterms && d, "null argument");
+        *nterms = op->op->nterms;
+        *d = static_cast<int64_t>(op->op->n.size());
+        if (n)
+            for (std::size_t k = 0; k < op->op->n.size(); ++k) n[k] = op->op->n[k];
+    });
+}
+
+ttr_status ttr_kron_op_factors(const ttr_kron_op* op, double* factors) {
+    return guard([&] {
+        need(op && op->op && factors, "null argument");
+        std::size_t off = 0;
+        for (const auto& term : op->op->host)
+            for (const auto& a : term) {
+                std::memcpy(factors + off, a.data(), sizeof(double) * a.size());
+                off += a.size();
+            }
+    });
+}
+
 ttr_status ttr_cookie_problem(ttr_ctx* ctx, int64_t num_param_modes, int64_t grid_size, int64_t num_param_samples,
                               double rho_min, double rho_max, ttr_kron_op** op, ttr_tt** rhs) {
     return guard_ctx(ctx, [&] {

@@ -5,6 +5,7 @@
 // same input and the same (reference xoshiro) stream. TEST INFRASTRUCTURE:
 // links the oracle (oracle/_build/libttr_oracle.so) only as the checker.
 // Prints one "dropin ok" line; a non-zero exit code names the failed check.
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <string>
@@ -153,6 +154,43 @@ int main() {
         EXPECT(O::relative_error(dt, to_oracle(dd)) <= 1e-10, "round_deterministic");
         const double ne = T::estimate_norm_krp(x, 16, 21), ne_o = O::estimate_norm_krp(xo, 16, 21, O::RngMode::Xoshiro);
         EXPECT(std::abs(ne - ne_o) <= 1e-12 * ne_o, "estimate_norm_krp");
+
+        // the TT-GMRES cookie harness (solver.hpp): the operator's factors, apply_operator,
+        // and tt_gmres on the small cookie problem (test_solver.cpp:109-125)
+        {
+            const auto cp = T::build_cookie_problem(2, 8, 4, 1.0, 10.0);
+            const auto co = O::build_cookie_problem(2, 8, 4, 1.0, 10.0);
+            bool same = cp.op.num_terms() == co.op.num_terms();
+            for (T::Index i = 0; same && i < cp.op.num_terms(); ++i)
+                for (T::Index k = 0; k < cp.op.order(); ++k)
+                    same = same && bitwise(cp.op.terms[static_cast<std::size_t>(i)][static_cast<std::size_t>(k)],
+                                           co.op.terms[static_cast<std::size_t>(i)][static_cast<std::size_t>(k)]);
+            EXPECT(same, "build_cookie_problem factors");
+            EXPECT(O::relative_error(co.rhs, to_oracle(cp.rhs)) <= 1e-14, "build_cookie_problem rhs");
+            const O::TT xr = O::random_gaussian_tt({64, 4, 4}, {1, 3, 2, 1}, 31);
+            const auto ad2 = T::apply_operator(cp.op, to_device(xr));
+            const auto ao2 = O::apply_operator(co.op, xr);
+            bool ok = ad2.terms.size() == ao2.size();
+            for (std::size_t i = 0; ok && i < ao2.size(); ++i) ok = O::relative_error(ao2[i], to_oracle(ad2.terms[i])) <= 1e-13;
+            EXPECT(ok, "apply_operator");
+            T::GMRESConfig gc;
+            gc.rel_tolerance = 1e-5;
+            gc.max_iterations = 120;
+            gc.strategy = T::RoundingStrategy::AdaptiveKRPSum;
+            gc.seed = 4;
+            O::GmresConfig go;
+            go.rel_tolerance = 1e-5;
+            go.max_iterations = 120;
+            go.strategy = O::GmresStrategy::AdaptiveKRPSum;
+            go.seed = 4;
+            const auto gd = T::tt_gmres(cp.op, cp.rhs, gc);
+            const auto gr = O::tt_gmres(co.op, co.rhs, go);
+            EXPECT(gd.converged && gr.converged && gd.iterations == gr.iterations, "tt_gmres iterations");
+            EXPECT(gd.max_rank_history.size() == gr.max_rank_history.size() &&
+                       std::equal(gd.max_rank_history.begin(), gd.max_rank_history.end(), gr.max_rank_history.begin()),
+                   "tt_gmres rank history");
+            EXPECT(O::relative_error(gr.solution, to_oracle(gd.solution)) <= 1e-8, "tt_gmres solution");
+        }
 
         // the TTTensor constructor's checks, in the reference's order (tensor.cpp:66-79)
         EXPECT(errc_of([] { T::TTTensor(std::vector<T::Core>{}); }) == T::Errc::EmptyCoreList, "EmptyCoreList");

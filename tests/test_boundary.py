@@ -120,7 +120,8 @@ def test_dropin_vs_oracle_runs_on_device(tmp_path):
     scaled, GaussianStream/draw_gaussian_factors/append_gaussian_columns (bitwise, reference
     stream), krp_partial_contractions_rl, append_krp_contractions, generate_residual_sketch,
     residual_norm_estimate, round_fixed_krp / round_adaptive_krp / round_deterministic /
-    estimate_norm_krp (reference stream), and the constructor's error kinds."""
+    estimate_norm_krp (reference stream), build_cookie_problem / apply_operator / tt_gmres, and
+    the constructor's error kinds."""
     exe = _build_dropin(tmp_path)
     out = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     assert out.returncode == 0, out.stdout + out.stderr
