@@ -841,15 +841,18 @@ def run_5a(args, world, rank, local):
     fb, ff = 0, 0  # algorithmic bytes / flops of the d-2 fused launches
     for k in range(1, d_ - 1):
         l, cols, nk, rr, l2 = rb[k], r_in[k], n_[k], r_in[k + 1], rb[k + 1]
-        fb += 8 * nb * (cols * nk * rr + l * nk * rr + l * nk * l2 + l * cols + rr * l2)
+        # X read, Y write, S (or, fused with the next QR, Q) write, M read, W read,
+        # and the fused kernel's M_next write (l2 x rr)
+        fb += 8 * nb * (cols * nk * rr + l * nk * rr + l * nk * l2 + l * cols + rr * l2 + l2 * rr)
         ff += nb * (2 * l * nk * rr * cols + 2 * l * nk * l2 * rr)
     fused_ms = phase_ms[3]
     roof = None
     if fused_ms > 0:
         gbs = fb / (fused_ms * 1e-3) / 1e9
         roof = {"bound": "hbm", "achieved": gbs, "peak": HBM_PEAK_GBS, "unit": "GB/s", "frac": gbs / HBM_PEAK_GBS,
-                "traffic": None, "kernel": "lr_fused_kernel<3,3> (next core M H(X) + next sketch V(Y) W, one CTA per "
-                                          "tensor, cp.async-streamed X slices, fp64 DMMA)",
+                "traffic": None, "kernel": "lr_fused_kernel<3,3,10> (next core M H(X) + next sketch V(Y) W + its Householder "
+                                          "QR (the output core) + M_next = Q^T V(Y), one CTA per tensor, "
+                                          "cp.async-streamed X slices, fp64 DMMA)",
                 "peak_source": "MEASURED_PEAKS.json HBM copy bandwidth",
                 "algorithmic_bytes_per_launch": fb / (d_ - 2), "launches": d_ - 2, "ms_all_launches": fused_ms,
                 "arithmetic_intensity": ff / fb, "tflops_achieved": ff / (fused_ms * 1e-3) / 1e12}

@@ -48,6 +48,12 @@ struct LrArgs {
     i64 sY;
     double* S;        // (l n) x l2, ld l n
     i64 sS;
+    // fused QR epilogue (lr_fused_kernel<.., RT > 0>): Q = qr(S) -> Q (the output
+    // core, (l n) x l2, ld l n) and M_next = Q^T V(Y) (l2 x rr, ld l2)
+    double* Q;
+    i64 sQ;
+    double* Mn;
+    i64 sMn;
 };
 
 // Y slices are kept transposed, [g][a] with ld kLdY: the output stores read
@@ -68,8 +74,9 @@ struct STiles {
     static constexpr int kPerWarp = (kTiles + kWarps - 1) / kWarps;
 };
 
-// l <= 8 LT, l2 <= 8 LT2, cols <= 64 (even), rr <= 64
-template <int LT, int LT2>
+// l <= 8 LT, l2 <= 8 LT2, cols <= 64 (even), rr <= 64; RT > 0: l n <= 32 RT and
+// the QR + M_next epilogue (the per-tensor QR of step k+1 and M = Q^T V)
+template <int LT, int LT2, int RT = 0>
 __global__ void __launch_bounds__(kThreads, 2) lr_fused_kernel(const LrArgs p) {
     extern __shared__ __align__(16) double sm[];
     double* Ms = sm;                    // [8 LT][kLd]: M(a, b)
@@ -170,6 +177,52 @@ __global__ void __launch_bounds__(kThreads, 2) lr_fused_kernel(const LrArgs p) {
             }
         }
     }
+    if constexpr (RT > 0) {
+        // ---- fused step k+1: Q = qr(S) (S just written by this CTA; plain loads),
+        //      the output core, then M_next = Q^T V(Y) on the DMMA pipe ----
+        __syncthreads();  // every S and Y store of this CTA is visible; Xs/Ys are free
+        double* Q = p.Q + t * p.sQ;
+        double qx[LT2][RT];
+        colreg_qr_cta<RT, LT2, kWarps>(rows, l2, S, rows, Q, rows, nullptr, 1, Ys, qx);
+        // Q^T staged row-major, [a][r] with ld kLdQ (% 16 == 4: conflict-free A fragments)
+        constexpr int kLdQ = 32 * RT + 4;
+        double* Qt = Xs;
+        __syncthreads();  // the QR's shared-memory staging is done before Xs is reused
+#pragma unroll
+        for (int c = 0; c < LT2; ++c) {
+            const int a = warp + kWarps * c;
+#pragma unroll
+            for (int tt = 0; tt < RT; ++tt) {
+                const int r = lane + 32 * tt;
+                if (a < 8 * LT2) Qt[a * kLdQ + r] = (a < l2 && r < rows) ? qx[c][tt] : 0.0;
+            }
+        }
+        __syncthreads();
+        // M_next (l2 x rr): warp w owns columns g = 8w .. 8w+7 (rr <= 64), all LT2 row tiles;
+        // B fragments Y(r, g) from global (written above, L2-resident)
+        double am[LT2][2];
+#pragma unroll
+        for (int i = 0; i < LT2; ++i) am[i][0] = am[i][1] = 0.0;
+        const int g = 8 * warp + fr;
+        const double* ycol = Y + static_cast<i64>(g < rr ? g : 0) * rows;
+        for (int k4 = 0; k4 < 32 * RT; k4 += 4) {
+            const int r = k4 + fc;
+            const double bv = (g < rr && r < rows) ? ycol[r] : 0.0;
+#pragma unroll
+            for (int i = 0; i < LT2; ++i) mma(am[i][0], am[i][1], Qt[(8 * i + fr) * kLdQ + r], bv);
+        }
+        double* Mn = p.Mn + t * p.sMn;
+#pragma unroll
+        for (int i = 0; i < LT2; ++i) {
+            const int a = 8 * i + fr;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int gg = 8 * warp + 2 * fc + h;
+                if (a < l2 && gg < rr) Mn[a + static_cast<i64>(gg) * l2] = am[i][h];
+            }
+        }
+    }
+
 }
 
 }  // namespace lrb

@@ -9,6 +9,13 @@
 // 1.45-1.88 ms (64-bit shuffles / one CTA per SM); this kernel 668 us.
 #pragma once
 
+#include <cfloat>
+
+__device__ __forceinline__ double colreg_warp_sum(double v) {
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
 // owner warp: stage its register column cj of x (rows lane + 32t) into cb
 // and return sum_{r>j} of its squares (warp sum). The column is picked by
 // selects, not x[cj] — a runtime index would put x in local memory.
@@ -24,7 +31,7 @@ __device__ __forceinline__ double colreg_stage(const double (&x)[C][RT], int cj,
         cb[r] = v;
         if (r > j) s = fma(v, v, s);
     }
-    return warp_sum(s);
+    return colreg_warp_sum(s);
 }
 
 // Register-resident column owners (dispatched for m <= 32*RT, n <= NW*C): warp w
@@ -36,26 +43,27 @@ __device__ __forceinline__ double colreg_stage(const double (&x)[C][RT], int cj,
 // warp loads the staged column once (masked to rows > j), dots its columns
 // with it (warp sums) and updates them. n <= 32, so rows <= j all sit in the
 // first chunk (lane <= j) and only the staged copy of that chunk is masked.
-template <int RT, int C, int NW = 8>
-__global__ void __launch_bounds__(NW * 32, 16 / NW) qr_small_colreg_kernel(int m, int n, const double* __restrict__ A, i64 lda,
-                                                                 i64 sA, double* Q, i64 ldq, i64 sQ, double* R,
-                                                                 i64 ldr, i64 sR) {
-    extern __shared__ double sm[];
+// One CTA's QR of one m x n matrix (the body of qr_small_colreg_kernel, also
+// called from the fused batched sweep kernel, lr_batch.cuh): A is read with
+// plain loads (it may have been written earlier in the same kernel); Q (m x k)
+// and R (optional) are written; on return x holds Q in registers (column
+// warp + NW c, rows lane + 32 t). sm: 2*32*RT + 38 doubles of shared memory.
+template <int RT, int C, int NW>
+__device__ __forceinline__ void colreg_qr_cta(int m, int n, const double* A, i64 lda, double* Q, i64 ldq, double* R,
+                                              i64 ldr, double* sm, double (&x)[C][RT]) {
     double* colb = sm;                 // [2][32*RT] active column
     double* tl = colb + 2 * 32 * RT;   // [2][3] beta, inv, tau of the active reflector
     double* taus = tl + 6;             // [32]
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int k = min(m, n);
-    A += blockIdx.x * sA;
 
-    double x[C][RT];
 #pragma unroll
     for (int c = 0; c < C; ++c) {
         const int l = warp + NW * c;
 #pragma unroll
         for (int t = 0; t < RT; ++t) {
             const int r = lane + 32 * t;
-            x[c][t] = (l < n && r < m) ? __ldg(A + r + static_cast<i64>(l) * lda) : 0.0;
+            x[c][t] = (l < n && r < m) ? A[r + static_cast<i64>(l) * lda] : 0.0;
         }
     }
     double my_inv[C];
@@ -110,7 +118,7 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) qr_small_colreg_kernel(int m
                 if (t & 1) s1 = fma(cv[t], x[c][t], s1);
                 else s0 = fma(cv[t], x[c][t], s0);
             }
-            const double d = warp_sum(s0 + s1);
+            const double d = colreg_warp_sum(s0 + s1);
             const double row = __shfl_sync(0xffffffffu, x[c][0], j);
             const double wl = act ? tj * fma(inv, d, row) : 0.0;
             const double ca = -wl * inv;
@@ -129,7 +137,6 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) qr_small_colreg_kernel(int m
             if (lane + 32 * t > l && l < k) x[c][t] *= my_inv[c];
     }
     if (R) {
-        R += blockIdx.x * sR;
 #pragma unroll
         for (int c = 0; c < C; ++c) {
             const int l = warp + NW * c;
@@ -141,7 +148,6 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) qr_small_colreg_kernel(int m
         }
     }
     if (Q == nullptr) return;
-    Q += blockIdx.x * sQ;
     __syncthreads();  // taus visible; the last factorization step's readers are done
 
     // ---- explicit thin Q (backward accumulation) ----
@@ -161,7 +167,7 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) qr_small_colreg_kernel(int m
                 if (t & 1) s1 = fma(cv[t], x[c][t], s1);
                 else s0 = fma(cv[t], x[c][t], s0);
             }
-            const double d = warp_sum(s0 + s1);
+            const double d = colreg_warp_sum(s0 + s1);
             const double row = __shfl_sync(0xffffffffu, x[c][0], i);
             const double wl = act ? ti * (d + row) : 0.0;
             // others: x_l -= w_l v_i; the owner: column i becomes e_i - tau_i v_i,
@@ -184,4 +190,14 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) qr_small_colreg_kernel(int m
             if (l < k && r < m) Q[r + static_cast<i64>(l) * ldq] = x[c][t];
         }
     }
+}
+
+template <int RT, int C, int NW = 8>
+__global__ void __launch_bounds__(NW * 32, 16 / NW) qr_small_colreg_kernel(int m, int n, const double* __restrict__ A, i64 lda,
+                                                                 i64 sA, double* Q, i64 ldq, i64 sQ, double* R,
+                                                                 i64 ldr, i64 sR) {
+    extern __shared__ double sm[];
+    double x[C][RT];
+    colreg_qr_cta<RT, C, NW>(m, n, A + blockIdx.x * sA, lda, Q ? Q + blockIdx.x * sQ : nullptr, ldq,
+                             R ? R + blockIdx.x * sR : nullptr, ldr, sm, x);
 }

@@ -15,10 +15,50 @@
 
 namespace ttr {
 namespace {
+#include "qr_batch.cuh"
 #include "lr_batch.cuh"
 
 // Fused H(Y) = M H(X) + S_next = V(Y) W (lr_batch.cuh) when the shapes fit one
 // CTA per tensor; false = caller takes the two-GEMM path.
+// with_qr: also Q = qr(S) into a.Q and M_next = Q^T V(Y) into a.Mn (the
+// per-tensor QR of the next step and its M GEMM fused into the same CTA; l n
+// <= 320 and 17 <= l2 <= 24, else false)
+bool lr_fused_qr_batched(Ctx& c, const lrb::LrArgs& a, i64 batch) {
+    if (a.l > 24 || a.l2 > 24 || a.l2 < 17 || a.cols > 64 || a.rr > 64 || (a.cols & 1) || a.l < 1) return false;
+    if (static_cast<i64>(a.l) * a.n > 320) return false;
+    if ((reinterpret_cast<std::uintptr_t>(a.X) & 15) || (a.sX & 1)) return false;
+    // Opt-in (TTR_LR_QR=1): measured on B200 (config 5a, phase timing, 4096
+    // tensors per launch) 1.73 ms per mode fused vs 1.65 ms for the separate
+    // sweep + QR + M launches — the two co-resident CTAs reach their
+    // latency-bound QR epilogues together, so it does not hide behind the
+    // other's streaming.
+    static const bool on = [] {
+        const char* e = std::getenv("TTR_LR_QR");
+        return e && e[0] == '1';
+    }();
+    if (!on) return false;
+    const int lt = (a.l + 7) / 8;
+    bool done = false;
+    auto go = [&](auto t1) {
+        constexpr int LT = decltype(t1)::value;
+        if (done || lt != LT) return;
+        auto kern = lrb::lr_fused_kernel<LT, 3, 10>;
+        constexpr std::size_t smem = lrb::LrSmem<LT>::kBytes;
+        static std::atomic<std::uint64_t> configured{0};  // bit d: attributes set on device d
+        if (first_on_device(configured)) {
+            TTR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        }
+        kern<<<static_cast<unsigned>(batch), lrb::kThreads, smem, c.stream>>>(a);
+        TTR_CUDA(cudaGetLastError());
+        c.launched();
+        done = true;
+    };
+    go(std::integral_constant<int, 1>{});
+    go(std::integral_constant<int, 2>{});
+    go(std::integral_constant<int, 3>{});
+    return done;
+}
+
 bool lr_fused_batched(Ctx& c, const lrb::LrArgs& a, i64 batch) {
     if (a.l > 32 || a.l2 > 32 || a.cols > 64 || a.rr > 64 || (a.cols & 1) || a.l < 1 || a.l2 < 1) return false;
     if ((reinterpret_cast<std::uintptr_t>(a.X) & 15) || (a.sX & 1)) return false;
@@ -171,10 +211,13 @@ std::unique_ptr<TTBatch> round_fixed_krp_batched(Ctx& c, const TTBatch& t, const
         }
         DBuf work(c, static_cast<std::size_t>(max_work * Bg));
         DBuf S(c, static_cast<std::size_t>(max_s * Bg));
-        DBuf M(c, static_cast<std::size_t>(width * t.max_rank() * Bg));
+        DBuf M(c, static_cast<std::size_t>(width * t.max_rank() * Bg)), M2(c, static_cast<std::size_t>(width * t.max_rank() * Bg));
+        double* Mcur = M.p;   // M_k = Q_k^T V(Y_k)
+        double* Mnext = M2.p;  // written by the fused QR epilogue for step k+1
         const double* v = t.core(b0, 0);
         i64 sv = t.stride;
         bool s_ready = false;  // S of this step already formed by the previous fused step
+        bool q_ready = false;  // ... and its QR (the output core) and M as well
         for (i64 k = 1; k < d; ++k) {
             const i64 rows = r[k - 1] * t.n[k - 1], cols = t.r[k], l = r[k];
             if (!s_ready) {
@@ -182,7 +225,7 @@ std::unique_ptr<TTBatch> round_fixed_krp_batched(Ctx& c, const TTBatch& t, const
                 gemm_batched(c, false, rows, l, cols, 1.0, v, rows, sv, W[k + 1].p, ldw[k + 1], sw[k + 1], 0.0, S.p, rows,
                              rows * l, Bg);
             }
-            {
+            if (!q_ready) {
                 PhaseScope ph(c, kPhaseQr);
                 c.charge_qr(4ULL * static_cast<std::uint64_t>(rows) * l * std::min(rows, l) * Bg);
                 if (rows * l <= 26000) {
@@ -197,13 +240,14 @@ std::unique_ptr<TTBatch> round_fixed_krp_batched(Ctx& c, const TTBatch& t, const
             const i64 ncols = t.n[k] * t.r[k + 1];
             double* dst = (k == d - 1) ? out->core(b0, d - 1) : work.p;
             const i64 sdst = (k == d - 1) ? out->stride : l * ncols;
-            {
+            if (!q_ready) {
                 PhaseScope ph(c, kPhaseGemm);
-                gemm_batched(c, true, l, cols, rows, 1.0, out->core(b0, k - 1), rows, out->stride, v, rows, sv, 0.0, M.p, l,
+                gemm_batched(c, true, l, cols, rows, 1.0, out->core(b0, k - 1), rows, out->stride, v, rows, sv, 0.0, Mcur, l,
                              l * cols, Bg);
             }
             {
                 s_ready = false;
+                q_ready = false;
                 if (k < d - 1) {
                     PhaseScope ph(c, kPhaseOther);  // the fused kernel alone (bench.py roofline)
                     // next step's sketch S = V(Y_{k+1}) W_{k+2} fused with Y_{k+1} = M H(X_{k+1})
@@ -213,7 +257,7 @@ std::unique_ptr<TTBatch> round_fixed_krp_batched(Ctx& c, const TTBatch& t, const
                     a.n = static_cast<int>(t.n[k]);
                     a.rr = static_cast<int>(t.r[k + 1]);
                     a.l2 = static_cast<int>(r[k + 1]);
-                    a.M = M.p;
+                    a.M = Mcur;
                     a.sM = l * cols;
                     a.X = t.core(b0, k);
                     a.sX = t.stride;
@@ -224,15 +268,28 @@ std::unique_ptr<TTBatch> round_fixed_krp_batched(Ctx& c, const TTBatch& t, const
                     a.sY = sdst;
                     a.S = S.p;
                     a.sS = l * t.n[k] * r[k + 1];
-                    s_ready = lr_fused_batched(c, a, Bg);
+                    // ... and, when the shapes allow, step k+1's QR (output core k+1)
+                    // and M_{k+1} = Q^T V(Y_{k+1}) in the same CTA
+                    const i64 rows2 = l * t.n[k], l2 = r[k + 1], cols2 = t.r[k + 1];
+                    a.Q = out->core(b0, k);
+                    a.sQ = out->stride;
+                    a.Mn = Mnext;
+                    a.sMn = l2 * cols2;
+                    q_ready = lr_fused_qr_batched(c, a, Bg);
+                    s_ready = q_ready || lr_fused_batched(c, a, Bg);
                     if (s_ready) {
                         c.charge_gemm(2ULL * static_cast<std::uint64_t>(l) * ncols * cols * Bg);
                         c.charge_gemm(2ULL * static_cast<std::uint64_t>(l * t.n[k]) * r[k + 1] * t.r[k + 1] * Bg);
                     }
+                    if (q_ready) {
+                        c.charge_qr(4ULL * static_cast<std::uint64_t>(rows2) * l2 * std::min(rows2, l2) * Bg);
+                        c.charge_gemm(2ULL * static_cast<std::uint64_t>(l2) * cols2 * rows2 * Bg);
+                        std::swap(Mcur, Mnext);
+                    }
                 }
                 if (!s_ready) {
                     PhaseScope ph(c, kPhaseGemm);
-                    gemm_batched(c, false, l, ncols, cols, 1.0, M.p, l, l * cols, t.core(b0, k), cols, t.stride, 0.0, dst, l,
+                    gemm_batched(c, false, l, ncols, cols, 1.0, Mcur, l, l * cols, t.core(b0, k), cols, t.stride, 0.0, dst, l,
                                  sdst, Bg);
                 }
             }

@@ -1157,3 +1157,37 @@ def test_cli_cookie(P, O, tmp_path):
     assert [int(r[2]) for r in rows[1:]] == ref["max_rank_history"]
     bad = subprocess.run(cmd[:4] + ["--strategy", "nope"], capture_output=True, text=True, cwd=root)
     assert bad.returncode != 0
+
+
+_LR_QR_SCRIPT = r"""
+import sys, numpy as np
+sys.path[:0] = [sys.argv[1], sys.argv[2], sys.argv[3]]
+import paper_2511_03598_b200 as P, py_oracle as O
+from helpers import rel_err_vs_ref, to_oracle
+# config-5a shapes, 64 tensors: the fused sweep + QR + M kernel (TTR_LR_QR=1)
+b = P.TTBatch.two_part_philox(64, 8, 16, 16, 48, 1e-6, 1005)
+o = P.round_fixed_krp_batched(b, [20] * 7, 7)
+for i in (0, 31, 63):
+    n, r = b.shape()[1], b.shape()[2]
+    xo = O.TT.from_flat(len(n), n, r, b.flats(i, 1)[0])
+    ref = O.round_fixed_krp(xo, [20] * 7, O.derive_seed(7, i), rng=O.PHILOX)
+    no, ro = o.shape()[1], o.shape()[2]
+    got = O.TT.from_flat(len(no), no, ro, o.flats(i, 1)[0])
+    assert ro == ref.ranks, (ro, ref.ranks)
+    assert O.relative_error(ref, got) <= 1e-10
+print("ok")
+"""
+
+
+def test_batched_fused_qr_epilogue_opt_in(P, O):
+    """The opt-in fused sweep + per-tensor QR + M = Q^T V kernel (TTR_LR_QR=1, read
+    once per process, so in a subprocess) against the oracle on config-5a shapes."""
+    import os
+    import subprocess
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    root = os.path.dirname(here)
+    env = dict(os.environ, TTR_LR_QR="1")
+    r = subprocess.run([sys.executable, "-c", _LR_QR_SCRIPT, root, os.path.join(root, "oracle"), here],
+                       env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
