@@ -123,6 +123,7 @@ struct Ctx {
     // qr_spec_used records that it did. The flag holds the smallest mode whose
     // factorisation broke down (kQrNoBreakdown: none).
     bool qr_spec = false, qr_spec_used = false;
+    int qr_tag = -1;  // >= 0: the thin_qr being enqueued may use Cholesky-QR panels (K4d) under this tag
     i64 qr_hh_from = INT32_MAX;
     int* qr_flag = nullptr;
     int* qr_flag_dev();
@@ -259,6 +260,10 @@ constexpr int kQrNoBreakdown = 0x7f7f7f7f;  // flag value after a 0x7f byte mems
 bool cholqr_fits(i64 m, i64 n);
 void thin_qr_cholesky(Ctx& c, i64 m, i64 n, const double* A, i64 lda, double* Q, i64 ldq, double* R, i64 ldr,
                       int tag = 0);
+
+// Cholesky-QR panel with Householder reconstruction (qr_chol.cu, K4d): the rows
+// x b panel P -> R (P's top block), V (rows x b, unit lower), T (ld 32), tau.
+void cqr_panel(Ctx& c, i64 rows, i64 b, double* P, i64 ldp, double* V, i64 ldv, double* T, double* tau, int tag);
 
 // ---- SVD (svd.cu) -----------------------------------------------------------
 // Thin SVD of a small m x n matrix (m, n <= ~1024) by one-sided Jacobi on the

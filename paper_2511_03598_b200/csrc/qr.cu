@@ -846,10 +846,33 @@ void thin_qr(Ctx& c, i64 m, i64 n, const double* A, i64 lda, double* Q, i64 ldq,
     DBuf Wb(c, static_cast<std::size_t>(kPanel * std::max<i64>(n, 1)));
     DBuf Wb2(c, static_cast<std::size_t>(kPanel * std::max<i64>(n, 1)));
 
+    // Cholesky-QR panels with Householder reconstruction (K4d, qr_chol.cu) when
+    // the caller speculates (c.qr_tag >= 0: a breakdown reruns the call on the
+    // Householder panels). Opt-in (TTR_QR_CQR=1): measured on B200 at the 5b
+    // shape ~315 us per 40,960 x 32 panel (nine small launches: three passes of
+    // partial Grams, a one-CTA Cholesky + inverse and the row-parallel apply,
+    // then the reconstruction) against 145 us for the grid panel.
+    static const bool cqr_on = [] {
+        const char* e = std::getenv("TTR_QR_CQR");
+        return e && e[0] == '1';
+    }();
+    const bool cqr = cqr_on && c.qr_tag >= 0;
     for (i64 p = 0; p < npanels; ++p) {
         const i64 j0 = p * kPanel, bb = std::min<i64>(kPanel, k - j0), rows = m - j0;
         double* V = Vall.p + j0 + j0 * ldw;  // rows x bb block at (j0, j0), ld ldw
         double* T = Ts.p + p * kPanel * kPanel;
+        if (cqr && rows >= 4 * kPanel) {
+            cqr_panel(c, rows, bb, work.p + j0 + j0 * ldw, ldw, V, ldw, T, tau.p + j0, c.qr_tag);
+            c.qr_spec_used = true;
+            const i64 ntrail = n - j0 - bb;
+            if (ntrail > 0) {
+                double* At = work.p + j0 + (j0 + bb) * ldw;
+                gemm(c, true, bb, ntrail, rows, 1.0, V, ldw, At, ldw, 0.0, Wb.p, kPanel, false);    // V^T A
+                gemm(c, true, bb, ntrail, bb, 1.0, T, kPanel, Wb.p, kPanel, 0.0, Wb2.p, kPanel, false);  // T^T (V^T A)
+                gemm(c, false, rows, ntrail, bb, -1.0, V, ldw, Wb2.p, kPanel, 1.0, At, ldw, false);  // A -= V (.)
+            }
+            continue;
+        }
         RegQrArgs a{};
         a.rows = static_cast<int>(rows);
         a.b = static_cast<int>(bb);

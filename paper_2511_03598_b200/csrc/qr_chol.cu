@@ -508,6 +508,220 @@ void launch_trsm(Ctx& c, i64 m, i64 n, const double* A, i64 lda, const double* R
     c.launched();
 }
 
+// ---------------------------------------------------------------------------
+// K4d: Cholesky-QR panels with Householder reconstruction (the blocked
+// Householder QR's panel factorisation without a cross-CTA exchange per
+// column). A rows x b panel (b <= 32) is orthogonalised by shifted CholeskyQR3
+// (every pass: partial Grams per CTA -> one CTA reduces them in a fixed order,
+// factors the 32 x 32 Gram and inverts the factor -> Q = P R^{-1} row by row),
+// then the Householder vectors are rebuilt from Q (Ballard, Demmel, Grigori,
+// Jacquelin, Nguyen, Solomonik 2014): the LU without pivoting of Q_1 - S with
+// s_k = -sign of the running pivot gives Y_1 = L, U, and Y_2 = Q_2 U^{-1},
+// T = -U S Y_1^{-T}, R = S R_chol — exactly the (V, T, R) of the panel the
+// blocked QR's trailing updates and explicit-Q formation consume (H = I - V T V^T
+// with H [R; 0] = P).
+
+constexpr int kCqrThreads = 256;
+
+__global__ void __launch_bounds__(kCqrThreads) cqr_gram_partial(int rows, int b, const double* P, i64 ldp, int rpc,
+                                                               double* part) {
+    __shared__ double tile[32][33];
+    const int tid = threadIdx.x;
+    const int r0 = blockIdx.x * rpc, r1 = min(rows, r0 + rpc);
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int c0 = r0; c0 < r1; c0 += 32) {
+        __syncthreads();
+        for (int e = tid; e < 1024; e += kCqrThreads) {
+            const int rr = e & 31, col = e >> 5, r = c0 + rr;
+            tile[rr][col] = (r < r1 && col < b) ? P[r + static_cast<i64>(col) * ldp] : 0.0;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int e = tid + kCqrThreads * q, i = e & 31, j = e >> 5;
+            double a = acc[q];
+#pragma unroll 8
+            for (int rr = 0; rr < 32; ++rr) a = fma(tile[rr][i], tile[rr][j], a);
+            acc[q] = a;
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) part[static_cast<i64>(blockIdx.x) * 1024 + tid + kCqrThreads * q] = acc[q];
+}
+
+// One CTA of 1024 threads, thread = matrix entry (i, j): G = sum of the
+// partial Grams (fixed order, 8 interleaved partial sums); mode 1 adds the
+// shift coeff * trace(G), mode 2 requires ||G - I||_F <= 1/2; R = chol(G) by
+// 32 deferred-scaling elimination steps (one barrier each), Rinv by
+// Gauss-Jordan on [R | I] (32 steps), Rtot = R Rtot (first: Rtot = R).
+// Breakdown -> atomicMin(flag, tag).
+constexpr int kCholSmall = 1024;
+__global__ void __launch_bounds__(kCholSmall) cqr_chol32(int nparts, const double* part, int b, int mode, double coeff,
+                                                        double* Rinv, double* Rtot, int first, int* flag, int tag) {
+    __shared__ double G[32][33], X[32][33], Rt[32][33];
+    __shared__ double red[32], pv[32];
+    __shared__ int bad;
+    const int e = threadIdx.x, i = e & 31, j = e >> 5, lane = e & 31, warp = e >> 5;
+    if (e == 0) bad = 0;
+    {
+        double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        int g = 0;
+        for (; g + 8 <= nparts; g += 8) {
+            double v[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) v[q] = part[static_cast<i64>(g + q) * 1024 + e];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) acc[q] += v[q];
+        }
+        for (int q = 0; g < nparts; ++g, ++q) acc[q] += part[static_cast<i64>(g) * 1024 + e];
+        const double sacc = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+        G[i][j] = (i < b && j < b) ? sacc : (i == j ? 1.0 : 0.0);
+        if (!first) Rt[i][j] = Rtot[e];
+    }
+    __syncthreads();
+    if (mode != 0) {
+        double v = 0.0;
+        if (i < b && j < b) {
+            if (mode == 1) v = (i == j) ? G[i][i] : 0.0;
+            else {
+                const double d = G[i][j] - (i == j ? 1.0 : 0.0);
+                v = d * d;
+            }
+        }
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) red[warp] = v;
+        __syncthreads();
+        double tot = 0.0;
+        for (int w = 0; w < 32; ++w) tot += red[w];
+        if (mode == 1 && i == j && i < b) G[i][i] += coeff * tot;
+        if (mode == 2 && e == 0 && !(tot <= 0.25)) bad = 1;
+        __syncthreads();
+    }
+    // Cholesky with deferred scaling: step k, G(i, j) -= G(k, i) G(k, j) / g_kk for k < i <= j
+    for (int k = 0; k < 32; ++k) {
+        double piv = G[k][k];
+        if (!(piv > 0.0) || !isfinite(piv)) {
+            if (e == 0) bad = 1;
+            piv = 1.0;
+        }
+        if (e == 0) pv[k] = piv;
+        const double upd = (i > k && j >= i) ? G[k][i] * G[k][j] / piv : 0.0;
+        __syncthreads();
+        if (i > k && j >= i) G[i][j] -= upd;
+        __syncthreads();
+    }
+    // R(i, j) = G(i, j) / sqrt(g_ii) (j > i), R(i, i) = sqrt(g_ii)
+    {
+        const double r = sqrt(pv[i]);
+        const double v = (j > i) ? G[i][j] / r : (j == i ? r : 0.0);
+        __syncthreads();
+        G[i][j] = v;
+        X[i][j] = (i == j) ? 1.0 : 0.0;
+        __syncthreads();
+    }
+    // Gauss-Jordan on the upper triangle, last column first: X <- R^{-1}
+    for (int k = 31; k >= 0; --k) {
+        const double rkk = G[k][k];
+        const double xk = X[k][j] / rkk;  // row k scaled (read before the barrier)
+        const double rik = G[i][k];
+        __syncthreads();
+        if (i == k) X[k][j] = xk;
+        else if (i < k) X[i][j] = fma(-rik, xk, X[i][j]);
+        __syncthreads();
+    }
+    Rinv[e] = i <= j ? X[i][j] : 0.0;
+    double v;
+    if (first) {
+        v = i <= j ? G[i][j] : 0.0;
+    } else {  // Rtot <- R Rtot (both upper)
+        v = 0.0;
+        for (int q = i; q <= j; ++q) v = fma(G[i][q], Rt[q][j], v);
+        if (i > j) v = 0.0;
+    }
+    Rtot[e] = v;
+    if (e == 0 && bad) atomicMin(flag, tag);
+}
+
+// Q = P M for M upper triangular 32 x 32 (column-major), one row per thread
+// (P and Q may alias: a thread reads its whole row before writing it).
+__global__ void __launch_bounds__(kCqrThreads) cqr_apply(int rows, int b, const double* P, i64 ldp, const double* M,
+                                                        double* Q, i64 ldq) {
+    __shared__ double Ms[32][33];
+    for (int e = threadIdx.x; e < 1024; e += kCqrThreads) Ms[e & 31][e >> 5] = M[e];
+    __syncthreads();
+    for (int r = blockIdx.x * kCqrThreads + threadIdx.x; r < rows; r += gridDim.x * kCqrThreads) {
+        double x[32];
+#pragma unroll
+        for (int k = 0; k < 32; ++k) x[k] = k < b ? P[r + static_cast<i64>(k) * ldp] : 0.0;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+            double sacc = 0.0;
+#pragma unroll
+            for (int k = 0; k <= j; ++k) sacc = fma(x[k], Ms[k][j], sacc);
+            if (j < b) Q[r + static_cast<i64>(j) * ldq] = sacc;
+        }
+    }
+}
+
+// Householder reconstruction (one CTA of 1024 threads, thread = entry (i, j)):
+// from Q_1 (top b x b of Q) and the Cholesky-QR factor Rtot -> T (ld 32,
+// upper), the top block of V (unit lower), R = S Rtot into the panel's top
+// block (ld ldr), Uinv = U^{-1}, tau = diag(T).
+__global__ void __launch_bounds__(kCholSmall) cqr_hr(int b, const double* Q, i64 ldq, const double* Rtot, double* T,
+                                                    double* V, i64 ldv, double* Rout, i64 ldr, double* Uinv, double* tau) {
+    __shared__ double A[32][33], Li[32][33], Ui[32][33];
+    __shared__ double s[32];
+    const int e = threadIdx.x, i = e & 31, j = e >> 5;
+    A[i][j] = (i < b && j < b) ? Q[i + static_cast<i64>(j) * ldq] : (i == j ? 1.0 : 0.0);
+    Li[i][j] = (i == j) ? 1.0 : 0.0;
+    Ui[i][j] = (i == j) ? 1.0 : 0.0;
+    __syncthreads();
+    // LU without pivoting of Q_1 - S, s_k = -sign(running pivot): step k (one barrier pair)
+    for (int k = 0; k < 32; ++k) {
+        const double akk = A[k][k];
+        const double sk = k < b ? (akk >= 0.0 ? -1.0 : 1.0) : 0.0;
+        const double ukk = akk - sk;  // |ukk| >= 1 for k < b
+        const double lik = (i > k) ? A[i][k] / ukk : 0.0;
+        const double akj = A[k][j];
+        __syncthreads();
+        if (e == 0) s[k] = sk;
+        if (i == k && j == k) A[k][k] = ukk;
+        if (i > k && j == k) A[i][k] = lik;
+        if (i > k && j > k) A[i][j] = fma(-lik, akj, A[i][j]);
+        __syncthreads();
+    }
+    // Li = L^{-1} (unit lower; forward Gauss-Jordan), Ui = U^{-1} (upper; backward)
+    for (int k = 0; k < 32; ++k) {
+        const double lik = (i > k) ? A[i][k] : 0.0;
+        const double xk = Li[k][j];
+        __syncthreads();
+        if (i > k) Li[i][j] = fma(-lik, xk, Li[i][j]);
+        __syncthreads();
+    }
+    for (int k = 31; k >= 0; --k) {
+        const double ukk = A[k][k];
+        const double xk = Ui[k][j] / ukk;
+        const double uik = A[i][k];
+        __syncthreads();
+        if (i == k) Ui[k][j] = xk;
+        else if (i < k) Ui[i][j] = fma(-uik, xk, Ui[i][j]);
+        __syncthreads();
+    }
+    // T = -U S L^{-T}: T(i, j) = -sum_{i <= k <= j} U(i, k) s_k Li(j, k)
+    double t = 0.0;
+    if (i <= j) {
+        for (int k = i; k <= j; ++k) t = fma(A[i][k] * s[k], Li[j][k], t);
+        t = -t;
+    }
+    if (i < b && j < b) {
+        T[i + 32 * j] = t;
+        if (i == j) tau[j] = t;
+        V[i + static_cast<i64>(j) * ldv] = i > j ? A[i][j] : (i == j ? 1.0 : 0.0);
+        if (i <= j) Rout[i + static_cast<i64>(j) * ldr] = s[i] * Rtot[i + 32 * j];
+    }
+    Uinv[e] = i <= j ? Ui[i][j] : 0.0;
+}
+
 }  // namespace
 
 // Passes: two shifted (each lowers kappa by ~sqrt(11 (mn + n^2) u), enough for
@@ -563,6 +777,42 @@ void thin_qr_cholesky(Ctx& c, i64 m, i64 n, const double* A, i64 lda, double* Q,
             acc = dst;
         }
     }
+}
+
+
+// K4d host: factor the rows x b panel P (ld ldp, b <= 32, rows >= 2b) into the
+// blocked QR's (R in P's top block, V, T, tau); breakdown -> the context's QR
+// flag with `tag` (the caller speculates, see with_qr_speculation).
+void cqr_panel(Ctx& c, i64 rows, i64 b, double* P, i64 ldp, double* V, i64 ldv, double* T, double* tau, int tag) {
+    if (b < 1 || b > 32 || rows < 2 * b) fail(Errc::InvalidArgument, "cqr_panel: shape outside the panel path");
+    const i64 G = std::max<i64>(1, std::min<i64>(c.sm_count, (rows + 255) / 256));
+    const i64 rpc = ((rows + G - 1) / G + 31) / 32 * 32;
+    const double u = DBL_EPSILON / 2;
+    const double coeff = 11.0 * (static_cast<double>(rows) * b + static_cast<double>(b) * (b + 1)) * u;
+    DBuf part(c, static_cast<std::size_t>(G * 1024)), Qp(c, static_cast<std::size_t>(rows * 32)),
+        mats(c, static_cast<std::size_t>(3 * 1024));
+    double* Rinv = mats.p;
+    double* Rtot = mats.p + 1024;
+    double* Uinv = mats.p + 2048;
+    const unsigned agrid = static_cast<unsigned>(std::min<i64>(4 * c.sm_count, (rows + kCqrThreads - 1) / kCqrThreads));
+    int* flag = c.qr_flag_dev();
+    for (int pass = 0; pass < 3; ++pass) {
+        const double* src = pass == 0 ? P : Qp.p;
+        const i64 lds = pass == 0 ? ldp : rows;
+        cqr_gram_partial<<<static_cast<unsigned>(G), kCqrThreads, 0, c.stream>>>(static_cast<int>(rows), static_cast<int>(b),
+                                                                             src, lds, static_cast<int>(rpc), part.p);
+        cqr_chol32<<<1, kCholSmall, 0, c.stream>>>(static_cast<int>(G), part.p, static_cast<int>(b),
+                                                     pass == 0 ? 1 : (pass == 2 ? 2 : 0), coeff, Rinv, Rtot,
+                                                     pass == 0 ? 1 : 0, flag, tag);
+        cqr_apply<<<agrid, kCqrThreads, 0, c.stream>>>(static_cast<int>(rows), static_cast<int>(b), src, lds, Rinv, Qp.p,
+                                                        rows);
+        c.launched(3);
+    }
+    cqr_hr<<<1, kCholSmall, 0, c.stream>>>(static_cast<int>(b), Qp.p, rows, Rtot, T, V, ldv, P, ldp, Uinv, tau);
+    cqr_apply<<<agrid, kCqrThreads, 0, c.stream>>>(static_cast<int>(rows - b), static_cast<int>(b), Qp.p + b, rows, Uinv,
+                                                    V + b, ldv);
+    TTR_CUDA(cudaGetLastError());
+    c.launched(2);
 }
 
 }  // namespace ttr

@@ -398,6 +398,9 @@ void with_qr_speculation(Ctx& c, const std::function<void()>& body) {
         body();
         if (!c.qr_spec_used) break;
         const int failed = c.qr_flag_read();
+        static const bool trace = std::getenv("TTR_QR_SPEC_TRACE") != nullptr;  // diagnostics
+        if (trace) std::fprintf(stderr, "qr speculation: first broken mode %d (hh_from %lld)\n", failed,
+                                static_cast<long long>(c.qr_hh_from));
         if (failed < 0) break;
         // modes before `failed` reproduce bitwise on the rerun; from there on
         // the sweep takes the Householder QR (strictly decreasing: terminates)
@@ -481,7 +484,15 @@ void rand_orth_sweep(Ctx& c, const TTDev& t, i64 width, const std::vector<const 
                 thin_qr_cholesky(c, rows, l, S.p, rows, out->core(k - 1), rows, nullptr, 1, static_cast<int>(k));
                 c.qr_spec_used = true;
             } else {
-                thin_qr(c, rows, l, S.p, rows, out->core(k - 1), rows, nullptr, 1);
+                // the blocked Householder QR may take Cholesky-QR panels (K4d) under this mode's tag
+                c.qr_tag = (c.qr_spec && k < c.qr_hh_from) ? static_cast<int>(k) : -1;
+                try {
+                    thin_qr(c, rows, l, S.p, rows, out->core(k - 1), rows, nullptr, 1);
+                } catch (...) {
+                    c.qr_tag = -1;
+                    throw;
+                }
+                c.qr_tag = -1;
             }
         }
         if (c.io) c.io->out_done(c.stream, static_cast<std::size_t>(k - 1));  // output core k-1 final: D2H
@@ -678,7 +689,11 @@ bool Plan::capture(bool spec, cudaGraph_t& g_out, cudaGraphExec_t& e_out) {
 void Plan::execute() {
     TTR_CUDA(cudaGraphLaunch(exec, c.stream));
     std::uint64_t launches = launches_per_run;
-    if (speculative && c.qr_flag_read() >= 0) {
+    const int failed = speculative ? c.qr_flag_read() : -1;
+    static const bool trace = std::getenv("TTR_QR_SPEC_TRACE") != nullptr;  // diagnostics
+    if (trace && speculative) std::fprintf(stderr, "plan replay: first broken mode %d (hh_from %lld)\n", failed,
+                                           static_cast<long long>(hh_from));
+    if (failed >= 0) {
         if (!exec_safe) capture(false, graph_safe, exec_safe);
         TTR_CUDA(cudaGraphLaunch(exec_safe, c.stream));
         launches += launches_per_run;

@@ -160,6 +160,40 @@ print("ok")
 """
 
 
+_CQR_PANEL_SCRIPT = r"""
+import sys, numpy as np
+sys.path[:0] = [sys.argv[1], sys.argv[2], sys.argv[3]]
+import paper_2511_03598_b200 as P, py_oracle as O
+from helpers import rel_err_vs_ref, to_device
+# mode-2 sketch 7,680 x 120 (> one cluster of rows: the grid-panel blocked QR)
+x = O.two_part_tt(4, 64, 100, 140, 1e-8, 3101)
+y = P.round_fixed_krp(to_device(x), [120] * 3, 7, rng=P.RNG_PHILOX)
+ref = O.round_fixed_krp(x, [120] * 3, 7, rng=O.PHILOX)
+assert y.ranks() == ref.ranks, (y.ranks(), ref.ranks)
+assert rel_err_vs_ref(ref, y) <= 1e-10
+t = to_device(x)
+plan = P.FixedKrpPlan(t, [120] * 3, 7)
+plan.execute()
+assert np.array_equal(plan.output.flat(), y.flat())
+plan.close()
+print("ok")
+"""
+
+
+def test_fixed_krp_cholesky_qr_panels_opt_in(P, O):
+    """The opt-in Cholesky-QR panels with Householder reconstruction (TTR_QR_CQR=1,
+    K4d) in the blocked grid QR of the sweep: oracle parity, plan == eager."""
+    import os
+    import subprocess
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    root = os.path.dirname(here)
+    env = dict(os.environ, TTR_QR_CQR="1")
+    r = subprocess.run([sys.executable, "-c", _CQR_PANEL_SCRIPT, root, os.path.join(root, "oracle"), here],
+                       env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
+
+
 def test_fixed_krp_cholesky_sweep_and_fallback(P, O):
     """The opt-in Cholesky-QR sweep (TTR_QR_CHOL=1, read once per process, so
     in a subprocess): oracle parity, and exactly rank-deficient sketches either
