@@ -39,6 +39,8 @@ import statistics
 import subprocess
 import sys
 import threading
+
+import numpy as np
 import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
@@ -516,8 +518,9 @@ ADAPTIVE = {
 
 
 def run_adaptive(args, world, rank, local):
-    """Configs 2 and 4: adaptive-rank KRP rounding (host-driven growth decisions, eager API).
-    One step = one round_adaptive_krp; independent tensor per rank (weak scaling)."""
+    """Configs 2 and 4: adaptive-rank KRP rounding. One step = one round_adaptive_krp through its
+    CUDA-graph plan (the eager call's time is reported beside it); independent tensor per rank
+    (weak scaling)."""
     import torch
     import paper_2511_03598_b200 as P
     if world > 1:
@@ -542,25 +545,40 @@ def run_adaptive(args, world, rank, local):
     launches_per_step = ctx.kernel_launches() - l0
     out_ranks = out.ranks()
     del out
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    # the eager call (host-side growth decisions), timed for reference
     for _ in range(args.warmup):
         del_ = P.round_adaptive_krp(y, cfgA)
         del del_
     torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(args.steps):
+        o = P.round_adaptive_krp(y, cfgA)
+        del o
+    e1.record(stream)
+    torch.cuda.synchronize()
+    eager_ms = e0.elapsed_time(e1) / args.steps
+    # the timed API: the CUDA-graph plan (ttr_plan_adaptive_krp) — the recorded growth
+    # decisions replayed by one graph launch and re-checked on the device per step
+    plan = P.AdaptiveKrpPlan(y, cfgA)
+    for _ in range(args.warmup):
+        plan.execute()
+    torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
     l0 = ctx.kernel_launches()
     with ClockSampler(local) as clk:
         e0.record(stream)
         for _ in range(args.steps):
-            o = P.round_adaptive_krp(y, cfgA)
-            del o
+            plan.execute()
         e1.record(stream)
         torch.cuda.synchronize()
     launches = ctx.kernel_launches() - l0
     ms = e0.elapsed_time(e1) / args.steps
+    plan_equal = bool(np.array_equal(plan.output.flat(), P.round_adaptive_krp(y, cfgA).flat()))
+    rerecords = plan.rerecords()
     if world > 1:
         t = torch.tensor([ms], device="cuda")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
@@ -604,7 +622,8 @@ def run_adaptive(args, world, rank, local):
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             P.lib().ttr_tt_copy_from_host(ctx._h, y._h, C.c_void_p(host_in.data_ptr()))
-            o = P.round_adaptive_krp(y, cfgA)
+            plan.execute()
+            o = plan.output
             _, _, ot = o.shape()
             host_out = torch.empty(ot, dtype=torch.float64, pin_memory=True) if it == 0 else host_out
             P.lib().ttr_tt_download(ctx._h, o._h, C.c_void_p(host_out.data_ptr()))
@@ -620,8 +639,8 @@ def run_adaptive(args, world, rank, local):
             e2e_ms = float(t.item())
         e2e = {"value": flops * world / (e2e_ms * 1e-3) / 1e12, "unit": "TFLOP/s", "ms_per_step": e2e_ms,
                "h2d_bytes_per_step": 8 * total, "d2h_bytes_per_step": out_bytes,
-               "timing": "host wall clock: pinned H2D of the cores (ttr_tt_copy_from_host) + round_adaptive_krp + "
-                         "D2H of the result (ttr_tt_download, synchronising)"}
+               "timing": "host wall clock: pinned H2D of the cores (ttr_tt_copy_from_host) + the adaptive plan's "
+                         "execute (graph replay + device-side decision check) + D2H of the result (ttr_tt_download)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -642,7 +661,11 @@ def run_adaptive(args, world, rank, local):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (device-generated input)",
             "config": {"workload": a["desc"], "output_ranks": out_ranks, "flops_per_step": flops,
-                       "input_gb": 8 * total / 1e9, "api": "round_adaptive_krp (eager; host-side growth decisions)",
+                       "input_gb": 8 * total / 1e9,
+                       "api": "AdaptiveKrpPlan (ttr_plan_adaptive_krp: CUDA graph of round_adaptive_krp with the "
+                              "recorded growth decisions, each re-checked on the device) replayed per step",
+                       "eager_ms_per_step": eager_ms, "plan_bitwise_equal_eager": plan_equal,
+                       "plan_rerecords": rerecords,
                        "l2": "inputs exceed L2" if 8 * total > 126e6 else "input fits L2 (126 MB); not flushed",
                        "parallelism": f"{world} independent tensors"},
             "roofline": roof, "clocks": clk.summary(), "gpu_launches": launches,

@@ -199,6 +199,15 @@ ttr_status ttr_plan_destroy(ttr_plan* plan);
 
 ttr_status ttr_round_adaptive_krp(ttr_ctx* ctx, const ttr_tt* tt, const ttr_adaptive_cfg* cfg,
                                   ttr_tt** out);
+/* CUDA-graph plan of round_adaptive_krp (Philox generator only): an eager run
+ * records the growth decisions, the round is captured with them (no host round
+ * trip per growth test) and every decision is re-checked on the device during
+ * ttr_plan_execute; when the input's contents give another decision anywhere,
+ * execute redoes the call eagerly and re-records the plan (the output may then
+ * change shape: re-read it with ttr_plan_output). execute synchronises. */
+ttr_status ttr_plan_adaptive_krp(ttr_ctx* ctx, const ttr_tt* tt, const ttr_adaptive_cfg* cfg, ttr_plan** out);
+/* How often an adaptive plan had to re-record (0 for fixed-rank plans). */
+ttr_status ttr_plan_rerecords(const ttr_plan* plan, int64_t* count);
 /* Adaptive rounding of sum(terms) WITHOUT forming the formal sum
  * (round_sum_adaptive_krp, sum_round.hpp:29 / sum_round.cpp:52-173): one
  * shared factor draw, one KRP sketch per term; eps > 0, f_inc in (0,1). An

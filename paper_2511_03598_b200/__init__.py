@@ -470,6 +470,54 @@ class AdaptiveConfig:
     rng: int = RNG_PHILOX
 
 
+def _adaptive_cfg(cfg: AdaptiveConfig):
+    c = _AdaptiveCfg()
+    c.tolerance, c.f_init, c.f_inc, c.seed = cfg.tolerance, cfg.f_init, cfg.f_inc, cfg.seed
+    c.has_known_norm = 1 if cfg.known_norm is not None else 0
+    c.known_norm = cfg.known_norm or 0.0
+    cap = _i64(cfg.max_rank_cap) if cfg.max_rank_cap is not None else None
+    c.max_rank_cap = C.cast(cap, C.POINTER(C.c_int64)) if cap is not None else None
+    c.max_rank_cap_len = len(cfg.max_rank_cap) if cfg.max_rank_cap is not None else 0
+    c.rng_mode = cfg.rng
+    return c, cap
+
+
+class AdaptiveKrpPlan:
+    """CUDA-graph plan of round_adaptive_krp (ttr_plan_adaptive_krp): the growth
+    decisions of an eager run are replayed by the graph and re-checked on the
+    device; `execute()` re-records when the input's contents decide otherwise.
+    `output` re-reads the plan-owned result (its shape may change then)."""
+
+    def __init__(self, tt: TTTensor, cfg: AdaptiveConfig):
+        self.ctx = tt.ctx
+        self.input = tt
+        c, self._cap = _adaptive_cfg(cfg)
+        self._h = C.c_void_p()
+        _check(lib().ttr_plan_adaptive_krp(tt.ctx._h, tt._h, C.byref(c), C.byref(self._h)))
+
+    @property
+    def output(self) -> TTTensor:
+        out = C.c_void_p()
+        _check(lib().ttr_plan_output(self._h, C.byref(out)))
+        return _BorrowedTT(out, self.ctx, self)
+
+    def execute(self):
+        _check(lib().ttr_plan_execute(self._h))
+
+    def rerecords(self) -> int:
+        v = C.c_int64()
+        _check(lib().ttr_plan_rerecords(self._h, C.byref(v)))
+        return v.value
+
+    def close(self):
+        if getattr(self, "_h", None) and self._h.value and _lib is not None and _ctx_alive(self):
+            _lib.ttr_plan_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        self.close()
+
+
 def round_adaptive_krp(tt: TTTensor, cfg: AdaptiveConfig) -> TTTensor:
     c = _AdaptiveCfg()
     c.tolerance, c.f_init, c.f_inc, c.seed = cfg.tolerance, cfg.f_init, cfg.f_inc, cfg.seed

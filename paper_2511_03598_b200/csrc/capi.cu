@@ -352,8 +352,16 @@ ttr_status ttr_plan_fixed_krp_host(ttr_ctx* ctx, ttr_tt* tt, const int64_t* rank
 
 ttr_status ttr_plan_execute(ttr_plan* plan) {
     return guard([&] {
-        need(plan && plan->plan, "null plan");
-        plan->plan->execute();
+        need(plan && (plan->plan || plan->aplan), "null plan");
+        if (plan->aplan) plan->aplan->execute();
+        else plan->plan->execute();
+    });
+}
+
+ttr_status ttr_plan_rerecords(const ttr_plan* plan, int64_t* count) {
+    return guard([&] {
+        need(plan && count, "null argument");
+        *count = plan->aplan ? plan->aplan->rerecords : 0;
     });
 }
 
@@ -368,8 +376,46 @@ ttr_status ttr_plan_destroy(ttr_plan* plan) {
     return guard([&] {
         if (!plan) return;
         cudaStreamSynchronize(plan->ctx->c.stream);
+        plan->aplan.reset();
         plan->plan.reset();
         delete plan;
+    });
+}
+
+static AdaptiveCfg adaptive_cfg_of(const ttr_tt* tt, const ttr_adaptive_cfg* cfg) {
+    need(cfg->rng_mode == TTR_RNG_PHILOX || cfg->rng_mode == TTR_RNG_XOSHIRO, "unknown rng mode");
+    AdaptiveCfg a;
+    a.tolerance = cfg->tolerance;
+    a.f_init = cfg->f_init;
+    a.f_inc = cfg->f_inc;
+    a.seed = cfg->seed;
+    a.has_known_norm = cfg->has_known_norm != 0;
+    a.known_norm = cfg->known_norm;
+    if (cfg->max_rank_cap) {
+        if (cfg->max_rank_cap_len != tt->t->d() - 1) fail(Errc::InvalidRanks, "max_rank_cap needs d-1 entries");
+        for (int64_t k = 0; k < cfg->max_rank_cap_len; ++k)
+            if (cfg->max_rank_cap[k] < 1) fail(Errc::InvalidRanks, "rank caps must be >= 1");
+    }
+    a.max_rank_cap = cfg->max_rank_cap;
+    a.rng_mode = cfg->rng_mode;
+    return a;
+}
+
+ttr_status ttr_plan_adaptive_krp(ttr_ctx* ctx, const ttr_tt* tt, const ttr_adaptive_cfg* cfg, ttr_plan** out) {
+    return guard_ctx(ctx, [&] {
+        check_same_ctx(ctx, tt);
+        need(cfg && out, "null argument");
+        AdaptiveCfg a = adaptive_cfg_of(tt, cfg);
+        if (!(a.tolerance > 0.0 && a.tolerance < 1.0)) fail(Errc::InvalidArgument, "adaptive tolerance must lie in (0,1)");
+        auto* p = new ttr_plan;
+        try {
+            p->aplan = std::make_unique<AdaptivePlan>(ctx->c, *tt->t, a, &p->out.t);
+        } catch (...) {
+            delete p;
+            throw;
+        }
+        p->ctx = ctx;
+        *out = p;
     });
 }
 

@@ -761,7 +761,27 @@ static i64 ceil_fraction(double f, i64 n) {  // round_rand.cpp:46-48
     return std::max<i64>(1, static_cast<i64>(std::ceil(f * static_cast<double>(n))));
 }
 
+namespace {
+// Device side of a replayed growth decision (AdaptivePlan): tau from the
+// initial sketch norm, and the check that the recorded decision is the one the
+// data gives (same IEEE operations as the host path, so the same bits).
+__global__ void adaptive_tau_kernel(const double* nrm2, double width, double tol, double sqrt_d1, double* tau) {
+    *tau = tol * (sqrt(*nrm2) / sqrt(width)) / sqrt_d1;
+}
+__global__ void adaptive_verify_kernel(const double* est2, double b_inc, const double* tau, int recorded_stop,
+                                       int* mismatch) {
+    const bool stop = sqrt(*est2) / sqrt(b_inc) <= *tau;
+    if (stop != (recorded_stop != 0)) *mismatch = 1;
+}
+}  // namespace
+
 std::unique_ptr<TTDev> round_adaptive_krp(Ctx& c, const TTDev& t, const AdaptiveCfg& cfg, std::vector<double>* trace) {
+    return round_adaptive_krp_impl(c, t, cfg, trace, nullptr, nullptr);
+}
+
+std::unique_ptr<TTDev> round_adaptive_krp_impl(Ctx& c, const TTDev& t, const AdaptiveCfg& cfg,
+                                               std::vector<double>* trace, AdaptiveTape* tape, TTDev* out_into) {
+    const bool replay = tape != nullptr && tape->replay;
     if (!(cfg.tolerance > 0.0 && cfg.tolerance < 1.0)) fail(Errc::InvalidArgument, "adaptive tolerance must lie in (0,1)");
     if (!(cfg.f_init > 0.0 && cfg.f_init < 1.0) || !(cfg.f_inc > 0.0 && cfg.f_inc < 1.0))
         fail(Errc::InvalidArgument, "block fractions must lie in (0,1)");
@@ -779,16 +799,26 @@ std::unique_ptr<TTDev> round_adaptive_krp(Ctx& c, const TTDev& t, const Adaptive
     Sketch sk(c, t, cap, cfg.rng_mode, cfg.seed);
     sk.append(2, width);
 
-    double nrm;
+    double nrm = 0.0, tau = 0.0;
     if (cfg.has_known_norm) {
         nrm = cfg.known_norm;
+        tau = cfg.tolerance * nrm / std::sqrt(static_cast<double>(d - 1));
+        if (replay) fill(c, tape->d_tau, 1, tau);
     } else {  // reuse the initial contraction (round_rand.cpp:113-116)
         const i64 rows = t.n[0], cols = t.r[1];
         DBuf S0(c, static_cast<std::size_t>(rows * width));
         gemm(c, false, rows, width, cols, 1.0, t.core(0), rows, sk.W[2].p, sk.ldw[2], 0.0, S0.p, rows);
-        nrm = frob_norm(c, rows, width, S0.p, rows) / std::sqrt(static_cast<double>(width));
+        if (replay) {  // tau stays on the device
+            frob_norm_sq(c, rows, width, S0.p, rows, tape->d_scratch);
+            adaptive_tau_kernel<<<1, 1, 0, c.stream>>>(tape->d_scratch, static_cast<double>(width), cfg.tolerance,
+                                                       std::sqrt(static_cast<double>(d - 1)), tape->d_tau);
+            TTR_CUDA(cudaGetLastError());
+            c.launched();
+        } else {
+            nrm = frob_norm(c, rows, width, S0.p, rows) / std::sqrt(static_cast<double>(width));
+            tau = cfg.tolerance * nrm / std::sqrt(static_cast<double>(d - 1));
+        }
     }
-    const double tau = cfg.tolerance * nrm / std::sqrt(static_cast<double>(d - 1));
     if (trace) trace->clear();
 
     // device buffers sized for the largest mode
@@ -841,9 +871,22 @@ std::unique_ptr<TTDev> round_adaptive_krp(Ctx& c, const TTDev& t, const Adaptive
             // S -= Q (Q^T S)
             gemm(c, true, q, b_inc, rows, 1.0, Qb.p, rows, Sb.p, rows, 0.0, P.p, q);
             gemm(c, false, rows, b_inc, q, -1.0, Qb.p, rows, P.p, q, 1.0, Sb.p, rows);
-            const double est = frob_norm(c, rows, b_inc, Sb.p, rows) / std::sqrt(static_cast<double>(b_inc));
-            if (trace) trace->push_back(est);
-            if (est <= tau) break;
+            bool stop;
+            if (replay) {  // the recorded decision, checked against the data on the device
+                if (tape->pos >= tape->stops.size()) fail(Errc::InvalidArgument, "adaptive plan: decision tape exhausted");
+                stop = tape->stops[tape->pos++] != 0;
+                frob_norm_sq(c, rows, b_inc, Sb.p, rows, tape->d_scratch + 1);
+                adaptive_verify_kernel<<<1, 1, 0, c.stream>>>(tape->d_scratch + 1, static_cast<double>(b_inc), tape->d_tau,
+                                                              stop ? 1 : 0, tape->d_mismatch);
+                TTR_CUDA(cudaGetLastError());
+                c.launched();
+            } else {
+                const double est = frob_norm(c, rows, b_inc, Sb.p, rows) / std::sqrt(static_cast<double>(b_inc));
+                if (trace) trace->push_back(est);
+                stop = est <= tau;
+                if (tape) tape->stops.push_back(stop ? 1 : 0);
+            }
+            if (stop) break;
             const i64 grow = std::min(b_inc, rbar - q);
             growth_basis(c, rows, q, grow, Qb.p, Sb.p, Qn.p, P.p);
             q += grow;
@@ -862,11 +905,107 @@ std::unique_ptr<TTDev> round_adaptive_krp(Ctx& c, const TTDev& t, const Adaptive
     }
     std::vector<i64> r(d + 1, 1);
     for (i64 k = 1; k < d; ++k) r[k] = shapes[k - 1][2];
-    auto out = std::make_unique<TTDev>(c, t.n, r);
+    std::unique_ptr<TTDev> made;
+    TTDev* out = out_into;
+    if (out) {
+        if (out->r != r || out->n != t.n) fail(Errc::InvalidArgument, "adaptive plan: output shape changed");
+    } else {
+        made = std::make_unique<TTDev>(c, t.n, r);
+        out = made.get();
+    }
     for (i64 k = 0; k < d - 1; ++k)
         copy_matrix(c, out->core_size(k), 1, out_cores[k].p, out->core_size(k), out->core(k), out->core_size(k));
     copy_matrix(c, out->core_size(d - 1), 1, cur.p, out->core_size(d - 1), out->core(d - 1), out->core_size(d - 1));
-    return out;
+    return made;
+}
+
+// ---------------------------------------------------------------------------
+// CUDA-graph plan of round_adaptive_krp: an eager run records the growth
+// decisions; the round is captured with those decisions (no host round trip
+// per growth test) and every decision re-checked on the device; a replay whose
+// data gives another decision anywhere sets a flag, read once after the graph,
+// and the call is redone eagerly (and the plan re-recorded).
+AdaptivePlan::AdaptivePlan(Ctx& cc, const TTDev& in_, const AdaptiveCfg& cfg_, std::unique_ptr<TTDev>* slot)
+    : c(cc), in(in_), cfg(cfg_), out_slot(slot) {
+    if (cfg.rng_mode != TTR_RNG_PHILOX) fail(Errc::InvalidArgument, "plans need the device (Philox) generator");
+    if (cfg.max_rank_cap) {
+        caps.assign(cfg.max_rank_cap, cfg.max_rank_cap + (in.d() - 1));
+        cfg.max_rank_cap = caps.data();
+    }
+    dev = DBuf(c, 4);
+    tape.d_tau = dev.p;
+    tape.d_scratch = dev.p + 1;  // [2]: nrm^2, est^2
+    tape.d_mismatch = reinterpret_cast<int*>(dev.p + 3);
+    rebuild();
+}
+
+void AdaptivePlan::rebuild() {
+    if (exec) cudaGraphExecDestroy(exec);
+    if (graph) cudaGraphDestroy(graph);
+    exec = nullptr;
+    graph = nullptr;
+    tape = AdaptiveTape{false, {}, 0, tape.d_tau, tape.d_scratch, tape.d_mismatch};
+    *out_slot = round_adaptive_krp_impl(c, in, cfg, nullptr, &tape, nullptr);  // record
+    TTR_CUDA(cudaStreamSynchronize(c.stream));
+    const bool timing = c.timing;
+    c.timing = false;
+    const Counts saved = c.counts;
+    const std::uint64_t l0 = c.launches;
+    if (!counted) {
+        ++c.live_plans;  // the captured split-K scratch is never freed under the graph
+        counted = true;
+    }
+    tape.replay = true;
+    tape.pos = 0;
+    TTR_CUDA(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal));
+    try {
+        TTR_CUDA(cudaMemsetAsync(tape.d_mismatch, 0, sizeof(int), c.stream));
+        round_adaptive_krp_impl(c, in, cfg, nullptr, &tape, out_slot->get());
+        if (tape.pos != tape.stops.size()) fail(Errc::InvalidArgument, "adaptive plan: decision tape not consumed");
+    } catch (...) {
+        cudaGraph_t g;
+        cudaStreamEndCapture(c.stream, &g);
+        if (g) cudaGraphDestroy(g);
+        c.timing = timing;
+        c.counts = saved;
+        c.launches = l0;
+        throw;
+    }
+    TTR_CUDA(cudaStreamEndCapture(c.stream, &graph));
+    launches_per_run = c.launches - l0;
+    flops = c.counts;
+    flops.gemm -= saved.gemm;
+    flops.qr -= saved.qr;
+    flops.svd -= saved.svd;
+    flops.sketch -= saved.sketch;
+    flops.rng -= saved.rng;
+    c.counts = saved;
+    c.launches = l0;
+    c.timing = timing;
+    TTR_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+}
+
+void AdaptivePlan::execute() {
+    TTR_CUDA(cudaGraphLaunch(exec, c.stream));
+    int* hm = reinterpret_cast<int*>(c.host_scalars + 12);
+    TTR_CUDA(cudaMemcpyAsync(hm, tape.d_mismatch, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+    TTR_CUDA(cudaStreamSynchronize(c.stream));
+    c.counts.gemm += flops.gemm;
+    c.counts.qr += flops.qr;
+    c.counts.svd += flops.svd;
+    c.counts.sketch += flops.sketch;
+    c.counts.rng += flops.rng;
+    c.launched(static_cast<int>(launches_per_run));
+    if (*hm != 0) {  // another decision somewhere: redo eagerly (record) and re-capture
+        ++rerecords;
+        rebuild();
+    }
+}
+
+AdaptivePlan::~AdaptivePlan() {
+    if (exec) cudaGraphExecDestroy(exec);
+    if (graph) cudaGraphDestroy(graph);
+    if (counted && --c.live_plans == 0) c.release_retired();
 }
 
 }  // namespace ttr

@@ -118,6 +118,40 @@ struct Plan {
 };
 
 std::unique_ptr<TTDev> round_adaptive_krp(Ctx& c, const TTDev& t, const AdaptiveCfg& cfg, std::vector<double>* trace);
+
+// Growth decisions of one adaptive round: recorded by an eager run, replayed
+// (and verified on the device) by a captured one (AdaptivePlan).
+struct AdaptiveTape {
+    bool replay = false;
+    std::vector<char> stops;  // one per growth test: 1 = the residual estimate met tau
+    std::size_t pos = 0;
+    double* d_tau = nullptr;
+    double* d_scratch = nullptr;  // [2]
+    int* d_mismatch = nullptr;
+};
+// round_adaptive_krp with an optional decision tape and output tensor (the
+// plan's replay writes into the recorded run's output; returns null then)
+std::unique_ptr<TTDev> round_adaptive_krp_impl(Ctx& c, const TTDev& t, const AdaptiveCfg& cfg,
+                                               std::vector<double>* trace, AdaptiveTape* tape, TTDev* out_into);
+struct AdaptivePlan {
+    Ctx& c;
+    const TTDev& in;
+    AdaptiveCfg cfg;
+    std::vector<i64> caps;
+    std::unique_ptr<TTDev>* out_slot;  // the caller-visible output (replaced when the plan re-records)
+    AdaptiveTape tape;
+    DBuf dev;
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    std::uint64_t launches_per_run = 0;
+    Counts flops;
+    bool counted = false;
+    int rerecords = 0;
+    AdaptivePlan(Ctx& c, const TTDev& in, const AdaptiveCfg& cfg, std::unique_ptr<TTDev>* out_slot);
+    ~AdaptivePlan();
+    void rebuild();
+    void execute();
+};
 // round_rand.cpp:66-78 — Rand-Orth with a Gaussian TT sketch (reference xoshiro stream for R)
 std::unique_ptr<TTDev> round_rand_orth_tt(Ctx& c, const TTDev& t, const std::vector<i64>& target_ranks,
                                           std::uint64_t seed, int rng_mode);
@@ -150,6 +184,7 @@ struct ttr_batch {
 };
 struct ttr_plan {
     std::unique_ptr<ttr::Plan> plan;
+    std::unique_ptr<ttr::AdaptivePlan> aplan;
     ttr_tt out;
     ttr_ctx* ctx = nullptr;
 };

@@ -1225,3 +1225,32 @@ def test_batched_fused_qr_epilogue_opt_in(P, O):
     r = subprocess.run([sys.executable, "-c", _LR_QR_SCRIPT, root, os.path.join(root, "oracle"), here],
                        env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
+
+
+
+def test_adaptive_plan_replays_and_rerecords(P, O):
+    """ttr_plan_adaptive_krp: the graph replay of the recorded growth decisions is
+    bitwise the eager call; refilled with data that decides differently, the plan
+    notices on the device, redoes the call and re-records (output = eager on the
+    new data, identical ranks to the oracle)."""
+    x1 = O.two_part_tt(6, 16, 6, 30, 1e-6, 3301)
+    x2 = O.two_part_tt(6, 16, 10, 26, 1e-3, 3302)  # same formal ranks, other decisions
+    cfg = P.AdaptiveConfig(tolerance=1e-4, f_init=0.1, f_inc=0.05, seed=7)
+    t = to_device(x1)
+    plan = P.AdaptiveKrpPlan(t, cfg)
+    eager = P.round_adaptive_krp(to_device(x1), cfg)
+    for _ in range(2):
+        plan.execute()
+        assert np.array_equal(plan.output.flat(), eager.flat())
+    assert plan.rerecords() == 0
+    P.copy_from_host(t, x2.flat())
+    plan.execute()
+    assert plan.rerecords() == 1
+    e2 = P.round_adaptive_krp(to_device(x2), cfg)
+    assert plan.output.ranks() == e2.ranks()
+    assert np.array_equal(plan.output.flat(), e2.flat())
+    ref = O.round_adaptive_krp(x2, tolerance=1e-4, f_init=0.1, f_inc=0.05, seed=7, rng=O.PHILOX)
+    assert e2.ranks() == ref.ranks
+    plan.execute()  # replays the re-recorded graph
+    assert plan.rerecords() == 1 and np.array_equal(plan.output.flat(), e2.flat())
+    plan.close()
