@@ -433,7 +433,11 @@ int jacobi_columns(Ctx& c, i64 M, i64 Nn, double* A, i64 lda) {
         // block Jacobi in one cluster: 2 blocks of b columns per CTA, b ~ 16
         // (one warp per pair), G <= 16 CTAs, blocks staged through registers
         const i64 max_smem = 227 * 1024 - 64;
-        G = std::max<i64>(1, (Nn + 31) / 32);
+        static const int g_env = [] {  // experiments: TTR_SVD_G = cluster size
+            const char* e = std::getenv("TTR_SVD_G");
+            return e ? std::atoi(e) : 0;
+        }();
+        G = g_env > 0 ? g_env : std::max<i64>(1, (Nn + 31) / 32);
         b = (Nn + 2 * G - 1) / (2 * G);
         auto fits = [&] { return 2 * b * M * 8 <= max_smem && b * M <= static_cast<i64>(kJStage) * kJw * 32; };
         auto fits4 = [&] { return 4 * b * M * 8 <= max_smem && (b * M) % 2 == 0; };
