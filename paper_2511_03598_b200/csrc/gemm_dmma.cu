@@ -690,7 +690,12 @@ void krp_step(Ctx& c, i64 r_left, i64 n, i64 r_right, i64 N, const double* X, co
             const char* e = std::getenv("TTR_KRP_SPLIT_CTAS");
             return e ? std::max(1, std::atoi(e)) : 2;  // 2: fewer split-K partials (5b sketch 47.2 -> 46.6 ms)
         }();
-        const i64 target = static_cast<i64>(waves) * c.sm_count;
+        i64 target = static_cast<i64>(waves) * c.sm_count;
+        // short contractions (config 3: 1,600 k-tiles over 4 row tiles): one CTA
+        // per SM when two would leave < 32 k-tiles per split (pipeline fill and
+        // the split-K reduction dominate): config-3 sketch 3.40 -> 3.26 ms; the
+        // 5b middle cores keep two (216 k-tiles per split)
+        if (waves == 2 && mtiles < target && total_kt / ((target + mtiles - 1) / mtiles) < 32) target = c.sm_count;
         if (mtiles < target && total_kt >= 8) {
             i64 s = (target + mtiles - 1) / mtiles;
             s = std::min<i64>(s, std::max(1, total_kt / 8));
