@@ -300,6 +300,17 @@ ttr_status ttr_thin_qr(ttr_ctx* ctx, int64_t m, int64_t n, const double* host_a,
  * call on the Householder path). No reference counterpart: a test hook. */
 ttr_status ttr_thin_qr_cholesky(ttr_ctx* ctx, int64_t m, int64_t n, const double* host_a, double* host_q,
                                 double* host_r, int* breakdown);
+/* Batched shifted CholeskyQR3 (qr_chol.cu K4e: the per-tensor QRs of the
+ * batched sweep) of `batch` host m x n matrices stored back to back (column-
+ * major, n <= 32, 2n <= m <= 2048): q likewise; flags[b] = 1 when matrix b broke
+ * down (its q is then unusable). No reference counterpart: a test hook. */
+ttr_status ttr_thin_qr_cholesky_batched(ttr_ctx* ctx, int64_t m, int64_t n, int64_t batch, const double* host_a,
+                                        double* host_q, int* host_flags);
+/* The same on strided device pointers (Q may alias A); d_flags[b] is set to 1
+ * on breakdown and never cleared (the caller zeroes it); no synchronisation. */
+ttr_status ttr_dev_thin_qr_cholesky_batched(ttr_ctx* ctx, int64_t m, int64_t n, int64_t batch, const double* dA,
+                                            int64_t lda, int64_t stride_a, double* dQ, int64_t ldq, int64_t stride_q,
+                                            int* d_flags);
 /* Device-pointer variants (column-major, caller-owned device memory, ordered
  * on the context stream, no synchronisation): thin QR (Q and/or R may be
  * NULL) and C = alpha op(A) B + beta C. */

@@ -746,6 +746,19 @@ def thin_qr_cholesky(a: np.ndarray, ctx: Optional[Context] = None):
     return q.reshape(n, m).T.copy(), r.reshape(n, n).T.copy(), bool(bd.value)
 
 
+def thin_qr_cholesky_batched(a: np.ndarray, ctx: Optional[Context] = None):
+    """Batched sCQR3 on the device (qr_chol.cu K4e) of a (batch, m, n) array:
+    (q of the same shape, per-matrix breakdown flags)."""
+    ctx = ctx or default_context()
+    bsz, m, n = a.shape
+    flat = np.ascontiguousarray(np.swapaxes(np.asarray(a, dtype=np.float64), 1, 2)).reshape(-1)
+    q = np.empty(bsz * m * n)
+    flags = np.zeros(bsz, dtype=np.int32)
+    _check(lib().ttr_thin_qr_cholesky_batched(ctx._h, C.c_int64(m), C.c_int64(n), C.c_int64(bsz), _dptr(flat),
+                                              _dptr(q), flags.ctypes.data_as(C.POINTER(C.c_int))))
+    return np.swapaxes(q.reshape(bsz, n, m), 1, 2).copy(), flags.astype(bool)
+
+
 def gemm(a: np.ndarray, b: np.ndarray, trans_a: bool = False, ctx: Optional[Context] = None) -> np.ndarray:
     ctx = ctx or default_context()
     if trans_a:

@@ -564,6 +564,35 @@ ttr_status ttr_dev_thin_qr_cholesky(ttr_ctx* ctx, int64_t m, int64_t n, const do
     });
 }
 
+ttr_status ttr_thin_qr_cholesky_batched(ttr_ctx* ctx, int64_t m, int64_t n, int64_t batch, const double* host_a,
+                                        double* host_q, int* host_flags) {
+    return guard_ctx(ctx, [&] {
+        need(ctx && host_a && host_q && host_flags && batch >= 0, "null argument");
+        need(cholqr_small_fits(m, n), "shape outside the batched Cholesky-QR path (n <= 32, 2n <= m <= 2048)");
+        if (batch == 0) return;
+        const std::size_t tot = static_cast<std::size_t>(m * n * batch);
+        DBuf a(ctx->c, tot), q(ctx->c, tot), f(ctx->c, static_cast<std::size_t>((batch + 1) / 2));
+        int* flags = reinterpret_cast<int*>(f.p);
+        TTR_CUDA(cudaMemcpyAsync(a.p, host_a, sizeof(double) * tot, cudaMemcpyHostToDevice, ctx->c.stream));
+        TTR_CUDA(cudaMemsetAsync(flags, 0, sizeof(int) * batch, ctx->c.stream));
+        cholqr_small_batched(ctx->c, m, n, a.p, m, m * n, q.p, m, m * n, batch, flags);
+        TTR_CUDA(cudaMemcpyAsync(host_q, q.p, sizeof(double) * tot, cudaMemcpyDeviceToHost, ctx->c.stream));
+        TTR_CUDA(cudaMemcpyAsync(host_flags, flags, sizeof(int) * batch, cudaMemcpyDeviceToHost, ctx->c.stream));
+        TTR_CUDA(cudaStreamSynchronize(ctx->c.stream));
+    });
+}
+
+ttr_status ttr_dev_thin_qr_cholesky_batched(ttr_ctx* ctx, int64_t m, int64_t n, int64_t batch, const double* dA,
+                                            int64_t lda, int64_t stride_a, double* dQ, int64_t ldq, int64_t stride_q,
+                                            int* d_flags) {
+    return guard_ctx(ctx, [&] {
+        need(ctx && dA && dQ && d_flags && batch >= 0, "null argument");
+        need(cholqr_small_fits(m, n) && lda >= m && ldq >= m && stride_a >= lda * n && stride_q >= ldq * n,
+             "bad shape");
+        if (batch > 0) cholqr_small_batched(ctx->c, m, n, dA, lda, stride_a, dQ, ldq, stride_q, batch, d_flags);
+    });
+}
+
 ttr_status ttr_dev_thin_qr(ttr_ctx* ctx, int64_t m, int64_t n, const double* dA, int64_t lda, double* dQ, int64_t ldq,
                            double* dR, int64_t ldr) {
     return guard_ctx(ctx, [&] {

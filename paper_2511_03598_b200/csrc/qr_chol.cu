@@ -722,6 +722,300 @@ __global__ void __launch_bounds__(kCholSmall) cqr_hr(int b, const double* Q, i64
     Uinv[e] = i <= j ? Ui[i][j] : 0.0;
 }
 
+// ---------------------------------------------------------------------------
+// K4e: batched CholeskyQR2 / shifted CholeskyQR3 of small tall matrices (config
+// 5a: 4096 x 5 QRs of 256/320 x 20 per call), one CTA per matrix, the matrix
+// column-major in shared memory (ld = 4 mod 16: the DMMA fragment loads below are
+// conflict-free) and updated in place. Per pass:
+//   G = S^T S      fp64 DMMA m8n8k4, the upper tile pairs of the NT x NT tile
+//                  grid (8-column tiles, padded columns read as zero), k split
+//                  over kSqGramWarps warps, partials summed in a fixed order
+//                  (deterministic);
+//   R, R^{-1}      one warp, lane c holding column c of [G | I] (the G part in
+//                  registers, the I part in registers for NT <= 3, else in G's
+//                  storage): Gaussian elimination with symmetric multipliers (row
+//                  k of the trailing upper part, broadcast through shared
+//                  memory); the scaled rows give R and R^{-T};
+//   S <- S R^{-1}  fp64 DMMA, warp per 8-row tile, R^{-1} fragments in registers.
+// Passes: CholeskyQR2 (plain, plain with the ||G - I||_F <= 1/2 check: Q_1 well
+// conditioned, so the second pass is accurate to O(u)); if that breaks down (a
+// non-positive or non-finite pivot, or the check), the CTA reloads A and runs
+// the shifted CholeskyQR3 (s = 11 (m n + n (n+1)) u tr(G), then plain, then plain
+// with the check). A breakdown there sets flags[b] (never cleared; the batched
+// caller redoes that tensor on the Householder path).
+constexpr int kSqGramWarps = 4;
+#ifndef SQ_MINB
+#define SQ_MINB 2  // CTAs per SM the register budget is sized for (3 spills the NT = 3 Cholesky)
+#endif
+
+__device__ __forceinline__ void sq_dmma(double& c0, double& c1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(c0), "+d"(c1)
+                 : "d"(a), "d"(b));
+}
+
+__host__ __device__ constexpr int sq_ld(int m) { return ((m + 7) / 8 * 8 + 11) / 16 * 16 + 4; }
+
+template <int NT>
+__host__ __device__ constexpr int sq_pairs() {
+    return NT * (NT + 1) / 2;
+}
+
+template <int NT>
+std::size_t sq_smem(int m, int n) {
+    const int np = 8 * NT;
+    return sizeof(double) * (static_cast<std::size_t>(n) * sq_ld(m) + kSqGramWarps * sq_pairs<NT>() * 64 +
+                             static_cast<std::size_t>(np) * (np + 2));
+}
+
+#ifdef TTR_SQ_TRACE
+__device__ unsigned long long g_sq_trace[8];
+#define SQ_T(i) do { if (threadIdx.x == 0) { long long t_ = clock64(); atomicAdd(&g_sq_trace[i], static_cast<unsigned long long>(t_ - t_last)); t_last = t_; } } while (0)
+#else
+#define SQ_T(i) do { } while (0)
+#endif
+
+template <int NT>
+__global__ void __launch_bounds__(256, SQ_MINB) cholqr_small_kernel(int m, int n, const double* A, i64 lda, i64 sA, double* Q,
+                                                          i64 ldq, i64 sQ, double coeff, int* flags) {
+#ifdef TTR_SQ_TRACE
+    long long t_last = clock64();
+#endif
+    constexpr int NP = 8 * NT, NPAIR = sq_pairs<NT>();
+    extern __shared__ __align__(16) double sq[];
+    const int ld = sq_ld(m), m8 = (m + 7) / 8 * 8;
+    double* S = sq;                                   // [n][ld]
+    double* part = S + static_cast<i64>(n) * ld;      // [kSqGramWarps][NPAIR][64]
+    double* G = part + kSqGramWarps * NPAIR * 64;     // [NP][NP + 1]: G, then R^{-T}
+    __shared__ int bad;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+    const int lr = lane & 3, lc = lane >> 2;
+    A += blockIdx.x * sA;
+    Q += blockIdx.x * sQ;
+    // S <- A: 16-byte cp.async chunks when the columns allow (all in flight at
+    // once), else plain loads; rows m..m8-1 zero
+    auto load_s = [&] {
+        if ((m & 1) == 0 && (lda & 1) == 0 && (reinterpret_cast<std::uintptr_t>(A) & 15) == 0) {
+            const int hm = m >> 1;
+            for (int e = tid; e < n * hm; e += blockDim.x) {
+                const int c = e / hm, r = 2 * (e - c * hm);
+                const unsigned dst = smem_u32(S + c * ld + r);
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(A + r + static_cast<i64>(c) * lda));
+            }
+            asm volatile("cp.async.commit_group;\n" ::);
+        } else {
+            for (int e = tid; e < n * m; e += blockDim.x) {
+                const int c = e / m, r = e - c * m;
+                S[c * ld + r] = A[r + static_cast<i64>(c) * lda];
+            }
+        }
+        for (int e = tid; e < n * (m8 - m); e += blockDim.x) {
+            const int c = e / (m8 - m), r = m + e - c * (m8 - m);
+            S[c * ld + r] = 0.0;
+        }
+        if (tid == 0) bad = 0;
+        asm volatile("cp.async.wait_all;\n" ::);
+        __syncthreads();
+    };
+    load_s();
+    SQ_T(0);
+    // CholeskyQR2 (plain, plain with the check) first; if it breaks down, the
+    // shifted CholeskyQR3 (shifted, plain, plain with the check) from A again
+    bool fallback = false;
+    for (int stage = 0; stage < (fallback ? 3 : 2);) {
+        const int kind = fallback ? stage : stage + 1;  // 0 shifted, 1 plain, 2 plain + check
+        // ---- Gram partials: warp w takes k-steps w, w + kSqGramWarps, ... ----
+        if (warp < kSqGramWarps) {
+            double acc[NPAIR][2];
+#pragma unroll
+            for (int p = 0; p < NPAIR; ++p) acc[p][0] = acc[p][1] = 0.0;
+            for (int k0 = 4 * warp; k0 < m8; k0 += 4 * kSqGramWarps) {
+                double v[NT];
+#pragma unroll
+                for (int t = 0; t < NT; ++t) {
+                    const int col = 8 * t + lc;
+                    v[t] = (col < n) ? S[col * ld + k0 + lr] : 0.0;
+                }
+                int p = 0;
+#pragma unroll
+                for (int i = 0; i < NT; ++i)
+#pragma unroll
+                    for (int j = i; j < NT; ++j, ++p) sq_dmma(acc[p][0], acc[p][1], v[i], v[j]);
+            }
+#pragma unroll
+            for (int p = 0; p < NPAIR; ++p) {
+                part[(warp * NPAIR + p) * 64 + 2 * lane] = acc[p][0];
+                part[(warp * NPAIR + p) * 64 + 2 * lane + 1] = acc[p][1];
+            }
+        }
+        __syncthreads();
+        SQ_T(1);
+        // ---- fixed-order sum of the partials into G (tile pair p = (i, j), i <= j) ----
+        for (int e = tid; e < NPAIR * 64; e += blockDim.x) {
+            const int p = e >> 6, q = e & 63;
+            double g = 0.0;
+#pragma unroll
+            for (int w = 0; w < kSqGramWarps; ++w) g += part[(w * NPAIR + p) * 64 + q];
+            int i = 0, pp = p;
+            while (pp >= NT - i) {
+                pp -= NT - i;
+                ++i;
+            }
+            const int j = i + pp;
+            const int ql = q >> 1;  // C fragment: row ql >> 2, columns 2 (ql & 3) + (q & 1)
+            G[(8 * i + (ql >> 2)) * (NP + 1) + 8 * j + 2 * (ql & 3) + (q & 1)] = g;
+        }
+        __syncthreads();
+        SQ_T(2);
+        // ---- R and R^{-1} by one warp: lane c holds column c of the upper part
+        // of G and column c of the identity (registers for NT <= 3, else the
+        // identity part in G's own storage); padded steps k >= n are skipped ----
+        if (warp == 0) {
+            constexpr bool kXReg = NT <= 3;
+            double L[NP], XR[kXReg ? NP : 1];
+            double* xs = G + lane;  // X[k][lane] = xs[k * (NP + 1)] (kXReg: at the end)
+            double* rowk = G + NP * (NP + 1);  // [NP], 16-byte aligned
+#pragma unroll
+            for (int k = 0; k < NP; ++k) {
+                const bool real = lane < n;
+                L[k] = real ? (k <= lane ? G[k * (NP + 1) + lane] : 0.0) : (k == lane ? 1.0 : 0.0);
+            }
+            auto xget = [&](int k) -> double {
+                if constexpr (kXReg) return XR[k];
+                else return (lane < NP) ? xs[k * (NP + 1)] : 0.0;
+            };
+            auto xset = [&](int k, double v) {
+                if constexpr (kXReg) XR[k] = v;
+                else if (lane < NP) xs[k * (NP + 1)] = v;
+            };
+#pragma unroll
+            for (int k = 0; k < NP; ++k) xset(k, (k == lane) ? 1.0 : 0.0);
+            if (kind != 1) {
+                double acc = 0.0;
+                if (lane < n) {
+#pragma unroll
+                    for (int k = 0; k < NP; ++k)
+                        if (k <= lane) {
+                            if (kind == 0) {
+                                acc += (k == lane) ? L[k] : 0.0;
+                            } else {
+                                const double dd = L[k] - (k == lane ? 1.0 : 0.0);
+                                acc = fma(k == lane ? 1.0 : 2.0, dd * dd, acc);
+                            }
+                        }
+                }
+                for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+                if (kind == 0) {
+                    const double shift = coeff * acc;
+#pragma unroll
+                    for (int k = 0; k < NP; ++k)
+                        if (k == lane && lane < n) L[k] += shift;
+                } else if (!(acc <= 0.25) && lane == 0) {
+                    bad = 1;
+                }
+            }
+            bool broke = false;
+#pragma unroll
+            for (int k = 0; k < NP; ++k) {
+                if (k < n) {
+                    // row k of the trailing part, broadcast through shared memory
+                    __syncwarp();
+                    if (lane < NP) rowk[lane] = L[k];
+                    __syncwarp();
+                    double piv = rowk[k];
+                    if (!(piv > 0.0) || !isfinite(piv)) {
+                        broke = true;
+                        piv = 1.0;
+                    }
+                    const double is = rsqrt(piv), rp = is * is;
+                    const double fl = L[k] * rp;
+                    const double xk = xget(k);
+                    const double fx = xk * rp;
+#pragma unroll
+                    for (int i2 = (k + 1) & ~1; i2 < NP; i2 += 2) {
+                        const double2 v = *reinterpret_cast<const double2*>(rowk + i2);
+                        if (i2 > k) {
+                            L[i2] = fma(-v.x, fl, L[i2]);
+                            xset(i2, fma(-v.x, fx, xget(i2)));
+                        }
+                        L[i2 + 1] = fma(-v.y, fl, L[i2 + 1]);
+                        xset(i2 + 1, fma(-v.y, fx, xget(i2 + 1)));
+                    }
+                    L[k] *= is;
+                    xset(k, xk * is);
+                }
+            }
+            if (broke && lane == 0) bad = 1;
+            if constexpr (kXReg) {
+                if (lane < NP) {
+#pragma unroll
+                    for (int k = 0; k < NP; ++k) xs[k * (NP + 1)] = XR[k];
+                }
+            }
+            // now X = R^{-T}: R^{-1}[kk][jj] = G[jj * (NP + 1) + kk]
+        }
+        __syncthreads();
+        SQ_T(3);
+        if (!fallback && bad) {
+            fallback = true;
+            stage = 0;
+            __syncthreads();
+            load_s();
+            continue;
+        }
+        // ---- S <- S R^{-1}: warp per 8-row tile, R^{-1} fragments in registers ----
+        {
+            double bf[NT][2 * NT];  // bf[j][ks]: k = 4 ks + lr, column 8 j + lc (ks < 2 (j + 1))
+#pragma unroll
+            for (int j = 0; j < NT; ++j)
+#pragma unroll
+                for (int ks = 0; ks < 2 * NT; ++ks)
+                    bf[j][ks] = (ks < 2 * (j + 1)) ? G[(8 * j + lc) * (NP + 1) + 4 * ks + lr] : 0.0;
+            for (int rt = warp; rt < m8 / 8; rt += nwarps) {
+                const int r0 = 8 * rt;
+                double af[2 * NT];
+#pragma unroll
+                for (int ks = 0; ks < 2 * NT; ++ks) {
+                    const int col = 4 * ks + lr;
+                    af[ks] = (col < n) ? S[col * ld + r0 + lc] : 0.0;
+                }
+                double cc[NT][2];
+#pragma unroll
+                for (int j = 0; j < NT; ++j) {
+                    cc[j][0] = cc[j][1] = 0.0;
+#pragma unroll
+                    for (int ks = 0; ks < 2 * (j + 1); ++ks) sq_dmma(cc[j][0], cc[j][1], af[ks], bf[j][ks]);
+                }
+                __syncwarp();
+#pragma unroll
+                for (int j = 0; j < NT; ++j)
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) {
+                        const int col = 8 * j + 2 * lr + e;
+                        if (col < n) S[col * ld + r0 + lc] = cc[j][e];
+                    }
+            }
+        }
+        __syncthreads();
+        SQ_T(4);
+        ++stage;
+    }
+    if ((m & 1) == 0 && (ldq & 1) == 0 && (reinterpret_cast<std::uintptr_t>(Q) & 15) == 0) {
+        const int hm = m >> 1;
+        for (int e = tid; e < n * hm; e += blockDim.x) {
+            const int c = e / hm, r = 2 * (e - c * hm);
+            *reinterpret_cast<double2*>(Q + r + static_cast<i64>(c) * ldq) = *reinterpret_cast<const double2*>(S + c * ld + r);
+        }
+    } else {
+        for (int e = tid; e < n * m; e += blockDim.x) {
+            const int c = e / m, r = e - c * m;
+            Q[r + static_cast<i64>(c) * ldq] = S[c * ld + r];
+        }
+    }
+    SQ_T(5);
+    if (tid == 0 && bad) flags[blockIdx.x] = 1;  // sticky across the modes of one call
+}
+
 }  // namespace
 
 // Passes: two shifted (each lowers kappa by ~sqrt(11 (mn + n^2) u), enough for
@@ -813,6 +1107,46 @@ void cqr_panel(Ctx& c, i64 rows, i64 b, double* P, i64 ldp, double* V, i64 ldv, 
                                                     V + b, ldv);
     TTR_CUDA(cudaGetLastError());
     c.launched(2);
+}
+
+
+bool cholqr_small_fits(i64 m, i64 n) {
+    return n >= 1 && n <= 32 && m >= 2 * n && m <= 2048 && sq_smem<4>(static_cast<int>(m), static_cast<int>(n)) <= 200 * 1024;
+}
+
+template <int NT>
+static void cholqr_small_launch(Ctx& c, int m, int n, const double* A, i64 lda, i64 sA, double* Q, i64 ldq, i64 sQ,
+                                i64 batch, double coeff, int* flags) {
+    const std::size_t smem = sq_smem<NT>(m, n);
+    static std::atomic<std::uint64_t> configured{0};
+    if (first_on_device(configured)) set_max_dynamic_smem(reinterpret_cast<const void*>(cholqr_small_kernel<NT>));
+    static const int warps_env = [] {
+        const char* e = std::getenv("TTR_SQ_WARPS");
+        return e ? std::atoi(e) : 0;
+    }();
+    // 4 warps: more CTAs per SM hide the one-warp Cholesky (measured 154 vs 165 us
+    // per 2048 320 x 20 matrices with 8)
+    const int warps = warps_env > 0 ? std::max(kSqGramWarps, std::min(8, warps_env)) : kSqGramWarps;
+    cholqr_small_kernel<NT><<<static_cast<unsigned>(batch), 32 * warps, smem, c.stream>>>(m, n, A, lda, sA, Q, ldq, sQ,
+                                                                                        coeff, flags);
+}
+
+// K4e host: batched CholeskyQR2 / sCQR3 of `batch` m x n matrices (strided); flags[b] = 1 on breakdown.
+void cholqr_small_batched(Ctx& c, i64 m, i64 n, const double* A, i64 lda, i64 sA, double* Q, i64 ldq, i64 sQ, i64 batch,
+                          int* flags) {
+    if (!cholqr_small_fits(m, n)) fail(Errc::InvalidArgument, "cholqr_small: shape outside the path");
+    if (batch <= 0) return;
+    const double u = DBL_EPSILON / 2;
+    const double coeff = 11.0 * (static_cast<double>(m) * n + static_cast<double>(n) * (n + 1)) * u;
+    const int mi = static_cast<int>(m), ni = static_cast<int>(n);
+    switch ((ni + 7) / 8) {
+        case 1: cholqr_small_launch<1>(c, mi, ni, A, lda, sA, Q, ldq, sQ, batch, coeff, flags); break;
+        case 2: cholqr_small_launch<2>(c, mi, ni, A, lda, sA, Q, ldq, sQ, batch, coeff, flags); break;
+        case 3: cholqr_small_launch<3>(c, mi, ni, A, lda, sA, Q, ldq, sQ, batch, coeff, flags); break;
+        default: cholqr_small_launch<4>(c, mi, ni, A, lda, sA, Q, ldq, sQ, batch, coeff, flags); break;
+    }
+    TTR_CUDA(cudaGetLastError());
+    c.launched();
 }
 
 }  // namespace ttr

@@ -175,6 +175,47 @@ std::unique_ptr<TTBatch> round_fixed_krp_batched(Ctx& c, const TTBatch& t, const
     }();
     // (phase timing — bench.py's per-kernel roofline run — needs one stream)
     const i64 G = c.timing ? 1 : std::max<i64>(1, std::min<i64>(groups_env > 0 ? groups_env : (B >= 1024 ? 2 : 1), B));
+
+    // Per-tensor QRs of the sweep by batched CholeskyQR2 / shifted CholeskyQR3
+    // (K4e, qr_chol.cu) where the sketch is structurally full rank (wbound, as in
+    // rand_orth_sweep) and the shape fits; a tensor whose factorisation broke
+    // down is redone afterwards through round_fixed_krp with its own seed (the
+    // Householder path). TTR_BATCH_CQR=0 keeps the batched Householder QR.
+    static const int cqr_env = [] {
+        const char* e = std::getenv("TTR_BATCH_CQR");
+        return e ? std::atoi(e) : 1;
+    }();
+    std::vector<i64> wbound(static_cast<std::size_t>(d + 2), 0);
+    wbound[d] = std::min({t.r[d - 1], t.n[d - 1], width});
+    for (i64 k = d - 1; k >= 2; --k) wbound[k] = std::min({t.r[k - 1], width, t.n[k - 1] * wbound[k + 1]});
+    auto cqr_mode = [&](i64 k) {
+        const i64 rows = r[k - 1] * t.n[k - 1], l = r[k];
+        return cqr_env == 1 && rows >= 2 * l && cholqr_small_fits(rows, l) && wbound[k + 1] >= l;
+    };
+    bool any_cqr = false;
+    for (i64 k = 1; k < d; ++k) any_cqr = any_cqr || cqr_mode(k);
+    DBuf flag_buf;
+    int* flags = nullptr;
+    if (any_cqr) {
+        flag_buf = DBuf(c, static_cast<std::size_t>((B + 1) / 2));
+        flags = reinterpret_cast<int*>(flag_buf.p);
+        TTR_CUDA(cudaMemsetAsync(flags, 0, sizeof(int) * static_cast<std::size_t>(B), c.stream));
+    }
+    auto redo_broken = [&] {
+        if (!any_cqr) return;
+        std::vector<int> h(static_cast<std::size_t>(B));
+        TTR_CUDA(cudaMemcpyAsync(h.data(), flags, sizeof(int) * h.size(), cudaMemcpyDeviceToHost, c.stream));
+        TTR_CUDA(cudaStreamSynchronize(c.stream));
+        for (i64 b = 0; b < B; ++b) {
+            if (!h[static_cast<std::size_t>(b)]) continue;
+            auto one = batch_get(c, t, b);
+            auto y = round_fixed_krp(c, *one, targets, derive_seed(seed, static_cast<std::uint64_t>(b)), TTR_RNG_PHILOX);
+            for (i64 k = 0; k < d; ++k)
+                TTR_CUDA(cudaMemcpyAsync(out->core(b, k), y->core(k), sizeof(double) * y->core_size(k),
+                                         cudaMemcpyDeviceToDevice, c.stream));
+        }
+    };
+    if (any_cqr) TTR_CUDA(cudaStreamSynchronize(c.stream));  // flags zeroed before the side streams start
     auto run_group = [&](i64 b0, i64 Bg) {
 
         // ---- sketch: W_k for k = d..2 (Omega_k drawn per tensor from derive_seed(seed, b)) ----
@@ -228,7 +269,10 @@ std::unique_ptr<TTBatch> round_fixed_krp_batched(Ctx& c, const TTBatch& t, const
             if (!q_ready) {
                 PhaseScope ph(c, kPhaseQr);
                 c.charge_qr(4ULL * static_cast<std::uint64_t>(rows) * l * std::min(rows, l) * Bg);
-                if (rows * l <= 26000) {
+                if (cqr_mode(k)) {
+                    cholqr_small_batched(c, rows, l, S.p, rows, rows * l, out->core(b0, k - 1), rows, out->stride, Bg,
+                                         flags + b0);
+                } else if (rows * l <= 26000) {
                     qr_small_batched(c, rows, l, S.p, rows, rows * l, out->core(b0, k - 1), rows, out->stride, nullptr, 1, 0, Bg);
                 } else {
                     const Counts keep = c.counts;
@@ -299,6 +343,7 @@ std::unique_ptr<TTBatch> round_fixed_krp_batched(Ctx& c, const TTBatch& t, const
     };
     if (G == 1) {
         run_group(0, B);
+        redo_broken();
         return out;
     }
     c.fork_side(static_cast<int>(G));
@@ -330,6 +375,7 @@ std::unique_ptr<TTBatch> round_fixed_krp_batched(Ctx& c, const TTBatch& t, const
     restore();
     c.join_side(static_cast<int>(G));
     for (double* w : works) TTR_CUDA(cudaFreeAsync(w, c.stream));
+    redo_broken();
     return out;
 }
 

@@ -117,6 +117,42 @@ def test_thin_qr_cholesky_rank_deficient(P, m, n, rank):
         assert np.linalg.norm(q @ r - a) <= 1e-13 * np.sqrt(m * n) * max(1.0, np.linalg.norm(a))
 
 
+@pytest.mark.parametrize("m,n", [(320, 20), (256, 20), (64, 8), (101, 13), (512, 32), (40, 20), (1024, 17)])
+def test_thin_qr_cholesky_batched(P, m, n):
+    """Batched CholeskyQR2 / sCQR3 (K4e): per matrix orthonormal Q with A = Q Q^T A
+    for well-conditioned, graded (kappa 1e6: CQR2) and ill-conditioned (kappa
+    1e11: CQR2 breaks down, the kernel redoes the matrix as sCQR3) members; exactly
+    rank-deficient and zero members raise their flag or still give a valid basis."""
+    rng = np.random.default_rng(m * 31 + n)
+    mats = []
+    for kind in ("gauss", "graded", "ill", "gauss", "rankdef", "zero", "ill", "gauss"):
+        if kind == "gauss":
+            a = rng.standard_normal((m, n))
+        elif kind in ("graded", "ill"):
+            u, _ = np.linalg.qr(rng.standard_normal((m, n)))
+            v, _ = np.linalg.qr(rng.standard_normal((n, n)))
+            a = (u * np.logspace(0, -6 if kind == "graded" else -11, n)) @ v.T
+        elif kind == "rankdef":
+            a = rng.standard_normal((m, n // 2)) @ rng.standard_normal((n // 2, n))
+        else:
+            a = np.zeros((m, n))
+        mats.append((kind, a))
+    q, flags = P.thin_qr_cholesky_batched(np.stack([a for _, a in mats]))
+    for b, (kind, a) in enumerate(mats):
+        if kind == "zero":
+            assert flags[b]
+        if kind in ("gauss", "graded", "ill"):
+            assert not flags[b], (b, kind)
+        if not flags[b]:
+            assert np.linalg.norm(q[b].T @ q[b] - np.eye(n)) <= 1e-12 * np.sqrt(n), (b, kind)
+            assert np.linalg.norm(q[b] @ (q[b].T @ a) - a) <= 1e-13 * np.sqrt(m * n) * np.linalg.norm(a), (b, kind)
+    # the same basis as Householder up to column signs (well-conditioned member)
+    qh, _ = P.thin_qr(mats[0][1])
+    signs = np.sign(np.sum(q[0] * qh, axis=0))
+    assert np.all(np.abs(signs) == 1)
+    assert np.linalg.norm(q[0] - qh * signs) <= 1e-11 * np.sqrt(n)
+
+
 def _padded_low_rank(O, modes, true_r, pad_r, seed):
     x = O.random_gaussian_tt(modes, true_r, seed)
     out = []
@@ -1226,6 +1262,56 @@ def test_batched_fused_qr_epilogue_opt_in(P, O):
                        env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
 
+
+
+_BATCH_CQR_SCRIPT = r"""
+import sys, numpy as np
+sys.path[:0] = [sys.argv[1], sys.argv[2], sys.argv[3]]
+import paper_2511_03598_b200 as P, py_oracle as O
+from test_gpu_parity import _padded_low_rank
+# config-5a shapes, 64 tensors (TTR_BATCH_CQR=1: the per-tensor QRs of modes 2..6 by K4e)
+b = P.TTBatch.two_part_philox(64, 8, 16, 16, 48, 1e-6, 1005)
+o = P.round_fixed_krp_batched(b, [20] * 7, 7)
+n, r = b.shape()[1], b.shape()[2]
+no, ro = o.shape()[1], o.shape()[2]
+for i in (0, 31, 63):
+    xo = O.TT.from_flat(len(n), n, r, b.flats(i, 1)[0])
+    ref = O.round_fixed_krp(xo, [20] * 7, O.derive_seed(7, i), rng=O.PHILOX)
+    assert ro == ref.ranks, (ro, ref.ranks)
+    assert O.relative_error(ref, O.TT.from_flat(len(no), no, ro, o.flats(i, 1)[0])) <= 1e-10
+# exactly rank-deficient members (true rank 8 stored as 64): their sketches are
+# singular, the Cholesky QR breaks down and those tensors are redone on the
+# Householder path; the full-rank members keep the batched result
+xs = [O.two_part_tt(8, 16, 16, 48, 1e-6, O.derive_seed(1005, i)) for i in range(6)]
+for i in (1, 4):
+    xs[i] = _padded_low_rank(O, [16] * 8, [1] + [8] * 7 + [1], [1] + [64] * 7 + [1], 50 + i)
+bb = P.TTBatch.from_flats(n, r, [x.flat() for x in xs])
+ob = P.round_fixed_krp_batched(bb, [20] * 7, 9)
+for i in range(6):
+    ref = O.round_fixed_krp(xs[i], [20] * 7, O.derive_seed(9, i), rng=O.PHILOX)
+    got = O.TT.from_flat(len(no), no, ro, ob.flats(i, 1)[0])
+    assert np.all(np.isfinite(got.flat()))
+    assert O.relative_error(ref, got) <= 1e-10, i
+print("ok")
+"""
+
+
+@pytest.mark.parametrize("mode", ["1", "0"])
+def test_batched_cholesky_qr_modes(P, O, mode):
+    """The batched sweep with its per-tensor QRs by batched CholeskyQR2/sCQR3
+    (TTR_BATCH_CQR=1, the default) and by the batched Householder QR only
+    (TTR_BATCH_CQR=0; read once per process, so in a subprocess): oracle parity on
+    config-5a shapes, and rank-deficient members (Cholesky breakdown) redone on
+    the Householder path."""
+    import os
+    import subprocess
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    root = os.path.dirname(here)
+    env = dict(os.environ, TTR_BATCH_CQR=mode)
+    r = subprocess.run([sys.executable, "-c", _BATCH_CQR_SCRIPT, root, os.path.join(root, "oracle"), here],
+                       env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
 
 
 def test_adaptive_plan_replays_and_rerecords(P, O):

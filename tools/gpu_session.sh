@@ -1,4 +1,5 @@
-set -x
-timeout 900 python -m pytest tests/test_gpu_parity.py -q -p no:cacheprovider -k "fixed_krp or plan or full_size_fixed" > gpurun_out/t1.log 2>&1; grep -E "^E |passed|failed" gpurun_out/t1.log | head
-for v in 0 1; do TTR_QR_CQR=$v TTR_QR_SPEC_TRACE=1 timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-e2e 2>gpurun_out/err_$v.log | tail -1 > gpurun_out/c5b_$v.json; grep -c "broken mode -1" gpurun_out/err_$v.log; grep "broken mode [0-9]" gpurun_out/err_$v.log | sort | uniq -c | head -3; python -c "import json; d=json.load(open('gpurun_out/c5b_$v.json')); print($v, d['ms_per_step'])"; done
-ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/l5b.csv python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > /dev/null 2>&1; python tools/launch_table.py gpurun_out/l5b.csv 14
+mkdir -p gpurun_out
+timeout 1500 python -m pytest tests/test_gpu_parity.py -q -m gpu -p no:cacheprovider -k "batched or cholesky or config5a" > gpurun_out/s_test.log 2>&1; tail -3 gpurun_out/s_test.log
+timeout 300 python tools/cqr_small_bench.py 2048 2>&1 | tail -8
+timeout 300 python bench.py --config 5a --no-cpu-baseline > gpurun_out/s_5a.log 2>&1
+tail -1 gpurun_out/s_5a.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(round(d['ms_per_step'],3), d['phase_ms'], d['e2e']['ms_per_step'])"
