@@ -302,7 +302,7 @@ ttr_status ttr_thin_qr_cholesky(ttr_ctx* ctx, int64_t m, int64_t n, const double
                                 double* host_r, int* breakdown);
 /* Batched shifted CholeskyQR3 (qr_chol.cu K4e: the per-tensor QRs of the
  * batched sweep) of `batch` host m x n matrices stored back to back (column-
- * major, n <= 32, 2n <= m <= 2048): q likewise; flags[b] = 1 when matrix b broke
+ * major, n <= 32, n <= m <= 2048): q likewise; flags[b] = 1 when matrix b broke
  * down (its q is then unusable). No reference counterpart: a test hook. */
 ttr_status ttr_thin_qr_cholesky_batched(ttr_ctx* ctx, int64_t m, int64_t n, int64_t batch, const double* host_a,
                                         double* host_q, int* host_flags);

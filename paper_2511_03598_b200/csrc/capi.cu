@@ -568,7 +568,7 @@ ttr_status ttr_thin_qr_cholesky_batched(ttr_ctx* ctx, int64_t m, int64_t n, int6
                                         double* host_q, int* host_flags) {
     return guard_ctx(ctx, [&] {
         need(ctx && host_a && host_q && host_flags && batch >= 0, "null argument");
-        need(cholqr_small_fits(m, n), "shape outside the batched Cholesky-QR path (n <= 32, 2n <= m <= 2048)");
+        need(cholqr_small_fits(m, n), "shape outside the batched Cholesky-QR path (n <= 32, n <= m <= 2048)");
         if (batch == 0) return;
         const std::size_t tot = static_cast<std::size_t>(m * n * batch);
         DBuf a(ctx->c, tot), q(ctx->c, tot), f(ctx->c, static_cast<std::size_t>((batch + 1) / 2));

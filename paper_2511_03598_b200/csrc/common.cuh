@@ -265,7 +265,7 @@ void thin_qr_cholesky(Ctx& c, i64 m, i64 n, const double* A, i64 lda, double* Q,
 // x b panel P -> R (P's top block), V (rows x b, unit lower), T (ld 32), tau.
 void cqr_panel(Ctx& c, i64 rows, i64 b, double* P, i64 ldp, double* V, i64 ldv, double* T, double* tau, int tag);
 
-// Batched CholeskyQR2 / sCQR3 of small m x n matrices (K4e, n <= 32, 2n <= m,
+// Batched CholeskyQR2 / sCQR3 of small m x n matrices (K4e, n <= 32, n <= m,
 // the matrix in shared memory): flags[b] = 1 when matrix b broke down (its Q is
 // then unusable).
 bool cholqr_small_fits(i64 m, i64 n);

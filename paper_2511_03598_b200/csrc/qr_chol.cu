@@ -1111,7 +1111,7 @@ void cqr_panel(Ctx& c, i64 rows, i64 b, double* P, i64 ldp, double* V, i64 ldv, 
 
 
 bool cholqr_small_fits(i64 m, i64 n) {
-    return n >= 1 && n <= 32 && m >= 2 * n && m <= 2048 && sq_smem<4>(static_cast<int>(m), static_cast<int>(n)) <= 200 * 1024;
+    return n >= 1 && n <= 32 && m >= n && m <= 2048 && sq_smem<4>(static_cast<int>(m), static_cast<int>(n)) <= 200 * 1024;
 }
 
 template <int NT>

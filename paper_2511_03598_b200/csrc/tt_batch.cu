@@ -190,7 +190,7 @@ std::unique_ptr<TTBatch> round_fixed_krp_batched(Ctx& c, const TTBatch& t, const
     for (i64 k = d - 1; k >= 2; --k) wbound[k] = std::min({t.r[k - 1], width, t.n[k - 1] * wbound[k + 1]});
     auto cqr_mode = [&](i64 k) {
         const i64 rows = r[k - 1] * t.n[k - 1], l = r[k];
-        return cqr_env == 1 && rows >= 2 * l && cholqr_small_fits(rows, l) && wbound[k + 1] >= l;
+        return cqr_env == 1 && cholqr_small_fits(rows, l) && wbound[k + 1] >= l;
     };
     bool any_cqr = false;
     for (i64 k = 1; k < d; ++k) any_cqr = any_cqr || cqr_mode(k);

@@ -117,7 +117,7 @@ def test_thin_qr_cholesky_rank_deficient(P, m, n, rank):
         assert np.linalg.norm(q @ r - a) <= 1e-13 * np.sqrt(m * n) * max(1.0, np.linalg.norm(a))
 
 
-@pytest.mark.parametrize("m,n", [(320, 20), (256, 20), (64, 8), (101, 13), (512, 32), (40, 20), (1024, 17)])
+@pytest.mark.parametrize("m,n", [(320, 20), (256, 20), (64, 8), (101, 13), (512, 32), (40, 20), (1024, 17), (16, 16), (21, 20)])
 def test_thin_qr_cholesky_batched(P, m, n):
     """Batched CholeskyQR2 / sCQR3 (K4e): per matrix orthonormal Q with A = Q Q^T A
     for well-conditioned, graded (kappa 1e6: CQR2) and ill-conditioned (kappa
