@@ -144,6 +144,9 @@ def cpu_desc(cfg, threads):
             f"{threads} host threads, wall clock around the call")
 
 
+REF_BUDGET_S = 240.0  # CPU seconds of rounds the reference arm may spend (see run_reference)
+
+
 def run_reference(args, world, rank):
     """--impl reference: the reference's CPU implementation of the path (the oracle
     port — the reference itself cannot be built here) on the host cores,
@@ -166,16 +169,27 @@ def run_reference(args, world, rank):
     x = cpu_input(O, cfg)
     gen_s = time.perf_counter() - t0
     ranks = [cfg["ell"]] * (cfg["d"] - 1)
-    for _ in range(args.warmup):
+    # One step is one full round (16-17 s for 5b on 16 threads). The run is bounded
+    # to REF_BUDGET_S of CPU rounds so that any --steps/--warmup ends within minutes:
+    # at least one warm-up and two timed rounds, then as many of the asked ones as fit
+    # (steps_run / warmup_run say what ran; the value is per round, so it is unaffected).
+    t_run = time.perf_counter()
+    first = cpu_round(O, x, ranks, 7)
+    per = max(first[0], 1e-3)
+    fit = max(3, int(REF_BUDGET_S / per))
+    warm = min(args.warmup, max(1, fit - 2)) if args.warmup > 0 else 0
+    steps = max(1, min(args.steps, fit - warm))
+    for _ in range(max(0, warm - 1)):
         cpu_round(O, x, ranks, 7)
-    res = [cpu_round(O, x, ranks, 7) for _ in range(args.steps)]
+    res = ([] if warm > 0 else [first]) + [cpu_round(O, x, ranks, 7) for _ in range(steps - (0 if warm > 0 else 1))]
     secs = [r[0] for r in res]
     flops = res[0][1]
     ms = sum(secs) / len(secs) * 1e3
     tflops = flops / (ms * 1e-3) / 1e12
     line = {
         "impl": "reference", "metric": METRIC, "value": tflops, "unit": "TFLOP/s", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "steps": args.steps, "warmup": args.warmup, "steps_run": len(secs), "warmup_run": warm,
+        "run_seconds": time.perf_counter() - t_run, "ms_per_step": ms,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (host Philox Gaussian cores, bitwise the device generator)",
         "config": {"workload": f"config {args.config} fixed-rank KRP rounding round_fixed_krp(Y, "
