@@ -293,6 +293,14 @@ ttr_status ttr_philox_factor(ttr_ctx* ctx, uint64_t seed, int64_t mode, int64_t 
  * the device (linalg::thin_qr, linalg.hpp:22-25). q: m x n, r: n x n. */
 ttr_status ttr_thin_qr(ttr_ctx* ctx, int64_t m, int64_t n, const double* host_a, double* host_q,
                        double* host_r);
+/* thin_qr as the Rand-Orth sweep calls it (round_rand.cpp:33-37 through
+ * linalg::thin_qr_q), with the sweep's speculation tag set: the blocked
+ * Householder QR may factor its panels by Cholesky-QR with Householder
+ * reconstruction (qr_chol.cu K4d/K4f). *breakdown = 1 when a panel broke down
+ * (q and r are then unusable; the rounding entry points rerun such a call on
+ * the Householder panels). No reference counterpart: a test hook. */
+ttr_status ttr_thin_qr_speculative(ttr_ctx* ctx, int64_t m, int64_t n, const double* host_a, double* host_q,
+                                   double* host_r, int* breakdown);
 /* Shifted Cholesky QR (sCQR3, the sweep's speculative QR; qr_chol.cu) of a
  * host m x n matrix (m >= n, n <= 416): q m x n, r n x n upper. *breakdown = 1
  * when a Cholesky factorisation broke down or the third Gram matrix was far

@@ -733,6 +733,22 @@ def thin_qr(a: np.ndarray, ctx: Optional[Context] = None):
     return q.reshape(k, m).T.copy(), r.reshape(n, k).T.copy()
 
 
+def thin_qr_speculative(a: np.ndarray, ctx: Optional[Context] = None):
+    """thin_qr with the sweep's speculation tag set: the blocked Householder QR may
+    take the Cholesky-QR panels (qr_chol.cu K4d/K4f). Returns (q, r, breakdown);
+    on breakdown q and r are unspecified (the sweep reruns on the Householder panels)."""
+    ctx = ctx or default_context()
+    m, n = a.shape
+    k = min(m, n)
+    flat = np.ascontiguousarray(np.asarray(a, dtype=np.float64).T).reshape(-1)
+    q = np.empty(m * k)
+    r = np.empty(k * n)
+    bd = C.c_int(0)
+    _check(lib().ttr_thin_qr_speculative(ctx._h, C.c_int64(m), C.c_int64(n), _dptr(flat), _dptr(q), _dptr(r),
+                                         C.byref(bd)))
+    return q.reshape(k, m).T.copy(), r.reshape(n, k).T.copy(), bool(bd.value)
+
+
 def thin_qr_cholesky(a: np.ndarray, ctx: Optional[Context] = None):
     """sCQR3 on the device (qr_chol.cu): (q, r, breakdown)."""
     ctx = ctx or default_context()

@@ -537,6 +537,30 @@ ttr_status ttr_thin_qr(ttr_ctx* ctx, int64_t m, int64_t n, const double* host_a,
     });
 }
 
+ttr_status ttr_thin_qr_speculative(ttr_ctx* ctx, int64_t m, int64_t n, const double* host_a, double* host_q,
+                                   double* host_r, int* breakdown) {
+    return guard_ctx(ctx, [&] {
+        need(ctx && host_a && breakdown, "null argument");
+        need(m >= 1 && n >= 1, "empty shape");
+        const i64 k = std::min(m, n);
+        DBuf a(ctx->c, static_cast<std::size_t>(m * n)), q(ctx->c, static_cast<std::size_t>(m * k)),
+            r(ctx->c, static_cast<std::size_t>(k * n));
+        TTR_CUDA(cudaMemcpyAsync(a.p, host_a, sizeof(double) * m * n, cudaMemcpyHostToDevice, ctx->c.stream));
+        ctx->c.qr_flag_reset();
+        ctx->c.qr_tag = 0;  // the blocked QR may take the Cholesky-QR panels (K4d/K4f)
+        try {
+            thin_qr(ctx->c, m, n, a.p, m, q.p, m, r.p, k);
+        } catch (...) {
+            ctx->c.qr_tag = -1;
+            throw;
+        }
+        ctx->c.qr_tag = -1;
+        if (host_q) TTR_CUDA(cudaMemcpyAsync(host_q, q.p, sizeof(double) * m * k, cudaMemcpyDeviceToHost, ctx->c.stream));
+        if (host_r) TTR_CUDA(cudaMemcpyAsync(host_r, r.p, sizeof(double) * k * n, cudaMemcpyDeviceToHost, ctx->c.stream));
+        *breakdown = ctx->c.qr_flag_read() >= 0 ? 1 : 0;
+    });
+}
+
 ttr_status ttr_thin_qr_cholesky(ttr_ctx* ctx, int64_t m, int64_t n, const double* host_a, double* host_q,
                                 double* host_r, int* breakdown) {
     return guard_ctx(ctx, [&] {
@@ -598,7 +622,15 @@ ttr_status ttr_dev_thin_qr(ttr_ctx* ctx, int64_t m, int64_t n, const double* dA,
     return guard_ctx(ctx, [&] {
         need(ctx && dA, "null argument");
         need(m >= 1 && n >= 1 && lda >= m && (!dQ || ldq >= m), "bad shape");
-        thin_qr(ctx->c, m, n, dA, lda, dQ, ldq, dR, ldr);
+        static const bool spec = std::getenv("TTR_QR_DEV_SPEC") != nullptr;  // tools/qr_bench.py: time the speculative panels
+        ctx->c.qr_tag = spec ? 0 : -1;
+        try {
+            thin_qr(ctx->c, m, n, dA, lda, dQ, ldq, dR, ldr);
+        } catch (...) {
+            ctx->c.qr_tag = -1;
+            throw;
+        }
+        ctx->c.qr_tag = -1;
     });
 }
 

@@ -124,6 +124,7 @@ struct Ctx {
     // factorisation broke down (kQrNoBreakdown: none).
     bool qr_spec = false, qr_spec_used = false;
     int qr_tag = -1;  // >= 0: the thin_qr being enqueued may use Cholesky-QR panels (K4d) under this tag
+    int qr_checked_depth = 0;  // thin_qr's checked mode: 1 while its Householder rerun is being enqueued
     i64 qr_hh_from = INT32_MAX;
     int* qr_flag = nullptr;
     int* qr_flag_dev();
@@ -199,6 +200,10 @@ inline i64 even_ld(i64 rows) { return rows < 1 ? 2 : round_up(rows, 2); }
 void gemm(Ctx& c, bool trans_a, i64 M, i64 N, i64 K, double alpha, const double* A, i64 lda,
           const double* B, i64 ldb, double beta, double* C, i64 ldc, bool count = true,
           bool upper_tiles = false /* only output tiles touching the upper triangle (Gram matrices) */);
+// C = lt^T (A^T B), A stored K x M with M <= 32 rows of output, lt M x M (ldlt): the
+// blocked QR's W = T^T (V^T A_trail); tmp: M x N scratch (ld M).
+void gemm_tn_lt(Ctx& c, i64 M, i64 N, i64 K, const double* A, i64 lda, const double* B, i64 ldb, const double* lt,
+                i64 ldlt, double* C, i64 ldc, double* tmp, bool count = true);
 // KRP sketch step (sketch.cpp:15-40 restated as one GEMM):
 //   W_out(:, c) = sum_{g, j} H(X)(:, g*n + j) * Omega(j, c) * Wt(c, g)
 // X is the r_left x n x r_right core (H unfolding, ld = r_left), Omega is

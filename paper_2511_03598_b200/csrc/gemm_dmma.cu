@@ -52,6 +52,11 @@ struct GemmArgs {
     // left unspecified; Gram matrices whose consumer reads the upper triangle)
     int upper;
     int prefetch_c;  // 2-stage TMA kernel: load C before the main loop (TTR_GEMM_PREC=0 disables)
+    // host only: fold C <- lt^T C (lt: M x M, ld ldlt, M <= 32) into the wide split-K reduction;
+    // lt_done says whether run_gemm did (it needs >= 16 splits), see gemm_tn_lt
+    const double* lt;
+    i64 ldlt;
+    int lt_done;
 };
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
@@ -334,6 +339,42 @@ __global__ void __launch_bounds__(256) splitk_reduce_wide(const double* __restri
     }
 }
 
+// The same sum for an M <= 32 row product (block = column n, lane = row),
+// followed by C(:, n) = lt^T (alpha * sum): the blocked QR's T^T (V^T A) without a
+// launch of its own for the 32 x 32 factor. Fixed summation orders -> deterministic.
+__global__ void __launch_bounds__(256) splitk_reduce_wide_lt(const double* __restrict__ work, int S, int M, int N,
+                                                             double alpha, const double* __restrict__ lt, i64 ldlt,
+                                                             double* C, i64 ldc) {
+    __shared__ double red[8][33];
+    __shared__ double sv[32];
+    const i64 total = static_cast<i64>(M) * N;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, n = blockIdx.x;
+    const i64 idx = static_cast<i64>(n) * M + lane;
+    double s0 = 0.0, s1 = 0.0;
+    if (lane < M) {
+        int z = warp;
+        for (; z + 8 < S; z += 16) {
+            s0 += work[static_cast<i64>(z) * total + idx];
+            s1 += work[static_cast<i64>(z + 8) * total + idx];
+        }
+        if (z < S) s0 += work[static_cast<i64>(z) * total + idx];
+    }
+    red[warp][lane] = s0 + s1;
+    __syncthreads();
+    if (warp == 0) {
+        double s = 0.0;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) s += red[w][lane];
+        sv[lane] = lane < M ? alpha * s : 0.0;
+        __syncwarp();
+        if (lane < M) {
+            double v = 0.0;
+            for (int m = 0; m < M; ++m) v = fma(lt[m + static_cast<i64>(lane) * ldlt], sv[m], v);
+            C[lane + static_cast<i64>(n) * ldc] = v;
+        }
+    }
+}
+
 // C = alpha * sum_s work[s] + beta * C (split order fixed); optional C^T copy.
 __global__ void splitk_reduce(const double* __restrict__ work, int S, int M, int N, double alpha, double beta,
                               double* C, i64 ldc, double* Ct, i64 ldct) {
@@ -595,7 +636,11 @@ void run_gemm(Ctx& c, bool AT, int KM, int BK, GemmArgs& a, bool va2, bool vb2, 
         const i64 total = static_cast<i64>(a.M) * a.N;
         // choice by split count only: a column's bits must not depend on N
         // (KRP append == one-shot)
-        if (splits >= 16) {
+        if (splits >= 16 && a.lt && a.M <= 32 && beta == 0.0 && !Ct) {
+            splitk_reduce_wide_lt<<<static_cast<unsigned>(a.N), 256, 0, c.stream>>>(a.work, splits, a.M, a.N, alpha, a.lt,
+                                                                                    a.ldlt, C, ldc);
+            a.lt_done = 1;
+        } else if (splits >= 16) {
             splitk_reduce_wide<<<static_cast<unsigned>((total + 31) / 32), 256, 0, c.stream>>>(
                 a.work, splits, a.M, a.N, alpha, beta, C, ldc, Ct, ldct);
         } else {
@@ -654,6 +699,53 @@ void gemm(Ctx& c, bool trans_a, i64 M, i64 N, i64 K, double alpha, const double*
     const int per_sm = (bm * bn >= 128 * 64) ? 2 : (bm * bn >= 64 * 64 ? 4 : 8);
     const int splits = choose_splits(c, tiles, total_kt, tma_tiles ? per_sm : 2);
     run_gemm(c, trans_a, 0, 16, a, va2, vb2, splits, C, ldc, alpha, beta, nullptr, 0, skinny, 0, medium, narrow_n);
+}
+
+// C = lt^T (A^T B) for an M <= 32 row product (A stored K x M): the blocked QR's
+// W = T^T (V^T A_trail). The 32 x 32 factor rides on the wide split-K reduction
+// when the product is split >= 16 ways (tall panels); otherwise it takes the small
+// GEMM of its own through `tmp` (M x N, ld M).
+void gemm_tn_lt(Ctx& c, i64 M, i64 N, i64 K, const double* A, i64 lda, const double* B, i64 ldb, const double* lt,
+                i64 ldlt, double* C, i64 ldc, double* tmp, bool count) {
+    if (M <= 0 || N <= 0) return;
+    if (count) c.charge_gemm(2ULL * static_cast<std::uint64_t>(M) * N * K + 2ULL * static_cast<std::uint64_t>(M) * M * N);
+    static const bool fold = [] {  // experiments: TTR_GEMM_LTFOLD=0 = separate launches
+        const char* e = std::getenv("TTR_GEMM_LTFOLD");
+        return !(e && e[0] == '0');
+    }();
+    if (M > 32 || K <= 0 || !fold) {
+        gemm(c, true, M, N, K, 1.0, A, lda, B, ldb, 0.0, tmp, M, false);
+        gemm(c, true, M, N, M, 1.0, lt, ldlt, tmp, M, 0.0, C, ldc, false);
+        return;
+    }
+    GemmArgs a{};
+    a.M = static_cast<int>(M);
+    a.N = static_cast<int>(N);
+    a.K = static_cast<int>(K);
+    a.A = A;
+    a.lda = lda;
+    a.B = B;
+    a.ldb = ldb;
+    a.lt = lt;
+    a.ldlt = ldlt;
+    // the geometry of gemm() for a skinny (M <= 32) product
+    const bool va2 = aligned16(A) && (lda % 2 == 0);
+    const bool vb2 = aligned16(B) && (ldb % 2 == 0);
+    const bool tma_tiles = tma_enabled() && va2 && vb2;
+    const i64 bm = kSkBM, bn = tma_tiles ? 64 : kSkBN;
+    const i64 tiles = ((M + bm - 1) / bm) * ((N + bn - 1) / bn);
+    const int total_kt = static_cast<int>((K + 15) / 16);
+    const int splits = choose_splits(c, tiles, total_kt, tma_tiles ? 8 : 2);
+    // run_gemm's own rounding of the split count decides whether the wide reduction runs
+    const int s1 = std::max(1, std::min(splits, total_kt)), per = (total_kt + s1 - 1) / s1;
+    if ((total_kt + per - 1) / per >= 16) {
+        run_gemm(c, true, 0, 16, a, va2, vb2, splits, C, ldc, 1.0, 0.0, nullptr, 0, true, 0, false, false);
+        if (!a.lt_done) throw Error(TTR_ERR_INTERNAL, "gemm_tn_lt: the folded reduction did not run");
+    } else {
+        a.lt = nullptr;
+        run_gemm(c, true, 0, 16, a, va2, vb2, splits, tmp, M, 1.0, 0.0, nullptr, 0, true, 0, false, false);
+        gemm(c, true, M, N, M, 1.0, lt, ldlt, tmp, M, 0.0, C, ldc, false);
+    }
 }
 
 void krp_step(Ctx& c, i64 r_left, i64 n, i64 r_right, i64 N, const double* X, const double* Omega, i64 ldo,

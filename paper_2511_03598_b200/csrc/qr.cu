@@ -659,6 +659,16 @@ void qr_small_batched(Ctx& c, i64 m, i64 n, const double* A, i64 lda, i64 sA, do
     c.launched();
 }
 
+namespace {
+bool cqr_checked_on() {  // experiments: TTR_QR_CHECKED=0 = non-speculating callers keep the Householder panels
+    static const bool on = [] {
+        const char* e = std::getenv("TTR_QR_CHECKED");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+}  // namespace
+
 void thin_qr(Ctx& c, i64 m, i64 n, const double* A, i64 lda, double* Q, i64 ldq, double* R, i64 ldr) {
     const i64 k = std::min(m, n);
     c.charge_qr(4ULL * static_cast<std::uint64_t>(m) * n * k);
@@ -735,7 +745,46 @@ void thin_qr(Ctx& c, i64 m, i64 n, const double* A, i64 lda, double* Q, i64 ldq,
         const char* e = std::getenv("TTR_QR_TSQR");
         return e && e[0] == '1';
     }();
-    if (!old_panels && m <= kPushMaxRows && n > kPanel) {
+    // Cholesky-QR panels with Householder reconstruction (qr_chol.cu: K4f, one
+    // cooperative kernel per panel; K4d, separate launches) when the caller
+    // speculates (c.qr_tag >= 0: a breakdown reruns the call on the Householder
+    // panels). Default since K4f (40,960 x 320: 2.69 -> 1.89 ms, 7,040 x 110: 0.465 ->
+    // 0.366 ms); TTR_QR_CQR=0 keeps the Householder panels.
+    static const bool cqr_on = [] {
+        const char* e = std::getenv("TTR_QR_CQR");
+        return !(e && e[0] == '0');
+    }();
+    bool cqr = cqr_on && c.qr_tag >= 0 && n > kPanel && m >= 8 * kPanel;
+    // Callers that do not speculate themselves (TT-SVD orthogonalisations, the
+    // C-ABI thin_qr): the same panels in a checked call — factor under a private
+    // tag, read the breakdown flag (one stream synchronisation per QR) and redo the
+    // QR on the Householder panels if a panel broke down. Not inside a stream
+    // capture (no synchronisation there) and not under an outer speculation (the
+    // flag is the caller's).
+    if (!cqr && cqr_on && c.qr_tag < 0 && !c.qr_spec && n > kPanel && m >= 8 * kPanel && A != Q && cqr_checked_on()) {
+        cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+        TTR_CUDA(cudaStreamIsCapturing(c.stream, &cap));
+        if (cap == cudaStreamCaptureStatusNone) {
+            const Counts saved = c.counts;
+            c.qr_flag_reset();
+            c.qr_tag = 0;
+            try {
+                thin_qr(c, m, n, A, lda, Q, ldq, R, ldr);
+            } catch (...) {
+                c.qr_tag = -1;
+                throw;
+            }
+            c.qr_tag = -1;
+            c.counts = saved;  // charged once, above
+            if (c.qr_flag_read() < 0) return;
+            c.qr_checked_depth = 1;  // the rerun below keeps the Householder panels
+        }
+    }
+    if (c.qr_checked_depth) {
+        cqr = false;
+        c.qr_checked_depth = 0;
+    }
+    if (!old_panels && m <= kPushMaxRows && n > kPanel && !cqr) {
         qr_blocked_push(c, 1, m, n, A, lda, 0, Q, ldq, 0, R, ldr, 0);
         return;
     }
@@ -846,17 +895,6 @@ void thin_qr(Ctx& c, i64 m, i64 n, const double* A, i64 lda, double* Q, i64 ldq,
     DBuf Wb(c, static_cast<std::size_t>(kPanel * std::max<i64>(n, 1)));
     DBuf Wb2(c, static_cast<std::size_t>(kPanel * std::max<i64>(n, 1)));
 
-    // Cholesky-QR panels with Householder reconstruction (K4d, qr_chol.cu) when
-    // the caller speculates (c.qr_tag >= 0: a breakdown reruns the call on the
-    // Householder panels). Opt-in (TTR_QR_CQR=1): measured on B200 at the 5b
-    // shape ~315 us per 40,960 x 32 panel (nine small launches: three passes of
-    // partial Grams, a one-CTA Cholesky + inverse and the row-parallel apply,
-    // then the reconstruction) against 145 us for the grid panel.
-    static const bool cqr_on = [] {
-        const char* e = std::getenv("TTR_QR_CQR");
-        return e && e[0] == '1';
-    }();
-    const bool cqr = cqr_on && c.qr_tag >= 0;
     for (i64 p = 0; p < npanels; ++p) {
         const i64 j0 = p * kPanel, bb = std::min<i64>(kPanel, k - j0), rows = m - j0;
         double* V = Vall.p + j0 + j0 * ldw;  // rows x bb block at (j0, j0), ld ldw
@@ -867,8 +905,7 @@ void thin_qr(Ctx& c, i64 m, i64 n, const double* A, i64 lda, double* Q, i64 ldq,
             const i64 ntrail = n - j0 - bb;
             if (ntrail > 0) {
                 double* At = work.p + j0 + (j0 + bb) * ldw;
-                gemm(c, true, bb, ntrail, rows, 1.0, V, ldw, At, ldw, 0.0, Wb.p, kPanel, false);    // V^T A
-                gemm(c, true, bb, ntrail, bb, 1.0, T, kPanel, Wb.p, kPanel, 0.0, Wb2.p, kPanel, false);  // T^T (V^T A)
+                gemm_tn_lt(c, bb, ntrail, rows, V, ldw, At, ldw, T, kPanel, Wb2.p, kPanel, Wb.p, false);  // T^T (V^T A)
                 gemm(c, false, rows, ntrail, bb, -1.0, V, ldw, Wb2.p, kPanel, 1.0, At, ldw, false);  // A -= V (.)
             }
             continue;
@@ -888,8 +925,7 @@ void thin_qr(Ctx& c, i64 m, i64 n, const double* A, i64 lda, double* Q, i64 ldq,
         const i64 ntrail = n - j0 - bb;
         if (ntrail > 0) {
             double* At = work.p + j0 + (j0 + bb) * ldw;
-            gemm(c, true, bb, ntrail, rows, 1.0, V, ldw, At, ldw, 0.0, Wb.p, kPanel, false);    // V^T A
-            gemm(c, true, bb, ntrail, bb, 1.0, T, kPanel, Wb.p, kPanel, 0.0, Wb2.p, kPanel, false);  // T^T (V^T A)
+            gemm_tn_lt(c, bb, ntrail, rows, V, ldw, At, ldw, T, kPanel, Wb2.p, kPanel, Wb.p, false);  // T^T (V^T A)
             gemm(c, false, rows, ntrail, bb, -1.0, V, ldw, Wb2.p, kPanel, 1.0, At, ldw, false);  // A -= V (.)
         }
     }

@@ -25,9 +25,16 @@
 // sketches still get the reference's behaviour.
 #include <cfloat>
 #include <cmath>
+#include <atomic>
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+
+#include <cooperative_groups.h>
 
 #include "common.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace ttr {
 namespace {
@@ -1016,6 +1023,446 @@ __global__ void __launch_bounds__(256, SQ_MINB) cholqr_small_kernel(int m, int n
     if (tid == 0 && bad) flags[blockIdx.x] = 1;  // sticky across the modes of one call
 }
 
+// ---------------------------------------------------------------------------
+// K4f: the K4d panel (Cholesky-QR + Householder reconstruction) as ONE
+// cooperative kernel, so a 32-column panel costs 4-6 grid barriers instead of
+// one cross-CTA exchange per column (qr_panel.cuh: ~4.5 us per column at
+// 40,960 rows) or K4d's eleven dependent launches. CTA `rank` keeps its rpc
+// rows of the panel column-major in shared memory (the K4e layout, ld = 4 mod
+// 16) plus a shadow copy of the panel's top b x b block, which takes every
+// S <- S R^{-1} with the own rows: all CTAs then hold the same Q_1 bit for bit
+// and run the Householder reconstruction redundantly (no broadcast barrier).
+// Per pass:
+//   partial Gram of the own rows   fp64 DMMA, upper 8 x 8 tile pairs, k split
+//                                  over kFpGramWarps warps, fixed-order sums;
+//   grid sum                       partials to global, grid barrier, CTA `rank`
+//                                  sums a slice of the 640 entries over all
+//                                  CTAs (one warp per entry, fixed order), grid
+//                                  barrier, every CTA reads the 640 sums: all
+//                                  CTAs see the same G and take the same branches;
+//   R, R^{-T}                      warp 0 (the K4e elimination), redundantly;
+//   S <- S R^{-1}                  fp64 DMMA, warp per 8-row tile.
+// Pass 0 factors G as it is unless a pivot fell below 1e-6 of its diagonal entry
+// (or was not positive), in which case the same G is refactored with the sCQR
+// shift s = coeff tr(G). Every later pass first tests ||G - I||_F <= 1/2: when it
+// holds the pass is the last one (its input was well conditioned, so its output
+// is orthonormal to O(u)); a fifth pass, a non-positive pivot after pass 0 or a
+// non-finite entry is a breakdown (flag <- tag, nothing written; the caller
+// reruns the QR on the Householder panels). A well conditioned panel takes two
+// passes (4 grid barriers), an ill conditioned one three (6).
+// Then (Ballard et al. 2014, as cqr_hr above): LU without pivoting of Q_1 - S,
+// V_2 = Q_2 U^{-1} by the same DMMA apply, CTA 0 writes V_1 = L, T = -U S L^{-T},
+// tau = diag(T) and R = S R_p ... R_1 into the panel's top block.
+constexpr int kFpThreads = 512, kFpWarps = kFpThreads / 32, kFpGramWarps = 8, kFpFacWarps = 8, kFpPairs = 10, kFpEntries = kFpPairs * 64,
+              kFpMaxRpc = 320, kFpMaxPasses = 4;
+constexpr double kFpAnalyticDev2 = 1e-18;  // ||G - I||_F^2 below which a pass takes the first-order factor
+
+struct FusedPanelArgs {
+    int rows, b, rpc;  // rpc: rows per CTA, a multiple of 8, <= kFpMaxRpc
+    double* P;         // rows x b panel (R is written into its top block)
+    i64 ldp;
+    double* V;
+    i64 ldv;
+    double* T;
+    double* tau;
+    double* gpart;  // [gridDim.x][640] partial Grams (upper tile pairs, C-fragment order)
+    double* gsum;   // [640] their sum
+    double coeff;   // shift coefficient: s = coeff * trace(G)
+    int* flag;
+    int tag;
+    long long* trace;  // [64] phase time stamps of CTA 0 (diagnostics) or null
+};
+
+__host__ __device__ constexpr int fp_ld(int rpc) { return sq_ld(rpc + 32); }
+__host__ __device__ constexpr std::size_t fp_smem_doubles(int rpc) {
+    return static_cast<std::size_t>(32) * fp_ld(rpc) + kFpGramWarps * kFpEntries + 4 * (32 * 33 + 2) + 5 * 32;
+}
+
+__global__ void __launch_bounds__(kFpThreads, 1) cqr_panel_fused(FusedPanelArgs p) {
+    cg::grid_group grid = cg::this_grid();
+    extern __shared__ __align__(16) double fsm[];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int lr = lane & 3, lc = lane >> 2;
+    const int rank = blockIdx.x, G = gridDim.x;
+    const int b = p.b, rpc = p.rpc;
+    const int r0 = rank * rpc, nr = max(0, min(p.rows, r0 + rpc) - r0);
+    const int mt = rpc + 32, ld = fp_ld(rpc);
+    constexpr int LM = 33, MS = 32 * 33 + 1;  // small-matrix row stride (odd: conflict-free columns), slot size (even)
+    double* S = fsm;                                // [32][ld]: own rows 0..rpc-1, shadow top block rpc..rpc+31
+    double* part = S + 32 * ld;                     // [kFpGramWarps][640]; the HR scratch afterwards
+    double* Gm = part + kFpGramWarps * kFpEntries;  // [32][33] the summed Gram (upper)
+    double* RX = Gm + MS + 1;    // [32][33] row k: R(k, c) for c >= k, X(k, c) = R^{-T}(k, c) for c < k
+    double* RTa = RX + MS + 1;   // [32][33] R_p ... R_1 (CTA 0), ping
+    double* RTb = RTa + MS + 1;  // pong
+    double* rowk = RTb + MS + 1;  // [2][32] the pivot row, double buffered
+    double* d0s = rowk + 64;      // [32] (spare)
+    double* xdg = d0s + 32;       // [32] X(k, k) (then U^{-1}(k, k))
+    double* sg = xdg + 32;        // [32] HR signs
+    __shared__ int s_bad, s_final;
+    int stamp = 0;
+    auto mark = [&] {
+        if (p.trace && rank == 0 && tid == 0 && stamp < 64) p.trace[stamp] = clock64();
+        ++stamp;
+    };
+    mark();
+    // ---- load: own rows, zero padding, shadow top block (all loads in flight) ----
+    {
+        constexpr int kLd = (32 * (kFpMaxRpc + 32) + kFpThreads - 1) / kFpThreads;  // 22 elements per thread
+        double v[kLd];
+#pragma unroll
+        for (int u = 0; u < kLd; ++u) {
+            const int e = tid + u * kFpThreads, c = e / mt, r = e - c * mt;
+            v[u] = 0.0;
+            if (c < b) {
+                if (r < nr) v[u] = p.P[(r0 + r) + static_cast<i64>(c) * p.ldp];
+                else if (r >= rpc && r - rpc < b) v[u] = p.P[(r - rpc) + static_cast<i64>(c) * p.ldp];
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kLd; ++u) {
+            const int e = tid + u * kFpThreads, c = e / mt, r = e - c * mt;
+            if (c < 32) S[c * ld + r] = v[u];
+        }
+    }
+    if (tid == 0) {
+        s_bad = 0;
+        s_final = 0;
+    }
+    __syncthreads();
+    mark();
+
+    // S <- S M on `ntiles` 8-row tiles, M upper triangular in the RX/xdg layout:
+    // M(k, c) = RX[c][k] for k < c, xdg[c] for k = c
+    auto apply = [&](int ntiles, int nwarps) {
+        double bf[4][8];
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int ks = 0; ks < 8; ++ks) {
+                const int c = 8 * j + lc, k = 4 * ks + lr;
+                bf[j][ks] = (ks < 2 * (j + 1)) ? (k < c ? RX[c * LM + k] : (k == c ? xdg[c] : 0.0)) : 0.0;
+            }
+        for (int rt = warp; rt < ntiles; rt += nwarps) {
+            const int rr = 8 * rt;
+            double af[8];
+#pragma unroll
+            for (int ks = 0; ks < 8; ++ks) af[ks] = S[(4 * ks + lr) * ld + rr + lc];
+            double cc[4][2];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                cc[j][0] = cc[j][1] = 0.0;
+#pragma unroll
+                for (int ks = 0; ks < 2 * (j + 1); ++ks) sq_dmma(cc[j][0], cc[j][1], af[ks], bf[j][ks]);
+            }
+            __syncwarp();
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int col = 8 * j + 2 * lr + e;
+                    if (col < b) S[col * ld + rr + lc] = cc[j][e];
+                }
+        }
+    };
+
+    double* RT = RTa;  // current R_p ... R_1 (CTA 0)
+    bool done = false;
+    for (int pass = 0; !done; ++pass) {
+        // ---- partial Gram of the own rows ----
+        if (warp < kFpGramWarps) {
+            double acc[kFpPairs][2];
+#pragma unroll
+            for (int q = 0; q < kFpPairs; ++q) acc[q][0] = acc[q][1] = 0.0;
+            for (int k0 = 4 * warp; k0 < rpc; k0 += 4 * kFpGramWarps) {
+                double v[4];
+#pragma unroll
+                for (int t = 0; t < 4; ++t) v[t] = S[(8 * t + lc) * ld + k0 + lr];
+                int q = 0;
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int j = i; j < 4; ++j, ++q) sq_dmma(acc[q][0], acc[q][1], v[i], v[j]);
+            }
+#pragma unroll
+            for (int q = 0; q < kFpPairs; ++q)
+                *reinterpret_cast<double2*>(part + (warp * kFpPairs + q) * 64 + 2 * lane) = make_double2(acc[q][0], acc[q][1]);
+        }
+        __syncthreads();
+        for (int e = tid; e < kFpEntries; e += kFpThreads) {
+            double g = 0.0;
+#pragma unroll
+            for (int w = 0; w < kFpGramWarps; ++w) g += part[w * kFpEntries + e];
+            p.gpart[static_cast<i64>(rank) * kFpEntries + e] = g;
+        }
+        mark();
+        grid.sync();
+        mark();
+        // ---- slice of the grid sum: one warp per entry, fixed order ----
+        {
+            const int eper = (kFpEntries + G - 1) / G, e0 = rank * eper;
+            for (int ee = warp; ee < eper; ee += kFpWarps) {
+                const int e = e0 + ee;
+                if (e < kFpEntries) {
+                    double a = 0.0;
+                    for (int g = lane; g < G; g += 32) a += __ldcg(p.gpart + static_cast<i64>(g) * kFpEntries + e);
+                    for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+                    if (lane == 0) p.gsum[e] = a;
+                }
+            }
+        }
+        mark();
+        grid.sync();
+        mark();
+        for (int e = tid; e < kFpEntries; e += kFpThreads) {
+            const int q = e >> 6, f = e & 63;
+            int i = 0, qq = q;
+            while (qq >= 4 - i) {
+                qq -= 4 - i;
+                ++i;
+            }
+            const int j = i + qq, fl = f >> 1;  // C fragment: row fl >> 2, columns 2 (fl & 3) + (f & 1)
+            Gm[(8 * i + (fl >> 2)) * LM + 8 * j + 2 * (fl & 3) + (f & 1)] = __ldcg(p.gsum + e);
+        }
+        __syncthreads();
+        // ---- R and R^{-T} by warps 0..7 (kFpFacWarps), four rows each, lane = column c.
+        // One array holds both triangles: entry (i, c) is G(i, c) for i <= c and, as the
+        // elimination reaches it, X(i, c) for i > c (the identity carried along; X(c, c)
+        // = 1 implicit). Step k: the owner of row k publishes it, one named barrier, then
+        // every row i > k takes W(i, c) -= G(k, i) f with ONE per-column factor: columns
+        // c > k are in their G part (f = G(k, c)/piv, rows i <= c), columns c <= k in their
+        // X part (f = X(k, c)/piv, every row). The scaled row k is R(k, c) for c >= k and
+        // X(k, c) = R^{-T}(k, c) for c < k. Every warp derives the same pivots and flags. ----
+        if (warp < kFpFacWarps) {
+            double W[4];
+            bool broke = false, ill = false, fin = false;
+            double dev2 = 1.0;
+            const bool real = lane < b;
+            for (int attempt = 0; attempt < 2; ++attempt) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int i = 4 * warp + q;
+                    W[q] = real ? (i <= lane ? Gm[i * LM + lane] : 0.0) : (i == lane ? 1.0 : 0.0);
+                }
+                const double dg = real ? Gm[lane * LM + lane] : 1.0;
+                double shift = 0.0;
+                if (pass == 0 && attempt == 1) {  // sCQR shift
+                    double tr = real ? dg : 0.0;
+                    for (int o = 16; o > 0; o >>= 1) tr += __shfl_xor_sync(0xffffffffu, tr, o);
+                    shift = p.coeff * tr;
+#pragma unroll
+                    for (int q = 0; q < 4; ++q)
+                        if (4 * warp + q == lane && real) W[q] += shift;
+                }
+                if (pass > 0) {  // ||G - I||_F^2 over the real columns (upper part counted twice)
+                    double acc = 0.0;
+                    if (real) {
+                        for (int i = 0; i <= lane; ++i) {
+                            const double dd = Gm[i * LM + lane] - (i == lane ? 1.0 : 0.0);
+                            acc = fma(i == lane ? 1.0 : 2.0, dd * dd, acc);
+                        }
+                    }
+                    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+                    fin = acc <= 0.25;  // false for NaN
+                    dev2 = acc;
+                }
+                broke = false;
+                ill = false;
+                if (pass > 0 && dev2 <= kFpAnalyticDev2) {
+                    // G = I + E with ||E||_F <= 1e-9: R = I + striu(E) + diag(E)/2 and R^{-1} = I -
+                    // striu(E) - diag(E)/2 up to O(||E||^2) <= 1e-18 -- no elimination sweep
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const int i = 4 * warp + q;
+                        if (i < b) {
+                            double v;
+                            if (!real) v = 0.0;
+                            else if (i < lane) v = Gm[i * LM + lane];                       // R(i, c) = E(i, c)
+                            else if (i == lane) v = 1.0 + 0.5 * (Gm[i * LM + i] - 1.0);     // R(i, i)
+                            else v = -Gm[lane * LM + i];                                    // X(i, c) = -E(c, i)
+                            RX[i * LM + lane] = v;
+                            if (i == lane) xdg[i] = 1.0 - 0.5 * (Gm[i * LM + i] - 1.0);
+                        }
+                    }
+                    break;
+                }
+#pragma unroll 1
+                for (int k = 0; k < b; ++k) {
+                    double* rb = rowk + 32 * (k & 1);
+                    if (warp == (k >> 2)) {
+                        double v = W[0];
+#pragma unroll
+                        for (int q = 1; q < 4; ++q) v = ((k & 3) == q) ? W[q] : v;
+                        rb[lane] = v;
+                    }
+                    asm volatile("bar.sync 1, %0;" ::"n"(kFpFacWarps * 32) : "memory");
+                    double piv = rb[k];
+                    if (!(piv > 0.0) || !isfinite(piv)) {
+                        broke = true;
+                        piv = 1.0;
+                    }
+                    // original diagonal of column k: Gm (+ shift on the second attempt)
+                    if (!(piv > 1e-6 * (Gm[k * LM + k] + shift))) ill = true;
+                    const double is = rsqrt(piv), rp = is * is;
+                    const double f = ((lane == k) ? 1.0 : rb[lane]) * rp;
+                    const bool xpart = lane <= k;
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const int i2 = 4 * warp + q;
+                        const double v = rb[i2];
+                        if (i2 > k && (xpart || i2 <= lane)) W[q] = fma(-v, f, W[q]);
+                        if (i2 == k) {
+                            W[q] *= is;
+                            RX[k * LM + lane] = W[q];
+                            if (lane == k) xdg[k] = is;
+                        }
+                    }
+                }
+                if (!(pass == 0 && attempt == 0 && (broke || ill))) break;
+                asm volatile("bar.sync 1, %0;" ::"n"(kFpFacWarps * 32) : "memory");  // rowk reused by the second attempt
+            }
+            for (int i = b + warp; i < 32; i += kFpFacWarps) {  // padded rows: identity
+                RX[i * LM + lane] = (i == lane) ? 1.0 : 0.0;
+                if (lane == i) xdg[i] = 1.0;
+            }
+            if (tid == 0) {
+                if (broke || (pass > 0 && !fin && pass + 1 >= kFpMaxPasses)) s_bad = 1;
+                s_final = fin ? 1 : 0;
+            }
+        }
+        __syncthreads();
+        mark();
+        if (s_bad) {  // the same decision in every CTA (identical G)
+            if (rank == 0 && tid == 0) atomicMin(p.flag, p.tag);
+            return;
+        }
+        done = s_final != 0;
+        if (rank == 0) {  // RT <- R RT (first pass: RT = R), two entries per thread
+            double* RTn = (RT == RTa) ? RTb : RTa;
+            for (int e = tid; e < 1024; e += kFpThreads) {
+                const int i = e >> 5, c = e & 31;
+                double a = 0.0;
+                if (i <= c) {
+                    if (pass == 0) a = RX[i * LM + c];
+                    else
+                        for (int q = i; q <= c; ++q) a = fma(RX[i * LM + q], RT[q * LM + c], a);
+                }
+                RTn[i * LM + c] = a;
+            }
+            RT = RTn;
+        }
+        apply(mt / 8, kFpWarps);
+        __syncthreads();
+        mark();
+    }
+
+    // ---- Householder reconstruction from Q_1 (the shadow block), redundantly in every
+    // CTA: ONE Gauss-Jordan sweep over A = Q_1 - S by warps 0..7 (four rows each, lane =
+    // column), one named barrier per step. Step k: the owner publishes row k, every warp
+    // the column-k entries of its rows; s_k = -sign(a_kk), u_kk = a_kk - s_k; every row
+    // i != k takes A(i, c) -= m_i A(k, c) for c > k with m_i = A(i, k) / u_kk and keeps m_i
+    // in place of A(i, k). Rows below k thus build L and U (LU without pivoting, the
+    // pivot row saved to LUm as it is used), rows above k reduce U to its diagonal:
+    // their multipliers are U^{-1}(i, k) = -m_i / u_ii. ----
+    double* LUm = part;           // [32][33] L \ U
+    double* ZS = LUm + MS + 1;    // [32][33] L^{-1} (CTA 0)
+    double* colk = ZS + MS + 1;   // [2][32] column k of the sweep
+    double* zrow = colk + 64;     // [2][32] row k of L^{-1} so far (CTA 0)
+    if (warp < kFpFacWarps) {
+        double W[4], Z[4];  // Z: rows of L^{-1} (CTA 0 only: the identity under the same row operations)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int i = 4 * warp + q;
+            W[q] = (i < b && lane < b) ? S[lane * ld + rpc + i] : (i == lane ? 1.0 : 0.0);
+            Z[q] = (i == lane) ? 1.0 : 0.0;
+        }
+#pragma unroll 1
+        for (int k = 0; k < 32; ++k) {
+            double* rb = rowk + 32 * (k & 1);
+            double* cb = colk + 32 * (k & 1);
+            double* zb = zrow + 32 * (k & 1);
+            if (warp == (k >> 2)) {
+                double v = W[0], z = Z[0];
+#pragma unroll
+                for (int q = 1; q < 4; ++q) {
+                    v = ((k & 3) == q) ? W[q] : v;
+                    z = ((k & 3) == q) ? Z[q] : z;
+                }
+                rb[lane] = v;
+                if (rank == 0) zb[lane] = z;
+            }
+            if (lane == k) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) cb[4 * warp + q] = W[q];
+            }
+            asm volatile("bar.sync 1, %0;" ::"n"(kFpFacWarps * 32) : "memory");
+            const double akk = rb[k];
+            const double sk = k < b ? (akk >= 0.0 ? -1.0 : 1.0) : 0.0;
+            const double ukk = akk - sk;  // |ukk| >= 1 for k < b
+            const double inv = 1.0 / ukk;
+            const double rkc = rb[lane];
+            const double zkc = rank == 0 ? zb[lane] : 0.0;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int i = 4 * warp + q;
+                if (i != k) {
+                    const double m = cb[i] * inv;
+                    if (lane > k) W[q] = fma(-m, rkc, W[q]);
+                    if (lane == k) W[q] = m;
+                    if (rank == 0 && i > k) Z[q] = fma(-m, zkc, Z[q]);
+                } else {
+                    if (lane == k) {
+                        W[q] = ukk;
+                        sg[k] = sk;
+                    }
+                    if (lane >= k) LUm[k * LM + lane] = W[q];  // U(k, c), c >= k
+                }
+            }
+        }
+        // L below the diagonal; U^{-1} into the apply layout (RX/xdg; R no longer needed)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int i = 4 * warp + q;
+            const double rd = 1.0 / __shfl_sync(0xffffffffu, W[q], i);
+            if (lane < i) LUm[i * LM + lane] = W[q];
+            else if (lane == i) xdg[i] = rd;
+            else RX[lane * LM + i] = -W[q] * rd;
+            if (rank == 0) ZS[i * LM + lane] = Z[q];
+        }
+    }
+    __syncthreads();
+    mark();
+    apply(rpc / 8, kFpWarps);  // V_2 = Q_2 U^{-1} on the own rows
+    __syncthreads();
+    // ---- V: own rows (global rows < b: the unit lower L of the LU) ----
+    for (int c = warp; c < b; c += kFpWarps) {
+        double* dst = p.V + static_cast<i64>(c) * p.ldv;
+        for (int r = lane; r < nr; r += 32) {
+            const int g = r0 + r;
+            double v;
+            if (g >= b) v = S[c * ld + r];
+            else v = g > c ? LUm[g * LM + c] : (g == c ? 1.0 : 0.0);
+            dst[g] = v;
+        }
+    }
+    if (rank == 0) {
+        // T = -U S L^{-T}: T(i, j) = -sum_{i <= k <= j} U(i, k) s_k Z(j, k); R = S RT
+        for (int e = tid; e < 1024; e += kFpThreads) {
+            const int i = e & 31, jj = e >> 5;
+            double t = 0.0;
+            if (i <= jj) {
+                for (int k = i; k <= jj; ++k) t = fma(LUm[i * LM + k] * sg[k], ZS[jj * LM + k], t);
+                t = -t;
+            }
+            if (i < b && jj < b) {
+                p.T[i + 32 * jj] = t;
+                if (i == jj) p.tau[jj] = t;
+                if (i <= jj) p.P[i + static_cast<i64>(jj) * p.ldp] = sg[i] * RT[i * LM + jj];
+            }
+        }
+    }
+    mark();
+}
+
 }  // namespace
 
 // Passes: two shifted (each lowers kappa by ~sqrt(11 (mn + n^2) u), enough for
@@ -1077,8 +1524,60 @@ void thin_qr_cholesky(Ctx& c, i64 m, i64 n, const double* A, i64 lda, double* Q,
 // K4d host: factor the rows x b panel P (ld ldp, b <= 32, rows >= 2b) into the
 // blocked QR's (R in P's top block, V, T, tau); breakdown -> the context's QR
 // flag with `tag` (the caller speculates, see with_qr_speculation).
+// K4f host: the fused cooperative panel when the rows fit one CTA per SM
+// (<= kFpMaxRpc rows each); false = not taken (the caller uses K4d's launches).
+bool cqr_panel_fused_launch(Ctx& c, i64 rows, i64 b, double* P, i64 ldp, double* V, i64 ldv, double* T, double* tau,
+                            int tag) {
+    i64 rpc = ((rows + c.sm_count - 1) / c.sm_count + 7) / 8 * 8;
+    rpc = std::max<i64>(rpc, 64);
+    if (rpc > kFpMaxRpc) return false;
+    const i64 G = (rows + rpc - 1) / rpc;
+    static std::atomic<std::uint64_t> configured{0};  // bit d: attributes set on device d
+    if (first_on_device(configured)) set_max_dynamic_smem(reinterpret_cast<const void*>(cqr_panel_fused));
+    static const bool trace_on = std::getenv("TTR_QR_TRACE") != nullptr;  // diagnostics (eager calls only)
+    const double u = DBL_EPSILON / 2;
+    DBuf xb(c, static_cast<std::size_t>((G + 1) * kFpEntries)), tr(c, trace_on ? 64 : 1);
+    FusedPanelArgs a{};
+    a.rows = static_cast<int>(rows);
+    a.b = static_cast<int>(b);
+    a.rpc = static_cast<int>(rpc);
+    a.P = P;
+    a.ldp = ldp;
+    a.V = V;
+    a.ldv = ldv;
+    a.T = T;
+    a.tau = tau;
+    a.gpart = xb.p;
+    a.gsum = xb.p + G * kFpEntries;
+    a.coeff = 11.0 * (static_cast<double>(rows) * b + static_cast<double>(b) * (b + 1)) * u;
+    a.flag = c.qr_flag_dev();
+    a.tag = tag;
+    a.trace = trace_on ? reinterpret_cast<long long*>(tr.p) : nullptr;
+    if (trace_on) TTR_CUDA(cudaMemsetAsync(tr.p, 0, 64 * sizeof(double), c.stream));
+    void* args[] = {&a};
+    TTR_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(cqr_panel_fused), dim3(static_cast<unsigned>(G)),
+                                         dim3(kFpThreads), args, sizeof(double) * fp_smem_doubles(static_cast<int>(rpc)),
+                                         c.stream));
+    c.launched();
+    if (trace_on) {
+        long long h[64];
+        TTR_CUDA(cudaMemcpyAsync(h, tr.p, sizeof(h), cudaMemcpyDeviceToHost, c.stream));
+        TTR_CUDA(cudaStreamSynchronize(c.stream));
+        std::fprintf(stderr, "cqr_panel_fused rows %lld b %lld rpc %lld grid %lld: cycles", static_cast<long long>(rows),
+                     static_cast<long long>(b), static_cast<long long>(rpc), static_cast<long long>(G));
+        for (int i = 1; i < 64 && h[i]; ++i) std::fprintf(stderr, " %lld", h[i] - h[i - 1]);
+        std::fprintf(stderr, "\n");
+    }
+    return true;
+}
+
 void cqr_panel(Ctx& c, i64 rows, i64 b, double* P, i64 ldp, double* V, i64 ldv, double* T, double* tau, int tag) {
     if (b < 1 || b > 32 || rows < 2 * b) fail(Errc::InvalidArgument, "cqr_panel: shape outside the panel path");
+    static const bool fused_on = [] {  // experiments: TTR_QR_CQR_FUSED=0 = K4d's separate launches
+        const char* e = std::getenv("TTR_QR_CQR_FUSED");
+        return !(e && e[0] == '0');
+    }();
+    if (fused_on && cqr_panel_fused_launch(c, rows, b, P, ldp, V, ldv, T, tau, tag)) return;
     const i64 G = std::max<i64>(1, std::min<i64>(c.sm_count, (rows + 255) / 256));
     const i64 rpc = ((rows + G - 1) / G + 31) / 32 * 32;
     const double u = DBL_EPSILON / 2;

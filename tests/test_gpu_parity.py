@@ -216,17 +216,37 @@ print("ok")
 """
 
 
-def test_fixed_krp_cholesky_qr_panels_opt_in(P, O):
-    """The opt-in Cholesky-QR panels with Householder reconstruction (TTR_QR_CQR=1,
-    K4d) in the blocked grid QR of the sweep: oracle parity, plan == eager."""
+@pytest.mark.parametrize("knobs", [{"TTR_QR_CQR": "1"}, {"TTR_QR_CQR": "1", "TTR_QR_CQR_FUSED": "0"},
+                                   {"TTR_QR_CQR": "0"}],
+                         ids=["fused-K4f", "launches-K4d", "householder-panels"])
+def test_fixed_krp_cholesky_qr_panels(P, O, knobs):
+    """The sweep's blocked grid QR with its three panel kernels — the Cholesky-QR
+    panels with Householder reconstruction as one cooperative kernel (K4f, the
+    default), as separate launches (K4d), and the Householder panels: oracle
+    parity, plan == eager (the knobs are read once per process: subprocess)."""
     import os
     import subprocess
     import sys
     here = os.path.dirname(os.path.abspath(__file__))
     root = os.path.dirname(here)
-    env = dict(os.environ, TTR_QR_CQR="1")
+    env = dict(os.environ, **knobs)
     r = subprocess.run([sys.executable, "-c", _CQR_PANEL_SCRIPT, root, os.path.join(root, "oracle"), here],
                        env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
+
+
+def test_fused_cholesky_qr_panel_kernel(P):
+    """K4f (one cooperative kernel per Cholesky-QR panel): A = QR, Q^T Q = I and an
+    upper R on Gaussian, graded, nearly dependent and 5b-like matrices (panels of 32
+    and fewer columns, two- and three-pass panels); a rank-deficient matrix flags
+    a breakdown or yields a valid factorisation (tools/qr_fused_check.py)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, TTR_QR_CQR="1")
+    r = subprocess.run([sys.executable, os.path.join(root, "tools", "qr_fused_check.py")], env=env,
+                       capture_output=True, text=True, timeout=900)
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
 
 
