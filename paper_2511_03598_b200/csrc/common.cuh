@@ -124,7 +124,19 @@ struct Ctx {
     // factorisation broke down (kQrNoBreakdown: none).
     bool qr_spec = false, qr_spec_used = false;
     int qr_tag = -1;  // >= 0: the thin_qr being enqueued may use Cholesky-QR panels (K4d) under this tag
-    int qr_checked_depth = 0;  // thin_qr's checked mode: 1 while its Householder rerun is being enqueued
+    // Checked Cholesky-QR calls under a recorded plan (AdaptivePlan): the eager
+    // recording run appends each call's outcome (1 = a panel broke down and the QR
+    // took the Householder panels); the captured replay reads them back and routes
+    // a breakdown of a captured Cholesky-QR kernel to `flag` (the plan's mismatch
+    // flag: the replay is then redone eagerly and re-recorded).
+    struct QrTape {
+        std::vector<char> took_hh;
+        std::size_t pos = 0;
+        bool replay = false;
+        int* flag = nullptr;
+    };
+    QrTape* qr_tape = nullptr;
+    int* qr_flag_override = nullptr;  // set while a replayed call is enqueued: breakdowns write -1 here
     i64 qr_hh_from = INT32_MAX;
     int* qr_flag = nullptr;
     int* qr_flag_dev();
@@ -269,6 +281,8 @@ void thin_qr_cholesky(Ctx& c, i64 m, i64 n, const double* A, i64 lda, double* Q,
 // Cholesky-QR panel with Householder reconstruction (qr_chol.cu, K4d): the rows
 // x b panel P -> R (P's top block), V (rows x b, unit lower), T (ld 32), tau.
 void cqr_panel(Ctx& c, i64 rows, i64 b, double* P, i64 ldp, double* V, i64 ldv, double* T, double* tau, int tag);
+bool cqr_single(Ctx& c, i64 m, i64 n, const double* A, i64 lda, double* Q, i64 ldq, double* R, i64 ldr, int* flag,
+                int tag);
 
 // Batched CholeskyQR2 / sCQR3 of small m x n matrices (K4e, n <= 32, n <= m,
 // the matrix in shared memory): flags[b] = 1 when matrix b broke down (its Q is

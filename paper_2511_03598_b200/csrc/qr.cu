@@ -660,6 +660,7 @@ void qr_small_batched(Ctx& c, i64 m, i64 n, const double* A, i64 lda, i64 sA, do
 }
 
 namespace {
+i64 kCqrSingleMaxRows(Ctx& c) { return 320LL * c.sm_count; }  // K4f: <= 320 rows per CTA, one CTA per SM
 bool cqr_checked_on() {  // experiments: TTR_QR_CHECKED=0 = non-speculating callers keep the Householder panels
     static const bool on = [] {
         const char* e = std::getenv("TTR_QR_CHECKED");
@@ -754,35 +755,48 @@ void thin_qr(Ctx& c, i64 m, i64 n, const double* A, i64 lda, double* Q, i64 ldq,
         const char* e = std::getenv("TTR_QR_CQR");
         return !(e && e[0] == '0');
     }();
-    bool cqr = cqr_on && c.qr_tag >= 0 && n > kPanel && m >= 8 * kPanel;
+    const bool cqr_shape = m >= 8 * kPanel && (n > kPanel || (m >= 8 * n && m <= kCqrSingleMaxRows(c)));
+    bool cqr = cqr_on && c.qr_tag >= 0 && cqr_shape;
     // Callers that do not speculate themselves (TT-SVD orthogonalisations, the
-    // C-ABI thin_qr): the same panels in a checked call — factor under a private
-    // tag, read the breakdown flag (one stream synchronisation per QR) and redo the
-    // QR on the Householder panels if a panel broke down. Not inside a stream
-    // capture (no synchronisation there) and not under an outer speculation (the
-    // flag is the caller's).
-    if (!cqr && cqr_on && c.qr_tag < 0 && !c.qr_spec && n > kPanel && m >= 8 * kPanel && A != Q && cqr_checked_on()) {
+    // adaptive growth blocks, the C-ABI thin_qr): the same kernels in a checked
+    // call — factor under a private tag, read the breakdown flag (one stream
+    // synchronisation per QR) and redo the QR on the Householder panels if a
+    // panel broke down. Under a recorded plan (Ctx::QrTape) the recording run
+    // notes each outcome and the captured replay follows it without a
+    // synchronisation, a breakdown there raising the plan's mismatch flag.
+    // Never under an outer speculation (the flag is the caller's).
+    if (!cqr && cqr_on && c.qr_tag < 0 && !c.qr_spec && cqr_shape && A != Q && cqr_checked_on()) {
         cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
         TTR_CUDA(cudaStreamIsCapturing(c.stream, &cap));
-        if (cap == cudaStreamCaptureStatusNone) {
-            const Counts saved = c.counts;
-            c.qr_flag_reset();
+        Ctx::QrTape* tp = c.qr_tape;
+        const Counts saved = c.counts;  // charged once, above
+        auto inner = [&](int* override_flag) {
             c.qr_tag = 0;
+            c.qr_flag_override = override_flag;
             try {
                 thin_qr(c, m, n, A, lda, Q, ldq, R, ldr);
             } catch (...) {
                 c.qr_tag = -1;
+                c.qr_flag_override = nullptr;
                 throw;
             }
             c.qr_tag = -1;
-            c.counts = saved;  // charged once, above
-            if (c.qr_flag_read() < 0) return;
-            c.qr_checked_depth = 1;  // the rerun below keeps the Householder panels
+            c.qr_flag_override = nullptr;
+            c.counts = saved;
+        };
+        if (tp && tp->replay) {
+            if (tp->pos >= tp->took_hh.size()) fail(Errc::InvalidArgument, "plan: QR decision tape exhausted");
+            if (!tp->took_hh[tp->pos++]) {
+                inner(tp->flag);
+                return;
+            }
+        } else if (cap == cudaStreamCaptureStatusNone) {
+            c.qr_flag_reset();
+            inner(nullptr);
+            const bool broke = c.qr_flag_read() >= 0;
+            if (tp) tp->took_hh.push_back(broke ? 1 : 0);
+            if (!broke) return;
         }
-    }
-    if (c.qr_checked_depth) {
-        cqr = false;
-        c.qr_checked_depth = 0;
     }
     if (!old_panels && m <= kPushMaxRows && n > kPanel && !cqr) {
         qr_blocked_push(c, 1, m, n, A, lda, 0, Q, ldq, 0, R, ldr, 0);
@@ -846,7 +860,12 @@ void thin_qr(Ctx& c, i64 m, i64 n, const double* A, i64 lda, double* Q, i64 ldq,
         c.counts = saved;
         return;
     }
-    // ---- <= 32 columns: one panel launch ----
+    // ---- <= 32 columns: the fused Cholesky-QR kernel as a plain thin QR when the
+    // caller speculates (K4f, hr = 0), else one Householder panel launch ----
+    if (n <= kPanel && cqr && cqr_single(c, m, n, A, lda, Q, ldq, R, ldr, nullptr, c.qr_tag)) {
+        c.qr_spec_used = true;
+        return;
+    }
     if (n <= kPanel) {
         DBuf tau(c, static_cast<std::size_t>(k));
         RegQrArgs a{};

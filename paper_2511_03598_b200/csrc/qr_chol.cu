@@ -1071,6 +1071,12 @@ struct FusedPanelArgs {
     int* flag;
     int tag;
     long long* trace;  // [64] phase time stamps of CTA 0 (diagnostics) or null
+    // hr = 0: a plain thin QR of the panel instead of the blocked QR's (V, T, R):
+    // Q = P R^{-1} to V (ldv) when V is set, R = R_p ... R_1 (positive diagonal) to
+    // Rout (ldr) when set; P is not written and no reconstruction runs
+    int hr;
+    double* Rout;
+    i64 ldr;
 };
 
 __host__ __device__ constexpr int fp_ld(int rpc) { return sq_ld(rpc + 32); }
@@ -1355,6 +1361,22 @@ __global__ void __launch_bounds__(kFpThreads, 1) cqr_panel_fused(FusedPanelArgs 
         mark();
     }
 
+    if (!p.hr) {  // plain thin QR: Q from the own rows, R from CTA 0
+        if (p.V) {
+            for (int c = warp; c < b; c += kFpWarps) {
+                double* dst = p.V + static_cast<i64>(c) * p.ldv;
+                for (int r = lane; r < nr; r += 32) dst[r0 + r] = S[c * ld + r];
+            }
+        }
+        if (rank == 0 && p.Rout) {
+            for (int e = tid; e < 1024; e += kFpThreads) {
+                const int i = e & 31, jj = e >> 5;
+                if (i < b && jj < b) p.Rout[i + static_cast<i64>(jj) * p.ldr] = (i <= jj) ? RT[i * LM + jj] : 0.0;
+            }
+        }
+        return;
+    }
+
     // ---- Householder reconstruction from Q_1 (the shadow block), redundantly in every
     // CTA: ONE Gauss-Jordan sweep over A = Q_1 - S by warps 0..7 (four rows each, lane =
     // column), one named barrier per step. Step k: the owner publishes row k, every warp
@@ -1527,7 +1549,7 @@ void thin_qr_cholesky(Ctx& c, i64 m, i64 n, const double* A, i64 lda, double* Q,
 // K4f host: the fused cooperative panel when the rows fit one CTA per SM
 // (<= kFpMaxRpc rows each); false = not taken (the caller uses K4d's launches).
 bool cqr_panel_fused_launch(Ctx& c, i64 rows, i64 b, double* P, i64 ldp, double* V, i64 ldv, double* T, double* tau,
-                            int tag) {
+                            int tag, int hr = 1, double* Rout = nullptr, i64 ldr = 1, int* flag = nullptr) {
     i64 rpc = ((rows + c.sm_count - 1) / c.sm_count + 7) / 8 * 8;
     rpc = std::max<i64>(rpc, 64);
     if (rpc > kFpMaxRpc) return false;
@@ -1550,8 +1572,11 @@ bool cqr_panel_fused_launch(Ctx& c, i64 rows, i64 b, double* P, i64 ldp, double*
     a.gpart = xb.p;
     a.gsum = xb.p + G * kFpEntries;
     a.coeff = 11.0 * (static_cast<double>(rows) * b + static_cast<double>(b) * (b + 1)) * u;
-    a.flag = c.qr_flag_dev();
-    a.tag = tag;
+    a.flag = flag ? flag : (c.qr_flag_override ? c.qr_flag_override : c.qr_flag_dev());
+    a.tag = c.qr_flag_override && !flag ? -1 : tag;
+    a.hr = hr;
+    a.Rout = Rout;
+    a.ldr = ldr;
     a.trace = trace_on ? reinterpret_cast<long long*>(tr.p) : nullptr;
     if (trace_on) TTR_CUDA(cudaMemsetAsync(tr.p, 0, 64 * sizeof(double), c.stream));
     void* args[] = {&a};
@@ -1571,6 +1596,16 @@ bool cqr_panel_fused_launch(Ctx& c, i64 rows, i64 b, double* P, i64 ldp, double*
     return true;
 }
 
+// K4f as a thin QR of an m x n matrix with n <= 32 (the adaptive growth blocks): Q
+// (may be null) and R (may be null, n x n upper with a positive diagonal). A is
+// only read. Breakdown -> atomicMin(*flag, tag) (flag null: the context's QR
+// flag). false = shape outside the kernel (the caller keeps its Householder QR).
+bool cqr_single(Ctx& c, i64 m, i64 n, const double* A, i64 lda, double* Q, i64 ldq, double* R, i64 ldr, int* flag,
+                int tag) {
+    if (n < 1 || n > 32 || m < 8 * n || m < 256) return false;
+    return cqr_panel_fused_launch(c, m, n, const_cast<double*>(A), lda, Q, ldq, nullptr, nullptr, tag, 0, R, ldr, flag);
+}
+
 void cqr_panel(Ctx& c, i64 rows, i64 b, double* P, i64 ldp, double* V, i64 ldv, double* T, double* tau, int tag) {
     if (b < 1 || b > 32 || rows < 2 * b) fail(Errc::InvalidArgument, "cqr_panel: shape outside the panel path");
     static const bool fused_on = [] {  // experiments: TTR_QR_CQR_FUSED=0 = K4d's separate launches
@@ -1588,7 +1623,8 @@ void cqr_panel(Ctx& c, i64 rows, i64 b, double* P, i64 ldp, double* V, i64 ldv, 
     double* Rtot = mats.p + 1024;
     double* Uinv = mats.p + 2048;
     const unsigned agrid = static_cast<unsigned>(std::min<i64>(4 * c.sm_count, (rows + kCqrThreads - 1) / kCqrThreads));
-    int* flag = c.qr_flag_dev();
+    int* flag = c.qr_flag_override ? c.qr_flag_override : c.qr_flag_dev();
+    if (c.qr_flag_override) tag = -1;
     for (int pass = 0; pass < 3; ++pass) {
         const double* src = pass == 0 ? P : Qp.p;
         const i64 lds = pass == 0 ? ldp : rows;

@@ -945,8 +945,17 @@ void AdaptivePlan::rebuild() {
     exec = nullptr;
     graph = nullptr;
     tape = AdaptiveTape{false, {}, 0, tape.d_tau, tape.d_scratch, tape.d_mismatch};
+    qr_tape = Ctx::QrTape{};
+    qr_tape.flag = tape.d_mismatch;
+    struct TapeScope {  // the context follows this plan's QR tape while it records and captures
+        Ctx& c;
+        ~TapeScope() { c.qr_tape = nullptr; }
+    } tape_scope{c};
+    c.qr_tape = &qr_tape;
     *out_slot = round_adaptive_krp_impl(c, in, cfg, nullptr, &tape, nullptr);  // record
     TTR_CUDA(cudaStreamSynchronize(c.stream));
+    qr_tape.replay = true;
+    qr_tape.pos = 0;
     const bool timing = c.timing;
     c.timing = false;
     const Counts saved = c.counts;
@@ -962,6 +971,7 @@ void AdaptivePlan::rebuild() {
         TTR_CUDA(cudaMemsetAsync(tape.d_mismatch, 0, sizeof(int), c.stream));
         round_adaptive_krp_impl(c, in, cfg, nullptr, &tape, out_slot->get());
         if (tape.pos != tape.stops.size()) fail(Errc::InvalidArgument, "adaptive plan: decision tape not consumed");
+        if (qr_tape.pos != qr_tape.took_hh.size()) fail(Errc::InvalidArgument, "adaptive plan: QR tape not consumed");
     } catch (...) {
         cudaGraph_t g;
         cudaStreamEndCapture(c.stream, &g);

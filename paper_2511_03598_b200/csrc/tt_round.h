@@ -140,6 +140,7 @@ struct AdaptivePlan {
     std::vector<i64> caps;
     std::unique_ptr<TTDev>* out_slot;  // the caller-visible output (replaced when the plan re-records)
     AdaptiveTape tape;
+    Ctx::QrTape qr_tape;  // which growth/initial QRs took the Householder panels (checked Cholesky-QR, qr.cu)
     DBuf dev;
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;

@@ -37,6 +37,19 @@ check("graded 1e-10", a)
 m = 40960
 u = rng.standard_normal((m, 300)) @ rng.standard_normal((300, 320)) + 1e-8 * rng.standard_normal((m, 320))
 check("5b-like 40960x320", u)
+# single-panel QRs (the adaptive growth blocks): the fused kernel as a plain thin QR
+for (m, n) in [(25600, 16), (960, 10), (12800, 32), (3000, 5), (47000, 20)]:
+    check(f"single-panel gauss {m}x{n}", rng.standard_normal((m, n)))
+a = rng.standard_normal((25600, 16)) * np.logspace(0, -12, 16)
+check("single-panel graded 1e-12", a)
+# the checked (non-speculating) call: breakdown -> Householder rerun inside thin_qr
+a = rng.standard_normal((9000, 30)) @ rng.standard_normal((30, 64))
+q, r = P.thin_qr(a)
+print("checked rank-deficient: orth", np.linalg.norm(q.T @ q - np.eye(64)), "res", np.linalg.norm(a - q @ r) / np.linalg.norm(a))
+assert np.linalg.norm(q.T @ q - np.eye(64)) <= 1e-12 and np.linalg.norm(a - q @ r) <= 1e-13 * np.linalg.norm(a)
+a = np.zeros((4000, 12)); a[:, :5] = rng.standard_normal((4000, 5))
+q, r = P.thin_qr(a)
+assert np.linalg.norm(a - q @ r) <= 1e-13 * np.linalg.norm(a), "zero columns"
 # exactly rank deficient
 a = rng.standard_normal((9000, 30)) @ rng.standard_normal((30, 64))
 check("rank-deficient", a, expect_break=None)
