@@ -29,6 +29,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
+#include <type_traits>
 
 #include <cooperative_groups.h>
 
@@ -1291,15 +1292,13 @@ __global__ void __launch_bounds__(kFpThreads, 1) cqr_panel_fused(FusedPanelArgs 
                     }
                     break;
                 }
-#pragma unroll 1
-                for (int k = 0; k < b; ++k) {
+                // one elimination step; Q = k & 3 is a compile-time constant so that the
+                // owner's row W[Q] is a register (a run-time select puts W in local memory)
+                auto chol_step = [&](int k, auto qc) {
+                    constexpr int Q = decltype(qc)::value;
                     double* rb = rowk + 32 * (k & 1);
-                    if (warp == (k >> 2)) {
-                        double v = W[0];
-#pragma unroll
-                        for (int q = 1; q < 4; ++q) v = ((k & 3) == q) ? W[q] : v;
-                        rb[lane] = v;
-                    }
+                    const bool owner = warp == (k >> 2);
+                    if (owner) rb[lane] = W[Q];
                     asm volatile("bar.sync 1, %0;" ::"n"(kFpFacWarps * 32) : "memory");
                     double piv = rb[k];
                     if (!(piv > 0.0) || !isfinite(piv)) {
@@ -1315,13 +1314,21 @@ __global__ void __launch_bounds__(kFpThreads, 1) cqr_panel_fused(FusedPanelArgs 
                     for (int q = 0; q < 4; ++q) {
                         const int i2 = 4 * warp + q;
                         const double v = rb[i2];
-                        if (i2 > k && (xpart || i2 <= lane)) W[q] = fma(-v, f, W[q]);
-                        if (i2 == k) {
-                            W[q] *= is;
-                            RX[k * LM + lane] = W[q];
-                            if (lane == k) xdg[k] = is;
-                        }
+                        const double upd = fma(-v, f, W[q]);
+                        W[q] = (i2 > k && (xpart || i2 <= lane)) ? upd : W[q];
                     }
+                    if (owner) {
+                        W[Q] *= is;
+                        RX[k * LM + lane] = W[Q];
+                        if (lane == k) xdg[k] = is;
+                    }
+                };
+#pragma unroll 1
+                for (int k0 = 0; k0 < b; k0 += 4) {
+                    chol_step(k0, std::integral_constant<int, 0>{});
+                    if (k0 + 1 < b) chol_step(k0 + 1, std::integral_constant<int, 1>{});
+                    if (k0 + 2 < b) chol_step(k0 + 2, std::integral_constant<int, 2>{});
+                    if (k0 + 3 < b) chol_step(k0 + 3, std::integral_constant<int, 3>{});
                 }
                 if (!(pass == 0 && attempt == 0 && (broke || ill))) break;
                 asm volatile("bar.sync 1, %0;" ::"n"(kFpFacWarps * 32) : "memory");  // rowk reused by the second attempt
@@ -1397,20 +1404,15 @@ __global__ void __launch_bounds__(kFpThreads, 1) cqr_panel_fused(FusedPanelArgs 
             W[q] = (i < b && lane < b) ? S[lane * ld + rpc + i] : (i == lane ? 1.0 : 0.0);
             Z[q] = (i == lane) ? 1.0 : 0.0;
         }
-#pragma unroll 1
-        for (int k = 0; k < 32; ++k) {
+        auto gj_step = [&](int k, auto qc) {  // Q = k & 3 at compile time (see chol_step)
+            constexpr int Q = decltype(qc)::value;
             double* rb = rowk + 32 * (k & 1);
             double* cb = colk + 32 * (k & 1);
             double* zb = zrow + 32 * (k & 1);
-            if (warp == (k >> 2)) {
-                double v = W[0], z = Z[0];
-#pragma unroll
-                for (int q = 1; q < 4; ++q) {
-                    v = ((k & 3) == q) ? W[q] : v;
-                    z = ((k & 3) == q) ? Z[q] : z;
-                }
-                rb[lane] = v;
-                if (rank == 0) zb[lane] = z;
+            const bool owner = warp == (k >> 2);
+            if (owner) {
+                rb[lane] = W[Q];
+                if (rank == 0) zb[lane] = Z[Q];
             }
             if (lane == k) {
 #pragma unroll
@@ -1426,19 +1428,29 @@ __global__ void __launch_bounds__(kFpThreads, 1) cqr_panel_fused(FusedPanelArgs 
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 const int i = 4 * warp + q;
-                if (i != k) {
-                    const double m = cb[i] * inv;
-                    if (lane > k) W[q] = fma(-m, rkc, W[q]);
-                    if (lane == k) W[q] = m;
-                    if (rank == 0 && i > k) Z[q] = fma(-m, zkc, Z[q]);
-                } else {
-                    if (lane == k) {
-                        W[q] = ukk;
-                        sg[k] = sk;
-                    }
-                    if (lane >= k) LUm[k * LM + lane] = W[q];  // U(k, c), c >= k
+                const double m = cb[i] * inv;
+                const double upd = fma(-m, rkc, W[q]);
+                const double wq = (lane > k) ? upd : ((lane == k) ? m : W[q]);
+                const double zu = fma(-m, zkc, Z[q]);
+                if (!(owner && q == Q)) {
+                    W[q] = wq;
+                    if (rank == 0 && i > k) Z[q] = zu;
                 }
             }
+            if (owner) {
+                if (lane == k) {
+                    W[Q] = ukk;
+                    sg[k] = sk;
+                }
+                if (lane >= k) LUm[k * LM + lane] = W[Q];  // U(k, c), c >= k
+            }
+        };
+#pragma unroll 1
+        for (int k0 = 0; k0 < 32; k0 += 4) {
+            gj_step(k0, std::integral_constant<int, 0>{});
+            gj_step(k0 + 1, std::integral_constant<int, 1>{});
+            gj_step(k0 + 2, std::integral_constant<int, 2>{});
+            gj_step(k0 + 3, std::integral_constant<int, 3>{});
         }
         // L below the diagonal; U^{-1} into the apply layout (RX/xdg; R no longer needed)
 #pragma unroll
