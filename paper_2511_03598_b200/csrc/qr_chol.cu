@@ -1043,19 +1043,22 @@ __global__ void __launch_bounds__(256, SQ_MINB) cholqr_small_kernel(int m, int n
 //                                  CTAs see the same G and take the same branches;
 //   R, R^{-T}                      warp 0 (the K4e elimination), redundantly;
 //   S <- S R^{-1}                  fp64 DMMA, warp per 8-row tile.
-// Pass 0 factors G as it is unless a pivot fell below 1e-6 of its diagonal entry
+// A pass factors G as it is unless a pivot fell below 1e-6 of its diagonal entry
 // (or was not positive), in which case the same G is refactored with the sCQR
-// shift s = coeff tr(G). Every later pass first tests ||G - I||_F <= 1/2: when it
-// holds the pass is the last one (its input was well conditioned, so its output
-// is orthonormal to O(u)); a fifth pass, a non-positive pivot after pass 0 or a
-// non-finite entry is a breakdown (flag <- tag, nothing written; the caller
-// reruns the QR on the Householder panels). A well conditioned panel takes two
-// passes (4 grid barriers), an ill conditioned one three (6).
+// shift s = coeff tr(G) (each shifted pass lowers the condition number by about
+// sqrt(s)/||A||: one for kappa ~ 1e8, two for the 1e8-1e12 of a panel that
+// straddles the numerical rank of the sketch). Every pass after the first tests
+// ||G - I||_F <= 1/2 first: when it holds the pass is the last one (its input was
+// well conditioned, so its output is orthonormal to O(u)); a seventh pass, a
+// non-positive pivot under the shift or a non-finite entry is a breakdown (flag
+// <- tag, nothing written; the caller reruns the QR on the Householder panels).
+// A well conditioned panel takes two passes (4 grid barriers), an ill
+// conditioned one three or four.
 // Then (Ballard et al. 2014, as cqr_hr above): LU without pivoting of Q_1 - S,
 // V_2 = Q_2 U^{-1} by the same DMMA apply, CTA 0 writes V_1 = L, T = -U S L^{-T},
 // tau = diag(T) and R = S R_p ... R_1 into the panel's top block.
 constexpr int kFpThreads = 512, kFpWarps = kFpThreads / 32, kFpGramWarps = 8, kFpFacWarps = 8, kFpPairs = 10, kFpEntries = kFpPairs * 64,
-              kFpMaxRpc = 320, kFpMaxPasses = 4;
+              kFpMaxRpc = 320, kFpMaxPasses = 6;
 constexpr double kFpAnalyticDev2 = 1e-18;  // ||G - I||_F^2 below which a pass takes the first-order factor
 
 struct FusedPanelArgs {
@@ -1252,7 +1255,7 @@ __global__ void __launch_bounds__(kFpThreads, 1) cqr_panel_fused(FusedPanelArgs 
                 }
                 const double dg = real ? Gm[lane * LM + lane] : 1.0;
                 double shift = 0.0;
-                if (pass == 0 && attempt == 1) {  // sCQR shift
+                if (attempt == 1) {  // sCQR shift
                     double tr = real ? dg : 0.0;
                     for (int o = 16; o > 0; o >>= 1) tr += __shfl_xor_sync(0xffffffffu, tr, o);
                     shift = p.coeff * tr;
@@ -1330,7 +1333,7 @@ __global__ void __launch_bounds__(kFpThreads, 1) cqr_panel_fused(FusedPanelArgs 
                     if (k0 + 2 < b) chol_step(k0 + 2, std::integral_constant<int, 2>{});
                     if (k0 + 3 < b) chol_step(k0 + 3, std::integral_constant<int, 3>{});
                 }
-                if (!(pass == 0 && attempt == 0 && (broke || ill))) break;
+                if (!(attempt == 0 && (broke || ill))) break;
                 asm volatile("bar.sync 1, %0;" ::"n"(kFpFacWarps * 32) : "memory");  // rowk reused by the second attempt
             }
             for (int i = b + warp; i < 32; i += kFpFacWarps) {  // padded rows: identity
@@ -1345,7 +1348,10 @@ __global__ void __launch_bounds__(kFpThreads, 1) cqr_panel_fused(FusedPanelArgs 
         __syncthreads();
         mark();
         if (s_bad) {  // the same decision in every CTA (identical G)
-            if (rank == 0 && tid == 0) atomicMin(p.flag, p.tag);
+            if (rank == 0 && tid == 0) {
+                atomicMin(p.flag, p.tag);
+                if (p.trace) p.trace[63] = -(pass + 1);  // diagnostics: the pass that broke down
+            }
             return;
         }
         done = s_final != 0;
@@ -1602,7 +1608,8 @@ bool cqr_panel_fused_launch(Ctx& c, i64 rows, i64 b, double* P, i64 ldp, double*
         TTR_CUDA(cudaStreamSynchronize(c.stream));
         std::fprintf(stderr, "cqr_panel_fused rows %lld b %lld rpc %lld grid %lld: cycles", static_cast<long long>(rows),
                      static_cast<long long>(b), static_cast<long long>(rpc), static_cast<long long>(G));
-        for (int i = 1; i < 64 && h[i]; ++i) std::fprintf(stderr, " %lld", h[i] - h[i - 1]);
+        for (int i = 1; i < 63 && h[i]; ++i) std::fprintf(stderr, " %lld", h[i] - h[i - 1]);
+        if (h[63] < 0) std::fprintf(stderr, " BREAKDOWN in pass %lld", -h[63] - 1);
         std::fprintf(stderr, "\n");
     }
     return true;

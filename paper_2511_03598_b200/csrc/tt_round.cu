@@ -393,8 +393,10 @@ void with_qr_speculation(Ctx& c, const std::function<void()>& body) {
     } restore{c};
     c.qr_spec = true;
     c.qr_hh_from = INT32_MAX;
+    const Counts saved = c.counts;
     for (;;) {
         c.qr_spec_used = false;
+        c.counts = saved;  // a rerun is charged once (the reference's flop counts)
         body();
         if (!c.qr_spec_used) break;
         const int failed = c.qr_flag_read();
@@ -485,7 +487,9 @@ void rand_orth_sweep(Ctx& c, const TTDev& t, i64 width, const std::vector<const 
                 c.qr_spec_used = true;
             } else {
                 // the blocked Householder QR may take Cholesky-QR panels (K4d) under this mode's tag
-                c.qr_tag = (c.qr_spec && k < c.qr_hh_from) ? static_cast<int>(k) : -1;
+                // (not where the sketch is rank-deficient by construction, wbound above: its
+                // panels would break down and the whole call would run twice)
+                c.qr_tag = (c.qr_spec && k < c.qr_hh_from && wbound[k + 1] >= l && rows >= l) ? static_cast<int>(k) : -1;
                 try {
                     thin_qr(c, rows, l, S.p, rows, out->core(k - 1), rows, nullptr, 1);
                 } catch (...) {
