@@ -216,6 +216,38 @@ print("ok")
 """
 
 
+def test_fixed_krp_straddling_panel_runs_once(P, O):
+    """Config-5b structure at reduced size (rank 40 + 1e-8 x rank 88, l = 64: the
+    second 32-column panel of every sketch holds 8 dominant directions and 24 at
+    1e-8, kappa ~ 1e8-1e9): the Cholesky-QR panel takes its shifted passes instead
+    of breaking down, so the eager call runs ONCE (about as many kernel launches as
+    one replay of its plan), charges the reference's flops once, and matches the
+    oracle; the last bond (n_d < l, rank-deficient by construction) does not
+    speculate."""
+    x = O.two_part_tt(6, 48, 40, 88, 1e-8, 4101)
+    ranks = [64] * 5
+    y = to_device(x)
+    ctx = y.ctx
+    P.round_fixed_krp(y, ranks, 7, rng=P.RNG_PHILOX)  # warm-up: pools, kernel attributes
+    ctx.reset_counters()
+    O.flops_reset()
+    l0 = ctx.kernel_launches()
+    out = P.round_fixed_krp(y, ranks, 7, rng=P.RNG_PHILOX)
+    eager_launches = ctx.kernel_launches() - l0
+    ref = O.round_fixed_krp(x, ranks, 7, rng=O.PHILOX)
+    dev, rf = ctx.counters(), O.flops_get()
+    assert (dev.gemm, dev.qr, dev.svd, dev.sketch) == (rf["gemm"], rf["qr"], rf["svd"], rf["sketch"])
+    assert out.ranks() == ref.ranks
+    assert rel_err_vs_ref(ref, out) <= 1e-10
+    plan = P.FixedKrpPlan(y, ranks, 7)
+    l1 = ctx.kernel_launches()
+    plan.execute()
+    plan_launches = ctx.kernel_launches() - l1
+    assert np.array_equal(plan.output.flat(), out.flat())
+    plan.close()
+    assert eager_launches <= 1.2 * plan_launches, (eager_launches, plan_launches)
+
+
 @pytest.mark.parametrize("knobs", [{"TTR_QR_CQR": "1"}, {"TTR_QR_CQR": "1", "TTR_QR_CQR_FUSED": "0"},
                                    {"TTR_QR_CQR": "0"}],
                          ids=["fused-K4f", "launches-K4d", "householder-panels"])
