@@ -1,5 +1,12 @@
-// qr_chol.cu — K4c: shifted Cholesky QR (sCQR) for the tall-skinny sketches
-// of the Rand-Orth sweep and the TT-SVD orthogonalisations.
+// qr_chol.cu — Cholesky-QR kernels:
+//   K4c  whole-matrix shifted Cholesky QR of a tall-skinny sketch (opt-in, below),
+//   K4d  Cholesky-QR panels with Householder reconstruction as separate launches,
+//   K4e  batched CholeskyQR2 / sCQR3 of small matrices (the batched sweep, config 5a),
+//   K4f  the K4d panel as ONE cooperative kernel — the default panel factorisation
+//        of the blocked Householder QR and the thin QR of <= 32-column blocks.
+//
+// K4c: shifted Cholesky QR (sCQR) for the tall-skinny sketches of the Rand-Orth
+// sweep and the TT-SVD orthogonalisations.
 //
 // linalg::thin_qr_q (proj/core/src/linalg.cpp:44-56) is called by the sweep
 // only for an orthonormal basis of range(S) (round_rand.cpp:33-37); the
