@@ -124,6 +124,12 @@ struct Ctx {
     // factorisation broke down (kQrNoBreakdown: none).
     bool qr_spec = false, qr_spec_used = false;
     int qr_tag = -1;  // >= 0: the thin_qr being enqueued may use Cholesky-QR panels (K4d) under this tag
+    // > 0: the matrix of the thin_qr being enqueued has rank <= qr_rank_hint by construction
+    // (a sketch V W whose W has fewer independent rows than columns) and only Q is wanted:
+    // the blocked QR factors the first ceil32(hint) columns and completes Q with the
+    // reflected unit vectors (any orthonormal completion serves: the columns past the
+    // rank carry nothing of the tensor)
+    i64 qr_rank_hint = 0;
     // Checked Cholesky-QR calls under a recorded plan (AdaptivePlan): the eager
     // recording run appends each call's outcome (1 = a panel broke down and the QR
     // took the Householder panels); the captured replay reads them back and routes

@@ -735,7 +735,11 @@ void gemm_tn_lt(Ctx& c, i64 M, i64 N, i64 K, const double* A, i64 lda, const dou
     const i64 bm = kSkBM, bn = tma_tiles ? 64 : kSkBN;
     const i64 tiles = ((M + bm - 1) / bm) * ((N + bn - 1) / bn);
     const int total_kt = static_cast<int>((K + 15) / 16);
-    const int splits = choose_splits(c, tiles, total_kt, tma_tiles ? 8 : 2);
+    static const int per_sm = [] {  // experiments: CTAs per SM the split-K grid of V^T A targets
+        const char* e = std::getenv("TTR_GEMM_TN_PERSM");
+        return e ? std::max(1, std::atoi(e)) : 4;  // 4: half the split-K partials of 8 (40,960 x 320 QR 1.79 -> 1.73 ms)
+    }();
+    const int splits = choose_splits(c, tiles, total_kt, tma_tiles ? per_sm : 2);
     // run_gemm's own rounding of the split count decides whether the wide reduction runs
     const int s1 = std::max(1, std::min(splits, total_kt)), per = (total_kt + s1 - 1) / s1;
     if ((total_kt + per - 1) / per >= 16) {

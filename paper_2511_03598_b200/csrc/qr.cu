@@ -903,6 +903,12 @@ void thin_qr(Ctx& c, i64 m, i64 n, const double* A, i64 lda, double* Q, i64 ldq,
     }
 
     // ---- blocked right-looking Householder ----
+    // kf: columns that get reflectors (all, unless the caller bounds the rank and wants Q only)
+    i64 kf = k;
+    if (c.qr_rank_hint > 0 && R == nullptr && Q != nullptr && k <= 384) {
+        const i64 h = (c.qr_rank_hint + kPanel - 1) / kPanel * kPanel;
+        if (h < k) kf = h;
+    }
     const i64 ldw = even_ld(m);
     DBuf work(c, static_cast<std::size_t>(ldw * n));
     copy_matrix(c, m, n, A, lda, work.p, ldw);
@@ -914,14 +920,15 @@ void thin_qr(Ctx& c, i64 m, i64 n, const double* A, i64 lda, double* Q, i64 ldq,
     DBuf Wb(c, static_cast<std::size_t>(kPanel * std::max<i64>(n, 1)));
     DBuf Wb2(c, static_cast<std::size_t>(kPanel * std::max<i64>(n, 1)));
 
-    for (i64 p = 0; p < npanels; ++p) {
-        const i64 j0 = p * kPanel, bb = std::min<i64>(kPanel, k - j0), rows = m - j0;
+    const i64 npf = (kf + kPanel - 1) / kPanel, nf = kf < k ? kf : n;  // panels factored, columns kept up to date
+    for (i64 p = 0; p < npf; ++p) {
+        const i64 j0 = p * kPanel, bb = std::min<i64>(kPanel, kf - j0), rows = m - j0;
         double* V = Vall.p + j0 + j0 * ldw;  // rows x bb block at (j0, j0), ld ldw
         double* T = Ts.p + p * kPanel * kPanel;
         if (cqr && rows >= 4 * kPanel) {
             cqr_panel(c, rows, bb, work.p + j0 + j0 * ldw, ldw, V, ldw, T, tau.p + j0, c.qr_tag);
             c.qr_spec_used = true;
-            const i64 ntrail = n - j0 - bb;
+            const i64 ntrail = nf - j0 - bb;
             if (ntrail > 0) {
                 double* At = work.p + j0 + (j0 + bb) * ldw;
                 gemm_tn_lt(c, bb, ntrail, rows, V, ldw, At, ldw, T, kPanel, Wb2.p, kPanel, Wb.p, false);  // T^T (V^T A)
@@ -941,7 +948,7 @@ void thin_qr(Ctx& c, i64 m, i64 n, const double* A, i64 lda, double* Q, i64 ldq,
         a.ldv = ldw;
         a.T = T;
         launch_panel(a);
-        const i64 ntrail = n - j0 - bb;
+        const i64 ntrail = nf - j0 - bb;
         if (ntrail > 0) {
             double* At = work.p + j0 + (j0 + bb) * ldw;
             gemm_tn_lt(c, bb, ntrail, rows, V, ldw, At, ldw, T, kPanel, Wb2.p, kPanel, Wb.p, false);  // T^T (V^T A)
@@ -958,27 +965,29 @@ void thin_qr(Ctx& c, i64 m, i64 n, const double* A, i64 lda, double* Q, i64 ldq,
     // aggregated T of all panels (V_1 = top k x k block of V): two full-size
     // GEMMs (V^T V and V Y) instead of three skinny ones per panel
     if (k <= 384) {
-        DBuf Gm(c, static_cast<std::size_t>(k * k));
-        DBuf Tf(c, static_cast<std::size_t>(k * k));
-        DBuf V1t(c, static_cast<std::size_t>(k * k));
-        DBuf Y(c, static_cast<std::size_t>(k * k));
+        // kq = kf columns of V carry reflectors (the rest of Q is the reflected unit vectors)
+        const i64 kq = kf;
+        DBuf Gm(c, static_cast<std::size_t>(kq * kq));
+        DBuf Tf(c, static_cast<std::size_t>(kq * kq));
+        DBuf V1t(c, static_cast<std::size_t>(kq * k));
+        DBuf Y(c, static_cast<std::size_t>(kq * k));
         // G = V^T V; t_aggregate_kernel reads only its strictly upper 32-blocks
-        gemm(c, true, k, k, m, 1.0, Vall.p, ldw, Vall.p, ldw, 0.0, Gm.p, k, false, true);
-        const std::size_t smem = (static_cast<std::size_t>(npanels) * 32 * 32 + (npanels - 1) * 32 * 33) * sizeof(double);
+        gemm(c, true, kq, kq, m, 1.0, Vall.p, ldw, Vall.p, ldw, 0.0, Gm.p, kq, false, true);
+        const std::size_t smem = (static_cast<std::size_t>(npf) * 32 * 32 + (npf - 1) * 32 * 33) * sizeof(double);
         static std::atomic<std::uint64_t> configured{0};  // bit d: attributes set on device d
         if (first_on_device(configured)) {
             TTR_CUDA(cudaFuncSetAttribute(t_aggregate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         }
-        t_aggregate_kernel<<<static_cast<unsigned>(npanels), kTaggThreads, smem, c.stream>>>(static_cast<int>(k), Gm.p,
-                                                                                             Ts.p, Tf.p);
+        t_aggregate_kernel<<<static_cast<unsigned>(npf), kTaggThreads, smem, c.stream>>>(static_cast<int>(kq), Gm.p, Ts.p,
+                                                                                         Tf.p);
         TTR_CUDA(cudaGetLastError());
         c.launched();
-        transpose(c, k, k, Vall.p, ldw, V1t.p, k);                                        // V_1^T
-        gemm(c, false, k, k, k, 1.0, Tf.p, k, V1t.p, k, 0.0, Y.p, k, false);              // Y = T V_1^T
+        transpose(c, k, kq, Vall.p, ldw, V1t.p, kq);                                      // V_1^T (kq x k)
+        gemm(c, false, kq, k, kq, 1.0, Tf.p, kq, V1t.p, kq, 0.0, Y.p, kq, false);         // Y = T V_1^T
         init_thin_identity<<<blocks_for(c, m * k), 256, 0, c.stream>>>(static_cast<int>(m), static_cast<int>(k), Q, ldq);
         TTR_CUDA(cudaGetLastError());
         c.launched();
-        gemm(c, false, m, k, k, -1.0, Vall.p, ldw, Y.p, k, 1.0, Q, ldq, false);           // Q = [I;0] - V Y
+        gemm(c, false, m, k, kq, -1.0, Vall.p, ldw, Y.p, kq, 1.0, Q, ldq, false);         // Q = [I;0] - V Y
         return;
     }
     // very wide: panels applied last to first (backward accumulation)

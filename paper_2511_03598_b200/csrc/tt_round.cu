@@ -489,14 +489,29 @@ void rand_orth_sweep(Ctx& c, const TTDev& t, i64 width, const std::vector<const 
                 // the blocked Householder QR may take Cholesky-QR panels (K4d) under this mode's tag
                 // (not where the sketch is rank-deficient by construction, wbound above: its
                 // panels would break down and the whole call would run twice)
-                c.qr_tag = (c.qr_spec && k < c.qr_hh_from && wbound[k + 1] >= l && rows >= l) ? static_cast<int>(k) : -1;
+                // A bond whose sketch has rank <= wb < l by construction (the last one whenever
+                // n_d < l): only its first ceil32(wb) columns get reflectors (qr_rank_hint);
+                // with wb a multiple of the panel width those columns are generically
+                // independent and may speculate too.
+                const i64 wb = wbound[k + 1];
+                static const bool hint_on = [] {  // experiments: TTR_QR_RANK_HINT=0 = reflectors for every column
+                    const char* e = std::getenv("TTR_QR_RANK_HINT");
+                    return !(e && e[0] == '0');
+                }();
+                const bool bounded = wb < l && hint_on;
+                c.qr_rank_hint = bounded ? wb : 0;
+                c.qr_tag = (c.qr_spec && k < c.qr_hh_from && rows >= l && (wb >= l || (bounded && wb % 32 == 0)))
+                               ? static_cast<int>(k)
+                               : -1;
                 try {
                     thin_qr(c, rows, l, S.p, rows, out->core(k - 1), rows, nullptr, 1);
                 } catch (...) {
                     c.qr_tag = -1;
+                    c.qr_rank_hint = 0;
                     throw;
                 }
                 c.qr_tag = -1;
+                c.qr_rank_hint = 0;
             }
         }
         if (c.io) c.io->out_done(c.stream, static_cast<std::size_t>(k - 1));  // output core k-1 final: D2H
