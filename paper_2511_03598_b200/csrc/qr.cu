@@ -299,6 +299,11 @@ __global__ void init_thin_identity(int m, int k, double* Q, i64 ldq, i64 sQ = 0)
     }
 }
 
+__global__ void add_unit_diagonal(int k, double* Q, i64 ldq) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j < k) Q[j + static_cast<i64>(j) * ldq] += 1.0;
+}
+
 __global__ void copy_upper(int k, int n, const double* A, i64 lda, double* R, i64 ldr, i64 sA = 0, i64 sR = 0) {
     A += blockIdx.y * sA;
     R += blockIdx.y * sR;
@@ -984,10 +989,12 @@ void thin_qr(Ctx& c, i64 m, i64 n, const double* A, i64 lda, double* Q, i64 ldq,
         c.launched();
         transpose(c, k, kq, Vall.p, ldw, V1t.p, kq);                                      // V_1^T (kq x k)
         gemm(c, false, kq, k, kq, 1.0, Tf.p, kq, V1t.p, kq, 0.0, Y.p, kq, false);         // Y = T V_1^T
-        init_thin_identity<<<blocks_for(c, m * k), 256, 0, c.stream>>>(static_cast<int>(m), static_cast<int>(k), Q, ldq);
+        // Q = [I;0] - V Y: the product alone (no pass over Q to preset the identity and to
+        // read it back), then + 1 on the diagonal (-(V Y) + 1 rounds as the fused form does)
+        gemm(c, false, m, k, kq, -1.0, Vall.p, ldw, Y.p, kq, 0.0, Q, ldq, false);
+        add_unit_diagonal<<<static_cast<unsigned>((k + 255) / 256), 256, 0, c.stream>>>(static_cast<int>(k), Q, ldq);
         TTR_CUDA(cudaGetLastError());
         c.launched();
-        gemm(c, false, m, k, kq, -1.0, Vall.p, ldw, Y.p, kq, 1.0, Q, ldq, false);         // Q = [I;0] - V Y
         return;
     }
     // very wide: panels applied last to first (backward accumulation)
