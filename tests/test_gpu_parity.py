@@ -1366,6 +1366,40 @@ def test_batched_cholesky_qr_modes(P, O, mode):
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
 
 
+def test_adaptive_plan_qr_breakdown_in_replay(P, O):
+    """Sketch blocks tall enough for the fused Cholesky-QR kernel (K4f as the thin QR
+    of the initial and growth blocks, rows > 512): the plan replays bitwise the
+    eager call; refilled with an all-zero tensor every captured Cholesky-QR kernel
+    breaks down (zero Gram matrix), the replay raises the plan's flag, the call is
+    redone eagerly — checked QRs falling back to the Householder panels — and
+    re-recorded with those QRs on the Householder path; the result is the zero
+    tensor with the oracle's ranks, and the next replay needs no further redo."""
+    x1 = O.two_part_tt(5, 48, 8, 28, 1e-6, 3401)
+    cfg = P.AdaptiveConfig(tolerance=1e-4, f_init=0.1, f_inc=0.05, seed=7)
+    t = to_device(x1)
+    plan = P.AdaptiveKrpPlan(t, cfg)
+    eager = P.round_adaptive_krp(to_device(x1), cfg)
+    ref = O.round_adaptive_krp(x1, tolerance=1e-4, f_init=0.1, f_inc=0.05, seed=7, rng=O.PHILOX)
+    plan.execute()
+    assert np.array_equal(plan.output.flat(), eager.flat())
+    assert eager.ranks() == ref.ranks and rel_err_vs_ref(ref, eager) <= 1e-10
+    assert plan.rerecords() == 0
+    zero = np.zeros_like(x1.flat())
+    P.copy_from_host(t, zero)
+    plan.execute()
+    assert plan.rerecords() == 1
+    out = plan.output
+    assert np.all(np.isfinite(out.flat()))
+    n, r, _ = x1.shape()
+    xz = O.TT.from_flat(len(n), n, r, zero)
+    refz = O.round_adaptive_krp(xz, tolerance=1e-4, f_init=0.1, f_inc=0.05, seed=7, rng=O.PHILOX)
+    assert out.ranks() == refz.ranks
+    assert P.norm_exact(out) == 0.0
+    plan.execute()
+    assert plan.rerecords() == 1
+    plan.close()
+
+
 def test_adaptive_plan_replays_and_rerecords(P, O):
     """ttr_plan_adaptive_krp: the graph replay of the recorded growth decisions is
     bitwise the eager call; refilled with data that decides differently, the plan
