@@ -760,7 +760,9 @@ void thin_qr(Ctx& c, i64 m, i64 n, const double* A, i64 lda, double* Q, i64 ldq,
         const char* e = std::getenv("TTR_QR_CQR");
         return !(e && e[0] == '0');
     }();
-    const bool cqr_shape = m >= 8 * kPanel && (n > kPanel || (m >= 8 * n && m <= kCqrSingleMaxRows(c)));
+    // (rows beyond the fused kernel's one-CTA-per-SM capacity keep the Householder
+    // panels: K4d's separate launches are slower than those)
+    const bool cqr_shape = m >= 8 * kPanel && m <= kCqrSingleMaxRows(c) && (n > kPanel || m >= 8 * n);
     bool cqr = cqr_on && c.qr_tag >= 0 && cqr_shape;
     // Callers that do not speculate themselves (TT-SVD orthogonalisations, the
     // adaptive growth blocks, the C-ABI thin_qr): the same kernels in a checked
