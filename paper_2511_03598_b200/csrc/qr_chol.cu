@@ -1065,7 +1065,7 @@ __global__ void __launch_bounds__(256, SQ_MINB) cholqr_small_kernel(int m, int n
 // V_2 = Q_2 U^{-1} by the same DMMA apply, CTA 0 writes V_1 = L, T = -U S L^{-T},
 // tau = diag(T) and R = S R_p ... R_1 into the panel's top block.
 constexpr int kFpThreads = 512, kFpWarps = kFpThreads / 32, kFpGramWarps = 8, kFpFacWarps = 8, kFpPairs = 10, kFpEntries = kFpPairs * 64,
-              kFpMaxRpc = 320, kFpMaxPasses = 6;
+              kFpMaxRpc = 320, kFpMaxPasses = 6, kFpDirectG = 32;
 constexpr double kFpAnalyticDev2 = 1e-18;  // ||G - I||_F^2 below which a pass takes the first-order factor
 
 struct FusedPanelArgs {
@@ -1205,15 +1205,43 @@ __global__ void __launch_bounds__(kFpThreads, 1) cqr_panel_fused(FusedPanelArgs 
                 *reinterpret_cast<double2*>(part + (warp * kFpPairs + q) * 64 + 2 * lane) = make_double2(acc[q][0], acc[q][1]);
         }
         __syncthreads();
+        // few CTAs (kFpDirectG): every CTA sums all partials itself after ONE barrier (the
+        // partials double-buffered by pass parity: the next pass's writes cannot overtake
+        // a late reader), else the two-stage sum below
+        const bool direct = G <= kFpDirectG;
+        double* gp = p.gpart + (direct && (pass & 1) ? static_cast<i64>(G) * kFpEntries : 0);
         for (int e = tid; e < kFpEntries; e += kFpThreads) {
             double g = 0.0;
 #pragma unroll
             for (int w = 0; w < kFpGramWarps; ++w) g += part[w * kFpEntries + e];
-            p.gpart[static_cast<i64>(rank) * kFpEntries + e] = g;
+            gp[static_cast<i64>(rank) * kFpEntries + e] = g;
         }
         mark();
         grid.sync();
         mark();
+        if (direct) {
+            for (int e = tid; e < kFpEntries; e += kFpThreads) {
+                double a = 0.0;
+                for (int g0 = 0; g0 < G; g0 += 8) {  // eight loads in flight, summed in rank order
+                    double v[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u)
+                        v[u] = (g0 + u < G) ? __ldcg(gp + static_cast<i64>(g0 + u) * kFpEntries + e) : 0.0;
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) a += v[u];
+                }
+                const int q = e >> 6, f = e & 63;
+                int i = 0, qq = q;
+                while (qq >= 4 - i) {
+                    qq -= 4 - i;
+                    ++i;
+                }
+                const int j = i + qq, fl = f >> 1;
+                Gm[(8 * i + (fl >> 2)) * LM + 8 * j + 2 * (fl & 3) + (f & 1)] = a;
+            }
+            mark();
+            mark();
+        } else {
         // ---- slice of the grid sum: one warp per entry, fixed order ----
         {
             const int eper = (kFpEntries + G - 1) / G, e0 = rank * eper;
@@ -1240,6 +1268,7 @@ __global__ void __launch_bounds__(kFpThreads, 1) cqr_panel_fused(FusedPanelArgs 
             const int j = i + qq, fl = f >> 1;  // C fragment: row fl >> 2, columns 2 (fl & 3) + (f & 1)
             Gm[(8 * i + (fl >> 2)) * LM + 8 * j + 2 * (fl & 3) + (f & 1)] = __ldcg(p.gsum + e);
         }
+        }  // two-stage sum
         __syncthreads();
         // ---- R and R^{-T} by warps 0..7 (kFpFacWarps), four rows each, lane = column c.
         // One array holds both triangles: entry (i, c) is G(i, c) for i <= c and, as the
@@ -1583,7 +1612,7 @@ bool cqr_panel_fused_launch(Ctx& c, i64 rows, i64 b, double* P, i64 ldp, double*
     if (first_on_device(configured)) set_max_dynamic_smem(reinterpret_cast<const void*>(cqr_panel_fused));
     static const bool trace_on = std::getenv("TTR_QR_TRACE") != nullptr;  // diagnostics (eager calls only)
     const double u = DBL_EPSILON / 2;
-    DBuf xb(c, static_cast<std::size_t>((G + 1) * kFpEntries)), tr(c, trace_on ? 64 : 1);
+    DBuf xb(c, static_cast<std::size_t>((2 * G + 1) * kFpEntries)), tr(c, trace_on ? 64 : 1);  // partials (x 2: kFpDirectG) + sum
     FusedPanelArgs a{};
     a.rows = static_cast<int>(rows);
     a.b = static_cast<int>(b);
@@ -1595,7 +1624,7 @@ bool cqr_panel_fused_launch(Ctx& c, i64 rows, i64 b, double* P, i64 ldp, double*
     a.T = T;
     a.tau = tau;
     a.gpart = xb.p;
-    a.gsum = xb.p + G * kFpEntries;
+    a.gsum = xb.p + 2 * G * kFpEntries;
     a.coeff = 11.0 * (static_cast<double>(rows) * b + static_cast<double>(b) * (b + 1)) * u;
     a.flag = flag ? flag : (c.qr_flag_override ? c.qr_flag_override : c.qr_flag_dev());
     a.tag = c.qr_flag_override && !flag ? -1 : tag;
