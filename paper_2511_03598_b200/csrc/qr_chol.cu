@@ -728,8 +728,8 @@ __global__ void __launch_bounds__(kCholSmall) cqr_hr(int b, const double* Q, i64
         for (int k = i; k <= j; ++k) t = fma(A[i][k] * s[k], Li[j][k], t);
         t = -t;
     }
+    T[i + 32 * j] = (i < b && j < b) ? t : 0.0;  // the whole block: zero past b (the T aggregation reads all of it)
     if (i < b && j < b) {
-        T[i + 32 * j] = t;
         if (i == j) tau[j] = t;
         V[i + static_cast<i64>(j) * ldv] = i > j ? A[i][j] : (i == j ? 1.0 : 0.0);
         if (i <= j) Rout[i + static_cast<i64>(j) * ldr] = s[i] * Rtot[i + 32 * j];
@@ -1529,8 +1529,9 @@ __global__ void __launch_bounds__(kFpThreads, 1) cqr_panel_fused(FusedPanelArgs 
                 for (int k = i; k <= jj; ++k) t = fma(LUm[i * LM + k] * sg[k], ZS[jj * LM + k], t);
                 t = -t;
             }
+            // the whole 32 x 32 block (zero past b: the T aggregation reads all of it)
+            p.T[i + 32 * jj] = (i < b && jj < b) ? t : 0.0;
             if (i < b && jj < b) {
-                p.T[i + 32 * jj] = t;
                 if (i == jj) p.tau[jj] = t;
                 if (i <= jj) p.P[i + static_cast<i64>(jj) * p.ldp] = sg[i] * RT[i * LM + jj];
             }
